@@ -1,0 +1,313 @@
+#!/usr/bin/env python
+"""ACE hot-path benchmark (BASELINE.json metric: ACE points/sec, hash + insert
++ score, on 1 B200; roofline fraction reported beside it).
+
+One step = one pass of the batch pipeline over the workload: reset the sketch,
+build_sketch (hash + insert every row) then detect_batch (score every row,
+mu - sigma threshold, flags) — ace_sketch_build_detect through the C ABI.
+Default workload: BASELINE config 2 (configs[1]: N=500,000, d=120, K=15,
+L=50), inputs resident in HBM (240 MB > the 126 MB L2, so no flush needed).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C]
+  python bench.py --impl reference ...   # the reference's CPU implementation
+
+Multi-GPU (torchrun): replicas only — each rank runs the full workload on its
+own GPU (the north star is single-GPU, no inter-GPU exchange); value = total
+points of all ranks / max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "ACE points/sec (hash+insert+score) on 1 B200; % of binding FP32/HBM/L2-atomic roofline"
+UNIT = "points/s"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured (MEASURED_PEAKS.json)"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [v.strip() for v in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_baseline(cfg: int, sample: int):
+    """The compiled reference (oracle/_ref) on a bounded sample: insert on one
+    core (single writer, sketch.hpp:23-24), detect_batch on all cores."""
+    from oracle import REF_SO, Oracle, Reference
+    from paper_1706_06664_b200 import workloads as W
+    w = W.CONFIGS[cfg]
+    x, _ = W.host_rows(cfg, 0, sample)
+    cores = os.cpu_count() or 1
+    if REF_SO.exists():
+        ref = Reference()
+        ti, td, _rep = ref.time_build_detect(w.w_seed, x, w.k_bits, w.num_tables, 0)
+        kind = "reference"
+    else:  # the C restatement (same algorithm), single thread throughout
+        o = Oracle()
+        t0 = time.perf_counter()
+        wm = o.directions(w.w_seed, w.dim, w.k_bits, w.num_tables)
+        ids, _ = o.buckets(wm, x, w.k_bits, w.num_tables, threads=1)
+        sk = o.sketch(w.k_bits, w.num_tables, 32)
+        sk.insert_ids(ids)
+        ti = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        o.buckets(wm, x, w.k_bits, w.num_tables, threads=cores)
+        sk.score_ids(ids)
+        td = time.perf_counter() - t0
+        kind = "port"
+    return {"value": sample / (ti + td), "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"first {sample} rows of config {cfg}: insert on 1 core ({ti:.2f} s), "
+                      f"detect_batch on {cores} threads ({td:.2f} s)"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    from paper_1706_06664_b200 import workloads as W
+    w = W.CONFIGS[args.config]
+    sample = args.ref_sample
+    times = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(args.config, sample)
+        if i >= args.warmup:
+            times.append(sample / cb["value"])
+    t = statistics.mean(times)
+    value = sample / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": f"cfg{args.config} {w.name} sample={sample} rows",
+                                        "N": sample, "d": w.dim, "K": w.k_bits, "L": w.num_tables},
+        "cpu_baseline": {**cb, "value": value},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ace", choices=["ace", "reference"])
+    ap.add_argument("--ref-sample", type=int, default=20_000,
+                    help="rows per step of the --impl reference arm")
+    ap.add_argument("--cpu-sample", type=int, default=150_000,
+                    help="rows of the cpu_baseline leg (10-30 s of CPU work)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1706_06664_b200 import _native as N
+    from paper_1706_06664_b200 import ace
+    from paper_1706_06664_b200 import workloads as W
+
+    ws, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = W.CONFIGS[args.config]
+    assert w.mode == "batch", "bench workload must be a batch configuration"
+    n = w.n
+    x = torch.empty((n, w.dim), dtype=torch.float32, device="cuda")
+    W.device_rows(args.config, 0, n, x.data_ptr())
+    torch.cuda.synchronize()
+    fam = ace.SrpFamily(ace.SrpConfig(dim=w.dim, k_bits=w.k_bits, num_tables=w.num_tables,
+                                      seed=w.w_seed))
+    sk = ace.AceSketch(fam, ace.CounterWidth.k32)
+    stream = torch.cuda.current_stream()
+    sk.set_stream(stream.cuda_stream)
+    N.dev().ace_sketch_set_timing(sk.handle, 1)
+    flags = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
+
+    def step():
+        sk.reset()
+        return sk.build_detect(x, flags_out=flags)
+
+    for _ in range(max(3, args.warmup)):
+        rep = step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    launches0 = N.dev().ace_kernel_launches()
+    phase = np.zeros(3)
+    import ctypes as C
+    ms3 = (C.c_double * 3)()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        rep = step()
+        N.dev().ace_sketch_timings(sk.handle, ms3)
+        phase += np.array(ms3[:])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = N.dev().ace_kernel_launches() - launches0
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    value = n * ws / (ms * 1e-3)
+    phase /= args.steps
+
+    # e2e: same metric through the public API from pinned host memory (H2D of
+    # the rows and D2H of the flag bitmap inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.empty((n, w.dim), dtype=torch.float32, pin_memory=True)
+        xh.copy_(x)
+        xnp = xh.numpy()
+        sk_e = ace.AceSketch(fam, ace.CounterWidth.k32)
+        sk_e.set_stream(stream.cuda_stream)
+        for _ in range(2):
+            sk_e.reset()
+            ace._detect(sk_e, xnp, build=True)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        reps = max(3, args.steps // 2)
+        for _ in range(reps):
+            sk_e.reset()
+            ace._detect(sk_e, xnp, build=True)
+        torch.cuda.synchronize()
+        te = (time.perf_counter() - t0) / reps
+        if ws > 1:
+            t = torch.tensor([te], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        e2e = {"value": n * ws / te, "unit": UNIT, "h2d_bytes_per_step": n * w.dim * 4,
+               "d2h_bytes_per_step": ((n + 31) // 32) * 4 + 200,
+               "note": "wall clock around ace_sketch_build_detect with pinned host rows"}
+
+    pk, pk_src = peaks()
+    flops = 2.0 * w.dim * w.k_bits * w.num_tables * n
+    hash_ms = phase[0]
+    fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
+    roofline = {
+        "bound": "fp32",
+        "kernel": "hash_simt_kernel (SIMT FP32 projection + FP64 near-tie recheck + packing + fused insert)",
+        "achieved": flops / (hash_ms * 1e-3) / 1e12 if hash_ms > 0 else None,
+        "peak": fp32_peak,
+        "unit": "TFLOP/s",
+        "frac": (flops / (hash_ms * 1e-3) / 1e12) / fp32_peak if hash_ms > 0 else None,
+        "traffic": None,
+        "peak_source": "spec-derived FP32 FFMA: 148 SM x 128 lanes x 2 x 1.965 GHz "
+                       f"(bf16 tensor peak for reference: {pk.get('bf16_tflops')} TF/s {pk_src})",
+        "algorithmic_flops_per_launch": flops,
+        "kernel_share_of_step": hash_ms / ms if ms else None,
+    }
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": f"synthetic (datagen cfg {args.config}, seed {w.data_seed})",
+        "config": {"workload": f"cfg{args.config} {w.name}: build_sketch + detect_batch",
+                   "N": n, "d": w.dim, "K": w.k_bits, "L": w.num_tables, "counter_width": 32,
+                   "l2": f"inputs {n * w.dim * 4 / 1e6:.0f} MB > 126 MB L2 (no flush needed)",
+                   "parallelism": f"replicas x{ws}"},
+        "roofline": roofline,
+        "phases_ms": {"hash_insert": phase[0], "score": phase[1], "threshold_flags": phase[2]},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "e2e": e2e,
+        "exactness": {"rechecked": int(rep.stats.rechecked), "flipped": int(rep.stats.flipped),
+                      "ambiguous": int(rep.ambiguous), "replayed": bool(rep.replayed),
+                      "reported": int(rep.reported)},
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.config, min(args.cpu_sample, n))
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

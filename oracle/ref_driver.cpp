@@ -1,0 +1,249 @@
+// ref_driver.cpp — extern "C" harness around the UNMODIFIED reference ACE
+// library, compiled from /root/reference/proj/src by oracle/Makefile into
+// oracle/_ref/libaceref.so (git-ignored; travels to the GPU box prebuilt).
+//
+// TEST / BASELINE INFRASTRUCTURE ONLY: used by tests/ to pin the C oracle and
+// generate golden digests, and by bench.py's cpu_baseline and --impl
+// reference legs to time the reference's own CPU implementation.  Every call
+// below goes through the reference's public API (proj/include/ace/*.hpp).
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "ace/detect.hpp"
+#include "ace/errors.hpp"
+#include "ace/estimators.hpp"
+#include "ace/sketch.hpp"
+#include "ace/srp.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+ace::SrpConfig make_cfg(uint64_t dim, uint32_t k, uint32_t l, uint64_t seed) {
+  ace::SrpConfig c;
+  c.dim = dim;
+  c.k_bits = k;
+  c.num_tables = l;
+  c.seed = seed;
+  return c;
+}
+
+struct RefSketch {
+  ace::AceSketch sketch;
+  RefSketch(const ace::SrpFamily& f, ace::CounterWidth w) : sketch(f, w) {}
+};
+
+std::vector<double> row_f64(const float* x, uint64_t dim, uint64_t i) {
+  std::vector<double> r(dim);
+  for (uint64_t c = 0; c < dim; ++c) r[c] = static_cast<double>(x[i * dim + c]);
+  return r;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// W via SrpFamily::direction (srp.cpp:115-123), row t*K+b.
+int ref_directions(uint64_t seed, uint64_t dim, uint32_t k, uint32_t l, double* w) {
+  try {
+    ace::SrpFamily fam(make_cfg(dim, k, l, seed));
+    for (uint32_t t = 0; t < l; ++t)
+      for (uint32_t b = 0; b < k; ++b) {
+        auto v = fam.direction(t, b);
+        std::memcpy(w + (static_cast<uint64_t>(t) * k + b) * dim, v.data(), dim * sizeof(double));
+      }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// Bucket ids via SrpFamily::bucket (srp.cpp:106-113), table-major ids[t*n+i],
+// rows as (double) of fp32 X; `threads` workers (bucket is const, thread-safe).
+int ref_buckets(uint64_t seed, uint64_t dim, uint32_t k, uint32_t l, const float* x,
+                uint64_t n, uint32_t* ids, int threads) {
+  try {
+    const ace::SrpFamily fam(make_cfg(dim, k, l, seed));
+    if (threads < 1) threads = 1;
+    std::vector<std::thread> pool;
+    const uint64_t chunk = (n + threads - 1) / threads;
+    for (int w = 0; w < threads; ++w) {
+      const uint64_t lo = std::min<uint64_t>(n, w * chunk), hi = std::min<uint64_t>(n, lo + chunk);
+      pool.emplace_back([&, lo, hi] {
+        for (uint64_t i = lo; i < hi; ++i) {
+          const auto r = row_f64(x, dim, i);
+          for (uint32_t t = 0; t < l; ++t) ids[static_cast<uint64_t>(t) * n + i] = fam.bucket(t, r);
+        }
+      });
+    }
+    for (auto& t : pool) t.join();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+void* ref_sketch_new(uint64_t seed, uint64_t dim, uint32_t k, uint32_t l, uint32_t width) {
+  try {
+    const ace::SrpFamily fam(make_cfg(dim, k, l, seed));
+    return new RefSketch(fam, width == 16 ? ace::CounterWidth::k16 : ace::CounterWidth::k32);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+void ref_sketch_free(void* h) { delete static_cast<RefSketch*>(h); }
+
+// AceSketch::insert (sketch.cpp:50-72) for each row in order.
+int ref_sketch_insert(void* h, const float* x, uint64_t n, uint64_t dim) {
+  try {
+    auto& s = static_cast<RefSketch*>(h)->sketch;
+    for (uint64_t i = 0; i < n; ++i) s.insert(row_f64(x, dim, i));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+int ref_sketch_insert_f64(void* h, const double* x, uint64_t n, uint64_t dim) {
+  try {
+    auto& s = static_cast<RefSketch*>(h)->sketch;
+    for (uint64_t i = 0; i < n; ++i) s.insert(std::span<const double>(x + i * dim, dim));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// AceSketch::remove (sketch.cpp:74-106); returns -2 on InconsistentDelete.
+int ref_sketch_remove(void* h, const float* x, uint64_t n, uint64_t dim) {
+  try {
+    auto& s = static_cast<RefSketch*>(h)->sketch;
+    for (uint64_t i = 0; i < n; ++i) s.remove(row_f64(x, dim, i));
+    return 0;
+  } catch (const ace::InconsistentDelete& e) {
+    g_err = e.what();
+    return -2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// AceSketch::score (sketch.cpp:108-116).
+int ref_sketch_score(void* h, const float* x, uint64_t n, uint64_t dim, double* scores) {
+  try {
+    auto& s = static_cast<RefSketch*>(h)->sketch;
+    for (uint64_t i = 0; i < n; ++i) scores[i] = s.score(row_f64(x, dim, i)).value;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+uint64_t ref_sketch_size(void* h) { return static_cast<RefSketch*>(h)->sketch.size(); }
+double ref_sketch_mean(void* h) { return static_cast<RefSketch*>(h)->sketch.mean(); }
+int ref_sketch_saturated(void* h) { return static_cast<RefSketch*>(h)->sketch.saturated(); }
+
+void ref_sketch_counters(void* h, uint64_t* out) {
+  const auto flat = static_cast<RefSketch*>(h)->sketch.counters_flat();
+  std::memcpy(out, flat.data(), flat.size() * sizeof(uint64_t));
+}
+
+// detect_batch (detect.cpp:12-74) on the rows; also returns the per-row flags
+// (score < threshold, the reference's own rule at detect.cpp:60, recomputed
+// from AceSketch::score since the report carries only counts).
+int ref_detect_batch(void* h, const float* x, uint64_t n, uint64_t dim, unsigned threads,
+                     double* mean, double* sd, double* thr, uint64_t* reported,
+                     double* elapsed, uint8_t* flags) {
+  try {
+    auto& s = static_cast<RefSketch*>(h)->sketch;
+    ace::Dataset data;
+    data.rows = n;
+    data.cols = dim;
+    data.values.resize(n * dim);
+    for (uint64_t i = 0; i < n * dim; ++i) data.values[i] = static_cast<double>(x[i]);
+    const auto rep = ace::detect_batch(s, data, threads);
+    *mean = rep.score_mean;
+    *sd = rep.score_stddev;
+    *thr = rep.threshold;
+    *reported = rep.reported;
+    *elapsed = rep.elapsed_seconds;
+    if (flags)
+      for (uint64_t i = 0; i < n; ++i) flags[i] = s.score(data.row(i)).value < rep.threshold;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// Streaming batch: detect_stream (detect.cpp:76-84) for every row against the
+// counts at batch start (empty sketch -> flag 0, where detect_stream throws),
+// then insert the rows in order.
+int ref_stream_batch(void* h, const float* x, uint64_t n, uint64_t dim, double alpha,
+                     double* scores, uint8_t* flags) {
+  try {
+    auto& s = static_cast<RefSketch*>(h)->sketch;
+    for (uint64_t i = 0; i < n; ++i) {
+      const auto r = row_f64(x, dim, i);
+      if (s.size() == 0) {
+        if (scores) scores[i] = s.score(r).value;
+        if (flags) flags[i] = 0;
+      } else {
+        const auto [est, flag] = ace::detect_stream(s, r, alpha);
+        if (scores) scores[i] = est.value;
+        if (flags) flags[i] = flag;
+      }
+    }
+    for (uint64_t i = 0; i < n; ++i) s.insert(row_f64(x, dim, i));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// CPU baseline timing: insert rows on 1 core (single-writer), then score them
+// with detect_batch on `threads` cores (0 = hardware_concurrency).  Seconds.
+int ref_time_build_detect(uint64_t seed, const float* x, uint64_t n, uint64_t dim, uint32_t k,
+                          uint32_t l, unsigned threads, double* t_insert, double* t_detect,
+                          uint64_t* reported) {
+  try {
+    const ace::SrpFamily fam(make_cfg(dim, k, l, seed));
+    ace::AceSketch s(fam, ace::CounterWidth::k32);
+    ace::Dataset data;
+    data.rows = n;
+    data.cols = dim;
+    data.values.resize(n * dim);
+    for (uint64_t i = 0; i < n * dim; ++i) data.values[i] = static_cast<double>(x[i]);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (uint64_t i = 0; i < n; ++i) s.insert(data.row(i));
+    const auto t1 = std::chrono::steady_clock::now();
+    const auto rep = ace::detect_batch(s, data, threads);
+    const auto t2 = std::chrono::steady_clock::now();
+    *t_insert = std::chrono::duration<double>(t1 - t0).count();
+    *t_detect = std::chrono::duration<double>(t2 - t1).count();
+    *reported = rep.reported;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,715 @@
+// C ABI of libace_dev.so (include/ace_b200.h): handles, staging, pipelines.
+// Each entry point cites the reference function it stands in for.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "ace_kernels.cuh"
+
+namespace ace_dev {
+
+thread_local std::string g_err;
+std::atomic<unsigned long long> g_launches{0};
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+}  // namespace ace_dev
+
+using namespace ace_dev;
+
+namespace {
+
+constexpr uint32_t kMaxKBits = 30;  // srp.cpp:15
+
+ace_status fail(ace_status code, const std::string& msg) {
+  set_error(msg);
+  return code;
+}
+
+#define ACE_CUDA(call)                                                                     \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(e_ == cudaErrorMemoryAllocation ? ACE_E_NOMEM : ACE_E_CUDA,              \
+                  std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #call);    \
+  } while (0)
+
+// Growable device buffer.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    size_t grow = std::max(want, static_cast<size_t>(1) << 20);
+    cudaError_t e = cudaMalloc(&p, grow);
+    if (e == cudaSuccess) bytes = grow;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+}  // namespace
+
+struct AceFamily {
+  FamilyDev d{};
+  float margin_c = 0.f;
+  std::atomic<int> refs{1};
+};
+
+struct AceSketch {
+  AceFamily* fam = nullptr;
+  uint32_t width = 32;
+  uint32_t cap = 0xffffffffu;
+  uint64_t num_counters = 0;
+  uint32_t* counters = nullptr;
+  DevState* st = nullptr;    // device
+  DevState* hst = nullptr;   // pinned host mirror
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  DevBuf ids, sums, stage, flags, scores, demand;
+  // phase timing (ace_sketch_set_timing)
+  bool timing = false;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool ev_used[4] = {false, false, false, false};
+  void mark(int i) {
+    if (timing) {
+      cudaEventRecord(ev[i], stream);
+      ev_used[i] = true;
+    }
+  }
+};
+
+namespace {
+
+void family_release(AceFamily* f) {
+  if (!f) return;
+  if (f->refs.fetch_sub(1) == 1) {
+    cudaFree(f->d.w64);
+    cudaFree(f->d.w32t);
+    cudaFree(f->d.wnorm);
+    delete f;
+  }
+}
+
+ace_status check_x(const AceFamily* f, const void* x, int dtype, uint64_t n, uint64_t ld,
+                   int where) {
+  if (dtype != ACE_F32 && dtype != ACE_F64) return fail(ACE_E_CONTRACT, "ace: dtype must be ACE_F32 or ACE_F64");
+  if (where != ACE_HOST && where != ACE_DEVICE) return fail(ACE_E_CONTRACT, "ace: bad memory location");
+  if (n > 0 && !x) return fail(ACE_E_CONTRACT, "ace: null point matrix");
+  if (ld < f->d.dim)
+    return fail(ACE_E_CONTRACT, "AceSketch: expected vector of length " + std::to_string(f->d.dim) +
+                                    ", received row stride " + std::to_string(ld));
+  return ACE_OK;
+}
+
+// Device view of the point matrix (copies host input into the staging buffer).
+ace_status stage_x(AceSketch* sk, DevBuf& stage, cudaStream_t s, const void* x, int dtype,
+                   uint64_t n, uint64_t ld, int where, const void** xd, uint64_t* ldd) {
+  if (where == ACE_DEVICE || n == 0) {
+    *xd = x;
+    *ldd = ld;
+    return ACE_OK;
+  }
+  const size_t esz = dtype == ACE_F64 ? 8 : 4;
+  const uint64_t dim = sk ? sk->fam->d.dim : 0;
+  (void)dim;
+  ACE_CUDA(stage.ensure(n * ld * esz));
+  ACE_CUDA(cudaMemcpyAsync(stage.p, x, n * ld * esz, cudaMemcpyHostToDevice, s));
+  *xd = stage.p;
+  *ldd = ld;
+  return ACE_OK;
+}
+
+HashArgs make_hash_args(const AceFamily* f, const void* xd, int dtype, uint64_t n, uint64_t ld,
+                        uint32_t* ids, uint64_t stride, DevState* st) {
+  HashArgs a{};
+  a.x = xd;
+  a.x_f64 = dtype == ACE_F64;
+  a.n = n;
+  a.ld = ld;
+  a.fam = f->d;
+  a.margin_c = f->margin_c;
+  a.ids = ids;
+  a.ids_stride = stride;
+  a.id_base = 0;
+  a.counters = nullptr;
+  a.insert = 0;
+  a.cap = 0xffffffffu;
+  a.st = st;
+  return a;
+}
+
+// Zero the per-call accumulators (sum_lo .. underflow are contiguous).
+cudaError_t zero_call_fields(AceSketch* sk) {
+  char* base = reinterpret_cast<char*>(sk->st);
+  const size_t off = offsetof(DevState, sum_lo);
+  const size_t end = offsetof(DevState, underflow) + sizeof(unsigned long long);
+  return cudaMemsetAsync(base + off, 0, end - off, sk->stream);
+}
+
+ace_status pull_state(AceSketch* sk) {
+  ACE_CUDA(cudaMemcpyAsync(sk->hst, sk->st, sizeof(DevState), cudaMemcpyDeviceToHost, sk->stream));
+  ACE_CUDA(cudaStreamSynchronize(sk->stream));
+  return ACE_OK;
+}
+
+double host_mean(const DevState& s, uint32_t tables) {
+  if (s.n == 0) return 0.0;
+  const unsigned long long den = s.n * tables;
+  return static_cast<double>(s.T / den) + static_cast<double>(s.T % den) / static_cast<double>(den);
+}
+
+void fill_stats(AceHashStats* stats, const DevState& s, uint64_t n, const AceFamily* f) {
+  if (!stats) return;
+  stats->projections = n * f->d.rows;
+  stats->rechecked = s.rechecked;
+  stats->flipped = s.flipped;
+}
+
+ace_status copy_out(void* dst, const void* src, size_t bytes, int where, cudaStream_t s) {
+  if (!dst || bytes == 0) return ACE_OK;
+  ACE_CUDA(cudaMemcpyAsync(dst, src, bytes,
+                           where == ACE_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+  return ACE_OK;
+}
+
+// hash n rows into sk->ids (table-major, stride n); optional fused insert.
+ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64_t ld, int insert) {
+  const AceFamily* f = sk->fam;
+  ACE_CUDA(sk->ids.ensure(static_cast<size_t>(n) * f->d.tables * sizeof(uint32_t)));
+  for (bool& u : sk->ev_used) u = false;
+  sk->mark(0);
+  HashArgs a = make_hash_args(f, xd, dtype, n, ld, sk->ids.as<uint32_t>(), n, sk->st);
+  a.insert = insert;
+  a.counters = sk->counters;
+  a.cap = sk->cap;
+  ACE_CUDA(launch_hash_simt(a, sk->stream));
+  if (insert && sk->width == 16)
+    ACE_CUDA(launch_cap(sk->counters, sk->num_counters, sk->cap, sk->st, sk->stream));
+  sk->mark(1);
+  return ACE_OK;
+}
+
+// score from sk->ids; threshold + flags; fills report.
+ace_status run_detect_tail(AceSketch* sk, uint64_t n, uint32_t* flag_bits, double* scores,
+                           int out_where, AceBatchReport* report) {
+  const AceFamily* f = sk->fam;
+  ACE_CUDA(sk->sums.ensure(n * sizeof(uint64_t)));
+  ACE_CUDA(sk->flags.ensure(((n + 31) / 32) * sizeof(uint32_t)));
+  double* dscores = nullptr;
+  if (scores) {
+    if (out_where == ACE_DEVICE) {
+      dscores = scores;
+    } else {
+      ACE_CUDA(sk->scores.ensure(n * sizeof(double)));
+      dscores = sk->scores.as<double>();
+    }
+  }
+  uint32_t* dflags = (flag_bits && out_where == ACE_DEVICE) ? flag_bits : sk->flags.as<uint32_t>();
+  ACE_CUDA(launch_score(sk->ids.as<uint32_t>(), n, n, f->d.tables, f->d.k_bits, sk->counters,
+                        sk->sums.as<uint64_t>(), dscores, sk->st, sk->stream));
+  sk->mark(2);
+  ACE_CUDA(launch_finalize_batch(n, f->d.tables, sk->st, sk->stream));
+  ACE_CUDA(launch_flags(sk->sums.as<uint64_t>(), n, dflags, sk->st, 0, sk->stream));
+  ACE_CUDA(launch_replay(sk->sums.as<uint64_t>(), n, f->d.tables, sk->st, sk->stream));
+  ACE_CUDA(launch_flags(sk->sums.as<uint64_t>(), n, dflags, sk->st, 1, sk->stream));
+  sk->mark(3);
+  if (flag_bits && out_where == ACE_HOST) {
+    ace_status r = copy_out(flag_bits, dflags, ((n + 31) / 32) * sizeof(uint32_t), ACE_HOST, sk->stream);
+    if (r != ACE_OK) return r;
+  }
+  if (scores && out_where == ACE_HOST) {
+    ace_status r = copy_out(scores, dscores, n * sizeof(double), ACE_HOST, sk->stream);
+    if (r != ACE_OK) return r;
+  }
+  ace_status r = pull_state(sk);
+  if (r != ACE_OK) return r;
+  const DevState& s = *sk->hst;
+  if (s.sum_hi != 0) return fail(ACE_E_DATA, "detect_batch: score sum exceeds 2^64");
+  if (report) {
+    report->score_mean = s.mean;
+    report->score_stddev = s.sd;
+    report->threshold = s.thr;
+    report->reported = s.reported;
+    report->ambiguous = s.ambiguous;
+    report->replayed = s.replayed;
+  }
+  return ACE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ace_last_error(void) { return g_err.c_str(); }
+
+const char* ace_version(void) { return "ace-b200 0.1 sm_100a"; }
+
+int ace_device_available(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n > 0;
+}
+
+uint64_t ace_kernel_launches(void) { return g_launches.load(); }
+
+// SrpFamily::SrpFamily (srp.cpp:24-49): validation + W upload.
+ace_status ace_family_create(uint64_t dim, uint32_t k_bits, uint32_t num_tables, double noise_scale,
+                             const double* w_host, AceFamily** out) {
+  if (!out) return fail(ACE_E_CONTRACT, "ace_family_create: null out");
+  *out = nullptr;
+  if (dim == 0) return fail(ACE_E_CONTRACT, "SrpFamily: dim must be >= 1");
+  if (k_bits < 1 || k_bits > kMaxKBits)
+    return fail(ACE_E_CONTRACT, "SrpFamily: k_bits must be in [1, " + std::to_string(kMaxKBits) + "]");
+  if (num_tables < 1) return fail(ACE_E_CONTRACT, "SrpFamily: num_tables must be >= 1");
+  if (noise_scale < 0.0) return fail(ACE_E_CONTRACT, "SrpFamily: noise_scale must be >= 0");
+  if (noise_scale > 0.0)
+    return fail(ACE_E_UNSUPPORTED,
+                "SrpFamily: the noisy (private) hash variant has no device path");
+  if (!w_host) return fail(ACE_E_CONTRACT, "ace_family_create: null W");
+  if (!ace_device_available()) return fail(ACE_E_CUDA, "ace: no CUDA device available");
+
+  AceFamily* f = new AceFamily();
+  FamilyDev& d = f->d;
+  d.dim = dim;
+  d.k_bits = k_bits;
+  d.tables = num_tables;
+  d.rows = k_bits * num_tables;
+  d.tpt = static_cast<uint32_t>(kTileCols) / k_bits;
+  d.ntiles = (num_tables + d.tpt - 1) / d.tpt;
+  d.ncols = d.ntiles * kTileCols;
+  d.dpad = (dim + 31) / 32 * 32;
+  // fast-path error bound: fp32 FMA fold of fp32-rounded W and x against
+  // the binary64 fold, relative to ||w|| ||x||.
+  f->margin_c = static_cast<float>((static_cast<double>(dim) + 6.0) * 0x1.0p-24 * 1.01);
+
+  std::vector<float> w32t(static_cast<size_t>(d.dpad) * d.ncols, 0.0f);
+  std::vector<float> wn(d.ncols, 0.0f);
+  for (uint32_t j = 0; j < d.ntiles; ++j)
+    for (uint32_t c = 0; c < d.tpt * k_bits; ++c) {
+      const uint32_t table = j * d.tpt + c / k_bits;
+      if (table >= num_tables) continue;
+      const uint64_t r = static_cast<uint64_t>(table) * k_bits + c % k_bits;
+      double ss = 0.0;
+      for (uint64_t i = 0; i < dim; ++i) {
+        const double w = w_host[r * dim + i];
+        w32t[i * d.ncols + j * kTileCols + c] = static_cast<float>(w);
+        ss += w * w;
+      }
+      float nb = static_cast<float>(std::sqrt(ss) * (1.0 + 1e-12));
+      wn[j * kTileCols + c] = std::nextafter(nb, INFINITY);
+    }
+  auto cleanup = [&]() { family_release(f); };
+  cudaError_t e;
+  if ((e = cudaMalloc(&d.w64, sizeof(double) * d.rows * dim)) != cudaSuccess ||
+      (e = cudaMalloc(&d.w32t, sizeof(float) * w32t.size())) != cudaSuccess ||
+      (e = cudaMalloc(&d.wnorm, sizeof(float) * wn.size())) != cudaSuccess ||
+      (e = cudaMemcpy(d.w64, w_host, sizeof(double) * d.rows * dim, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(d.w32t, w32t.data(), sizeof(float) * w32t.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(d.wnorm, wn.data(), sizeof(float) * wn.size(), cudaMemcpyHostToDevice)) != cudaSuccess) {
+    cleanup();
+    return fail(e == cudaErrorMemoryAllocation ? ACE_E_NOMEM : ACE_E_CUDA,
+                std::string("ace_family_create: ") + cudaGetErrorString(e));
+  }
+  *out = f;
+  return ACE_OK;
+}
+
+ace_status ace_family_destroy(AceFamily* fam) {
+  family_release(fam);
+  return ACE_OK;
+}
+
+// SrpFamily::bucket (srp.cpp:106-113) for every row and table.
+ace_status ace_family_buckets(AceFamily* fam, const void* x, int dtype, uint64_t n, uint64_t ld,
+                              int x_where, uint32_t* ids, int ids_where, AceHashStats* stats) {
+  if (!fam) return fail(ACE_E_CONTRACT, "ace_family_buckets: null family");
+  ace_status r = check_x(fam, x, dtype, n, ld, x_where);
+  if (r != ACE_OK) return r;
+  AceSketch* sk = nullptr;
+  r = ace_sketch_create(fam, 32, &sk);
+  if (r != ACE_OK) return r;
+  const void* xd;
+  uint64_t ldd;
+  r = stage_x(sk, sk->stage, sk->stream, x, dtype, n, ld, x_where, &xd, &ldd);
+  if (r == ACE_OK) r = run_hash(sk, xd, dtype, n, ldd, 0);
+  if (r == ACE_OK && n)
+    r = copy_out(ids, sk->ids.p, static_cast<size_t>(n) * fam->d.tables * sizeof(uint32_t),
+                 ids_where, sk->stream);
+  if (r == ACE_OK) r = pull_state(sk);
+  if (r == ACE_OK) fill_stats(stats, *sk->hst, n, fam);
+  ace_sketch_destroy(sk);
+  return r;
+}
+
+// AceSketch::AceSketch (sketch.cpp:10-17): zeroed table-major counters.
+ace_status ace_sketch_create(AceFamily* fam, uint32_t counter_width, AceSketch** out) {
+  if (!out || !fam) return fail(ACE_E_CONTRACT, "ace_sketch_create: null argument");
+  *out = nullptr;
+  if (counter_width != 16 && counter_width != 32)
+    return fail(ACE_E_CONTRACT, "AceSketch: counter width must be 16 or 32");
+  AceSketch* sk = new AceSketch();
+  sk->fam = fam;
+  fam->refs.fetch_add(1);
+  sk->width = counter_width;
+  sk->cap = counter_width == 16 ? 0xffffu : 0xffffffffu;
+  sk->num_counters = static_cast<uint64_t>(fam->d.tables) << fam->d.k_bits;
+  cudaError_t e;
+  if ((e = cudaStreamCreateWithFlags(&sk->own, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaMalloc(&sk->counters, sk->num_counters * sizeof(uint32_t))) != cudaSuccess ||
+      (e = cudaMalloc(&sk->st, sizeof(DevState))) != cudaSuccess ||
+      (e = cudaMallocHost(&sk->hst, sizeof(DevState))) != cudaSuccess) {
+    ace_sketch_destroy(sk);
+    return fail(e == cudaErrorMemoryAllocation ? ACE_E_NOMEM : ACE_E_CUDA,
+                std::string("ace_sketch_create: ") + cudaGetErrorString(e));
+  }
+  sk->stream = sk->own;
+  memset(sk->hst, 0, sizeof(DevState));
+  ace_status r = ace_sketch_reset(sk);
+  if (r != ACE_OK) {
+    ace_sketch_destroy(sk);
+    return r;
+  }
+  *out = sk;
+  return ACE_OK;
+}
+
+ace_status ace_sketch_reset(AceSketch* sk) {
+  if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_reset: null sketch");
+  ACE_CUDA(cudaMemsetAsync(sk->counters, 0, sk->num_counters * sizeof(uint32_t), sk->stream));
+  ACE_CUDA(cudaMemsetAsync(sk->st, 0, sizeof(DevState), sk->stream));
+  ACE_CUDA(cudaStreamSynchronize(sk->stream));
+  memset(sk->hst, 0, sizeof(DevState));
+  return ACE_OK;
+}
+
+ace_status ace_sketch_clone(const AceSketch* src, AceSketch** out) {
+  if (!src || !out) return fail(ACE_E_CONTRACT, "ace_sketch_clone: null argument");
+  ace_status r = ace_sketch_create(src->fam, src->width, out);
+  if (r != ACE_OK) return r;
+  AceSketch* d = *out;
+  ACE_CUDA(cudaStreamSynchronize(src->stream));
+  ACE_CUDA(cudaMemcpyAsync(d->counters, src->counters, src->num_counters * sizeof(uint32_t),
+                           cudaMemcpyDeviceToDevice, d->stream));
+  ACE_CUDA(cudaMemcpyAsync(d->st, src->st, sizeof(DevState), cudaMemcpyDeviceToDevice, d->stream));
+  return pull_state(d);
+}
+
+ace_status ace_sketch_destroy(AceSketch* sk) {
+  if (!sk) return ACE_OK;
+  if (sk->stream) cudaStreamSynchronize(sk->stream);
+  sk->ids.release();
+  sk->sums.release();
+  sk->stage.release();
+  sk->flags.release();
+  sk->scores.release();
+  sk->demand.release();
+  if (sk->counters) cudaFree(sk->counters);
+  if (sk->st) cudaFree(sk->st);
+  if (sk->hst) cudaFreeHost(sk->hst);
+  if (sk->own) cudaStreamDestroy(sk->own);
+  for (cudaEvent_t& e : sk->ev)
+    if (e) cudaEventDestroy(e);
+  family_release(sk->fam);
+  delete sk;
+  return ACE_OK;
+}
+
+ace_status ace_sketch_set_stream(AceSketch* sk, void* cuda_stream) {
+  if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_set_stream: null sketch");
+  ACE_CUDA(cudaStreamSynchronize(sk->stream));
+  sk->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : sk->own;
+  return ACE_OK;
+}
+
+// AceSketch::insert (sketch.cpp:50-72), rows in order.
+ace_status ace_sketch_insert(AceSketch* sk, const void* x, int dtype, uint64_t n, uint64_t ld,
+                             int x_where, AceHashStats* stats) {
+  if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_insert: null sketch");
+  ace_status r = check_x(sk->fam, x, dtype, n, ld, x_where);
+  if (r != ACE_OK) return r;
+  ACE_CUDA(zero_call_fields(sk));
+  const void* xd;
+  uint64_t ldd;
+  r = stage_x(sk, sk->stage, sk->stream, x, dtype, n, ld, x_where, &xd, &ldd);
+  if (r == ACE_OK && n) r = run_hash(sk, xd, dtype, n, ldd, 1);
+  if (r == ACE_OK) r = pull_state(sk);
+  if (r == ACE_OK) fill_stats(stats, *sk->hst, n, sk->fam);
+  return r;
+}
+
+// AceSketch::remove (sketch.cpp:74-106), all-or-nothing over the batch.
+ace_status ace_sketch_remove(AceSketch* sk, const void* x, int dtype, uint64_t n, uint64_t ld,
+                             int x_where, AceHashStats* stats) {
+  if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_remove: null sketch");
+  ace_status r = check_x(sk->fam, x, dtype, n, ld, x_where);
+  if (r != ACE_OK) return r;
+  if (n == 0) return ACE_OK;
+  if (sk->width == 16 && sk->hst->saturated)
+    return fail(ACE_E_UNSUPPORTED, "AceSketch: delete from a saturated 16-bit sketch has no exact inverse");
+  ACE_CUDA(zero_call_fields(sk));
+  const void* xd;
+  uint64_t ldd;
+  r = stage_x(sk, sk->stage, sk->stream, x, dtype, n, ld, x_where, &xd, &ldd);
+  if (r == ACE_OK) r = run_hash(sk, xd, dtype, n, ldd, 0);
+  if (r != ACE_OK) return r;
+  ACE_CUDA(sk->demand.ensure(sk->num_counters * sizeof(uint32_t)));
+  ACE_CUDA(launch_remove_check(sk->ids.as<uint32_t>(), n, sk->fam->d.tables, sk->fam->d.k_bits,
+                               sk->counters, sk->demand.as<uint32_t>(), sk->st, sk->stream));
+  r = pull_state(sk);
+  if (r != ACE_OK) return r;
+  if (sk->hst->underflow)
+    return fail(ACE_E_INCONSISTENT,
+                "AceSketch: delete target counter is zero (item was never inserted)");
+  ACE_CUDA(launch_apply_ids(sk->ids.as<uint32_t>(), n, sk->fam->d.tables, sk->fam->d.k_bits,
+                            sk->counters, sk->cap, -1, sk->st, sk->stream));
+  r = pull_state(sk);
+  if (r == ACE_OK) fill_stats(stats, *sk->hst, n, sk->fam);
+  return r;
+}
+
+// AceSketch::score (sketch.cpp:108-116) for every row.
+ace_status ace_sketch_score(AceSketch* sk, const void* x, int dtype, uint64_t n, uint64_t ld,
+                            int x_where, double* scores, uint64_t* sums, int out_where,
+                            AceHashStats* stats) {
+  if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_score: null sketch");
+  ace_status r = check_x(sk->fam, x, dtype, n, ld, x_where);
+  if (r != ACE_OK) return r;
+  if (n == 0) return ACE_OK;
+  ACE_CUDA(zero_call_fields(sk));
+  const void* xd;
+  uint64_t ldd;
+  r = stage_x(sk, sk->stage, sk->stream, x, dtype, n, ld, x_where, &xd, &ldd);
+  if (r == ACE_OK) r = run_hash(sk, xd, dtype, n, ldd, 0);
+  if (r != ACE_OK) return r;
+  double* dsc = nullptr;
+  uint64_t* dsum = nullptr;
+  if (scores) {
+    if (out_where == ACE_DEVICE) dsc = scores;
+    else {
+      ACE_CUDA(sk->scores.ensure(n * sizeof(double)));
+      dsc = sk->scores.as<double>();
+    }
+  }
+  if (sums) {
+    if (out_where == ACE_DEVICE) dsum = sums;
+    else {
+      ACE_CUDA(sk->sums.ensure(n * sizeof(uint64_t)));
+      dsum = sk->sums.as<uint64_t>();
+    }
+  }
+  ACE_CUDA(launch_score(sk->ids.as<uint32_t>(), n, n, sk->fam->d.tables, sk->fam->d.k_bits,
+                        sk->counters, dsum, dsc, sk->st, sk->stream));
+  if (out_where == ACE_HOST) {
+    if (scores && (r = copy_out(scores, dsc, n * sizeof(double), ACE_HOST, sk->stream)) != ACE_OK) return r;
+    if (sums && (r = copy_out(sums, dsum, n * sizeof(uint64_t), ACE_HOST, sk->stream)) != ACE_OK) return r;
+  }
+  r = pull_state(sk);
+  if (r == ACE_OK) fill_stats(stats, *sk->hst, n, sk->fam);
+  return r;
+}
+
+// detect_batch (detect.cpp:12-74).
+ace_status ace_sketch_detect_batch(AceSketch* sk, const void* x, int dtype, uint64_t n, uint64_t ld,
+                                   int x_where, uint32_t* flag_bits, double* scores, int out_where,
+                                   AceBatchReport* report, AceHashStats* stats) {
+  if (!sk) return fail(ACE_E_CONTRACT, "detect_batch: null sketch");
+  if (n == 0) return fail(ACE_E_CONTRACT, "detect_batch: empty dataset");
+  if (ld < sk->fam->d.dim) return fail(ACE_E_CONTRACT, "detect_batch: data dimension mismatch");
+  ace_status r = check_x(sk->fam, x, dtype, n, ld, x_where);
+  if (r != ACE_OK) return r;
+  const auto t0 = std::chrono::steady_clock::now();
+  ACE_CUDA(zero_call_fields(sk));
+  const void* xd;
+  uint64_t ldd;
+  r = stage_x(sk, sk->stage, sk->stream, x, dtype, n, ld, x_where, &xd, &ldd);
+  if (r == ACE_OK) r = run_hash(sk, xd, dtype, n, ldd, 0);
+  if (r == ACE_OK) r = run_detect_tail(sk, n, flag_bits, scores, out_where, report);
+  if (r == ACE_OK) {
+    fill_stats(stats, *sk->hst, n, sk->fam);
+    if (report)
+      report->elapsed_seconds =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+  return r;
+}
+
+// build_sketch (estimators.cpp:79-92) followed by detect_batch (detect.cpp:12-74).
+ace_status ace_sketch_build_detect(AceSketch* sk, const void* x, int dtype, uint64_t n, uint64_t ld,
+                                   int x_where, uint32_t* flag_bits, double* scores, int out_where,
+                                   AceBatchReport* report, AceHashStats* stats) {
+  if (!sk) return fail(ACE_E_CONTRACT, "build_sketch: null sketch");
+  if (n == 0) return fail(ACE_E_CONTRACT, "build_sketch: empty dataset");
+  ace_status r = check_x(sk->fam, x, dtype, n, ld, x_where);
+  if (r != ACE_OK) return r;
+  const auto t0 = std::chrono::steady_clock::now();
+  ACE_CUDA(zero_call_fields(sk));
+  const void* xd;
+  uint64_t ldd;
+  r = stage_x(sk, sk->stage, sk->stream, x, dtype, n, ld, x_where, &xd, &ldd);
+  if (r == ACE_OK) r = run_hash(sk, xd, dtype, n, ldd, 1);
+  if (r == ACE_OK) r = run_detect_tail(sk, n, flag_bits, scores, out_where, report);
+  if (r == ACE_OK) {
+    fill_stats(stats, *sk->hst, n, sk->fam);
+    if (report)
+      report->elapsed_seconds =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+  return r;
+}
+
+// detect_stream (detect.cpp:76-84) for a batch, then insert (ace_cli.cpp:177-183).
+ace_status ace_sketch_stream_batch(AceSketch* sk, const void* x, int dtype, uint64_t n, uint64_t ld,
+                                   int x_where, double alpha, uint32_t* flag_bits, double* scores,
+                                   int out_where, AceStreamReport* report, AceHashStats* stats) {
+  if (!sk) return fail(ACE_E_CONTRACT, "detect_stream: null sketch");
+  if (!(alpha >= 0.0)) return fail(ACE_E_CONTRACT, "detect_stream: alpha must be >= 0");
+  ace_status r = check_x(sk->fam, x, dtype, n, ld, x_where);
+  if (r != ACE_OK) return r;
+  if (n == 0) return ACE_OK;
+  const AceFamily* f = sk->fam;
+  ACE_CUDA(zero_call_fields(sk));
+  const void* xd;
+  uint64_t ldd;
+  r = stage_x(sk, sk->stage, sk->stream, x, dtype, n, ld, x_where, &xd, &ldd);
+  if (r == ACE_OK) r = run_hash(sk, xd, dtype, n, ldd, 0);
+  if (r != ACE_OK) return r;
+  ACE_CUDA(sk->flags.ensure(((n + 31) / 32) * sizeof(uint32_t)));
+  double* dsc = nullptr;
+  if (scores) {
+    if (out_where == ACE_DEVICE) dsc = scores;
+    else {
+      ACE_CUDA(sk->scores.ensure(n * sizeof(double)));
+      dsc = sk->scores.as<double>();
+    }
+  }
+  uint32_t* dflags = (flag_bits && out_where == ACE_DEVICE) ? flag_bits : sk->flags.as<uint32_t>();
+  ACE_CUDA(launch_stream_score(sk->ids.as<uint32_t>(), n, f->d.tables, f->d.k_bits, sk->counters,
+                               alpha, dflags, dsc, sk->st, sk->stream));
+  sk->mark(2);
+  ACE_CUDA(launch_apply_ids(sk->ids.as<uint32_t>(), n, f->d.tables, f->d.k_bits, sk->counters,
+                            sk->cap, +1, sk->st, sk->stream));
+  if (sk->width == 16) ACE_CUDA(launch_cap(sk->counters, sk->num_counters, sk->cap, sk->st, sk->stream));
+  sk->mark(3);
+  if (out_where == ACE_HOST) {
+    if (flag_bits &&
+        (r = copy_out(flag_bits, dflags, ((n + 31) / 32) * sizeof(uint32_t), ACE_HOST, sk->stream)) != ACE_OK)
+      return r;
+    if (scores && (r = copy_out(scores, dsc, n * sizeof(double), ACE_HOST, sk->stream)) != ACE_OK) return r;
+  }
+  r = pull_state(sk);
+  if (r != ACE_OK) return r;
+  fill_stats(stats, *sk->hst, n, f);
+  if (report) {
+    report->mean_before = sk->hst->mean_before;
+    report->cut = sk->hst->cut;
+    report->reported = sk->hst->reported;
+    report->ambiguous = sk->hst->ambiguous;
+  }
+  return ACE_OK;
+}
+
+// size / mean / saturated (sketch.hpp:44-46).
+ace_status ace_sketch_info(const AceSketch* sk, uint64_t* n, double* mean, int* saturated) {
+  if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_info: null sketch");
+  AceSketch* m = const_cast<AceSketch*>(sk);
+  ace_status r = pull_state(m);
+  if (r != ACE_OK) return r;
+  if (n) *n = sk->hst->n;
+  if (mean) *mean = host_mean(*sk->hst, sk->fam->d.tables);
+  if (saturated) *saturated = sk->hst->saturated;
+  return ACE_OK;
+}
+
+// counters_flat (sketch.cpp:126-130).
+ace_status ace_sketch_counters(const AceSketch* sk, uint64_t* counters) {
+  if (!sk || !counters) return fail(ACE_E_CONTRACT, "ace_sketch_counters: null argument");
+  std::vector<uint32_t> tmp(sk->num_counters);
+  ACE_CUDA(cudaMemcpyAsync(tmp.data(), sk->counters, sk->num_counters * sizeof(uint32_t),
+                           cudaMemcpyDeviceToHost, sk->stream));
+  ACE_CUDA(cudaStreamSynchronize(sk->stream));
+  for (uint64_t i = 0; i < sk->num_counters; ++i) counters[i] = tmp[i];
+  return ACE_OK;
+}
+
+ace_status ace_sketch_counters_u32(const AceSketch* sk, uint32_t* counters, int where) {
+  if (!sk || !counters) return fail(ACE_E_CONTRACT, "ace_sketch_counters_u32: null argument");
+  ACE_CUDA(cudaMemcpyAsync(counters, sk->counters, sk->num_counters * sizeof(uint32_t),
+                           where == ACE_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                           sk->stream));
+  ACE_CUDA(cudaStreamSynchronize(sk->stream));
+  return ACE_OK;
+}
+
+// AceSketch::restore (sketch.cpp:132-150).
+ace_status ace_sketch_restore(AceSketch* sk, const uint64_t* counters, uint64_t num_counters,
+                              uint64_t n, double mean, int saturated) {
+  if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_restore: null sketch");
+  if (num_counters != sk->num_counters)
+    return fail(ACE_E_CONTRACT, "AceSketch::restore: counter payload size " + std::to_string(num_counters) +
+                                    " does not match L * 2^K = " + std::to_string(sk->num_counters));
+  std::vector<uint32_t> tmp(num_counters);
+  for (uint64_t i = 0; i < num_counters; ++i) {
+    if (counters[i] > sk->cap) return fail(ACE_E_CONTRACT, "AceSketch::restore: counter exceeds width");
+    tmp[i] = static_cast<uint32_t>(counters[i]);
+  }
+  ACE_CUDA(cudaMemcpyAsync(sk->counters, tmp.data(), num_counters * sizeof(uint32_t),
+                           cudaMemcpyHostToDevice, sk->stream));
+  ACE_CUDA(cudaStreamSynchronize(sk->stream));
+  DevState s{};
+  s.n = n;
+  s.T = static_cast<unsigned long long>(std::llround(mean * static_cast<double>(n) * sk->fam->d.tables));
+  s.saturated = saturated ? 1 : 0;
+  *sk->hst = s;
+  ACE_CUDA(cudaMemcpyAsync(sk->st, sk->hst, sizeof(DevState), cudaMemcpyHostToDevice, sk->stream));
+  ACE_CUDA(cudaStreamSynchronize(sk->stream));
+  return ACE_OK;
+}
+
+const uint32_t* ace_sketch_device_counters(const AceSketch* sk) { return sk ? sk->counters : nullptr; }
+
+ace_status ace_sketch_set_timing(AceSketch* sk, int enable) {
+  if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_set_timing: null sketch");
+  if (enable)
+    for (cudaEvent_t& e : sk->ev)
+      if (!e) ACE_CUDA(cudaEventCreate(&e));
+  sk->timing = enable != 0;
+  return ACE_OK;
+}
+
+ace_status ace_sketch_timings(const AceSketch* sk, double* ms3) {
+  if (!sk || !ms3) return fail(ACE_E_CONTRACT, "ace_sketch_timings: null argument");
+  for (int i = 0; i < 3; ++i) {
+    ms3[i] = 0.0;
+    if (sk->timing && sk->ev_used[i] && sk->ev_used[i + 1]) {
+      float ms = 0.f;
+      ACE_CUDA(cudaEventSynchronize(sk->ev[i + 1]));
+      ACE_CUDA(cudaEventElapsedTime(&ms, sk->ev[i], sk->ev[i + 1]));
+      ms3[i] = ms;
+    }
+  }
+  return ACE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,367 @@
+// libace.so — the reference's C++ ACE API (include/ace/b200_api.hpp) over the
+// B200 C ABI (include/ace_b200.h).  Host responsibilities only: seeded W
+// generation (construction time, must match glibc libm bit-for-bit, so it
+// cannot move to the device), argument validation, exception mapping, and
+// label tallies.  Every hash / count / score / threshold runs on the GPU.
+#include <cmath>
+#include <cstring>
+#include <numbers>
+#include <string>
+
+#include "ace/b200_api.hpp"
+#include "ace_b200.h"
+
+namespace ace {
+
+namespace {
+
+[[noreturn]] void raise(ace_status st) {
+  const std::string msg = ace_last_error();
+  switch (st) {
+    case ACE_E_CONTRACT: throw ContractViolation(msg);
+    case ACE_E_UNSUPPORTED: throw UnsupportedOperation(msg);
+    case ACE_E_INCONSISTENT: throw InconsistentDelete(msg);
+    case ACE_E_DATA: throw DataError(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+inline void ok(ace_status st) {
+  if (st != ACE_OK) raise(st);
+}
+
+// Stream seed of direction (table, b): srp.cpp:17-20.
+std::uint64_t seed_of(std::uint64_t master, std::size_t table, std::size_t b, std::uint32_t k) {
+  return rng::mix_seed(master, table * k + b);
+}
+
+std::vector<double> generate_w(const SrpConfig& c) {
+  std::vector<double> w(static_cast<std::size_t>(c.k_bits) * c.num_tables * c.dim);
+  for (std::size_t t = 0; t < c.num_tables; ++t)
+    for (std::size_t b = 0; b < c.k_bits; ++b) {
+      rng::NormalStream g(seed_of(c.seed, t, b, c.k_bits));
+      double* out = w.data() + (t * c.k_bits + b) * c.dim;
+      for (std::size_t i = 0; i < c.dim; ++i) out[i] = g.next();
+    }
+  return w;
+}
+
+}  // namespace
+
+// ---- rng: restatement of rng.hpp:10-58 ------------------------------------
+namespace rng {
+std::uint64_t splitmix64(std::uint64_t& state) {
+  std::uint64_t z = (state += 0x9e3779b97f4a7c15ULL);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+std::uint64_t mix_seed(std::uint64_t seed, std::uint64_t index) {
+  std::uint64_t s = seed ^ (0x9e3779b97f4a7c15ULL * (index + 1));
+  return splitmix64(s);
+}
+double unit_double(std::uint64_t bits) { return static_cast<double>((bits >> 11) + 1) * 0x1.0p-53; }
+std::uint64_t bounded(std::uint64_t bits, std::uint64_t bound) {
+  return static_cast<std::uint64_t>((static_cast<unsigned __int128>(bits) * bound) >> 64);
+}
+double NormalStream::next() {
+  if (cached_valid_) {
+    cached_valid_ = false;
+    return cached_;
+  }
+  const double u1 = unit_double(splitmix64(s_));
+  const double u2 = unit_double(splitmix64(s_));
+  const double radius = std::sqrt(-2.0 * std::log(u1));
+  const double angle = 2.0 * std::numbers::pi * u2;
+  cached_ = radius * std::sin(angle);
+  cached_valid_ = true;
+  return radius * std::cos(angle);
+}
+}  // namespace rng
+
+// ---- SrpFamily --------------------------------------------------------------
+SrpFamily::SrpFamily(const SrpConfig& cfg) : cfg_(cfg) {
+  // srp.cpp:25-32
+  if (cfg_.dim == 0) throw ContractViolation("SrpFamily: dim must be >= 1");
+  if (cfg_.k_bits < 1 || cfg_.k_bits > 30) throw ContractViolation("SrpFamily: k_bits must be in [1, 30]");
+  if (cfg_.num_tables < 1) throw ContractViolation("SrpFamily: num_tables must be >= 1");
+  if (cfg_.noise_scale < 0.0) throw ContractViolation("SrpFamily: noise_scale must be >= 0");
+  w_ = std::make_shared<const std::vector<double>>(generate_w(cfg_));
+  dev_ = std::make_shared<std::shared_ptr<::AceFamily>>();
+}
+
+::AceFamily* SrpFamily::device() const {
+  if (!*dev_) {
+    ::AceFamily* f = nullptr;
+    ok(ace_family_create(cfg_.dim, cfg_.k_bits, cfg_.num_tables, cfg_.noise_scale, w_->data(), &f));
+    *dev_ = std::shared_ptr<::AceFamily>(f, [](::AceFamily* p) { ace_family_destroy(p); });
+  }
+  return dev_->get();
+}
+
+void SrpFamily::check(std::size_t table, std::size_t b, std::span<const double> x) const {
+  // srp.cpp:66-76
+  if (x.size() != cfg_.dim)
+    throw ContractViolation("SrpFamily: expected vector of length " + std::to_string(cfg_.dim) +
+                            ", received " + std::to_string(x.size()));
+  if (table >= cfg_.num_tables) throw ContractViolation("SrpFamily: table index out of range");
+  if (b >= cfg_.k_bits) throw ContractViolation("SrpFamily: bit index out of range");
+}
+
+std::uint32_t SrpFamily::bucket(std::size_t table, std::span<const double> x) const {
+  check(table, 0, x);
+  std::vector<std::uint32_t> ids(cfg_.num_tables);
+  ok(ace_family_buckets(device(), x.data(), ACE_F64, 1, cfg_.dim, ACE_HOST, ids.data(), ACE_HOST,
+                        nullptr));
+  return ids[table];
+}
+
+std::uint32_t SrpFamily::bit(std::size_t table, std::size_t b, std::span<const double> x) const {
+  check(table, b, x);
+  return (bucket(table, x) >> (cfg_.k_bits - 1 - b)) & 1u;
+}
+
+std::vector<std::uint32_t> SrpFamily::buckets(std::span<const float> rows, std::size_t n) const {
+  if (rows.size() != n * cfg_.dim) throw ContractViolation("SrpFamily::buckets: rows size != n * dim");
+  std::vector<std::uint32_t> ids(n * cfg_.num_tables);
+  if (n)
+    ok(ace_family_buckets(device(), rows.data(), ACE_F32, n, cfg_.dim, ACE_HOST, ids.data(),
+                          ACE_HOST, nullptr));
+  return ids;
+}
+
+std::vector<double> SrpFamily::direction(std::size_t table, std::size_t b) const {
+  if (table >= cfg_.num_tables || b >= cfg_.k_bits)
+    throw ContractViolation("SrpFamily: direction index out of range");
+  const double* row = w_->data() + (table * cfg_.k_bits + b) * cfg_.dim;
+  return std::vector<double>(row, row + cfg_.dim);
+}
+
+void SrpFamily::reset_noise_stream(std::uint64_t) const {
+  if (cfg_.noise_scale > 0.0)
+    throw UnsupportedOperation("SrpFamily: the noisy hash variant has no device path");
+}
+
+// collision_probability (srp.cpp:130-146): closed-form statistic, not on the
+// hashing path; kept for API completeness.
+double collision_probability(std::span<const double> x, std::span<const double> y) {
+  if (x.size() != y.size()) throw ContractViolation("collision_probability: length mismatch");
+  double xy = 0.0, xx = 0.0, yy = 0.0;
+  for (std::size_t i = 0; i < x.size(); ++i) {
+    xy += x[i] * y[i];
+    xx += x[i] * x[i];
+    yy += y[i] * y[i];
+  }
+  if (xx == 0.0 || yy == 0.0)
+    throw std::domain_error("collision_probability: zero-norm vector, cosine undefined");
+  double c = xy / (std::sqrt(xx) * std::sqrt(yy));
+  c = c < -1.0 ? -1.0 : (c > 1.0 ? 1.0 : c);
+  return 1.0 - std::acos(c) / std::numbers::pi;
+}
+
+// ---- AceSketch --------------------------------------------------------------
+AceSketch::AceSketch(const SrpFamily& family, CounterWidth width) : family_(family), width_(width) {
+  ok(ace_sketch_create(family_.device(), static_cast<std::uint32_t>(width_), &dev_));
+}
+
+AceSketch::AceSketch(const AceSketch& o) : family_(o.family_), width_(o.width_) {
+  ok(ace_sketch_clone(o.dev_, &dev_));
+}
+
+AceSketch& AceSketch::operator=(const AceSketch& o) {
+  if (this == &o) return *this;
+  ::AceSketch* d = nullptr;
+  ok(ace_sketch_clone(o.dev_, &d));
+  ace_sketch_destroy(dev_);
+  dev_ = d;
+  family_ = o.family_;
+  width_ = o.width_;
+  return *this;
+}
+
+AceSketch::AceSketch(AceSketch&& o) noexcept : family_(o.family_), width_(o.width_), dev_(o.dev_) {
+  o.dev_ = nullptr;
+}
+
+AceSketch& AceSketch::operator=(AceSketch&& o) noexcept {
+  if (this != &o) {
+    ace_sketch_destroy(dev_);
+    family_ = o.family_;
+    width_ = o.width_;
+    dev_ = o.dev_;
+    o.dev_ = nullptr;
+  }
+  return *this;
+}
+
+AceSketch::~AceSketch() { ace_sketch_destroy(dev_); }
+
+void AceSketch::check_dim(std::span<const double> x) const {
+  // sketch.cpp:19-24
+  if (x.size() != family_.config().dim)
+    throw ContractViolation("AceSketch: expected vector of length " +
+                            std::to_string(family_.config().dim) + ", received " +
+                            std::to_string(x.size()));
+}
+
+void AceSketch::insert(std::span<const double> x) {
+  check_dim(x);
+  ok(ace_sketch_insert(dev_, x.data(), ACE_F64, 1, x.size(), ACE_HOST, nullptr));
+}
+
+void AceSketch::remove(std::span<const double> x) {
+  check_dim(x);
+  if (family_.config().noise_scale > 0.0)  // sketch.cpp:76-79
+    throw UnsupportedOperation(
+        "AceSketch: delete is unsupported with noisy hashes (buckets are not reproducible)");
+  ok(ace_sketch_remove(dev_, x.data(), ACE_F64, 1, x.size(), ACE_HOST, nullptr));
+}
+
+ScoreEstimate AceSketch::score(std::span<const double> q) const {
+  check_dim(q);
+  double v = 0.0;
+  ok(ace_sketch_score(dev_, q.data(), ACE_F64, 1, q.size(), ACE_HOST, &v, nullptr, ACE_HOST,
+                      nullptr));
+  return {v, family_.config().k_bits, family_.config().num_tables};
+}
+
+void AceSketch::insert_batch(std::span<const float> rows, std::size_t n) {
+  const auto d = family_.config().dim;
+  if (rows.size() != n * d) throw ContractViolation("AceSketch::insert_batch: rows size != n * dim");
+  if (n) ok(ace_sketch_insert(dev_, rows.data(), ACE_F32, n, d, ACE_HOST, nullptr));
+}
+
+std::vector<double> AceSketch::score_batch(std::span<const float> rows, std::size_t n) const {
+  const auto d = family_.config().dim;
+  if (rows.size() != n * d) throw ContractViolation("AceSketch::score_batch: rows size != n * dim");
+  std::vector<double> out(n);
+  if (n)
+    ok(ace_sketch_score(dev_, rows.data(), ACE_F32, n, d, ACE_HOST, out.data(), nullptr, ACE_HOST,
+                        nullptr));
+  return out;
+}
+
+std::uint64_t AceSketch::size() const {
+  std::uint64_t n = 0;
+  ok(ace_sketch_info(dev_, &n, nullptr, nullptr));
+  return n;
+}
+
+double AceSketch::mean() const {
+  double m = 0.0;
+  ok(ace_sketch_info(dev_, nullptr, &m, nullptr));
+  return m;
+}
+
+bool AceSketch::saturated() const {
+  int s = 0;
+  ok(ace_sketch_info(dev_, nullptr, nullptr, &s));
+  return s != 0;
+}
+
+std::size_t AceSketch::counter_bytes() const {
+  return num_counters() * (width_ == CounterWidth::k16 ? 2 : 4);
+}
+
+std::uint64_t AceSketch::counter(std::size_t table, std::size_t bucket) const {
+  if (table >= family_.config().num_tables || bucket >= family_.num_buckets())
+    throw ContractViolation("AceSketch: counter index out of range");
+  return counters_flat()[table * family_.num_buckets() + bucket];
+}
+
+std::vector<std::uint64_t> AceSketch::counters_flat() const {
+  std::vector<std::uint64_t> out(num_counters());
+  ok(ace_sketch_counters(dev_, out.data()));
+  return out;
+}
+
+AceSketch AceSketch::restore(const SrpFamily& family, CounterWidth width,
+                             std::vector<std::uint64_t> counters, std::uint64_t n, double mean,
+                             bool saturated) {
+  AceSketch s(family, width);
+  ok(ace_sketch_restore(s.dev_, counters.data(), counters.size(), n, mean, saturated ? 1 : 0));
+  return s;
+}
+
+// ---- detection --------------------------------------------------------------
+DetectionReport detect_batch(const AceSketch& sketch, const Dataset& data, unsigned) {
+  // detect.cpp:14-16
+  if (data.rows == 0) throw ContractViolation("detect_batch: empty dataset");
+  if (data.cols != sketch.family().config().dim)
+    throw ContractViolation("detect_batch: data dimension mismatch");
+  std::vector<std::uint32_t> bits((data.rows + 31) / 32);
+  AceBatchReport r{};
+  ok(ace_sketch_detect_batch(sketch.device(), data.values.data(), ACE_F64, data.rows, data.cols,
+                             ACE_HOST, bits.data(), nullptr, ACE_HOST, &r, nullptr));
+  DetectionReport rep;
+  rep.reported = r.reported;
+  rep.threshold = r.threshold;
+  rep.score_mean = r.score_mean;
+  rep.score_stddev = r.score_stddev;
+  rep.elapsed_seconds = r.elapsed_seconds;
+  rep.has_labels = data.labels.has_value();
+  rep.total_labeled_anomalies = data.labeled_anomalies();
+  if (rep.has_labels)  // label tallies, detect.cpp:59-68
+    for (std::size_t i = 0; i < data.rows; ++i) {
+      const bool flagged = (bits[i >> 5] >> (i & 31)) & 1u;
+      const bool anomalous = (*data.labels)[i] != 0;
+      if (flagged && anomalous) ++rep.correctly_reported;
+      if (!flagged && anomalous) ++rep.missed;
+    }
+  return rep;
+}
+
+std::pair<ScoreEstimate, bool> detect_stream(const AceSketch& sketch, std::span<const double> q,
+                                             double alpha) {
+  // detect.cpp:79-83
+  if (alpha < 0.0) throw ContractViolation("detect_stream: alpha must be >= 0");
+  if (sketch.size() == 0) throw ContractViolation("detect_stream: empty sketch");
+  const ScoreEstimate e = sketch.score(q);
+  return {e, e.value <= sketch.mean() - alpha};
+}
+
+std::vector<std::uint8_t> stream_batch(AceSketch& sketch, std::span<const float> rows, std::size_t n,
+                                       double alpha) {
+  const auto d = sketch.family().config().dim;
+  if (rows.size() != n * d) throw ContractViolation("stream_batch: rows size != n * dim");
+  std::vector<std::uint32_t> bits((n + 31) / 32);
+  std::vector<std::uint8_t> flags(n);
+  if (!n) return flags;
+  ok(ace_sketch_stream_batch(sketch.device(), rows.data(), ACE_F32, n, d, ACE_HOST, alpha,
+                             bits.data(), nullptr, ACE_HOST, nullptr, nullptr));
+  for (std::size_t i = 0; i < n; ++i) flags[i] = (bits[i >> 5] >> (i & 31)) & 1u;
+  return flags;
+}
+
+AceSketch build_sketch(const Dataset& data, std::uint32_t k_bits, std::uint32_t num_tables,
+                       std::uint64_t seed, double noise_scale, CounterWidth width) {
+  // estimators.cpp:79-92
+  if (data.rows == 0) throw ContractViolation("build_sketch: empty dataset");
+  SrpConfig cfg;
+  cfg.dim = data.cols;
+  cfg.k_bits = k_bits;
+  cfg.num_tables = num_tables;
+  cfg.seed = seed;
+  cfg.noise_scale = noise_scale;
+  AceSketch sketch{SrpFamily(cfg), width};
+  ok(ace_sketch_insert(sketch.device(), data.values.data(), ACE_F64, data.rows, data.cols, ACE_HOST,
+                       nullptr));
+  return sketch;
+}
+
+}  // namespace ace
+
+// W generation for non-C++ hosts (the Python mirror): the same generator as
+// SrpFamily's constructor.
+extern "C" int ace_generate_directions(uint64_t seed, uint64_t dim, uint32_t k_bits,
+                                       uint32_t num_tables, double* w) {
+  if (!w || dim == 0 || k_bits < 1 || k_bits > 30 || num_tables < 1) return 1;
+  ace::SrpConfig c;
+  c.dim = dim;
+  c.k_bits = k_bits;
+  c.num_tables = num_tables;
+  c.seed = seed;
+  const auto v = ace::generate_w(c);
+  std::memcpy(w, v.data(), v.size() * sizeof(double));
+  return 0;
+}

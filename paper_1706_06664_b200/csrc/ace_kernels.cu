@@ -1,0 +1,829 @@
+// ACE hot-path kernels for sm_100a (SIMT path + integer pipeline).
+//
+// Reference semantics:
+//   p_{t,b}(x)  = binary64 left fold over i of W[t*K+b][i] * x_i   (srp.cpp:78-91)
+//   bit         = p >= 0 (sign(0) -> 1)                            (srp.cpp:103)
+//   bucket_t(x) = bits packed MSB-first, bit 0 most significant    (srp.cpp:106-113)
+//   insert      = C[t*2^K+bucket]++, numerator += 2*pre+1          (sketch.cpp:50-72)
+//   score       = (sum_t C[t*2^K+bucket_t(q)]) / L                 (sketch.cpp:108-116)
+//   detect      = flag score < mean - stddev (population)          (detect.cpp:44-60)
+//   stream      = flag score <= mean - alpha                       (detect.cpp:76-84)
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "ace_kernels.cuh"
+
+namespace ace_dev {
+
+namespace {
+
+constexpr int BM = 128;          // points per CTA tile
+constexpr int BN = kTileCols;    // directions per CTA tile
+constexpr int BK = 32;           // K-chunk
+constexpr int NT = 256;          // threads
+constexpr int XS = BM + 4;       // padded row of the transposed X tile
+constexpr int NT_CAP = 1024;     // near-tie list capacity per tile
+
+// ---- small helpers -------------------------------------------------------
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// numerator contribution of m consecutive inserts into a counter whose
+// (uncapped) value before them was `old`: sum_{r<m} (2*min(old+r, cap) + 1).
+__device__ __forceinline__ unsigned long long insert_numerator(unsigned long long old,
+                                                               unsigned long long m,
+                                                               unsigned long long cap) {
+  unsigned long long u = old >= cap ? 0ull : (cap - old < m ? cap - old : m);
+  return u * (2ull * old + u) + (m - u) * (2ull * cap + 1ull);
+}
+
+__device__ __forceinline__ void atomic_add_u128(unsigned long long* lo, unsigned long long* hi,
+                                                unsigned long long vlo, unsigned long long vhi) {
+  const unsigned long long old = atomicAdd(lo, vlo);
+  const unsigned long long carry = (old + vlo < old) ? 1ull : 0ull;
+  if (vhi + carry) atomicAdd(hi, vhi + carry);
+}
+
+// Exact reference projection: binary64 mul-then-add fold from +0.0.
+__device__ __forceinline__ double exact_projection(const double* __restrict__ w,
+                                                   const void* x, int x_f64,
+                                                   uint64_t row, uint64_t ld,
+                                                   uint64_t dim) {
+  double acc = 0.0;
+  if (x_f64) {
+    const double* xr = static_cast<const double*>(x) + row * ld;
+    for (uint64_t i = 0; i < dim; ++i) acc = __dadd_rn(acc, __dmul_rn(w[i], xr[i]));
+  } else {
+    const float* xr = static_cast<const float*>(x) + row * ld;
+    for (uint64_t i = 0; i < dim; ++i)
+      acc = __dadd_rn(acc, __dmul_rn(w[i], static_cast<double>(xr[i])));
+  }
+  return acc;
+}
+
+// ---- hash (SIMT FP32 + FP64 recheck) --------------------------------------
+
+struct HashSmem {
+  float xs[2][BK][XS];
+  float ws[2][BK][BN];
+};
+
+__global__ void __launch_bounds__(NT, 2) hash_simt_kernel(const HashArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  HashSmem& sm = *reinterpret_cast<HashSmem*>(smem_raw);
+  __shared__ float nrm[BM];
+  __shared__ uint32_t bits[BM][4];
+  __shared__ uint32_t nt_list[NT_CAP];
+  __shared__ int nt_count;
+  __shared__ unsigned long long blk_T, blk_rechk, blk_flip;
+
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const uint64_t m0 = static_cast<uint64_t>(blockIdx.x) * BM;
+  const int tile = blockIdx.y;
+  const uint32_t col0 = static_cast<uint32_t>(tile) * BN;
+  const uint64_t dim = a.fam.dim;
+  const uint32_t ncols = a.fam.ncols;
+  const int nk = static_cast<int>((dim + BK - 1) / BK);
+
+  for (int i = tid; i < BM * 4; i += NT) (&bits[0][0])[i] = 0u;
+  if (tid == 0) {
+    nt_count = 0;
+    blk_T = 0;
+    blk_rechk = 0;
+    blk_flip = 0;
+  }
+
+  // loader mapping: rows lrow + 32*i (i<4), k = 4*lkq + e (e<4)
+  const int lrow = tid >> 3, lkq = tid & 7;
+  double sq[4] = {0.0, 0.0, 0.0, 0.0};
+  float xr[4][4];
+  float4 wr[4];
+
+  auto load_chunk = [&](int kc) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint64_t row = m0 + lrow + 32 * i;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint64_t k = static_cast<uint64_t>(kc) * BK + 4 * lkq + e;
+        float v = 0.0f;
+        if (row < a.n && k < dim) {
+          if (a.x_f64) {
+            const double dv = static_cast<const double*>(a.x)[row * a.ld + k];
+            v = static_cast<float>(dv);
+            sq[i] += dv * dv;
+          } else {
+            v = static_cast<const float*>(a.x)[row * a.ld + k];
+            sq[i] += static_cast<double>(v) * static_cast<double>(v);
+          }
+        }
+        xr[i][e] = v;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int idx = tid + NT * j;
+      const int r = idx >> 5, c4 = idx & 31;
+      wr[j] = *reinterpret_cast<const float4*>(
+          a.fam.w32t + (static_cast<uint64_t>(kc) * BK + r) * ncols + col0 + 4 * c4);
+    }
+  };
+  auto store_chunk = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sm.xs[buf][4 * lkq + e][lrow + 32 * i] = xr[i][e];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int idx = tid + NT * j;
+      const int r = idx >> 5, c4 = idx & 31;
+      *reinterpret_cast<float4*>(&sm.ws[buf][r][4 * c4]) = wr[j];
+    }
+  };
+
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+
+  load_chunk(0);
+  store_chunk(0);
+  __syncthreads();
+  for (int kc = 0; kc < nk; ++kc) {
+    const int buf = kc & 1;
+    if (kc + 1 < nk) load_chunk(kc + 1);
+#pragma unroll 8
+    for (int k = 0; k < BK; ++k) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&sm.xs[buf][k][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&sm.xs[buf][k][64 + ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&sm.ws[buf][k][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&sm.ws[buf][k][64 + tx * 4]);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = __fmaf_rn(av[i], bv[j], acc[i][j]);
+    }
+    if (kc + 1 < nk) store_chunk(buf ^ 1);
+    __syncthreads();
+  }
+
+  // ---- row norms (upper bounds), reduced over the 8 loader lanes of a row
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double v = sq[i];
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    if (lkq == 0) {
+      const double r = sqrt(v) * (1.0 + 0x1.0p-40);
+      float f = __double2float_ru(r);
+      if (!(r < 1e30) || (r > 0.0 && r < 1e-30)) f = INFINITY;  // force exact
+      nrm[lrow + 32 * i] = f;
+    }
+  }
+  __syncthreads();
+
+  // ---- fast signs, near-tie detection
+  const uint32_t K = a.fam.k_bits;
+  const uint32_t valid_cols = a.fam.tpt * K;
+  const uint32_t tables_here =
+      min(a.fam.tpt, a.fam.tables - static_cast<uint32_t>(tile) * a.fam.tpt);
+  const uint32_t used_cols = tables_here * K;
+  (void)valid_cols;
+  const float abs_eps = static_cast<float>(dim) * 0x1.0p-148f;
+  unsigned long long over_mask = 0ull, over_val = 0ull;  // inline rechecks
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int pt = (i < 4) ? ty * 4 + i : 64 + ty * 4 + (i - 4);
+    const uint64_t row = m0 + pt;
+    const float nx = nrm[pt];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t col = (j < 4) ? tx * 4 + j : 64 + tx * 4 + (j - 4);
+      if (row >= a.n || col >= used_cols || nx == 0.0f) continue;
+      const float thr = __fmaf_ru(a.margin_c * nx, a.fam.wnorm[col0 + col], abs_eps);
+      if (!(fabsf(acc[i][j]) > thr)) {
+        const int slot = atomicAdd(&nt_count, 1);
+        if (slot < NT_CAP) {
+          nt_list[slot] = (static_cast<uint32_t>(pt) << 8) | col;
+        } else {
+          const uint32_t table = tile * a.fam.tpt + col / K, b = col % K;
+          const double p = exact_projection(a.fam.w64 + (static_cast<uint64_t>(table) * K + b) * dim,
+                                            a.x, a.x_f64, row, a.ld, dim);
+          const int bit = p >= 0.0;
+          if (bit != (acc[i][j] >= 0.0f)) atomicAdd(&blk_flip, 1ull);
+          atomicAdd(&blk_rechk, 1ull);
+          over_mask |= 1ull << (i * 8 + j);
+          if (bit) over_val |= 1ull << (i * 8 + j);
+        }
+      }
+    }
+  }
+  // fast sign bits (with inline overrides) -> bits[pt][col/32]
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int pt = (i < 4) ? ty * 4 + i : 64 + ty * 4 + (i - 4);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t nib = 0;
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int j = h * 4 + jj;
+        const int q = i * 8 + j;
+        const uint32_t bit = ((over_mask >> q) & 1ull) ? static_cast<uint32_t>((over_val >> q) & 1ull)
+                                                       : (acc[i][j] >= 0.0f ? 1u : 0u);
+        nib |= bit << jj;
+      }
+      const uint32_t col = h * 64 + tx * 4;
+      if (nib) atomicOr(&bits[pt][col >> 5], nib << (col & 31));
+    }
+  }
+  __syncthreads();
+
+  // ---- exact recheck of listed near-ties (one thread per item)
+  const int listed = min(nt_count, NT_CAP);
+  for (int it = tid; it < listed; it += NT) {
+    const uint32_t e = nt_list[it];
+    const int pt = static_cast<int>(e >> 8);
+    const uint32_t col = e & 0xffu;
+    const uint32_t table = tile * a.fam.tpt + col / K, b = col % K;
+    const double p = exact_projection(a.fam.w64 + (static_cast<uint64_t>(table) * K + b) * dim, a.x,
+                                      a.x_f64, m0 + pt, a.ld, dim);
+    const uint32_t mask = 1u << (col & 31);
+    const bool fast = (bits[pt][col >> 5] & mask) != 0u;
+    const bool exact = p >= 0.0;
+    if (exact != fast) {
+      if (exact)
+        atomicOr(&bits[pt][col >> 5], mask);
+      else
+        atomicAnd(&bits[pt][col >> 5], ~mask);
+      atomicAdd(&blk_flip, 1ull);
+    }
+    atomicAdd(&blk_rechk, 1ull);
+  }
+  __syncthreads();
+
+  // ---- buckets (MSB-first), ids, fused insert
+  const int lane = tid & 31;
+  const uint32_t kmask = (K >= 32) ? 0xffffffffu : ((1u << K) - 1u);
+  unsigned long long dT = 0ull;
+  for (uint32_t tt = tid / BM; tt < tables_here; tt += NT / BM) {
+    const int pt = tid % BM;
+    const uint64_t row = m0 + pt;
+    const bool valid = row < a.n;
+    const uint32_t s0 = tt * K;
+    const uint32_t w = s0 >> 5;
+    const unsigned long long v64 =
+        static_cast<unsigned long long>(bits[pt][w]) |
+        (w + 1 < 4 ? static_cast<unsigned long long>(bits[pt][w + 1]) << 32 : 0ull);
+    const uint32_t field = static_cast<uint32_t>(v64 >> (s0 & 31)) & kmask;
+    const uint32_t bucket = __brev(field) >> (32 - K);
+    const uint32_t table = tile * a.fam.tpt + tt;
+    if (valid) a.ids[static_cast<uint64_t>(table) * a.ids_stride + a.id_base + row] = bucket;
+    if (a.insert) {
+      const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+      if (valid) {
+        const unsigned peers = __match_any_sync(vmask, bucket);
+        if (lane == __ffs(peers) - 1) {
+          const unsigned m = __popc(peers);
+          const unsigned old =
+              atomicAdd(&a.counters[(static_cast<uint64_t>(table) << K) + bucket], m);
+          if (old > 0xffffffffu - m) a.st->saturated = 1;
+          dT += insert_numerator(old, m, a.cap);
+        }
+      }
+    }
+  }
+  if (a.insert) {
+    dT = warp_sum_u64(dT);
+    if (lane == 0 && dT) atomicAdd(&blk_T, dT);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (blk_T) atomicAdd(&a.st->T, blk_T);
+    if (blk_rechk) atomicAdd(&a.st->rechecked, blk_rechk);
+    if (blk_flip) atomicAdd(&a.st->flipped, blk_flip);
+    if (a.insert && blockIdx.x == 0 && blockIdx.y == 0) atomicAdd(&a.st->n, a.n);
+  }
+}
+
+// ---- counters from ids (streaming insert / remove) -------------------------
+
+__global__ void apply_ids_kernel(const uint32_t* __restrict__ ids, uint64_t n, uint32_t tables,
+                                 uint32_t k_bits, uint32_t* counters, uint32_t cap, int sign,
+                                 DevState* st) {
+  __shared__ unsigned long long blk;
+  if (threadIdx.x == 0) blk = 0ull;
+  __syncthreads();
+  const uint64_t total = n * tables;
+  const int lane = threadIdx.x & 31;
+  unsigned long long dT = 0ull;
+  for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x; base < total;
+       base += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t idx = base + threadIdx.x;
+    const bool valid = idx < total;
+    unsigned long long key = 0ull;
+    if (valid) {
+      const uint64_t t = idx / n;
+      key = (t << k_bits) | ids[idx];
+    }
+    const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+    if (valid) {
+      const unsigned peers = __match_any_sync(vmask, key);
+      if (lane == __ffs(peers) - 1) {
+        const unsigned m = __popc(peers);
+        if (sign > 0) {
+          const unsigned old = atomicAdd(&counters[key], m);
+          if (old > 0xffffffffu - m) st->saturated = 1;
+          dT += insert_numerator(old, m, cap);
+        } else {
+          // removals: numerator sum_{r<m} (2*(old-r) - 1) = m*(2*old - m)
+          const unsigned old = atomicSub(&counters[key], m);
+          dT += static_cast<unsigned long long>(m) * (2ull * old - m);
+        }
+      }
+    }
+  }
+  dT = warp_sum_u64(dT);
+  if (lane == 0 && dT) atomicAdd(&blk, dT);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (sign > 0) {
+      if (blk) atomicAdd(&st->T, blk);
+      if (blockIdx.x == 0) atomicAdd(&st->n, n);
+    } else {
+      if (blk) atomicAdd(&st->T, 0ull - blk);
+      if (blockIdx.x == 0) atomicAdd(&st->n, 0ull - n);
+    }
+  }
+}
+
+__global__ void remove_demand_kernel(const uint32_t* __restrict__ ids, uint64_t n, uint32_t tables,
+                                     uint32_t k_bits, uint32_t* demand) {
+  const uint64_t total = n * tables;
+  for (uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t t = idx / n;
+    atomicAdd(&demand[(t << k_bits) | ids[idx]], 1u);
+  }
+}
+
+__global__ void remove_verify_kernel(const uint32_t* __restrict__ demand,
+                                     const uint32_t* __restrict__ counters, uint64_t num,
+                                     DevState* st) {
+  unsigned long long bad = 0;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < num;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    bad += demand[i] > counters[i];
+  bad = warp_sum_u64(bad);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(&st->underflow, bad);
+}
+
+__global__ void cap_kernel(uint32_t* counters, uint64_t num, uint32_t cap, DevState* st) {
+  int sat = 0;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < num;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t c = counters[i];
+    if (c > cap) {
+      counters[i] = cap;
+      sat = 1;
+    }
+  }
+  if (__any_sync(0xffffffffu, sat) && (threadIdx.x & 31) == 0) st->saturated = 1;
+}
+
+// ---- scoring -----------------------------------------------------------------
+
+__global__ void score_kernel(const uint32_t* __restrict__ ids, uint64_t ids_stride, uint64_t n,
+                             uint32_t tables, uint32_t k_bits, const uint32_t* __restrict__ counters,
+                             uint64_t* __restrict__ sums, double* __restrict__ scores,
+                             DevState* st) {
+  __shared__ unsigned long long s_lo, s_hi, q_lo, q_hi;
+  if (threadIdx.x == 0) s_lo = s_hi = q_lo = q_hi = 0ull;
+  __syncthreads();
+  unsigned long long acc = 0ull, sq_lo = 0ull, sq_hi = 0ull;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    unsigned long long S = 0ull;
+    uint32_t t = 0;
+    for (; t + 4 <= tables; t += 4) {
+      const uint32_t b0 = ids[(uint64_t)t * ids_stride + i];
+      const uint32_t b1 = ids[(uint64_t)(t + 1) * ids_stride + i];
+      const uint32_t b2 = ids[(uint64_t)(t + 2) * ids_stride + i];
+      const uint32_t b3 = ids[(uint64_t)(t + 3) * ids_stride + i];
+      S += counters[((uint64_t)t << k_bits) + b0];
+      S += counters[((uint64_t)(t + 1) << k_bits) + b1];
+      S += counters[((uint64_t)(t + 2) << k_bits) + b2];
+      S += counters[((uint64_t)(t + 3) << k_bits) + b3];
+    }
+    for (; t < tables; ++t) S += counters[((uint64_t)t << k_bits) + ids[(uint64_t)t * ids_stride + i]];
+    if (sums) sums[i] = S;
+    if (scores) scores[i] = __ddiv_rn(static_cast<double>(S), static_cast<double>(tables));
+    acc += S;
+    const unsigned long long lo = S * S, hi = __umul64hi(S, S);
+    const unsigned long long nlo = sq_lo + lo;
+    sq_hi += hi + (nlo < sq_lo ? 1ull : 0ull);
+    sq_lo = nlo;
+  }
+  // block reduction via shared atomics (u128 with carry)
+  atomicAdd(&s_lo, acc);  // sum S fits u64 per block
+  atomic_add_u128(&q_lo, &q_hi, sq_lo, sq_hi);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomic_add_u128(&st->sum_lo, &st->sum_hi, s_lo, s_hi);
+    atomic_add_u128(&st->sq_lo, &st->sq_hi, q_lo, q_hi);
+  }
+}
+
+// ---- detect_batch threshold (1 thread) -------------------------------------
+
+struct U192 {
+  unsigned long long w[3];  // little-endian limbs
+};
+
+__device__ U192 mul_u128_u64(unsigned long long lo, unsigned long long hi, unsigned long long m) {
+  U192 r;
+  r.w[0] = lo * m;
+  const unsigned long long c0 = __umul64hi(lo, m);
+  const unsigned long long p1 = hi * m;
+  const unsigned long long c1 = __umul64hi(hi, m);
+  r.w[1] = p1 + c0;
+  r.w[2] = c1 + (r.w[1] < p1 ? 1ull : 0ull);
+  return r;
+}
+__device__ bool ge192(const U192& a, const U192& b) {
+  for (int i = 2; i >= 0; --i)
+    if (a.w[i] != b.w[i]) return a.w[i] > b.w[i];
+  return true;
+}
+__device__ U192 sub192(const U192& a, const U192& b) {
+  U192 r;
+  unsigned long long borrow = 0;
+  for (int i = 0; i < 3; ++i) {
+    const unsigned long long d = a.w[i] - b.w[i];
+    const unsigned long long d2 = d - borrow;
+    borrow = (a.w[i] < b.w[i]) || (d < borrow) ? 1ull : 0ull;
+    r.w[i] = d2;
+  }
+  return r;
+}
+__device__ U192 add192(const U192& a, const U192& b) {
+  U192 r;
+  unsigned long long carry = 0;
+  for (int i = 0; i < 3; ++i) {
+    const unsigned long long s = a.w[i] + b.w[i];
+    const unsigned long long s2 = s + carry;
+    carry = (s < a.w[i]) || (s2 < s) ? 1ull : 0ull;
+    r.w[i] = s2;
+  }
+  return r;
+}
+__device__ U192 shr192(const U192& a, int k) {  // k in {1, 2}
+  U192 r;
+  r.w[0] = (a.w[0] >> k) | (a.w[1] << (64 - k));
+  r.w[1] = (a.w[1] >> k) | (a.w[2] << (64 - k));
+  r.w[2] = a.w[2] >> k;
+  return r;
+}
+__device__ bool is_zero192(const U192& a) { return (a.w[0] | a.w[1] | a.w[2]) == 0ull; }
+__device__ double to_double192(const U192& a) {
+  return static_cast<double>(a.w[2]) * 0x1.0p128 + static_cast<double>(a.w[1]) * 0x1.0p64 +
+         static_cast<double>(a.w[0]);
+}
+
+// floor(sqrt(v)) for v < 2^192 (digit-by-digit).
+__device__ U192 isqrt192(U192 v) {
+  U192 res = {{0, 0, 0}};
+  U192 bit = {{0, 0, 1ull << 62}};
+  while (!ge192(v, bit) && !is_zero192(bit)) bit = shr192(bit, 2);
+  while (!is_zero192(bit)) {
+    const U192 t = add192(res, bit);
+    if (ge192(v, t)) {
+      v = sub192(v, t);
+      res = add192(shr192(res, 1), bit);
+    } else {
+      res = shr192(res, 1);
+    }
+    bit = shr192(bit, 2);
+  }
+  return res;
+}
+
+__global__ void finalize_batch_kernel(uint64_t n, uint32_t tables, DevState* st) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const unsigned long long sum = st->sum_lo;  // sum_hi == 0 checked on host
+  // V = N * sum S^2 - (sum S)^2  (exact, >= 0)
+  const U192 a = mul_u128_u64(st->sq_lo, st->sq_hi, n);
+  U192 b;
+  b.w[0] = sum * sum;
+  b.w[1] = __umul64hi(sum, sum);
+  b.w[2] = 0;
+  const U192 V = ge192(a, b) ? sub192(a, b) : U192{{0, 0, 0}};
+  const U192 r = isqrt192(V);
+  // flag <=> S/L < sum/(N L) - sqrt(V)/(N L) <=> N*S <= sum - isqrt(V) - 1
+  long long s_cut = -1;
+  if (r.w[2] == 0 && r.w[1] == 0 && r.w[0] < sum) {
+    const unsigned long long q = sum - r.w[0] - 1ull;
+    s_cut = static_cast<long long>(q / n);
+  }
+  const double NL = static_cast<double>(n) * static_cast<double>(tables);
+  const double mean = static_cast<double>(sum) / NL;
+  const double sd = sqrt(to_double192(V)) / NL;
+  const double thr = mean - sd;
+  // rigorous band for the reference's rounded statistics (detect.cpp:44-50)
+  const double u = 0x1.0p-53;
+  const double Nf = static_cast<double>(n);
+  const double e_mean = (Nf + 3.0) * u * fabs(mean);
+  const double B2 = 2.0 * (2.0 * (Nf + 10.0) * u * (sd * sd + mean * mean) + 2.0 * e_mean * e_mean);
+  double d_sd = sqrt(B2);
+  if (sd > 0.0 && B2 / sd < d_sd) d_sd = B2 / sd;
+  d_sd += 2.0 * u * sd;
+  const double delta = 2.0 * (e_mean + d_sd + 2.0 * u * fabs(thr)) + 4.0 * u * (fabs(mean) + sd);
+  const double L = static_cast<double>(tables);
+  st->s_cut = s_cut;
+  st->s_lo = static_cast<long long>(ceil((thr - delta) * L * (1.0 - 4.0 * u)) - 1.0);
+  st->s_hi = static_cast<long long>(floor((thr + delta) * L * (1.0 + 4.0 * u)) + 1.0);
+  if (st->s_lo < 0) st->s_lo = 0;
+  // tighten: only integer S whose score can lie within delta of thr
+  while (st->s_lo <= st->s_hi && static_cast<double>(st->s_lo) / L < thr - delta) ++st->s_lo;
+  while (st->s_hi >= st->s_lo && static_cast<double>(st->s_hi) / L > thr + delta) --st->s_hi;
+  st->mean = mean;
+  st->sd = sd;
+  st->thr = thr;
+  st->replayed = 0;
+  st->reported = 0;
+  st->ambiguous = 0;
+}
+
+__global__ void flags_kernel(const uint64_t* __restrict__ sums, uint64_t n,
+                             uint32_t* __restrict__ flag_bits, DevState* st, int pass) {
+  if (pass == 1 && !st->replayed) return;
+  const long long cut = st->s_cut, lo = st->s_lo, hi = st->s_hi;
+  unsigned long long rep = 0, amb = 0;
+  const uint64_t words = (n + 31) / 32;
+  for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x; base < words * 32;
+       base += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t i = base + threadIdx.x;
+    bool f = false;
+    if (i < n) {
+      const long long S = static_cast<long long>(sums[i]);
+      f = S <= cut;
+      if (pass == 0 && S >= lo && S <= hi) ++amb;
+    }
+    const unsigned w = __ballot_sync(0xffffffffu, f);
+    if ((threadIdx.x & 31) == 0 && (i >> 5) < words) {
+      if (flag_bits) flag_bits[i >> 5] = w;
+      rep += __popc(w);
+    }
+  }
+  rep = warp_sum_u64(rep);
+  amb = warp_sum_u64(amb);
+  if ((threadIdx.x & 31) == 0) {
+    if (rep) atomicAdd(&st->reported, rep);
+    if (amb) atomicAdd(&st->ambiguous, amb);
+  }
+}
+
+// Sequential replay of detect.cpp:44-50 in binary64 (one block, thread 0 folds).
+__global__ void replay_kernel(const uint64_t* __restrict__ sums, uint64_t n, uint32_t tables,
+                              DevState* st) {
+  if (st->ambiguous == 0) return;
+  __shared__ double buf[1024];
+  __shared__ double s_sum, s_mean, s_sq;
+  const double L = static_cast<double>(tables);
+  if (threadIdx.x == 0) s_sum = 0.0;
+  for (uint64_t base = 0; base < n; base += 1024) {
+    __syncthreads();
+    const uint64_t i = base + threadIdx.x;
+    if (i < n) buf[threadIdx.x] = __ddiv_rn(static_cast<double>(sums[i]), L);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = s_sum;
+      const uint64_t m = n - base < 1024 ? n - base : 1024;
+      for (uint64_t j = 0; j < m; ++j) s = __dadd_rn(s, buf[j]);
+      s_sum = s;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_mean = __ddiv_rn(s_sum, static_cast<double>(n));
+    s_sq = 0.0;
+  }
+  for (uint64_t base = 0; base < n; base += 1024) {
+    __syncthreads();
+    const uint64_t i = base + threadIdx.x;
+    if (i < n) buf[threadIdx.x] = __ddiv_rn(static_cast<double>(sums[i]), L);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double q = s_sq;
+      const double mu = s_mean;
+      const uint64_t m = n - base < 1024 ? n - base : 1024;
+      for (uint64_t j = 0; j < m; ++j) {
+        const double t = __dsub_rn(buf[j], mu);
+        q = __dadd_rn(q, __dmul_rn(t, t));
+      }
+      s_sq = q;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double mean = s_mean;
+    const double sd = __dsqrt_rn(__ddiv_rn(s_sq, static_cast<double>(n)));
+    const double thr = __dsub_rn(mean, sd);
+    // largest S with fl(S / L) < thr (fl(S/L) is nondecreasing in S)
+    long long cut = -1;
+    if (thr > 0.0) {
+      long long k = static_cast<long long>(floor(thr * L)) + 3;
+      while (k >= 0 && !(__ddiv_rn(static_cast<double>(k), L) < thr)) --k;
+      cut = k;
+    }
+    st->s_cut = cut;
+    st->mean = mean;
+    st->sd = sd;
+    st->thr = thr;
+    st->reported = 0;
+    st->replayed = 1;
+  }
+}
+
+// ---- streaming -------------------------------------------------------------
+
+__device__ double sketch_mean(const DevState* st, uint32_t tables) {
+  const unsigned long long n = st->n;
+  if (n == 0) return 0.0;
+  const unsigned long long den = n * tables;
+  const unsigned long long q = st->T / den, r = st->T % den;
+  return static_cast<double>(q) + static_cast<double>(r) / static_cast<double>(den);
+}
+
+__global__ void stream_score_kernel(const uint32_t* __restrict__ ids, uint64_t n, uint32_t tables,
+                                    uint32_t k_bits, const uint32_t* __restrict__ counters,
+                                    double alpha, uint32_t* __restrict__ flag_bits,
+                                    double* __restrict__ scores, DevState* st) {
+  __shared__ double s_cut, s_band;
+  __shared__ int s_live;
+  if (threadIdx.x == 0) {
+    const double mu = sketch_mean(st, tables);
+    s_cut = mu - alpha;
+    s_live = st->n > 0;
+    s_band = 0x1.0p-30 * fmax(1.0, fabs(mu));
+    if (blockIdx.x == 0) {
+      st->cut = s_cut;
+      st->mean_before = mu;
+    }
+  }
+  __syncthreads();
+  const double cut = s_cut, band = s_band;
+  const int live = s_live;
+  const double L = static_cast<double>(tables);
+  unsigned long long rep = 0, amb = 0;
+  const uint64_t words = (n + 31) / 32;
+  for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x; base < words * 32;
+       base += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t i = base + threadIdx.x;
+    bool f = false;
+    if (i < n) {
+      unsigned long long S = 0ull;
+      for (uint32_t t = 0; t < tables; ++t)
+        S += counters[((uint64_t)t << k_bits) + ids[(uint64_t)t * n + i]];
+      const double sc = __ddiv_rn(static_cast<double>(S), L);
+      if (scores) scores[i] = sc;
+      f = live && sc <= cut;
+      if (live && fabs(sc - cut) <= band) ++amb;
+    }
+    const unsigned w = __ballot_sync(0xffffffffu, f);
+    if ((threadIdx.x & 31) == 0 && (i >> 5) < words) {
+      if (flag_bits) flag_bits[i >> 5] = w;
+      rep += __popc(w);
+    }
+  }
+  rep = warp_sum_u64(rep);
+  amb = warp_sum_u64(amb);
+  if ((threadIdx.x & 31) == 0) {
+    if (rep) atomicAdd(&st->reported, rep);
+    if (amb) atomicAdd(&st->ambiguous, amb);
+  }
+}
+
+__global__ void sum_squares_kernel(const uint32_t* __restrict__ c, uint64_t num,
+                                   unsigned long long* out) {
+  unsigned long long s = 0;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < num;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    s += static_cast<unsigned long long>(c[i]) * c[i];
+  s = warp_sum_u64(s);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
+int grid_for(uint64_t work, int threads, int max_blocks = 148 * 16) {
+  uint64_t b = (work + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > static_cast<uint64_t>(max_blocks)) b = max_blocks;
+  return static_cast<int>(b);
+}
+
+}  // namespace
+
+size_t hash_simt_smem_bytes() { return sizeof(HashSmem); }
+
+cudaError_t launch_hash_simt(const HashArgs& a, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(hash_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sizeof(HashSmem)));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  if (a.n == 0) return cudaSuccess;
+  const dim3 grid(static_cast<unsigned>((a.n + BM - 1) / BM), a.fam.ntiles);
+  hash_simt_kernel<<<grid, NT, sizeof(HashSmem), s>>>(a);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_apply_ids(const uint32_t* ids, uint64_t n, uint32_t tables, uint32_t k_bits,
+                             uint32_t* counters, uint32_t cap, int sign, DevState* st,
+                             cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  apply_ids_kernel<<<grid_for(n * tables, 256), 256, 0, s>>>(ids, n, tables, k_bits, counters, cap,
+                                                             sign, st);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_remove_check(const uint32_t* ids, uint64_t n, uint32_t tables, uint32_t k_bits,
+                                const uint32_t* counters, uint32_t* scratch, DevState* st,
+                                cudaStream_t s) {
+  const uint64_t num = static_cast<uint64_t>(tables) << k_bits;
+  cudaError_t e = cudaMemsetAsync(scratch, 0, num * sizeof(uint32_t), s);
+  if (e != cudaSuccess) return e;
+  remove_demand_kernel<<<grid_for(n * tables, 256), 256, 0, s>>>(ids, n, tables, k_bits, scratch);
+  remove_verify_kernel<<<grid_for(num, 256), 256, 0, s>>>(scratch, counters, num, st);
+  count_launch(2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cap(uint32_t* counters, uint64_t num, uint32_t cap, DevState* st,
+                       cudaStream_t s) {
+  cap_kernel<<<grid_for(num, 256), 256, 0, s>>>(counters, num, cap, st);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_score(const uint32_t* ids, uint64_t ids_stride, uint64_t n, uint32_t tables,
+                         uint32_t k_bits, const uint32_t* counters, uint64_t* sums, double* scores,
+                         DevState* st, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  score_kernel<<<grid_for(n, 256), 256, 0, s>>>(ids, ids_stride, n, tables, k_bits, counters, sums,
+                                                scores, st);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize_batch(uint64_t n, uint32_t tables, DevState* st, cudaStream_t s) {
+  finalize_batch_kernel<<<1, 32, 0, s>>>(n, tables, st);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_flags(const uint64_t* sums, uint64_t n, uint32_t* flag_bits, DevState* st,
+                         int pass, cudaStream_t s) {
+  flags_kernel<<<grid_for(n, 256), 256, 0, s>>>(sums, n, flag_bits, st, pass);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_replay(const uint64_t* sums, uint64_t n, uint32_t tables, DevState* st,
+                          cudaStream_t s) {
+  replay_kernel<<<1, 1024, 0, s>>>(sums, n, tables, st);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stream_score(const uint32_t* ids, uint64_t n, uint32_t tables, uint32_t k_bits,
+                                const uint32_t* counters, double alpha, uint32_t* flag_bits,
+                                double* scores, DevState* st, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  stream_score_kernel<<<grid_for(n, 256), 256, 0, s>>>(ids, n, tables, k_bits, counters, alpha,
+                                                       flag_bits, scores, st);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sum_squares(const uint32_t* counters, uint64_t num, unsigned long long* out,
+                               cudaStream_t s) {
+  sum_squares_kernel<<<grid_for(num, 256), 256, 0, s>>>(counters, num, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace ace_dev

@@ -1,0 +1,69 @@
+// Kernel entry points of libace_dev.so (implemented in ace_kernels.cu).
+#pragma once
+#include "ace_common.cuh"
+
+namespace ace_dev {
+
+struct HashArgs {
+  const void* x;
+  int x_f64;
+  uint64_t n, ld;          // rows, row stride (elements)
+  FamilyDev fam;
+  float margin_c;          // relative error bound of the fast projection
+  uint32_t* ids;           // table-major, ids[t * ids_stride + i]
+  uint64_t ids_stride;
+  uint64_t id_base;        // ids written at column id_base + i
+  // fused insert (batch build): counters += 1 at each bucket
+  uint32_t* counters;      // L x 2^K
+  int insert;
+  uint32_t cap;            // 0xffff (k16) or 0xffffffff (k32)
+  DevState* st;
+};
+
+// SIMT FP32 projection + FP64 near-tie recheck + bucket packing (+ insert).
+cudaError_t launch_hash_simt(const HashArgs& a, cudaStream_t s);
+size_t hash_simt_smem_bytes();
+
+// Counter updates from ids (streaming insert / remove), warp-aggregated.
+//   sign = +1 insert, -1 remove (remove assumes validation passed).
+cudaError_t launch_apply_ids(const uint32_t* ids, uint64_t n, uint32_t tables,
+                             uint32_t k_bits, uint32_t* counters, uint32_t cap,
+                             int sign, DevState* st, cudaStream_t s);
+// Remove validation: counts, per counter, how many removals target it and
+// flags underflow (any count < demand).  scratch: L x 2^K u32, zeroed here.
+cudaError_t launch_remove_check(const uint32_t* ids, uint64_t n, uint32_t tables,
+                                uint32_t k_bits, const uint32_t* counters,
+                                uint32_t* scratch, DevState* st, cudaStream_t s);
+
+// Sticky saturation for k16: clamp to cap, set st->saturated.
+cudaError_t launch_cap(uint32_t* counters, uint64_t num, uint32_t cap, DevState* st,
+                       cudaStream_t s);
+
+// Scores: S_i = sum_t counters[t*2^K + ids[t*stride+i]]; optional outputs;
+// accumulates sum S and sum S^2 into st (u128).
+cudaError_t launch_score(const uint32_t* ids, uint64_t ids_stride, uint64_t n,
+                         uint32_t tables, uint32_t k_bits, const uint32_t* counters,
+                         uint64_t* sums, double* scores, DevState* st, cudaStream_t s);
+
+// detect_batch threshold: exact integer cut + rigorous ambiguity band.
+cudaError_t launch_finalize_batch(uint64_t n, uint32_t tables, DevState* st,
+                                  cudaStream_t s);
+// flags from sums (pass 0: exact cut, counts ambiguity; pass 1: only if
+// the sequential replay ran).
+cudaError_t launch_flags(const uint64_t* sums, uint64_t n, uint32_t* flag_bits,
+                         DevState* st, int pass, cudaStream_t s);
+// Sequential replay of detect.cpp:44-50 when the band is not empty.
+cudaError_t launch_replay(const uint64_t* sums, uint64_t n, uint32_t tables,
+                          DevState* st, cudaStream_t s);
+
+// Streaming: score against current counts, flag score <= mean - alpha.
+cudaError_t launch_stream_score(const uint32_t* ids, uint64_t n, uint32_t tables,
+                                uint32_t k_bits, const uint32_t* counters,
+                                double alpha, uint32_t* flag_bits, double* scores,
+                                DevState* st, cudaStream_t s);
+
+// Sum of squares of all counters (T after restore with exact state).
+cudaError_t launch_sum_squares(const uint32_t* counters, uint64_t num,
+                               unsigned long long* out, cudaStream_t s);
+
+}  // namespace ace_dev

@@ -1,0 +1,202 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's own
+outputs (golden digests made by the compiled reference) and the C oracle.
+
+Bar: bit-exact bucket ids, counters, scores and flags; sketch mean and the
+detect statistics within 1e-9 relative (the reference's binary64 recurrences
+are order-dependent; the device keeps exact integers)."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle import detect_from_scores
+from paper_1706_06664_b200 import _native as N
+from paper_1706_06664_b200 import ace
+from paper_1706_06664_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+REL = 1e-9
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def family(cfg):
+    w = W.CONFIGS[cfg]
+    return ace.SrpFamily(ace.SrpConfig(dim=w.dim, k_bits=w.k_bits, num_tables=w.num_tables,
+                                       seed=w.w_seed))
+
+
+def close(a, b, rel=REL):
+    return abs(a - b) <= rel * max(1.0, abs(b))
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+def test_batch_pipeline_matches_reference(cuda, golden, cfg):
+    e = golden["configs"][str(cfg)]
+    x, lab = W.host_rows(cfg, 0, e["n"])
+    assert sha(x) == e["x_sha256"]
+    fam = family(cfg)
+    ids = fam.buckets(x)
+    assert sha(ids) == e["ids_sha256"], "bucket ids differ from the reference"
+    sk = ace.AceSketch(fam, ace.CounterWidth.k32)
+    xd = cuda.from_numpy(x).cuda()
+    rep = sk.build_detect(xd)
+    assert rep.stats.rechecked >= rep.stats.flipped
+    assert sha(sk.counters_u32()) == e["counters_sha256"]
+    assert sk.size() == e["size"]
+    assert close(sk.mean(), float.fromhex(e["mean"]))
+    assert int(rep.reported) == e["reported"]
+    assert sha(np.packbits(rep.flags, bitorder="little")) == e["flags_sha256"]
+    assert close(rep.score_mean, float.fromhex(e["det_mean"]))
+    assert close(rep.score_stddev, float.fromhex(e["det_sd"]))
+    assert close(rep.threshold, float.fromhex(e["det_thr"]))
+    # scores bit-exact (S / L with integer S)
+    assert sha(sk.score_batch(xd)) == e["scores_sha256"]
+    # host-memory input path gives the same counters
+    sk2 = ace.AceSketch(fam, ace.CounterWidth.k32)
+    rep2 = sk2.build_detect(x)
+    assert np.array_equal(sk2.counters_u32(), sk.counters_u32())
+    assert np.array_equal(rep2.flags, rep.flags)
+
+
+def test_stream_matches_reference(cuda, golden):
+    e = golden["configs"]["5"]
+    fam = family(5)
+    sk = ace.AceSketch(fam, ace.CounterWidth.k32)
+    for b, pb in enumerate(e["per_batch"]):
+        x, _ = W.host_rows(5, b * e["batch"], e["batch"])
+        assert sha(x) == pb["x_sha256"]
+        flags, scores, rep = sk.stream_batch(x, e["alpha"], scores=True)
+        assert sha(np.packbits(flags, bitorder="little")) == pb["flags_sha256"], b
+        assert int(flags.sum()) == pb["reported"]
+        assert sha(scores) == pb["scores_sha256"], b
+        assert rep.ambiguous == 0
+        assert close(sk.mean(), float.fromhex(pb["mean_after"]))
+    assert sha(sk.counters_u32()) == e["counters_sha256"]
+    assert sk.size() == e["size"]
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_near_tie_stress_exact(cuda, oracle_c, dtype):
+    """Points built to sit within ~1e-9 of many hyperplanes: the fast path's
+    margin routes them to the FP64 recheck and every id still matches."""
+    d, k, l, seed = 96, 15, 50, 7
+    fam = ace.SrpFamily(ace.SrpConfig(dim=d, k_bits=k, num_tables=l, seed=seed))
+    w = fam.directions
+    rng = np.random.default_rng(3)
+    n = 4096
+    x = rng.standard_normal((n, d))
+    r = rng.integers(0, k * l, n)
+    wr = w[r]
+    eps = rng.choice([0.0, 1e-12, -1e-12, 1e-9, -1e-9, 1e-7], n)
+    x = x - ((x * wr).sum(1) / (wr * wr).sum(1))[:, None] * wr + eps[:, None] * wr
+    x = x.astype(dtype)
+    st = N.AceHashStats()
+    ids = fam.buckets(x, stats=st)
+    ref_ids, near = oracle_c.buckets(w, x, k, l, rel_eps=1e-6)
+    assert np.array_equal(ids, ref_ids)
+    assert st.rechecked >= near  # every sub-1e-6 projection went to the recheck
+
+
+def test_edge_cases(cuda, oracle_c):
+    d, k, l = 10, 4, 6
+    fam = ace.SrpFamily(ace.SrpConfig(dim=d, k_bits=k, num_tables=l, seed=11))
+    w = fam.directions
+    x = np.zeros((77, d), dtype=np.float32)          # zero rows -> all-ones buckets
+    x[1] = np.nan                                     # NaN -> p NaN -> bit 0
+    x[2, 0] = np.inf
+    x[3] = 1e-38                                      # tiny
+    x[4] = 3e37                                       # huge
+    x[5:] = np.random.default_rng(0).standard_normal((72, d)).astype(np.float32)
+    ids = fam.buckets(x)
+    ref, _ = oracle_c.buckets(w, x, k, l)
+    assert np.array_equal(ids, ref)
+    assert (ids[:, 0] == (1 << k) - 1).all()
+    # ragged n and strided rows (ld > dim) through torch views
+    xt = cuda.from_numpy(np.random.default_rng(1).standard_normal((1001, 2 * d)).astype(np.float32)).cuda()
+    view = xt[:, :d]
+    ids_v = fam.buckets(view)
+    ref_v, _ = oracle_c.buckets(w, view.cpu().numpy(), k, l)
+    assert np.array_equal(ids_v, ref_v)
+    # empty batch is a no-op; empty detect is a contract violation
+    sk = ace.AceSketch(fam, ace.CounterWidth.k32)
+    sk.insert(np.zeros((0, d), dtype=np.float32))
+    assert sk.size() == 0
+    with pytest.raises(ace.ContractViolation):
+        ace.detect_batch(sk, np.zeros((0, d), dtype=np.float32))
+    with pytest.raises(ace.ContractViolation):
+        sk.insert(np.zeros((3, d + 1), dtype=np.float32))
+    with pytest.raises(ace.ContractViolation):
+        sk.stream_batch(np.zeros((3, d), dtype=np.float32), -1.0)
+
+
+@pytest.mark.parametrize("k", [1, 8, 16, 18, 30])
+def test_k_range_packing(cuda, oracle_c, k):
+    d = 12
+    l = 3 if k == 30 else 9
+    fam = ace.SrpFamily(ace.SrpConfig(dim=d, k_bits=k, num_tables=l, seed=k))
+    x = np.random.default_rng(k).standard_normal((513, d)).astype(np.float32)
+    ids = fam.buckets(x)
+    ref, _ = oracle_c.buckets(fam.directions, x, k, l)
+    assert np.array_equal(ids, ref)
+    assert int(ids.max()) < (1 << k)
+
+
+def test_k16_saturation_and_remove(cuda, oracle_c, reference):
+    d, k, l, seed = 3, 2, 2, 4
+    fam = ace.SrpFamily(ace.SrpConfig(dim=d, k_bits=k, num_tables=l, seed=seed))
+    x = np.tile(np.array([[0.5, -1.0, 2.0]], dtype=np.float32), (70000, 1))
+    sk = ace.AceSketch(fam, ace.CounterWidth.k16)
+    sk.insert(x[:30000])
+    sk.insert(x[30000:])
+    rs = reference.sketch(seed, d, k, l, 16)
+    rs.insert(x)
+    assert sk.saturated() and rs.saturated()
+    assert np.array_equal(sk.counters_flat(), rs.counters())
+    assert close(sk.mean(), rs.mean())
+
+
+def test_remove_and_inconsistent_delete(cuda, reference):
+    d, k, l, seed = 8, 6, 10, 3
+    fam = ace.SrpFamily(ace.SrpConfig(dim=d, k_bits=k, num_tables=l, seed=seed))
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((500, d)).astype(np.float32)
+    sk = ace.AceSketch(fam, ace.CounterWidth.k32)
+    sk.insert(x)
+    sk.remove(x[:200])
+    rs = reference.sketch(seed, d, k, l, 32)
+    rs.insert(x)
+    assert rs.remove(x[:200]) == 0
+    assert np.array_equal(sk.counters_flat(), rs.counters())
+    assert sk.size() == rs.size() == 300
+    assert close(sk.mean(), rs.mean())
+    before = sk.counters_flat()
+    never = rng.standard_normal((1, d)).astype(np.float32) * 100
+    sk2 = ace.AceSketch(fam, ace.CounterWidth.k32)
+    with pytest.raises(ace.InconsistentDelete):
+        sk2.remove(never)
+    sk.remove(x[200:])
+    assert sk.size() == 0 and sk.mean() == 0.0
+    assert int(sk.counters_flat().sum()) == 0
+    assert before.sum() == 300 * l
+
+
+def test_restore_clone_roundtrip(cuda):
+    w = W.CONFIGS[1]
+    fam = family(1)
+    x, _ = W.host_rows(1, 0, 5000)
+    sk = ace.AceSketch(fam, ace.CounterWidth.k32)
+    sk.insert(x)
+    c = sk.copy()
+    r = ace.AceSketch.restore(fam, ace.CounterWidth.k32, sk.counters_flat(), sk.size(), sk.mean(), False)
+    q = x[:100]
+    assert np.array_equal(sk.score_batch(q), r.score_batch(q))
+    assert np.array_equal(sk.score_batch(q), c.score_batch(q))
+    c.insert(x[:10])
+    assert c.size() == sk.size() + 10
+    assert close(r.mean(), sk.mean())
+    with pytest.raises(ace.ContractViolation):
+        ace.AceSketch.restore(fam, ace.CounterWidth.k32, np.zeros(5, np.uint64), 0, 0.0, False)
+    assert w.dim == 40
