@@ -93,7 +93,7 @@ def _load(name: str, table: dict) -> C.CDLL:
         raise ImportError(
             f"{path} is missing: build the native libraries first "
             "(python -m paper_1706_06664_b200.build); there is no fallback path")
-    lib = C.CDLL(str(path), mode=C.RTLD_GLOBAL)
+    lib = C.CDLL(str(path), mode=C.RTLD_LOCAL)
     for sym, (res, args) in table.items():
         fn = getattr(lib, sym)
         fn.restype = res

@@ -57,8 +57,8 @@ def build_host(force: bool = False) -> Path:
     src = CSRC / "ace_host.cpp"
     deps = [src, INC / "ace_b200.h", *INC.glob("ace/*.hpp"), LIB / "libace_dev.so"]
     if force or _stale(out, deps):
-        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", f"-I{INC}", "-o", str(out),
-              str(src), f"-L{LIB}", "-lace_dev", "-Wl,-rpath,$ORIGIN"])
+        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-Wl,-Bsymbolic", f"-I{INC}", "-o",
+              str(out), str(src), f"-L{LIB}", "-lace_dev", "-Wl,-rpath,$ORIGIN"])
     return out
 
 
