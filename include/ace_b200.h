@@ -93,6 +93,12 @@ ace_status ace_family_create(uint64_t dim, uint32_t k_bits, uint32_t num_tables,
                              double noise_scale, const double* w_host,
                              AceFamily** out);
 ace_status ace_family_destroy(AceFamily* fam);
+/* Projection kernel selection: 0 = automatic (tcgen05 when the shape is
+ * supported), 1 = SIMT FP32 kernel, 2 = tcgen05 kernel (ACE_E_UNSUPPORTED if
+ * the shape is not).  For testing both paths; results are identical. */
+ace_status ace_family_set_kernel(AceFamily* fam, int which);
+/* Which kernel the next hash will use (1 SIMT, 2 tcgen05). */
+int ace_family_kernel(const AceFamily* fam);
 /* Bucket ids of n points for all L tables (SrpFamily::bucket,
  * srp.cpp:106-113, batched).  ids: L*n uint32, table-major, in `ids_where`
  * memory. */

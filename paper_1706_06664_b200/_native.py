@@ -52,6 +52,8 @@ ABI = {
     "ace_kernel_launches": (_u64, []),
     "ace_family_create": (_i, [_u64, _u32, _u32, _d, _vp, _P(_vp)]),
     "ace_family_destroy": (_i, [_vp]),
+    "ace_family_set_kernel": (_i, [_vp, _i]),
+    "ace_family_kernel": (_i, [_vp]),
     "ace_family_buckets": (_i, [_vp, _vp, _i, _u64, _u64, _i, _vp, _i, _P(AceHashStats)]),
     "ace_sketch_create": (_i, [_vp, _u32, _P(_vp)]),
     "ace_sketch_clone": (_i, [_vp, _P(_vp)]),

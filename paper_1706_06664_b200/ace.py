@@ -174,6 +174,14 @@ class SrpFamily:
     def config(self) -> SrpConfig:
         return self._cfg
 
+    def set_kernel(self, which: str) -> None:
+        """Projection kernel: "auto", "simt" or "tc" (tcgen05)."""
+        code = {"auto": 0, "simt": 1, "tc": 2}[which]
+        _check(N.dev().ace_family_set_kernel(self.handle, code))
+
+    def kernel(self) -> str:
+        return {1: "simt", 2: "tc"}[N.dev().ace_family_kernel(self.handle)]
+
     def num_buckets(self) -> int:
         return 1 << self._cfg.k_bits
 

@@ -44,7 +44,7 @@ def _stale(out: Path, deps: list[Path]) -> bool:
 
 def build_dev(force: bool = False) -> Path:
     out = LIB / "libace_dev.so"
-    srcs = [CSRC / "ace_api.cu", CSRC / "ace_kernels.cu"]
+    srcs = [CSRC / "ace_api.cu", CSRC / "ace_kernels.cu", CSRC / "ace_hash_tc.cu"]
     deps = srcs + list(CSRC.glob("*.cuh")) + [INC / "ace_b200.h"]
     if force or _stale(out, deps):
         _run([_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",

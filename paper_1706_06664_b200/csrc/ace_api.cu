@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "ace_kernels.cuh"
+#include "ace_tc.cuh"
 
 namespace ace_dev {
 
@@ -70,8 +71,11 @@ struct DevBuf {
 
 struct AceFamily {
   FamilyDev d{};
+  TcFamily tc{};
+  int kernel = 0;  // 0 auto, 1 SIMT, 2 tcgen05
   float margin_c = 0.f;
   std::atomic<int> refs{1};
+  bool use_tc() const { return tc.enabled && kernel != 1; }
 };
 
 struct AceSketch {
@@ -84,7 +88,7 @@ struct AceSketch {
   DevState* hst = nullptr;   // pinned host mirror
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
-  DevBuf ids, sums, stage, flags, scores, demand;
+  DevBuf ids, sums, stage, flags, scores, demand, near, overflow;
   // phase timing (ace_sketch_set_timing)
   bool timing = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -105,6 +109,7 @@ void family_release(AceFamily* f) {
     cudaFree(f->d.w64);
     cudaFree(f->d.w32t);
     cudaFree(f->d.wnorm);
+    tc_free_family(&f->tc);
     delete f;
   }
 }
@@ -197,11 +202,44 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
   ACE_CUDA(sk->ids.ensure(static_cast<size_t>(n) * f->d.tables * sizeof(uint32_t)));
   for (bool& u : sk->ev_used) u = false;
   sk->mark(0);
-  HashArgs a = make_hash_args(f, xd, dtype, n, ld, sk->ids.as<uint32_t>(), n, sk->st);
-  a.insert = insert;
-  a.counters = sk->counters;
-  a.cap = sk->cap;
-  ACE_CUDA(launch_hash_simt(a, sk->stream));
+  if (f->use_tc()) {
+    TcArgs t{};
+    t.x = xd;
+    t.x_f64 = dtype == ACE_F64;
+    t.n = n;
+    t.ld = ld;
+    t.dim = f->d.dim;
+    t.k_bits = f->d.k_bits;
+    t.tables = f->d.tables;
+    t.tpt = f->d.tpt;
+    t.ntiles = f->d.ntiles;
+    t.nkc = f->tc.nkc;
+    t.w16 = f->tc.w16;
+    // error bound of the fp16x3 split relative to ||x~|| ||w^||
+    t.margin_c = static_cast<float>(
+        2.0 * (4.0 * 0x1.0p-22 + 0x1.0p-23 * (12.0 * f->tc.nkc + 16.0) * 1.01 + (t.x_f64 ? 0x1.0p-23 : 0.0)));
+    t.ids = sk->ids.as<uint32_t>();
+    uint64_t cap = n * f->d.rows / 1024;
+    cap = std::min<uint64_t>(std::max<uint64_t>(cap, 1u << 20), 1u << 25);
+    ACE_CUDA(sk->near.ensure(cap * sizeof(unsigned long long)));
+    ACE_CUDA(sk->overflow.ensure(((n + 31) / 32) * sizeof(uint32_t)));
+    ACE_CUDA(cudaMemsetAsync(sk->overflow.p, 0, ((n + 31) / 32) * sizeof(uint32_t), sk->stream));
+    t.near_list = sk->near.as<unsigned long long>();
+    t.near_cap = sk->near.bytes / sizeof(unsigned long long);
+    t.overflow_rows = sk->overflow.as<uint32_t>();
+    t.st = sk->st;
+    ACE_CUDA(launch_hash_tc(t, sk->stream));
+    ACE_CUDA(launch_recheck(t, f->d.w64, sk->stream));
+    if (insert)
+      ACE_CUDA(launch_apply_ids(sk->ids.as<uint32_t>(), n, f->d.tables, f->d.k_bits, sk->counters, sk->cap,
+                                +1, sk->st, sk->stream));
+  } else {
+    HashArgs a = make_hash_args(f, xd, dtype, n, ld, sk->ids.as<uint32_t>(), n, sk->st);
+    a.insert = insert;
+    a.counters = sk->counters;
+    a.cap = sk->cap;
+    ACE_CUDA(launch_hash_simt(a, sk->stream));
+  }
   if (insert && sk->width == 16)
     ACE_CUDA(launch_cap(sk->counters, sk->num_counters, sk->cap, sk->st, sk->stream));
   sk->mark(1);
@@ -321,6 +359,7 @@ ace_status ace_family_create(uint64_t dim, uint32_t k_bits, uint32_t num_tables,
       wn[j * kTileCols + c] = std::nextafter(nb, INFINITY);
     }
   auto cleanup = [&]() { family_release(f); };
+  f->tc = TcFamily{};
   cudaError_t e;
   if ((e = cudaMalloc(&d.w64, sizeof(double) * d.rows * dim)) != cudaSuccess ||
       (e = cudaMalloc(&d.w32t, sizeof(float) * w32t.size())) != cudaSuccess ||
@@ -332,9 +371,25 @@ ace_status ace_family_create(uint64_t dim, uint32_t k_bits, uint32_t num_tables,
     return fail(e == cudaErrorMemoryAllocation ? ACE_E_NOMEM : ACE_E_CUDA,
                 std::string("ace_family_create: ") + cudaGetErrorString(e));
   }
+  if ((e = tc_prepare_family(d, &f->tc)) != cudaSuccess) {
+    cleanup();
+    return fail(ACE_E_CUDA, std::string("ace_family_create (tcgen05 operands): ") + cudaGetErrorString(e));
+  }
   *out = f;
   return ACE_OK;
 }
+
+ace_status ace_family_set_kernel(AceFamily* fam, int which) {
+  if (!fam) return fail(ACE_E_CONTRACT, "ace_family_set_kernel: null family");
+  if (which < 0 || which > 2) return fail(ACE_E_CONTRACT, "ace_family_set_kernel: which must be 0, 1 or 2");
+  if (which == 2 && !fam->tc.enabled)
+    return fail(ACE_E_UNSUPPORTED, "ace_family_set_kernel: tcgen05 path does not support dim " +
+                                       std::to_string(fam->d.dim));
+  fam->kernel = which;
+  return ACE_OK;
+}
+
+int ace_family_kernel(const AceFamily* fam) { return fam && fam->use_tc() ? 2 : 1; }
 
 ace_status ace_family_destroy(AceFamily* fam) {
   family_release(fam);
@@ -425,6 +480,8 @@ ace_status ace_sketch_destroy(AceSketch* sk) {
   sk->flags.release();
   sk->scores.release();
   sk->demand.release();
+  sk->near.release();
+  sk->overflow.release();
   if (sk->counters) cudaFree(sk->counters);
   if (sk->st) cudaFree(sk->st);
   if (sk->hst) cudaFreeHost(sk->hst);

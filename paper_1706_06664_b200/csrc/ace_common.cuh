@@ -20,6 +20,8 @@ struct DevState {
   unsigned long long ambiguous;
   unsigned long long rechecked;
   unsigned long long flipped;
+  unsigned long long near_count;     // tc path: near-tie items pushed
+  unsigned long long near_overflow;  // tc path: list overflowed (rows rechecked in full)
   unsigned long long underflow;  // remove: counters that would go negative
   int saturated;
   int replayed;

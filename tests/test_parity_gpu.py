@@ -32,12 +32,14 @@ def close(a, b, rel=REL):
     return abs(a - b) <= rel * max(1.0, abs(b))
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
-def test_batch_pipeline_matches_reference(cuda, golden, cfg):
+@pytest.mark.parametrize("cfg,kernel", [(1, "auto"), (2, "auto"), (3, "auto"), (4, "auto"),
+                                        (1, "simt"), (2, "simt"), (3, "simt")])
+def test_batch_pipeline_matches_reference(cuda, golden, cfg, kernel):
     e = golden["configs"][str(cfg)]
     x, lab = W.host_rows(cfg, 0, e["n"])
     assert sha(x) == e["x_sha256"]
     fam = family(cfg)
+    fam.set_kernel(kernel)
     ids = fam.buckets(x)
     assert sha(ids) == e["ids_sha256"], "bucket ids differ from the reference"
     sk = ace.AceSketch(fam, ace.CounterWidth.k32)
@@ -61,9 +63,11 @@ def test_batch_pipeline_matches_reference(cuda, golden, cfg):
     assert np.array_equal(rep2.flags, rep.flags)
 
 
-def test_stream_matches_reference(cuda, golden):
+@pytest.mark.parametrize("kernel", ["auto", "simt"])
+def test_stream_matches_reference(cuda, golden, kernel):
     e = golden["configs"]["5"]
     fam = family(5)
+    fam.set_kernel(kernel)
     sk = ace.AceSketch(fam, ace.CounterWidth.k32)
     for b, pb in enumerate(e["per_batch"]):
         x, _ = W.host_rows(5, b * e["batch"], e["batch"])
@@ -79,11 +83,13 @@ def test_stream_matches_reference(cuda, golden):
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
-def test_near_tie_stress_exact(cuda, oracle_c, dtype):
+@pytest.mark.parametrize("kernel", ["tc", "simt"])
+def test_near_tie_stress_exact(cuda, oracle_c, dtype, kernel):
     """Points built to sit within ~1e-9 of many hyperplanes: the fast path's
     margin routes them to the FP64 recheck and every id still matches."""
     d, k, l, seed = 96, 15, 50, 7
     fam = ace.SrpFamily(ace.SrpConfig(dim=d, k_bits=k, num_tables=l, seed=seed))
+    fam.set_kernel(kernel)
     w = fam.directions
     rng = np.random.default_rng(3)
     n = 4096
@@ -100,9 +106,11 @@ def test_near_tie_stress_exact(cuda, oracle_c, dtype):
     assert st.rechecked >= near  # every sub-1e-6 projection went to the recheck
 
 
-def test_edge_cases(cuda, oracle_c):
+@pytest.mark.parametrize("kernel", ["tc", "simt"])
+def test_edge_cases(cuda, oracle_c, kernel):
     d, k, l = 10, 4, 6
     fam = ace.SrpFamily(ace.SrpConfig(dim=d, k_bits=k, num_tables=l, seed=11))
+    fam.set_kernel(kernel)
     w = fam.directions
     x = np.zeros((77, d), dtype=np.float32)          # zero rows -> all-ones buckets
     x[1] = np.nan                                     # NaN -> p NaN -> bit 0
@@ -133,10 +141,12 @@ def test_edge_cases(cuda, oracle_c):
 
 
 @pytest.mark.parametrize("k", [1, 8, 16, 18, 30])
-def test_k_range_packing(cuda, oracle_c, k):
+@pytest.mark.parametrize("kernel", ["tc", "simt"])
+def test_k_range_packing(cuda, oracle_c, k, kernel):
     d = 12
     l = 3 if k == 30 else 9
     fam = ace.SrpFamily(ace.SrpConfig(dim=d, k_bits=k, num_tables=l, seed=k))
+    fam.set_kernel(kernel)
     x = np.random.default_rng(k).standard_normal((513, d)).astype(np.float32)
     ids = fam.buckets(x)
     ref, _ = oracle_c.buckets(fam.directions, x, k, l)
@@ -200,3 +210,20 @@ def test_restore_clone_roundtrip(cuda):
     with pytest.raises(ace.ContractViolation):
         ace.AceSketch.restore(fam, ace.CounterWidth.k32, np.zeros(5, np.uint64), 0, 0.0, False)
     assert w.dim == 40
+
+
+@pytest.mark.parametrize("d", [1, 3, 63, 64, 65, 127, 129, 192, 255, 256])
+def test_tc_dims_and_overflow_path(cuda, oracle_c, d):
+    """Every K-chunk count of the tcgen05 kernel; list-overflow rows (NaN rows
+    force every projection onto the exact path) still give exact ids."""
+    k, l = 15, 20
+    fam = ace.SrpFamily(ace.SrpConfig(dim=d, k_bits=k, num_tables=l, seed=d))
+    assert fam.kernel() == "tc"
+    rng = np.random.default_rng(d)
+    x = rng.standard_normal((2000, d)).astype(np.float32)
+    x[::50] = np.nan
+    x[7::61] = 0.0
+    ids = fam.buckets(x)
+    ref, _ = oracle_c.buckets(fam.directions, x, k, l)
+    assert np.array_equal(ids, ref)
+    assert (ids[:, 0] == 0).all()  # NaN -> all bits 0
