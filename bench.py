@@ -216,9 +216,9 @@ def main():
     clocks = Clocks(local)
     clocks.start()
     launches0 = N.dev().ace_kernel_launches()
-    phase = np.zeros(3)
+    phase = np.zeros(4)
     import ctypes as C
-    ms3 = (C.c_double * 3)()
+    ms3 = (C.c_double * 4)()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record(stream)
@@ -293,7 +293,8 @@ def main():
                    "l2": f"inputs {n * w.dim * 4 / 1e6:.0f} MB > 126 MB L2 (no flush needed)",
                    "parallelism": f"replicas x{ws}"},
         "roofline": roofline,
-        "phases_ms": {"hash_insert": phase[0], "score": phase[1], "threshold_flags": phase[2]},
+        "phases_ms": {"hash_insert": phase[0], "score": phase[1], "threshold_flags": phase[2],
+                      "projection_kernel": phase[3]},
         "gpu_launches": int(launches),
         "clocks": clk,
         "e2e": e2e,

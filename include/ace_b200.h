@@ -174,10 +174,11 @@ const uint32_t* ace_sketch_device_counters(const AceSketch* sk);
 /* Number of kernels this library has launched since load (diagnostics). */
 uint64_t ace_kernel_launches(void);
 /* Phase timing with CUDA events on the sketch's stream (off by default):
- * after each call, ms[0] = hash (+ fused insert), ms[1] = score,
- * ms[2] = threshold + flags (batch) or stream flags + insert (stream). */
+ * after each call, ms[0] = hash (+ recheck + insert), ms[1] = score,
+ * ms[2] = threshold + flags (batch) or stream flags + insert (stream),
+ * ms[3] = the projection kernel alone (tcgen05 path). */
 ace_status ace_sketch_set_timing(AceSketch* sk, int enable);
-ace_status ace_sketch_timings(const AceSketch* sk, double* ms3);
+ace_status ace_sketch_timings(const AceSketch* sk, double* ms4);
 
 #ifdef __cplusplus
 }

@@ -2,6 +2,7 @@
 // Each entry point cites the reference function it stands in for.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -88,11 +89,11 @@ struct AceSketch {
   DevState* hst = nullptr;   // pinned host mirror
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
-  DevBuf ids, sums, stage, flags, scores, demand, near, overflow;
+  DevBuf ids, sums, stage, flags, scores, demand, near, overflow, x16, rowthr;
   // phase timing (ace_sketch_set_timing)
   bool timing = false;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  bool ev_used[4] = {false, false, false, false};
+  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  bool ev_used[6] = {false, false, false, false, false, false};
   void mark(int i) {
     if (timing) {
       cudaEventRecord(ev[i], stream);
@@ -212,7 +213,7 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
     t.k_bits = f->d.k_bits;
     t.tables = f->d.tables;
     t.tpt = f->d.tpt;
-    t.ntiles = f->d.ntiles;
+    t.ntiles = f->tc.ntiles;
     t.nkc = f->tc.nkc;
     t.w16 = f->tc.w16;
     // error bound of the fp16x3 split relative to ||x~|| ||w^||
@@ -224,11 +225,26 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
     ACE_CUDA(sk->near.ensure(cap * sizeof(unsigned long long)));
     ACE_CUDA(sk->overflow.ensure(((n + 31) / 32) * sizeof(uint32_t)));
     ACE_CUDA(cudaMemsetAsync(sk->overflow.p, 0, ((n + 31) / 32) * sizeof(uint32_t), sk->stream));
+    const uint64_t tiles = (n + 127) / 128;
+    ACE_CUDA(sk->x16.ensure(tiles * f->tc.nkc * 2 * 16384));
+    ACE_CUDA(sk->rowthr.ensure(tiles * 128 * sizeof(float)));
+    t.x16 = sk->x16.as<uint16_t>();
+    t.rowthr = sk->rowthr.as<float>();
     t.near_list = sk->near.as<unsigned long long>();
     t.near_cap = sk->near.bytes / sizeof(unsigned long long);
     t.overflow_rows = sk->overflow.as<uint32_t>();
     t.st = sk->st;
+    {
+      static int dbg = -1;
+      if (dbg < 0) {
+        const char* e = getenv("ACE_TC_DBG");
+        dbg = e ? atoi(e) : 0;
+      }
+      t.dbg = dbg;
+    }
+    sk->mark(4);
     ACE_CUDA(launch_hash_tc(t, sk->stream));
+    sk->mark(5);
     ACE_CUDA(launch_recheck(t, f->d.w64, sk->stream));
     if (insert)
       ACE_CUDA(launch_apply_ids(sk->ids.as<uint32_t>(), n, f->d.tables, f->d.k_bits, sk->counters, sk->cap,
@@ -482,6 +498,8 @@ ace_status ace_sketch_destroy(AceSketch* sk) {
   sk->demand.release();
   sk->near.release();
   sk->overflow.release();
+  sk->x16.release();
+  sk->rowthr.release();
   if (sk->counters) cudaFree(sk->counters);
   if (sk->st) cudaFree(sk->st);
   if (sk->hst) cudaFreeHost(sk->hst);
@@ -757,12 +775,14 @@ ace_status ace_sketch_set_timing(AceSketch* sk, int enable) {
 
 ace_status ace_sketch_timings(const AceSketch* sk, double* ms3) {
   if (!sk || !ms3) return fail(ACE_E_CONTRACT, "ace_sketch_timings: null argument");
-  for (int i = 0; i < 3; ++i) {
+  const int pairs[4][2] = {{0, 1}, {1, 2}, {2, 3}, {4, 5}};
+  for (int i = 0; i < 4; ++i) {
     ms3[i] = 0.0;
-    if (sk->timing && sk->ev_used[i] && sk->ev_used[i + 1]) {
+    const int a = pairs[i][0], b = pairs[i][1];
+    if (sk->timing && sk->ev_used[a] && sk->ev_used[b]) {
       float ms = 0.f;
-      ACE_CUDA(cudaEventSynchronize(sk->ev[i + 1]));
-      ACE_CUDA(cudaEventElapsedTime(&ms, sk->ev[i], sk->ev[i + 1]));
+      ACE_CUDA(cudaEventSynchronize(sk->ev[b]));
+      ACE_CUDA(cudaEventElapsedTime(&ms, sk->ev[a], sk->ev[b]));
       ms3[i] = ms;
     }
   }

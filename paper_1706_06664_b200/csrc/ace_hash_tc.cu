@@ -13,11 +13,12 @@
 //
 // Warp roles (256 threads, one CTA per SM, persistent over point tiles):
 //   warp 0      W producer: cp.async.bulk of pre-swizzled W blocks (TMA engine)
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2-3   X converters: fp32 rows -> scaled fp16 hi/lo, SW128 K-major smem
-//   warps 4-7   epilogue: tcgen05.ld accumulators -> signs, near ties, buckets
-// Pipelines (mbarriers): W stages full/empty, A buffers full/empty,
-// 4 TMEM accumulator buffers of 128 columns full/empty.
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (A from TMEM)
+//   warps 2-5   X converters: one point row per thread, fp32 -> scaled fp16
+//               hi/lo, tcgen05.st into the TMEM A operand
+//   warps 6-9   epilogue: tcgen05.ld accumulators -> signs, near ties, buckets
+// Pipelines (mbarriers): W smem stages full/empty, TMEM A buffers full/empty,
+// 2 TMEM accumulator buffers of 128 columns full/empty.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -32,21 +33,25 @@ constexpr int kRows = 128;                 // points per tile (MMA M)
 constexpr int kChunk = 64;                 // K elements per chunk (128 B of fp16)
 constexpr int kBlockBytes = kRows * 128;   // one 128 x 64 fp16 block = 16 KB
 constexpr int kAccBufs = 4;                // TMEM accumulators (4 x 128 columns)
-constexpr int kMaxWStages = 4;
-constexpr int kThreads = 256;
+constexpr int kMaxWStages = 6;
+constexpr int kThreads = 192;
 constexpr size_t kSmemLimit = 232448;      // 227 KB per CTA
+constexpr uint32_t kCluster = 1;           // CTAs sharing each W stage (TMA multicast)
 
 struct TcLayout {
   uint32_t nkc, n_abuf, n_wst;
   size_t a_bytes, w_bytes, total;
 };
 
+// Shared memory: the A tile (x, fp16 hi | lo, SW128 image from the pre-pass),
+// double buffered when dpad <= 128, then a ring of W stages (32 KB each).
+// TMEM: 4 accumulators x 128 columns.
 __host__ __device__ inline TcLayout tc_layout(uint32_t nkc) {
   TcLayout L;
   L.nkc = nkc;
   L.n_abuf = nkc <= 2 ? 2 : 1;
   L.a_bytes = static_cast<size_t>(L.n_abuf) * nkc * 2 * kBlockBytes;
-  const size_t room = kSmemLimit - 2048 - 1024 - L.a_bytes;  // static smem + align slack
+  const size_t room = kSmemLimit - 1024 - 1024 - L.a_bytes;
   size_t st = room / (2 * kBlockBytes);
   if (st > kMaxWStages) st = kMaxWStages;
   L.n_wst = static_cast<uint32_t>(st);
@@ -87,6 +92,29 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_mc(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                            uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
+      "%4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -160,33 +188,151 @@ __device__ __forceinline__ double exact_proj(const double* __restrict__ w, const
   return acc;
 }
 
-// ---- the kernel ----------------------------------------------------------------
+// ---- X conversion pre-pass ------------------------------------------------------
+
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+  return (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(b))) << 16) |
+         __half_as_ushort(__float2half_rn(a));
+}
+
+// Element k of a row (fp32 or fp64 source), 0 beyond dim.
+__device__ __forceinline__ float load_x(const TcArgs& a, uint64_t row, uint64_t k) {
+  if (k >= a.dim) return 0.0f;
+  if (a.x_f64) return static_cast<float>(static_cast<const double*>(a.x)[row * a.ld + k]);
+  return static_cast<const float*>(a.x)[row * a.ld + k];
+}
+
+// One warp per row: max |x| (NaN > inf > finite as magnitude bits), power-of-
+// two scale to [2^14, 2^15), fp16 hi + lo split written straight into the
+// SW128 K-major shared-memory image of its 128-row tile, and the row's error
+// threshold thr = c * ||x~|| * 2^14 + abs (-1: exact zero row, +inf: recheck all).
+// Rows past n (tile padding) are written as zeros.
+__global__ void __launch_bounds__(256) convert_x_kernel(const TcArgs a, uint64_t rows_padded) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  const uint32_t groups = (a.nkc * kChunk + 127) / 128;
+  const bool vec4 = !a.x_f64 && (a.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
+  for (uint64_t row = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows_padded;
+       row += warps) {
+    const bool live = row < a.n;
+    uint32_t mb = 0u;
+    if (live) {
+      for (uint32_t g = 0; g < groups; ++g) {
+        const uint64_t k0 = g * 128u + lane * 4u;
+        if (vec4 && k0 + 3 < a.dim) {
+          const uint4 u = *reinterpret_cast<const uint4*>(static_cast<const float*>(a.x) + row * a.ld + k0);
+          mb = max(mb, max(max(u.x & 0x7fffffffu, u.y & 0x7fffffffu), max(u.z & 0x7fffffffu, u.w & 0x7fffffffu)));
+        } else {
+          for (uint32_t e = 0; e < 4; ++e) mb = max(mb, __float_as_uint(load_x(a, row, k0 + e)) & 0x7fffffffu);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+    const bool nan = mb > 0x7f800000u;
+    const float m = __uint_as_float(nan ? 0x7f800000u : mb);
+    const bool zero = (m == 0.0f);
+    const bool wild = nan || !(m < 0x1.0p100f) || (!zero && m < 0x1.0p-100f);
+    float scale = 0.0f;
+    if (live && !zero && !wild) {
+      const int e = static_cast<int>((__float_as_uint(m) >> 23) & 0xffu) - 127;
+      scale = __uint_as_float(static_cast<uint32_t>(127 + 14 - e) << 23);
+    }
+    const uint64_t tile = row / kRows;
+    const uint32_t r = static_cast<uint32_t>(row % kRows);
+    float ss = 0.0f;
+    for (uint32_t g = 0; g < groups; ++g) {
+      const uint32_t k0 = g * 128u + lane * 4u;
+      const uint32_t kc = k0 / kChunk, kk = k0 % kChunk;
+      if (kc >= a.nkc) continue;
+      float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      if (live && scale != 0.0f) {
+        if (vec4 && k0 + 3 < a.dim) {
+          const float4 u = *reinterpret_cast<const float4*>(static_cast<const float*>(a.x) + row * a.ld + k0);
+          v[0] = u.x;
+          v[1] = u.y;
+          v[2] = u.z;
+          v[3] = u.w;
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) v[e] = load_x(a, row, k0 + e);
+        }
+      }
+      uint32_t hi[2], lo[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const float x0 = v[2 * i] * scale, x1 = v[2 * i + 1] * scale;
+        ss = fmaf(x0, x0, fmaf(x1, x1, ss));
+        const float h0 = __half2float(__float2half_rn(x0)), h1 = __half2float(__float2half_rn(x1));
+        hi[i] = pack_h2(h0, h1);
+        lo[i] = pack_h2(x0 - h0, x1 - h1);
+      }
+      uint8_t* blk = reinterpret_cast<uint8_t*>(a.x16) + ((tile * a.nkc + kc) * 2) * kBlockBytes;
+      const uint32_t off = sw128_off(r, kk);
+      *reinterpret_cast<uint2*>(blk + off) = make_uint2(hi[0], hi[1]);
+      *reinterpret_cast<uint2*>(blk + kBlockBytes + off) = make_uint2(lo[0], lo[1]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) {
+      float thr;
+      if (!live || zero) {
+        thr = -1.0f;
+      } else if (wild) {
+        thr = __int_as_float(0x7f800000);
+      } else {
+        const float nx = sqrtf(ss * (1.0f + static_cast<float>(a.dim + 4) * 0x1.0p-23f)) * (1.0f + 0x1.0p-20f);
+        thr = a.margin_c * nx * 16384.0f + static_cast<float>(a.dim) * 0x1.0p-10f;
+      }
+      a.rowthr[row] = thr;
+    }
+  }
+}
+
+// Cold path: push the near-tie columns (bit jj of mask = column dir0 + jj).
+__device__ __noinline__ void push_near_mask(DevState* st, unsigned long long* list, unsigned long long cap,
+                                            uint32_t* overflow_rows, uint32_t mask, uint64_t row, uint32_t dir0) {
+  while (mask) {
+    const uint32_t jj = __ffs(mask) - 1;
+    mask &= mask - 1;
+    const unsigned long long slot = atomicAdd(&st->near_count, 1ull);
+    if (slot < cap) {
+      list[slot] = (static_cast<unsigned long long>(row) << 32) | (dir0 + jj);
+    } else {
+      atomicOr(&overflow_rows[row >> 5], 1u << (row & 31));
+      st->near_overflow = 1;
+    }
+  }
+}
+
+// ---- the projection kernel ----------------------------------------------------------
 
 __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t bar_wfull[kMaxWStages], bar_wempty[kMaxWStages];
   __shared__ __align__(8) uint64_t bar_afull[2], bar_aempty[2];
   __shared__ __align__(8) uint64_t bar_accfull[kAccBufs], bar_accempty[kAccBufs];
-  __shared__ float rowthr[2][kRows];
   __shared__ uint32_t tmem_base_sh;
 
   const TcLayout L = tc_layout(a.nkc);
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* A = base;                  // [n_abuf][nkc][2][16 KB]
+  uint8_t* Asm = base;                // [n_abuf][nkc][2][16 KB]
   uint8_t* Wsm = base + L.a_bytes;    // [n_wst][2][16 KB]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t n_tiles = (a.n + kRows - 1) / kRows;
   const uint32_t K = a.k_bits;
+  const uint32_t R = a.k_bits * a.tables;  // directions, packed densely in 128-column tiles
+  const uint32_t a_tile_bytes = a.nkc * 2u * kBlockBytes;
 
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < L.n_wst; ++s) {
       mbar_init(&bar_wfull[s], 1);
-      mbar_init(&bar_wempty[s], 1);
+      mbar_init(&bar_wempty[s], kCluster);  // every CTA's MMA must have released the stage
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&bar_afull[b], 2);   // two converter warps
-      mbar_init(&bar_aempty[b], 5);  // MMA commit + four epilogue warps
+      mbar_init(&bar_afull[b], 1);
+      mbar_init(&bar_aempty[b], 1);
     }
     for (int b = 0; b < kAccBufs; ++b) {
       mbar_init(&bar_accfull[b], 1);
@@ -201,25 +347,45 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
   }
   tc_before();
   __syncthreads();
+  cluster_sync_all();  // remote CTAs may signal our barriers from here on
   tc_after();
   const uint32_t tmem_base = tmem_base_sh;
+  const uint32_t crank = cluster_ctarank();
+  const uint16_t cmask = static_cast<uint16_t>((1u << kCluster) - 1u);
+  // every CTA runs the same number of tile iterations (tiles past the end are
+  // skipped by the epilogue) so a cluster's shared W pipeline stays in lockstep
+  const uint64_t iters = (n_tiles + gridDim.x - 1) / gridDim.x;
+  const uint64_t t_end = static_cast<uint64_t>(blockIdx.x) + iters * gridDim.x;
 
   if (warp == 0) {
-    // ---------------- W producer ----------------
+    // ---------------- producer: A tile (once per tile) + W stages ----------------
     if (lane == 0) {
-      uint32_t s = 0, ph = 0;
-      for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      uint32_t s = 0, ph = 0, it = 0;
+      for (uint64_t t = blockIdx.x; t < t_end; t += gridDim.x, ++it) {
+        const uint32_t buf = it % L.n_abuf, use = it / L.n_abuf;
+        mbar_wait(&bar_aempty[buf], (use & 1u) ^ 1u);
+        const uint64_t tt = t < n_tiles ? t : n_tiles - 1;  // past the end: reload the last tile
+        mbar_expect_tx(&bar_afull[buf], a_tile_bytes);
+        bulk_g2s(Asm + static_cast<size_t>(buf) * a_tile_bytes,
+                 reinterpret_cast<const uint8_t*>(a.x16) + tt * a_tile_bytes, a_tile_bytes, &bar_afull[buf]);
         for (uint32_t j = 0; j < a.ntiles; ++j) {
-          const uint32_t tables_here = min(a.tpt, a.tables - j * a.tpt);
-          const uint32_t nmma = (tables_here * K + 15u) & ~15u;
+          const uint32_t nmma = (min(128u, R - j * 128u) + 15u) & ~15u;
           const uint32_t bytes = nmma * 128u;
+          const uint32_t part = bytes / kCluster;  // this CTA's slice, multicast to the cluster
           for (uint32_t kc = 0; kc < a.nkc; ++kc) {
             mbar_wait(&bar_wempty[s], ph ^ 1u);
             mbar_expect_tx(&bar_wfull[s], 2u * bytes);
-            const uint16_t* src = a.w16 + (static_cast<uint64_t>(j) * a.nkc + kc) * 2u * (kBlockBytes / 2);
+            const uint8_t* src =
+                reinterpret_cast<const uint8_t*>(a.w16) + (static_cast<uint64_t>(j) * a.nkc + kc) * 2u * kBlockBytes;
             uint8_t* dst = Wsm + static_cast<size_t>(s) * 2 * kBlockBytes;
-            bulk_g2s(dst, src, bytes, &bar_wfull[s]);
-            bulk_g2s(dst + kBlockBytes, src + kBlockBytes / 2, bytes, &bar_wfull[s]);
+            if (kCluster == 1) {
+              bulk_g2s(dst, src, bytes, &bar_wfull[s]);
+              bulk_g2s(dst + kBlockBytes, src + kBlockBytes, bytes, &bar_wfull[s]);
+            } else {
+              const uint32_t o = crank * part;
+              bulk_g2s_mc(dst + o, src + o, part, &bar_wfull[s], cmask);
+              bulk_g2s_mc(dst + kBlockBytes + o, src + kBlockBytes + o, part, &bar_wfull[s], cmask);
+            }
             if (++s == L.n_wst) {
               s = 0;
               ph ^= 1u;
@@ -229,17 +395,16 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
+    // ---------------- MMA issuer (A and B from shared memory) ----------------
     if (lane == 0) {
       uint32_t s = 0, wph = 0, acc = 0, accph = 0, it = 0;
-      for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+      for (uint64_t t = blockIdx.x; t < t_end; t += gridDim.x, ++it) {
         const uint32_t buf = it % L.n_abuf, use = it / L.n_abuf;
         mbar_wait(&bar_afull[buf], use & 1u);
         tc_after();
-        const uint8_t* Ab = A + static_cast<size_t>(buf) * a.nkc * 2 * kBlockBytes;
+        const uint8_t* Ab = Asm + static_cast<size_t>(buf) * a_tile_bytes;
         for (uint32_t j = 0; j < a.ntiles; ++j) {
-          const uint32_t tables_here = min(a.tpt, a.tables - j * a.tpt);
-          const uint32_t nmma = (tables_here * K + 15u) & ~15u;
+          const uint32_t nmma = (min(128u, R - j * 128u) + 15u) & ~15u;
           const uint32_t idesc = idesc_f16(nmma);
           mbar_wait(&bar_accempty[acc], accph ^ 1u);
           tc_after();
@@ -248,17 +413,22 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
             mbar_wait(&bar_wfull[s], wph);
             tc_after();
             const uint32_t a_hi = smem_u32(Ab + (static_cast<size_t>(kc) * 2 + 0) * kBlockBytes);
-            const uint32_t a_lo = smem_u32(Ab + (static_cast<size_t>(kc) * 2 + 1) * kBlockBytes);
+            const uint32_t a_lo = a_hi + kBlockBytes;
             const uint32_t b_hi = smem_u32(Wsm + static_cast<size_t>(s) * 2 * kBlockBytes);
             const uint32_t b_lo = b_hi + kBlockBytes;
+            if (!(a.dbg & 2)) {
 #pragma unroll
-            for (uint32_t kk = 0; kk < 4; ++kk) {
-              const uint32_t off = kk * 32u;  // 16 fp16 along K
-              mma_f16(dt, sw128_desc(a_hi + off), sw128_desc(b_hi + off), idesc, (kc | kk) != 0u);
-              mma_f16(dt, sw128_desc(a_lo + off), sw128_desc(b_hi + off), idesc, 1u);
-              mma_f16(dt, sw128_desc(a_hi + off), sw128_desc(b_lo + off), idesc, 1u);
+              for (uint32_t kk = 0; kk < 4; ++kk) {
+                const uint32_t off = kk * 32u;  // 16 fp16 along K
+                mma_f16(dt, sw128_desc(a_hi + off), sw128_desc(b_hi + off), idesc, (kc | kk) != 0u);
+                mma_f16(dt, sw128_desc(a_lo + off), sw128_desc(b_hi + off), idesc, 1u);
+                mma_f16(dt, sw128_desc(a_hi + off), sw128_desc(b_lo + off), idesc, 1u);
+              }
             }
-            mma_commit(&bar_wempty[s]);
+            if (kCluster == 1)
+              mma_commit(&bar_wempty[s]);
+            else
+              mma_commit_mc(&bar_wempty[s], cmask);
             if (++s == L.n_wst) {
               s = 0;
               wph ^= 1u;
@@ -274,143 +444,69 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
       }
     }
     __syncwarp();
-  } else if (warp < 4) {
-    // ---------------- X converters ----------------
-    const uint32_t cw = warp - 2;
-    uint32_t it = 0;
-    const uint32_t groups = (a.nkc * kChunk + 127) / 128;  // 128 K per lane-group pass
-    for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
-      const uint32_t buf = it % L.n_abuf, use = it / L.n_abuf;
-      mbar_wait(&bar_aempty[buf], (use & 1u) ^ 1u);
-      uint8_t* Ab = A + static_cast<size_t>(buf) * a.nkc * 2 * kBlockBytes;
-      for (uint32_t r = cw; r < kRows; r += 2) {
-        const uint64_t row = t * kRows + r;
-        const bool live = row < a.n;
-        float v[2][4];
-        float m = 0.0f;
-#pragma unroll
-        for (uint32_t g = 0; g < 2; ++g)
-#pragma unroll
-          for (uint32_t e = 0; e < 4; ++e) {
-            const uint64_t k = g * 128u + lane * 4u + e;
-            float val = 0.0f;
-            if (live && g < groups && k < a.dim) {
-              if (a.x_f64)
-                val = static_cast<float>(static_cast<const double*>(a.x)[row * a.ld + k]);
-              else
-                val = static_cast<const float*>(a.x)[row * a.ld + k];
-            }
-            v[g][e] = val;
-            m = fmaxf(m, fabsf(val));
-            if (val != val) m = __int_as_float(0x7f800000);  // NaN -> force exact path
-          }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        const bool zero = (m == 0.0f);
-        const bool wild = !(m < 0x1.0p100f) || (!zero && m < 0x1.0p-100f);
-        float scale = 1.0f;
-        if (!zero && !wild) {
-          const int e = static_cast<int>((__float_as_uint(m) >> 23) & 0xffu) - 127;
-          scale = __uint_as_float(static_cast<uint32_t>(127 + 14 - e) << 23);
-        }
-        float ss = 0.0f;
-#pragma unroll
-        for (uint32_t g = 0; g < 2; ++g) {
-          if (g >= groups) break;
-          const uint32_t k0 = g * 128u + lane * 4u;  // 4 consecutive K
-          const uint32_t kc = k0 / kChunk, kk = k0 % kChunk;
-          __half hi[4], lo[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float xs = wild ? 0.0f : v[g][e] * scale;
-            ss = fmaf(xs, xs, ss);
-            hi[e] = __float2half_rn(xs);
-            lo[e] = __float2half_rn(xs - __half2float(hi[e]));
-          }
-          if (kc < a.nkc) {
-            uint8_t* blk = Ab + static_cast<size_t>(kc) * 2 * kBlockBytes;
-            const uint32_t off = sw128_off(r, kk);
-            uint2 ph, pl;
-            ph.x = (static_cast<uint32_t>(__half_as_ushort(hi[1])) << 16) | __half_as_ushort(hi[0]);
-            ph.y = (static_cast<uint32_t>(__half_as_ushort(hi[3])) << 16) | __half_as_ushort(hi[2]);
-            pl.x = (static_cast<uint32_t>(__half_as_ushort(lo[1])) << 16) | __half_as_ushort(lo[0]);
-            pl.y = (static_cast<uint32_t>(__half_as_ushort(lo[3])) << 16) | __half_as_ushort(lo[2]);
-            *reinterpret_cast<uint2*>(blk + off) = ph;
-            *reinterpret_cast<uint2*>(blk + kBlockBytes + off) = pl;
-          }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-        if (lane == 0) {
-          float thr;
-          if (!live || zero) {
-            thr = -1.0f;  // exact zeros: every projection is +-0, bit 1
-          } else if (wild) {
-            thr = __int_as_float(0x7f800000);  // recheck every projection exactly
-          } else {
-            const float nx = sqrtf(ss * (1.0f + static_cast<float>(a.dim + 4) * 0x1.0p-23f)) * (1.0f + 0x1.0p-20f);
-            thr = a.margin_c * nx * 16384.0f + static_cast<float>(a.dim) * 0x1.0p-10f;
-          }
-          rowthr[buf][r] = thr;
-        }
-      }
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bar_afull[buf]);
-    }
   } else {
-    // ---------------- epilogue ----------------
-    const uint32_t q = warp - 4;  // TMEM lane quarter
+    // ---------------- epilogue (warps 2-5; TMEM lane quarter = warp % 4) ----------------
+    // Per 32-column chunk: sign bits packed MSB-first (one funnel shift per
+    // column), near ties by one unsigned min over |v| (bits << 1), four
+    // independent chains for ILP; buckets cut out of the column stream with
+    // funnel shifts, tables straddling direction tiles carried in prev3.
+    const uint32_t q = warp & 3;
     const uint32_t r = q * 32u + lane;
-    uint32_t it = 0, acc = 0, accph = 0;
-    for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
-      const uint32_t buf = it % L.n_abuf, use = it / L.n_abuf;
-      mbar_wait(&bar_afull[buf], use & 1u);
-      const float thr = rowthr[buf][r];
+    const uint32_t kmask = (K >= 32u) ? 0xffffffffu : ((1u << K) - 1u);
+    uint32_t acc = 0, accph = 0;
+    for (uint64_t t = blockIdx.x; t < t_end; t += gridDim.x) {
       const uint64_t row = t * kRows + r;
       const bool valid = row < a.n;
+      const float thr = valid ? a.rowthr[row] : -1.0f;
+      const bool zero_row = thr < 0.0f;
+      const uint32_t thr_u = zero_row ? 0u : (isinf(thr) ? 0xffffffffu : (__float_as_uint(thr) << 1));
+      uint32_t prev3 = 0u;
+      uint32_t next_table = 0;
       for (uint32_t j = 0; j < a.ntiles; ++j) {
-        const uint32_t tables_here = min(a.tpt, a.tables - j * a.tpt);
-        const uint32_t used = tables_here * K;
-        const uint32_t table0 = j * a.tpt;
+        const uint32_t used = min(128u, R - j * 128u);
+        const uint32_t col0 = j * 128u;
         mbar_wait(&bar_accfull[acc], accph);
         tc_after();
-        uint32_t bucket = 0, b = 0, tt = 0;
-        for (uint32_t c0 = 0; c0 < used; c0 += 32) {
-          uint32_t v[32];
-          ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + acc * 128u + c0, v);
-          tmem_wait_ld();
-          const uint32_t ncol = min(32u, used - c0);
-          bool anynear = false;
+        uint32_t sg0 = 0u, sg1 = 0u, sg2 = 0u, sg3 = 0u;
+        if (!(a.dbg & 1)) {
+#pragma unroll 1
+          for (uint32_t cc = 0; cc < used; cc += 32u) {
+            uint32_t v[32];
+            ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + acc * 128u + cc, v);
+            tmem_wait_ld();
+            const uint32_t ncol = min(32u, used - cc);
+            uint32_t n4[4] = {0u, 0u, 0u, 0u}, m4[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+            if (ncol == 32u) {
 #pragma unroll
-          for (uint32_t jj = 0; jj < 32; ++jj) {
-            if (jj < ncol) {
-              const float f = __uint_as_float(v[jj]);
-              bucket = (bucket << 1) | (f >= 0.0f ? 1u : 0u);
-              anynear |= !(fabsf(f) > thr);
-              if (++b == K) {
-                if (valid) a.ids[static_cast<uint64_t>(table0 + tt) * a.n + row] = bucket;
-                ++tt;
-                b = 0;
-                bucket = 0;
-              }
-            }
-          }
-          if (anynear && valid) {
+              for (int jj = 0; jj < 8; ++jj)
 #pragma unroll
-            for (uint32_t jj = 0; jj < 32; ++jj) {
-              const float f = __uint_as_float(v[jj]);
-              if (jj < ncol && !(fabsf(f) > thr)) {
-                const uint32_t dir = table0 * K + c0 + jj;
-                const unsigned long long slot = atomicAdd(&a.st->near_count, 1ull);
-                if (slot < a.near_cap) {
-                  a.near_list[slot] = (static_cast<unsigned long long>(row) << 32) | dir;
-                } else {
-                  atomicOr(&a.overflow_rows[row >> 5], 1u << (row & 31));
-                  a.st->near_overflow = 1;
+                for (int g = 0; g < 4; ++g) {
+                  n4[g] = (n4[g] << 1) | (v[g * 8 + jj] >> 31);
+                  m4[g] = min(m4[g], v[g * 8 + jj] << 1);
                 }
-              }
+            } else {
+#pragma unroll
+              for (int jj = 0; jj < 8; ++jj)
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                  n4[g] = (n4[g] << 1) | (v[g * 8 + jj] >> 31);
+                  if (static_cast<uint32_t>(g * 8 + jj) < ncol) m4[g] = min(m4[g], v[g * 8 + jj] << 1);
+                }
             }
+            const uint32_t neg = (n4[0] << 24) | (n4[1] << 16) | (n4[2] << 8) | n4[3];
+            const uint32_t mn = min(min(m4[0], m4[1]), min(m4[2], m4[3]));
+            if (!zero_row && valid && mn <= thr_u) {
+              uint32_t nm = 0u;
+#pragma unroll
+              for (int jj = 0; jj < 32; ++jj)
+                nm |= ((static_cast<uint32_t>(jj) < ncol && (v[jj] << 1) <= thr_u) ? 1u : 0u) << jj;
+              push_near_mask(a.st, a.near_list, a.near_cap, a.overflow_rows, nm, row, col0 + cc);
+            }
+            const uint32_t sgw = zero_row ? 0xffffffffu : ~neg;  // bit (31-jj) = column cc+jj >= 0
+            sg0 = cc == 0 ? sgw : sg0;
+            sg1 = cc == 32 ? sgw : sg1;
+            sg2 = cc == 64 ? sgw : sg2;
+            sg3 = cc == 96 ? sgw : sg3;
           }
         }
         tc_before();
@@ -420,14 +516,27 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
           acc = 0;
           accph ^= 1u;
         }
+        // buckets of the tables whose last column lies in this tile: bits
+        // [t*K, t*K+K) of the big-endian column stream, words 4j-1 .. 4j+3
+        const uint32_t end_col = col0 + used;
+        for (; next_table < a.tables && (next_table + 1) * K <= end_col; ++next_table) {
+          const uint32_t s0 = next_table * K;
+          const int wi = static_cast<int>(s0 >> 5) - static_cast<int>(4 * j);  // -1 .. 3
+          const uint32_t off = s0 & 31u;
+          const uint32_t hi = wi < 0 ? prev3 : (wi == 0 ? sg0 : (wi == 1 ? sg1 : (wi == 2 ? sg2 : sg3)));
+          const uint32_t lo = wi < 0 ? sg0 : (wi == 0 ? sg1 : (wi == 1 ? sg2 : (wi == 2 ? sg3 : 0u)));
+          const unsigned long long win = (static_cast<unsigned long long>(hi) << 32) | lo;
+          const uint32_t bucket = static_cast<uint32_t>(win >> (64u - off - K)) & kmask;
+          if (valid) a.ids[static_cast<uint64_t>(next_table) * a.n + row] = bucket;
+        }
+        prev3 = sg3;
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bar_aempty[buf]);
     }
   }
 
   tc_before();
   __syncthreads();
+  cluster_sync_all();  // no CTA leaves while its peers may still multicast into it
   tc_after();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
@@ -498,20 +607,17 @@ __global__ void dir_norm_kernel(const double* __restrict__ w64, uint64_t dim, ui
 }
 
 __global__ void pack_w16_kernel(const double* __restrict__ w64, const double* __restrict__ inv,
-                                FamilyDev f, uint32_t nkc, uint16_t* w16) {
-  const uint64_t total = static_cast<uint64_t>(f.ntiles) * kRows * nkc * kChunk;
+                                FamilyDev f, uint32_t ntiles, uint32_t nkc, uint16_t* w16) {
+  const uint64_t total = static_cast<uint64_t>(ntiles) * kRows * nkc * kChunk;
   for (uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
        idx += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint32_t k = idx % (nkc * kChunk);
     const uint32_t rr = (idx / (nkc * kChunk)) % kRows;
     const uint32_t j = static_cast<uint32_t>(idx / (static_cast<uint64_t>(nkc) * kChunk * kRows));
     const uint32_t kc = k / kChunk, kk = k % kChunk;
-    const uint32_t table = j * f.tpt + rr / f.k_bits;
+    const uint64_t dir = static_cast<uint64_t>(j) * kRows + rr;  // directions packed densely
     double w = 0.0;
-    if (rr < f.tpt * f.k_bits && table < f.tables && k < f.dim) {
-      const uint64_t dir = static_cast<uint64_t>(table) * f.k_bits + rr % f.k_bits;
-      w = w64[dir * f.dim + k] * inv[dir];
-    }
+    if (dir < f.rows && k < f.dim) w = w64[dir * f.dim + k] * inv[dir];
     const __half hi = __double2half(w);
     const __half lo = __double2half(w - static_cast<double>(__half2float(hi)));
     uint8_t* blk = reinterpret_cast<uint8_t*>(w16) + ((static_cast<uint64_t>(j) * nkc + kc) * 2) * kBlockBytes;
@@ -532,15 +638,16 @@ cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc) {
   if (!tc_supported(f.dim) || f.k_bits > 128) return cudaSuccess;
   const uint32_t nkc = static_cast<uint32_t>((f.dim + kChunk - 1) / kChunk);
   const TcLayout L = tc_layout(nkc);
-  if (L.n_wst < 2) return cudaSuccess;
+  if (nkc > 4 || tc_layout(nkc).n_wst < 2) return cudaSuccess;
   tc->nkc = nkc;
-  const size_t bytes = static_cast<size_t>(f.ntiles) * nkc * 2 * kBlockBytes;
+  tc->ntiles = (f.rows + kRows - 1) / kRows;
+  const size_t bytes = static_cast<size_t>(tc->ntiles) * nkc * 2 * kBlockBytes;
   cudaError_t e = cudaMalloc(&tc->w16, bytes);
   if (e != cudaSuccess) return e;
   double* inv = nullptr;
   if ((e = cudaMalloc(&inv, sizeof(double) * f.rows)) != cudaSuccess) return e;
   dir_norm_kernel<<<(f.rows + 127) / 128, 128>>>(f.w64, f.dim, f.rows, inv);
-  pack_w16_kernel<<<1024, 256>>>(f.w64, inv, f, nkc, tc->w16);
+  pack_w16_kernel<<<1024, 256>>>(f.w64, inv, f, tc->ntiles, nkc, tc->w16);
   count_launch(2);
   e = cudaDeviceSynchronize();
   cudaFree(inv);
@@ -567,10 +674,33 @@ cudaError_t launch_hash_tc(const TcArgs& a, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const uint64_t tiles = (a.n + kRows - 1) / kRows;
-  const unsigned grid = static_cast<unsigned>(tiles < static_cast<uint64_t>(sms) ? tiles : sms);
-  hash_tc_kernel<<<grid, kThreads, tc_layout(a.nkc).total, s>>>(a);
+  {
+    const uint64_t rows = tiles * kRows;
+    uint64_t blocks = (rows + 7) / 8;
+    if (blocks > static_cast<uint64_t>(sms) * 16) blocks = static_cast<uint64_t>(sms) * 16;
+    convert_x_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(a, rows);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  uint64_t grid = tiles < static_cast<uint64_t>(sms) ? tiles : static_cast<uint64_t>(sms);
+  grid = (grid + kCluster - 1) / kCluster * kCluster;
+  if (grid > static_cast<uint64_t>(sms)) grid = static_cast<uint64_t>(sms) / kCluster * kCluster;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = tc_layout(a.nkc).total;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, hash_tc_kernel, a);
   count_launch();
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_recheck(const TcArgs& a, const double* w64, cudaStream_t s) {

@@ -336,21 +336,29 @@ __global__ void apply_ids_kernel(const uint32_t* __restrict__ ids, uint64_t n, u
       const uint64_t t = idx / n;
       key = (t << k_bits) | ids[idx];
     }
-    const unsigned vmask = __ballot_sync(0xffffffffu, valid);
-    if (valid) {
-      const unsigned peers = __match_any_sync(vmask, key);
-      if (lane == __ffs(peers) - 1) {
-        const unsigned m = __popc(peers);
+    // up to three ballot rounds aggregate runs of equal counters, then the
+    // remaining lanes update individually
+    unsigned rem = __ballot_sync(0xffffffffu, valid);
+    for (int round = 0; round < 4 && rem; ++round) {
+      const int leader = __ffs(rem) - 1;
+      const unsigned long long kl = __shfl_sync(0xffffffffu, key, leader);
+      const unsigned eq = __ballot_sync(0xffffffffu, key == kl) & rem;
+      const bool solo = round == 3;  // last round: every remaining lane for itself
+      const bool mine = solo ? ((rem >> lane) & 1u) : (lane == leader);
+      if (mine) {
+        const unsigned m = solo ? 1u : __popc(eq);
+        const unsigned long long kk = solo ? key : kl;
         if (sign > 0) {
-          const unsigned old = atomicAdd(&counters[key], m);
+          const unsigned old = atomicAdd(&counters[kk], m);
           if (old > 0xffffffffu - m) st->saturated = 1;
           dT += insert_numerator(old, m, cap);
         } else {
           // removals: numerator sum_{r<m} (2*(old-r) - 1) = m*(2*old - m)
-          const unsigned old = atomicSub(&counters[key], m);
+          const unsigned old = atomicSub(&counters[kk], m);
           dT += static_cast<unsigned long long>(m) * (2ull * old - m);
         }
       }
+      rem = solo ? 0u : (rem & ~eq);
     }
   }
   dT = warp_sum_u64(dT);
@@ -364,6 +372,59 @@ __global__ void apply_ids_kernel(const uint32_t* __restrict__ ids, uint64_t n, u
       if (blk) atomicAdd(&st->T, 0ull - blk);
       if (blockIdx.x == 0) atomicAdd(&st->n, 0ull - n);
     }
+  }
+}
+
+// Insert from table-major ids with a shared-memory privatised histogram per
+// (table, row chunk): warp-aggregated shared atomics, then one global atomic
+// per touched bucket (K <= 15: 2^K u32 fit in shared memory).
+__global__ void apply_ids_smem_kernel(const uint32_t* __restrict__ ids, uint64_t n, uint32_t k_bits,
+                                      uint64_t chunk, uint32_t* counters, uint32_t cap, DevState* st) {
+  extern __shared__ uint32_t hist[];
+  __shared__ unsigned long long blk;
+  const uint32_t nb = 1u << k_bits;
+  const uint32_t t = blockIdx.x;
+  const uint64_t r0 = static_cast<uint64_t>(blockIdx.y) * chunk;
+  const uint64_t r1 = min(n, r0 + chunk);
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
+  if (threadIdx.x == 0) blk = 0ull;
+  __syncthreads();
+  const uint32_t* col = ids + static_cast<uint64_t>(t) * n;
+  const int lane = threadIdx.x & 31;
+  for (uint64_t base = r0; base < r1; base += blockDim.x) {
+    const uint64_t i = base + threadIdx.x;
+    const bool valid = i < r1;
+    const uint32_t b = valid ? col[i] : 0u;
+    // aggregate up to three runs of equal buckets per warp (clustered data),
+    // the remaining lanes add individually
+    unsigned rem = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+    for (int round = 0; round < 3 && rem; ++round) {
+      const int leader = __ffs(rem) - 1;
+      const uint32_t bl = __shfl_sync(0xffffffffu, b, leader);
+      const unsigned eq = __ballot_sync(0xffffffffu, b == bl) & rem;
+      if (lane == leader) atomicAdd(&hist[bl], static_cast<uint32_t>(__popc(eq)));
+      rem &= ~eq;
+    }
+    if ((rem >> lane) & 1u) atomicAdd(&hist[b], 1u);
+  }
+  __syncthreads();
+  unsigned long long dT = 0ull;
+  uint32_t* ct = counters + (static_cast<uint64_t>(t) << k_bits);
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
+    const uint32_t m = hist[b];
+    if (m) {
+      const uint32_t old = atomicAdd(&ct[b], m);
+      if (old > 0xffffffffu - m) st->saturated = 1;
+      dT += insert_numerator(old, m, cap);
+    }
+  }
+  dT = warp_sum_u64(dT);
+  if (lane == 0 && dT) atomicAdd(&blk, dT);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (blk) atomicAdd(&st->T, blk);
+    if (blockIdx.x == 0 && blockIdx.y == 0) atomicAdd(&st->n, n);
   }
 }
 
@@ -754,6 +815,22 @@ cudaError_t launch_apply_ids(const uint32_t* ids, uint64_t n, uint32_t tables, u
                              uint32_t* counters, uint32_t cap, int sign, DevState* st,
                              cudaStream_t s) {
   if (n == 0) return cudaSuccess;
+  if (sign > 0 && k_bits <= 15 && n >= 4096) {
+    static bool configured = false;
+    if (!configured) {
+      cudaError_t e = cudaFuncSetAttribute(apply_ids_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(sizeof(uint32_t) << 15));
+      if (e != cudaSuccess) return e;
+      configured = true;
+    }
+    uint64_t chunks = (296 + tables - 1) / tables;
+    if (chunks > (n + 4095) / 4096) chunks = (n + 4095) / 4096;
+    const uint64_t chunk = (n + chunks - 1) / chunks;
+    const dim3 grid(tables, static_cast<unsigned>((n + chunk - 1) / chunk));
+    apply_ids_smem_kernel<<<grid, 1024, sizeof(uint32_t) << k_bits, s>>>(ids, n, k_bits, chunk, counters, cap, st);
+    count_launch();
+    return cudaGetLastError();
+  }
   apply_ids_kernel<<<grid_for(n * tables, 256), 256, 0, s>>>(ids, n, tables, k_bits, counters, cap,
                                                              sign, st);
   count_launch();

@@ -5,13 +5,15 @@
 namespace ace_dev {
 
 // Fast-path operands of the tensor-core projection:
-//   W rows normalised to ||w|| = 2^14 (binary64), split into fp16 hi + lo,
-//   stored per (direction tile j, K-chunk kc) as two 128-row x 64-col blocks
+//   W rows normalised to ||w|| = 2^14 (binary64), split into fp16 hi + lo;
+//   directions packed densely (tile j = directions 128j..128j+127, tables may
+//   straddle tiles), stored per (tile j, K-chunk kc) as two 128-row x 64-col blocks
 //   in the canonical K-major SWIZZLE_128B shared-memory image (16 KB each),
 //   so one cp.async.bulk per block lands them ready for tcgen05.mma.
 struct TcFamily {
   uint16_t* w16 = nullptr;   // [ntiles][nkc][2][128*64] fp16 (swizzled)
   uint32_t nkc = 0;          // K-chunks of 64: dpad64 / 64
+  uint32_t ntiles = 0;       // 128-direction tiles (directions packed densely)
   int enabled = 0;
 };
 
@@ -21,12 +23,15 @@ struct TcArgs {
   uint64_t n, ld, dim;
   uint32_t k_bits, tables, tpt, ntiles, nkc;
   const uint16_t* w16;
+  uint16_t* x16;              // converted x tiles (pre-pass output), SW128 image
+  float* rowthr;              // per-row error threshold (pre-pass output)
   float margin_c;             // relative error bound
   uint32_t* ids;              // table-major, stride n
   unsigned long long* near_list;  // (row << 32) | direction
   unsigned long long near_cap;
   uint32_t* overflow_rows;    // bitmap over rows; rows rechecked in full
   DevState* st;
+  int dbg;  // experiments: 1 = skip epilogue work, 2 = skip MMAs
 };
 
 cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc);
