@@ -99,6 +99,16 @@ class Clocks:
                 "samples": len(sm)}
 
 
+def _profiled_traffic(kernel: str, cfg: int):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full
+    summary (profiles/traffic.json), or None."""
+    p = ROOT / "profiles" / "traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    return d.get(f"cfg{cfg}", {}).get(kernel)
+
+
 def dist_setup():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -216,9 +226,9 @@ def main():
     clocks = Clocks(local)
     clocks.start()
     launches0 = N.dev().ace_kernel_launches()
-    phase = np.zeros(4)
+    phase = np.zeros(5)
     import ctypes as C
-    ms3 = (C.c_double * 4)()
+    ms3 = (C.c_double * 5)()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record(stream)
@@ -268,21 +278,48 @@ def main():
                "note": "wall clock around ace_sketch_build_detect with pinned host rows"}
 
     pk, pk_src = peaks()
-    flops = 2.0 * w.dim * w.k_bits * w.num_tables * n
-    hash_ms = phase[0]
-    fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
-    roofline = {
-        "bound": "fp32",
-        "kernel": "hash_simt_kernel (SIMT FP32 projection + FP64 near-tie recheck + packing + fused insert)",
-        "achieved": flops / (hash_ms * 1e-3) / 1e12 if hash_ms > 0 else None,
-        "peak": fp32_peak,
-        "unit": "TFLOP/s",
-        "frac": (flops / (hash_ms * 1e-3) / 1e12) / fp32_peak if hash_ms > 0 else None,
-        "traffic": None,
-        "peak_source": "spec-derived FP32 FFMA: 148 SM x 128 lanes x 2 x 1.965 GHz "
-                       f"(bf16 tensor peak for reference: {pk.get('bf16_tflops')} TF/s {pk_src})",
-        "algorithmic_flops_per_launch": flops,
-        "kernel_share_of_step": hash_ms / ms if ms else None,
+    flops = 2.0 * w.dim * w.k_bits * w.num_tables * n  # one fp32 projection pass
+    kernel = N.dev().ace_family_kernel(fam.handle)
+    if kernel == 2:
+        kern_ms = phase[4]
+        peak = pk["bf16_tflops"]
+        traffic = _profiled_traffic("hash_tc_kernel", args.config)
+        roofline = {
+            "bound": "tensor",
+            "kernel": "hash_tc_kernel (tcgen05 fp16x3-split projection, TMEM accumulators, sign/near-tie/bucket epilogue)",
+            "achieved": flops / (kern_ms * 1e-3) / 1e12 if kern_ms > 0 else None,
+            "peak": peak,
+            "unit": "TFLOP/s",
+            "frac": (flops / (kern_ms * 1e-3) / 1e12) / peak if kern_ms > 0 else None,
+            "traffic": traffic,
+            "peak_source": f"bf16 dense {pk_src} (burst); algorithmic flops = 2*d*K*L per point, "
+                           "the 3 split passes count against achieved",
+            "algorithmic_flops_per_launch": flops,
+            "kernel_ms": kern_ms,
+            "kernel_share_of_step": kern_ms / ms if ms else None,
+        }
+    else:
+        kern_ms = phase[0]
+        fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
+        roofline = {
+            "bound": "fp32",
+            "kernel": "hash_simt_kernel (SIMT FP32 projection + FP64 near-tie recheck + packing + fused insert)",
+            "achieved": flops / (kern_ms * 1e-3) / 1e12 if kern_ms > 0 else None,
+            "peak": fp32_peak, "unit": "TFLOP/s",
+            "frac": (flops / (kern_ms * 1e-3) / 1e12) / fp32_peak if kern_ms > 0 else None,
+            "traffic": None, "peak_source": "spec FP32 FFMA (148 SM x 128 x 2 x 1.965 GHz)",
+            "algorithmic_flops_per_launch": flops, "kernel_ms": kern_ms,
+            "kernel_share_of_step": kern_ms / ms if ms else None,
+        }
+    x_bytes = n * w.dim * 4
+    conv_ms = phase[3]
+    kernels = {
+        "convert_x (hbm)": {"ms": conv_ms, "GB/s": x_bytes / (conv_ms * 1e-3) / 1e9 if conv_ms else None,
+                            "frac_hbm": (x_bytes / (conv_ms * 1e-3) / 1e9) / pk["hbm_gbs"] if conv_ms else None},
+        "hash_tc (tensor)": {"ms": phase[4]},
+        "recheck+insert": {"ms": phase[0] - phase[3] - phase[4]},
+        "score": {"ms": phase[1]},
+        "threshold+flags": {"ms": phase[2]},
     }
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -294,7 +331,8 @@ def main():
                    "parallelism": f"replicas x{ws}"},
         "roofline": roofline,
         "phases_ms": {"hash_insert": phase[0], "score": phase[1], "threshold_flags": phase[2],
-                      "projection_kernel": phase[3]},
+                      "convert_x": phase[3], "projection_kernel": phase[4]},
+        "kernels": kernels,
         "gpu_launches": int(launches),
         "clocks": clk,
         "e2e": e2e,

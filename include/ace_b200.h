@@ -176,9 +176,9 @@ uint64_t ace_kernel_launches(void);
 /* Phase timing with CUDA events on the sketch's stream (off by default):
  * after each call, ms[0] = hash (+ recheck + insert), ms[1] = score,
  * ms[2] = threshold + flags (batch) or stream flags + insert (stream),
- * ms[3] = the projection kernel alone (tcgen05 path). */
+ * ms[3] = x conversion pre-pass, ms[4] = tcgen05 projection kernel. */
 ace_status ace_sketch_set_timing(AceSketch* sk, int enable);
-ace_status ace_sketch_timings(const AceSketch* sk, double* ms4);
+ace_status ace_sketch_timings(const AceSketch* sk, double* ms5);
 
 #ifdef __cplusplus
 }

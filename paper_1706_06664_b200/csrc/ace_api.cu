@@ -92,8 +92,8 @@ struct AceSketch {
   DevBuf ids, sums, stage, flags, scores, demand, near, overflow, x16, rowthr;
   // phase timing (ace_sketch_set_timing)
   bool timing = false;
-  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-  bool ev_used[6] = {false, false, false, false, false, false};
+  cudaEvent_t ev[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  bool ev_used[7] = {false, false, false, false, false, false, false};
   void mark(int i) {
     if (timing) {
       cudaEventRecord(ev[i], stream);
@@ -197,6 +197,12 @@ ace_status copy_out(void* dst, const void* src, size_t bytes, int where, cudaStr
   return ACE_OK;
 }
 
+// 32-bit sketches cannot saturate while n stays below 2^32 - 1, so their
+// insert merge may skip the pre-add values and recompute T = sum c^2.
+bool fire_and_forget_ok(const AceSketch* sk, uint64_t n) {
+  return sk->width == 32 && !sk->hst->saturated && sk->hst->n + n < 0xffffffffull;
+}
+
 // hash n rows into sk->ids (table-major, stride n); optional fused insert.
 ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64_t ld, int insert) {
   const AceFamily* f = sk->fam;
@@ -243,12 +249,14 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
       t.dbg = dbg;
     }
     sk->mark(4);
+    ACE_CUDA(launch_convert_x(t, sk->stream));
+    sk->mark(6);
     ACE_CUDA(launch_hash_tc(t, sk->stream));
     sk->mark(5);
     ACE_CUDA(launch_recheck(t, f->d.w64, sk->stream));
     if (insert)
       ACE_CUDA(launch_apply_ids(sk->ids.as<uint32_t>(), n, f->d.tables, f->d.k_bits, sk->counters, sk->cap,
-                                +1, sk->st, sk->stream));
+                                +1, sk->st, sk->stream, !fire_and_forget_ok(sk, n)));
   } else {
     HashArgs a = make_hash_args(f, xd, dtype, n, ld, sk->ids.as<uint32_t>(), n, sk->st);
     a.insert = insert;
@@ -684,7 +692,7 @@ ace_status ace_sketch_stream_batch(AceSketch* sk, const void* x, int dtype, uint
                                alpha, dflags, dsc, sk->st, sk->stream));
   sk->mark(2);
   ACE_CUDA(launch_apply_ids(sk->ids.as<uint32_t>(), n, f->d.tables, f->d.k_bits, sk->counters,
-                            sk->cap, +1, sk->st, sk->stream));
+                            sk->cap, +1, sk->st, sk->stream, !fire_and_forget_ok(sk, n)));
   if (sk->width == 16) ACE_CUDA(launch_cap(sk->counters, sk->num_counters, sk->cap, sk->st, sk->stream));
   sk->mark(3);
   if (out_where == ACE_HOST) {
@@ -775,8 +783,8 @@ ace_status ace_sketch_set_timing(AceSketch* sk, int enable) {
 
 ace_status ace_sketch_timings(const AceSketch* sk, double* ms3) {
   if (!sk || !ms3) return fail(ACE_E_CONTRACT, "ace_sketch_timings: null argument");
-  const int pairs[4][2] = {{0, 1}, {1, 2}, {2, 3}, {4, 5}};
-  for (int i = 0; i < 4; ++i) {
+  const int pairs[5][2] = {{0, 1}, {1, 2}, {2, 3}, {4, 6}, {6, 5}};
+  for (int i = 0; i < 5; ++i) {
     ms3[i] = 0.0;
     const int a = pairs[i][0], b = pairs[i][1];
     if (sk->timing && sk->ev_used[a] && sk->ev_used[b]) {

@@ -177,13 +177,37 @@ __device__ __forceinline__ uint32_t sw128_off(uint32_t r, uint32_t k) {
 
 __device__ __forceinline__ double exact_proj(const double* __restrict__ w, const void* x, int x_f64,
                                              uint64_t row, uint64_t ld, uint64_t dim) {
+  // binary64 left fold, mul then add, from +0.0 (srp.cpp:78-91); operands
+  // are loaded 8 ahead so only the add chain is serial
   double acc = 0.0;
+  uint64_t i = 0;
   if (x_f64) {
     const double* xr = static_cast<const double*>(x) + row * ld;
-    for (uint64_t i = 0; i < dim; ++i) acc = __dadd_rn(acc, __dmul_rn(w[i], xr[i]));
+    for (; i + 8 <= dim; i += 8) {
+      double wv[8], xv[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        wv[k] = w[i + k];
+        xv[k] = xr[i + k];
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc = __dadd_rn(acc, __dmul_rn(wv[k], xv[k]));
+    }
+    for (; i < dim; ++i) acc = __dadd_rn(acc, __dmul_rn(w[i], xr[i]));
   } else {
     const float* xr = static_cast<const float*>(x) + row * ld;
-    for (uint64_t i = 0; i < dim; ++i) acc = __dadd_rn(acc, __dmul_rn(w[i], static_cast<double>(xr[i])));
+    for (; i + 8 <= dim; i += 8) {
+      double wv[8];
+      float xv[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        wv[k] = w[i + k];
+        xv[k] = xr[i + k];
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc = __dadd_rn(acc, __dmul_rn(wv[k], static_cast<double>(xv[k])));
+    }
+    for (; i < dim; ++i) acc = __dadd_rn(acc, __dmul_rn(w[i], static_cast<double>(xr[i])));
   }
   return acc;
 }
@@ -202,33 +226,46 @@ __device__ __forceinline__ float load_x(const TcArgs& a, uint64_t row, uint64_t 
   return static_cast<const float*>(a.x)[row * a.ld + k];
 }
 
-// One warp per row: max |x| (NaN > inf > finite as magnitude bits), power-of-
-// two scale to [2^14, 2^15), fp16 hi + lo split written straight into the
-// SW128 K-major shared-memory image of its 128-row tile, and the row's error
-// threshold thr = c * ||x~|| * 2^14 + abs (-1: exact zero row, +inf: recheck all).
-// Rows past n (tile padding) are written as zeros.
+// Eight lanes per row (four rows per warp, values held in registers): max |x|
+// (NaN > inf > finite as magnitude bits), power-of-two scale to [2^14, 2^15),
+// fp16 hi + lo split written straight into the SW128 K-major shared-memory
+// image of its 128-row tile, and the row's error threshold
+// thr = c * ||x~|| * 2^14 + abs (-1: exact zero row, +inf: recheck all).
+// Lane l8 of a row owns K elements 32g + 4*l8 .. +3 (coalesced 128 B per
+// group).  Rows past n (tile padding) are written as zeros.
 __global__ void __launch_bounds__(256) convert_x_kernel(const TcArgs a, uint64_t rows_padded) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
-  const uint32_t groups = (a.nkc * kChunk + 127) / 128;
+  const uint32_t lane = threadIdx.x & 31, l8 = lane & 7;
+  const uint64_t slots = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 3);
+  const uint32_t groups = a.nkc * 2;  // 32 K per group, <= 8
   const bool vec4 = !a.x_f64 && (a.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
-  for (uint64_t row = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows_padded;
-       row += warps) {
+  for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 3); base < rows_padded; base += slots) {
+    const uint64_t row = base + (threadIdx.x >> 3);
+    const bool inb = row < rows_padded;
     const bool live = row < a.n;
+    float v[8][4];
     uint32_t mb = 0u;
-    if (live) {
-      for (uint32_t g = 0; g < groups; ++g) {
-        const uint64_t k0 = g * 128u + lane * 4u;
+#pragma unroll
+    for (uint32_t g = 0; g < 8; ++g) {
+      const uint64_t k0 = g * 32u + l8 * 4u;
+      v[g][0] = v[g][1] = v[g][2] = v[g][3] = 0.0f;
+      if (g < groups && live) {
         if (vec4 && k0 + 3 < a.dim) {
-          const uint4 u = *reinterpret_cast<const uint4*>(static_cast<const float*>(a.x) + row * a.ld + k0);
-          mb = max(mb, max(max(u.x & 0x7fffffffu, u.y & 0x7fffffffu), max(u.z & 0x7fffffffu, u.w & 0x7fffffffu)));
+          const float4 u = *reinterpret_cast<const float4*>(static_cast<const float*>(a.x) + row * a.ld + k0);
+          v[g][0] = u.x;
+          v[g][1] = u.y;
+          v[g][2] = u.z;
+          v[g][3] = u.w;
         } else {
-          for (uint32_t e = 0; e < 4; ++e) mb = max(mb, __float_as_uint(load_x(a, row, k0 + e)) & 0x7fffffffu);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) v[g][e] = load_x(a, row, k0 + e);
         }
       }
-    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+      for (int e = 0; e < 4; ++e) mb = max(mb, __float_as_uint(v[g][e]) & 0x7fffffffu);
+    }
+    mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, 1));
+    mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, 2));
+    mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, 4));
     const bool nan = mb > 0x7f800000u;
     const float m = __uint_as_float(nan ? 0x7f800000u : mb);
     const bool zero = (m == 0.0f);
@@ -241,27 +278,15 @@ __global__ void __launch_bounds__(256) convert_x_kernel(const TcArgs a, uint64_t
     const uint64_t tile = row / kRows;
     const uint32_t r = static_cast<uint32_t>(row % kRows);
     float ss = 0.0f;
-    for (uint32_t g = 0; g < groups; ++g) {
-      const uint32_t k0 = g * 128u + lane * 4u;
-      const uint32_t kc = k0 / kChunk, kk = k0 % kChunk;
-      if (kc >= a.nkc) continue;
-      float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-      if (live && scale != 0.0f) {
-        if (vec4 && k0 + 3 < a.dim) {
-          const float4 u = *reinterpret_cast<const float4*>(static_cast<const float*>(a.x) + row * a.ld + k0);
-          v[0] = u.x;
-          v[1] = u.y;
-          v[2] = u.z;
-          v[3] = u.w;
-        } else {
 #pragma unroll
-          for (int e = 0; e < 4; ++e) v[e] = load_x(a, row, k0 + e);
-        }
-      }
+    for (uint32_t g = 0; g < 8; ++g) {
+      if (g >= groups || !inb) continue;
+      const uint32_t k0 = g * 32u + l8 * 4u;
+      const uint32_t kc = k0 / kChunk, kk = k0 % kChunk;
       uint32_t hi[2], lo[2];
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const float x0 = v[2 * i] * scale, x1 = v[2 * i + 1] * scale;
+        const float x0 = v[g][2 * i] * scale, x1 = v[g][2 * i + 1] * scale;
         ss = fmaf(x0, x0, fmaf(x1, x1, ss));
         const float h0 = __half2float(__float2half_rn(x0)), h1 = __half2float(__float2half_rn(x1));
         hi[i] = pack_h2(h0, h1);
@@ -272,9 +297,10 @@ __global__ void __launch_bounds__(256) convert_x_kernel(const TcArgs a, uint64_t
       *reinterpret_cast<uint2*>(blk + off) = make_uint2(hi[0], hi[1]);
       *reinterpret_cast<uint2*>(blk + kBlockBytes + off) = make_uint2(lo[0], lo[1]);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    if (lane == 0) {
+    ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+    ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+    ss += __shfl_xor_sync(0xffffffffu, ss, 4);
+    if (l8 == 0 && inb) {
       float thr;
       if (!live || zero) {
         thr = -1.0f;
@@ -567,8 +593,15 @@ __global__ void recheck_list_kernel(const TcArgs a, const double* __restrict__ w
     }
     ++rr;
   }
-  if (rr) atomicAdd(&blk_r, rr);
-  if (ff) atomicAdd(&blk_f, ff);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    rr += __shfl_xor_sync(0xffffffffu, rr, o);
+    ff += __shfl_xor_sync(0xffffffffu, ff, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (rr) atomicAdd(&blk_r, rr);
+    if (ff) atomicAdd(&blk_f, ff);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     if (blk_r) atomicAdd(&a.st->rechecked, blk_r);
@@ -674,15 +707,6 @@ cudaError_t launch_hash_tc(const TcArgs& a, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const uint64_t tiles = (a.n + kRows - 1) / kRows;
-  {
-    const uint64_t rows = tiles * kRows;
-    uint64_t blocks = (rows + 7) / 8;
-    if (blocks > static_cast<uint64_t>(sms) * 16) blocks = static_cast<uint64_t>(sms) * 16;
-    convert_x_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(a, rows);
-    count_launch();
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
   uint64_t grid = tiles < static_cast<uint64_t>(sms) ? tiles : static_cast<uint64_t>(sms);
   grid = (grid + kCluster - 1) / kCluster * kCluster;
   if (grid > static_cast<uint64_t>(sms)) grid = static_cast<uint64_t>(sms) / kCluster * kCluster;
@@ -701,6 +725,22 @@ cudaError_t launch_hash_tc(const TcArgs& a, cudaStream_t s) {
   cudaError_t e = cudaLaunchKernelEx(&cfg, hash_tc_kernel, a);
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_convert_x(const TcArgs& a, cudaStream_t s) {
+  if (a.n == 0) return cudaSuccess;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const uint64_t rows = (a.n + kRows - 1) / kRows * kRows;
+  uint64_t blocks = (rows + 31) / 32;  // 32 rows per 256-thread block
+  if (blocks > static_cast<uint64_t>(sms) * 8) blocks = static_cast<uint64_t>(sms) * 8;
+  convert_x_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(a, rows);
+  count_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t launch_recheck(const TcArgs& a, const double* w64, cudaStream_t s) {

@@ -42,6 +42,18 @@ __device__ __forceinline__ unsigned long long insert_numerator(unsigned long lon
   return u * (2ull * old + u) + (m - u) * (2ull * cap + 1ull);
 }
 
+// Warp sum of a u128 held as (lo, hi).
+__device__ __forceinline__ void warp_sum_u128(unsigned long long& lo, unsigned long long& hi) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long olo = __shfl_xor_sync(0xffffffffu, lo, o);
+    const unsigned long long ohi = __shfl_xor_sync(0xffffffffu, hi, o);
+    const unsigned long long nlo = lo + olo;
+    hi += ohi + (nlo < lo ? 1ull : 0ull);
+    lo = nlo;
+  }
+}
+
 __device__ __forceinline__ void atomic_add_u128(unsigned long long* lo, unsigned long long* hi,
                                                 unsigned long long vlo, unsigned long long vhi) {
   const unsigned long long old = atomicAdd(lo, vlo);
@@ -54,14 +66,37 @@ __device__ __forceinline__ double exact_projection(const double* __restrict__ w,
                                                    const void* x, int x_f64,
                                                    uint64_t row, uint64_t ld,
                                                    uint64_t dim) {
+  // binary64 left fold, mul then add, from +0.0 (srp.cpp:78-91); operands
+  // are loaded 8 ahead so only the add chain is serial
   double acc = 0.0;
+  uint64_t i = 0;
   if (x_f64) {
     const double* xr = static_cast<const double*>(x) + row * ld;
-    for (uint64_t i = 0; i < dim; ++i) acc = __dadd_rn(acc, __dmul_rn(w[i], xr[i]));
+    for (; i + 8 <= dim; i += 8) {
+      double wv[8], xv[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        wv[k] = w[i + k];
+        xv[k] = xr[i + k];
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc = __dadd_rn(acc, __dmul_rn(wv[k], xv[k]));
+    }
+    for (; i < dim; ++i) acc = __dadd_rn(acc, __dmul_rn(w[i], xr[i]));
   } else {
     const float* xr = static_cast<const float*>(x) + row * ld;
-    for (uint64_t i = 0; i < dim; ++i)
-      acc = __dadd_rn(acc, __dmul_rn(w[i], static_cast<double>(xr[i])));
+    for (; i + 8 <= dim; i += 8) {
+      double wv[8];
+      float xv[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        wv[k] = w[i + k];
+        xv[k] = xr[i + k];
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc = __dadd_rn(acc, __dmul_rn(wv[k], static_cast<double>(xv[k])));
+    }
+    for (; i < dim; ++i) acc = __dadd_rn(acc, __dmul_rn(w[i], static_cast<double>(xr[i])));
   }
   return acc;
 }
@@ -375,56 +410,98 @@ __global__ void apply_ids_kernel(const uint32_t* __restrict__ ids, uint64_t n, u
   }
 }
 
-// Insert from table-major ids with a shared-memory privatised histogram per
-// (table, row chunk): warp-aggregated shared atomics, then one global atomic
-// per touched bucket (K <= 15: 2^K u32 fit in shared memory).
-__global__ void apply_ids_smem_kernel(const uint32_t* __restrict__ ids, uint64_t n, uint32_t k_bits,
-                                      uint64_t chunk, uint32_t* counters, uint32_t cap, DevState* st) {
-  extern __shared__ uint32_t hist[];
-  __shared__ unsigned long long blk;
-  const uint32_t nb = 1u << k_bits;
-  const uint32_t t = blockIdx.x;
-  const uint64_t r0 = static_cast<uint64_t>(blockIdx.y) * chunk;
-  const uint64_t r1 = min(n, r0 + chunk);
-  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
-  if (threadIdx.x == 0) blk = 0ull;
+__global__ void sum_squares_kernel(const uint32_t* __restrict__ c, uint64_t num,
+                                   unsigned long long* out) {
+  unsigned long long s = 0;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < num;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    s += static_cast<unsigned long long>(c[i]) * c[i];
+  s = warp_sum_u64(s);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
+// Insert from table-major ids with a shared-memory privatised histogram:
+// block b owns the contiguous item range [b*per, (b+1)*per) of the flattened
+// table-major id array (spanning at most a few tables), counts into a 2^K u32
+// shared histogram with warp-aggregated shared atomics, and merges it into the
+// global counters (one atomic per touched bucket) whenever the table changes.
+// kTrackT: accumulate the insert numerators from the pre-add counter values
+// (needed for 16-bit sketches, whose counters saturate); 32-bit sketches
+// recompute T = sum c^2 afterwards, so their merge is fire-and-forget.
+template <bool kTrackT>
+__device__ void flush_hist(uint32_t* hist, uint32_t nb, uint32_t* ct, uint32_t cap, DevState* st,
+                           unsigned long long& dT) {
   __syncthreads();
-  const uint32_t* col = ids + static_cast<uint64_t>(t) * n;
-  const int lane = threadIdx.x & 31;
-  for (uint64_t base = r0; base < r1; base += blockDim.x) {
-    const uint64_t i = base + threadIdx.x;
-    const bool valid = i < r1;
-    const uint32_t b = valid ? col[i] : 0u;
-    // aggregate up to three runs of equal buckets per warp (clustered data),
-    // the remaining lanes add individually
-    unsigned rem = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-    for (int round = 0; round < 3 && rem; ++round) {
-      const int leader = __ffs(rem) - 1;
-      const uint32_t bl = __shfl_sync(0xffffffffu, b, leader);
-      const unsigned eq = __ballot_sync(0xffffffffu, b == bl) & rem;
-      if (lane == leader) atomicAdd(&hist[bl], static_cast<uint32_t>(__popc(eq)));
-      rem &= ~eq;
-    }
-    if ((rem >> lane) & 1u) atomicAdd(&hist[b], 1u);
-  }
-  __syncthreads();
-  unsigned long long dT = 0ull;
-  uint32_t* ct = counters + (static_cast<uint64_t>(t) << k_bits);
+#pragma unroll 4
   for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
     const uint32_t m = hist[b];
     if (m) {
-      const uint32_t old = atomicAdd(&ct[b], m);
-      if (old > 0xffffffffu - m) st->saturated = 1;
-      dT += insert_numerator(old, m, cap);
+      hist[b] = 0u;
+      if (kTrackT) {
+        const uint32_t old = atomicAdd(&ct[b], m);
+        if (old > 0xffffffffu - m) st->saturated = 1;
+        dT += insert_numerator(old, m, cap);
+      } else {
+        atomicAdd(&ct[b], m);  // result unused: RED
+      }
     }
+  }
+  __syncthreads();
+}
+
+template <bool kTrackT>
+__global__ void __launch_bounds__(1024) apply_ids_smem_kernel(const uint32_t* __restrict__ ids, uint64_t n,
+                                                              uint32_t tables, uint32_t k_bits, uint64_t per,
+                                                              uint32_t* counters, uint32_t cap, DevState* st) {
+  extern __shared__ uint32_t hist[];
+  __shared__ unsigned long long blk;
+  const uint32_t nb = 1u << k_bits;
+  const uint64_t total = n * tables;
+  const uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * per;
+  const uint64_t i1 = min(total, i0 + per);
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
+  if (threadIdx.x == 0) blk = 0ull;
+  const int lane = threadIdx.x & 31;
+  unsigned long long dT = 0ull;
+  constexpr int kDepth = 8;  // ids in flight per thread
+  for (uint64_t seg = i0; seg < i1;) {
+    const uint64_t t = seg / n;                      // table of this segment
+    const uint64_t seg_end = min(i1, (t + 1) * n);   // stay within the table
+    __syncthreads();
+    for (uint64_t base = seg; base < seg_end; base += static_cast<uint64_t>(blockDim.x) * kDepth) {
+      uint32_t bv[kDepth];
+#pragma unroll
+      for (int u = 0; u < kDepth; ++u) {
+        const uint64_t i = base + static_cast<uint64_t>(u) * blockDim.x + threadIdx.x;
+        bv[u] = i < seg_end ? __ldcs(ids + i) : 0xffffffffu;  // streamed once: evict-first
+      }
+#pragma unroll
+      for (int u = 0; u < kDepth; ++u) {
+        const uint32_t b = bv[u];
+        const bool valid = b != 0xffffffffu;
+        // aggregate up to three runs of equal buckets per warp (clustered data),
+        // the remaining lanes add individually
+        unsigned rem = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+        for (int round = 0; round < 3 && rem; ++round) {
+          const int leader = __ffs(rem) - 1;
+          const uint32_t bl = __shfl_sync(0xffffffffu, b, leader);
+          const unsigned eq = __ballot_sync(0xffffffffu, b == bl) & rem;
+          if (lane == leader) atomicAdd(&hist[bl], static_cast<uint32_t>(__popc(eq)));
+          rem &= ~eq;
+        }
+        if ((rem >> lane) & 1u) atomicAdd(&hist[b], 1u);
+      }
+    }
+    flush_hist<kTrackT>(hist, nb, counters + (t << k_bits), cap, st, dT);
+    seg = seg_end;
   }
   dT = warp_sum_u64(dT);
   if (lane == 0 && dT) atomicAdd(&blk, dT);
   __syncthreads();
   if (threadIdx.x == 0) {
     if (blk) atomicAdd(&st->T, blk);
-    if (blockIdx.x == 0 && blockIdx.y == 0) atomicAdd(&st->n, n);
+    if (blockIdx.x == 0) atomicAdd(&st->n, n);
   }
 }
 
@@ -468,23 +545,19 @@ __global__ void score_kernel(const uint32_t* __restrict__ ids, uint64_t ids_stri
                              uint32_t tables, uint32_t k_bits, const uint32_t* __restrict__ counters,
                              uint64_t* __restrict__ sums, double* __restrict__ scores,
                              DevState* st) {
-  __shared__ unsigned long long s_lo, s_hi, q_lo, q_hi;
-  if (threadIdx.x == 0) s_lo = s_hi = q_lo = q_hi = 0ull;
-  __syncthreads();
   unsigned long long acc = 0ull, sq_lo = 0ull, sq_hi = 0ull;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     unsigned long long S = 0ull;
     uint32_t t = 0;
-    for (; t + 4 <= tables; t += 4) {
-      const uint32_t b0 = ids[(uint64_t)t * ids_stride + i];
-      const uint32_t b1 = ids[(uint64_t)(t + 1) * ids_stride + i];
-      const uint32_t b2 = ids[(uint64_t)(t + 2) * ids_stride + i];
-      const uint32_t b3 = ids[(uint64_t)(t + 3) * ids_stride + i];
-      S += counters[((uint64_t)t << k_bits) + b0];
-      S += counters[((uint64_t)(t + 1) << k_bits) + b1];
-      S += counters[((uint64_t)(t + 2) << k_bits) + b2];
-      S += counters[((uint64_t)(t + 3) << k_bits) + b3];
+    for (; t + 8 <= tables; t += 8) {
+      uint32_t b[8], c[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) b[u] = ids[(uint64_t)(t + u) * ids_stride + i];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) c[u] = counters[((uint64_t)(t + u) << k_bits) + b[u]];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) S += c[u];
     }
     for (; t < tables; ++t) S += counters[((uint64_t)t << k_bits) + ids[(uint64_t)t * ids_stride + i]];
     if (sums) sums[i] = S;
@@ -495,13 +568,27 @@ __global__ void score_kernel(const uint32_t* __restrict__ ids, uint64_t ids_stri
     sq_hi += hi + (nlo < sq_lo ? 1ull : 0ull);
     sq_lo = nlo;
   }
-  // block reduction via shared atomics (u128 with carry)
-  atomicAdd(&s_lo, acc);  // sum S fits u64 per block
-  atomic_add_u128(&q_lo, &q_hi, sq_lo, sq_hi);
+  // warp reductions, then thread 0 folds the warps and issues the global atomics
+  __shared__ unsigned long long w_s[32], w_qlo[32], w_qhi[32];
+  acc = warp_sum_u64(acc);
+  warp_sum_u128(sq_lo, sq_hi);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    w_s[wid] = acc;
+    w_qlo[wid] = sq_lo;
+    w_qhi[wid] = sq_hi;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    atomic_add_u128(&st->sum_lo, &st->sum_hi, s_lo, s_hi);
-    atomic_add_u128(&st->sq_lo, &st->sq_hi, q_lo, q_hi);
+    unsigned long long ts = 0, tlo = 0, thi = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      ts += w_s[w];
+      const unsigned long long nlo = tlo + w_qlo[w];
+      thi += w_qhi[w] + (nlo < tlo ? 1ull : 0ull);
+      tlo = nlo;
+    }
+    atomic_add_u128(&st->sum_lo, &st->sum_hi, ts, 0ull);
+    atomic_add_u128(&st->sq_lo, &st->sq_hi, tlo, thi);
   }
 }
 
@@ -775,15 +862,6 @@ __global__ void stream_score_kernel(const uint32_t* __restrict__ ids, uint64_t n
   }
 }
 
-__global__ void sum_squares_kernel(const uint32_t* __restrict__ c, uint64_t num,
-                                   unsigned long long* out) {
-  unsigned long long s = 0;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < num;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    s += static_cast<unsigned long long>(c[i]) * c[i];
-  s = warp_sum_u64(s);
-  if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
-}
 
 int grid_for(uint64_t work, int threads, int max_blocks = 148 * 16) {
   uint64_t b = (work + threads - 1) / threads;
@@ -813,21 +891,41 @@ cudaError_t launch_hash_simt(const HashArgs& a, cudaStream_t s) {
 
 cudaError_t launch_apply_ids(const uint32_t* ids, uint64_t n, uint32_t tables, uint32_t k_bits,
                              uint32_t* counters, uint32_t cap, int sign, DevState* st,
-                             cudaStream_t s) {
+                             cudaStream_t s, bool track_t) {
   if (n == 0) return cudaSuccess;
   if (sign > 0 && k_bits <= 15 && n >= 4096) {
     static bool configured = false;
     if (!configured) {
-      cudaError_t e = cudaFuncSetAttribute(apply_ids_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaError_t e = cudaFuncSetAttribute(apply_ids_smem_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(sizeof(uint32_t) << 15));
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(apply_ids_smem_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(sizeof(uint32_t) << 15));
       if (e != cudaSuccess) return e;
       configured = true;
     }
-    uint64_t chunks = (296 + tables - 1) / tables;
-    if (chunks > (n + 4095) / 4096) chunks = (n + 4095) / 4096;
-    const uint64_t chunk = (n + chunks - 1) / chunks;
-    const dim3 grid(tables, static_cast<unsigned>((n + chunk - 1) / chunk));
-    apply_ids_smem_kernel<<<grid, 1024, sizeof(uint32_t) << k_bits, s>>>(ids, n, k_bits, chunk, counters, cap, st);
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const uint64_t total = n * tables;
+    uint64_t blocks = static_cast<uint64_t>(sms);
+    if (blocks > total / 4096) blocks = total / 4096 > 0 ? total / 4096 : 1;
+    const uint64_t per = (total + blocks - 1) / blocks;
+    const unsigned grid = static_cast<unsigned>((total + per - 1) / per);
+    const size_t smem = sizeof(uint32_t) << k_bits;
+    if (track_t) {
+      apply_ids_smem_kernel<true><<<grid, 1024, smem, s>>>(ids, n, tables, k_bits, per, counters, cap, st);
+    } else {
+      apply_ids_smem_kernel<false><<<grid, 1024, smem, s>>>(ids, n, tables, k_bits, per, counters, cap, st);
+      // T = sum of squared counters (exact for unsaturated 32-bit sketches)
+      cudaMemsetAsync(&st->T, 0, sizeof(st->T), s);
+      sum_squares_kernel<<<grid_for((static_cast<uint64_t>(tables) << k_bits), 256), 256, 0, s>>>(
+          counters, static_cast<uint64_t>(tables) << k_bits, &st->T);
+      count_launch();
+    }
     count_launch();
     return cudaGetLastError();
   }

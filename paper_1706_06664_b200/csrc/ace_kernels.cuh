@@ -26,9 +26,11 @@ size_t hash_simt_smem_bytes();
 
 // Counter updates from ids (streaming insert / remove), warp-aggregated.
 //   sign = +1 insert, -1 remove (remove assumes validation passed).
+//   track_t = false (32-bit, no saturation possible): T is recomputed as
+//   sum c^2 instead of accumulated from returned pre-add values.
 cudaError_t launch_apply_ids(const uint32_t* ids, uint64_t n, uint32_t tables,
                              uint32_t k_bits, uint32_t* counters, uint32_t cap,
-                             int sign, DevState* st, cudaStream_t s);
+                             int sign, DevState* st, cudaStream_t s, bool track_t = true);
 // Remove validation: counts, per counter, how many removals target it and
 // flags underflow (any count < demand).  scratch: L x 2^K u32, zeroed here.
 cudaError_t launch_remove_check(const uint32_t* ids, uint64_t n, uint32_t tables,

@@ -36,6 +36,8 @@ struct TcArgs {
 
 cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc);
 void tc_free_family(TcFamily* tc);
+// X -> fp16 hi/lo SW128 tile image + per-row thresholds (must precede the hash)
+cudaError_t launch_convert_x(const TcArgs& a, cudaStream_t s);
 cudaError_t launch_hash_tc(const TcArgs& a, cudaStream_t s);
 // Exact FP64 recheck of the near-tie list (patches ids) + rows that
 // overflowed the list (all projections recomputed).
