@@ -27,6 +27,7 @@ void set_error(const std::string& msg) { g_err = msg; }
 using namespace ace_dev;
 
 namespace {
+unsigned long long* g_tc_prof = nullptr;
 
 constexpr uint32_t kMaxKBits = 30;  // srp.cpp:15
 
@@ -247,6 +248,13 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
         dbg = e ? atoi(e) : 0;
       }
       t.dbg = dbg;
+      static unsigned long long* prof = nullptr;
+      if (getenv("ACE_TC_PROF")) {
+        if (!prof) cudaMalloc(&prof, 8 * sizeof(unsigned long long));
+        cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), sk->stream);
+      }
+      t.prof = prof;
+      g_tc_prof = prof;
     }
     sk->mark(4);
     ACE_CUDA(launch_convert_x(t, sk->stream));
@@ -335,6 +343,15 @@ int ace_device_available(void) {
 }
 
 uint64_t ace_kernel_launches(void) { return g_launches.load(); }
+
+// Instrumentation readout (ACE_TC_PROF set): wait cycles per barrier kind of
+// the last tcgen05 projection launch, summed over CTAs.  Not part of the ABI
+// contract in include/ace_b200.h.
+int ace_debug_tc_prof(unsigned long long* out8) {
+  if (!g_tc_prof) return -1;
+  cudaDeviceSynchronize();
+  return cudaMemcpy(out8, g_tc_prof, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : -2;
+}
 
 // SrpFamily::SrpFamily (srp.cpp:24-49): validation + W upload.
 ace_status ace_family_create(uint64_t dim, uint32_t k_bits, uint32_t num_tables, double noise_scale,

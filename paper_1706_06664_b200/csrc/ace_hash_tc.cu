@@ -32,9 +32,9 @@ namespace {
 constexpr int kRows = 128;                 // points per tile (MMA M)
 constexpr int kChunk = 64;                 // K elements per chunk (128 B of fp16)
 constexpr int kBlockBytes = kRows * 128;   // one 128 x 64 fp16 block = 16 KB
-constexpr int kAccBufs = 4;                // TMEM accumulators (4 x 128 columns)
+constexpr int kAccBufs = 3;                // max TMEM accumulators (x 128 columns)
 constexpr int kMaxWStages = 6;
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;
 constexpr size_t kSmemLimit = 232448;      // 227 KB per CTA
 constexpr uint32_t kCluster = 1;           // CTAs sharing each W stage (TMA multicast)
 
@@ -43,15 +43,18 @@ struct TcLayout {
   size_t a_bytes, w_bytes, total;
 };
 
-// Shared memory: the A tile (x, fp16 hi | lo, SW128 image from the pre-pass),
-// double buffered when dpad <= 128, then a ring of W stages (32 KB each).
-// TMEM: 4 accumulators x 128 columns.
+// Shared memory: one A tile (x, fp16 hi | lo, SW128 image from the pre-pass;
+// released as soon as tcgen05.cp has moved it into TMEM), then a ring of W
+// stages (32 KB each).  TMEM: accumulators of 128 columns, then the A operand
+// (hi | lo, 2 fp16 per column, dpad columns).
+__host__ __device__ inline uint32_t tc_acc_bufs(uint32_t nkc) { return nkc <= 2 ? 3u : 2u; }
+
 __host__ __device__ inline TcLayout tc_layout(uint32_t nkc) {
   TcLayout L;
   L.nkc = nkc;
-  L.n_abuf = nkc <= 2 ? 2 : 1;
+  L.n_abuf = 1;
   L.a_bytes = static_cast<size_t>(L.n_abuf) * nkc * 2 * kBlockBytes;
-  const size_t room = kSmemLimit - 1024 - 1024 - L.a_bytes;
+  const size_t room = kSmemLimit - 8192 - 1024 - L.a_bytes;  // static smem (barriers, sign words) + align
   size_t st = room / (2 * kBlockBytes);
   if (st > kMaxWStages) st = kMaxWStages;
   L.n_wst = static_cast<uint32_t>(st);
@@ -86,6 +89,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// mbar_wait that adds the cycles spent waiting to *acc (instrumentation)
+__device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, unsigned long long* acc) {
+  if (acc) {
+    const long long t0 = clock64();
+    mbar_wait(bar, parity);
+    *acc += static_cast<unsigned long long>(clock64() - t0);
+  } else {
+    mbar_wait(bar, parity);
+  }
+}
+
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -108,6 +122,18 @@ __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
       "h"(mask)
       : "memory");
 }
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "elect.sync _|P, 0xffffffff;\n"
+      "selp.u32 %0, 1, 0, P;\n"
+      "}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -150,6 +176,19 @@ __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b,
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc));
+}
+__device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -339,6 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
   __shared__ __align__(8) uint64_t bar_afull[2], bar_aempty[2];
   __shared__ __align__(8) uint64_t bar_accfull[kAccBufs], bar_accempty[kAccBufs];
   __shared__ uint32_t tmem_base_sh;
+  __shared__ uint32_t sgbuf[kAccBufs][4][kRows];  // epilogue sign words per accumulator
 
   const TcLayout L = tc_layout(a.nkc);
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -362,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
     }
     for (int b = 0; b < kAccBufs; ++b) {
       mbar_init(&bar_accfull[b], 1);
-      mbar_init(&bar_accempty[b], 4);
+      mbar_init(&bar_accempty[b], 8);  // eight epilogue warps
     }
     fence_mbar_init();
   }
@@ -382,24 +422,36 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
   // skipped by the epilogue) so a cluster's shared W pipeline stays in lockstep
   const uint64_t iters = (n_tiles + gridDim.x - 1) / gridDim.x;
   const uint64_t t_end = static_cast<uint64_t>(blockIdx.x) + iters * gridDim.x;
+  // instrumentation (a.prof != null): cycles waiting per barrier kind, per CTA:
+  // [0] prod a_empty [1] prod w_empty [2] mma a_full [3] mma acc_empty
+  // [4] mma w_full [5] epilogue acc_full (warp 2..5 lane 0 summed) [6] total
+  const bool prof = a.prof != nullptr;
+  unsigned long long pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const long long t_start = clock64();
 
   if (warp == 0) {
     // ---------------- producer: A tile (once per tile) + W stages ----------------
     if (lane == 0) {
       uint32_t s = 0, ph = 0, it = 0;
       for (uint64_t t = blockIdx.x; t < t_end; t += gridDim.x, ++it) {
-        const uint32_t buf = it % L.n_abuf, use = it / L.n_abuf;
-        mbar_wait(&bar_aempty[buf], (use & 1u) ^ 1u);
+        mbar_wait_t(&bar_aempty[0], (it & 1u) ^ 1u, prof ? &pw[0] : nullptr);
         const uint64_t tt = t < n_tiles ? t : n_tiles - 1;  // past the end: reload the last tile
-        mbar_expect_tx(&bar_afull[buf], a_tile_bytes);
-        bulk_g2s(Asm + static_cast<size_t>(buf) * a_tile_bytes,
-                 reinterpret_cast<const uint8_t*>(a.x16) + tt * a_tile_bytes, a_tile_bytes, &bar_afull[buf]);
+        mbar_expect_tx(&bar_afull[0], a_tile_bytes);
+        bulk_g2s(Asm, reinterpret_cast<const uint8_t*>(a.x16) + tt * a_tile_bytes, a_tile_bytes, &bar_afull[0]);
         for (uint32_t j = 0; j < a.ntiles; ++j) {
           const uint32_t nmma = (min(128u, R - j * 128u) + 15u) & ~15u;
           const uint32_t bytes = nmma * 128u;
           const uint32_t part = bytes / kCluster;  // this CTA's slice, multicast to the cluster
           for (uint32_t kc = 0; kc < a.nkc; ++kc) {
-            mbar_wait(&bar_wempty[s], ph ^ 1u);
+            mbar_wait_t(&bar_wempty[s], ph ^ 1u, prof ? &pw[1] : nullptr);
+            if ((a.dbg & 8) && (it & 1u)) {  // experiment: skip W traffic on odd tiles
+              mbar_arrive(&bar_wfull[s]);
+              if (++s == L.n_wst) {
+                s = 0;
+                ph ^= 1u;
+              }
+              continue;
+            }
             mbar_expect_tx(&bar_wfull[s], 2u * bytes);
             const uint8_t* src =
                 reinterpret_cast<const uint8_t*>(a.w16) + (static_cast<uint64_t>(j) * a.nkc + kc) * 2u * kBlockBytes;
@@ -421,64 +473,86 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (A and B from shared memory) ----------------
-    if (lane == 0) {
+    // ---------------- MMA issuer: A smem -> TMEM (tcgen05.cp), then TS MMAs ----------------
+    // The whole warp walks the schedule (operands stay warp-uniform, so the
+    // descriptors live in uniform registers); one elected lane issues.
+    {
       uint32_t s = 0, wph = 0, acc = 0, accph = 0, it = 0;
+      const uint32_t nacc = tc_acc_bufs(a.nkc);
+      const uint32_t ta_hi = tmem_base + nacc * 128u, ta_lo = ta_hi + a.nkc * 32u;  // dpad/2 columns each
+      const uint32_t a_base = smem_u32(Asm), w_base = smem_u32(Wsm);
       for (uint64_t t = blockIdx.x; t < t_end; t += gridDim.x, ++it) {
-        const uint32_t buf = it % L.n_abuf, use = it / L.n_abuf;
-        mbar_wait(&bar_afull[buf], use & 1u);
+        mbar_wait_t(&bar_afull[0], it & 1u, (prof && lane == 0) ? &pw[2] : nullptr);
         tc_after();
-        const uint8_t* Ab = Asm + static_cast<size_t>(buf) * a_tile_bytes;
+        // copies execute in issue order after this CTA's earlier MMAs, so the
+        // previous tile's reads of TMEM A are complete before it is replaced
+        if (elect_one()) {
+          for (uint32_t kc = 0; kc < a.nkc; ++kc) {
+            const uint32_t ah = a_base + kc * 2u * kBlockBytes;
+#pragma unroll
+            for (uint32_t kk = 0; kk < 4; ++kk) {
+              tmem_cp_128x256b(ta_hi + (kc * 4u + kk) * 8u, sw128_desc(ah + kk * 32u));
+              tmem_cp_128x256b(ta_lo + (kc * 4u + kk) * 8u, sw128_desc(ah + kBlockBytes + kk * 32u));
+            }
+          }
+          mma_commit(&bar_aempty[0]);  // shared-memory A free once the copies land
+        }
+        __syncwarp();
         for (uint32_t j = 0; j < a.ntiles; ++j) {
           const uint32_t nmma = (min(128u, R - j * 128u) + 15u) & ~15u;
           const uint32_t idesc = idesc_f16(nmma);
-          mbar_wait(&bar_accempty[acc], accph ^ 1u);
+          mbar_wait_t(&bar_accempty[acc], accph ^ 1u, (prof && lane == 0) ? &pw[3] : nullptr);
           tc_after();
           const uint32_t dt = tmem_base + acc * 128u;
           for (uint32_t kc = 0; kc < a.nkc; ++kc) {
-            mbar_wait(&bar_wfull[s], wph);
+            mbar_wait_t(&bar_wfull[s], wph, (prof && lane == 0) ? &pw[4] : nullptr);
             tc_after();
-            const uint32_t a_hi = smem_u32(Ab + (static_cast<size_t>(kc) * 2 + 0) * kBlockBytes);
-            const uint32_t a_lo = a_hi + kBlockBytes;
-            const uint32_t b_hi = smem_u32(Wsm + static_cast<size_t>(s) * 2 * kBlockBytes);
-            const uint32_t b_lo = b_hi + kBlockBytes;
-            if (!(a.dbg & 2)) {
+            const uint32_t b_hi = w_base + s * 2u * kBlockBytes;
+            const uint64_t dbh = sw128_desc(b_hi), dbl = sw128_desc(b_hi + kBlockBytes);
+            if (elect_one()) {
+              if (!(a.dbg & 2)) {
 #pragma unroll
-              for (uint32_t kk = 0; kk < 4; ++kk) {
-                const uint32_t off = kk * 32u;  // 16 fp16 along K
-                mma_f16(dt, sw128_desc(a_hi + off), sw128_desc(b_hi + off), idesc, (kc | kk) != 0u);
-                mma_f16(dt, sw128_desc(a_lo + off), sw128_desc(b_hi + off), idesc, 1u);
-                mma_f16(dt, sw128_desc(a_hi + off), sw128_desc(b_lo + off), idesc, 1u);
+                for (uint32_t kk = 0; kk < 4; ++kk) {
+                  const uint32_t acol = (kc * 4u + kk) * 8u;  // 16 fp16 = 8 TMEM columns
+                  const uint64_t off = kk * 2u;                // 32 B along K in SW128, >> 4
+                  mma_f16_ts(dt, ta_hi + acol, dbh + off, idesc, (kc | kk) != 0u);
+                  mma_f16_ts(dt, ta_lo + acol, dbh + off, idesc, 1u);
+                  mma_f16_ts(dt, ta_hi + acol, dbl + off, idesc, 1u);
+                }
               }
+              if (kCluster == 1)
+                mma_commit(&bar_wempty[s]);
+              else
+                mma_commit_mc(&bar_wempty[s], cmask);
             }
-            if (kCluster == 1)
-              mma_commit(&bar_wempty[s]);
-            else
-              mma_commit_mc(&bar_wempty[s], cmask);
+            __syncwarp();
             if (++s == L.n_wst) {
               s = 0;
               wph ^= 1u;
             }
           }
-          mma_commit(&bar_accfull[acc]);
-          if (++acc == kAccBufs) {
+          if (elect_one()) mma_commit(&bar_accfull[acc]);
+          __syncwarp();
+          if (++acc == nacc) {
             acc = 0;
             accph ^= 1u;
           }
         }
-        mma_commit(&bar_aempty[buf]);
       }
     }
-    __syncwarp();
   } else {
-    // ---------------- epilogue (warps 2-5; TMEM lane quarter = warp % 4) ----------------
-    // Per 32-column chunk: sign bits packed MSB-first (one funnel shift per
+    // ---------------- epilogue (warps 2-9) ----------------
+    // Two warps per TMEM lane quarter (q = warp % 4): half h = 0 takes
+    // columns 0-63 of each direction tile, h = 1 columns 64-127.  Per
+    // 32-column chunk: sign bits packed MSB-first (one funnel shift per
     // column), near ties by one unsigned min over |v| (bits << 1), four
-    // independent chains for ILP; buckets cut out of the column stream with
-    // funnel shifts, tables straddling direction tiles carried in prev3.
-    const uint32_t q = warp & 3;
+    // independent chains for ILP.  The pair swaps sign words through shared
+    // memory (named barrier 1 + q) and each cuts out alternate tables' buckets;
+    // tables straddling direction tiles use the carried last word prev3.
+    const uint32_t q = warp & 3, h = (warp - 2) >> 2;
     const uint32_t r = q * 32u + lane;
     const uint32_t kmask = (K >= 32u) ? 0xffffffffu : ((1u << K) - 1u);
+    const uint32_t nacc = tc_acc_bufs(a.nkc);
     uint32_t acc = 0, accph = 0;
     for (uint64_t t = blockIdx.x; t < t_end; t += gridDim.x) {
       const uint64_t row = t * kRows + r;
@@ -491,12 +565,13 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
       for (uint32_t j = 0; j < a.ntiles; ++j) {
         const uint32_t used = min(128u, R - j * 128u);
         const uint32_t col0 = j * 128u;
-        mbar_wait(&bar_accfull[acc], accph);
+        mbar_wait_t(&bar_accfull[acc], accph, (prof && lane == 0) ? &pw[5] : nullptr);
         tc_after();
-        uint32_t sg0 = 0u, sg1 = 0u, sg2 = 0u, sg3 = 0u;
         if (!(a.dbg & 1)) {
 #pragma unroll 1
-          for (uint32_t cc = 0; cc < used; cc += 32u) {
+          for (uint32_t c = 2 * h; c < 2 * h + 2; ++c) {
+            const uint32_t cc = c * 32u;
+            if (cc >= used) break;
             uint32_t v[32];
             ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + acc * 128u + cc, v);
             tmem_wait_ld();
@@ -528,24 +603,20 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
                 nm |= ((static_cast<uint32_t>(jj) < ncol && (v[jj] << 1) <= thr_u) ? 1u : 0u) << jj;
               push_near_mask(a.st, a.near_list, a.near_cap, a.overflow_rows, nm, row, col0 + cc);
             }
-            const uint32_t sgw = zero_row ? 0xffffffffu : ~neg;  // bit (31-jj) = column cc+jj >= 0
-            sg0 = cc == 0 ? sgw : sg0;
-            sg1 = cc == 32 ? sgw : sg1;
-            sg2 = cc == 64 ? sgw : sg2;
-            sg3 = cc == 96 ? sgw : sg3;
+            sgbuf[acc][c][r] = zero_row ? 0xffffffffu : ~neg;  // bit (31-jj) = column cc+jj >= 0
           }
         }
         tc_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar_accempty[acc]);
-        if (++acc == kAccBufs) {
-          acc = 0;
-          accph ^= 1u;
-        }
+        asm volatile("bar.sync %0, 64;" ::"r"(1u + q) : "memory");  // the quarter's two warps
+        const uint32_t sg0 = sgbuf[acc][0][r], sg1 = sgbuf[acc][1][r], sg2 = sgbuf[acc][2][r],
+                       sg3 = sgbuf[acc][3][r];
         // buckets of the tables whose last column lies in this tile: bits
         // [t*K, t*K+K) of the big-endian column stream, words 4j-1 .. 4j+3
         const uint32_t end_col = col0 + used;
         for (; next_table < a.tables && (next_table + 1) * K <= end_col; ++next_table) {
+          if ((next_table & 1u) != h) continue;  // alternate tables per half
           const uint32_t s0 = next_table * K;
           const int wi = static_cast<int>(s0 >> 5) - static_cast<int>(4 * j);  // -1 .. 3
           const uint32_t off = s0 & 31u;
@@ -556,10 +627,20 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
           if (valid) a.ids[static_cast<uint64_t>(next_table) * a.n + row] = bucket;
         }
         prev3 = sg3;
+        if (++acc == nacc) {
+          acc = 0;
+          accph ^= 1u;
+        }
       }
     }
   }
 
+  if (prof) {
+    if (warp == 0 && lane == 0) pw[6] = static_cast<unsigned long long>(clock64() - t_start);
+    if ((warp == 0 || warp == 1 || warp >= 2) && lane == 0)
+      for (int i = 0; i < 7; ++i)
+        if (pw[i]) atomicAdd(&a.prof[i], pw[i]);
+  }
   tc_before();
   __syncthreads();
   cluster_sync_all();  // no CTA leaves while its peers may still multicast into it

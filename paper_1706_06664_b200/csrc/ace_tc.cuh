@@ -31,7 +31,8 @@ struct TcArgs {
   unsigned long long near_cap;
   uint32_t* overflow_rows;    // bitmap over rows; rows rechecked in full
   DevState* st;
-  int dbg;  // experiments: 1 = skip epilogue work, 2 = skip MMAs
+  int dbg;  // experiments: 1 = skip epilogue work, 2 = skip MMAs, 4 = skip convert, 8 = half W
+  unsigned long long* prof;  // instrumentation: wait cycles per barrier kind (or null)
 };
 
 cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc);
