@@ -172,6 +172,84 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_stream(args, w, ws, rank, local):
+    """Config 5: the streaming driver over N rows in batches (score against the
+    counts at batch start, flag score <= mean - alpha, insert), one step = the
+    whole stream from an empty sketch.  Reports points/s and p50/p99 of the
+    per-batch device latency."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1706_06664_b200 import _native as N
+    from paper_1706_06664_b200 import ace
+    from paper_1706_06664_b200 import workloads as W
+
+    n = w.n if args.rows is None else min(w.n, args.rows)
+    x = torch.empty((n, w.dim), dtype=torch.float32, device="cuda")
+    chunk = 8 * 1024 * 1024
+    for r0 in range(0, n, chunk):
+        m = min(chunk, n - r0)
+        W.device_rows(w.cfg, r0, m, x[r0:r0 + m].data_ptr())
+    torch.cuda.synchronize()
+    fam = ace.SrpFamily(ace.SrpConfig(dim=w.dim, k_bits=w.k_bits, num_tables=w.num_tables, seed=w.w_seed))
+    sk = ace.AceSketch(fam, ace.CounterWidth.k32)
+    stream = torch.cuda.current_stream()
+    sk.set_stream(stream.cuda_stream)
+    flags = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
+
+    def step():
+        sk.reset()
+        return sk.stream_run(x, w.batch, w.alpha, flags_out=flags)
+
+    for _ in range(max(3, args.warmup)):
+        _, lat, rep = step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    launches0 = N.dev().ace_kernel_launches()
+    lats = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        _, lat, rep = step()
+        lats.append(lat)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = N.dev().ace_kernel_launches() - launches0
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    lat_all = np.concatenate(lats)
+    value = n * ws / (ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": f"synthetic (datagen cfg {w.cfg}, seed {w.data_seed})",
+        "config": {"workload": f"cfg{w.cfg} {w.name}: streaming score -> flag (mean - alpha) -> insert",
+                   "N": n, "d": w.dim, "K": w.k_bits, "L": w.num_tables, "batch": w.batch,
+                   "alpha": w.alpha, "counter_width": 32,
+                   "l2": f"inputs {n * w.dim * 4 / 1e9:.1f} GB > 126 MB L2",
+                   "parallelism": f"replicas x{ws}"},
+        "batch_latency_ms": {"p50": float(np.percentile(lat_all, 50)),
+                             "p99": float(np.percentile(lat_all, 99)),
+                             "max": float(lat_all.max()), "batches_per_step": int(len(lats[0]))},
+        "gpu_launches": int(launches), "clocks": clk,
+        "exactness": {"rechecked": int(sk.last_stats.rechecked), "flipped": int(sk.last_stats.flipped),
+                      "ambiguous": int(rep.ambiguous), "reported": int(rep.reported)},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -185,6 +263,7 @@ def main():
                     help="rows of the cpu_baseline leg (10-30 s of CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--rows", type=int, default=None, help="stream mode: limit N (smoke runs)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -201,7 +280,8 @@ def main():
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w = W.CONFIGS[args.config]
-    assert w.mode == "batch", "bench workload must be a batch configuration"
+    if w.mode == "stream":
+        return run_stream(args, w, ws, rank, local)
     n = w.n
     x = torch.empty((n, w.dim), dtype=torch.float32, device="cuda")
     W.device_rows(args.config, 0, n, x.data_ptr())

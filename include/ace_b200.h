@@ -158,6 +158,19 @@ ace_status ace_sketch_stream_batch(AceSketch* sk, const void* x, int dtype,
                                    double* scores, int out_where,
                                    AceStreamReport* report, AceHashStats* stats);
 
+/* The streaming driver over many batches: rows [0, n) in consecutive
+ * batches of `batch` rows (a positive multiple of 32), each handled exactly
+ * like ace_sketch_stream_batch, all queued on the sketch's stream with no
+ * host synchronisation until the end.  flag_bits: (n+31)/32 words;
+ * batch_ms (host, ceil(n/batch) floats, may be NULL): per-batch device
+ * latency from CUDA events; report->reported / ambiguous are run totals. */
+ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype,
+                                 uint64_t n, uint64_t ld, int x_where,
+                                 uint64_t batch, double alpha,
+                                 uint32_t* flag_bits, int out_where,
+                                 float* batch_ms, AceStreamReport* report,
+                                 AceHashStats* stats);
+
 /* State (sketch.hpp:44-69). */
 ace_status ace_sketch_info(const AceSketch* sk, uint64_t* n, double* mean,
                            int* saturated);

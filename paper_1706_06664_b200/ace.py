@@ -424,6 +424,29 @@ class AceSketch:
         return _bits_to_bool(bits, p.n), sc, rep
 
 
+    def stream_run(self, x, batch: int, alpha: float, flags_out=None, latencies: bool = True):
+        """The streaming driver over consecutive batches of `batch` rows (score
+        against counts at batch start, flag score <= mean - alpha, insert), queued
+        without host synchronisation.  Returns (flags bool array or the device
+        bitmap, per-batch device latency in ms, AceStreamReport with run totals)."""
+        p = _Points(x, self._dim())
+        rep = N.AceStreamReport()
+        nb = (p.n + batch - 1) // batch
+        lat = np.empty(nb, dtype=np.float32) if latencies else None
+        if flags_out is not None:
+            _check(N.dev().ace_sketch_stream_run(self._h, p.ptr, p.dtype, p.n, p.ld, p.where, batch,
+                                                 float(alpha), flags_out.data_ptr(), N.ACE_DEVICE,
+                                                 lat.ctypes.data if lat is not None else None,
+                                                 C.byref(rep), C.byref(self.last_stats)))
+            return flags_out, lat, rep
+        bits = np.zeros((p.n + 31) // 32, dtype=np.uint32)
+        _check(N.dev().ace_sketch_stream_run(self._h, p.ptr, p.dtype, p.n, p.ld, p.where, batch,
+                                             float(alpha), bits.ctypes.data, N.ACE_HOST,
+                                             lat.ctypes.data if lat is not None else None,
+                                             C.byref(rep), C.byref(self.last_stats)))
+        return _bits_to_bool(bits, p.n), lat, rep
+
+
 # --------------------------------------------------------------- dataset -----
 # reference dataset.hpp:14-31
 

@@ -232,6 +232,7 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
     ACE_CUDA(sk->near.ensure(cap * sizeof(unsigned long long)));
     ACE_CUDA(sk->overflow.ensure(((n + 31) / 32) * sizeof(uint32_t)));
     ACE_CUDA(cudaMemsetAsync(sk->overflow.p, 0, ((n + 31) / 32) * sizeof(uint32_t), sk->stream));
+    ACE_CUDA(cudaMemsetAsync(&sk->st->near_count, 0, 2 * sizeof(unsigned long long), sk->stream));
     const uint64_t tiles = (n + 127) / 128;
     ACE_CUDA(sk->x16.ensure(tiles * f->tc.nkc * 2 * 16384));
     ACE_CUDA(sk->rowthr.ensure(tiles * 128 * sizeof(float)));
@@ -491,11 +492,12 @@ ace_status ace_sketch_create(AceFamily* fam, uint32_t counter_width, AceSketch**
   return ACE_OK;
 }
 
+// Stream-ordered: later calls on the sketch's stream see the zeroed state; the
+// host mirror is cleared at once (its next refresh comes after these memsets).
 ace_status ace_sketch_reset(AceSketch* sk) {
   if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_reset: null sketch");
   ACE_CUDA(cudaMemsetAsync(sk->counters, 0, sk->num_counters * sizeof(uint32_t), sk->stream));
   ACE_CUDA(cudaMemsetAsync(sk->st, 0, sizeof(DevState), sk->stream));
-  ACE_CUDA(cudaStreamSynchronize(sk->stream));
   memset(sk->hst, 0, sizeof(DevState));
   return ACE_OK;
 }
@@ -705,6 +707,7 @@ ace_status ace_sketch_stream_batch(AceSketch* sk, const void* x, int dtype, uint
     }
   }
   uint32_t* dflags = (flag_bits && out_where == ACE_DEVICE) ? flag_bits : sk->flags.as<uint32_t>();
+  ACE_CUDA(cudaMemsetAsync(&sk->st->batch_sum, 0, sizeof(unsigned long long), sk->stream));
   ACE_CUDA(launch_stream_score(sk->ids.as<uint32_t>(), n, f->d.tables, f->d.k_bits, sk->counters,
                                alpha, dflags, dsc, sk->st, sk->stream));
   sk->mark(2);
@@ -720,6 +723,69 @@ ace_status ace_sketch_stream_batch(AceSketch* sk, const void* x, int dtype, uint
   }
   r = pull_state(sk);
   if (r != ACE_OK) return r;
+  fill_stats(stats, *sk->hst, n, f);
+  if (report) {
+    report->mean_before = sk->hst->mean_before;
+    report->cut = sk->hst->cut;
+    report->reported = sk->hst->reported;
+    report->ambiguous = sk->hst->ambiguous;
+  }
+  return ACE_OK;
+}
+
+// The streaming driver (ace_cli.cpp:173-186 with the insert deferred to each
+// batch end) over many batches, queued without host synchronisation.
+ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64_t n, uint64_t ld, int x_where,
+                                 uint64_t batch, double alpha, uint32_t* flag_bits, int out_where,
+                                 float* batch_ms, AceStreamReport* report, AceHashStats* stats) {
+  if (!sk) return fail(ACE_E_CONTRACT, "detect_stream: null sketch");
+  if (!(alpha >= 0.0)) return fail(ACE_E_CONTRACT, "detect_stream: alpha must be >= 0");
+  if (batch == 0 || batch % 32 != 0) return fail(ACE_E_CONTRACT, "stream_run: batch must be a positive multiple of 32");
+  ace_status r = check_x(sk->fam, x, dtype, n, ld, x_where);
+  if (r != ACE_OK) return r;
+  if (n == 0) return ACE_OK;
+  const AceFamily* f = sk->fam;
+  const size_t esz = dtype == ACE_F64 ? 8 : 4;
+  const uint64_t nb = (n + batch - 1) / batch;
+  const bool ff = fire_and_forget_ok(sk, n);
+  ACE_CUDA(zero_call_fields(sk));
+  ACE_CUDA(sk->flags.ensure(((n + 31) / 32) * sizeof(uint32_t)));
+  uint32_t* dflags = (flag_bits && out_where == ACE_DEVICE) ? flag_bits : sk->flags.as<uint32_t>();
+  std::vector<cudaEvent_t> ev;
+  if (batch_ms) {
+    ev.resize(nb + 1);
+    for (auto& e : ev) ACE_CUDA(cudaEventCreate(&e));
+  }
+  for (uint64_t b = 0; b < nb; ++b) {
+    const uint64_t r0 = b * batch, rows = std::min(batch, n - r0);
+    if (batch_ms) ACE_CUDA(cudaEventRecord(ev[b], sk->stream));
+    const void* xb = static_cast<const char*>(x) + r0 * ld * esz;
+    const void* xd;
+    uint64_t ldd;
+    r = stage_x(sk, sk->stage, sk->stream, xb, dtype, rows, ld, x_where, &xd, &ldd);
+    if (r == ACE_OK) r = run_hash(sk, xd, dtype, rows, ldd, 0);
+    if (r != ACE_OK) return r;
+    ACE_CUDA(cudaMemsetAsync(&sk->st->batch_sum, 0, sizeof(unsigned long long), sk->stream));
+    ACE_CUDA(launch_stream_score(sk->ids.as<uint32_t>(), rows, f->d.tables, f->d.k_bits, sk->counters, alpha,
+                                 dflags + r0 / 32, nullptr, sk->st, sk->stream));
+    ACE_CUDA(launch_apply_ids(sk->ids.as<uint32_t>(), rows, f->d.tables, f->d.k_bits, sk->counters, sk->cap, +1,
+                              sk->st, sk->stream, !ff));
+    if (sk->width == 16) ACE_CUDA(launch_cap(sk->counters, sk->num_counters, sk->cap, sk->st, sk->stream));
+  }
+  if (batch_ms) ACE_CUDA(cudaEventRecord(ev[nb], sk->stream));
+  if (flag_bits && out_where == ACE_HOST)
+    if ((r = copy_out(flag_bits, dflags, ((n + 31) / 32) * sizeof(uint32_t), ACE_HOST, sk->stream)) != ACE_OK)
+      return r;
+  r = pull_state(sk);
+  if (r != ACE_OK) return r;
+  if (batch_ms) {
+    for (uint64_t b = 0; b < nb; ++b) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[b], ev[b + 1]);
+      batch_ms[b] = ms;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
   fill_stats(stats, *sk->hst, n, f);
   if (report) {
     report->mean_before = sk->hst->mean_before;

@@ -568,42 +568,49 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
         mbar_wait_t(&bar_accfull[acc], accph, (prof && lane == 0) ? &pw[5] : nullptr);
         tc_after();
         if (!(a.dbg & 1)) {
-#pragma unroll 1
-          for (uint32_t c = 2 * h; c < 2 * h + 2; ++c) {
-            const uint32_t cc = c * 32u;
-            if (cc >= used) break;
-            uint32_t v[32];
-            ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + acc * 128u + cc, v);
+          const uint32_t c0 = 64u * h;  // this half's first column
+          if (c0 < used) {
+            // both 32-column loads in flight before one wait
+            uint32_t v[64];
+            ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + acc * 128u + c0, v);
+            if (c0 + 32u < used) ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + acc * 128u + c0 + 32u, (v + 32));
             tmem_wait_ld();
-            const uint32_t ncol = min(32u, used - cc);
-            uint32_t n4[4] = {0u, 0u, 0u, 0u}, m4[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
-            if (ncol == 32u) {
 #pragma unroll
-              for (int jj = 0; jj < 8; ++jj)
+            for (uint32_t g2 = 0; g2 < 2; ++g2) {
+              const uint32_t cc = c0 + 32u * g2;
+              if (cc < used) {
+                const uint32_t* vv = v + 32 * g2;
+                const uint32_t ncol = min(32u, used - cc);
+                uint32_t n4[4] = {0u, 0u, 0u, 0u}, m4[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+                if (ncol == 32u) {
 #pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                  n4[g] = (n4[g] << 1) | (v[g * 8 + jj] >> 31);
-                  m4[g] = min(m4[g], v[g * 8 + jj] << 1);
+                  for (int jj = 0; jj < 8; ++jj)
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                      n4[g] = (n4[g] << 1) | (vv[g * 8 + jj] >> 31);
+                      m4[g] = min(m4[g], vv[g * 8 + jj] << 1);
+                    }
+                } else {
+#pragma unroll
+                  for (int jj = 0; jj < 8; ++jj)
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                      n4[g] = (n4[g] << 1) | (vv[g * 8 + jj] >> 31);
+                      if (static_cast<uint32_t>(g * 8 + jj) < ncol) m4[g] = min(m4[g], vv[g * 8 + jj] << 1);
+                    }
                 }
-            } else {
+                const uint32_t neg = (n4[0] << 24) | (n4[1] << 16) | (n4[2] << 8) | n4[3];
+                const uint32_t mn = min(min(m4[0], m4[1]), min(m4[2], m4[3]));
+                if (!zero_row && valid && mn <= thr_u) {
+                  uint32_t nm = 0u;
 #pragma unroll
-              for (int jj = 0; jj < 8; ++jj)
-#pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                  n4[g] = (n4[g] << 1) | (v[g * 8 + jj] >> 31);
-                  if (static_cast<uint32_t>(g * 8 + jj) < ncol) m4[g] = min(m4[g], v[g * 8 + jj] << 1);
+                  for (int jj = 0; jj < 32; ++jj)
+                    nm |= ((static_cast<uint32_t>(jj) < ncol && (vv[jj] << 1) <= thr_u) ? 1u : 0u) << jj;
+                  push_near_mask(a.st, a.near_list, a.near_cap, a.overflow_rows, nm, row, col0 + cc);
                 }
+                sgbuf[acc][2 * h + g2][r] = zero_row ? 0xffffffffu : ~neg;  // bit (31-jj) = column cc+jj >= 0
+              }
             }
-            const uint32_t neg = (n4[0] << 24) | (n4[1] << 16) | (n4[2] << 8) | n4[3];
-            const uint32_t mn = min(min(m4[0], m4[1]), min(m4[2], m4[3]));
-            if (!zero_row && valid && mn <= thr_u) {
-              uint32_t nm = 0u;
-#pragma unroll
-              for (int jj = 0; jj < 32; ++jj)
-                nm |= ((static_cast<uint32_t>(jj) < ncol && (v[jj] << 1) <= thr_u) ? 1u : 0u) << jj;
-              push_near_mask(a.st, a.near_list, a.near_cap, a.overflow_rows, nm, row, col0 + cc);
-            }
-            sgbuf[acc][c][r] = zero_row ? 0xffffffffu : ~neg;  // bit (31-jj) = column cc+jj >= 0
           }
         }
         tc_before();

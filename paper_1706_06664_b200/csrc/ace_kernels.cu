@@ -412,10 +412,19 @@ __global__ void apply_ids_kernel(const uint32_t* __restrict__ ids, uint64_t n, u
 
 __global__ void sum_squares_kernel(const uint32_t* __restrict__ c, uint64_t num,
                                    unsigned long long* out) {
+  // uint4 loads (counter arrays are 16-byte aligned, num a multiple of 2^K)
   unsigned long long s = 0;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < num;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    s += static_cast<unsigned long long>(c[i]) * c[i];
+  const uint64_t n4 = num / 4;
+  const uint4* c4 = reinterpret_cast<const uint4*>(c);
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint4 v = c4[i];
+    s += static_cast<unsigned long long>(v.x) * v.x + static_cast<unsigned long long>(v.y) * v.y +
+         static_cast<unsigned long long>(v.z) * v.z + static_cast<unsigned long long>(v.w) * v.w;
+  }
+  if (blockIdx.x == 0)
+    for (uint64_t i = n4 * 4 + threadIdx.x; i < num; i += blockDim.x)
+      s += static_cast<unsigned long long>(c[i]) * c[i];
   s = warp_sum_u64(s);
   if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
 }
@@ -449,6 +458,9 @@ __device__ void flush_hist(uint32_t* hist, uint32_t nb, uint32_t* ct, uint32_t c
   __syncthreads();
 }
 
+// Without kTrackT the merge is fire-and-forget and the caller recomputes
+// T = sum c^2 (a bucket's ids may be split across blocks, so per-block counts
+// cannot give the exact increment).
 template <bool kTrackT>
 __global__ void __launch_bounds__(1024) apply_ids_smem_kernel(const uint32_t* __restrict__ ids, uint64_t n,
                                                               uint32_t tables, uint32_t k_bits, uint64_t per,
@@ -833,7 +845,7 @@ __global__ void stream_score_kernel(const uint32_t* __restrict__ ids, uint64_t n
   const double cut = s_cut, band = s_band;
   const int live = s_live;
   const double L = static_cast<double>(tables);
-  unsigned long long rep = 0, amb = 0;
+  unsigned long long rep = 0, amb = 0, bsum = 0;
   const uint64_t words = (n + 31) / 32;
   for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x; base < words * 32;
        base += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -841,8 +853,18 @@ __global__ void stream_score_kernel(const uint32_t* __restrict__ ids, uint64_t n
     bool f = false;
     if (i < n) {
       unsigned long long S = 0ull;
-      for (uint32_t t = 0; t < tables; ++t)
-        S += counters[((uint64_t)t << k_bits) + ids[(uint64_t)t * n + i]];
+      uint32_t t = 0;
+      for (; t + 8 <= tables; t += 8) {
+        uint32_t b[8], c[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) b[u] = ids[(uint64_t)(t + u) * n + i];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) c[u] = counters[((uint64_t)(t + u) << k_bits) + b[u]];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) S += c[u];
+      }
+      for (; t < tables; ++t) S += counters[((uint64_t)t << k_bits) + ids[(uint64_t)t * n + i]];
+      bsum += S;
       const double sc = __ddiv_rn(static_cast<double>(S), L);
       if (scores) scores[i] = sc;
       f = live && sc <= cut;
@@ -856,9 +878,11 @@ __global__ void stream_score_kernel(const uint32_t* __restrict__ ids, uint64_t n
   }
   rep = warp_sum_u64(rep);
   amb = warp_sum_u64(amb);
+  bsum = warp_sum_u64(bsum);
   if ((threadIdx.x & 31) == 0) {
     if (rep) atomicAdd(&st->reported, rep);
     if (amb) atomicAdd(&st->ambiguous, amb);
+    if (bsum) atomicAdd(&st->batch_sum, bsum);
   }
 }
 
@@ -922,8 +946,8 @@ cudaError_t launch_apply_ids(const uint32_t* ids, uint64_t n, uint32_t tables, u
       apply_ids_smem_kernel<false><<<grid, 1024, smem, s>>>(ids, n, tables, k_bits, per, counters, cap, st);
       // T = sum of squared counters (exact for unsaturated 32-bit sketches)
       cudaMemsetAsync(&st->T, 0, sizeof(st->T), s);
-      sum_squares_kernel<<<grid_for((static_cast<uint64_t>(tables) << k_bits), 256), 256, 0, s>>>(
-          counters, static_cast<uint64_t>(tables) << k_bits, &st->T);
+      const uint64_t num = static_cast<uint64_t>(tables) << k_bits;
+      sum_squares_kernel<<<grid_for(num / 4 + 1, 256, sms * 4), 256, 0, s>>>(counters, num, &st->T);
       count_launch();
     }
     count_launch();

@@ -227,3 +227,21 @@ def test_tc_dims_and_overflow_path(cuda, oracle_c, d):
     ref, _ = oracle_c.buckets(fam.directions, x, k, l)
     assert np.array_equal(ids, ref)
     assert (ids[:, 0] == 0).all()  # NaN -> all bits 0
+
+
+def test_stream_run_matches_reference(cuda, golden):
+    """The queued multi-batch driver gives the golden per-batch flags."""
+    e = golden["configs"]["5"]
+    fam = family(5)
+    sk = ace.AceSketch(fam, ace.CounterWidth.k32)
+    nb = len(e["per_batch"])
+    x, _ = W.host_rows(5, 0, nb * e["batch"])
+    flags, lat, rep = sk.stream_run(cuda.from_numpy(x).cuda(), e["batch"], e["alpha"])
+    assert len(lat) == nb and (lat > 0).all()
+    for b, pb in enumerate(e["per_batch"]):
+        fb = flags[b * e["batch"]:(b + 1) * e["batch"]]
+        assert sha(np.packbits(fb, bitorder="little")) == pb["flags_sha256"], b
+    assert sha(sk.counters_u32()) == e["counters_sha256"]
+    assert rep.ambiguous == 0
+    with pytest.raises(ace.ContractViolation):
+        sk.stream_run(x[:100], 33, 1.0)
