@@ -223,6 +223,7 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
     t.ntiles = f->tc.ntiles;
     t.nkc = f->tc.nkc;
     t.w16 = f->tc.w16;
+    tc_fill_tables(&t);
     // error bound of the fp16x3 split relative to ||x~|| ||w^||
     t.margin_c = static_cast<float>(
         2.0 * (4.0 * 0x1.0p-22 + 0x1.0p-23 * (12.0 * f->tc.nkc + 16.0) * 1.01 + (t.x_f64 ? 0x1.0p-23 : 0.0)));
@@ -260,12 +261,30 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
     sk->mark(4);
     ACE_CUDA(launch_convert_x(t, sk->stream));
     sk->mark(6);
+    // Fused epilogue insert (global REDs) only where the separate insert would
+    // use global atomics too (K > 15: no shared-memory histogram); with K <= 15
+    // the privatised histogram absorbs hot buckets far better.
+    static int fused_env = -2;
+    if (fused_env == -2) {
+      const char* e = getenv("ACE_FUSED_INSERT");
+      fused_env = e ? atoi(e) : -1;
+    }
+    const bool fused = insert && sk->width == 32 && fire_and_forget_ok(sk, n) &&
+                       (fused_env >= 0 ? fused_env == 1 : f->d.k_bits > 15);
+    t.w64 = f->d.w64;
+    t.counters = sk->counters;
+    t.fused_insert = fused ? 1 : 0;
     ACE_CUDA(launch_hash_tc(t, sk->stream));
     sk->mark(5);
     ACE_CUDA(launch_recheck(t, f->d.w64, sk->stream));
-    if (insert)
+    if (fused) {
+      // T = sum of squared counters (exact: 32-bit, unsaturated)
+      ACE_CUDA(cudaMemsetAsync(&sk->st->T, 0, sizeof(unsigned long long), sk->stream));
+      ACE_CUDA(launch_sum_squares(sk->counters, sk->num_counters, &sk->st->T, sk->stream));
+    } else if (insert) {
       ACE_CUDA(launch_apply_ids(sk->ids.as<uint32_t>(), n, f->d.tables, f->d.k_bits, sk->counters, sk->cap,
                                 +1, sk->st, sk->stream, !fire_and_forget_ok(sk, n)));
+    }
   } else {
     HashArgs a = make_hash_args(f, xd, dtype, n, ld, sk->ids.as<uint32_t>(), n, sk->st);
     a.insert = insert;

@@ -23,6 +23,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "ace_tc.cuh"
 
 namespace ace_dev {
@@ -251,6 +253,12 @@ __device__ __forceinline__ double exact_proj(const double* __restrict__ w, const
   return acc;
 }
 
+__device__ __forceinline__ unsigned long long warp_sum_u64_tc(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 // ---- X conversion pre-pass ------------------------------------------------------
 
 __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
@@ -354,20 +362,37 @@ __global__ void __launch_bounds__(256) convert_x_kernel(const TcArgs a, uint64_t
   }
 }
 
-// Cold path: push the near-tie columns (bit jj of mask = column dir0 + jj).
-__device__ __noinline__ void push_near_mask(DevState* st, unsigned long long* list, unsigned long long cap,
-                                            uint32_t* overflow_rows, uint32_t mask, uint64_t row, uint32_t dir0) {
+// Cold path: push the near-tie columns (bit jj of mask = column dir0 + jj)
+// into this CTA's list segment; a full segment flags the whole row instead.
+__device__ __noinline__ void push_near_mask(DevState* st, unsigned long long* seg, unsigned long long seg_cap,
+                                            uint32_t* seg_n, uint32_t* overflow_rows, uint32_t mask, uint64_t row,
+                                            uint32_t dir0) {
   while (mask) {
     const uint32_t jj = __ffs(mask) - 1;
     mask &= mask - 1;
-    const unsigned long long slot = atomicAdd(&st->near_count, 1ull);
-    if (slot < cap) {
-      list[slot] = (static_cast<unsigned long long>(row) << 32) | (dir0 + jj);
+    const uint32_t slot = atomicAdd(seg_n, 1u);
+    if (slot < seg_cap) {
+      seg[slot] = (static_cast<unsigned long long>(row) << 32) | (dir0 + jj);
     } else {
       atomicOr(&overflow_rows[row >> 5], 1u << (row & 31));
       st->near_overflow = 1;
     }
   }
+}
+
+// Warp-aggregated counter increments for one table: lanes holding equal
+// buckets are merged over up to three ballot rounds, the rest add singly.
+__device__ __forceinline__ void insert_bucket_warp(uint32_t* ct, uint32_t bucket, bool valid, uint32_t lane) {
+  unsigned rem = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+  for (int round = 0; round < 3 && rem; ++round) {
+    const int leader = __ffs(rem) - 1;
+    const uint32_t bl = __shfl_sync(0xffffffffu, bucket, leader);
+    const unsigned eq = __ballot_sync(0xffffffffu, bucket == bl) & rem;
+    if (lane == static_cast<uint32_t>(leader)) atomicAdd(&ct[bl], static_cast<uint32_t>(__popc(eq)));
+    rem &= ~eq;
+  }
+  if ((rem >> lane) & 1u) atomicAdd(&ct[bucket], 1u);
 }
 
 // ---- the projection kernel ----------------------------------------------------------
@@ -379,6 +404,8 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
   __shared__ __align__(8) uint64_t bar_accfull[kAccBufs], bar_accempty[kAccBufs];
   __shared__ uint32_t tmem_base_sh;
   __shared__ uint32_t sgbuf[kAccBufs][4][kRows];  // epilogue sign words per accumulator
+  __shared__ uint32_t seg_n;                        // near ties pushed by this CTA
+  __shared__ unsigned long long blk_rech, blk_flip;
 
   const TcLayout L = tc_layout(a.nkc);
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -392,6 +419,8 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
   const uint32_t a_tile_bytes = a.nkc * 2u * kBlockBytes;
 
   if (threadIdx.x == 0) {
+    seg_n = 0;
+    blk_rech = blk_flip = 0;
     for (uint32_t s = 0; s < L.n_wst; ++s) {
       mbar_init(&bar_wfull[s], 1);
       mbar_init(&bar_wempty[s], kCluster);  // every CTA's MMA must have released the stage
@@ -426,6 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
   // [0] prod a_empty [1] prod w_empty [2] mma a_full [3] mma acc_empty
   // [4] mma w_full [5] epilogue acc_full (warp 2..5 lane 0 summed) [6] total
   const bool prof = a.prof != nullptr;
+  const unsigned long long seg_cap = a.near_cap / gridDim.x;
   unsigned long long pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const long long t_start = clock64();
 
@@ -561,7 +591,6 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
       const bool zero_row = thr < 0.0f;
       const uint32_t thr_u = zero_row ? 0u : (isinf(thr) ? 0xffffffffu : (__float_as_uint(thr) << 1));
       uint32_t prev3 = 0u;
-      uint32_t next_table = 0;
       for (uint32_t j = 0; j < a.ntiles; ++j) {
         const uint32_t used = min(128u, R - j * 128u);
         const uint32_t col0 = j * 128u;
@@ -606,7 +635,8 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
 #pragma unroll
                   for (int jj = 0; jj < 32; ++jj)
                     nm |= ((static_cast<uint32_t>(jj) < ncol && (vv[jj] << 1) <= thr_u) ? 1u : 0u) << jj;
-                  push_near_mask(a.st, a.near_list, a.near_cap, a.overflow_rows, nm, row, col0 + cc);
+                  push_near_mask(a.st, a.near_list + blockIdx.x * seg_cap, seg_cap, &seg_n, a.overflow_rows, nm, row,
+                             col0 + cc);
                 }
                 sgbuf[acc][2 * h + g2][r] = zero_row ? 0xffffffffu : ~neg;  // bit (31-jj) = column cc+jj >= 0
               }
@@ -617,27 +647,70 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar_accempty[acc]);
         asm volatile("bar.sync %0, 64;" ::"r"(1u + q) : "memory");  // the quarter's two warps
-        const uint32_t sg0 = sgbuf[acc][0][r], sg1 = sgbuf[acc][1][r], sg2 = sgbuf[acc][2][r],
-                       sg3 = sgbuf[acc][3][r];
-        // buckets of the tables whose last column lies in this tile: bits
-        // [t*K, t*K+K) of the big-endian column stream, words 4j-1 .. 4j+3
-        const uint32_t end_col = col0 + used;
-        for (; next_table < a.tables && (next_table + 1) * K <= end_col; ++next_table) {
-          if ((next_table & 1u) != h) continue;  // alternate tables per half
-          const uint32_t s0 = next_table * K;
+        // buckets of the tables whose last column lies in this tile (host
+        // precomputed range, alternate tables per half): bits [t*K, t*K+K) of
+        // the big-endian column stream, words 4j-1 (prev3) .. 4j+3 (sgbuf)
+        const uint32_t tb = j == 0 ? 0u : a.tab_end[j - 1], te = a.tab_end[j];
+        uint32_t* idp = a.ids + row;
+        for (uint32_t tt = tb + h; tt < te; tt += 2) {
+          const uint32_t s0 = tt * K;
           const int wi = static_cast<int>(s0 >> 5) - static_cast<int>(4 * j);  // -1 .. 3
           const uint32_t off = s0 & 31u;
-          const uint32_t hi = wi < 0 ? prev3 : (wi == 0 ? sg0 : (wi == 1 ? sg1 : (wi == 2 ? sg2 : sg3)));
-          const uint32_t lo = wi < 0 ? sg0 : (wi == 0 ? sg1 : (wi == 1 ? sg2 : (wi == 2 ? sg3 : 0u)));
+          const uint32_t hi = wi < 0 ? prev3 : sgbuf[acc][wi][r];
+          const uint32_t lo = wi < 3 ? sgbuf[acc][wi + 1][r] : 0u;
           const unsigned long long win = (static_cast<unsigned long long>(hi) << 32) | lo;
           const uint32_t bucket = static_cast<uint32_t>(win >> (64u - off - K)) & kmask;
-          if (valid) a.ids[static_cast<uint64_t>(next_table) * a.n + row] = bucket;
+          if (valid) idp[static_cast<uint64_t>(tt) * a.n] = bucket;
+          if (a.fused_insert) insert_bucket_warp(a.counters + (static_cast<uint64_t>(tt) << K), bucket, valid, lane);
         }
+        const uint32_t sg3 = sgbuf[acc][3][r];
         prev3 = sg3;
         if (++acc == nacc) {
           acc = 0;
           accph ^= 1u;
         }
+      }
+    }
+    // ---- exact recheck of this CTA's near ties (binary64 fold, srp.cpp:78-91):
+    // wrong fast bits are flipped in ids and, with the fused insert, the count
+    // moves from the old bucket to the corrected one (counters commute).
+    asm volatile("bar.sync 5, 256;" ::: "memory");  // the eight epilogue warps
+    {
+      const uint32_t et = threadIdx.x - 64u;
+      const uint32_t cnt = static_cast<uint32_t>(min(static_cast<unsigned long long>(seg_n), seg_cap));
+      const unsigned long long* seg = a.near_list + blockIdx.x * seg_cap;
+      unsigned long long rr = 0, ff = 0;
+      for (uint32_t i = et; i < cnt; i += 256u) {
+        const unsigned long long item = seg[i];
+        const uint64_t row = item >> 32;
+        const uint32_t dir = static_cast<uint32_t>(item & 0xffffffffu);
+        const uint32_t table = dir / K, bpos = K - 1u - dir % K;
+        const double p = exact_proj(a.w64 + static_cast<uint64_t>(dir) * a.dim, a.x, a.x_f64, row, a.ld, a.dim);
+        uint32_t* id = &a.ids[static_cast<uint64_t>(table) * a.n + row];
+        const uint32_t exact = p >= 0.0 ? 1u : 0u;
+        if (((*id >> bpos) & 1u) != exact) {
+          const uint32_t old = atomicXor(id, 1u << bpos);
+          if (a.fused_insert) {
+            uint32_t* ct = a.counters + (static_cast<uint64_t>(table) << K);
+            atomicSub(&ct[old], 1u);
+            atomicAdd(&ct[old ^ (1u << bpos)], 1u);
+          }
+          ++ff;
+        }
+        ++rr;
+      }
+      rr = warp_sum_u64_tc(rr);
+      ff = warp_sum_u64_tc(ff);
+      if (lane == 0) {
+        if (rr) atomicAdd(&blk_rech, rr);
+        if (ff) atomicAdd(&blk_flip, ff);
+      }
+      asm volatile("bar.sync 5, 256;" ::: "memory");
+      if (et == 0) {
+        if (blk_rech) atomicAdd(&a.st->rechecked, blk_rech);
+        if (blk_flip) atomicAdd(&a.st->flipped, blk_flip);
+        if (seg_n) atomicAdd(&a.st->near_count, static_cast<unsigned long long>(seg_n));
+        if (a.fused_insert && blockIdx.x == 0) atomicAdd(&a.st->n, a.n);
       }
     }
   }
@@ -712,7 +785,14 @@ __global__ void recheck_rows_kernel(const TcArgs a, const double* __restrict__ w
                                   a.ld, a.dim);
       bucket = (bucket << 1) | (p >= 0.0 ? 1u : 0u);
     }
-    a.ids[static_cast<uint64_t>(table) * a.n + row] = bucket;
+    uint32_t* id = &a.ids[static_cast<uint64_t>(table) * a.n + row];
+    const uint32_t old = *id;
+    *id = bucket;
+    if (a.fused_insert && old != bucket) {
+      uint32_t* ct = a.counters + (static_cast<uint64_t>(table) << K);
+      atomicSub(&ct[old], 1u);
+      atomicAdd(&ct[bucket], 1u);
+    }
     atomicAdd(&a.st->rechecked, static_cast<unsigned long long>(K));
   }
 }
@@ -752,6 +832,13 @@ __global__ void pack_w16_kernel(const double* __restrict__ w64, const double* __
 
 bool tc_supported(uint64_t dim) { return dim >= 1 && dim <= 256; }
 
+void tc_fill_tables(TcArgs* a) {
+  for (uint32_t j = 0; j < a->ntiles && j < 64; ++j) {
+    const uint32_t end_col = std::min((j + 1) * 128u, a->k_bits * a->tables);
+    a->tab_end[j] = static_cast<uint16_t>(std::min(end_col / a->k_bits, a->tables));
+  }
+}
+
 size_t tc_smem_bytes(uint32_t nkc) { return tc_layout(nkc).total; }
 
 cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc) {
@@ -759,7 +846,7 @@ cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc) {
   if (!tc_supported(f.dim) || f.k_bits > 128) return cudaSuccess;
   const uint32_t nkc = static_cast<uint32_t>((f.dim + kChunk - 1) / kChunk);
   const TcLayout L = tc_layout(nkc);
-  if (nkc > 4 || tc_layout(nkc).n_wst < 2) return cudaSuccess;
+  if (nkc > 4 || tc_layout(nkc).n_wst < 2 || f.rows > 64u * 128u) return cudaSuccess;
   tc->nkc = nkc;
   tc->ntiles = (f.rows + kRows - 1) / kRows;
   const size_t bytes = static_cast<size_t>(tc->ntiles) * nkc * 2 * kBlockBytes;
@@ -832,9 +919,8 @@ cudaError_t launch_convert_x(const TcArgs& a, cudaStream_t s) {
 }
 
 cudaError_t launch_recheck(const TcArgs& a, const double* w64, cudaStream_t s) {
-  recheck_list_kernel<<<592, 256, 0, s>>>(a, w64);
   recheck_rows_kernel<<<592, 256, 0, s>>>(a, w64);
-  count_launch(2);
+  count_launch(1);
   return cudaGetLastError();
 }
 

@@ -27,21 +27,28 @@ struct TcArgs {
   float* rowthr;              // per-row error threshold (pre-pass output)
   float margin_c;             // relative error bound
   uint32_t* ids;              // table-major, stride n
-  unsigned long long* near_list;  // (row << 32) | direction
-  unsigned long long near_cap;
+  unsigned long long* near_list;  // (row << 32) | direction; one segment per CTA
+  unsigned long long near_cap;    // total entries (the kernel uses near_cap / grid per CTA)
+  const double* w64;              // the reference's W (binary64) for the exact recheck
+  uint32_t* counters;             // fused insert target (fused_insert != 0)
+  int fused_insert;               // 32-bit sketch: insert buckets in the epilogue
   uint32_t* overflow_rows;    // bitmap over rows; rows rechecked in full
   DevState* st;
+  uint16_t tab_end[64];      // tables completed by the end of direction tile j
   int dbg;  // experiments: 1 = skip epilogue work, 2 = skip MMAs, 4 = skip convert, 8 = half W
   unsigned long long* prof;  // instrumentation: wait cycles per barrier kind (or null)
 };
 
 cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc);
+// per-tile table ranges (TcArgs::tab_end) from k_bits, tables, ntiles
+void tc_fill_tables(TcArgs* a);
 void tc_free_family(TcFamily* tc);
 // X -> fp16 hi/lo SW128 tile image + per-row thresholds (must precede the hash)
 cudaError_t launch_convert_x(const TcArgs& a, cudaStream_t s);
 cudaError_t launch_hash_tc(const TcArgs& a, cudaStream_t s);
-// Exact FP64 recheck of the near-tie list (patches ids) + rows that
-// overflowed the list (all projections recomputed).
+// Rows whose near ties overflowed their CTA's list: every bucket recomputed
+// exactly (counters moved when the insert was fused).  The listed near ties
+// are rechecked inside hash_tc_kernel itself.
 cudaError_t launch_recheck(const TcArgs& a, const double* w64, cudaStream_t s);
 size_t tc_smem_bytes(uint32_t nkc);
 bool tc_supported(uint64_t dim);
