@@ -230,7 +230,13 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
     t.ids = sk->ids.as<uint32_t>();
     uint64_t cap = n * f->d.rows / 1024;
     cap = std::min<uint64_t>(std::max<uint64_t>(cap, 1u << 20), 1u << 25);
-    ACE_CUDA(sk->near.ensure(cap * sizeof(unsigned long long)));
+    {
+      // the kernel's near-tie list is all ~0 between launches (entries are
+      // reset as they are rechecked); fill a newly allocated one
+      const void* before = sk->near.p;
+      ACE_CUDA(sk->near.ensure(cap * sizeof(unsigned long long)));
+      if (sk->near.p != before) ACE_CUDA(cudaMemsetAsync(sk->near.p, 0xff, sk->near.bytes, sk->stream));
+    }
     ACE_CUDA(sk->overflow.ensure(((n + 31) / 32) * sizeof(uint32_t)));
     ACE_CUDA(cudaMemsetAsync(sk->overflow.p, 0, ((n + 31) / 32) * sizeof(uint32_t), sk->stream));
     ACE_CUDA(cudaMemsetAsync(&sk->st->near_count, 0, 2 * sizeof(unsigned long long), sk->stream));
@@ -252,8 +258,9 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
       t.dbg = dbg;
       static unsigned long long* prof = nullptr;
       if (getenv("ACE_TC_PROF")) {
-        if (!prof) cudaMalloc(&prof, 8 * sizeof(unsigned long long));
-        cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), sk->stream);
+        if (!prof) cudaMalloc(&prof, 32 * sizeof(unsigned long long));
+        cudaMemsetAsync(prof, 0, 32 * sizeof(unsigned long long), sk->stream);
+        cudaMemsetAsync(prof + 10, 0xff, sizeof(unsigned long long), sk->stream);  // min start
       }
       t.prof = prof;
       g_tc_prof = prof;
@@ -262,15 +269,15 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
     ACE_CUDA(launch_convert_x(t, sk->stream));
     sk->mark(6);
     // Fused epilogue insert (global REDs) only where the separate insert would
-    // use global atomics too (K > 15: no shared-memory histogram); with K <= 15
-    // the privatised histogram absorbs hot buckets far better.
+    // use global atomics too (K > 20); otherwise the shared-memory histogram
+    // (split into 2^15-bin parts for K > 15) absorbs hot buckets far better.
     static int fused_env = -2;
     if (fused_env == -2) {
       const char* e = getenv("ACE_FUSED_INSERT");
       fused_env = e ? atoi(e) : -1;
     }
     const bool fused = insert && sk->width == 32 && fire_and_forget_ok(sk, n) &&
-                       (fused_env >= 0 ? fused_env == 1 : f->d.k_bits > 15);
+                       (fused_env >= 0 ? fused_env == 1 : f->d.k_bits > 20);
     t.w64 = f->d.w64;
     t.counters = sk->counters;
     t.fused_insert = fused ? 1 : 0;
@@ -367,10 +374,10 @@ uint64_t ace_kernel_launches(void) { return g_launches.load(); }
 // Instrumentation readout (ACE_TC_PROF set): wait cycles per barrier kind of
 // the last tcgen05 projection launch, summed over CTAs.  Not part of the ABI
 // contract in include/ace_b200.h.
-int ace_debug_tc_prof(unsigned long long* out8) {
+int ace_debug_tc_prof(unsigned long long* out32) {
   if (!g_tc_prof) return -1;
   cudaDeviceSynchronize();
-  return cudaMemcpy(out8, g_tc_prof, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : -2;
+  return cudaMemcpy(out32, g_tc_prof, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : -2;
 }
 
 // SrpFamily::SrpFamily (srp.cpp:24-49): validation + W upload.

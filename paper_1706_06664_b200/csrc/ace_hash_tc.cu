@@ -36,7 +36,17 @@ constexpr int kChunk = 64;                 // K elements per chunk (128 B of fp1
 constexpr int kBlockBytes = kRows * 128;   // one 128 x 64 fp16 block = 16 KB
 constexpr int kAccBufs = 3;                // max TMEM accumulators (x 128 columns)
 constexpr int kMaxWStages = 6;
-constexpr int kThreads = 320;
+#ifndef ACE_SLEEPY
+#define ACE_SLEEPY 64  // ns back-off of off-critical-path barrier waits (0: spin)
+#endif
+#ifndef ACE_KC_FENCE
+#define ACE_KC_FENCE 0
+#endif
+#ifndef ACE_RW
+#define ACE_RW 1  // recheck warps: 0 none (tail only), 1 recheck warps during the main loop
+#endif
+constexpr int kThreads = ACE_RW ? 384 : 320;  // producer, MMA, 8 epilogue warps, 2 recheck warps
+constexpr uint32_t kTail = ACE_RW ? 320 : 256;  // epilogue + recheck threads
 constexpr size_t kSmemLimit = 232448;      // 227 KB per CTA
 constexpr uint32_t kCluster = 1;           // CTAs sharing each W stage (TMA multicast)
 
@@ -90,6 +100,36 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+// Wait for warps off the critical MMA path: back off between polls so the
+// polling does not compete with the tensor pipe for shared memory.
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleepy(uint64_t* bar, uint32_t parity, unsigned long long* acc) {
+#if ACE_SLEEPY
+  const long long t0 = acc ? clock64() : 0;
+  while (!mbar_try(bar, parity)) __nanosleep(ACE_SLEEPY);
+  if (acc) *acc += static_cast<unsigned long long>(clock64() - t0);
+#else
+  if (acc) {
+    const long long t0 = clock64();
+    mbar_wait(bar, parity);
+    *acc += static_cast<unsigned long long>(clock64() - t0);
+  } else {
+    mbar_wait(bar, parity);
+  }
+#endif
 }
 // mbar_wait that adds the cycles spent waiting to *acc (instrumentation)
 __device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, unsigned long long* acc) {
@@ -253,6 +293,13 @@ __device__ __forceinline__ double exact_proj(const double* __restrict__ w, const
   return acc;
 }
 
+__device__ __forceinline__ void cp_async_4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
 __device__ __forceinline__ unsigned long long warp_sum_u64_tc(unsigned long long v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -395,6 +442,111 @@ __device__ __forceinline__ void insert_bucket_warp(uint32_t* ct, uint32_t bucket
   if ((rem >> lane) & 1u) atomicAdd(&ct[bucket], 1u);
 }
 
+// Binary64 left fold, mul then add, from +0.0 (srp.cpp:78-91), operands 8
+// ahead; gives up (returns false) as soon as *done reaches `until` (the
+// epilogue has finished: the shared tail takes the item).  Out of line: cold
+// code kept away from the main loop's instruction cache footprint.
+__device__ __noinline__ bool exact_proj_until(const double* __restrict__ w, const void* x, int x_f64, uint64_t row,
+                                              uint64_t ld, uint32_t dim, const uint32_t* done, uint32_t until,
+                                              double* out) {
+  double acc = 0.0;
+  for (uint32_t k0 = 0; k0 < dim; k0 += 8u) {
+    if (*reinterpret_cast<const volatile uint32_t*>(done) >= until) return false;
+    double wv[8], xv[8];
+#pragma unroll
+    for (uint32_t u = 0; u < 8u; ++u) {
+      const uint32_t k = min(k0 + u, dim - 1u);
+      wv[u] = __ldg(w + k);
+      xv[u] = x_f64 ? __ldg(static_cast<const double*>(x) + row * ld + k)
+                    : static_cast<double>(__ldg(static_cast<const float*>(x) + row * ld + k));
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < 8u; ++u)
+      if (k0 + u < dim) acc = __dadd_rn(acc, __dmul_rn(wv[u], xv[u]));
+  }
+  *out = acc;
+  return true;
+}
+
+// Shared tail of the near-tie recheck, run by the kTail epilogue + recheck
+// threads (named barrier 9) once the main loop is over: list slots
+// [from, cnt) that still hold an item (~0 = already rechecked) are rechecked
+// in chunks.  Every MMA has completed by then, so the whole dynamic shared
+// memory is free: each chunk's operands (x row and W row, element-major
+// [k][item] so the fold reads are conflict-free) are copied global -> shared
+// with cp.async (no register staging: all of them in flight at once), then
+// each thread folds one item.  Slots are reset to ~0 for the next launch.
+__device__ __noinline__ void recheck_tail(const void* x, int x_f64, uint64_t ld, uint32_t dim, const double* w64,
+                                          uint32_t* ids, uint64_t n, uint32_t* counters, int fused_insert,
+                                          uint32_t K, uint8_t* smem, size_t smem_bytes, unsigned long long* seg,
+                                          uint32_t from, uint32_t cnt, uint32_t et, unsigned long long& rr,
+                                          unsigned long long& ff) {
+  const uint32_t cap_items = min(static_cast<uint32_t>(smem_bytes / (16u * dim + 8u)), kTail);
+  unsigned long long* meta = reinterpret_cast<unsigned long long*>(smem);
+  double* xs = reinterpret_cast<double*>(smem + 8u * cap_items);
+  double* ws = xs + static_cast<size_t>(cap_items) * dim;
+  const uint32_t qd = kTail / dim, rd = kTail % dim;
+  for (uint32_t c0 = from; c0 < cnt; c0 += cap_items) {
+    const uint32_t m = min(cap_items, cnt - c0);
+    for (uint32_t i = et; i < m; i += kTail) {
+      meta[i] = seg[c0 + i];
+      seg[c0 + i] = ~0ull;
+    }
+    asm volatile("bar.sync 9, %0;" ::"r"(kTail) : "memory");
+    const uint32_t total = m * dim;
+    uint32_t ci = et / dim, ck = et - (et / dim) * dim;  // (item, k) of element e, advanced incrementally
+    for (uint32_t e = et; e < total; e += kTail) {
+      const unsigned long long item = meta[ci];
+      if (item != ~0ull) {
+        const uint64_t row = item >> 32;
+        const uint32_t dir = static_cast<uint32_t>(item & 0xffffffffu);
+        const size_t slot = static_cast<size_t>(ck) * cap_items + ci;
+        if (x_f64)
+          cp_async_8(xs + slot, static_cast<const double*>(x) + row * ld + ck);
+        else
+          cp_async_4(reinterpret_cast<float*>(xs) + slot, static_cast<const float*>(x) + row * ld + ck);
+        cp_async_8(ws + slot, w64 + static_cast<uint64_t>(dir) * dim + ck);
+      }
+      ci += qd;
+      ck += rd;
+      if (ck >= dim) {
+        ck -= dim;
+        ++ci;
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    asm volatile("bar.sync 9, %0;" ::"r"(kTail) : "memory");
+    if (et < m && meta[et] != ~0ull) {
+      // binary64 left fold, mul then add, from +0.0 (srp.cpp:78-91)
+      double acc = 0.0;
+      const float* xs32 = reinterpret_cast<const float*>(xs);
+#pragma unroll 8
+      for (uint32_t k = 0; k < dim; ++k) {
+        const size_t slot = static_cast<size_t>(k) * cap_items + et;
+        const double xv = x_f64 ? xs[slot] : static_cast<double>(xs32[slot]);
+        acc = __dadd_rn(acc, __dmul_rn(ws[slot], xv));
+      }
+      const unsigned long long item = meta[et];
+      const uint64_t row = item >> 32;
+      const uint32_t dir = static_cast<uint32_t>(item & 0xffffffffu);
+      const uint32_t table = dir / K, bpos = K - 1u - dir % K;
+      uint32_t* id = &ids[static_cast<uint64_t>(table) * n + row];
+      const uint32_t exact = acc >= 0.0 ? 1u : 0u;
+      if (((__ldcg(id) >> bpos) & 1u) != exact) {
+        const uint32_t old = atomicXor(id, 1u << bpos);
+        if (fused_insert) {
+          uint32_t* ct = counters + (static_cast<uint64_t>(table) << K);
+          atomicSub(&ct[old], 1u);
+          atomicAdd(&ct[old ^ (1u << bpos)], 1u);
+        }
+        ++ff;
+      }
+      ++rr;
+    }
+    asm volatile("bar.sync 9, %0;" ::"r"(kTail) : "memory");
+  }
+}
+
 // ---- the projection kernel ----------------------------------------------------------
 
 __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
@@ -403,8 +555,10 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
   __shared__ __align__(8) uint64_t bar_afull[2], bar_aempty[2];
   __shared__ __align__(8) uint64_t bar_accfull[kAccBufs], bar_accempty[kAccBufs];
   __shared__ uint32_t tmem_base_sh;
-  __shared__ uint32_t sgbuf[kAccBufs][4][kRows];  // epilogue sign words per accumulator
+  __shared__ uint32_t lastw[4][2][32];  // epilogue: last sign word of a direction tile, per quarter / parity
   __shared__ uint32_t seg_n;                        // near ties pushed by this CTA
+  __shared__ uint32_t tiles_done;                   // epilogue warps x tiles completed (ids stored)
+  __shared__ uint32_t min_next;                     // first list slot the recheck warps left over
   __shared__ unsigned long long blk_rech, blk_flip;
 
   const TcLayout L = tc_layout(a.nkc);
@@ -420,6 +574,8 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
 
   if (threadIdx.x == 0) {
     seg_n = 0;
+    tiles_done = 0;
+    min_next = ACE_RW ? 0xffffffffu : 0u;
     blk_rech = blk_flip = 0;
     for (uint32_t s = 0; s < L.n_wst; ++s) {
       mbar_init(&bar_wfull[s], 1);
@@ -431,7 +587,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
     }
     for (int b = 0; b < kAccBufs; ++b) {
       mbar_init(&bar_accfull[b], 1);
-      mbar_init(&bar_accempty[b], 8);  // eight epilogue warps
+      mbar_init(&bar_accempty[b], 4);  // one epilogue warp per lane quarter
     }
     fence_mbar_init();
   }
@@ -456,15 +612,18 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
   // [4] mma w_full [5] epilogue acc_full (warp 2..5 lane 0 summed) [6] total
   const bool prof = a.prof != nullptr;
   const unsigned long long seg_cap = a.near_cap / gridDim.x;
-  unsigned long long pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long pw[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   const long long t_start = clock64();
+  unsigned long long rr_own = 0, ff_own = 0;  // near ties rechecked / bits flipped by this thread
+  unsigned long long g_start = 0;
+  if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
 
   if (warp == 0) {
     // ---------------- producer: A tile (once per tile) + W stages ----------------
     if (lane == 0) {
       uint32_t s = 0, ph = 0, it = 0;
       for (uint64_t t = blockIdx.x; t < t_end; t += gridDim.x, ++it) {
-        mbar_wait_t(&bar_aempty[0], (it & 1u) ^ 1u, prof ? &pw[0] : nullptr);
+        mbar_wait_sleepy(&bar_aempty[0], (it & 1u) ^ 1u, prof ? &pw[0] : nullptr);
         const uint64_t tt = t < n_tiles ? t : n_tiles - 1;  // past the end: reload the last tile
         mbar_expect_tx(&bar_afull[0], a_tile_bytes);
         bulk_g2s(Asm, reinterpret_cast<const uint8_t*>(a.x16) + tt * a_tile_bytes, a_tile_bytes, &bar_afull[0]);
@@ -473,8 +632,8 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
           const uint32_t bytes = nmma * 128u;
           const uint32_t part = bytes / kCluster;  // this CTA's slice, multicast to the cluster
           for (uint32_t kc = 0; kc < a.nkc; ++kc) {
-            mbar_wait_t(&bar_wempty[s], ph ^ 1u, prof ? &pw[1] : nullptr);
-            if ((a.dbg & 8) && (it & 1u)) {  // experiment: skip W traffic on odd tiles
+            mbar_wait_sleepy(&bar_wempty[s], ph ^ 1u, prof ? &pw[1] : nullptr);
+            if ((a.dbg & 8) && it > 0) {  // experiment: W loaded for the first tile only
               mbar_arrive(&bar_wfull[s]);
               if (++s == L.n_wst) {
                 s = 0;
@@ -508,16 +667,19 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
     // descriptors live in uniform registers); one elected lane issues.
     {
       uint32_t s = 0, wph = 0, acc = 0, accph = 0, it = 0;
+      unsigned long long pmi = 0, pmn = 0, pcp = 0;  // instrumentation: MMA-group issue cycles / groups, A copies
+      const long long ploop = clock64();
       const uint32_t nacc = tc_acc_bufs(a.nkc);
       const uint32_t ta_hi = tmem_base + nacc * 128u, ta_lo = ta_hi + a.nkc * 32u;  // dpad/2 columns each
       const uint32_t a_base = smem_u32(Asm), w_base = smem_u32(Wsm);
       for (uint64_t t = blockIdx.x; t < t_end; t += gridDim.x, ++it) {
         mbar_wait_t(&bar_afull[0], it & 1u, (prof && lane == 0) ? &pw[2] : nullptr);
         tc_after();
+        const long long pc0 = prof ? clock64() : 0;
         // copies execute in issue order after this CTA's earlier MMAs, so the
         // previous tile's reads of TMEM A are complete before it is replaced
         if (elect_one()) {
-          for (uint32_t kc = 0; kc < a.nkc; ++kc) {
+          for (uint32_t kc = 0; kc < ((a.dbg & 512) && it > 0 ? 0u : a.nkc); ++kc) {  // 512: experiment, A once
             const uint32_t ah = a_base + kc * 2u * kBlockBytes;
 #pragma unroll
             for (uint32_t kk = 0; kk < 4; ++kk) {
@@ -528,6 +690,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
           mma_commit(&bar_aempty[0]);  // shared-memory A free once the copies land
         }
         __syncwarp();
+        if (prof) pcp += static_cast<unsigned long long>(clock64() - pc0);
         for (uint32_t j = 0; j < a.ntiles; ++j) {
           const uint32_t nmma = (min(128u, R - j * 128u) + 15u) & ~15u;
           const uint32_t idesc = idesc_f16(nmma);
@@ -537,6 +700,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
           for (uint32_t kc = 0; kc < a.nkc; ++kc) {
             mbar_wait_t(&bar_wfull[s], wph, (prof && lane == 0) ? &pw[4] : nullptr);
             tc_after();
+            const long long pi0 = prof ? clock64() : 0;
             const uint32_t b_hi = w_base + s * 2u * kBlockBytes;
             const uint64_t dbh = sw128_desc(b_hi), dbl = sw128_desc(b_hi + kBlockBytes);
             if (elect_one()) {
@@ -556,6 +720,10 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
                 mma_commit_mc(&bar_wempty[s], cmask);
             }
             __syncwarp();
+            if (prof) {
+              pmi += static_cast<unsigned long long>(clock64() - pi0);
+              ++pmn;
+            }
             if (++s == L.n_wst) {
               s = 0;
               wph ^= 1u;
@@ -569,157 +737,255 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
           }
         }
       }
-    }
-  } else {
-    // ---------------- epilogue (warps 2-9) ----------------
-    // Two warps per TMEM lane quarter (q = warp % 4): half h = 0 takes
-    // columns 0-63 of each direction tile, h = 1 columns 64-127.  Per
-    // 32-column chunk: sign bits packed MSB-first (one funnel shift per
-    // column), near ties by one unsigned min over |v| (bits << 1), four
-    // independent chains for ILP.  The pair swaps sign words through shared
-    // memory (named barrier 1 + q) and each cuts out alternate tables' buckets;
-    // tables straddling direction tiles use the carried last word prev3.
-    const uint32_t q = warp & 3, h = (warp - 2) >> 2;
-    const uint32_t r = q * 32u + lane;
-    const uint32_t kmask = (K >= 32u) ? 0xffffffffu : ((1u << K) - 1u);
-    const uint32_t nacc = tc_acc_bufs(a.nkc);
-    uint32_t acc = 0, accph = 0;
-    for (uint64_t t = blockIdx.x; t < t_end; t += gridDim.x) {
-      const uint64_t row = t * kRows + r;
-      const bool valid = row < a.n;
-      const float thr = valid ? a.rowthr[row] : -1.0f;
-      const bool zero_row = thr < 0.0f;
-      const uint32_t thr_u = zero_row ? 0u : (isinf(thr) ? 0xffffffffu : (__float_as_uint(thr) << 1));
-      uint32_t prev3 = 0u;
-      for (uint32_t j = 0; j < a.ntiles; ++j) {
-        const uint32_t used = min(128u, R - j * 128u);
-        const uint32_t col0 = j * 128u;
-        mbar_wait_t(&bar_accfull[acc], accph, (prof && lane == 0) ? &pw[5] : nullptr);
-        tc_after();
-        if (!(a.dbg & 1)) {
-          const uint32_t c0 = 64u * h;  // this half's first column
-          if (c0 < used) {
-            // both 32-column loads in flight before one wait
-            uint32_t v[64];
-            ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + acc * 128u + c0, v);
-            if (c0 + 32u < used) ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + acc * 128u + c0 + 32u, (v + 32));
-            tmem_wait_ld();
-#pragma unroll
-            for (uint32_t g2 = 0; g2 < 2; ++g2) {
-              const uint32_t cc = c0 + 32u * g2;
-              if (cc < used) {
-                const uint32_t* vv = v + 32 * g2;
-                const uint32_t ncol = min(32u, used - cc);
-                uint32_t n4[4] = {0u, 0u, 0u, 0u}, m4[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
-                if (ncol == 32u) {
-#pragma unroll
-                  for (int jj = 0; jj < 8; ++jj)
-#pragma unroll
-                    for (int g = 0; g < 4; ++g) {
-                      n4[g] = (n4[g] << 1) | (vv[g * 8 + jj] >> 31);
-                      m4[g] = min(m4[g], vv[g * 8 + jj] << 1);
-                    }
-                } else {
-#pragma unroll
-                  for (int jj = 0; jj < 8; ++jj)
-#pragma unroll
-                    for (int g = 0; g < 4; ++g) {
-                      n4[g] = (n4[g] << 1) | (vv[g * 8 + jj] >> 31);
-                      if (static_cast<uint32_t>(g * 8 + jj) < ncol) m4[g] = min(m4[g], vv[g * 8 + jj] << 1);
-                    }
-                }
-                const uint32_t neg = (n4[0] << 24) | (n4[1] << 16) | (n4[2] << 8) | n4[3];
-                const uint32_t mn = min(min(m4[0], m4[1]), min(m4[2], m4[3]));
-                if (!zero_row && valid && mn <= thr_u) {
-                  uint32_t nm = 0u;
-#pragma unroll
-                  for (int jj = 0; jj < 32; ++jj)
-                    nm |= ((static_cast<uint32_t>(jj) < ncol && (vv[jj] << 1) <= thr_u) ? 1u : 0u) << jj;
-                  push_near_mask(a.st, a.near_list + blockIdx.x * seg_cap, seg_cap, &seg_n, a.overflow_rows, nm, row,
-                             col0 + cc);
-                }
-                sgbuf[acc][2 * h + g2][r] = zero_row ? 0xffffffffu : ~neg;  // bit (31-jj) = column cc+jj >= 0
-              }
-            }
-          }
-        }
-        tc_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bar_accempty[acc]);
-        asm volatile("bar.sync %0, 64;" ::"r"(1u + q) : "memory");  // the quarter's two warps
-        // buckets of the tables whose last column lies in this tile (host
-        // precomputed range, alternate tables per half): bits [t*K, t*K+K) of
-        // the big-endian column stream, words 4j-1 (prev3) .. 4j+3 (sgbuf)
-        const uint32_t tb = j == 0 ? 0u : a.tab_end[j - 1], te = a.tab_end[j];
-        uint32_t* idp = a.ids + row;
-        for (uint32_t tt = tb + h; tt < te; tt += 2) {
-          const uint32_t s0 = tt * K;
-          const int wi = static_cast<int>(s0 >> 5) - static_cast<int>(4 * j);  // -1 .. 3
-          const uint32_t off = s0 & 31u;
-          const uint32_t hi = wi < 0 ? prev3 : sgbuf[acc][wi][r];
-          const uint32_t lo = wi < 3 ? sgbuf[acc][wi + 1][r] : 0u;
-          const unsigned long long win = (static_cast<unsigned long long>(hi) << 32) | lo;
-          const uint32_t bucket = static_cast<uint32_t>(win >> (64u - off - K)) & kmask;
-          if (valid) idp[static_cast<uint64_t>(tt) * a.n] = bucket;
-          if (a.fused_insert) insert_bucket_warp(a.counters + (static_cast<uint64_t>(tt) << K), bucket, valid, lane);
-        }
-        const uint32_t sg3 = sgbuf[acc][3][r];
-        prev3 = sg3;
-        if (++acc == nacc) {
-          acc = 0;
-          accph ^= 1u;
-        }
+      if (prof && pmn && lane == 0) {
+        atomicAdd(&a.prof[20], pmi);
+        atomicAdd(&a.prof[21], pmn);
+        atomicAdd(&a.prof[22], pcp);
+        atomicAdd(&a.prof[23], static_cast<unsigned long long>(clock64() - ploop));
+        atomicAdd(&a.prof[24], pw[2] + pw[3] + pw[4]);
       }
     }
-    // ---- exact recheck of this CTA's near ties (binary64 fold, srp.cpp:78-91):
-    // wrong fast bits are flipped in ids and, with the fused insert, the count
-    // moves from the old bucket to the corrected one (counters commute).
-    asm volatile("bar.sync 5, 256;" ::: "memory");  // the eight epilogue warps
-    {
-      const uint32_t et = threadIdx.x - 64u;
-      const uint32_t cnt = static_cast<uint32_t>(min(static_cast<unsigned long long>(seg_n), seg_cap));
-      const unsigned long long* seg = a.near_list + blockIdx.x * seg_cap;
-      unsigned long long rr = 0, ff = 0;
-      for (uint32_t i = et; i < cnt; i += 256u) {
-        const unsigned long long item = seg[i];
+  } else if (warp >= 10) {
+    // ---------------- recheck warps (10, 11) ----------------
+    // Exact binary64 recheck of near ties while the main loop runs: lane L of
+    // recheck warp w takes list slots w*32+L, +64, ... in order, waits until
+    // the slot is written and its tile's ids are stored (tiles_done), folds
+    // the exact projection, fixes the bit (and, with the fused insert, moves
+    // the count) and resets the slot to ~0.  When the epilogue finishes, the
+    // lanes stop; the shared tail takes the slots from min_next on.
+    const uint32_t total_done = 8u * static_cast<uint32_t>(iters);
+    unsigned long long* seg = a.near_list + blockIdx.x * seg_cap;
+    uint32_t i = (warp - 10u) * 32u + lane;
+    if (!(a.dbg & 32)) {
+      while (true) {
+        unsigned long long item = ~0ull;
+        while (true) {
+          if (*reinterpret_cast<volatile uint32_t*>(&tiles_done) >= total_done) break;
+          if (i < seg_cap) item = *reinterpret_cast<volatile unsigned long long*>(seg + i);
+          if (item != ~0ull) break;
+          __nanosleep(256);
+        }
+        if (item == ~0ull) break;
         const uint64_t row = item >> 32;
+        const uint32_t it = static_cast<uint32_t>(((row >> 7) - blockIdx.x) / gridDim.x);
+        while (*reinterpret_cast<volatile uint32_t*>(&tiles_done) < 8u * (it + 1u)) __nanosleep(128);
+        __threadfence_block();
         const uint32_t dir = static_cast<uint32_t>(item & 0xffffffffu);
         const uint32_t table = dir / K, bpos = K - 1u - dir % K;
-        const double p = exact_proj(a.w64 + static_cast<uint64_t>(dir) * a.dim, a.x, a.x_f64, row, a.ld, a.dim);
+        // binary64 left fold (srp.cpp:78-91), abandoned
+        // (slot left for the shared tail) once the epilogue has finished
+        double p = 0.0;
+        const bool abandoned = !exact_proj_until(a.w64 + static_cast<uint64_t>(dir) * a.dim, a.x, a.x_f64, row, a.ld,
+                                                 static_cast<uint32_t>(a.dim), &tiles_done, total_done, &p);
+        if (abandoned) break;
         uint32_t* id = &a.ids[static_cast<uint64_t>(table) * a.n + row];
         const uint32_t exact = p >= 0.0 ? 1u : 0u;
-        if (((*id >> bpos) & 1u) != exact) {
+        if (((__ldcg(id) >> bpos) & 1u) != exact) {
           const uint32_t old = atomicXor(id, 1u << bpos);
           if (a.fused_insert) {
             uint32_t* ct = a.counters + (static_cast<uint64_t>(table) << K);
             atomicSub(&ct[old], 1u);
             atomicAdd(&ct[old ^ (1u << bpos)], 1u);
           }
-          ++ff;
+          ++ff_own;
         }
-        ++rr;
+        ++rr_own;
+        seg[i] = ~0ull;
+        i += 64u;
       }
-      rr = warp_sum_u64_tc(rr);
-      ff = warp_sum_u64_tc(ff);
+    }
+    atomicMin(&min_next, i);
+  } else {
+    // ---------------- epilogue (warps 2-9) ----------------
+    // Two warps per TMEM lane quarter (q = warp % 4) take alternate direction
+    // tiles (global tile counter g, owner h = g & 1), all 128 columns each, in
+    // two 64-column rounds (two 32-column loads in flight per round).  Per
+    // 32 columns: sign bits packed MSB-first (one funnel shift per column),
+    // near ties by one unsigned min over |v| (bits << 1), four independent
+    // chains for ILP.  The four sign words stay in registers; buckets of the
+    // tables ending in the tile are cut from them.  A table straddling the
+    // previous tile needs that tile's last word, which the partner warp
+    // publishes in shared memory (named barriers 1+q: h=0 -> h=1, 5+q:
+    // h=1 -> h=0, one arrive / one sync per tile, strictly alternating).
+    const uint32_t q = warp & 3, h = (warp - 2) >> 2;
+    const uint32_t r = q * 32u + lane;
+    const uint32_t kmask = (K >= 32u) ? 0xffffffffu : ((1u << K) - 1u);
+    const uint32_t nacc = tc_acc_bufs(a.nkc);
+    const uint64_t g_total = iters * a.ntiles;
+    uint32_t acc = 0, accph = 0;
+    uint64_t g = 0;
+    long long pc_ext = 0;
+    for (uint64_t t = blockIdx.x; t < t_end; t += gridDim.x) {
+      const uint64_t row = t * kRows + r;
+      const bool valid = row < a.n;
+      const float thr = valid ? a.rowthr[row] : -1.0f;
+      const bool zero_row = thr < 0.0f;
+      const uint32_t thr_u = zero_row ? 0u : (isinf(thr) ? 0xffffffffu : (__float_as_uint(thr) << 1));
+      for (uint32_t j = 0; j < a.ntiles; ++j, ++g) {
+        if ((g & 1u) == h) {
+          const uint32_t used = min(128u, R - j * 128u);
+          const uint32_t col0 = j * 128u;
+          mbar_wait_sleepy(&bar_accfull[acc], accph, (prof && lane == 0) ? &pw[5] : nullptr);
+          tc_after();
+          long long pc0 = prof ? clock64() : 0, pc1 = 0, pc2 = 0;
+          uint32_t wd0 = 0xffffffffu, wd1 = 0xffffffffu, wd2 = 0xffffffffu, wd3 = 0xffffffffu;
+          if (!(a.dbg & 1)) {
+            // one copy of the 64-column code (small instruction footprint)
+#pragma unroll 1
+            for (uint32_t hr = 0; hr < 2; ++hr) {
+              const uint32_t c0 = 64u * hr;
+              if (c0 >= used) break;
+              uint32_t v[64];
+              ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + acc * 128u + c0, v);
+              ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + acc * 128u + c0 + 32u, (v + 32));
+              tmem_wait_ld();
+              if (prof && hr == 0) pc1 = clock64();
+              uint32_t w2[2];
+              if (a.dbg & 16) {  // experiment: TMEM loads only
+                w2[0] = v[0] ^ v[63];
+                w2[1] = 0u;
+              } else {
+#pragma unroll
+                for (uint32_t g2 = 0; g2 < 2; ++g2) {
+                  const uint32_t cc = c0 + 32u * g2;
+                  const uint32_t* vv = v + 32 * g2;
+                  uint32_t n4[4] = {0u, 0u, 0u, 0u}, m4[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+#pragma unroll
+                  for (int jj = 0; jj < 8; ++jj)
+#pragma unroll
+                    for (int gq = 0; gq < 4; ++gq) {
+                      n4[gq] = (n4[gq] << 1) | (vv[gq * 8 + jj] >> 31);
+                      m4[gq] = min(m4[gq], vv[gq * 8 + jj] << 1);
+                    }
+                  const uint32_t neg = (n4[0] << 24) | (n4[1] << 16) | (n4[2] << 8) | n4[3];
+                  const uint32_t mn = min(min(m4[0], m4[1]), min(m4[2], m4[3]));
+                  // columns past `used` (padding / stale) are masked here, off the hot path
+                  if (!zero_row && valid && mn <= thr_u && cc < used) {
+                    const uint32_t ncol = min(32u, used - cc);
+                    uint32_t nm = 0u;
+#pragma unroll
+                    for (int jj = 0; jj < 32; ++jj) nm |= (((vv[jj] << 1) <= thr_u) ? 1u : 0u) << jj;
+                    if (ncol < 32u) nm &= (1u << ncol) - 1u;
+                    if (nm)
+                      push_near_mask(a.st, a.near_list + blockIdx.x * seg_cap, seg_cap, &seg_n, a.overflow_rows, nm,
+                                     row, col0 + cc);
+                  }
+                  w2[g2] = zero_row ? 0xffffffffu : ~neg;  // bit (31-jj) = column cc+jj >= 0
+                }
+              }
+              if (hr == 0) {
+                wd0 = w2[0];
+                wd1 = w2[1];
+              } else {
+                wd2 = w2[0];
+                wd3 = w2[1];
+              }
+            }
+          }
+          tc_before();
+          __syncwarp();
+          if (prof) pc2 = clock64();
+          if (lane == 0) mbar_arrive(&bar_accempty[acc]);
+          // last word of the previous tile (partner warp), for a straddling table
+          uint32_t prev = 0u;
+          if (g > 0) {
+            asm volatile("bar.sync %0, 64;" ::"r"((h == 1 ? 1u : 5u) + q) : "memory");
+            prev = lastw[q][(g - 1) & 1u][lane];
+          }
+          if (prof && lane == 0 && warp == 2) {
+            const long long pc3 = clock64();
+            atomicAdd(&a.prof[16], static_cast<unsigned long long>(pc1 - pc0));  // TMEM load + wait
+            atomicAdd(&a.prof[17], static_cast<unsigned long long>(pc2 - pc1));  // sign / near processing
+            atomicAdd(&a.prof[18], static_cast<unsigned long long>(pc3 - pc2));  // arrive + partner barrier
+            pc_ext = pc3;
+          }
+          // publish this tile's last word for the partner (next tile's owner)
+          if (g + 1 < g_total) {
+            lastw[q][g & 1u][lane] = wd3;
+            asm volatile("bar.arrive %0, 64;" ::"r"((h == 0 ? 1u : 5u) + q) : "memory");
+          }
+          // buckets of the tables whose last column lies in this tile (host
+          // precomputed range): bits [t*K, t*K+K) of the big-endian column
+          // stream, words 4j-1 (prev) .. 4j+3 (wd)
+          const uint32_t tb = j == 0 ? 0u : a.tab_end[j - 1], te = a.tab_end[j];
+          uint32_t* idp = a.ids + row;
+          for (uint32_t tt = tb; tt < te; ++tt) {
+            const uint32_t s0 = tt * K;
+            const int wi = static_cast<int>(s0 >> 5) - static_cast<int>(4 * j);  // -1 .. 3
+            const uint32_t off = s0 & 31u;
+            const uint32_t hi = wi < 0 ? prev : wi == 0 ? wd0 : wi == 1 ? wd1 : wi == 2 ? wd2 : wd3;
+            const uint32_t lo = wi < 0 ? wd0 : wi == 0 ? wd1 : wi == 1 ? wd2 : wi == 2 ? wd3 : 0u;
+            const unsigned long long win = (static_cast<unsigned long long>(hi) << 32) | lo;
+            const uint32_t bucket = static_cast<uint32_t>(win >> (64u - off - K)) & kmask;
+            if (valid && (!(a.dbg & 128) || bucket == 0xffffffffu)) idp[static_cast<uint64_t>(tt) * a.n] = bucket;
+            if (a.fused_insert) insert_bucket_warp(a.counters + (static_cast<uint64_t>(tt) << K), bucket, valid, lane);
+          }
+          if (prof && lane == 0 && warp == 2) atomicAdd(&a.prof[19], static_cast<unsigned long long>(clock64() - pc_ext));
+        }
+        if (++acc == nacc) {
+          acc = 0;
+          accph ^= 1u;
+        }
+      }
+      // this tile's ids (and near-list entries) are written: publish to the
+      // recheck warps
+      __syncwarp();
       if (lane == 0) {
-        if (rr) atomicAdd(&blk_rech, rr);
-        if (ff) atomicAdd(&blk_flip, ff);
-      }
-      asm volatile("bar.sync 5, 256;" ::: "memory");
-      if (et == 0) {
-        if (blk_rech) atomicAdd(&a.st->rechecked, blk_rech);
-        if (blk_flip) atomicAdd(&a.st->flipped, blk_flip);
-        if (seg_n) atomicAdd(&a.st->near_count, static_cast<unsigned long long>(seg_n));
-        if (a.fused_insert && blockIdx.x == 0) atomicAdd(&a.st->n, a.n);
+        __threadfence_block();
+        atomicAdd(&tiles_done, 1u);
       }
     }
   }
 
+  if (warp >= 2) {
+    // ---- shared tail: exact recheck (binary64 fold, srp.cpp:78-91) of the
+    // list slots the recheck warps did not reach.  Wrong fast bits are flipped
+    // in ids and, with the fused insert, the count moves from the old bucket
+    // to the corrected one (counters commute).
+    asm volatile("bar.sync 9, %0;" ::"r"(kTail) : "memory");  // epilogue done, recheck warps stopped
+    if (prof && warp == 2) pw[8] = static_cast<unsigned long long>(clock64() - t_start);
+    const uint32_t et = threadIdx.x - 64u;
+    const uint32_t cnt = static_cast<uint32_t>(min(static_cast<unsigned long long>(seg_n), seg_cap));
+    if (!(a.dbg & 32))
+      recheck_tail(a.x, a.x_f64, a.ld, static_cast<uint32_t>(a.dim), a.w64, a.ids, a.n, a.counters, a.fused_insert,
+                   K, base, L.a_bytes + L.w_bytes, a.near_list + blockIdx.x * seg_cap, min(min_next, cnt), cnt, et,
+                   rr_own, ff_own);
+    rr_own = warp_sum_u64_tc(rr_own);
+    ff_own = warp_sum_u64_tc(ff_own);
+    if (lane == 0) {
+      if (rr_own) atomicAdd(&blk_rech, rr_own);
+      if (ff_own) atomicAdd(&blk_flip, ff_own);
+    }
+    asm volatile("bar.sync 9, %0;" ::"r"(kTail) : "memory");
+    if (et == 0) {
+      if (blk_rech) atomicAdd(&a.st->rechecked, blk_rech);
+      if (blk_flip) atomicAdd(&a.st->flipped, blk_flip);
+      if (seg_n) atomicAdd(&a.st->near_count, static_cast<unsigned long long>(seg_n));
+      if (a.fused_insert && blockIdx.x == 0) atomicAdd(&a.st->n, a.n);
+    }
+  }
+
   if (prof) {
-    if (warp == 0 && lane == 0) pw[6] = static_cast<unsigned long long>(clock64() - t_start);
-    if ((warp == 0 || warp == 1 || warp >= 2) && lane == 0)
-      for (int i = 0; i < 7; ++i)
+    // [6] producer end [7] MMA end [8] epilogue main-loop end (warp 2)
+    // [9] epilogue tail end (warp 2), cycles from t_start; [10] min start /
+    // [11] max end of %globaltimer (ns) over CTAs
+    const unsigned long long dt = static_cast<unsigned long long>(clock64() - t_start);
+    if (lane == 0) {
+      if (warp == 0) pw[6] = dt;
+      if (warp == 1) pw[7] = dt;
+      if (warp == 2) pw[9] = dt;
+      for (int i = 0; i < 10; ++i)
         if (pw[i]) atomicAdd(&a.prof[i], pw[i]);
+      unsigned long long g;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      if (warp == 0) atomicMax(&a.prof[11], g);
+      if (warp == 2) {
+        atomicMax(&a.prof[12], pw[9]);
+        atomicMax(&a.prof[13], pw[8]);
+        atomicMax(&a.prof[14], static_cast<unsigned long long>(seg_n));
+      }
+      if (warp == 0) atomicMin(&a.prof[10], g_start);
+    }
   }
   tc_before();
   __syncthreads();

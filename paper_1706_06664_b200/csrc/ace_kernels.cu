@@ -461,51 +461,63 @@ __device__ void flush_hist(uint32_t* hist, uint32_t nb, uint32_t* ct, uint32_t c
 // Without kTrackT the merge is fire-and-forget and the caller recomputes
 // T = sum c^2 (a bucket's ids may be split across blocks, so per-block counts
 // cannot give the exact increment).
+//
+// Each table's 2^K buckets are split into parts of 2^part_bits bins (the
+// shared histogram stays <= 128 KB).  Block b counts part (b mod parts) over
+// row range (b / parts) of the flattened table-major ids; the blocks of one
+// range run side by side, so all but the first read of each id hit L2.
+// Equal buckets within a warp are merged by ballot rounds while the rounds
+// pay (a round that merges no other lane ends them: uniform data costs one).
 template <bool kTrackT>
 __global__ void __launch_bounds__(1024) apply_ids_smem_kernel(const uint32_t* __restrict__ ids, uint64_t n,
-                                                              uint32_t tables, uint32_t k_bits, uint64_t per,
-                                                              uint32_t* counters, uint32_t cap, DevState* st) {
+                                                              uint32_t tables, uint32_t k_bits, uint32_t part_bits,
+                                                              uint64_t per, uint32_t* counters, uint32_t cap,
+                                                              DevState* st) {
   extern __shared__ uint32_t hist[];
   __shared__ unsigned long long blk;
-  const uint32_t nb = 1u << k_bits;
+  const uint32_t nb = 1u << part_bits;
+  const uint32_t pshift = k_bits - part_bits;
+  const uint32_t part = blockIdx.x & ((1u << pshift) - 1u);
   const uint64_t total = n * tables;
-  const uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * per;
+  const uint64_t i0 = static_cast<uint64_t>(blockIdx.x >> pshift) * per;
   const uint64_t i1 = min(total, i0 + per);
   for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
   if (threadIdx.x == 0) blk = 0ull;
   const int lane = threadIdx.x & 31;
   unsigned long long dT = 0ull;
   constexpr int kDepth = 8;  // ids in flight per thread
+  const uint32_t step = blockDim.x * kDepth;
   for (uint64_t seg = i0; seg < i1;) {
-    const uint64_t t = seg / n;                      // table of this segment
-    const uint64_t seg_end = min(i1, (t + 1) * n);   // stay within the table
+    const uint64_t t = seg / n;
+    const uint64_t seg_end = min(i1, (t + 1) * n);  // stay within table t
     __syncthreads();
-    for (uint64_t base = seg; base < seg_end; base += static_cast<uint64_t>(blockDim.x) * kDepth) {
-      uint32_t bv[kDepth];
+    for (uint64_t base = seg; base < seg_end; base += step) {
+      const uint32_t len = static_cast<uint32_t>(min(seg_end - base, static_cast<uint64_t>(step)));
+      const uint32_t* src = ids + base;
+      // all loads issued before any use (clamped addresses, no branches)
+      uint32_t idv[kDepth];
+#pragma unroll
+      for (int u = 0; u < kDepth; ++u) idv[u] = __ldg(src + min(u * blockDim.x + threadIdx.x, len - 1u));
 #pragma unroll
       for (int u = 0; u < kDepth; ++u) {
-        const uint64_t i = base + static_cast<uint64_t>(u) * blockDim.x + threadIdx.x;
-        bv[u] = i < seg_end ? __ldcs(ids + i) : 0xffffffffu;  // streamed once: evict-first
-      }
-#pragma unroll
-      for (int u = 0; u < kDepth; ++u) {
-        const uint32_t b = bv[u];
-        const bool valid = b != 0xffffffffu;
-        // aggregate up to three runs of equal buckets per warp (clustered data),
-        // the remaining lanes add individually
-        unsigned rem = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-        for (int round = 0; round < 3 && rem; ++round) {
+        const uint32_t id = idv[u];
+        const uint32_t b =
+            (u * blockDim.x + threadIdx.x < len && (id >> part_bits) == part) ? (id & (nb - 1u)) : 0xffffffffu;
+        unsigned rem = __ballot_sync(0xffffffffu, b != 0xffffffffu);
+#pragma unroll 1
+        for (int round = 0; round < 4 && rem; ++round) {
           const int leader = __ffs(rem) - 1;
           const uint32_t bl = __shfl_sync(0xffffffffu, b, leader);
           const unsigned eq = __ballot_sync(0xffffffffu, b == bl) & rem;
+          if (eq == (1u << leader)) break;  // nothing merged: stop aggregating
           if (lane == leader) atomicAdd(&hist[bl], static_cast<uint32_t>(__popc(eq)));
           rem &= ~eq;
         }
         if ((rem >> lane) & 1u) atomicAdd(&hist[b], 1u);
       }
     }
-    flush_hist<kTrackT>(hist, nb, counters + (t << k_bits), cap, st, dT);
+    flush_hist<kTrackT>(hist, nb, counters + (t << k_bits) + (static_cast<uint64_t>(part) << part_bits), cap, st,
+                        dT);
     seg = seg_end;
   }
   dT = warp_sum_u64(dT);
@@ -917,7 +929,7 @@ cudaError_t launch_apply_ids(const uint32_t* ids, uint64_t n, uint32_t tables, u
                              uint32_t* counters, uint32_t cap, int sign, DevState* st,
                              cudaStream_t s, bool track_t) {
   if (n == 0) return cudaSuccess;
-  if (sign > 0 && k_bits <= 15 && n >= 4096) {
+  if (sign > 0 && k_bits <= 20 && n >= 4096) {
     static bool configured = false;
     if (!configured) {
       cudaError_t e = cudaFuncSetAttribute(apply_ids_smem_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -934,16 +946,20 @@ cudaError_t launch_apply_ids(const uint32_t* ids, uint64_t n, uint32_t tables, u
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
+    const uint32_t part_bits = k_bits < 15 ? k_bits : 15;
+    const uint32_t parts = 1u << (k_bits - part_bits);
     const uint64_t total = n * tables;
-    uint64_t blocks = static_cast<uint64_t>(sms);
-    if (blocks > total / 4096) blocks = total / 4096 > 0 ? total / 4096 : 1;
-    const uint64_t per = (total + blocks - 1) / blocks;
-    const unsigned grid = static_cast<unsigned>((total + per - 1) / per);
-    const size_t smem = sizeof(uint32_t) << k_bits;
+    uint64_t ranges = static_cast<uint64_t>(sms) / parts;
+    if (ranges < 1) ranges = 1;
+    if (ranges > total / 4096) ranges = total / 4096 > 0 ? total / 4096 : 1;
+    const uint64_t per = (total + ranges - 1) / ranges;
+    const unsigned grid = static_cast<unsigned>((total + per - 1) / per) * parts;
+    const size_t smem = sizeof(uint32_t) << part_bits;
     if (track_t) {
-      apply_ids_smem_kernel<true><<<grid, 1024, smem, s>>>(ids, n, tables, k_bits, per, counters, cap, st);
+      apply_ids_smem_kernel<true><<<grid, 1024, smem, s>>>(ids, n, tables, k_bits, part_bits, per, counters, cap, st);
     } else {
-      apply_ids_smem_kernel<false><<<grid, 1024, smem, s>>>(ids, n, tables, k_bits, per, counters, cap, st);
+      apply_ids_smem_kernel<false><<<grid, 1024, smem, s>>>(ids, n, tables, k_bits, part_bits, per, counters, cap,
+                                                             st);
       // T = sum of squared counters (exact for unsaturated 32-bit sketches)
       cudaMemsetAsync(&st->T, 0, sizeof(st->T), s);
       const uint64_t num = static_cast<uint64_t>(tables) << k_bits;

@@ -35,7 +35,7 @@ struct TcArgs {
   uint32_t* overflow_rows;    // bitmap over rows; rows rechecked in full
   DevState* st;
   uint16_t tab_end[64];      // tables completed by the end of direction tile j
-  int dbg;  // experiments: 1 = skip epilogue work, 2 = skip MMAs, 4 = skip convert, 8 = half W
+  int dbg;  // experiments: 1 = skip epilogue work, 2 = skip MMAs, 4 = skip convert, 8 = half W, 16 = TMEM loads only
   unsigned long long* prof;  // instrumentation: wait cycles per barrier kind (or null)
 };
 
