@@ -561,7 +561,8 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
   __shared__ uint32_t min_next;                     // first list slot the recheck warps left over
   __shared__ unsigned long long blk_rech, blk_flip;
 
-  const TcLayout L = tc_layout(a.nkc);
+  TcLayout L = tc_layout(a.nkc);
+  if (a.dbg >> 12) L.n_wst = min(L.n_wst, static_cast<uint32_t>(a.dbg >> 12));  // experiment: fewer W stages
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* Asm = base;                // [n_abuf][nkc][2][16 KB]
   uint8_t* Wsm = base + L.a_bytes;    // [n_wst][2][16 KB]
@@ -697,13 +698,16 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
           mbar_wait_t(&bar_accempty[acc], accph ^ 1u, (prof && lane == 0) ? &pw[3] : nullptr);
           tc_after();
           const uint32_t dt = tmem_base + acc * 128u;
-          for (uint32_t kc = 0; kc < a.nkc; ++kc) {
-            mbar_wait_t(&bar_wfull[s], wph, (prof && lane == 0) ? &pw[4] : nullptr);
-            tc_after();
-            const long long pi0 = prof ? clock64() : 0;
-            const uint32_t b_hi = w_base + s * 2u * kBlockBytes;
-            const uint64_t dbh = sw128_desc(b_hi), dbl = sw128_desc(b_hi + kBlockBytes);
-            if (elect_one()) {
+          // one elected burst per direction tile: the issuing lane waits for
+          // each stage itself (no warp-wide syncs between the MMA groups, so
+          // the tensor queue is refilled without gaps)
+          const long long pi0 = prof ? clock64() : 0;
+          if (elect_one()) {
+            uint32_t ss = s, ph = wph;
+            for (uint32_t kc = 0; kc < a.nkc; ++kc) {
+              mbar_wait(&bar_wfull[ss], ph);
+              const uint32_t b_hi = w_base + ss * 2u * kBlockBytes;
+              const uint64_t dbh = sw128_desc(b_hi), dbl = sw128_desc(b_hi + kBlockBytes);
               if (!(a.dbg & 2)) {
 #pragma unroll
                 for (uint32_t kk = 0; kk < 4; ++kk) {
@@ -715,22 +719,26 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
                 }
               }
               if (kCluster == 1)
-                mma_commit(&bar_wempty[s]);
+                mma_commit(&bar_wempty[ss]);
               else
-                mma_commit_mc(&bar_wempty[s], cmask);
+                mma_commit_mc(&bar_wempty[ss], cmask);
+              if (++ss == L.n_wst) {
+                ss = 0;
+                ph ^= 1u;
+              }
             }
-            __syncwarp();
-            if (prof) {
-              pmi += static_cast<unsigned long long>(clock64() - pi0);
-              ++pmn;
-            }
+            mma_commit(&bar_accfull[acc]);
+          }
+          __syncwarp();
+          for (uint32_t kc = 0; kc < a.nkc; ++kc)
             if (++s == L.n_wst) {
               s = 0;
               wph ^= 1u;
             }
+          if (prof) {
+            pmi += static_cast<unsigned long long>(clock64() - pi0);
+            pmn += a.nkc;
           }
-          if (elect_one()) mma_commit(&bar_accfull[acc]);
-          __syncwarp();
           if (++acc == nacc) {
             acc = 0;
             accph ^= 1u;

@@ -7,6 +7,10 @@
 //   bit 2: A columns / hi-lo operands vary like the kernel's fp16x3 split
 //   bit 3: B descriptor rotates over 4 shared-memory stages (32 KB apart)
 //   bit 4: random operand data instead of zeros
+//   bit 5: stage ring: the MMA warp waits on a full barrier per 12 MMAs and
+//          commits an empty barrier; a producer warp re-arms (4 stages)
+//   bit 6: the producer also bulk-copies 32 KB from global into the stage
+//   bit 7: whole warp walks the MMA loop (elect + __syncwarp), as the kernel
 // Prints cycles per MMA for each mode.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -23,11 +27,22 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint3
                "r"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
-__global__ void mma_pattern(int n_tiles, int mode, unsigned long long* out) {
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile("{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(
+                   smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+               : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+
+__global__ void mma_pattern(int n_tiles, int mode, const uint8_t* gsrc, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint32_t tbase;
-  __shared__ __align__(8) uint64_t bar, cbar;
+  __shared__ __align__(8) uint64_t bar, cbar, full[4], empty[4];
   if (threadIdx.x < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tbase)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -41,6 +56,10 @@ __global__ void mma_pattern(int n_tiles, int mode, unsigned long long* out) {
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&cbar)));
+    for (int i = 0; i < 4; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[i])));
+    }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("fence.proxy.async.shared::cta;");
@@ -56,18 +75,37 @@ __global__ void mma_pattern(int n_tiles, int mode, unsigned long long* out) {
                    "l"(sw128_desc(smem_u32(sm) + (kk & 3) * 32u + (kk >> 2) * 16384u)));
   }
   long long t0 = 0, t1 = 0;
+  if ((mode & 32) && threadIdx.x == 32) {
+    uint32_t s = 0, ph = 0;
+    for (int g = 0; g < n_tiles * 2; ++g) {
+      while (!mbar_try(&empty[s], ph ^ 1u)) __nanosleep(64);
+      if (mode & 64) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])), "r"(32768));
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(sm + 32768u * s)), "l"(gsrc + (static_cast<size_t>(g % 64) << 15)), "r"(32768),
+                     "r"(smem_u32(&full[s])) : "memory");
+      } else {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])));
+      }
+      if (++s == 4) { s = 0; ph ^= 1u; }
+    }
+  }
   if (threadIdx.x < 32) {
     t0 = clock64();
     uint32_t pred = 0;
     asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(pred));
-    if (pred) {
-      uint32_t s = 0;
+    if ((mode & 128) || pred) {
+      uint32_t s = 0, ph = 0;
       for (int tile = 0; tile < n_tiles; ++tile) {
         const uint32_t acc = (mode & 2) ? static_cast<uint32_t>(tile % 3) : 0u;
         const uint32_t dt = t + acc * 128u;
         for (uint32_t kc = 0; kc < 2; ++kc) {
+          if (mode & 32) mbar_wait(&full[s], ph);
+          uint32_t e = 1;
+          if (mode & 128) asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(e));
           const uint32_t bs = (mode & 8) ? s : 0u;
           const uint64_t dbh = sw128_desc(smem_u32(sm) + 32768u * bs), dbl = sw128_desc(smem_u32(sm) + 32768u * bs + 16384u);
+          if (e)
           for (uint32_t kk = 0; kk < 4; ++kk) {
             const uint32_t acol = (mode & 4) ? (kc * 4u + kk) * 8u : 0u;
             const uint32_t ahi = t + 384u + acol, alo = (mode & 4) ? ahi + 64u : ahi;
@@ -77,12 +115,17 @@ __global__ void mma_pattern(int n_tiles, int mode, unsigned long long* out) {
             mma_ts(dt, alo, dbh + off, idesc, 1u);
             mma_ts(dt, ahi, (mode & 4) ? dbl + off : dbh + off, idesc, 1u);
           }
-          if (mode & 1)
+          if ((mode & 1) && e)
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&cbar)));
+          if ((mode & 32) && e)
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&empty[s])));
+          if (mode & 128) __syncwarp();
           s = (s + 1) & 3u;
+          if (s == 0) ph ^= 1u;
         }
       }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
+      if (!(mode & 128) || pred)
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
     }
     __syncwarp();
     asm volatile("{\n.reg .pred p;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra W;\n}\n" ::"r"(smem_u32(&bar)));
@@ -100,12 +143,15 @@ int main() {
   cudaFuncSetAttribute(mma_pattern, cudaFuncAttributeMaxDynamicSharedMemorySize, 130 * 1024);
   unsigned long long* d;
   cudaMalloc(&d, 8);
+  uint8_t* src;
+  cudaMalloc(&src, 64 << 15);
+  cudaMemset(src, 0, 64 << 15);
   const int n_tiles = 2000;  // x 24 MMAs
-  for (int mode : {0, 1, 2, 4, 8, 16, 3, 7, 15, 31}) {
+  for (int mode : {0, 16, 15, 31, 15 | 32, 31 | 32, 15 | 32 | 64 | 128, 31 | 32 | 64 | 128, 0, 31}) {
     double per = 0;
     for (int rep = 0; rep < 2; ++rep) {
       cudaMemset(d, 0, 8);
-      mma_pattern<<<sms, 128, 130 * 1024>>>(n_tiles, mode, d);
+      mma_pattern<<<sms, 128, 130 * 1024>>>(n_tiles, mode, src, d);
       cudaDeviceSynchronize();
       unsigned long long cyc = 0;
       cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
