@@ -35,7 +35,13 @@ constexpr int kRows = 128;                 // points per tile (MMA M)
 constexpr int kChunk = 64;                 // K elements per chunk (128 B of fp16)
 constexpr int kBlockBytes = kRows * 128;   // one 128 x 64 fp16 block = 16 KB
 constexpr int kAccBufs = 3;                // max TMEM accumulators (x 128 columns)
-constexpr int kMaxWStages = 6;
+constexpr int kMaxWStages = 12;
+#ifndef ACE_TESTWAIT
+#define ACE_TESTWAIT 0
+#endif
+#ifndef ACE_WATCHDOG
+#define ACE_WATCHDOG 0
+#endif
 #ifndef ACE_SLEEPY
 #define ACE_SLEEPY 64  // ns back-off of off-critical-path barrier waits (0: spin)
 #endif
@@ -48,7 +54,14 @@ constexpr int kMaxWStages = 6;
 constexpr int kThreads = ACE_RW ? 384 : 320;  // producer, MMA, 8 epilogue warps, 2 recheck warps
 constexpr uint32_t kTail = ACE_RW ? 320 : 256;  // epilogue + recheck threads
 constexpr size_t kSmemLimit = 232448;      // 227 KB per CTA
-constexpr uint32_t kCluster = 1;           // CTAs sharing each W stage (TMA multicast)
+#ifndef ACE_PAIR
+#define ACE_PAIR 1
+#endif
+// CTA pair (cta_group::2): the two CTAs of a cluster run M = 256 MMAs issued
+// by the leader; each holds its own 128 points (A, accumulators) and half of
+// every W tile (64 directions), so MMA instructions and W bytes per point halve.
+constexpr uint32_t kPair = ACE_PAIR;
+constexpr uint32_t kCluster = kPair;
 
 struct TcLayout {
   uint32_t nkc, n_abuf, n_wst;
@@ -67,10 +80,10 @@ __host__ __device__ inline TcLayout tc_layout(uint32_t nkc) {
   L.n_abuf = 1;
   L.a_bytes = static_cast<size_t>(L.n_abuf) * nkc * 2 * kBlockBytes;
   const size_t room = kSmemLimit - 8192 - 1024 - L.a_bytes;  // static smem (barriers, sign words) + align
-  size_t st = room / (2 * kBlockBytes);
+  size_t st = room / (2 * kBlockBytes / kPair);  // a stage: hi + lo of this CTA's share of a W tile
   if (st > kMaxWStages) st = kMaxWStages;
   L.n_wst = static_cast<uint32_t>(st);
-  L.w_bytes = static_cast<size_t>(L.n_wst) * 2 * kBlockBytes;
+  L.w_bytes = static_cast<size_t>(L.n_wst) * 2 * kBlockBytes / kPair;
   L.total = L.a_bytes + L.w_bytes + 1024;
   return L;
 }
@@ -90,7 +103,29 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity);
+// Spin until the phase with `parity` completes.  With ACE_WATCHDOG a wait
+// longer than ~2^34 cycles (several seconds, a broken protocol) traps instead
+// of hanging the GPU (development builds).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if ACE_WATCHDOG
+  if (mbar_try(bar, parity)) return;
+  const long long t0 = clock64();
+  uint32_t n = 0;
+  while (!mbar_try(bar, parity))
+    if ((++n & 1023u) == 0 && clock64() - t0 > (1ll << 34)) __trap();
+#elif ACE_TESTWAIT
+  // non-suspending poll: the waiter sees the phase flip without a wake-up delay
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+#else
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -100,6 +135,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+#endif
 }
 // Wait for warps off the critical MMA path: back off between polls so the
 // polling does not compete with the tensor pipe for shared memory.
@@ -118,8 +154,12 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
 }
 __device__ __forceinline__ void mbar_wait_sleepy(uint64_t* bar, uint32_t parity, unsigned long long* acc) {
 #if ACE_SLEEPY
-  const long long t0 = acc ? clock64() : 0;
-  while (!mbar_try(bar, parity)) __nanosleep(ACE_SLEEPY);
+  const long long t0 = (acc || ACE_WATCHDOG) ? clock64() : 0;
+  uint32_t n = 0;
+  while (!mbar_try(bar, parity)) {
+    __nanosleep(ACE_SLEEPY);
+    if (ACE_WATCHDOG && (++n & 255u) == 0 && clock64() - t0 > (1ll << 34)) __trap();
+  }
   if (acc) *acc += static_cast<unsigned long long>(clock64() - t0);
 #else
   if (acc) {
@@ -147,21 +187,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s_mc(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                            uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
-      "%4;" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
-      : "memory");
-}
-__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "h"(mask)
       : "memory");
 }
 __device__ __forceinline__ bool elect_one() {
@@ -205,22 +230,18 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 }
 
 // kind::f16 instruction descriptor: A,B fp16 K-major, D fp32, M=128, N=n.
+// M = 128 per CTA (256 for the pair)
 __device__ __forceinline__ uint32_t idesc_f16(uint32_t n) {
-  return (1u << 4) | ((n >> 3) << 17) | ((128u >> 4) << 24);
+  return (1u << 4) | ((n >> 3) << 17) | (((128u * kPair) >> 4) << 24);
 }
 
-__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
-                                        uint32_t accumulate) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
-}
 __device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+#if ACE_PAIR == 2
+  // each CTA of the pair: its own shared memory -> its own TMEM, same addresses
+  asm volatile("tcgen05.cp.cta_group::2.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc));
+#else
   asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc));
+#endif
 }
 __device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
                                            uint32_t accumulate) {
@@ -228,14 +249,39 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uin
       "{\n"
       ".reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
+#if ACE_PAIR == 2
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n"
+#else
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+#endif
       "}\n" ::"r"(tmem_d),
       "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate));
 }
+// Commit: the barrier at this offset in every CTA of the pair gets one arrival
+// once all earlier tcgen05 operations of the issuing thread have completed.
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
+#if ACE_PAIR == 2
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+#else
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
                : "memory");
+#endif
+}
+// Arrive on the barrier at the same offset in CTA `rank` of the cluster.
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+  asm volatile(
+      "{\n"
+      ".reg .b32 ra;\n"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(rank)
+      : "memory");
 }
 
 #define ACE_TMEM_LD32(taddr, v)                                                                    \
@@ -578,36 +624,47 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
     tiles_done = 0;
     min_next = ACE_RW ? 0xffffffffu : 0u;
     blk_rech = blk_flip = 0;
+    // the leader's full barriers also wait for the peer's forwarded arrival,
+    // its accumulator-empty barriers for the peer's epilogue warps
+    const uint32_t fulls = (kPair == 2 && cluster_ctarank() == 0) ? 2u : 1u;
     for (uint32_t s = 0; s < L.n_wst; ++s) {
-      mbar_init(&bar_wfull[s], 1);
-      mbar_init(&bar_wempty[s], kCluster);  // every CTA's MMA must have released the stage
+      mbar_init(&bar_wfull[s], fulls);
+      mbar_init(&bar_wempty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&bar_afull[b], 1);
+      mbar_init(&bar_afull[b], fulls);
       mbar_init(&bar_aempty[b], 1);
     }
     for (int b = 0; b < kAccBufs; ++b) {
       mbar_init(&bar_accfull[b], 1);
-      mbar_init(&bar_accempty[b], 4);  // one epilogue warp per lane quarter
+      mbar_init(&bar_accempty[b], 4 * kPair);  // one epilogue warp per lane quarter, per CTA
     }
     fence_mbar_init();
   }
   if (warp == 1) {
+#if ACE_PAIR == 2
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+#else
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
                  "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+#endif
   }
   tc_before();
   __syncthreads();
   cluster_sync_all();  // remote CTAs may signal our barriers from here on
   tc_after();
   const uint32_t tmem_base = tmem_base_sh;
-  const uint32_t crank = cluster_ctarank();
-  const uint16_t cmask = static_cast<uint16_t>((1u << kCluster) - 1u);
-  // every CTA runs the same number of tile iterations (tiles past the end are
-  // skipped by the epilogue) so a cluster's shared W pipeline stays in lockstep
+  // Tile schedule: pair P (of npairs) takes tile groups P, P + npairs, ...;
+  // CTA `rank` of the pair takes tile kPair*group + rank.  Every CTA runs the
+  // same number of iterations (tiles past the end are skipped by the
+  // epilogue) so the pair's shared pipeline stays in lockstep.
+  const uint32_t rank = kPair == 2 ? cluster_ctarank() : 0u;
+  const uint32_t npairs = gridDim.x / kPair, pair = blockIdx.x / kPair;
   const uint64_t iters = (n_tiles + gridDim.x - 1) / gridDim.x;
-  const uint64_t t_end = static_cast<uint64_t>(blockIdx.x) + iters * gridDim.x;
+  auto tile_of = [&](uint64_t it) -> uint64_t { return (pair + it * npairs) * kPair + rank; };
   // instrumentation (a.prof != null): cycles waiting per barrier kind, per CTA:
   // [0] prod a_empty [1] prod w_empty [2] mma a_full [3] mma acc_empty
   // [4] mma w_full [5] epilogue acc_full (warp 2..5 lane 0 summed) [6] total
@@ -621,39 +678,28 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
 
   if (warp == 0) {
     // ---------------- producer: A tile (once per tile) + W stages ----------------
+    // A: this CTA's own 128 points.  W: this CTA's share of each direction
+    // tile (rows [64 rank, 64 rank + 64) of the hi and lo blocks in pair mode).
     if (lane == 0) {
-      uint32_t s = 0, ph = 0, it = 0;
-      for (uint64_t t = blockIdx.x; t < t_end; t += gridDim.x, ++it) {
-        mbar_wait_sleepy(&bar_aempty[0], (it & 1u) ^ 1u, prof ? &pw[0] : nullptr);
+      uint32_t s = 0, ph = 0;
+      const uint32_t share = kBlockBytes / kPair, half = share;  // bytes of one block per CTA
+      for (uint64_t it = 0; it < iters; ++it) {
+        const uint64_t t = tile_of(it);
+        mbar_wait_sleepy(&bar_aempty[0], (static_cast<uint32_t>(it) & 1u) ^ 1u, prof ? &pw[0] : nullptr);
         const uint64_t tt = t < n_tiles ? t : n_tiles - 1;  // past the end: reload the last tile
         mbar_expect_tx(&bar_afull[0], a_tile_bytes);
         bulk_g2s(Asm, reinterpret_cast<const uint8_t*>(a.x16) + tt * a_tile_bytes, a_tile_bytes, &bar_afull[0]);
         for (uint32_t j = 0; j < a.ntiles; ++j) {
-          const uint32_t nmma = (min(128u, R - j * 128u) + 15u) & ~15u;
-          const uint32_t bytes = nmma * 128u;
-          const uint32_t part = bytes / kCluster;  // this CTA's slice, multicast to the cluster
+          const uint32_t nmma = kPair == 2 ? 128u : ((min(128u, R - j * 128u) + 15u) & ~15u);
+          const uint32_t bytes = kPair == 2 ? share : nmma * 128u;
           for (uint32_t kc = 0; kc < a.nkc; ++kc) {
             mbar_wait_sleepy(&bar_wempty[s], ph ^ 1u, prof ? &pw[1] : nullptr);
-            if ((a.dbg & 8) && it > 0) {  // experiment: W loaded for the first tile only
-              mbar_arrive(&bar_wfull[s]);
-              if (++s == L.n_wst) {
-                s = 0;
-                ph ^= 1u;
-              }
-              continue;
-            }
             mbar_expect_tx(&bar_wfull[s], 2u * bytes);
-            const uint8_t* src =
-                reinterpret_cast<const uint8_t*>(a.w16) + (static_cast<uint64_t>(j) * a.nkc + kc) * 2u * kBlockBytes;
-            uint8_t* dst = Wsm + static_cast<size_t>(s) * 2 * kBlockBytes;
-            if (kCluster == 1) {
-              bulk_g2s(dst, src, bytes, &bar_wfull[s]);
-              bulk_g2s(dst + kBlockBytes, src + kBlockBytes, bytes, &bar_wfull[s]);
-            } else {
-              const uint32_t o = crank * part;
-              bulk_g2s_mc(dst + o, src + o, part, &bar_wfull[s], cmask);
-              bulk_g2s_mc(dst + kBlockBytes + o, src + kBlockBytes + o, part, &bar_wfull[s], cmask);
-            }
+            const uint8_t* src = reinterpret_cast<const uint8_t*>(a.w16) +
+                                 (static_cast<uint64_t>(j) * a.nkc + kc) * 2u * kBlockBytes + rank * share;
+            uint8_t* dst = Wsm + static_cast<size_t>(s) * 2u * half;
+            bulk_g2s(dst, src, bytes, &bar_wfull[s]);
+            bulk_g2s(dst + half, src + kBlockBytes, bytes, &bar_wfull[s]);
             if (++s == L.n_wst) {
               s = 0;
               ph ^= 1u;
@@ -662,25 +708,48 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
         }
       }
     }
+  } else if (warp == 1 && rank != 0) {
+    // ---------------- pair peer: forward stage arrivals to the leader ----------------
+    // The leader's MMAs read this CTA's A tile and W shares too: once a local
+    // copy has landed, arrive on the leader's barrier at the same offset.
+    if (lane == 0) {
+      uint32_t s = 0, wph = 0;
+      for (uint64_t it = 0; it < iters; ++it) {
+        mbar_wait(&bar_afull[0], static_cast<uint32_t>(it) & 1u);
+        mbar_arrive_remote(&bar_afull[0], 0);
+        for (uint32_t j = 0; j < a.ntiles; ++j)
+          for (uint32_t kc = 0; kc < a.nkc; ++kc) {
+            mbar_wait(&bar_wfull[s], wph);
+            mbar_arrive_remote(&bar_wfull[s], 0);
+            if (++s == L.n_wst) {
+              s = 0;
+              wph ^= 1u;
+            }
+          }
+      }
+    }
+    __syncwarp();
   } else if (warp == 1) {
     // ---------------- MMA issuer: A smem -> TMEM (tcgen05.cp), then TS MMAs ----------------
     // The whole warp walks the schedule (operands stay warp-uniform, so the
-    // descriptors live in uniform registers); one elected lane issues.
+    // descriptors live in uniform registers); one elected lane issues.  In
+    // pair mode this is the leader, its MMAs and copies cover both CTAs.
     {
-      uint32_t s = 0, wph = 0, acc = 0, accph = 0, it = 0;
+      uint32_t s = 0, wph = 0, acc = 0, accph = 0;
       unsigned long long pmi = 0, pmn = 0, pcp = 0;  // instrumentation: MMA-group issue cycles / groups, A copies
       const long long ploop = clock64();
       const uint32_t nacc = tc_acc_bufs(a.nkc);
       const uint32_t ta_hi = tmem_base + nacc * 128u, ta_lo = ta_hi + a.nkc * 32u;  // dpad/2 columns each
       const uint32_t a_base = smem_u32(Asm), w_base = smem_u32(Wsm);
-      for (uint64_t t = blockIdx.x; t < t_end; t += gridDim.x, ++it) {
-        mbar_wait_t(&bar_afull[0], it & 1u, (prof && lane == 0) ? &pw[2] : nullptr);
+      const uint32_t half = kBlockBytes / kPair;  // bytes of one W block (hi or lo) per CTA
+      for (uint64_t it = 0; it < iters; ++it) {
+        mbar_wait_t(&bar_afull[0], static_cast<uint32_t>(it) & 1u, (prof && lane == 0) ? &pw[2] : nullptr);
         tc_after();
         const long long pc0 = prof ? clock64() : 0;
         // copies execute in issue order after this CTA's earlier MMAs, so the
         // previous tile's reads of TMEM A are complete before it is replaced
         if (elect_one()) {
-          for (uint32_t kc = 0; kc < ((a.dbg & 512) && it > 0 ? 0u : a.nkc); ++kc) {  // 512: experiment, A once
+          for (uint32_t kc = 0; kc < a.nkc; ++kc) {
             const uint32_t ah = a_base + kc * 2u * kBlockBytes;
 #pragma unroll
             for (uint32_t kk = 0; kk < 4; ++kk) {
@@ -693,7 +762,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
         __syncwarp();
         if (prof) pcp += static_cast<unsigned long long>(clock64() - pc0);
         for (uint32_t j = 0; j < a.ntiles; ++j) {
-          const uint32_t nmma = (min(128u, R - j * 128u) + 15u) & ~15u;
+          const uint32_t nmma = kPair == 2 ? 128u : ((min(128u, R - j * 128u) + 15u) & ~15u);
           const uint32_t idesc = idesc_f16(nmma);
           mbar_wait_t(&bar_accempty[acc], accph ^ 1u, (prof && lane == 0) ? &pw[3] : nullptr);
           tc_after();
@@ -706,8 +775,8 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
             uint32_t ss = s, ph = wph;
             for (uint32_t kc = 0; kc < a.nkc; ++kc) {
               mbar_wait(&bar_wfull[ss], ph);
-              const uint32_t b_hi = w_base + ss * 2u * kBlockBytes;
-              const uint64_t dbh = sw128_desc(b_hi), dbl = sw128_desc(b_hi + kBlockBytes);
+              const uint32_t b_hi = w_base + ss * 2u * half;
+              const uint64_t dbh = sw128_desc(b_hi), dbl = sw128_desc(b_hi + half);
               if (!(a.dbg & 2)) {
 #pragma unroll
                 for (uint32_t kk = 0; kk < 4; ++kk) {
@@ -718,10 +787,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
                   mma_f16_ts(dt, ta_hi + acol, dbl + off, idesc, 1u);
                 }
               }
-              if (kCluster == 1)
-                mma_commit(&bar_wempty[ss]);
-              else
-                mma_commit_mc(&bar_wempty[ss], cmask);
+              mma_commit(&bar_wempty[ss]);
               if (++ss == L.n_wst) {
                 ss = 0;
                 ph ^= 1u;
@@ -775,7 +841,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
         }
         if (item == ~0ull) break;
         const uint64_t row = item >> 32;
-        const uint32_t it = static_cast<uint32_t>(((row >> 7) - blockIdx.x) / gridDim.x);
+        const uint32_t it = static_cast<uint32_t>(((row >> 7) / kPair - pair) / npairs);  // inverse of tile_of
         while (*reinterpret_cast<volatile uint32_t*>(&tiles_done) < 8u * (it + 1u)) __nanosleep(128);
         __threadfence_block();
         const uint32_t dir = static_cast<uint32_t>(item & 0xffffffffu);
@@ -823,7 +889,8 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
     uint32_t acc = 0, accph = 0;
     uint64_t g = 0;
     long long pc_ext = 0;
-    for (uint64_t t = blockIdx.x; t < t_end; t += gridDim.x) {
+    for (uint64_t it = 0; it < iters; ++it) {
+      const uint64_t t = tile_of(it);
       const uint64_t row = t * kRows + r;
       const bool valid = row < a.n;
       const float thr = valid ? a.rowthr[row] : -1.0f;
@@ -893,7 +960,12 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
           tc_before();
           __syncwarp();
           if (prof) pc2 = clock64();
-          if (lane == 0) mbar_arrive(&bar_accempty[acc]);
+          if (lane == 0) {
+            if (rank == 0)
+              mbar_arrive(&bar_accempty[acc]);
+            else
+              mbar_arrive_remote(&bar_accempty[acc], 0);  // the leader's MMA reuses our accumulator too
+          }
           // last word of the previous tile (partner warp), for a straddling table
           uint32_t prev = 0u;
           if (g > 0) {
@@ -999,8 +1071,13 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
   __syncthreads();
   cluster_sync_all();  // no CTA leaves while its peers may still multicast into it
   tc_after();
-  if (warp == 1)
+  if (warp == 1) {
+#if ACE_PAIR == 2
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+#else
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+#endif
+  }
 }
 
 // ---- near-tie recheck ------------------------------------------------------------
