@@ -265,8 +265,18 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
       t.prof = prof;
       g_tc_prof = prof;
     }
+    // X conversion inside the projection kernel (opt-in, ACE_FUSE_CONVERT=1:
+    // two converter warps per CTA are slower than the pre-pass on cfg 2/3,
+    // 0.60 vs 0.27 + 0.11 ms) when the rows are plain contiguous fp32
+    static int fuse_env = -2;
+    if (fuse_env == -2) {
+      const char* e = getenv("ACE_FUSE_CONVERT");
+      fuse_env = e ? atoi(e) : 0;
+    }
+    t.fuse_convert = fuse_env != 0 && !t.x_f64 && ld == f->d.dim && (reinterpret_cast<uintptr_t>(xd) & 15) == 0 &&
+                     tc_fuse_ok_dim(f->d.dim, f->tc.nkc);
     sk->mark(4);
-    ACE_CUDA(launch_convert_x(t, sk->stream));
+    if (!t.fuse_convert) ACE_CUDA(launch_convert_x(t, sk->stream));
     sk->mark(6);
     // Fused epilogue insert (global REDs) only where the separate insert would
     // use global atomics too (K > 20); otherwise the shared-memory histogram

@@ -65,26 +65,27 @@ constexpr uint32_t kCluster = kPair;
 
 struct TcLayout {
   uint32_t nkc, n_abuf, n_wst;
-  size_t a_bytes, w_bytes, total;
+  size_t a_bytes, raw_bytes, w_bytes, total;
 };
 
-// Shared memory: one A tile (x, fp16 hi | lo, SW128 image from the pre-pass;
-// released as soon as tcgen05.cp has moved it into TMEM), then a ring of W
-// stages (32 KB each).  TMEM: accumulators of 128 columns, then the A operand
-// (hi | lo, 2 fp16 per column, dpad columns).
+// Shared memory: one A tile (x, fp16 hi | lo, SW128 image; released as soon as
+// tcgen05.cp has moved it into TMEM), with the fused conversion a raw fp32 X
+// tile (128 rows, bulk-copied), then a ring of W stages (32 KB each).  TMEM:
+// accumulators of 128 columns, then the A operand (hi | lo, dpad columns).
 __host__ __device__ inline uint32_t tc_acc_bufs(uint32_t nkc) { return nkc <= 2 ? 3u : 2u; }
 
-__host__ __device__ inline TcLayout tc_layout(uint32_t nkc) {
+__host__ __device__ inline TcLayout tc_layout(uint32_t nkc, uint64_t dim = 0, bool fuse = false) {
   TcLayout L;
   L.nkc = nkc;
   L.n_abuf = 1;
   L.a_bytes = static_cast<size_t>(L.n_abuf) * nkc * 2 * kBlockBytes;
-  const size_t room = kSmemLimit - 8192 - 1024 - L.a_bytes;  // static smem (barriers, sign words) + align
+  L.raw_bytes = fuse ? (static_cast<size_t>(kRows) * dim * 4 + 1023) / 1024 * 1024 : 0;
+  const size_t room = kSmemLimit - 8192 - 1024 - L.a_bytes - L.raw_bytes;  // static smem + align
   size_t st = room / (2 * kBlockBytes / kPair);  // a stage: hi + lo of this CTA's share of a W tile
   if (st > kMaxWStages) st = kMaxWStages;
   L.n_wst = static_cast<uint32_t>(st);
   L.w_bytes = static_cast<size_t>(L.n_wst) * 2 * kBlockBytes / kPair;
-  L.total = L.a_bytes + L.w_bytes + 1024;
+  L.total = L.a_bytes + L.raw_bytes + L.w_bytes + 1024;
   return L;
 }
 
@@ -366,13 +367,72 @@ __device__ __forceinline__ float load_x(const TcArgs& a, uint64_t row, uint64_t 
   return static_cast<const float*>(a.x)[row * a.ld + k];
 }
 
-// Eight lanes per row (four rows per warp, values held in registers): max |x|
-// (NaN > inf > finite as magnitude bits), power-of-two scale to [2^14, 2^15),
-// fp16 hi + lo split written straight into the SW128 K-major shared-memory
-// image of its 128-row tile, and the row's error threshold
-// thr = c * ||x~|| * 2^14 + abs (-1: exact zero row, +inf: recheck all).
-// Lane l8 of a row owns K elements 32g + 4*l8 .. +3 (coalesced 128 B per
-// group).  Rows past n (tile padding) are written as zeros.
+// One row, eight lanes (l8) holding its values v[g][e] = x[32 g + 4 l8 + e]:
+// max |x| (NaN > inf > finite as magnitude bits), power-of-two scale to
+// [2^14, 2^15), fp16 hi + lo split written into the SW128 K-major image of
+// the row's 128-row tile (`tile`: [kc][hi | lo][16 KB]), and the row's error
+// threshold thr = c * ||x~|| * 2^14 + abs (-1: exact zero row or padding,
+// +inf: recheck every projection).
+__device__ __forceinline__ void convert_row(float (&v)[8][4], uint32_t l8, bool live, uint32_t groups, uint32_t nkc,
+                                            uint64_t dim, float margin_c, uint8_t* tile, uint32_t r, float* thr_dst) {
+  uint32_t mb = 0u;
+#pragma unroll
+  for (uint32_t g = 0; g < 8; ++g)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) mb = max(mb, __float_as_uint(v[g][e]) & 0x7fffffffu);
+  mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, 1));
+  mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, 2));
+  mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, 4));
+  const bool nan = mb > 0x7f800000u;
+  const float m = __uint_as_float(nan ? 0x7f800000u : mb);
+  const bool zero = (m == 0.0f);
+  const bool wild = nan || !(m < 0x1.0p100f) || (!zero && m < 0x1.0p-100f);
+  float scale = 0.0f;
+  if (live && !zero && !wild) {
+    const int e = static_cast<int>((__float_as_uint(m) >> 23) & 0xffu) - 127;
+    scale = __uint_as_float(static_cast<uint32_t>(127 + 14 - e) << 23);
+  }
+  float ss = 0.0f;
+#pragma unroll
+  for (uint32_t g = 0; g < 8; ++g) {
+    if (g >= groups) continue;
+    const uint32_t k0 = g * 32u + l8 * 4u;
+    const uint32_t kc = k0 / kChunk, kk = k0 % kChunk;
+    uint32_t hi[2], lo[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float x0 = v[g][2 * i] * scale, x1 = v[g][2 * i + 1] * scale;
+      ss = fmaf(x0, x0, fmaf(x1, x1, ss));
+      const float h0 = __half2float(__float2half_rn(x0)), h1 = __half2float(__float2half_rn(x1));
+      hi[i] = pack_h2(h0, h1);
+      lo[i] = pack_h2(x0 - h0, x1 - h1);
+    }
+    uint8_t* blk = tile + kc * 2u * kBlockBytes;
+    const uint32_t off = sw128_off(r, kk);
+    *reinterpret_cast<uint2*>(blk + off) = make_uint2(hi[0], hi[1]);
+    *reinterpret_cast<uint2*>(blk + kBlockBytes + off) = make_uint2(lo[0], lo[1]);
+  }
+  ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+  ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+  ss += __shfl_xor_sync(0xffffffffu, ss, 4);
+  if (l8 == 0) {
+    float thr;
+    if (!live || zero) {
+      thr = -1.0f;
+    } else if (wild) {
+      thr = __int_as_float(0x7f800000);
+    } else {
+      const float nx = sqrtf(ss * (1.0f + static_cast<float>(dim + 4) * 0x1.0p-23f)) * (1.0f + 0x1.0p-20f);
+      thr = margin_c * nx * 16384.0f + static_cast<float>(dim) * 0x1.0p-10f;
+    }
+    *thr_dst = thr;
+  }
+}
+
+// Pre-pass: eight lanes per row (four rows per warp, values in registers),
+// the SW128 image and thresholds written to global memory.  Lane l8 of a row
+// owns K elements 32g + 4*l8 .. +3 (coalesced 128 B per group).  Rows past n
+// (tile padding) are written as zeros.
 __global__ void __launch_bounds__(256) convert_x_kernel(const TcArgs a, uint64_t rows_padded) {
   const uint32_t lane = threadIdx.x & 31, l8 = lane & 7;
   const uint64_t slots = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 3);
@@ -383,7 +443,6 @@ __global__ void __launch_bounds__(256) convert_x_kernel(const TcArgs a, uint64_t
     const bool inb = row < rows_padded;
     const bool live = row < a.n;
     float v[8][4];
-    uint32_t mb = 0u;
 #pragma unroll
     for (uint32_t g = 0; g < 8; ++g) {
       const uint64_t k0 = g * 32u + l8 * 4u;
@@ -400,58 +459,12 @@ __global__ void __launch_bounds__(256) convert_x_kernel(const TcArgs a, uint64_t
           for (int e = 0; e < 4; ++e) v[g][e] = load_x(a, row, k0 + e);
         }
       }
-#pragma unroll
-      for (int e = 0; e < 4; ++e) mb = max(mb, __float_as_uint(v[g][e]) & 0x7fffffffu);
     }
-    mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, 1));
-    mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, 2));
-    mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, 4));
-    const bool nan = mb > 0x7f800000u;
-    const float m = __uint_as_float(nan ? 0x7f800000u : mb);
-    const bool zero = (m == 0.0f);
-    const bool wild = nan || !(m < 0x1.0p100f) || (!zero && m < 0x1.0p-100f);
-    float scale = 0.0f;
-    if (live && !zero && !wild) {
-      const int e = static_cast<int>((__float_as_uint(m) >> 23) & 0xffu) - 127;
-      scale = __uint_as_float(static_cast<uint32_t>(127 + 14 - e) << 23);
-    }
+    if (!inb) continue;  // (row-uniform per 8-lane group; shuffles stay within the group)
     const uint64_t tile = row / kRows;
-    const uint32_t r = static_cast<uint32_t>(row % kRows);
-    float ss = 0.0f;
-#pragma unroll
-    for (uint32_t g = 0; g < 8; ++g) {
-      if (g >= groups || !inb) continue;
-      const uint32_t k0 = g * 32u + l8 * 4u;
-      const uint32_t kc = k0 / kChunk, kk = k0 % kChunk;
-      uint32_t hi[2], lo[2];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const float x0 = v[g][2 * i] * scale, x1 = v[g][2 * i + 1] * scale;
-        ss = fmaf(x0, x0, fmaf(x1, x1, ss));
-        const float h0 = __half2float(__float2half_rn(x0)), h1 = __half2float(__float2half_rn(x1));
-        hi[i] = pack_h2(h0, h1);
-        lo[i] = pack_h2(x0 - h0, x1 - h1);
-      }
-      uint8_t* blk = reinterpret_cast<uint8_t*>(a.x16) + ((tile * a.nkc + kc) * 2) * kBlockBytes;
-      const uint32_t off = sw128_off(r, kk);
-      *reinterpret_cast<uint2*>(blk + off) = make_uint2(hi[0], hi[1]);
-      *reinterpret_cast<uint2*>(blk + kBlockBytes + off) = make_uint2(lo[0], lo[1]);
-    }
-    ss += __shfl_xor_sync(0xffffffffu, ss, 1);
-    ss += __shfl_xor_sync(0xffffffffu, ss, 2);
-    ss += __shfl_xor_sync(0xffffffffu, ss, 4);
-    if (l8 == 0 && inb) {
-      float thr;
-      if (!live || zero) {
-        thr = -1.0f;
-      } else if (wild) {
-        thr = __int_as_float(0x7f800000);
-      } else {
-        const float nx = sqrtf(ss * (1.0f + static_cast<float>(a.dim + 4) * 0x1.0p-23f)) * (1.0f + 0x1.0p-20f);
-        thr = a.margin_c * nx * 16384.0f + static_cast<float>(a.dim) * 0x1.0p-10f;
-      }
-      a.rowthr[row] = thr;
-    }
+    convert_row(v, l8, live, groups, a.nkc, a.dim, a.margin_c,
+                reinterpret_cast<uint8_t*>(a.x16) + tile * a.nkc * 2u * kBlockBytes, static_cast<uint32_t>(row % kRows),
+                &a.rowthr[row]);
   }
 }
 
@@ -595,6 +608,10 @@ __device__ __noinline__ void recheck_tail(const void* x, int x_f64, uint64_t ld,
 
 // ---- the projection kernel ----------------------------------------------------------
 
+// kFuse: X is converted inside the kernel (warps 10-11) from raw fp32 tiles
+// the producer bulk-copies, instead of by the convert_x_kernel pre-pass; the
+// near-tie recheck is then all done in the shared tail.
+template <bool kFuse>
 __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t bar_wfull[kMaxWStages], bar_wempty[kMaxWStages];
@@ -606,12 +623,15 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
   __shared__ uint32_t tiles_done;                   // epilogue warps x tiles completed (ids stored)
   __shared__ uint32_t min_next;                     // first list slot the recheck warps left over
   __shared__ unsigned long long blk_rech, blk_flip;
+  __shared__ __align__(8) uint64_t bar_rawfull, bar_rawempty, bar_thrfull[2], bar_threempty[2];
+  __shared__ float thr_sm[2][kRows];  // fused conversion: row thresholds per tile parity
 
-  TcLayout L = tc_layout(a.nkc);
+  TcLayout L = tc_layout(a.nkc, a.dim, kFuse);
   if (a.dbg >> 12) L.n_wst = min(L.n_wst, static_cast<uint32_t>(a.dbg >> 12));  // experiment: fewer W stages
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* Asm = base;                // [n_abuf][nkc][2][16 KB]
-  uint8_t* Wsm = base + L.a_bytes;    // [n_wst][2][16 KB]
+  uint8_t* Asm = base;                               // [n_abuf][nkc][2][16 KB]
+  uint8_t* Rsm = base + L.a_bytes;                   // fused: raw fp32 rows [128][dim]
+  uint8_t* Wsm = base + L.a_bytes + L.raw_bytes;     // [n_wst][2][16 KB / kPair]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t n_tiles = (a.n + kRows - 1) / kRows;
@@ -622,7 +642,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
   if (threadIdx.x == 0) {
     seg_n = 0;
     tiles_done = 0;
-    min_next = ACE_RW ? 0xffffffffu : 0u;
+    min_next = (ACE_RW && !kFuse) ? 0xffffffffu : 0u;
     blk_rech = blk_flip = 0;
     // the leader's full barriers also wait for the peer's forwarded arrival,
     // its accumulator-empty barriers for the peer's epilogue warps
@@ -632,9 +652,13 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
       mbar_init(&bar_wempty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&bar_afull[b], fulls);
+      mbar_init(&bar_afull[b], kFuse ? 2u : fulls);  // fused: the two converter warps
       mbar_init(&bar_aempty[b], 1);
+      mbar_init(&bar_thrfull[b], 2);
+      mbar_init(&bar_threempty[b], 8);
     }
+    mbar_init(&bar_rawfull, 1);
+    mbar_init(&bar_rawempty, 2);
     for (int b = 0; b < kAccBufs; ++b) {
       mbar_init(&bar_accfull[b], 1);
       mbar_init(&bar_accempty[b], 4 * kPair);  // one epilogue warp per lane quarter, per CTA
@@ -685,10 +709,24 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
       const uint32_t share = kBlockBytes / kPair, half = share;  // bytes of one block per CTA
       for (uint64_t it = 0; it < iters; ++it) {
         const uint64_t t = tile_of(it);
-        mbar_wait_sleepy(&bar_aempty[0], (static_cast<uint32_t>(it) & 1u) ^ 1u, prof ? &pw[0] : nullptr);
-        const uint64_t tt = t < n_tiles ? t : n_tiles - 1;  // past the end: reload the last tile
-        mbar_expect_tx(&bar_afull[0], a_tile_bytes);
-        bulk_g2s(Asm, reinterpret_cast<const uint8_t*>(a.x16) + tt * a_tile_bytes, a_tile_bytes, &bar_afull[0]);
+        if (kFuse) {
+          // raw fp32 rows of the tile (contiguous: ld == dim), converted by warps 10-11
+          mbar_wait_sleepy(&bar_rawempty, (static_cast<uint32_t>(it) & 1u) ^ 1u, prof ? &pw[0] : nullptr);
+          const uint64_t r0 = t * kRows;
+          const uint32_t rows = r0 < a.n ? static_cast<uint32_t>(a.n - r0 < kRows ? a.n - r0 : kRows) : 0u;
+          if (rows) {
+            const uint32_t bytes = rows * static_cast<uint32_t>(a.dim) * 4u;
+            mbar_expect_tx(&bar_rawfull, bytes);
+            bulk_g2s(Rsm, static_cast<const float*>(a.x) + r0 * a.dim, bytes, &bar_rawfull);
+          } else {
+            mbar_arrive(&bar_rawfull);
+          }
+        } else {
+          mbar_wait_sleepy(&bar_aempty[0], (static_cast<uint32_t>(it) & 1u) ^ 1u, prof ? &pw[0] : nullptr);
+          const uint64_t tt = t < n_tiles ? t : n_tiles - 1;  // past the end: reload the last tile
+          mbar_expect_tx(&bar_afull[0], a_tile_bytes);
+          bulk_g2s(Asm, reinterpret_cast<const uint8_t*>(a.x16) + tt * a_tile_bytes, a_tile_bytes, &bar_afull[0]);
+        }
         for (uint32_t j = 0; j < a.ntiles; ++j) {
           const uint32_t nmma = kPair == 2 ? 128u : ((min(128u, R - j * 128u) + 15u) & ~15u);
           const uint32_t bytes = kPair == 2 ? share : nmma * 128u;
@@ -819,6 +857,46 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
         atomicAdd(&a.prof[24], pw[2] + pw[3] + pw[4]);
       }
     }
+  } else if (kFuse && warp >= 10) {
+    // ---------------- converter warps (10, 11): raw fp32 tile -> A image ----------------
+    // Same arithmetic as convert_x_kernel; 8 lanes per row, rows from shared
+    // memory.  Hand-offs: raw buffer (producer), A buffer (MMA warp's copy to
+    // TMEM), thresholds (epilogue, double-buffered by tile parity).
+    const uint32_t l8 = lane & 7, groups = a.nkc * 2u;
+    const uint32_t dim = static_cast<uint32_t>(a.dim);
+    for (uint64_t it = 0; it < iters; ++it) {
+      const uint64_t t = tile_of(it);
+      const uint32_t p = static_cast<uint32_t>(it) & 1u;
+      mbar_wait_sleepy(&bar_rawfull, p, nullptr);
+      mbar_wait_sleepy(&bar_aempty[0], p ^ 1u, nullptr);
+      mbar_wait_sleepy(&bar_threempty[p], (static_cast<uint32_t>(it >> 1) & 1u) ^ 1u, nullptr);
+      for (uint32_t pass = 0; pass < kRows / 8u; ++pass) {
+        const uint32_t r = pass * 8u + (warp - 10u) * 4u + (lane >> 3);
+        const bool live = t * kRows + r < a.n;
+        float v[8][4];
+#pragma unroll
+        for (uint32_t g = 0; g < 8; ++g) {
+          const uint32_t k0 = g * 32u + l8 * 4u;
+          if (g < groups && live && k0 < dim) {  // dim % 4 == 0: whole float4 in range
+            const float4 u = *reinterpret_cast<const float4*>(Rsm + (static_cast<size_t>(r) * dim + k0) * 4u);
+            v[g][0] = u.x;
+            v[g][1] = u.y;
+            v[g][2] = u.z;
+            v[g][3] = u.w;
+          } else {
+            v[g][0] = v[g][1] = v[g][2] = v[g][3] = 0.0f;
+          }
+        }
+        convert_row(v, l8, live, groups, a.nkc, a.dim, a.margin_c, Asm, r, &thr_sm[p][r]);
+      }
+      fence_proxy_async();  // A image (generic stores) -> tcgen05.cp (async proxy)
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&bar_rawempty);
+        mbar_arrive(&bar_thrfull[p]);
+        mbar_arrive(&bar_afull[0]);
+      }
+    }
   } else if (warp >= 10) {
     // ---------------- recheck warps (10, 11) ----------------
     // Exact binary64 recheck of near ties while the main loop runs: lane L of
@@ -893,7 +971,16 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
       const uint64_t t = tile_of(it);
       const uint64_t row = t * kRows + r;
       const bool valid = row < a.n;
-      const float thr = valid ? a.rowthr[row] : -1.0f;
+      float thr;
+      if (kFuse) {
+        const uint32_t p = static_cast<uint32_t>(it) & 1u;
+        mbar_wait_sleepy(&bar_thrfull[p], static_cast<uint32_t>(it >> 1) & 1u, nullptr);
+        thr = valid ? thr_sm[p][r] : -1.0f;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_threempty[p]);
+      } else {
+        thr = valid ? a.rowthr[row] : -1.0f;
+      }
       const bool zero_row = thr < 0.0f;
       const uint32_t thr_u = zero_row ? 0u : (isinf(thr) ? 0xffffffffu : (__float_as_uint(thr) << 1));
       for (uint32_t j = 0; j < a.ntiles; ++j, ++g) {
@@ -1182,6 +1269,11 @@ __global__ void pack_w16_kernel(const double* __restrict__ w64, const double* __
 }  // namespace
 
 bool tc_supported(uint64_t dim) { return dim >= 1 && dim <= 256; }
+// The in-kernel conversion needs whole 16-byte rows and room for a raw tile
+// next to the A image and at least two W stages.
+bool tc_fuse_ok_dim(uint64_t dim, uint32_t nkc) {
+  return kPair == 1 && dim % 4 == 0 && nkc <= 2 && tc_layout(nkc, dim, true).n_wst >= 2;
+}
 
 void tc_fill_tables(TcArgs* a) {
   for (uint32_t j = 0; j < a->ntiles && j < 64; ++j) {
@@ -1211,9 +1303,14 @@ cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc) {
   e = cudaDeviceSynchronize();
   cudaFree(inv);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(hash_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  e = cudaFuncSetAttribute(hash_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(L.total));
   if (e != cudaSuccess) return e;
+  if (tc_fuse_ok_dim(f.dim, tc->nkc)) {
+    e = cudaFuncSetAttribute(hash_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(tc_layout(tc->nkc, f.dim, true).total));
+    if (e != cudaSuccess) return e;
+  }
   tc->enabled = 1;
   return cudaSuccess;
 }
@@ -1239,7 +1336,7 @@ cudaError_t launch_hash_tc(const TcArgs& a, cudaStream_t s) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = tc_layout(a.nkc).total;
+  cfg.dynamicSmemBytes = tc_layout(a.nkc, a.dim, a.fuse_convert != 0).total;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1248,7 +1345,8 @@ cudaError_t launch_hash_tc(const TcArgs& a, cudaStream_t s) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, hash_tc_kernel, a);
+  cudaError_t e = a.fuse_convert ? cudaLaunchKernelEx(&cfg, hash_tc_kernel<true>, a)
+                                 : cudaLaunchKernelEx(&cfg, hash_tc_kernel<false>, a);
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
 }

@@ -32,6 +32,7 @@ struct TcArgs {
   const double* w64;              // the reference's W (binary64) for the exact recheck
   uint32_t* counters;             // fused insert target (fused_insert != 0)
   int fused_insert;               // 32-bit sketch: insert buckets in the epilogue
+  int fuse_convert;               // convert X inside the projection kernel (no pre-pass)
   uint32_t* overflow_rows;    // bitmap over rows; rows rechecked in full
   DevState* st;
   uint16_t tab_end[64];      // tables completed by the end of direction tile j
@@ -52,5 +53,6 @@ cudaError_t launch_hash_tc(const TcArgs& a, cudaStream_t s);
 cudaError_t launch_recheck(const TcArgs& a, const double* w64, cudaStream_t s);
 size_t tc_smem_bytes(uint32_t nkc);
 bool tc_supported(uint64_t dim);
+bool tc_fuse_ok_dim(uint64_t dim, uint32_t nkc);
 
 }  // namespace ace_dev
