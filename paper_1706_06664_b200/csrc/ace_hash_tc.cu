@@ -373,11 +373,12 @@ __device__ __forceinline__ float load_x(const TcArgs& a, uint64_t row, uint64_t 
 // the row's 128-row tile (`tile`: [kc][hi | lo][16 KB]), and the row's error
 // threshold thr = c * ||x~|| * 2^14 + abs (-1: exact zero row or padding,
 // +inf: recheck every projection).
-__device__ __forceinline__ void convert_row(float (&v)[8][4], uint32_t l8, bool live, uint32_t groups, uint32_t nkc,
+template <uint32_t kG>
+__device__ __forceinline__ void convert_row(float (&v)[kG][4], uint32_t l8, bool live, uint32_t groups, uint32_t nkc,
                                             uint64_t dim, float margin_c, uint8_t* tile, uint32_t r, float* thr_dst) {
   uint32_t mb = 0u;
 #pragma unroll
-  for (uint32_t g = 0; g < 8; ++g)
+  for (uint32_t g = 0; g < kG; ++g)
 #pragma unroll
     for (int e = 0; e < 4; ++e) mb = max(mb, __float_as_uint(v[g][e]) & 0x7fffffffu);
   mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, 1));
@@ -394,7 +395,7 @@ __device__ __forceinline__ void convert_row(float (&v)[8][4], uint32_t l8, bool 
   }
   float ss = 0.0f;
 #pragma unroll
-  for (uint32_t g = 0; g < 8; ++g) {
+  for (uint32_t g = 0; g < kG; ++g) {
     if (g >= groups) continue;
     const uint32_t k0 = g * 32u + l8 * 4u;
     const uint32_t kc = k0 / kChunk, kk = k0 % kChunk;
@@ -433,6 +434,7 @@ __device__ __forceinline__ void convert_row(float (&v)[8][4], uint32_t l8, bool 
 // the SW128 image and thresholds written to global memory.  Lane l8 of a row
 // owns K elements 32g + 4*l8 .. +3 (coalesced 128 B per group).  Rows past n
 // (tile padding) are written as zeros.
+template <uint32_t kG>  // 32-element groups per row held in registers: 2 * nkc rounded up to 2, 4 or 8
 __global__ void __launch_bounds__(256) convert_x_kernel(const TcArgs a, uint64_t rows_padded) {
   const uint32_t lane = threadIdx.x & 31, l8 = lane & 7;
   const uint64_t slots = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 3);
@@ -442,9 +444,9 @@ __global__ void __launch_bounds__(256) convert_x_kernel(const TcArgs a, uint64_t
     const uint64_t row = base + (threadIdx.x >> 3);
     const bool inb = row < rows_padded;
     const bool live = row < a.n;
-    float v[8][4];
+    float v[kG][4];
 #pragma unroll
-    for (uint32_t g = 0; g < 8; ++g) {
+    for (uint32_t g = 0; g < kG; ++g) {
       const uint64_t k0 = g * 32u + l8 * 4u;
       v[g][0] = v[g][1] = v[g][2] = v[g][3] = 0.0f;
       if (g < groups && live) {
@@ -462,8 +464,8 @@ __global__ void __launch_bounds__(256) convert_x_kernel(const TcArgs a, uint64_t
     }
     if (!inb) continue;  // (row-uniform per 8-lane group; shuffles stay within the group)
     const uint64_t tile = row / kRows;
-    convert_row(v, l8, live, groups, a.nkc, a.dim, a.margin_c,
-                reinterpret_cast<uint8_t*>(a.x16) + tile * a.nkc * 2u * kBlockBytes, static_cast<uint32_t>(row % kRows),
+    convert_row<kG>(v, l8, live, groups, a.nkc, a.dim, a.margin_c,
+                    reinterpret_cast<uint8_t*>(a.x16) + tile * a.nkc * 2u * kBlockBytes, static_cast<uint32_t>(row % kRows),
                 &a.rowthr[row]);
   }
 }
@@ -887,7 +889,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
             v[g][0] = v[g][1] = v[g][2] = v[g][3] = 0.0f;
           }
         }
-        convert_row(v, l8, live, groups, a.nkc, a.dim, a.margin_c, Asm, r, &thr_sm[p][r]);
+        convert_row<8>(v, l8, live, groups, a.nkc, a.dim, a.margin_c, Asm, r, &thr_sm[p][r]);
       }
       fence_proxy_async();  // A image (generic stores) -> tcgen05.cp (async proxy)
       __syncwarp();
@@ -1361,8 +1363,14 @@ cudaError_t launch_convert_x(const TcArgs& a, cudaStream_t s) {
   }
   const uint64_t rows = (a.n + kRows - 1) / kRows * kRows;
   uint64_t blocks = (rows + 31) / 32;  // 32 rows per 256-thread block
-  if (blocks > static_cast<uint64_t>(sms) * 8) blocks = static_cast<uint64_t>(sms) * 8;
-  convert_x_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(a, rows);
+  if (blocks > static_cast<uint64_t>(sms) * 16) blocks = static_cast<uint64_t>(sms) * 16;
+  const uint32_t groups = a.nkc * 2u;
+  if (groups <= 2)
+    convert_x_kernel<2><<<static_cast<unsigned>(blocks), 256, 0, s>>>(a, rows);
+  else if (groups <= 4)
+    convert_x_kernel<4><<<static_cast<unsigned>(blocks), 256, 0, s>>>(a, rows);
+  else
+    convert_x_kernel<8><<<static_cast<unsigned>(blocks), 256, 0, s>>>(a, rows);
   count_launch();
   return cudaGetLastError();
 }
