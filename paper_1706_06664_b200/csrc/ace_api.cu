@@ -101,6 +101,32 @@ struct AceSketch {
       ev_used[i] = true;
     }
   }
+  // CUDA graph of the device work of a repeated batch call (build/detect with
+  // the same arguments): captured on the second identical call, replayed after
+  struct GraphKey {
+    const void* x = nullptr;
+    const void* flags = nullptr;
+    const void* scores = nullptr;
+    uint64_t n = 0, ld = 0;
+    int dtype = 0, where = 0, out_where = 0, build = 0, ff = 0;
+    cudaStream_t stream = nullptr;
+    const void* bufs[10] = {};  // the sketch's scratch buffers (a reallocation invalidates the graph)
+    bool operator==(const GraphKey& o) const {
+      for (int i = 0; i < 10; ++i)
+        if (bufs[i] != o.bufs[i]) return false;
+      return x == o.x && flags == o.flags && scores == o.scores && n == o.n && ld == o.ld && dtype == o.dtype &&
+             where == o.where && out_where == o.out_where && build == o.build && ff == o.ff && stream == o.stream;
+    }
+  };
+  GraphKey gkey, gseen;
+  bool gseen_valid = false;
+  cudaGraphExec_t gexec = nullptr;
+  unsigned long long glaunches = 0;
+  void drop_graph() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    gexec = nullptr;
+    gseen_valid = false;
+  }
 };
 
 namespace {
@@ -315,9 +341,25 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
   return ACE_OK;
 }
 
+// Device part of the detect tail: score from sk->ids; threshold + flags.
+ace_status run_detect_device(AceSketch* sk, uint64_t n, uint32_t* flag_bits, double* scores, int out_where,
+                             uint32_t** dflags_out, double** dscores_out);
+// Host part: outputs to host memory, state read-back, report.
+ace_status finish_detect(AceSketch* sk, uint64_t n, uint32_t* flag_bits, double* scores, int out_where,
+                         const uint32_t* dflags, const double* dscores, AceBatchReport* report);
+
 // score from sk->ids; threshold + flags; fills report.
 ace_status run_detect_tail(AceSketch* sk, uint64_t n, uint32_t* flag_bits, double* scores,
                            int out_where, AceBatchReport* report) {
+  uint32_t* dflags = nullptr;
+  double* dscores = nullptr;
+  ace_status r = run_detect_device(sk, n, flag_bits, scores, out_where, &dflags, &dscores);
+  if (r != ACE_OK) return r;
+  return finish_detect(sk, n, flag_bits, scores, out_where, dflags, dscores, report);
+}
+
+ace_status run_detect_device(AceSketch* sk, uint64_t n, uint32_t* flag_bits, double* scores, int out_where,
+                             uint32_t** dflags_out, double** dscores_out) {
   const AceFamily* f = sk->fam;
   ACE_CUDA(sk->sums.ensure(n * sizeof(uint64_t)));
   ACE_CUDA(sk->flags.ensure(((n + 31) / 32) * sizeof(uint32_t)));
@@ -339,6 +381,13 @@ ace_status run_detect_tail(AceSketch* sk, uint64_t n, uint32_t* flag_bits, doubl
   ACE_CUDA(launch_replay(sk->sums.as<uint64_t>(), n, f->d.tables, sk->st, sk->stream));
   ACE_CUDA(launch_flags(sk->sums.as<uint64_t>(), n, dflags, sk->st, 1, sk->stream));
   sk->mark(3);
+  *dflags_out = dflags;
+  *dscores_out = dscores;
+  return ACE_OK;
+}
+
+ace_status finish_detect(AceSketch* sk, uint64_t n, uint32_t* flag_bits, double* scores, int out_where,
+                         const uint32_t* dflags, const double* dscores, AceBatchReport* report) {
   if (flag_bits && out_where == ACE_HOST) {
     ace_status r = copy_out(flag_bits, dflags, ((n + 31) / 32) * sizeof(uint32_t), ACE_HOST, sk->stream);
     if (r != ACE_OK) return r;
@@ -553,6 +602,7 @@ ace_status ace_sketch_clone(const AceSketch* src, AceSketch** out) {
 ace_status ace_sketch_destroy(AceSketch* sk) {
   if (!sk) return ACE_OK;
   if (sk->stream) cudaStreamSynchronize(sk->stream);
+  sk->drop_graph();
   sk->ids.release();
   sk->sums.release();
   sk->stage.release();
@@ -668,6 +718,98 @@ ace_status ace_sketch_score(AceSketch* sk, const void* x, int dtype, uint64_t n,
   return r;
 }
 
+}  // extern "C"
+
+namespace {
+
+bool host_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// build (optional) + detect over one batch.  The device work is replayed from
+// a CUDA graph when the same call repeats (same buffers, sizes and stream;
+// captured on the second identical call, once every buffer is sized), so the
+// dozen launches and memsets of the pipeline cost one graph launch.
+ace_status batch_detect(AceSketch* sk, const void* x, int dtype, uint64_t n, uint64_t ld, int x_where,
+                        uint32_t* flag_bits, double* scores, int out_where, AceBatchReport* report, int build) {
+  AceSketch::GraphKey key;
+  key.x = x;
+  key.flags = flag_bits;
+  key.scores = scores;
+  key.n = n;
+  key.ld = ld;
+  key.dtype = dtype;
+  key.where = x_where;
+  key.out_where = out_where;
+  key.build = build;
+  key.ff = build ? (fire_and_forget_ok(sk, n) ? 1 : 0) : 2;
+  key.stream = sk->stream;
+  const DevBuf* bufs[10] = {&sk->ids, &sk->sums, &sk->stage, &sk->flags, &sk->scores,
+                            &sk->demand, &sk->near, &sk->overflow, &sk->x16, &sk->rowthr};
+  for (int i = 0; i < 10; ++i) key.bufs[i] = bufs[i]->p;
+  static int graphs_env = -2;
+  if (graphs_env == -2) {
+    const char* e = getenv("ACE_GRAPHS");
+    graphs_env = e ? atoi(e) : 1;
+  }
+  const bool eligible = graphs_env != 0 && !sk->timing && (x_where == ACE_DEVICE || host_pinned(x));
+  const void* xd = nullptr;
+  uint64_t ldd = 0;
+  uint32_t* dflags = nullptr;
+  double* dscores = nullptr;
+  auto device_work = [&]() -> ace_status {
+    ACE_CUDA(zero_call_fields(sk));
+    ace_status r = stage_x(sk, sk->stage, sk->stream, x, dtype, n, ld, x_where, &xd, &ldd);
+    if (r == ACE_OK) r = run_hash(sk, xd, dtype, n, ldd, build);
+    if (r == ACE_OK) r = run_detect_device(sk, n, flag_bits, scores, out_where, &dflags, &dscores);
+    return r;
+  };
+  ace_status r = ACE_OK;
+  if (eligible && sk->gexec && key == sk->gkey) {
+    ACE_CUDA(cudaGraphLaunch(sk->gexec, sk->stream));
+    count_launch(sk->glaunches);
+    // pointers the host part needs (same as at capture)
+    dflags = (flag_bits && out_where == ACE_DEVICE) ? flag_bits : sk->flags.as<uint32_t>();
+    dscores = scores ? (out_where == ACE_DEVICE ? scores : sk->scores.as<double>()) : nullptr;
+  } else if (eligible && sk->gseen_valid && key == sk->gseen) {
+    sk->drop_graph();
+    const unsigned long long l0 = ace_kernel_launches();
+    ACE_CUDA(cudaStreamBeginCapture(sk->stream, cudaStreamCaptureModeThreadLocal));
+    r = device_work();
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(sk->stream, &g);
+    if (r != ACE_OK) {
+      if (g) cudaGraphDestroy(g);
+      return r;
+    }
+    if (ce != cudaSuccess) return fail(ACE_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+    const cudaError_t ie = cudaGraphInstantiate(&sk->gexec, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) {
+      sk->gexec = nullptr;
+      return fail(ACE_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
+    }
+    sk->glaunches = ace_kernel_launches() - l0;
+    sk->gkey = key;
+    ACE_CUDA(cudaGraphLaunch(sk->gexec, sk->stream));
+  } else {
+    r = device_work();
+    if (r != ACE_OK) return r;
+    sk->gseen = key;
+    sk->gseen_valid = eligible;
+  }
+  return finish_detect(sk, n, flag_bits, scores, out_where, dflags, dscores, report);
+}
+
+}  // namespace
+
+extern "C" {
+
 // detect_batch (detect.cpp:12-74).
 ace_status ace_sketch_detect_batch(AceSketch* sk, const void* x, int dtype, uint64_t n, uint64_t ld,
                                    int x_where, uint32_t* flag_bits, double* scores, int out_where,
@@ -678,12 +820,7 @@ ace_status ace_sketch_detect_batch(AceSketch* sk, const void* x, int dtype, uint
   ace_status r = check_x(sk->fam, x, dtype, n, ld, x_where);
   if (r != ACE_OK) return r;
   const auto t0 = std::chrono::steady_clock::now();
-  ACE_CUDA(zero_call_fields(sk));
-  const void* xd;
-  uint64_t ldd;
-  r = stage_x(sk, sk->stage, sk->stream, x, dtype, n, ld, x_where, &xd, &ldd);
-  if (r == ACE_OK) r = run_hash(sk, xd, dtype, n, ldd, 0);
-  if (r == ACE_OK) r = run_detect_tail(sk, n, flag_bits, scores, out_where, report);
+  r = batch_detect(sk, x, dtype, n, ld, x_where, flag_bits, scores, out_where, report, 0);
   if (r == ACE_OK) {
     fill_stats(stats, *sk->hst, n, sk->fam);
     if (report)
@@ -702,12 +839,7 @@ ace_status ace_sketch_build_detect(AceSketch* sk, const void* x, int dtype, uint
   ace_status r = check_x(sk->fam, x, dtype, n, ld, x_where);
   if (r != ACE_OK) return r;
   const auto t0 = std::chrono::steady_clock::now();
-  ACE_CUDA(zero_call_fields(sk));
-  const void* xd;
-  uint64_t ldd;
-  r = stage_x(sk, sk->stage, sk->stream, x, dtype, n, ld, x_where, &xd, &ldd);
-  if (r == ACE_OK) r = run_hash(sk, xd, dtype, n, ldd, 1);
-  if (r == ACE_OK) r = run_detect_tail(sk, n, flag_bits, scores, out_where, report);
+  r = batch_detect(sk, x, dtype, n, ld, x_where, flag_bits, scores, out_where, report, 1);
   if (r == ACE_OK) {
     fill_stats(stats, *sk->hst, n, sk->fam);
     if (report)
