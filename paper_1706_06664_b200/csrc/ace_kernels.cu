@@ -952,6 +952,7 @@ cudaError_t launch_apply_ids(const uint32_t* ids, uint64_t n, uint32_t tables, u
     uint64_t ranges = static_cast<uint64_t>(sms) / parts;
     if (ranges < 1) ranges = 1;
     if (ranges > total / 4096) ranges = total / 4096 > 0 ? total / 4096 : 1;
+
     const uint64_t per = (total + ranges - 1) / ranges;
     const unsigned grid = static_cast<unsigned>((total + per - 1) / per) * parts;
     const size_t smem = sizeof(uint32_t) << part_bits;
