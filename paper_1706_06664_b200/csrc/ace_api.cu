@@ -90,7 +90,7 @@ struct AceSketch {
   DevState* hst = nullptr;   // pinned host mirror
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
-  DevBuf ids, sums, stage, flags, scores, demand, near, overflow, x16, rowthr;
+  DevBuf ids, sums, stage, flags, scores, demand, near, overflow, x16, rowthr, segc;
   // phase timing (ace_sketch_set_timing)
   bool timing = false;
   cudaEvent_t ev[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -110,9 +110,9 @@ struct AceSketch {
     uint64_t n = 0, ld = 0;
     int dtype = 0, where = 0, out_where = 0, build = 0, ff = 0;
     cudaStream_t stream = nullptr;
-    const void* bufs[10] = {};  // the sketch's scratch buffers (a reallocation invalidates the graph)
+    const void* bufs[11] = {};  // the sketch's scratch buffers (a reallocation invalidates the graph)
     bool operator==(const GraphKey& o) const {
-      for (int i = 0; i < 10; ++i)
+      for (int i = 0; i < 11; ++i)
         if (bufs[i] != o.bufs[i]) return false;
       return x == o.x && flags == o.flags && scores == o.scores && n == o.n && ld == o.ld && dtype == o.dtype &&
              where == o.where && out_where == o.out_where && build == o.build && ff == o.ff && stream == o.stream;
@@ -251,8 +251,10 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
     t.w16 = f->tc.w16;
     tc_fill_tables(&t);
     // error bound of the fp16x3 split relative to ||x~|| ||w^||
-    t.margin_c = static_cast<float>(
-        2.0 * (4.0 * 0x1.0p-22 + 0x1.0p-23 * (12.0 * f->tc.nkc + 16.0) * 1.01 + (t.x_f64 ? 0x1.0p-23 : 0.0)));
+    const bool kstream = tc_kstream(f->tc.nkc);
+    t.margin_c = kstream ? tck_margin(f->tc.nkc, t.x_f64 != 0)
+                         : static_cast<float>(2.0 * (4.0 * 0x1.0p-22 + 0x1.0p-23 * (12.0 * f->tc.nkc + 16.0) * 1.01 +
+                                                     (t.x_f64 ? 0x1.0p-23 : 0.0)));
     t.ids = sk->ids.as<uint32_t>();
     uint64_t cap = n * f->d.rows / 1024;
     cap = std::min<uint64_t>(std::max<uint64_t>(cap, 1u << 20), 1u << 25);
@@ -301,6 +303,28 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
     }
     t.fuse_convert = fuse_env != 0 && !t.x_f64 && ld == f->d.dim && (reinterpret_cast<uintptr_t>(xd) & 15) == 0 &&
                      tc_fuse_ok_dim(f->d.dim, f->tc.nkc);
+    if (kstream) {
+      // d > 256: K-streamed kernel with its own conversion and recheck
+      t.fuse_convert = 0;
+      t.fused_insert = 0;
+      t.w64 = f->d.w64;
+      ACE_CUDA(sk->segc.ensure(static_cast<size_t>(tck_grid(n)) * sizeof(uint32_t)));
+      t.seg_counts = sk->segc.as<uint32_t>();
+      sk->mark(4);
+      ACE_CUDA(launch_convert_x_wide(t, sk->stream));
+      sk->mark(6);
+      ACE_CUDA(launch_hash_tck(t, sk->stream));
+      sk->mark(5);
+      ACE_CUDA(launch_recheck_segs(t, sk->stream));
+      ACE_CUDA(launch_recheck(t, f->d.w64, sk->stream));
+      if (insert)
+        ACE_CUDA(launch_apply_ids(sk->ids.as<uint32_t>(), n, f->d.tables, f->d.k_bits, sk->counters, sk->cap,
+                                  +1, sk->st, sk->stream, !fire_and_forget_ok(sk, n)));
+      if (insert && sk->width == 16)
+        ACE_CUDA(launch_cap(sk->counters, sk->num_counters, sk->cap, sk->st, sk->stream));
+      sk->mark(1);
+      return ACE_OK;
+    }
     sk->mark(4);
     if (!t.fuse_convert) ACE_CUDA(launch_convert_x(t, sk->stream));
     sk->mark(6);
@@ -613,6 +637,7 @@ ace_status ace_sketch_destroy(AceSketch* sk) {
   sk->overflow.release();
   sk->x16.release();
   sk->rowthr.release();
+  sk->segc.release();
   if (sk->counters) cudaFree(sk->counters);
   if (sk->st) cudaFree(sk->st);
   if (sk->hst) cudaFreeHost(sk->hst);
@@ -749,9 +774,9 @@ ace_status batch_detect(AceSketch* sk, const void* x, int dtype, uint64_t n, uin
   key.build = build;
   key.ff = build ? (fire_and_forget_ok(sk, n) ? 1 : 0) : 2;
   key.stream = sk->stream;
-  const DevBuf* bufs[10] = {&sk->ids, &sk->sums, &sk->stage, &sk->flags, &sk->scores,
-                            &sk->demand, &sk->near, &sk->overflow, &sk->x16, &sk->rowthr};
-  for (int i = 0; i < 10; ++i) key.bufs[i] = bufs[i]->p;
+  const DevBuf* bufs[11] = {&sk->ids, &sk->sums, &sk->stage, &sk->flags, &sk->scores, &sk->demand,
+                            &sk->near, &sk->overflow, &sk->x16, &sk->rowthr, &sk->segc};
+  for (int i = 0; i < 11; ++i) key.bufs[i] = bufs[i]->p;
   static int graphs_env = -2;
   if (graphs_env == -2) {
     const char* e = getenv("ACE_GRAPHS");

@@ -1169,6 +1169,319 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
   }
 }
 
+// ---- K-streamed projection (d > 256) -----------------------------------------------
+//
+// A point tile no longer fits on chip (d = 4096: 2 MB of fp16 hi + lo), so A
+// is streamed in 64-wide K chunks next to the W chunks, one direction tile at
+// a time.  Accumulation is chunked: kKsSc K chunks go into a TMEM accumulator
+// (double-buffered), the epilogue adds the chunk results into fp32 running
+// sums in registers (64 columns per thread).  That keeps the rigorous error
+// bound at (12 kKsSc + nchunks + 16) ulp instead of growing with d, so near
+// ties stay rare; they are rechecked by recheck_segs_kernel afterwards.
+
+constexpr uint32_t kKsSc = 2;                  // K chunks per accumulation pass
+constexpr uint32_t kKsSlot = 4u * kBlockBytes;  // ring slot: A chunk (hi | lo) + W chunk (hi | lo)
+constexpr uint32_t kKsSlots = 3;
+constexpr int kKsThreads = 320;                // producer, MMA, 8 epilogue warps
+
+__host__ __device__ inline uint32_t ks_chunks(uint32_t nkc) { return (nkc + kKsSc - 1) / kKsSc; }
+__host__ inline size_t ks_smem_bytes() { return static_cast<size_t>(kKsSlots) * kKsSlot + 1024; }
+
+__global__ void __launch_bounds__(kKsThreads, 1) hash_tck_kernel(const TcArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t bar_full[kKsSlots], bar_empty[kKsSlots], bar_accfull[2], bar_accempty[2];
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ uint32_t sgbuf[2][4][kRows];  // sign words of a direction tile, by tile parity
+  __shared__ uint32_t seg_n;
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t n_tiles = (a.n + kRows - 1) / kRows;
+  const uint32_t K = a.k_bits, nkc = a.nkc, nch = ks_chunks(nkc);
+  const uint32_t R = a.k_bits * a.tables;
+  if (threadIdx.x == 0) {
+    seg_n = 0;
+    for (uint32_t i = 0; i < kKsSlots; ++i) {
+      mbar_init(&bar_full[i], 1);
+      mbar_init(&bar_empty[i], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bar_accfull[b], 1);
+      mbar_init(&bar_accempty[b], 8);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem_base = tmem_base_sh;
+  const uint64_t iters = (n_tiles + gridDim.x - 1) / gridDim.x;
+  const unsigned long long seg_cap = a.near_cap / gridDim.x;
+
+  if (warp == 0) {
+    // ---- producer: per (tile, direction tile, K chunk) one A chunk + one W chunk
+    if (lane == 0) {
+      uint32_t s = 0, ph = 0;
+      for (uint64_t it = 0; it < iters; ++it) {
+        const uint64_t t = blockIdx.x + it * gridDim.x;
+        const uint64_t tt = t < n_tiles ? t : n_tiles - 1;
+        for (uint32_t j = 0; j < a.ntiles; ++j)
+          for (uint32_t kc = 0; kc < nkc; ++kc) {
+            mbar_wait_sleepy(&bar_empty[s], ph ^ 1u, nullptr);
+            mbar_expect_tx(&bar_full[s], kKsSlot);
+            uint8_t* dst = base + static_cast<size_t>(s) * kKsSlot;
+            bulk_g2s(dst, reinterpret_cast<const uint8_t*>(a.x16) + (tt * nkc + kc) * 2u * kBlockBytes,
+                     2u * kBlockBytes, &bar_full[s]);
+            bulk_g2s(dst + 2u * kBlockBytes,
+                     reinterpret_cast<const uint8_t*>(a.w16) + (static_cast<uint64_t>(j) * nkc + kc) * 2u * kBlockBytes,
+                     2u * kBlockBytes, &bar_full[s]);
+            if (++s == kKsSlots) {
+              s = 0;
+              ph ^= 1u;
+            }
+          }
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer: A chunk -> TMEM (double-buffered), 12 TS MMAs per K chunk
+    uint32_t s = 0, ph = 0, ab = 0, abph = 0;
+    const uint32_t ta = tmem_base + 256u;  // A buffers: [2][hi 32 | lo 32 columns]
+    const uint32_t idesc = idesc_f16(128u);
+    for (uint64_t it = 0; it < iters; ++it)
+      for (uint32_t j = 0; j < a.ntiles; ++j)
+        for (uint32_t c = 0; c < nch; ++c) {
+          mbar_wait(&bar_accempty[ab], abph ^ 1u);
+          tc_after();
+          const uint32_t k0 = c * kKsSc, k1 = min(nkc, k0 + kKsSc);
+          const uint32_t dt = tmem_base + ab * 128u;
+          if (elect_one()) {
+            uint32_t ss = s, pp = ph;
+            for (uint32_t kc = k0; kc < k1; ++kc) {
+              mbar_wait(&bar_full[ss], pp);
+              const uint32_t sa = smem_u32(base + static_cast<size_t>(ss) * kKsSlot);
+              const uint32_t tb = ta + (kc & 1u) * 64u;
+#pragma unroll
+              for (uint32_t kk = 0; kk < 4; ++kk) {
+                tmem_cp_128x256b(tb + kk * 8u, sw128_desc(sa + kk * 32u));
+                tmem_cp_128x256b(tb + 32u + kk * 8u, sw128_desc(sa + kBlockBytes + kk * 32u));
+              }
+              const uint64_t dbh = sw128_desc(sa + 2u * kBlockBytes), dbl = sw128_desc(sa + 3u * kBlockBytes);
+#pragma unroll
+              for (uint32_t kk = 0; kk < 4; ++kk) {
+                const uint64_t off = kk * 2u;
+                mma_f16_ts(dt, tb + kk * 8u, dbh + off, idesc, (kc != k0 || kk != 0u) ? 1u : 0u);
+                mma_f16_ts(dt, tb + 32u + kk * 8u, dbh + off, idesc, 1u);
+                mma_f16_ts(dt, tb + kk * 8u, dbl + off, idesc, 1u);
+              }
+              mma_commit(&bar_empty[ss]);
+              if (++ss == kKsSlots) {
+                ss = 0;
+                pp ^= 1u;
+              }
+            }
+            mma_commit(&bar_accfull[ab]);
+          }
+          __syncwarp();
+          for (uint32_t kc = k0; kc < k1; ++kc)
+            if (++s == kKsSlots) {
+              s = 0;
+              ph ^= 1u;
+            }
+          ab ^= 1u;
+          if (ab == 0) abph ^= 1u;
+        }
+  } else {
+    // ---- epilogue (warps 2-9): two warps per lane quarter, 64 columns each
+    const uint32_t q = warp & 3, h = (warp - 2) >> 2;
+    const uint32_t r = q * 32u + lane;
+    const uint32_t kmask = (K >= 32u) ? 0xffffffffu : ((1u << K) - 1u);
+    uint32_t ab = 0, abph = 0, par = 0;
+    for (uint64_t it = 0; it < iters; ++it) {
+      const uint64_t t = blockIdx.x + it * gridDim.x;
+      const uint64_t row = t * kRows + r;
+      const bool valid = row < a.n;
+      const float thr = valid ? a.rowthr[row] : -1.0f;
+      const bool zero_row = thr < 0.0f;
+      uint32_t prev3 = 0u;
+      for (uint32_t j = 0; j < a.ntiles; ++j, par ^= 1u) {
+        const uint32_t used = min(128u, R - j * 128u);
+        float acc[64];
+#pragma unroll
+        for (int i = 0; i < 64; ++i) acc[i] = 0.0f;
+        for (uint32_t c = 0; c < nch; ++c) {
+          mbar_wait_sleepy(&bar_accfull[ab], abph, nullptr);
+          tc_after();
+          uint32_t v[64];
+          ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + ab * 128u + 64u * h, v);
+          ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + ab * 128u + 64u * h + 32u, (v + 32));
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 64; ++i) acc[i] += __uint_as_float(v[i]);
+          tc_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar_accempty[ab]);
+          ab ^= 1u;
+          if (ab == 0) abph ^= 1u;
+        }
+#pragma unroll
+        for (uint32_t g2 = 0; g2 < 2; ++g2) {
+          const uint32_t cc = 64u * h + 32u * g2;
+          uint32_t neg = 0u, nm = 0u;
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) {
+            const float p = acc[32 * g2 + jj];
+            neg = (neg << 1) | (__float_as_uint(p) >> 31);
+            nm |= ((!(fabsf(p) > thr)) ? 1u : 0u) << jj;  // NaN projections (wild rows) count as near
+          }
+          if (cc < used && !zero_row && valid) {
+            if (used - cc < 32u) nm &= (1u << (used - cc)) - 1u;
+            if (nm)
+              push_near_mask(a.st, a.near_list + blockIdx.x * seg_cap, seg_cap, &seg_n, a.overflow_rows, nm, row,
+                             j * 128u + cc);
+          }
+          sgbuf[par][2 * h + g2][r] = zero_row ? 0xffffffffu : ~neg;  // bit (31-jj) = column cc+jj >= 0
+        }
+        asm volatile("bar.sync %0, 64;" ::"r"(1u + q) : "memory");  // the quarter's two warps
+        const uint32_t tb = j == 0 ? 0u : a.tab_end[j - 1], te = a.tab_end[j];
+        uint32_t* idp = a.ids + row;
+        for (uint32_t tt = tb + h; tt < te; tt += 2) {
+          const uint32_t s0 = tt * K;
+          const int wi = static_cast<int>(s0 >> 5) - static_cast<int>(4 * j);  // -1 .. 3
+          const uint32_t off = s0 & 31u;
+          const uint32_t hi = wi < 0 ? prev3 : sgbuf[par][wi][r];
+          const uint32_t lo = wi < 3 ? sgbuf[par][wi + 1][r] : 0u;
+          const unsigned long long win = (static_cast<unsigned long long>(hi) << 32) | lo;
+          const uint32_t bucket = static_cast<uint32_t>(win >> (64u - off - K)) & kmask;
+          if (valid) idp[static_cast<uint64_t>(tt) * a.n] = bucket;
+        }
+        prev3 = sgbuf[par][3][r];
+      }
+    }
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (threadIdx.x == 0) {
+    a.seg_counts[blockIdx.x] = seg_n;
+    if (seg_n) atomicAdd(&a.st->near_count, static_cast<unsigned long long>(seg_n));
+  }
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+}
+
+// Conversion for the K-streamed path: one warp per row, any d.
+__global__ void __launch_bounds__(256) convert_x_wide_kernel(const TcArgs a, uint64_t rows_padded) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  const uint32_t dpad = a.nkc * kChunk;
+  for (uint64_t row = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows_padded;
+       row += warps) {
+    const bool live = row < a.n;
+    uint32_t mb = 0u;
+    if (live)
+      for (uint32_t k = lane; k < a.dim; k += 32u) mb = max(mb, __float_as_uint(load_x(a, row, k)) & 0x7fffffffu);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+    const bool nan = mb > 0x7f800000u;
+    const float m = __uint_as_float(nan ? 0x7f800000u : mb);
+    const bool zero = (m == 0.0f);
+    const bool wild = nan || !(m < 0x1.0p100f) || (!zero && m < 0x1.0p-100f);
+    float scale = 0.0f;
+    if (live && !zero && !wild) {
+      const int e = static_cast<int>((__float_as_uint(m) >> 23) & 0xffu) - 127;
+      scale = __uint_as_float(static_cast<uint32_t>(127 + 14 - e) << 23);
+    }
+    const uint64_t tile = row / kRows;
+    const uint32_t r = static_cast<uint32_t>(row % kRows);
+    float ss = 0.0f;
+    for (uint32_t k = 2u * lane; k < dpad; k += 64u) {
+      const float x0 = (live ? load_x(a, row, k) : 0.0f) * scale, x1 = (live ? load_x(a, row, k + 1) : 0.0f) * scale;
+      ss = fmaf(x0, x0, fmaf(x1, x1, ss));
+      const float h0 = __half2float(__float2half_rn(x0)), h1 = __half2float(__float2half_rn(x1));
+      uint8_t* blk = reinterpret_cast<uint8_t*>(a.x16) + ((tile * a.nkc + k / kChunk) * 2u) * kBlockBytes;
+      const uint32_t off = sw128_off(r, k % kChunk);
+      *reinterpret_cast<uint32_t*>(blk + off) = pack_h2(h0, h1);
+      *reinterpret_cast<uint32_t*>(blk + kBlockBytes + off) = pack_h2(x0 - h0, x1 - h1);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) {
+      float thr;
+      if (!live || zero) {
+        thr = -1.0f;
+      } else if (wild) {
+        thr = __int_as_float(0x7f800000);
+      } else {
+        const float nx = sqrtf(ss * (1.0f + static_cast<float>(a.dim + 4) * 0x1.0p-23f)) * (1.0f + 0x1.0p-20f);
+        thr = a.margin_c * nx * 16384.0f + static_cast<float>(a.dim) * 0x1.0p-10f;
+      }
+      a.rowthr[row] = thr;
+    }
+  }
+}
+
+// Near ties of the K-streamed kernel, one warp per list item.  Stage 1: the
+// projection in binary64 with FMAs across the warp, p1, and A = sum |x_i w_i|;
+// both p1 and the reference's left fold are within gamma_d * A of the exact
+// value, so |p1| > 2 gamma_d A (inflated) decides the reference's sign.
+// Stage 2 (rare): the reference's sequential fold itself (srp.cpp:78-91).
+__global__ void __launch_bounds__(256) recheck_segs_kernel(const TcArgs a, uint32_t grid) {
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const unsigned long long seg_cap = a.near_cap / grid;
+  const uint32_t K = a.k_bits;
+  const double gam = static_cast<double>(a.dim + 2) * 0x1.0p-53 / (1.0 - static_cast<double>(a.dim + 2) * 0x1.0p-53);
+  unsigned long long rr = 0, ff = 0;
+  for (uint32_t b = blockIdx.x; b < grid; b += gridDim.x) {
+    unsigned long long* seg = a.near_list + b * seg_cap;
+    const uint32_t cnt = static_cast<uint32_t>(min(static_cast<unsigned long long>(a.seg_counts[b]), seg_cap));
+    for (uint32_t i = wib; i < cnt; i += blockDim.x >> 5) {
+      const unsigned long long item = seg[i];
+      const uint64_t row = item >> 32;
+      const uint32_t dir = static_cast<uint32_t>(item & 0xffffffffu);
+      const double* w = a.w64 + static_cast<uint64_t>(dir) * a.dim;
+      double p = 0.0, ab = 0.0;
+      for (uint32_t k = lane; k < a.dim; k += 32u) {
+        const double xv = a.x_f64 ? static_cast<const double*>(a.x)[row * a.ld + k]
+                                  : static_cast<double>(static_cast<const float*>(a.x)[row * a.ld + k]);
+        const double t = xv * __ldg(w + k);
+        p += t;
+        ab += fabs(t);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        p += __shfl_xor_sync(0xffffffffu, p, o);
+        ab += __shfl_xor_sync(0xffffffffu, ab, o);
+      }
+      int bit;
+      if (fabs(p) > 2.0 * gam * ab * (1.0 + 4.0 * gam) + 0x1.0p-1000) {
+        bit = p >= 0.0 ? 1 : 0;
+      } else {
+        double e = 0.0;
+        if (lane == 0) e = exact_proj(w, a.x, a.x_f64, row, a.ld, a.dim);
+        e = __shfl_sync(0xffffffffu, e, 0);
+        bit = e >= 0.0 ? 1 : 0;
+      }
+      if (lane == 0) {
+        const uint32_t table = dir / K, bpos = K - 1u - dir % K;
+        uint32_t* id = &a.ids[static_cast<uint64_t>(table) * a.n + row];
+        if (static_cast<int>((*id >> bpos) & 1u) != bit) {
+          atomicXor(id, 1u << bpos);
+          ++ff;
+        }
+        ++rr;
+        seg[i] = ~0ull;  // the list is all ~0 between launches
+      }
+    }
+  }
+  if (lane == 0) {
+    if (rr) atomicAdd(&a.st->rechecked, rr);
+    if (ff) atomicAdd(&a.st->flipped, ff);
+  }
+}
+
 // ---- near-tie recheck ------------------------------------------------------------
 
 __global__ void recheck_list_kernel(const TcArgs a, const double* __restrict__ w64) {
@@ -1270,7 +1583,8 @@ __global__ void pack_w16_kernel(const double* __restrict__ w64, const double* __
 
 }  // namespace
 
-bool tc_supported(uint64_t dim) { return dim >= 1 && dim <= 256; }
+bool tc_supported(uint64_t dim) { return dim >= 1 && dim <= 8192; }
+bool tc_kstream(uint32_t nkc) { return nkc > 4; }
 // The in-kernel conversion needs whole 16-byte rows and room for a raw tile
 // next to the A image and at least two W stages.
 bool tc_fuse_ok_dim(uint64_t dim, uint32_t nkc) {
@@ -1291,7 +1605,7 @@ cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc) {
   if (!tc_supported(f.dim) || f.k_bits > 128) return cudaSuccess;
   const uint32_t nkc = static_cast<uint32_t>((f.dim + kChunk - 1) / kChunk);
   const TcLayout L = tc_layout(nkc);
-  if (nkc > 4 || tc_layout(nkc).n_wst < 2 || f.rows > 64u * 128u) return cudaSuccess;
+  if ((!tc_kstream(nkc) && tc_layout(nkc).n_wst < 2) || f.rows > 64u * 128u || kPair != 1) return cudaSuccess;
   tc->nkc = nkc;
   tc->ntiles = (f.rows + kRows - 1) / kRows;
   const size_t bytes = static_cast<size_t>(tc->ntiles) * nkc * 2 * kBlockBytes;
@@ -1305,6 +1619,13 @@ cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc) {
   e = cudaDeviceSynchronize();
   cudaFree(inv);
   if (e != cudaSuccess) return e;
+  if (tc_kstream(nkc)) {
+    e = cudaFuncSetAttribute(hash_tck_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(ks_smem_bytes()));
+    if (e != cudaSuccess) return e;
+    tc->enabled = 1;
+    return cudaSuccess;
+  }
   e = cudaFuncSetAttribute(hash_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(L.total));
   if (e != cudaSuccess) return e;
@@ -1373,6 +1694,51 @@ cudaError_t launch_convert_x(const TcArgs& a, cudaStream_t s) {
     convert_x_kernel<8><<<static_cast<unsigned>(blocks), 256, 0, s>>>(a, rows);
   count_launch();
   return cudaGetLastError();
+}
+
+static int tc_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
+uint32_t tck_grid(uint64_t n) {
+  const uint64_t tiles = (n + kRows - 1) / kRows;
+  return static_cast<uint32_t>(tiles < static_cast<uint64_t>(tc_sms()) ? tiles : tc_sms());
+}
+
+cudaError_t launch_convert_x_wide(const TcArgs& a, cudaStream_t s) {
+  if (a.n == 0) return cudaSuccess;
+  const uint64_t rows = (a.n + kRows - 1) / kRows * kRows;
+  uint64_t blocks = (rows + 7) / 8;  // 8 rows (warps) per block
+  if (blocks > static_cast<uint64_t>(tc_sms()) * 16) blocks = static_cast<uint64_t>(tc_sms()) * 16;
+  convert_x_wide_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(a, rows);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hash_tck(const TcArgs& a, cudaStream_t s) {
+  if (a.n == 0) return cudaSuccess;
+  hash_tck_kernel<<<tck_grid(a.n), kKsThreads, ks_smem_bytes(), s>>>(a);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_recheck_segs(const TcArgs& a, cudaStream_t s) {
+  if (a.n == 0) return cudaSuccess;
+  const uint32_t grid = tck_grid(a.n);
+  recheck_segs_kernel<<<grid, 256, 0, s>>>(a, grid);
+  count_launch();
+  return cudaGetLastError();
+}
+
+float tck_margin(uint32_t nkc, bool x_f64) {
+  return static_cast<float>(2.0 * (4.0 * 0x1.0p-22 + 0x1.0p-23 * (12.0 * kKsSc + ks_chunks(nkc) + 16.0) * 1.01 +
+                                   (x_f64 ? 0x1.0p-23 : 0.0)));
 }
 
 cudaError_t launch_recheck(const TcArgs& a, const double* w64, cudaStream_t s) {

@@ -33,6 +33,7 @@ struct TcArgs {
   uint32_t* counters;             // fused insert target (fused_insert != 0)
   int fused_insert;               // 32-bit sketch: insert buckets in the epilogue
   int fuse_convert;               // convert X inside the projection kernel (no pre-pass)
+  uint32_t* seg_counts;           // K-streamed kernel: near ties pushed per CTA
   uint32_t* overflow_rows;    // bitmap over rows; rows rechecked in full
   DevState* st;
   uint16_t tab_end[64];      // tables completed by the end of direction tile j
@@ -54,5 +55,13 @@ cudaError_t launch_recheck(const TcArgs& a, const double* w64, cudaStream_t s);
 size_t tc_smem_bytes(uint32_t nkc);
 bool tc_supported(uint64_t dim);
 bool tc_fuse_ok_dim(uint64_t dim, uint32_t nkc);
+// K-streamed kernel for d > 256 (nkc > 4): its own conversion, projection and
+// near-tie recheck (per-CTA list segments, counts in TcArgs::seg_counts)
+bool tc_kstream(uint32_t nkc);
+uint32_t tck_grid(uint64_t n);
+float tck_margin(uint32_t nkc, bool x_f64);
+cudaError_t launch_convert_x_wide(const TcArgs& a, cudaStream_t s);
+cudaError_t launch_hash_tck(const TcArgs& a, cudaStream_t s);
+cudaError_t launch_recheck_segs(const TcArgs& a, cudaStream_t s);
 
 }  // namespace ace_dev

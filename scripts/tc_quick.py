@@ -12,7 +12,7 @@ from paper_1706_06664_b200 import ace
 from paper_1706_06664_b200 import workloads as W
 
 o = Oracle()
-for (d, k, l, n) in [(40, 15, 50, 1000), (120, 15, 50, 5000), (64, 15, 50, 300), (128, 16, 100, 3000), (200, 18, 64, 700), (7, 3, 5, 100)]:
+for (d, k, l, n) in [(40, 15, 50, 1000), (120, 15, 50, 5000), (64, 15, 50, 300), (128, 16, 100, 3000), (200, 18, 64, 700), (7, 3, 5, 100), (300, 15, 20, 500), (1000, 18, 64, 700), (4096, 18, 64, 300)]:
     fam = ace.SrpFamily(ace.SrpConfig(dim=d, k_bits=k, num_tables=l, seed=3))
     x = np.random.default_rng(d).standard_normal((n, d)).astype(np.float32)
     st = N.AceHashStats()
