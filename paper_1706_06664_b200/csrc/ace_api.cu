@@ -256,8 +256,10 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
                          : static_cast<float>(2.0 * (4.0 * 0x1.0p-22 + 0x1.0p-23 * (12.0 * f->tc.nkc + 16.0) * 1.01 +
                                                      (t.x_f64 ? 0x1.0p-23 : 0.0)));
     t.ids = sk->ids.as<uint32_t>();
-    uint64_t cap = n * f->d.rows / 1024;
-    cap = std::min<uint64_t>(std::max<uint64_t>(cap, 1u << 20), 1u << 25);
+    // near-tie list: the K-streamed path's bound (large d, dense data) leaves
+    // far more near ties per row, size its list accordingly
+    uint64_t cap = tc_kstream(f->tc.nkc) ? n * f->d.rows / 48 : n * f->d.rows / 1024;
+    cap = std::min<uint64_t>(std::max<uint64_t>(cap, 1u << 20), tc_kstream(f->tc.nkc) ? (1u << 27) : (1u << 25));
     {
       // the kernel's near-tie list is all ~0 between launches (entries are
       // reset as they are rechecked); fill a newly allocated one
@@ -310,6 +312,7 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
       t.w64 = f->d.w64;
       ACE_CUDA(sk->segc.ensure(static_cast<size_t>(tck_grid(n)) * sizeof(uint32_t)));
       t.seg_counts = sk->segc.as<uint32_t>();
+      t.w32 = f->tc.w32;
       sk->mark(4);
       ACE_CUDA(launch_convert_x_wide(t, sk->stream));
       sk->mark(6);

@@ -1372,14 +1372,77 @@ __global__ void __launch_bounds__(kKsThreads, 1) hash_tck_kernel(const TcArgs a)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
 }
 
-// Conversion for the K-streamed path: one warp per row, any d.
+// Conversion for the K-streamed path: one warp per row, any d.  With fp32
+// rows of 16-byte multiples the row is read as float4 (held in registers for
+// both passes when d <= 4096).
+__device__ __forceinline__ void wide_store(const TcArgs& a, uint64_t tile, uint32_t r, uint32_t k, float x0, float x1,
+                                           float x2, float x3, float& ss) {
+  ss = fmaf(x0, x0, fmaf(x1, x1, fmaf(x2, x2, fmaf(x3, x3, ss))));
+  const float h0 = __half2float(__float2half_rn(x0)), h1 = __half2float(__float2half_rn(x1));
+  const float h2 = __half2float(__float2half_rn(x2)), h3 = __half2float(__float2half_rn(x3));
+  uint8_t* blk = reinterpret_cast<uint8_t*>(a.x16) + ((tile * a.nkc + k / kChunk) * 2u) * kBlockBytes;
+  const uint32_t off = sw128_off(r, k % kChunk);
+  *reinterpret_cast<uint2*>(blk + off) = make_uint2(pack_h2(h0, h1), pack_h2(h2, h3));
+  *reinterpret_cast<uint2*>(blk + kBlockBytes + off) = make_uint2(pack_h2(x0 - h0, x1 - h1), pack_h2(x2 - h2, x3 - h3));
+}
+
 __global__ void __launch_bounds__(256) convert_x_wide_kernel(const TcArgs a, uint64_t rows_padded) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
   const uint32_t dpad = a.nkc * kChunk;
+  const bool vec = !a.x_f64 && (a.dim % 4 == 0) && (a.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0) &&
+                   dpad <= 4096;
   for (uint64_t row = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows_padded;
        row += warps) {
     const bool live = row < a.n;
+    const uint64_t tile = row / kRows;
+    const uint32_t r = static_cast<uint32_t>(row % kRows);
+    if (vec) {
+      // lane owns float4 groups lane, lane + 32, ... (k = 4 * group)
+      float4 v[32];
+      uint32_t mb = 0u;
+      const float4* xr = reinterpret_cast<const float4*>(static_cast<const float*>(a.x) + row * a.ld);
+#pragma unroll
+      for (uint32_t i = 0; i < 32; ++i) {
+        const uint32_t g = lane + 32u * i;
+        v[i] = (live && 4u * g < a.dim) ? xr[g] : make_float4(0.f, 0.f, 0.f, 0.f);
+        mb = max(mb, max(max(__float_as_uint(v[i].x) & 0x7fffffffu, __float_as_uint(v[i].y) & 0x7fffffffu),
+                         max(__float_as_uint(v[i].z) & 0x7fffffffu, __float_as_uint(v[i].w) & 0x7fffffffu)));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+      const bool nan = mb > 0x7f800000u;
+      const float m = __uint_as_float(nan ? 0x7f800000u : mb);
+      const bool zero = (m == 0.0f);
+      const bool wild = nan || !(m < 0x1.0p100f) || (!zero && m < 0x1.0p-100f);
+      float scale = 0.0f;
+      if (live && !zero && !wild) {
+        const int e = static_cast<int>((__float_as_uint(m) >> 23) & 0xffu) - 127;
+        scale = __uint_as_float(static_cast<uint32_t>(127 + 14 - e) << 23);
+      }
+      float ss = 0.0f;
+#pragma unroll
+      for (uint32_t i = 0; i < 32; ++i) {
+        const uint32_t k = 4u * (lane + 32u * i);
+        if (k < dpad)
+          wide_store(a, tile, r, k, v[i].x * scale, v[i].y * scale, v[i].z * scale, v[i].w * scale, ss);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) {
+        float thr;
+        if (!live || zero) {
+          thr = -1.0f;
+        } else if (wild) {
+          thr = __int_as_float(0x7f800000);
+        } else {
+          const float nx = sqrtf(ss * (1.0f + static_cast<float>(a.dim + 4) * 0x1.0p-23f)) * (1.0f + 0x1.0p-20f);
+          thr = a.margin_c * nx * 16384.0f + static_cast<float>(a.dim) * 0x1.0p-10f;
+        }
+        a.rowthr[row] = thr;
+      }
+      continue;
+    }
     uint32_t mb = 0u;
     if (live)
       for (uint32_t k = lane; k < a.dim; k += 32u) mb = max(mb, __float_as_uint(load_x(a, row, k)) & 0x7fffffffu);
@@ -1394,17 +1457,12 @@ __global__ void __launch_bounds__(256) convert_x_wide_kernel(const TcArgs a, uin
       const int e = static_cast<int>((__float_as_uint(m) >> 23) & 0xffu) - 127;
       scale = __uint_as_float(static_cast<uint32_t>(127 + 14 - e) << 23);
     }
-    const uint64_t tile = row / kRows;
-    const uint32_t r = static_cast<uint32_t>(row % kRows);
     float ss = 0.0f;
-    for (uint32_t k = 2u * lane; k < dpad; k += 64u) {
-      const float x0 = (live ? load_x(a, row, k) : 0.0f) * scale, x1 = (live ? load_x(a, row, k + 1) : 0.0f) * scale;
-      ss = fmaf(x0, x0, fmaf(x1, x1, ss));
-      const float h0 = __half2float(__float2half_rn(x0)), h1 = __half2float(__float2half_rn(x1));
-      uint8_t* blk = reinterpret_cast<uint8_t*>(a.x16) + ((tile * a.nkc + k / kChunk) * 2u) * kBlockBytes;
-      const uint32_t off = sw128_off(r, k % kChunk);
-      *reinterpret_cast<uint32_t*>(blk + off) = pack_h2(h0, h1);
-      *reinterpret_cast<uint32_t*>(blk + kBlockBytes + off) = pack_h2(x0 - h0, x1 - h1);
+    for (uint32_t k = 4u * lane; k < dpad; k += 128u) {
+      float xv[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) xv[e] = (live ? load_x(a, row, k + e) : 0.0f) * scale;
+      wide_store(a, tile, r, k, xv[0], xv[1], xv[2], xv[3], ss);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
@@ -1423,32 +1481,60 @@ __global__ void __launch_bounds__(256) convert_x_wide_kernel(const TcArgs a, uin
   }
 }
 
-// Near ties of the K-streamed kernel, one warp per list item.  Stage 1: the
-// projection in binary64 with FMAs across the warp, p1, and A = sum |x_i w_i|;
-// both p1 and the reference's left fold are within gamma_d * A of the exact
-// value, so |p1| > 2 gamma_d A (inflated) decides the reference's sign.
-// Stage 2 (rare): the reference's sequential fold itself (srp.cpp:78-91).
+__global__ void w32_round_kernel(const double* __restrict__ w64, uint64_t n, float* __restrict__ w32) {
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    w32[i] = static_cast<float>(w64[i]);
+}
+
+// Near ties of the K-streamed kernel, one warp per list item, kKsRbPerSeg
+// blocks per CTA segment.  Stage 1: p1 = sum x_i w32_i in binary64 (the
+// products of two fp32 values are exact), w32 = w rounded to fp32, and
+// A = sum |x_i w32_i|.  |p1 - sum x_i w_i| <= 2^-24 (1 + 2^-23) A + gamma_d A
+// and the reference's left fold is within gamma_d sum |x_i w_i| of the exact
+// value, so |p1| above the sum of both decides the reference's sign.
+// Stage 2 (rare): the reference's sequential binary64 fold (srp.cpp:78-91).
+constexpr uint32_t kKsRbPerSeg = 8;
+
 __global__ void __launch_bounds__(256) recheck_segs_kernel(const TcArgs a, uint32_t grid) {
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const unsigned long long seg_cap = a.near_cap / grid;
   const uint32_t K = a.k_bits;
-  const double gam = static_cast<double>(a.dim + 2) * 0x1.0p-53 / (1.0 - static_cast<double>(a.dim + 2) * 0x1.0p-53);
+  const uint32_t dim = static_cast<uint32_t>(a.dim);
+  const double gam = static_cast<double>(dim + 2) * 0x1.0p-53 / (1.0 - static_cast<double>(dim + 2) * 0x1.0p-53);
+  const double bound_rel = (0x1.0p-24 * (1.0 + 0x1.0p-22) + 3.0 * gam) * (1.0 + 4.0 * gam);
+  const bool vec = !a.x_f64 && (dim % 4 == 0) && (a.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
   unsigned long long rr = 0, ff = 0;
-  for (uint32_t b = blockIdx.x; b < grid; b += gridDim.x) {
+  const uint32_t b = blockIdx.x / kKsRbPerSeg, sub = blockIdx.x % kKsRbPerSeg;
+  if (b < grid) {
     unsigned long long* seg = a.near_list + b * seg_cap;
     const uint32_t cnt = static_cast<uint32_t>(min(static_cast<unsigned long long>(a.seg_counts[b]), seg_cap));
-    for (uint32_t i = wib; i < cnt; i += blockDim.x >> 5) {
+    const uint32_t stride = kKsRbPerSeg * (blockDim.x >> 5);
+    for (uint32_t i = sub * (blockDim.x >> 5) + wib; i < cnt; i += stride) {
       const unsigned long long item = seg[i];
       const uint64_t row = item >> 32;
       const uint32_t dir = static_cast<uint32_t>(item & 0xffffffffu);
-      const double* w = a.w64 + static_cast<uint64_t>(dir) * a.dim;
+      const float* w = a.w32 + static_cast<uint64_t>(dir) * dim;
       double p = 0.0, ab = 0.0;
-      for (uint32_t k = lane; k < a.dim; k += 32u) {
-        const double xv = a.x_f64 ? static_cast<const double*>(a.x)[row * a.ld + k]
-                                  : static_cast<double>(static_cast<const float*>(a.x)[row * a.ld + k]);
-        const double t = xv * __ldg(w + k);
-        p += t;
-        ab += fabs(t);
+      if (vec) {
+        const float4* xr = reinterpret_cast<const float4*>(static_cast<const float*>(a.x) + row * a.ld);
+        const float4* wr = reinterpret_cast<const float4*>(w);
+#pragma unroll 4
+        for (uint32_t k = lane; k < dim / 4u; k += 32u) {
+          const float4 xv = xr[k], wv = __ldg(wr + k);
+          const double t0 = static_cast<double>(xv.x) * wv.x, t1 = static_cast<double>(xv.y) * wv.y;
+          const double t2 = static_cast<double>(xv.z) * wv.z, t3 = static_cast<double>(xv.w) * wv.w;
+          p += (t0 + t1) + (t2 + t3);
+          ab += (fabs(t0) + fabs(t1)) + (fabs(t2) + fabs(t3));
+        }
+      } else {
+        for (uint32_t k = lane; k < dim; k += 32u) {
+          const double xv = a.x_f64 ? static_cast<const double*>(a.x)[row * a.ld + k]
+                                    : static_cast<double>(static_cast<const float*>(a.x)[row * a.ld + k]);
+          const double t = xv * static_cast<double>(__ldg(w + k));  // x fp64 input: products rounded (in gam)
+          p += t;
+          ab += fabs(t);
+        }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -1456,11 +1542,11 @@ __global__ void __launch_bounds__(256) recheck_segs_kernel(const TcArgs a, uint3
         ab += __shfl_xor_sync(0xffffffffu, ab, o);
       }
       int bit;
-      if (fabs(p) > 2.0 * gam * ab * (1.0 + 4.0 * gam) + 0x1.0p-1000) {
+      if (fabs(p) > bound_rel * ab + 0x1.0p-1000) {
         bit = p >= 0.0 ? 1 : 0;
       } else {
         double e = 0.0;
-        if (lane == 0) e = exact_proj(w, a.x, a.x_f64, row, a.ld, a.dim);
+        if (lane == 0) e = exact_proj(a.w64 + static_cast<uint64_t>(dir) * dim, a.x, a.x_f64, row, a.ld, dim);
         e = __shfl_sync(0xffffffffu, e, 0);
         bit = e >= 0.0 ? 1 : 0;
       }
@@ -1623,6 +1709,11 @@ cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc) {
     e = cudaFuncSetAttribute(hash_tck_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(ks_smem_bytes()));
     if (e != cudaSuccess) return e;
+    e = cudaMalloc(&tc->w32, sizeof(float) * f.rows * f.dim);
+    if (e != cudaSuccess) return e;
+    w32_round_kernel<<<1024, 256>>>(f.w64, static_cast<uint64_t>(f.rows) * f.dim, tc->w32);
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return e;
     tc->enabled = 1;
     return cudaSuccess;
   }
@@ -1641,6 +1732,8 @@ cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc) {
 void tc_free_family(TcFamily* tc) {
   if (tc->w16) cudaFree(tc->w16);
   tc->w16 = nullptr;
+  if (tc->w32) cudaFree(tc->w32);
+  tc->w32 = nullptr;
   tc->enabled = 0;
 }
 
@@ -1731,7 +1824,7 @@ cudaError_t launch_hash_tck(const TcArgs& a, cudaStream_t s) {
 cudaError_t launch_recheck_segs(const TcArgs& a, cudaStream_t s) {
   if (a.n == 0) return cudaSuccess;
   const uint32_t grid = tck_grid(a.n);
-  recheck_segs_kernel<<<grid, 256, 0, s>>>(a, grid);
+  recheck_segs_kernel<<<grid * kKsRbPerSeg, 256, 0, s>>>(a, grid);
   count_launch();
   return cudaGetLastError();
 }
