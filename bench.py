@@ -369,10 +369,12 @@ def main():
     if kernel == 2:
         kern_ms = phase[4]
         peak = pk["bf16_tflops"]
-        traffic = _profiled_traffic("hash_tc_kernel", args.config)
+        kname = "hash_tck_kernel" if w.dim > 256 else "hash_tc_kernel"
+        traffic = _profiled_traffic(kname, args.config)
         roofline = {
             "bound": "tensor",
-            "kernel": "hash_tc_kernel (tcgen05 fp16x3-split projection, TMEM accumulators, sign/near-tie/bucket epilogue)",
+            "kernel": (kname + " (tcgen05 fp16x3-split projection, TMEM accumulators, sign/near-tie/bucket epilogue"
+                       + (", A and W streamed in K chunks)" if w.dim > 256 else ")")),
             "achieved": flops / (kern_ms * 1e-3) / 1e12 if kern_ms > 0 else None,
             "peak": peak,
             "unit": "TFLOP/s",

@@ -212,9 +212,10 @@ def test_restore_clone_roundtrip(cuda):
     assert w.dim == 40
 
 
-@pytest.mark.parametrize("d", [1, 3, 63, 64, 65, 127, 129, 192, 255, 256])
+@pytest.mark.parametrize("d", [1, 3, 63, 64, 65, 127, 129, 192, 255, 256, 257, 300, 1000, 4096])
 def test_tc_dims_and_overflow_path(cuda, oracle_c, d):
-    """Every K-chunk count of the tcgen05 kernel; list-overflow rows (NaN rows
+    """Every K-chunk count of the tcgen05 kernel (d > 256: the K-streamed
+    kernel); list-overflow rows (NaN rows
     force every projection onto the exact path) still give exact ids."""
     k, l = 15, 20
     fam = ace.SrpFamily(ace.SrpConfig(dim=d, k_bits=k, num_tables=l, seed=d))
