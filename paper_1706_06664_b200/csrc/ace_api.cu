@@ -952,21 +952,36 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
     ev.resize(nb + 1);
     for (auto& e : ev) ACE_CUDA(cudaEventCreate(&e));
   }
-  for (uint64_t b = 0; b < nb; ++b) {
-    const uint64_t r0 = b * batch, rows = std::min(batch, n - r0);
-    if (batch_ms) ACE_CUDA(cudaEventRecord(ev[b], sk->stream));
-    const void* xb = static_cast<const char*>(x) + r0 * ld * esz;
+  // Hashing does not depend on the counts, so the batches of a group are
+  // hashed by one projection launch (its fixed cost amortised); scoring and
+  // insertion then run batch by batch in the reference's order.  A group's
+  // first batch latency includes the group's hashing.
+  static int group_env = -1;
+  if (group_env < 0) {
+    const char* e = getenv("ACE_STREAM_GROUP");
+    group_env = e ? std::max(1, atoi(e)) : 8;
+  }
+  const uint64_t G = static_cast<uint64_t>(group_env);
+  for (uint64_t g0 = 0; g0 < nb; g0 += G) {
+    const uint64_t gb = std::min(G, nb - g0), gr0 = g0 * batch, grows = std::min(gb * batch, n - gr0);
+    if (batch_ms) ACE_CUDA(cudaEventRecord(ev[g0], sk->stream));
+    const void* xg = static_cast<const char*>(x) + gr0 * ld * esz;
     const void* xd;
     uint64_t ldd;
-    r = stage_x(sk, sk->stage, sk->stream, xb, dtype, rows, ld, x_where, &xd, &ldd);
-    if (r == ACE_OK) r = run_hash(sk, xd, dtype, rows, ldd, 0);
+    r = stage_x(sk, sk->stage, sk->stream, xg, dtype, grows, ld, x_where, &xd, &ldd);
+    if (r == ACE_OK) r = run_hash(sk, xd, dtype, grows, ldd, 0);
     if (r != ACE_OK) return r;
-    ACE_CUDA(cudaMemsetAsync(&sk->st->batch_sum, 0, sizeof(unsigned long long), sk->stream));
-    ACE_CUDA(launch_stream_score(sk->ids.as<uint32_t>(), rows, f->d.tables, f->d.k_bits, sk->counters, alpha,
-                                 dflags + r0 / 32, nullptr, sk->st, sk->stream));
-    ACE_CUDA(launch_apply_ids(sk->ids.as<uint32_t>(), rows, f->d.tables, f->d.k_bits, sk->counters, sk->cap, +1,
-                              sk->st, sk->stream, !ff));
-    if (sk->width == 16) ACE_CUDA(launch_cap(sk->counters, sk->num_counters, sk->cap, sk->st, sk->stream));
+    for (uint64_t b = g0; b < g0 + gb; ++b) {
+      const uint64_t r0 = b * batch, rows = std::min(batch, n - r0);
+      if (batch_ms && b != g0) ACE_CUDA(cudaEventRecord(ev[b], sk->stream));
+      const uint32_t* ids = sk->ids.as<uint32_t>() + (r0 - gr0);
+      ACE_CUDA(cudaMemsetAsync(&sk->st->batch_sum, 0, sizeof(unsigned long long), sk->stream));
+      ACE_CUDA(launch_stream_score(ids, rows, f->d.tables, f->d.k_bits, sk->counters, alpha, dflags + r0 / 32,
+                                   nullptr, sk->st, sk->stream, grows));
+      ACE_CUDA(launch_apply_ids(ids, rows, f->d.tables, f->d.k_bits, sk->counters, sk->cap, +1, sk->st, sk->stream,
+                                !ff, grows));
+      if (sk->width == 16) ACE_CUDA(launch_cap(sk->counters, sk->num_counters, sk->cap, sk->st, sk->stream));
+    }
   }
   if (batch_ms) ACE_CUDA(cudaEventRecord(ev[nb], sk->stream));
   if (flag_bits && out_where == ACE_HOST)

@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(NT, 2) hash_simt_kernel(const HashArgs a) {
 
 // ---- counters from ids (streaming insert / remove) -------------------------
 
-__global__ void apply_ids_kernel(const uint32_t* __restrict__ ids, uint64_t n, uint32_t tables,
+__global__ void apply_ids_kernel(const uint32_t* __restrict__ ids, uint64_t n, uint64_t ids_stride, uint32_t tables,
                                  uint32_t k_bits, uint32_t* counters, uint32_t cap, int sign,
                                  DevState* st) {
   __shared__ unsigned long long blk;
@@ -369,7 +369,7 @@ __global__ void apply_ids_kernel(const uint32_t* __restrict__ ids, uint64_t n, u
     unsigned long long key = 0ull;
     if (valid) {
       const uint64_t t = idx / n;
-      key = (t << k_bits) | ids[idx];
+      key = (t << k_bits) | ids[t * ids_stride + (idx - t * n)];
     }
     // up to three ballot rounds aggregate runs of equal counters, then the
     // remaining lanes update individually
@@ -472,7 +472,7 @@ template <bool kTrackT>
 __global__ void __launch_bounds__(1024) apply_ids_smem_kernel(const uint32_t* __restrict__ ids, uint64_t n,
                                                               uint32_t tables, uint32_t k_bits, uint32_t part_bits,
                                                               uint64_t per, uint32_t* counters, uint32_t cap,
-                                                              DevState* st) {
+                                                              DevState* st, uint64_t ids_stride) {
   extern __shared__ uint32_t hist[];
   __shared__ unsigned long long blk;
   const uint32_t nb = 1u << part_bits;
@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(1024) apply_ids_smem_kernel(const uint32_t* __
     __syncthreads();
     for (uint64_t base = seg; base < seg_end; base += step) {
       const uint32_t len = static_cast<uint32_t>(min(seg_end - base, static_cast<uint64_t>(step)));
-      const uint32_t* src = ids + base;
+      const uint32_t* src = ids + t * ids_stride + (base - t * n);
       // all loads issued before any use (clamped addresses, no branches)
       uint32_t idv[kDepth];
 #pragma unroll
@@ -837,7 +837,7 @@ __device__ double sketch_mean(const DevState* st, uint32_t tables) {
   return static_cast<double>(q) + static_cast<double>(r) / static_cast<double>(den);
 }
 
-__global__ void stream_score_kernel(const uint32_t* __restrict__ ids, uint64_t n, uint32_t tables,
+__global__ void stream_score_kernel(const uint32_t* __restrict__ ids, uint64_t n, uint64_t ids_stride, uint32_t tables,
                                     uint32_t k_bits, const uint32_t* __restrict__ counters,
                                     double alpha, uint32_t* __restrict__ flag_bits,
                                     double* __restrict__ scores, DevState* st) {
@@ -869,13 +869,13 @@ __global__ void stream_score_kernel(const uint32_t* __restrict__ ids, uint64_t n
       for (; t + 8 <= tables; t += 8) {
         uint32_t b[8], c[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) b[u] = ids[(uint64_t)(t + u) * n + i];
+        for (int u = 0; u < 8; ++u) b[u] = ids[(uint64_t)(t + u) * ids_stride + i];
 #pragma unroll
         for (int u = 0; u < 8; ++u) c[u] = counters[((uint64_t)(t + u) << k_bits) + b[u]];
 #pragma unroll
         for (int u = 0; u < 8; ++u) S += c[u];
       }
-      for (; t < tables; ++t) S += counters[((uint64_t)t << k_bits) + ids[(uint64_t)t * n + i]];
+      for (; t < tables; ++t) S += counters[((uint64_t)t << k_bits) + ids[(uint64_t)t * ids_stride + i]];
       bsum += S;
       const double sc = __ddiv_rn(static_cast<double>(S), L);
       if (scores) scores[i] = sc;
@@ -927,8 +927,9 @@ cudaError_t launch_hash_simt(const HashArgs& a, cudaStream_t s) {
 
 cudaError_t launch_apply_ids(const uint32_t* ids, uint64_t n, uint32_t tables, uint32_t k_bits,
                              uint32_t* counters, uint32_t cap, int sign, DevState* st,
-                             cudaStream_t s, bool track_t) {
+                             cudaStream_t s, bool track_t, uint64_t ids_stride) {
   if (n == 0) return cudaSuccess;
+  if (ids_stride == 0) ids_stride = n;
   if (sign > 0 && k_bits <= 20 && n >= 4096) {
     static bool configured = false;
     if (!configured) {
@@ -957,10 +958,11 @@ cudaError_t launch_apply_ids(const uint32_t* ids, uint64_t n, uint32_t tables, u
     const unsigned grid = static_cast<unsigned>((total + per - 1) / per) * parts;
     const size_t smem = sizeof(uint32_t) << part_bits;
     if (track_t) {
-      apply_ids_smem_kernel<true><<<grid, 1024, smem, s>>>(ids, n, tables, k_bits, part_bits, per, counters, cap, st);
+      apply_ids_smem_kernel<true><<<grid, 1024, smem, s>>>(ids, n, tables, k_bits, part_bits, per, counters, cap, st,
+                                                            ids_stride);
     } else {
       apply_ids_smem_kernel<false><<<grid, 1024, smem, s>>>(ids, n, tables, k_bits, part_bits, per, counters, cap,
-                                                             st);
+                                                             st, ids_stride);
       // T = sum of squared counters (exact for unsaturated 32-bit sketches)
       cudaMemsetAsync(&st->T, 0, sizeof(st->T), s);
       const uint64_t num = static_cast<uint64_t>(tables) << k_bits;
@@ -970,7 +972,7 @@ cudaError_t launch_apply_ids(const uint32_t* ids, uint64_t n, uint32_t tables, u
     count_launch();
     return cudaGetLastError();
   }
-  apply_ids_kernel<<<grid_for(n * tables, 256), 256, 0, s>>>(ids, n, tables, k_bits, counters, cap,
+  apply_ids_kernel<<<grid_for(n * tables, 256), 256, 0, s>>>(ids, n, ids_stride, tables, k_bits, counters, cap,
                                                              sign, st);
   count_launch();
   return cudaGetLastError();
@@ -1027,10 +1029,10 @@ cudaError_t launch_replay(const uint64_t* sums, uint64_t n, uint32_t tables, Dev
 
 cudaError_t launch_stream_score(const uint32_t* ids, uint64_t n, uint32_t tables, uint32_t k_bits,
                                 const uint32_t* counters, double alpha, uint32_t* flag_bits,
-                                double* scores, DevState* st, cudaStream_t s) {
+                                double* scores, DevState* st, cudaStream_t s, uint64_t ids_stride) {
   if (n == 0) return cudaSuccess;
-  stream_score_kernel<<<grid_for(n, 256), 256, 0, s>>>(ids, n, tables, k_bits, counters, alpha,
-                                                       flag_bits, scores, st);
+  stream_score_kernel<<<grid_for(n, 256), 256, 0, s>>>(ids, n, ids_stride ? ids_stride : n, tables, k_bits,
+                                                       counters, alpha, flag_bits, scores, st);
   count_launch();
   return cudaGetLastError();
 }

@@ -30,7 +30,8 @@ size_t hash_simt_smem_bytes();
 //   sum c^2 instead of accumulated from returned pre-add values.
 cudaError_t launch_apply_ids(const uint32_t* ids, uint64_t n, uint32_t tables,
                              uint32_t k_bits, uint32_t* counters, uint32_t cap,
-                             int sign, DevState* st, cudaStream_t s, bool track_t = true);
+                             int sign, DevState* st, cudaStream_t s, bool track_t = true,
+                             uint64_t ids_stride = 0);  // 0: n
 // Remove validation: counts, per counter, how many removals target it and
 // flags underflow (any count < demand).  scratch: L x 2^K u32, zeroed here.
 cudaError_t launch_remove_check(const uint32_t* ids, uint64_t n, uint32_t tables,
@@ -62,7 +63,7 @@ cudaError_t launch_replay(const uint64_t* sums, uint64_t n, uint32_t tables,
 cudaError_t launch_stream_score(const uint32_t* ids, uint64_t n, uint32_t tables,
                                 uint32_t k_bits, const uint32_t* counters,
                                 double alpha, uint32_t* flag_bits, double* scores,
-                                DevState* st, cudaStream_t s);
+                                DevState* st, cudaStream_t s, uint64_t ids_stride = 0);  // 0: n
 
 // Sum of squares of all counters (T after restore with exact state).
 cudaError_t launch_sum_squares(const uint32_t* counters, uint64_t num,
