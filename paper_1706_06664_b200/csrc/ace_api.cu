@@ -248,6 +248,7 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
     t.tpt = f->d.tpt;
     t.ntiles = f->tc.ntiles;
     t.nkc = f->tc.nkc;
+    t.tw = f->tc.tw;
     t.w16 = f->tc.w16;
     tc_fill_tables(&t);
     // error bound of the fp16x3 split relative to ||x~|| ||w^||
@@ -303,7 +304,7 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
       const char* e = getenv("ACE_FUSE_CONVERT");
       fuse_env = e ? atoi(e) : 0;
     }
-    t.fuse_convert = fuse_env != 0 && !t.x_f64 && ld == f->d.dim && (reinterpret_cast<uintptr_t>(xd) & 15) == 0 &&
+    t.fuse_convert = fuse_env != 0 && t.tw == 128 && !t.x_f64 && ld == f->d.dim && (reinterpret_cast<uintptr_t>(xd) & 15) == 0 &&
                      tc_fuse_ok_dim(f->d.dim, f->tc.nkc);
     if (kstream) {
       // d > 256: K-streamed kernel with its own conversion and recheck

@@ -72,19 +72,22 @@ struct TcLayout {
 // tcgen05.cp has moved it into TMEM), with the fused conversion a raw fp32 X
 // tile (128 rows, bulk-copied), then a ring of W stages (32 KB each).  TMEM:
 // accumulators of 128 columns, then the A operand (hi | lo, dpad columns).
-__host__ __device__ inline uint32_t tc_acc_bufs(uint32_t nkc) { return nkc <= 2 ? 3u : 2u; }
+__host__ __device__ inline uint32_t tc_acc_bufs(uint32_t nkc, uint32_t tw = 128) {
+  return tw > 128 ? 2u : (nkc <= 2 ? 3u : 2u);
+}
 
-__host__ __device__ inline TcLayout tc_layout(uint32_t nkc, uint64_t dim = 0, bool fuse = false) {
+__host__ __device__ inline TcLayout tc_layout(uint32_t nkc, uint64_t dim = 0, bool fuse = false, uint32_t tw = 128) {
   TcLayout L;
   L.nkc = nkc;
   L.n_abuf = 1;
   L.a_bytes = static_cast<size_t>(L.n_abuf) * nkc * 2 * kBlockBytes;
   L.raw_bytes = fuse ? (static_cast<size_t>(kRows) * dim * 4 + 1023) / 1024 * 1024 : 0;
   const size_t room = kSmemLimit - 8192 - 1024 - L.a_bytes - L.raw_bytes;  // static smem + align
-  size_t st = room / (2 * kBlockBytes / kPair);  // a stage: hi + lo of this CTA's share of a W tile
+  const size_t stage = 2u * tw * 128u / kPair;  // a stage: hi + lo of this CTA's share of a W tile
+  size_t st = room / stage;
   if (st > kMaxWStages) st = kMaxWStages;
   L.n_wst = static_cast<uint32_t>(st);
-  L.w_bytes = static_cast<size_t>(L.n_wst) * 2 * kBlockBytes / kPair;
+  L.w_bytes = static_cast<size_t>(L.n_wst) * stage;
   L.total = L.a_bytes + L.raw_bytes + L.w_bytes + 1024;
   return L;
 }
@@ -628,7 +631,8 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
   __shared__ __align__(8) uint64_t bar_rawfull, bar_rawempty, bar_thrfull[2], bar_threempty[2];
   __shared__ float thr_sm[2][kRows];  // fused conversion: row thresholds per tile parity
 
-  TcLayout L = tc_layout(a.nkc, a.dim, kFuse);
+  TcLayout L = tc_layout(a.nkc, a.dim, kFuse, a.tw);
+  const uint32_t TW = a.tw, wblk = a.tw * 128u;  // direction tile width, one W block (hi or lo) in bytes
   if (a.dbg >> 12) L.n_wst = min(L.n_wst, static_cast<uint32_t>(a.dbg >> 12));  // experiment: fewer W stages
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* Asm = base;                               // [n_abuf][nkc][2][16 KB]
@@ -730,16 +734,17 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
           bulk_g2s(Asm, reinterpret_cast<const uint8_t*>(a.x16) + tt * a_tile_bytes, a_tile_bytes, &bar_afull[0]);
         }
         for (uint32_t j = 0; j < a.ntiles; ++j) {
-          const uint32_t nmma = kPair == 2 ? 128u : ((min(128u, R - j * 128u) + 15u) & ~15u);
+          const uint32_t nmma = kPair == 2 ? 128u : ((min(TW, R - j * TW) + 15u) & ~15u);
           const uint32_t bytes = kPair == 2 ? share : nmma * 128u;
+          const uint32_t hblk = kPair == 2 ? half : wblk;  // stage layout: hi block, then lo block
           for (uint32_t kc = 0; kc < a.nkc; ++kc) {
             mbar_wait_sleepy(&bar_wempty[s], ph ^ 1u, prof ? &pw[1] : nullptr);
             mbar_expect_tx(&bar_wfull[s], 2u * bytes);
             const uint8_t* src = reinterpret_cast<const uint8_t*>(a.w16) +
-                                 (static_cast<uint64_t>(j) * a.nkc + kc) * 2u * kBlockBytes + rank * share;
-            uint8_t* dst = Wsm + static_cast<size_t>(s) * 2u * half;
+                                 (static_cast<uint64_t>(j) * a.nkc + kc) * 2u * wblk + rank * share;
+            uint8_t* dst = Wsm + static_cast<size_t>(s) * 2u * hblk;
             bulk_g2s(dst, src, bytes, &bar_wfull[s]);
-            bulk_g2s(dst + half, src + kBlockBytes, bytes, &bar_wfull[s]);
+            bulk_g2s(dst + hblk, src + wblk, bytes, &bar_wfull[s]);
             if (++s == L.n_wst) {
               s = 0;
               ph ^= 1u;
@@ -778,10 +783,10 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
       uint32_t s = 0, wph = 0, acc = 0, accph = 0;
       unsigned long long pmi = 0, pmn = 0, pcp = 0;  // instrumentation: MMA-group issue cycles / groups, A copies
       const long long ploop = clock64();
-      const uint32_t nacc = tc_acc_bufs(a.nkc);
-      const uint32_t ta_hi = tmem_base + nacc * 128u, ta_lo = ta_hi + a.nkc * 32u;  // dpad/2 columns each
+      const uint32_t nacc = tc_acc_bufs(a.nkc, TW);
+      const uint32_t ta_hi = tmem_base + nacc * TW, ta_lo = ta_hi + a.nkc * 32u;  // dpad/2 columns each
       const uint32_t a_base = smem_u32(Asm), w_base = smem_u32(Wsm);
-      const uint32_t half = kBlockBytes / kPair;  // bytes of one W block (hi or lo) per CTA
+      const uint32_t half = kPair == 2 ? kBlockBytes / kPair : wblk;  // bytes of one W block (hi or lo) per CTA
       for (uint64_t it = 0; it < iters; ++it) {
         mbar_wait_t(&bar_afull[0], static_cast<uint32_t>(it) & 1u, (prof && lane == 0) ? &pw[2] : nullptr);
         tc_after();
@@ -802,11 +807,11 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
         __syncwarp();
         if (prof) pcp += static_cast<unsigned long long>(clock64() - pc0);
         for (uint32_t j = 0; j < a.ntiles; ++j) {
-          const uint32_t nmma = kPair == 2 ? 128u : ((min(128u, R - j * 128u) + 15u) & ~15u);
+          const uint32_t nmma = kPair == 2 ? 128u : ((min(TW, R - j * TW) + 15u) & ~15u);
           const uint32_t idesc = idesc_f16(nmma);
           mbar_wait_t(&bar_accempty[acc], accph ^ 1u, (prof && lane == 0) ? &pw[3] : nullptr);
           tc_after();
-          const uint32_t dt = tmem_base + acc * 128u;
+          const uint32_t dt = tmem_base + acc * TW;
           // one elected burst per direction tile: the issuing lane waits for
           // each stage itself (no warp-wide syncs between the MMA groups, so
           // the tensor queue is refilled without gaps)
@@ -964,7 +969,8 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
     const uint32_t q = warp & 3, h = (warp - 2) >> 2;
     const uint32_t r = q * 32u + lane;
     const uint32_t kmask = (K >= 32u) ? 0xffffffffu : ((1u << K) - 1u);
-    const uint32_t nacc = tc_acc_bufs(a.nkc);
+    const uint32_t nacc = tc_acc_bufs(a.nkc, TW);
+    const uint32_t nwords = TW / 32u;  // sign words per direction tile (4 or 6)
     const uint64_t g_total = iters * a.ntiles;
     uint32_t acc = 0, accph = 0;
     uint64_t g = 0;
@@ -987,21 +993,22 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
       const uint32_t thr_u = zero_row ? 0u : (isinf(thr) ? 0xffffffffu : (__float_as_uint(thr) << 1));
       for (uint32_t j = 0; j < a.ntiles; ++j, ++g) {
         if ((g & 1u) == h) {
-          const uint32_t used = min(128u, R - j * 128u);
-          const uint32_t col0 = j * 128u;
+          const uint32_t used = min(TW, R - j * TW);
+          const uint32_t col0 = j * TW;
           mbar_wait_sleepy(&bar_accfull[acc], accph, (prof && lane == 0) ? &pw[5] : nullptr);
           tc_after();
           long long pc0 = prof ? clock64() : 0, pc1 = 0, pc2 = 0;
           uint32_t wd0 = 0xffffffffu, wd1 = 0xffffffffu, wd2 = 0xffffffffu, wd3 = 0xffffffffu;
+          uint32_t wd4 = 0xffffffffu, wd5 = 0xffffffffu;
           if (!(a.dbg & 1)) {
             // one copy of the 64-column code (small instruction footprint)
 #pragma unroll 1
-            for (uint32_t hr = 0; hr < 2; ++hr) {
+            for (uint32_t hr = 0; hr < nwords / 2u; ++hr) {
               const uint32_t c0 = 64u * hr;
               if (c0 >= used) break;
               uint32_t v[64];
-              ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + acc * 128u + c0, v);
-              ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + acc * 128u + c0 + 32u, (v + 32));
+              ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + acc * TW + c0, v);
+              ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + acc * TW + c0 + 32u, (v + 32));
               tmem_wait_ld();
               if (prof && hr == 0) pc1 = clock64();
               uint32_t w2[2];
@@ -1040,9 +1047,12 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
               if (hr == 0) {
                 wd0 = w2[0];
                 wd1 = w2[1];
-              } else {
+              } else if (hr == 1) {
                 wd2 = w2[0];
                 wd3 = w2[1];
+              } else {
+                wd4 = w2[0];
+                wd5 = w2[1];
               }
             }
           }
@@ -1070,20 +1080,32 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
           }
           // publish this tile's last word for the partner (next tile's owner)
           if (g + 1 < g_total) {
-            lastw[q][g & 1u][lane] = wd3;
+            lastw[q][g & 1u][lane] = nwords == 4u ? wd3 : wd5;
             asm volatile("bar.arrive %0, 64;" ::"r"((h == 0 ? 1u : 5u) + q) : "memory");
           }
           // buckets of the tables whose last column lies in this tile (host
           // precomputed range): bits [t*K, t*K+K) of the big-endian column
-          // stream, words 4j-1 (prev) .. 4j+3 (wd)
+          // stream, words nwords*j-1 (prev) .. nwords*j+nwords-1 (wd)
           const uint32_t tb = j == 0 ? 0u : a.tab_end[j - 1], te = a.tab_end[j];
           uint32_t* idp = a.ids + row;
           for (uint32_t tt = tb; tt < te; ++tt) {
             const uint32_t s0 = tt * K;
-            const int wi = static_cast<int>(s0 >> 5) - static_cast<int>(4 * j);  // -1 .. 3
+            const int wi = static_cast<int>(s0 >> 5) - static_cast<int>(nwords * j);  // -1 .. nwords-1
             const uint32_t off = s0 & 31u;
-            const uint32_t hi = wi < 0 ? prev : wi == 0 ? wd0 : wi == 1 ? wd1 : wi == 2 ? wd2 : wd3;
-            const uint32_t lo = wi < 0 ? wd0 : wi == 0 ? wd1 : wi == 1 ? wd2 : wi == 2 ? wd3 : 0u;
+            const uint32_t hi = wi < 0    ? prev
+                                : wi == 0 ? wd0
+                                : wi == 1 ? wd1
+                                : wi == 2 ? wd2
+                                : wi == 3 ? wd3
+                                : wi == 4 ? wd4
+                                          : wd5;
+            const uint32_t lo = wi < 0    ? wd0
+                                : wi == 0 ? wd1
+                                : wi == 1 ? wd2
+                                : wi == 2 ? wd3
+                                : wi == 3 ? wd4
+                                : wi == 4 ? wd5
+                                          : 0u;
             const unsigned long long win = (static_cast<unsigned long long>(hi) << 32) | lo;
             const uint32_t bucket = static_cast<uint32_t>(win >> (64u - off - K)) & kmask;
             if (valid && (!(a.dbg & 128) || bucket == 0xffffffffu)) idp[static_cast<uint64_t>(tt) * a.n] = bucket;
@@ -1647,23 +1669,24 @@ __global__ void dir_norm_kernel(const double* __restrict__ w64, uint64_t dim, ui
 }
 
 __global__ void pack_w16_kernel(const double* __restrict__ w64, const double* __restrict__ inv,
-                                FamilyDev f, uint32_t ntiles, uint32_t nkc, uint16_t* w16) {
-  const uint64_t total = static_cast<uint64_t>(ntiles) * kRows * nkc * kChunk;
+                                FamilyDev f, uint32_t ntiles, uint32_t nkc, uint32_t tw, uint16_t* w16) {
+  const uint64_t total = static_cast<uint64_t>(ntiles) * tw * nkc * kChunk;
+  const uint32_t wblk = tw * 128u;
   for (uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
        idx += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint32_t k = idx % (nkc * kChunk);
-    const uint32_t rr = (idx / (nkc * kChunk)) % kRows;
-    const uint32_t j = static_cast<uint32_t>(idx / (static_cast<uint64_t>(nkc) * kChunk * kRows));
+    const uint32_t rr = (idx / (nkc * kChunk)) % tw;
+    const uint32_t j = static_cast<uint32_t>(idx / (static_cast<uint64_t>(nkc) * kChunk * tw));
     const uint32_t kc = k / kChunk, kk = k % kChunk;
-    const uint64_t dir = static_cast<uint64_t>(j) * kRows + rr;  // directions packed densely
+    const uint64_t dir = static_cast<uint64_t>(j) * tw + rr;  // directions packed densely
     double w = 0.0;
     if (dir < f.rows && k < f.dim) w = w64[dir * f.dim + k] * inv[dir];
     const __half hi = __double2half(w);
     const __half lo = __double2half(w - static_cast<double>(__half2float(hi)));
-    uint8_t* blk = reinterpret_cast<uint8_t*>(w16) + ((static_cast<uint64_t>(j) * nkc + kc) * 2) * kBlockBytes;
+    uint8_t* blk = reinterpret_cast<uint8_t*>(w16) + ((static_cast<uint64_t>(j) * nkc + kc) * 2) * wblk;
     const uint32_t off = rr * 128u + ((((kk >> 3) ^ (rr & 7u)) & 7u) << 4) + ((kk & 7u) << 1);
     *reinterpret_cast<__half*>(blk + off) = hi;
-    *reinterpret_cast<__half*>(blk + kBlockBytes + off) = lo;
+    *reinterpret_cast<__half*>(blk + wblk + off) = lo;
   }
 }
 
@@ -1679,7 +1702,7 @@ bool tc_fuse_ok_dim(uint64_t dim, uint32_t nkc) {
 
 void tc_fill_tables(TcArgs* a) {
   for (uint32_t j = 0; j < a->ntiles && j < 64; ++j) {
-    const uint32_t end_col = std::min((j + 1) * 128u, a->k_bits * a->tables);
+    const uint32_t end_col = std::min((j + 1) * a->tw, a->k_bits * a->tables);
     a->tab_end[j] = static_cast<uint16_t>(std::min(end_col / a->k_bits, a->tables));
   }
 }
@@ -1690,17 +1713,27 @@ cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc) {
   tc->enabled = 0;
   if (!tc_supported(f.dim) || f.k_bits > 128) return cudaSuccess;
   const uint32_t nkc = static_cast<uint32_t>((f.dim + kChunk - 1) / kChunk);
-  const TcLayout L = tc_layout(nkc);
-  if ((!tc_kstream(nkc) && tc_layout(nkc).n_wst < 2) || f.rows > 64u * 128u || kPair != 1) return cudaSuccess;
+  // 192-direction tiles (MMA N = 192, two accumulators) for d <= 128: a third
+  // fewer MMA instructions and epilogue hand-offs than 128-direction tiles
+  static int tw_env = -1;
+  if (tw_env < 0) {
+    const char* e = getenv("ACE_TW");
+    tw_env = e ? atoi(e) : 192;
+  }
+  const uint32_t tw = (kPair == 1 && nkc <= 2 && tw_env == 192) ? 192u : 128u;
+  const TcLayout L = tc_layout(nkc, 0, false, tw);
+  if ((!tc_kstream(nkc) && L.n_wst < 2) || (tc_kstream(nkc) && kPair != 1)) return cudaSuccess;
   tc->nkc = nkc;
-  tc->ntiles = (f.rows + kRows - 1) / kRows;
-  const size_t bytes = static_cast<size_t>(tc->ntiles) * nkc * 2 * kBlockBytes;
+  tc->tw = tw;
+  tc->ntiles = (f.rows + tw - 1) / tw;
+  if (tc->ntiles > 64) return cudaSuccess;  // TcArgs::tab_end
+  const size_t bytes = static_cast<size_t>(tc->ntiles) * nkc * 2 * tw * 128u;
   cudaError_t e = cudaMalloc(&tc->w16, bytes);
   if (e != cudaSuccess) return e;
   double* inv = nullptr;
   if ((e = cudaMalloc(&inv, sizeof(double) * f.rows)) != cudaSuccess) return e;
   dir_norm_kernel<<<(f.rows + 127) / 128, 128>>>(f.w64, f.dim, f.rows, inv);
-  pack_w16_kernel<<<1024, 256>>>(f.w64, inv, f, tc->ntiles, nkc, tc->w16);
+  pack_w16_kernel<<<1024, 256>>>(f.w64, inv, f, tc->ntiles, nkc, tw, tc->w16);
   count_launch(2);
   e = cudaDeviceSynchronize();
   cudaFree(inv);
@@ -1720,7 +1753,7 @@ cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc) {
   e = cudaFuncSetAttribute(hash_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(L.total));
   if (e != cudaSuccess) return e;
-  if (tc_fuse_ok_dim(f.dim, tc->nkc)) {
+  if (tw == 128 && tc_fuse_ok_dim(f.dim, tc->nkc)) {
     e = cudaFuncSetAttribute(hash_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(tc_layout(tc->nkc, f.dim, true).total));
     if (e != cudaSuccess) return e;
@@ -1752,7 +1785,7 @@ cudaError_t launch_hash_tc(const TcArgs& a, cudaStream_t s) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = tc_layout(a.nkc, a.dim, a.fuse_convert != 0).total;
+  cfg.dynamicSmemBytes = tc_layout(a.nkc, a.dim, a.fuse_convert != 0, a.tw).total;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;

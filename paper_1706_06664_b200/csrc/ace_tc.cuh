@@ -14,7 +14,8 @@ struct TcFamily {
   uint16_t* w16 = nullptr;   // [ntiles][nkc][2][128*64] fp16 (swizzled)
   float* w32 = nullptr;      // K-streamed recheck: W rounded to fp32, [rows][dim]
   uint32_t nkc = 0;          // K-chunks of 64: dpad64 / 64
-  uint32_t ntiles = 0;       // 128-direction tiles (directions packed densely)
+  uint32_t ntiles = 0;       // direction tiles of tw directions (packed densely)
+  uint32_t tw = 128;         // direction tile width: 192 (d <= 128) or 128
   int enabled = 0;
 };
 
@@ -23,6 +24,7 @@ struct TcArgs {
   int x_f64;
   uint64_t n, ld, dim;
   uint32_t k_bits, tables, tpt, ntiles, nkc;
+  uint32_t tw;                // direction tile width (MMA N): 128 or 192
   const uint16_t* w16;
   uint16_t* x16;              // converted x tiles (pre-pass output), SW128 image
   float* rowthr;              // per-row error threshold (pre-pass output)
