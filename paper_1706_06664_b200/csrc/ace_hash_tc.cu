@@ -45,6 +45,9 @@ constexpr int kMaxWStages = 12;
 #ifndef ACE_SLEEPY
 #define ACE_SLEEPY 64  // ns back-off of off-critical-path barrier waits (0: spin)
 #endif
+#ifndef ACE_TILE_BURST
+#define ACE_TILE_BURST 0  // MMA issuer: 1 = one elected burst per point tile (measured slower), 0 = per direction tile
+#endif
 #ifndef ACE_KC_FENCE
 #define ACE_KC_FENCE 0
 #endif
@@ -806,6 +809,60 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
         }
         __syncwarp();
         if (prof) pcp += static_cast<unsigned long long>(clock64() - pc0);
+#if ACE_TILE_BURST
+        // one elected burst per point tile: the issuing lane waits for the
+        // accumulators and W stages itself, no warp-wide syncs in between
+        const long long pi0 = prof ? clock64() : 0;
+        if (elect_one()) {
+          uint32_t ss = s, ph = wph, ac = acc, acph = accph;
+          for (uint32_t j = 0; j < a.ntiles; ++j) {
+            const uint32_t nmma = kPair == 2 ? 128u : ((min(TW, R - j * TW) + 15u) & ~15u);
+            const uint32_t idesc = idesc_f16(nmma);
+            mbar_wait(&bar_accempty[ac], acph ^ 1u);
+            tc_after();
+            const uint32_t dt = tmem_base + ac * TW;
+            for (uint32_t kc = 0; kc < a.nkc; ++kc) {
+              mbar_wait(&bar_wfull[ss], ph);
+              const uint32_t b_hi = w_base + ss * 2u * half;
+              const uint64_t dbh = sw128_desc(b_hi), dbl = sw128_desc(b_hi + half);
+#pragma unroll
+              for (uint32_t kk = 0; kk < 4; ++kk) {
+                const uint32_t acol = (kc * 4u + kk) * 8u;
+                const uint64_t off = kk * 2u;
+                mma_f16_ts(dt, ta_hi + acol, dbh + off, idesc, (kc | kk) != 0u);
+                mma_f16_ts(dt, ta_lo + acol, dbh + off, idesc, 1u);
+                mma_f16_ts(dt, ta_hi + acol, dbl + off, idesc, 1u);
+              }
+              mma_commit(&bar_wempty[ss]);
+              if (++ss == L.n_wst) {
+                ss = 0;
+                ph ^= 1u;
+              }
+            }
+            mma_commit(&bar_accfull[ac]);
+            if (++ac == nacc) {
+              ac = 0;
+              acph ^= 1u;
+            }
+          }
+        }
+        __syncwarp();
+        for (uint32_t j = 0; j < a.ntiles; ++j) {
+          for (uint32_t kc = 0; kc < a.nkc; ++kc)
+            if (++s == L.n_wst) {
+              s = 0;
+              wph ^= 1u;
+            }
+          if (++acc == nacc) {
+            acc = 0;
+            accph ^= 1u;
+          }
+        }
+        if (prof) {
+          pmi += static_cast<unsigned long long>(clock64() - pi0);
+          pmn += a.nkc * a.ntiles;
+        }
+#else
         for (uint32_t j = 0; j < a.ntiles; ++j) {
           const uint32_t nmma = kPair == 2 ? 128u : ((min(TW, R - j * TW) + 15u) & ~15u);
           const uint32_t idesc = idesc_f16(nmma);
@@ -855,6 +912,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
             accph ^= 1u;
           }
         }
+#endif
       }
       if (prof && pmn && lane == 0) {
         atomicAdd(&a.prof[20], pmi);
@@ -1591,45 +1649,6 @@ __global__ void __launch_bounds__(256) recheck_segs_kernel(const TcArgs a, uint3
 }
 
 // ---- near-tie recheck ------------------------------------------------------------
-
-__global__ void recheck_list_kernel(const TcArgs a, const double* __restrict__ w64) {
-  __shared__ unsigned long long blk_r, blk_f;
-  if (threadIdx.x == 0) blk_r = blk_f = 0;
-  __syncthreads();
-  const unsigned long long cnt = min(a.st->near_count, a.near_cap);
-  const uint32_t K = a.k_bits;
-  unsigned long long rr = 0, ff = 0;
-  for (unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
-       i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
-    const unsigned long long item = a.near_list[i];
-    const uint64_t row = item >> 32;
-    const uint32_t dir = static_cast<uint32_t>(item & 0xffffffffu);
-    const uint32_t table = dir / K, bpos = K - 1u - dir % K;
-    const double p = exact_proj(w64 + static_cast<uint64_t>(dir) * a.dim, a.x, a.x_f64, row, a.ld, a.dim);
-    uint32_t* id = &a.ids[static_cast<uint64_t>(table) * a.n + row];
-    const uint32_t fast = (*id >> bpos) & 1u;
-    const uint32_t exact = p >= 0.0 ? 1u : 0u;
-    if (fast != exact) {
-      atomicXor(id, 1u << bpos);
-      ++ff;
-    }
-    ++rr;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    rr += __shfl_xor_sync(0xffffffffu, rr, o);
-    ff += __shfl_xor_sync(0xffffffffu, ff, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    if (rr) atomicAdd(&blk_r, rr);
-    if (ff) atomicAdd(&blk_f, ff);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (blk_r) atomicAdd(&a.st->rechecked, blk_r);
-    if (blk_f) atomicAdd(&a.st->flipped, blk_f);
-  }
-}
 
 // rows whose near ties overflowed the list: every bucket recomputed exactly
 __global__ void recheck_rows_kernel(const TcArgs a, const double* __restrict__ w64) {
