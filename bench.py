@@ -116,6 +116,24 @@ def dist_setup():
     return ws, rank, local
 
 
+def max_over_ranks(value: float, ws: int) -> float:
+    """Replicas: the job's time is the slowest rank's (all-reduce MAX; CUDA
+    tensor under NCCL, CPU tensor under gloo)."""
+    if ws <= 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([value], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def replica_value(points_per_rank: int, ws: int, ms_max: float) -> float:
+    """Whole-job points/s of N independent replicas (weak scaling)."""
+    return points_per_rank * ws / (ms_max * 1e-3)
+
+
 def cpu_baseline(cfg: int, sample: int):
     """The compiled reference (oracle/_ref) on a bounded sample: insert on one
     core (single writer, sketch.hpp:23-24), detect_batch on all cores."""
@@ -222,12 +240,9 @@ def run_stream(args, w, ws, rank, local):
     launches = N.dev().ace_kernel_launches() - launches0
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
-    if ws > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, ws)
     lat_all = np.concatenate(lats)
-    value = n * ws / (ms * 1e-3)
+    value = replica_value(n, ws, ms)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -317,9 +332,7 @@ def main():
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
     if ws > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms, ws)
         dist.barrier()
     # per-phase breakdown: a separate pass with per-phase CUDA events (outside
     # the timed region, so the events do not perturb the headline number)
@@ -334,7 +347,7 @@ def main():
         phase += np.array(ms5[:])
     N.dev().ace_sketch_set_timing(sk.handle, 0)
     phase /= phase_steps
-    value = n * ws / (ms * 1e-3)
+    value = replica_value(n, ws, ms)
 
     # e2e: same metric through the public API from pinned host memory (H2D of
     # the rows and D2H of the flag bitmap inside the timed region)
@@ -356,11 +369,8 @@ def main():
             ace._detect(sk_e, xnp, build=True)
         torch.cuda.synchronize()
         te = (time.perf_counter() - t0) / reps
-        if ws > 1:
-            t = torch.tensor([te], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            te = float(t.item())
-        e2e = {"value": n * ws / te, "unit": UNIT, "h2d_bytes_per_step": n * w.dim * 4,
+        te = max_over_ranks(te, ws)
+        e2e = {"value": replica_value(n, ws, te * 1e3), "unit": UNIT, "h2d_bytes_per_step": n * w.dim * 4,
                "d2h_bytes_per_step": ((n + 31) // 32) * 4 + 200,
                "note": "wall clock around ace_sketch_build_detect with pinned host rows"}
 

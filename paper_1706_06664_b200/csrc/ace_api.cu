@@ -376,16 +376,6 @@ ace_status run_detect_device(AceSketch* sk, uint64_t n, uint32_t* flag_bits, dou
 ace_status finish_detect(AceSketch* sk, uint64_t n, uint32_t* flag_bits, double* scores, int out_where,
                          const uint32_t* dflags, const double* dscores, AceBatchReport* report);
 
-// score from sk->ids; threshold + flags; fills report.
-ace_status run_detect_tail(AceSketch* sk, uint64_t n, uint32_t* flag_bits, double* scores,
-                           int out_where, AceBatchReport* report) {
-  uint32_t* dflags = nullptr;
-  double* dscores = nullptr;
-  ace_status r = run_detect_device(sk, n, flag_bits, scores, out_where, &dflags, &dscores);
-  if (r != ACE_OK) return r;
-  return finish_detect(sk, n, flag_bits, scores, out_where, dflags, dscores, report);
-}
-
 ace_status run_detect_device(AceSketch* sk, uint64_t n, uint32_t* flag_bits, double* scores, int out_where,
                              uint32_t** dflags_out, double** dscores_out) {
   const AceFamily* f = sk->fam;
