@@ -211,4 +211,13 @@ AceSketch build_sketch(const Dataset& data, std::uint32_t k_bits, std::uint32_t 
                        std::uint64_t seed, double noise_scale = 0.0,
                        CounterWidth width = CounterWidth::k16);
 
+// ---- ACE1 sketch files (reference io.hpp:23-27) ---------------------------
+namespace io {
+// Binary sketch persistence ("ACE1", 53-byte little-endian header, counters
+// table-major).  Round-trips counters, n, mean and configuration bit-exactly;
+// the bytes are the reference's for the same state.
+void save_sketch(const AceSketch& sketch, const std::string& path);
+AceSketch load_sketch(const std::string& path);
+}  // namespace io
+
 }  // namespace ace

@@ -197,11 +197,31 @@ class Reference:
         L.ref_time_build_detect.restype = _i
         L.ref_time_build_detect.argtypes = [_u64, _vp, _u64, _u64, _u32, _u32, C.c_uint, _P(_d),
                                             _P(_d), _P(_u64)]
+        L.ref_save_sketch.restype = _i
+        L.ref_save_sketch.argtypes = [_vp, C.c_char_p]
+        L.ref_load_sketch.restype = _vp
+        L.ref_load_sketch.argtypes = [C.c_char_p, _P(_i)]
+        L.ref_sketch_config.argtypes = [_vp, _P(_u64), _P(_u32), _P(_u32), _P(_u64), _P(_u32)]
         self.L = L
 
     def _ok(self, rc):
         if rc != 0:
             raise RuntimeError(self.L.ref_last_error().decode())
+
+    def load_sketch(self, path) -> "RefSketch":
+        """ace::io::load_sketch (io.cpp:213-244); DataError -> ValueError."""
+        st = _i()
+        h = self.L.ref_load_sketch(str(path).encode(), C.byref(st))
+        if not h:
+            msg = self.L.ref_last_error().decode()
+            raise (ValueError if st.value == -3 else RuntimeError)(msg)
+        dim, seed = _u64(), _u64()
+        k, l, width = _u32(), _u32(), _u32()
+        self.L.ref_sketch_config(h, C.byref(dim), C.byref(k), C.byref(l), C.byref(seed), C.byref(width))
+        r = RefSketch.__new__(RefSketch)
+        r.r, r.dim, r.k, r.l, r.h = self, dim.value, k.value, l.value, h
+        r.seed, r.width = seed.value, width.value
+        return r
 
     def directions(self, seed, dim, k, l):
         w = np.empty((k * l, dim), dtype=np.float64)
@@ -294,3 +314,7 @@ class RefSketch:
 
     def saturated(self):
         return bool(self.r.L.ref_sketch_saturated(self.h))
+
+    def save(self, path):
+        """ace::io::save_sketch (io.cpp:184-211)."""
+        self.r._ok(self.r.L.ref_save_sketch(self.h, str(path).encode()))

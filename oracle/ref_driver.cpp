@@ -18,6 +18,7 @@
 #include "ace/detect.hpp"
 #include "ace/errors.hpp"
 #include "ace/estimators.hpp"
+#include "ace/io.hpp"
 #include "ace/sketch.hpp"
 #include "ace/srp.hpp"
 
@@ -37,6 +38,7 @@ ace::SrpConfig make_cfg(uint64_t dim, uint32_t k, uint32_t l, uint64_t seed) {
 struct RefSketch {
   ace::AceSketch sketch;
   RefSketch(const ace::SrpFamily& f, ace::CounterWidth w) : sketch(f, w) {}
+  explicit RefSketch(ace::AceSketch s) : sketch(std::move(s)) {}
 };
 
 std::vector<double> row_f64(const float* x, uint64_t dim, uint64_t i) {
@@ -244,6 +246,46 @@ int ref_time_build_detect(uint64_t seed, const float* x, uint64_t n, uint64_t di
     g_err = e.what();
     return -1;
   }
+}
+
+// ACE1 sketch files through the reference's io (io.cpp:184-244): 0 ok,
+// -3 DataError (message in ref_last_error), -1 other.
+int ref_save_sketch(void* h, const char* path) {
+  try {
+    ace::io::save_sketch(static_cast<RefSketch*>(h)->sketch, path);
+    return 0;
+  } catch (const ace::DataError& e) {
+    g_err = e.what();
+    return -3;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+void* ref_load_sketch(const char* path, int* status) {
+  try {
+    auto* r = new RefSketch(ace::io::load_sketch(path));
+    *status = 0;
+    return r;
+  } catch (const ace::DataError& e) {
+    g_err = e.what();
+    *status = -3;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    *status = -1;
+  }
+  return nullptr;
+}
+
+void ref_sketch_config(void* h, uint64_t* dim, uint32_t* k, uint32_t* l, uint64_t* seed, uint32_t* width) {
+  const auto& s = static_cast<RefSketch*>(h)->sketch;
+  const auto& c = s.family().config();
+  *dim = c.dim;
+  *k = c.k_bits;
+  *l = c.num_tables;
+  *seed = c.seed;
+  *width = static_cast<uint32_t>(s.counter_width());
 }
 
 }  // extern "C"

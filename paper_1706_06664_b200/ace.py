@@ -137,19 +137,23 @@ class SrpConfig:
     cache_projections: bool = True
 
 
+def check_srp_config(cfg: SrpConfig) -> None:
+    """SrpFamily's configuration checks (srp.cpp:25-32)."""
+    if cfg.dim == 0:
+        raise ContractViolation("SrpFamily: dim must be >= 1")
+    if cfg.k_bits < 1 or cfg.k_bits > 30:
+        raise ContractViolation("SrpFamily: k_bits must be in [1, 30]")
+    if cfg.num_tables < 1:
+        raise ContractViolation("SrpFamily: num_tables must be >= 1")
+    if cfg.noise_scale < 0.0:
+        raise ContractViolation("SrpFamily: noise_scale must be >= 0")
+
+
 class SrpFamily:
     """Seeded SRP family; W generated on the host, hashing on the GPU."""
 
     def __init__(self, cfg: SrpConfig):
-        # srp.cpp:25-32
-        if cfg.dim == 0:
-            raise ContractViolation("SrpFamily: dim must be >= 1")
-        if cfg.k_bits < 1 or cfg.k_bits > 30:
-            raise ContractViolation("SrpFamily: k_bits must be in [1, 30]")
-        if cfg.num_tables < 1:
-            raise ContractViolation("SrpFamily: num_tables must be >= 1")
-        if cfg.noise_scale < 0.0:
-            raise ContractViolation("SrpFamily: noise_scale must be >= 0")
+        check_srp_config(cfg)
         self._cfg = SrpConfig(**cfg.__dict__)
         self._w = generate_directions(cfg.seed, cfg.dim, cfg.k_bits, cfg.num_tables)
         self._dev: Optional[C.c_void_p] = None
@@ -563,3 +567,7 @@ def build_sketch(data, k_bits: int, num_tables: int, seed: int, noise_scale: flo
     sk = AceSketch(fam, width)
     sk.insert(values)
     return sk
+
+
+# ACE1 sketch files (reference io.hpp:23-27)
+from .sketch_io import load_sketch, save_sketch  # noqa: E402

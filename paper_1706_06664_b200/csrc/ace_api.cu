@@ -91,6 +91,10 @@ struct AceSketch {
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   DevBuf ids, sums, stage, flags, scores, demand, near, overflow, x16, rowthr, segc;
+  // restore (e.g. an ACE1 file) reports the restored mean exactly until the
+  // next update, as the reference does (its mean is a stored recurrence)
+  bool mean_pinned = false;
+  double pinned_mean = 0.0;
   // phase timing (ace_sketch_set_timing)
   bool timing = false;
   cudaEvent_t ev[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -599,6 +603,7 @@ ace_status ace_sketch_create(AceFamily* fam, uint32_t counter_width, AceSketch**
 // host mirror is cleared at once (its next refresh comes after these memsets).
 ace_status ace_sketch_reset(AceSketch* sk) {
   if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_reset: null sketch");
+  sk->mean_pinned = false;
   ACE_CUDA(cudaMemsetAsync(sk->counters, 0, sk->num_counters * sizeof(uint32_t), sk->stream));
   ACE_CUDA(cudaMemsetAsync(sk->st, 0, sizeof(DevState), sk->stream));
   memset(sk->hst, 0, sizeof(DevState));
@@ -614,6 +619,8 @@ ace_status ace_sketch_clone(const AceSketch* src, AceSketch** out) {
   ACE_CUDA(cudaMemcpyAsync(d->counters, src->counters, src->num_counters * sizeof(uint32_t),
                            cudaMemcpyDeviceToDevice, d->stream));
   ACE_CUDA(cudaMemcpyAsync(d->st, src->st, sizeof(DevState), cudaMemcpyDeviceToDevice, d->stream));
+  d->mean_pinned = src->mean_pinned;
+  d->pinned_mean = src->pinned_mean;
   return pull_state(d);
 }
 
@@ -656,6 +663,7 @@ ace_status ace_sketch_insert(AceSketch* sk, const void* x, int dtype, uint64_t n
   if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_insert: null sketch");
   ace_status r = check_x(sk->fam, x, dtype, n, ld, x_where);
   if (r != ACE_OK) return r;
+  sk->mean_pinned = false;
   ACE_CUDA(zero_call_fields(sk));
   const void* xd;
   uint64_t ldd;
@@ -689,6 +697,7 @@ ace_status ace_sketch_remove(AceSketch* sk, const void* x, int dtype, uint64_t n
   if (sk->hst->underflow)
     return fail(ACE_E_INCONSISTENT,
                 "AceSketch: delete target counter is zero (item was never inserted)");
+  sk->mean_pinned = false;
   ACE_CUDA(launch_apply_ids(sk->ids.as<uint32_t>(), n, sk->fam->d.tables, sk->fam->d.k_bits,
                             sk->counters, sk->cap, -1, sk->st, sk->stream));
   r = pull_state(sk);
@@ -756,6 +765,7 @@ bool host_pinned(const void* p) {
 // dozen launches and memsets of the pipeline cost one graph launch.
 ace_status batch_detect(AceSketch* sk, const void* x, int dtype, uint64_t n, uint64_t ld, int x_where,
                         uint32_t* flag_bits, double* scores, int out_where, AceBatchReport* report, int build) {
+  if (build) sk->mean_pinned = false;
   AceSketch::GraphKey key;
   key.x = x;
   key.flags = flag_bits;
@@ -876,6 +886,7 @@ ace_status ace_sketch_stream_batch(AceSketch* sk, const void* x, int dtype, uint
   if (!(alpha >= 0.0)) return fail(ACE_E_CONTRACT, "detect_stream: alpha must be >= 0");
   ace_status r = check_x(sk->fam, x, dtype, n, ld, x_where);
   if (r != ACE_OK) return r;
+  sk->mean_pinned = false;
   if (n == 0) return ACE_OK;
   const AceFamily* f = sk->fam;
   ACE_CUDA(zero_call_fields(sk));
@@ -930,6 +941,7 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
   if (batch == 0 || batch % 32 != 0) return fail(ACE_E_CONTRACT, "stream_run: batch must be a positive multiple of 32");
   ace_status r = check_x(sk->fam, x, dtype, n, ld, x_where);
   if (r != ACE_OK) return r;
+  sk->mean_pinned = false;
   if (n == 0) return ACE_OK;
   const AceFamily* f = sk->fam;
   const size_t esz = dtype == ACE_F64 ? 8 : 4;
@@ -1005,7 +1017,7 @@ ace_status ace_sketch_info(const AceSketch* sk, uint64_t* n, double* mean, int* 
   ace_status r = pull_state(m);
   if (r != ACE_OK) return r;
   if (n) *n = sk->hst->n;
-  if (mean) *mean = host_mean(*sk->hst, sk->fam->d.tables);
+  if (mean) *mean = sk->mean_pinned ? sk->pinned_mean : host_mean(*sk->hst, sk->fam->d.tables);
   if (saturated) *saturated = sk->hst->saturated;
   return ACE_OK;
 }
@@ -1048,6 +1060,8 @@ ace_status ace_sketch_restore(AceSketch* sk, const uint64_t* counters, uint64_t 
   DevState s{};
   s.n = n;
   s.T = static_cast<unsigned long long>(std::llround(mean * static_cast<double>(n) * sk->fam->d.tables));
+  sk->mean_pinned = true;
+  sk->pinned_mean = mean;
   s.saturated = saturated ? 1 : 0;
   *sk->hst = s;
   ACE_CUDA(cudaMemcpyAsync(sk->st, sk->hst, sizeof(DevState), cudaMemcpyHostToDevice, sk->stream));

@@ -3,6 +3,9 @@
 // generation (construction time, must match glibc libm bit-for-bit, so it
 // cannot move to the device), argument validation, exception mapping, and
 // label tallies.  Every hash / count / score / threshold runs on the GPU.
+#include <bit>
+#include <fstream>
+#include <type_traits>
 #include <cmath>
 #include <cstring>
 #include <numbers>
@@ -348,6 +351,81 @@ AceSketch build_sketch(const Dataset& data, std::uint32_t k_bits, std::uint32_t 
                        nullptr));
   return sketch;
 }
+
+// ---- ACE1 sketch files (reference io.cpp:184-244) --------------------------
+namespace io {
+namespace {
+constexpr char kMagic[4] = {'A', 'C', 'E', '1'};
+
+template <typename T>
+void put_le(std::ostream& out, T v) {
+  unsigned char b[sizeof(T)];
+  for (std::size_t i = 0; i < sizeof(T); ++i)
+    b[i] = static_cast<unsigned char>((static_cast<std::make_unsigned_t<T>>(v) >> (8 * i)) & 0xff);
+  out.write(reinterpret_cast<const char*>(b), sizeof(T));
+}
+
+template <typename T>
+T get_le(std::istream& in) {
+  unsigned char b[sizeof(T)];
+  in.read(reinterpret_cast<char*>(b), sizeof(T));
+  if (!in) throw DataError("sketch file truncated");
+  std::make_unsigned_t<T> v = 0;
+  for (std::size_t i = 0; i < sizeof(T); ++i) v |= static_cast<std::make_unsigned_t<T>>(b[i]) << (8 * i);
+  return static_cast<T>(v);
+}
+}  // namespace
+
+void save_sketch(const AceSketch& sketch, const std::string& path) {
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw DataError("cannot open sketch file for write: " + path);
+  const auto& cfg = sketch.family().config();
+  out.write(kMagic, 4);
+  put_le(out, static_cast<std::uint32_t>(cfg.dim));
+  put_le(out, cfg.k_bits);
+  put_le(out, cfg.num_tables);
+  put_le(out, static_cast<std::uint32_t>(sketch.counter_width()));
+  put_le(out, cfg.seed);
+  put_le(out, std::bit_cast<std::uint64_t>(cfg.noise_scale));
+  put_le(out, sketch.size());
+  put_le(out, std::bit_cast<std::uint64_t>(sketch.mean()));
+  put_le(out, static_cast<std::uint8_t>(sketch.saturated() ? 1 : 0));
+  const auto counters = sketch.counters_flat();
+  if (sketch.counter_width() == CounterWidth::k16) {
+    for (auto c : counters) put_le(out, static_cast<std::uint16_t>(c));
+  } else {
+    for (auto c : counters) put_le(out, static_cast<std::uint32_t>(c));
+  }
+  if (!out) throw DataError("write failed: " + path);
+}
+
+AceSketch load_sketch(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw DataError("cannot open sketch file: " + path);
+  char magic[4];
+  in.read(magic, 4);
+  if (!in || std::memcmp(magic, kMagic, 4) != 0) throw DataError("bad magic in sketch file: " + path);
+  SrpConfig cfg;
+  cfg.dim = get_le<std::uint32_t>(in);
+  cfg.k_bits = get_le<std::uint32_t>(in);
+  cfg.num_tables = get_le<std::uint32_t>(in);
+  const std::uint32_t width_bits = get_le<std::uint32_t>(in);
+  cfg.seed = get_le<std::uint64_t>(in);
+  cfg.noise_scale = std::bit_cast<double>(get_le<std::uint64_t>(in));
+  const std::uint64_t n = get_le<std::uint64_t>(in);
+  const double mean = std::bit_cast<double>(get_le<std::uint64_t>(in));
+  const bool saturated = get_le<std::uint8_t>(in) != 0;
+  if (width_bits != 16 && width_bits != 32)
+    throw DataError("sketch file counter width must be 16 or 32, got " + std::to_string(width_bits));
+  const CounterWidth width = width_bits == 16 ? CounterWidth::k16 : CounterWidth::k32;
+  const SrpFamily family{cfg};
+  const std::size_t total = static_cast<std::size_t>(cfg.num_tables) << cfg.k_bits;
+  std::vector<std::uint64_t> counters(total);
+  for (auto& c : counters)
+    c = width == CounterWidth::k16 ? get_le<std::uint16_t>(in) : get_le<std::uint32_t>(in);
+  return AceSketch::restore(family, width, std::move(counters), n, mean, saturated);
+}
+}  // namespace io
 
 }  // namespace ace
 

@@ -5,6 +5,9 @@
 // run on the GPU by tests/test_cpp_dropin_gpu.py.  Prints PASS/FAIL lines;
 // exit code = number of failures.
 #include <cmath>
+#include <cstdlib>
+#include <fstream>
+#include <iterator>
 #include <cstdio>
 #include <functional>
 #include <string>
@@ -13,6 +16,7 @@
 #include "ace/detect.hpp"
 #include "ace/errors.hpp"
 #include "ace/estimators.hpp"
+#include "ace/io.hpp"
 #include "ace/rng.hpp"
 #include "ace/sketch.hpp"
 #include "ace/srp.hpp"
@@ -242,6 +246,46 @@ int main() {
     const ace::SrpFamily f{c};
     expect_throw<ace::UnsupportedOperation>([&] { f.bucket(0, normals(4, 1)); },
                                             "noisy hashing reports UnsupportedOperation");
+  }
+  // test_io.cpp: ACE1 save/load round-trips state and scores bit-exactly
+  {
+    const char* tmp = std::getenv("TMPDIR");
+    const std::string dir = tmp ? tmp : "/tmp";
+    const std::string path = dir + "/ace_dropin_sketch.ace";
+    ace::Dataset data;
+    data.rows = 120;
+    data.cols = 6;
+    for (std::size_t i = 0; i < data.rows; ++i) {
+      const auto r = normals(6, 1000 + i);
+      data.values.insert(data.values.end(), r.begin(), r.end());
+    }
+    const auto sketch = ace::build_sketch(data, 10, 20, 99);
+    ace::io::save_sketch(sketch, path);
+    const auto loaded = ace::io::load_sketch(path);
+    check(loaded.size() == sketch.size(), "ACE1: size round-trips");
+    check(loaded.mean() == sketch.mean(), "ACE1: mean round-trips bit-exactly");
+    check(loaded.saturated() == sketch.saturated(), "ACE1: saturation flag round-trips");
+    check(loaded.counter_width() == sketch.counter_width(), "ACE1: counter width round-trips");
+    check(loaded.family().config().seed == 99, "ACE1: seed round-trips");
+    check(loaded.counters_flat() == sketch.counters_flat(), "ACE1: counters round-trip");
+    bool same = true;
+    for (std::size_t i = 0; i < 100; ++i)
+      same = same && loaded.score(data.row(i % data.rows)).value == sketch.score(data.row(i % data.rows)).value;
+    check(same, "ACE1: scores of the loaded sketch are identical");
+    {
+      std::ofstream bad(dir + "/ace_dropin_bad.ace", std::ios::binary);
+      bad << "NOPEnotasketch";
+    }
+    expect_throw<ace::DataError>([&] { ace::io::load_sketch(dir + "/ace_dropin_bad.ace"); },
+                                 "ACE1: bad magic throws DataError");
+    std::ifstream in(path, std::ios::binary);
+    std::string bytes((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    {
+      std::ofstream tr(dir + "/ace_dropin_trunc.ace", std::ios::binary);
+      tr.write(bytes.data(), static_cast<std::streamsize>(bytes.size() - 7));
+    }
+    expect_throw<ace::DataError>([&] { ace::io::load_sketch(dir + "/ace_dropin_trunc.ace"); },
+                                 "ACE1: truncated payload throws DataError");
   }
   std::printf("%d failure(s)\n", failures);
   return failures;
