@@ -213,6 +213,14 @@ AceSketch build_sketch(const Dataset& data, std::uint32_t k_bits, std::uint32_t 
 
 // ---- ACE1 sketch files (reference io.hpp:23-27) ---------------------------
 namespace io {
+// CSV ingestion (reference io.hpp:16-21, io.cpp:89-182): comma-separated
+// numeric text, one row per instance; a header line is detected by a
+// non-numeric first token; label_column (0-based, negative from the end)
+// splits off a 0/1 label column; all-zero feature rows are rejected with
+// their line numbers.  Lines are parsed on all host threads; validation and
+// error messages follow the reference's line order exactly.
+Dataset load_dataset(const std::string& path, std::optional<int> label_column = std::nullopt);
+
 // Binary sketch persistence ("ACE1", 53-byte little-endian header, counters
 // table-major).  Round-trips counters, n, mean and configuration bit-exactly;
 // the bytes are the reference's for the same state.

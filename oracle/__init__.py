@@ -202,11 +202,32 @@ class Reference:
         L.ref_load_sketch.restype = _vp
         L.ref_load_sketch.argtypes = [C.c_char_p, _P(_i)]
         L.ref_sketch_config.argtypes = [_vp, _P(_u64), _P(_u32), _P(_u32), _P(_u64), _P(_u32)]
+        L.ref_load_dataset.restype = _i
+        L.ref_load_dataset.argtypes = [C.c_char_p, _i, _i, _vp, _vp, _vp, _vp]
+        L.ref_free.argtypes = [_vp]
         self.L = L
 
     def _ok(self, rc):
         if rc != 0:
             raise RuntimeError(self.L.ref_last_error().decode())
+
+    def load_dataset(self, path, label_column=None):
+        """ace::io::load_dataset: (values (rows, cols) f64, labels u8 or None);
+        DataError -> ValueError with the reference's message."""
+        vals, labs = _vp(), _vp()
+        rows, cols = _u64(), _u64()
+        rc = self.L.ref_load_dataset(str(path).encode(), int(label_column is not None), int(label_column or 0),
+                                     C.byref(vals), C.byref(rows), C.byref(cols), C.byref(labs))
+        if rc != 0:
+            raise (ValueError if rc == -3 else RuntimeError)(self.L.ref_last_error().decode())
+        n, d = rows.value, cols.value
+        v = np.ctypeslib.as_array(C.cast(vals, _P(_d)), shape=(n * d,)).copy().reshape(n, d)
+        lab = None
+        if labs.value:
+            lab = np.ctypeslib.as_array(C.cast(labs, _P(C.c_uint8)), shape=(n,)).copy()
+            self.L.ref_free(labs)
+        self.L.ref_free(vals)
+        return v, lab
 
     def load_sketch(self, path) -> "RefSketch":
         """ace::io::load_sketch (io.cpp:213-244); DataError -> ValueError."""

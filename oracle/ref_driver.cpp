@@ -9,7 +9,9 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <optional>
 #include <exception>
 #include <string>
 #include <thread>
@@ -277,6 +279,33 @@ void* ref_load_sketch(const char* path, int* status) {
   }
   return nullptr;
 }
+
+// ace::io::load_dataset (io.cpp:89-182): 0 ok with malloc'd values/labels
+// (free with ref_free), -3 DataError (message in ref_last_error).
+int ref_load_dataset(const char* path, int has_label, int label_column, double** values, uint64_t* rows,
+                     uint64_t* cols, uint8_t** labels) {
+  try {
+    const auto d = ace::io::load_dataset(path, has_label ? std::optional<int>(label_column) : std::nullopt);
+    *rows = d.rows;
+    *cols = d.cols;
+    *values = static_cast<double*>(std::malloc(sizeof(double) * std::max<size_t>(1, d.values.size())));
+    std::memcpy(*values, d.values.data(), sizeof(double) * d.values.size());
+    *labels = nullptr;
+    if (d.labels) {
+      *labels = static_cast<uint8_t*>(std::malloc(std::max<size_t>(1, d.labels->size())));
+      std::memcpy(*labels, d.labels->data(), d.labels->size());
+    }
+    return 0;
+  } catch (const ace::DataError& e) {
+    g_err = e.what();
+    return -3;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+void ref_free(void* p) { std::free(p); }
 
 void ref_sketch_config(void* h, uint64_t* dim, uint32_t* k, uint32_t* l, uint64_t* seed, uint32_t* width) {
   const auto& s = static_cast<RefSketch*>(h)->sketch;

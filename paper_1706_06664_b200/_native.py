@@ -82,6 +82,9 @@ ABI = {
 
 HOST_ABI = {
     "ace_generate_directions": (_i, [_u64, _u64, _u32, _u32, _vp]),
+    "ace_load_dataset_csv": (_i, [C.c_char_p, _i, _i, _vp, _vp, _vp, _vp]),
+    "ace_host_last_error": (C.c_char_p, []),
+    "ace_free": (None, [_vp]),
 }
 
 DATAGEN_ABI = {

@@ -570,4 +570,4 @@ def build_sketch(data, k_bits: int, num_tables: int, seed: int, noise_scale: flo
 
 
 # ACE1 sketch files (reference io.hpp:23-27)
-from .sketch_io import load_sketch, save_sketch  # noqa: E402
+from .sketch_io import load_dataset, load_sketch, save_sketch  # noqa: E402

@@ -6,6 +6,13 @@
 #include <bit>
 #include <fstream>
 #include <type_traits>
+#include <charconv>
+#include <thread>
+#include <optional>
+#include <string_view>
+#include <cstdlib>
+#include <iterator>
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <numbers>
@@ -13,6 +20,7 @@
 
 #include "ace/b200_api.hpp"
 #include "ace_b200.h"
+#include "ace_host.h"
 
 namespace ace {
 
@@ -355,6 +363,45 @@ AceSketch build_sketch(const Dataset& data, std::uint32_t k_bits, std::uint32_t 
 // ---- ACE1 sketch files (reference io.cpp:184-244) --------------------------
 namespace io {
 namespace {
+
+// ---- CSV (reference io.cpp:20-49, 89-182) ----
+std::string_view trim_csv(std::string_view s) {
+  while (!s.empty() && (s.front() == ' ' || s.front() == '\t' || s.front() == '\r')) s.remove_prefix(1);
+  while (!s.empty() && (s.back() == ' ' || s.back() == '\t' || s.back() == '\r')) s.remove_suffix(1);
+  return s;
+}
+
+bool parse_cell(std::string_view token, double& out) {
+  token = trim_csv(token);
+  if (token.empty()) return false;
+  const char* b = token.data();
+  const char* e = b + token.size();
+  auto [ptr, ec] = std::from_chars(b, e, out);
+  return ec == std::errc{} && ptr == e;
+}
+
+// One non-empty line, parsed: its cells' values and the first unparsable cell.
+struct ParsedLine {
+  std::size_t line_number = 0;
+  std::vector<double> cells;
+  std::vector<std::string_view> raw;  // kept only when a cell fails to parse
+  long bad = -1;                      // first unparsable cell, or -1
+};
+
+void parse_line(std::string_view view, ParsedLine& pl) {
+  std::size_t start = 0;
+  for (std::size_t i = 0; i <= view.size(); ++i) {
+    if (i == view.size() || view[i] == ',') {
+      const std::string_view cell = view.substr(start, i - start);
+      double v = 0.0;
+      if (!parse_cell(cell, v) && pl.bad < 0) pl.bad = static_cast<long>(pl.cells.size());
+      pl.cells.push_back(v);
+      pl.raw.push_back(cell);
+      start = i + 1;
+    }
+  }
+}
+
 constexpr char kMagic[4] = {'A', 'C', 'E', '1'};
 
 template <typename T>
@@ -375,6 +422,92 @@ T get_le(std::istream& in) {
   return static_cast<T>(v);
 }
 }  // namespace
+
+Dataset load_dataset(const std::string& path, std::optional<int> label_column) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw DataError("cannot open dataset file: " + path);
+  std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  // line table (std::getline semantics: '\n' separated, a final line without
+  // '\n' still counts; trimming removes '\r')
+  std::vector<std::pair<std::size_t, std::size_t>> lines;
+  for (std::size_t pos = 0; pos < text.size();) {
+    std::size_t nl = text.find('\n', pos);
+    if (nl == std::string::npos) nl = text.size();
+    lines.emplace_back(pos, nl - pos);
+    pos = nl + 1;
+  }
+  // parse every line on all host threads (pure per line)
+  std::vector<ParsedLine> parsed(lines.size());
+  const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(),
+                                                      static_cast<unsigned>(lines.size() / 4096 + 1)));
+  std::vector<std::thread> pool;
+  for (unsigned w = 0; w < nt; ++w)
+    pool.emplace_back([&, w] {
+      for (std::size_t i = w; i < lines.size(); i += nt) {
+        const std::string_view view = trim_csv(std::string_view(text).substr(lines[i].first, lines[i].second));
+        parsed[i].line_number = i + 1;
+        if (!view.empty()) parse_line(view, parsed[i]);
+      }
+    });
+  for (auto& t : pool) t.join();
+  // the reference's validation, in line order
+  Dataset data;
+  data.name = path;
+  std::vector<std::size_t> zero_rows;
+  bool first_data_line = true;
+  for (std::size_t i = 0; i < lines.size(); ++i) {
+    const ParsedLine& pl = parsed[i];
+    if (pl.cells.empty()) continue;  // blank line
+    if (first_data_line && pl.bad == 0) continue;  // header line
+    if (pl.bad >= 0)
+      throw DataError("unparsable cell at row " + std::to_string(pl.line_number) + ", column " +
+                      std::to_string(pl.bad + 1) + ": '" + std::string(trim_csv(pl.raw[pl.bad])) + "'");
+    std::optional<std::size_t> label_index;
+    if (label_column) {
+      const int raw = *label_column;
+      const long resolved = raw >= 0 ? raw : static_cast<long>(pl.cells.size()) + raw;
+      if (resolved < 0 || resolved >= static_cast<long>(pl.cells.size()))
+        throw DataError("label column " + std::to_string(raw) + " out of range at row " +
+                        std::to_string(pl.line_number));
+      label_index = static_cast<std::size_t>(resolved);
+    }
+    const std::size_t nf = pl.cells.size() - (label_index ? 1 : 0);
+    if (first_data_line) {
+      data.cols = nf;
+      if (label_column) data.labels.emplace();
+      first_data_line = false;
+    } else if (nf != data.cols) {
+      throw DataError("ragged row " + std::to_string(pl.line_number) + ": expected " + std::to_string(data.cols) +
+                      " feature columns, found " + std::to_string(nf));
+    }
+    bool all_zero = true;
+    for (std::size_t c = 0; c < pl.cells.size(); ++c)
+      if ((!label_index || c != *label_index) && pl.cells[c] != 0.0) {
+        all_zero = false;
+        break;
+      }
+    if (all_zero) {
+      zero_rows.push_back(pl.line_number);
+      continue;
+    }
+    if (label_index) {
+      const double lv = pl.cells[*label_index];
+      if (lv != 0.0 && lv != 1.0)
+        throw DataError("label at row " + std::to_string(pl.line_number) + " is not 0 or 1");
+      data.labels->push_back(lv != 0.0 ? 1 : 0);
+    }
+    for (std::size_t c = 0; c < pl.cells.size(); ++c)
+      if (!label_index || c != *label_index) data.values.push_back(pl.cells[c]);
+    ++data.rows;
+  }
+  if (!zero_rows.empty()) {
+    std::string rows;
+    for (std::size_t i = 0; i < zero_rows.size(); ++i) rows += (i ? "," : "") + std::to_string(zero_rows[i]);
+    throw DataError("all-zero feature rows rejected (cosine undefined): " + rows);
+  }
+  if (data.rows == 0) throw DataError("empty dataset file: " + path);
+  return data;
+}
 
 void save_sketch(const AceSketch& sketch, const std::string& path) {
   std::ofstream out(path, std::ios::binary);
@@ -428,6 +561,39 @@ AceSketch load_sketch(const std::string& path) {
 }  // namespace io
 
 }  // namespace ace
+
+// CSV ingestion for non-C++ hosts (the Python mirror): ace::io::load_dataset.
+// Returns 0 and malloc'd values (rows x cols f64) / labels (rows u8, only with
+// a label column), ACE_E_DATA with the message in ace_host_last_error(), or
+// ACE_E_CONTRACT for null arguments.  Free with ace_free().
+namespace {
+thread_local std::string g_host_err;
+}
+extern "C" const char* ace_host_last_error(void) { return g_host_err.c_str(); }
+extern "C" void ace_free(void* p) { std::free(p); }
+extern "C" int ace_load_dataset_csv(const char* path, int has_label, int label_column, double** values,
+                                    uint64_t* rows, uint64_t* cols, uint8_t** labels) {
+  if (!path || !values || !rows || !cols || !labels) return ACE_E_CONTRACT;
+  try {
+    const auto d = ace::io::load_dataset(path, has_label ? std::optional<int>(label_column) : std::nullopt);
+    *rows = d.rows;
+    *cols = d.cols;
+    *values = static_cast<double*>(std::malloc(sizeof(double) * std::max<size_t>(1, d.values.size())));
+    std::memcpy(*values, d.values.data(), sizeof(double) * d.values.size());
+    *labels = nullptr;
+    if (d.labels) {
+      *labels = static_cast<uint8_t*>(std::malloc(std::max<size_t>(1, d.labels->size())));
+      std::memcpy(*labels, d.labels->data(), d.labels->size());
+    }
+    return 0;
+  } catch (const ace::DataError& e) {
+    g_host_err = e.what();
+    return ACE_E_DATA;
+  } catch (const std::exception& e) {
+    g_host_err = e.what();
+    return ACE_E_CONTRACT;
+  }
+}
 
 // W generation for non-C++ hosts (the Python mirror): the same generator as
 // SrpFamily's constructor.

@@ -1,4 +1,6 @@
-"""ACE1 sketch files (reference io.hpp:23-27, io.cpp:184-244).
+"""ACE1 sketch files (reference io.hpp:23-27, io.cpp:184-244) and CSV
+ingestion (io.hpp:16-21, io.cpp:89-182, parsed by libace.so on all host
+threads).
 
 Layout, little-endian, 53-byte header (AceSketch::kHeaderBytes):
     "ACE1" | dim u32 | k_bits u32 | num_tables u32 | width u32 (16/32) |
@@ -9,10 +11,12 @@ what the reference's save_sketch writes for the same state.
 """
 from __future__ import annotations
 
+import ctypes as C
 import struct
 
 import numpy as np
 
+from . import _native as N
 from . import ace
 
 MAGIC = b"ACE1"
@@ -78,3 +82,27 @@ def load_sketch(path) -> "ace.AceSketch":
     fam = ace.SrpFamily(h["cfg"])
     width = ace.CounterWidth.k16 if h["width"] == 16 else ace.CounterWidth.k32
     return ace.AceSketch.restore(fam, width, counters, h["n"], h["mean"], h["saturated"])
+
+
+def load_dataset(path, label_column=None) -> "ace.Dataset":
+    """ace::io::load_dataset: header auto-detected, optional 0/1 label column
+    (negative counts from the end), all-zero rows rejected (DataError)."""
+    vals, labs = C.c_void_p(), C.c_void_p()
+    rows, cols = C.c_uint64(), C.c_uint64()
+    rc = N.host().ace_load_dataset_csv(str(path).encode(), int(label_column is not None),
+                                       int(label_column or 0), C.byref(vals), C.byref(rows), C.byref(cols),
+                                       C.byref(labs))
+    if rc != 0:
+        msg = N.host().ace_host_last_error().decode()
+        raise (ace.DataError if rc == N.ACE_E_DATA else ace.ContractViolation)(msg)
+    try:
+        n, d = rows.value, cols.value
+        values = np.ctypeslib.as_array(C.cast(vals, C.POINTER(C.c_double)), shape=(n * d,)).copy().reshape(n, d)
+        labels = None
+        if labs.value:
+            labels = np.ctypeslib.as_array(C.cast(labs, C.POINTER(C.c_uint8)), shape=(n,)).copy()
+    finally:
+        N.host().ace_free(vals)
+        if labs.value:
+            N.host().ace_free(labs)
+    return ace.Dataset(values=values, labels=labels, name=str(path))

@@ -32,7 +32,10 @@ def test_header_symbols_exported():
 
 def test_dropin_library_loads():
     lib = N.host()
-    assert hasattr(lib, "ace_generate_directions")
+    text = re.sub(r"/\*.*?\*/", "", (ROOT / "include" / "ace_host.h").read_text(), flags=re.S)
+    host_syms = sorted(set(re.findall(r"\b(ace_[a-z0-9_]+)\s*\(", text)))
+    assert host_syms and all(hasattr(lib, s) for s in host_syms)
+    assert sorted(N.HOST_ABI) == host_syms
     # C++ API symbols of the drop-in (mangled) are present
     names = (N.LIB_DIR / "libace.so").read_bytes()
     for frag in (b"SrpFamily", b"AceSketch", b"detect_batch", b"detect_stream", b"build_sketch"):
