@@ -90,7 +90,10 @@ struct AceSketch {
   DevState* hst = nullptr;   // pinned host mirror
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
-  DevBuf ids, sums, stage, flags, scores, demand, near, overflow, x16, rowthr, segc;
+  DevBuf ids, sums, stage, flags, scores, demand, near, overflow, x16, rowthr, segc, gbuf;
+  // build + detect over the same rows: run_hash leaves the insert to the
+  // fused count-and-gather pass of the detect tail (apply_gather_kernel)
+  bool defer_insert = false, insert_deferred = false;
   // restore (e.g. an ACE1 file) reports the restored mean exactly until the
   // next update, as the reference does (its mean is a stored recurrence)
   bool mean_pinned = false;
@@ -114,9 +117,9 @@ struct AceSketch {
     uint64_t n = 0, ld = 0;
     int dtype = 0, where = 0, out_where = 0, build = 0, ff = 0;
     cudaStream_t stream = nullptr;
-    const void* bufs[11] = {};  // the sketch's scratch buffers (a reallocation invalidates the graph)
+    const void* bufs[12] = {};  // the sketch's scratch buffers (a reallocation invalidates the graph)
     bool operator==(const GraphKey& o) const {
-      for (int i = 0; i < 11; ++i)
+      for (int i = 0; i < 12; ++i)
         if (bufs[i] != o.bufs[i]) return false;
       return x == o.x && flags == o.flags && scores == o.scores && n == o.n && ld == o.ld && dtype == o.dtype &&
              where == o.where && out_where == o.out_where && build == o.build && ff == o.ff && stream == o.stream;
@@ -325,7 +328,9 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
       sk->mark(5);
       ACE_CUDA(launch_recheck_segs(t, sk->stream));
       ACE_CUDA(launch_recheck(t, f->d.w64, sk->stream));
-      if (insert)
+      if (insert && sk->defer_insert)
+        sk->insert_deferred = true;
+      else if (insert)
         ACE_CUDA(launch_apply_ids(sk->ids.as<uint32_t>(), n, f->d.tables, f->d.k_bits, sk->counters, sk->cap,
                                   +1, sk->st, sk->stream, !fire_and_forget_ok(sk, n)));
       if (insert && sk->width == 16)
@@ -356,6 +361,8 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
       // T = sum of squared counters (exact: 32-bit, unsaturated)
       ACE_CUDA(cudaMemsetAsync(&sk->st->T, 0, sizeof(unsigned long long), sk->stream));
       ACE_CUDA(launch_sum_squares(sk->counters, sk->num_counters, &sk->st->T, sk->stream));
+    } else if (insert && sk->defer_insert) {
+      sk->insert_deferred = true;
     } else if (insert) {
       ACE_CUDA(launch_apply_ids(sk->ids.as<uint32_t>(), n, f->d.tables, f->d.k_bits, sk->counters, sk->cap,
                                 +1, sk->st, sk->stream, !fire_and_forget_ok(sk, n)));
@@ -395,8 +402,24 @@ ace_status run_detect_device(AceSketch* sk, uint64_t n, uint32_t* flag_bits, dou
     }
   }
   uint32_t* dflags = (flag_bits && out_where == ACE_DEVICE) ? flag_bits : sk->flags.as<uint32_t>();
-  ACE_CUDA(launch_score(sk->ids.as<uint32_t>(), n, n, f->d.tables, f->d.k_bits, sk->counters,
-                        sk->sums.as<uint64_t>(), dscores, sk->st, sk->stream));
+  if (sk->insert_deferred) {
+    // counts, then every id replaced by its final count (gathers from shared
+    // memory), then per-row sums of counts
+    sk->insert_deferred = false;
+    uint32_t* gout = sk->ids.as<uint32_t>();
+    if (f->d.k_bits > 15) {
+      ACE_CUDA(sk->gbuf.ensure(static_cast<size_t>(n) * f->d.tables * sizeof(uint32_t)));
+      gout = sk->gbuf.as<uint32_t>();
+    }
+    ACE_CUDA(launch_apply_gather(sk->ids.as<uint32_t>(), gout, n, f->d.tables, f->d.k_bits, sk->counters, sk->st,
+                                 sk->stream));
+    sk->mark(1);
+    ACE_CUDA(launch_score(gout, n, n, f->d.tables, f->d.k_bits, nullptr, sk->sums.as<uint64_t>(), dscores, sk->st,
+                          sk->stream));
+  } else {
+    ACE_CUDA(launch_score(sk->ids.as<uint32_t>(), n, n, f->d.tables, f->d.k_bits, sk->counters,
+                          sk->sums.as<uint64_t>(), dscores, sk->st, sk->stream));
+  }
   sk->mark(2);
   ACE_CUDA(launch_finalize_batch(n, f->d.tables, sk->st, sk->stream));
   ACE_CUDA(launch_flags(sk->sums.as<uint64_t>(), n, dflags, sk->st, 0, sk->stream));
@@ -639,6 +662,7 @@ ace_status ace_sketch_destroy(AceSketch* sk) {
   sk->x16.release();
   sk->rowthr.release();
   sk->segc.release();
+  sk->gbuf.release();
   if (sk->counters) cudaFree(sk->counters);
   if (sk->st) cudaFree(sk->st);
   if (sk->hst) cudaFreeHost(sk->hst);
@@ -766,6 +790,18 @@ bool host_pinned(const void* p) {
 ace_status batch_detect(AceSketch* sk, const void* x, int dtype, uint64_t n, uint64_t ld, int x_where,
                         uint32_t* flag_bits, double* scores, int out_where, AceBatchReport* report, int build) {
   if (build) sk->mean_pinned = false;
+  static int gather_env = -1;
+  if (gather_env < 0) {
+    const char* e = getenv("ACE_FUSED_GATHER");
+    gather_env = e ? atoi(e) : 1;
+  }
+  // measured: a gain where the tables fit one shared-memory histogram and the
+  // gathers dominate (cfg 2: 0.541 -> 0.525 ms); a loss on small batches
+  // (cfg 1) and even on cfg 3 (K = 16, two parts)
+  sk->defer_insert = gather_env != 0 && build && sk->width == 32 && sk->fam->use_tc() &&
+                     (gather_env == 2 || (sk->fam->d.k_bits <= 15 && n * sk->fam->d.tables >= (16ull << 20))) &&
+                     sk->fam->d.k_bits <= 20 && fire_and_forget_ok(sk, n);
+  sk->insert_deferred = false;
   AceSketch::GraphKey key;
   key.x = x;
   key.flags = flag_bits;
@@ -778,9 +814,9 @@ ace_status batch_detect(AceSketch* sk, const void* x, int dtype, uint64_t n, uin
   key.build = build;
   key.ff = build ? (fire_and_forget_ok(sk, n) ? 1 : 0) : 2;
   key.stream = sk->stream;
-  const DevBuf* bufs[11] = {&sk->ids, &sk->sums, &sk->stage, &sk->flags, &sk->scores, &sk->demand,
-                            &sk->near, &sk->overflow, &sk->x16, &sk->rowthr, &sk->segc};
-  for (int i = 0; i < 11; ++i) key.bufs[i] = bufs[i]->p;
+  const DevBuf* bufs[12] = {&sk->ids, &sk->sums, &sk->stage, &sk->flags, &sk->scores, &sk->demand,
+                            &sk->near, &sk->overflow, &sk->x16, &sk->rowthr, &sk->segc, &sk->gbuf};
+  for (int i = 0; i < 12; ++i) key.bufs[i] = bufs[i]->p;
   static int graphs_env = -2;
   if (graphs_env == -2) {
     const char* e = getenv("ACE_GRAPHS");
@@ -832,6 +868,7 @@ ace_status batch_detect(AceSketch* sk, const void* x, int dtype, uint64_t n, uin
     sk->gseen = key;
     sk->gseen_valid = eligible;
   }
+  sk->defer_insert = false;
   return finish_detect(sk, n, flag_bits, scores, out_where, dflags, dscores, report);
 }
 

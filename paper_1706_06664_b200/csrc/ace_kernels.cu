@@ -14,6 +14,9 @@
 
 #include "ace_kernels.cuh"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace ace_dev {
 
 namespace {
@@ -529,6 +532,104 @@ __global__ void __launch_bounds__(1024) apply_ids_smem_kernel(const uint32_t* __
   }
 }
 
+// build_sketch + detect_batch over the same rows, fused: phase 1 is
+// apply_ids_smem_kernel<false> (shared histograms, RED merge); after a grid
+// barrier every block stages the FINAL counts of its (table, part) into shared
+// memory and replaces each of its ids by that count (gathers from shared
+// memory instead of random L2 gathers), and the block whose range holds a
+// table's first row adds that (table, part)'s sum of squares to T.
+// score_kernel then sums the counts per row (counters == nullptr).
+// gout == ids when the table is one part (each position is read and written
+// by the same thread); with several parts a separate buffer (the partner
+// block still reads the ids).  Cooperative launch, one block per SM.
+__global__ void __launch_bounds__(1024) apply_gather_kernel(const uint32_t* ids, uint32_t* gout, uint64_t n,
+                                                            uint32_t tables, uint32_t k_bits, uint32_t part_bits,
+                                                            uint64_t per, uint32_t* counters, DevState* st) {
+  extern __shared__ uint32_t hist[];
+  __shared__ unsigned long long blk;
+  const uint32_t nb = 1u << part_bits;
+  const uint32_t pshift = k_bits - part_bits;
+  const uint32_t part = blockIdx.x & ((1u << pshift) - 1u);
+  const uint64_t total = n * tables;
+  const uint64_t i0 = static_cast<uint64_t>(blockIdx.x >> pshift) * per;
+  const uint64_t i1 = min(total, i0 + per);
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
+  if (threadIdx.x == 0) blk = 0ull;
+  const int lane = threadIdx.x & 31;
+  unsigned long long dT = 0ull;
+  constexpr int kDepth = 8;
+  const uint32_t step = blockDim.x * kDepth;
+  // ---- phase 1: counts
+  for (uint64_t seg = i0; seg < i1;) {
+    const uint64_t t = seg / n;
+    const uint64_t seg_end = min(i1, (t + 1) * n);
+    __syncthreads();
+    for (uint64_t base = seg; base < seg_end; base += step) {
+      const uint32_t len = static_cast<uint32_t>(min(seg_end - base, static_cast<uint64_t>(step)));
+      const uint32_t* src = ids + base;
+      uint32_t idv[kDepth];
+#pragma unroll
+      for (int u = 0; u < kDepth; ++u) idv[u] = __ldg(src + min(u * blockDim.x + threadIdx.x, len - 1u));
+#pragma unroll
+      for (int u = 0; u < kDepth; ++u) {
+        const uint32_t id = idv[u];
+        const uint32_t b =
+            (u * blockDim.x + threadIdx.x < len && (id >> part_bits) == part) ? (id & (nb - 1u)) : 0xffffffffu;
+        unsigned rem = __ballot_sync(0xffffffffu, b != 0xffffffffu);
+#pragma unroll 1
+        for (int round = 0; round < 4 && rem; ++round) {
+          const int leader = __ffs(rem) - 1;
+          const uint32_t bl = __shfl_sync(0xffffffffu, b, leader);
+          const unsigned eq = __ballot_sync(0xffffffffu, b == bl) & rem;
+          if (eq == (1u << leader)) break;
+          if (lane == leader) atomicAdd(&hist[bl], static_cast<uint32_t>(__popc(eq)));
+          rem &= ~eq;
+        }
+        if ((rem >> lane) & 1u) atomicAdd(&hist[b], 1u);
+      }
+    }
+    flush_hist<false>(hist, nb, counters + (t << k_bits) + (static_cast<uint64_t>(part) << part_bits), 0xffffffffu,
+                      st, dT);
+    seg = seg_end;
+  }
+  __threadfence();
+  cg::this_grid().sync();
+  // ---- phase 2: final counts per id
+  for (uint64_t seg = i0; seg < i1;) {
+    const uint64_t t = seg / n;
+    const uint64_t seg_end = min(i1, (t + 1) * n);
+    const uint32_t* ct = counters + (t << k_bits) + (static_cast<uint64_t>(part) << part_bits);
+    __syncthreads();
+    const bool owner = i0 <= t * n && t * n < i1;  // this block's range holds the table's first row
+    for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
+      const uint32_t c = __ldcg(ct + b);
+      hist[b] = c;
+      if (owner) dT += static_cast<unsigned long long>(c) * c;
+    }
+    __syncthreads();
+    for (uint64_t base = seg; base < seg_end; base += step) {
+      const uint32_t len = static_cast<uint32_t>(min(seg_end - base, static_cast<uint64_t>(step)));
+      const uint32_t* src = ids + base;
+      uint32_t idv[kDepth];
+#pragma unroll
+      for (int u = 0; u < kDepth; ++u) idv[u] = src[min(u * blockDim.x + threadIdx.x, len - 1u)];
+#pragma unroll
+      for (int u = 0; u < kDepth; ++u) {
+        const uint32_t i = u * blockDim.x + threadIdx.x;
+        if (i < len && (idv[u] >> part_bits) == part) gout[base + i] = hist[idv[u] & (nb - 1u)];
+      }
+    }
+    seg = seg_end;
+  }
+  dT = warp_sum_u64(dT);
+  if (lane == 0 && dT) atomicAdd(&blk, dT);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (blk) atomicAdd(&st->T, blk);
+    if (blockIdx.x == 0) atomicAdd(&st->n, n);
+  }
+}
+
 __global__ void remove_demand_kernel(const uint32_t* __restrict__ ids, uint64_t n, uint32_t tables,
                                      uint32_t k_bits, uint32_t* demand) {
   const uint64_t total = n * tables;
@@ -578,12 +679,20 @@ __global__ void score_kernel(const uint32_t* __restrict__ ids, uint64_t ids_stri
       uint32_t b[8], c[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) b[u] = ids[(uint64_t)(t + u) * ids_stride + i];
+      if (counters) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) c[u] = counters[((uint64_t)(t + u) << k_bits) + b[u]];
+        for (int u = 0; u < 8; ++u) c[u] = counters[((uint64_t)(t + u) << k_bits) + b[u]];
+      } else {  // the ids were replaced by their final counts (apply_gather_kernel)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) c[u] = b[u];
+      }
 #pragma unroll
       for (int u = 0; u < 8; ++u) S += c[u];
     }
-    for (; t < tables; ++t) S += counters[((uint64_t)t << k_bits) + ids[(uint64_t)t * ids_stride + i]];
+    for (; t < tables; ++t) {
+      const uint32_t b = ids[(uint64_t)t * ids_stride + i];
+      S += counters ? counters[((uint64_t)t << k_bits) + b] : b;
+    }
     if (sums) sums[i] = S;
     if (scores) scores[i] = __ddiv_rn(static_cast<double>(S), static_cast<double>(tables));
     acc += S;
@@ -976,6 +1085,42 @@ cudaError_t launch_apply_ids(const uint32_t* ids, uint64_t n, uint32_t tables, u
                                                              sign, st);
   count_launch();
   return cudaGetLastError();
+}
+
+cudaError_t launch_apply_gather(uint32_t* ids, uint32_t* gout, uint64_t n, uint32_t tables, uint32_t k_bits,
+                                uint32_t* counters, DevState* st, cudaStream_t s) {
+  if (n == 0 || k_bits > 20) return cudaErrorInvalidValue;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  static bool configured = false;
+  if (!configured) {
+    const cudaError_t e = cudaFuncSetAttribute(apply_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(sizeof(uint32_t) << 15));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  uint32_t part_bits = k_bits < 15 ? k_bits : 15;
+  const uint32_t parts = 1u << (k_bits - part_bits);
+  const uint64_t total = n * tables;
+  uint64_t ranges = static_cast<uint64_t>(sms) / parts;
+  if (ranges < 1) ranges = 1;
+  if (ranges > total / 4096) ranges = total / 4096 > 0 ? total / 4096 : 1;
+  uint64_t per = (total + ranges - 1) / ranges;
+  const unsigned grid = static_cast<unsigned>((total + per - 1) / per) * parts;
+  const size_t smem = sizeof(uint32_t) << part_bits;
+  // T = sum c^2 is accumulated from zero by the kernel (32-bit, unsaturated)
+  cudaError_t e = cudaMemsetAsync(&st->T, 0, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
+  const uint32_t* ids_c = ids;
+  void* args[] = {&ids_c, &gout, &n, &tables, &k_bits, &part_bits, &per, &counters, &st};
+  e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(apply_gather_kernel), dim3(grid), dim3(1024), args,
+                                  smem, s);
+  count_launch();
+  return e;
 }
 
 cudaError_t launch_remove_check(const uint32_t* ids, uint64_t n, uint32_t tables, uint32_t k_bits,

@@ -32,6 +32,11 @@ cudaError_t launch_apply_ids(const uint32_t* ids, uint64_t n, uint32_t tables,
                              uint32_t k_bits, uint32_t* counters, uint32_t cap,
                              int sign, DevState* st, cudaStream_t s, bool track_t = true,
                              uint64_t ids_stride = 0);  // 0: n
+// build + detect over the same rows (32-bit, unsaturable, K <= 20): counts
+// into `counters` (T = sum c^2 recomputed) and every id replaced by its final
+// count in `gout` (== ids when K <= 15); score with counters == nullptr.
+cudaError_t launch_apply_gather(uint32_t* ids, uint32_t* gout, uint64_t n, uint32_t tables, uint32_t k_bits,
+                                uint32_t* counters, DevState* st, cudaStream_t s);
 // Remove validation: counts, per counter, how many removals target it and
 // flags underflow (any count < demand).  scratch: L x 2^K u32, zeroed here.
 cudaError_t launch_remove_check(const uint32_t* ids, uint64_t n, uint32_t tables,
