@@ -280,3 +280,43 @@ def test_repeated_calls_replay_graph(cuda, golden, cfg):
         sk.reset()
         sk.build_detect(xp)
         assert sha(sk.counters_u32()) == e["counters_sha256"]
+
+
+def test_fused_gather_path_all_shapes(cuda, golden):
+    """The fused count-and-gather pass (forced on with ACE_FUSED_GATHER=2, in
+    a subprocess: the switch is read once) on configs 1, 2 and the K = 16
+    prefix of 3 (two histogram parts): reference counters and flags."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    code = r'''
+import hashlib, json, sys
+import numpy as np, torch
+sys.path.insert(0, %r)
+from paper_1706_06664_b200 import ace
+from paper_1706_06664_b200 import workloads as W
+g = json.loads(open(%r).read())
+out = {}
+for cfg in (1, 2, 3):
+    e = g["configs"][str(cfg)]
+    w = W.CONFIGS[cfg]
+    x, _ = W.host_rows(cfg, 0, e["n"])
+    fam = ace.SrpFamily(ace.SrpConfig(dim=w.dim, k_bits=w.k_bits, num_tables=w.num_tables, seed=w.w_seed))
+    sk = ace.AceSketch(fam, ace.CounterWidth.k32)
+    rep = sk.build_detect(torch.from_numpy(x).cuda())
+    out[cfg] = [hashlib.sha256(sk.counters_u32().tobytes()).hexdigest(),
+                hashlib.sha256(np.packbits(rep.flags, bitorder="little").tobytes()).hexdigest(), int(rep.reported)]
+print(json.dumps(out))
+''' % (str(root), str(root / "tests" / "golden" / "golden.json"))
+    env = dict(os.environ, ACE_FUSED_GATHER="2")
+    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    got = json.loads(res.stdout.strip().splitlines()[-1])
+    for cfg in ("1", "2", "3"):
+        e = golden["configs"][cfg]
+        assert got[cfg][0] == e["counters_sha256"], cfg
+        assert got[cfg][1] == e["flags_sha256"], cfg
+        assert got[cfg][2] == e["reported"], cfg
