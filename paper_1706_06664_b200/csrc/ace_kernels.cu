@@ -809,7 +809,18 @@ __global__ void finalize_batch_kernel(uint64_t n, uint32_t tables, DevState* st)
   b.w[1] = __umul64hi(sum, sum);
   b.w[2] = 0;
   const U192 V = ge192(a, b) ? sub192(a, b) : U192{{0, 0, 0}};
-  const U192 r = isqrt192(V);
+  U192 r;
+  if (V.w[2] == 0 && V.w[1] < (1ull << 40)) {
+    // V < 2^104: a binary64 estimate is within a few units of isqrt(V);
+    // settle it exactly with 128-bit squares
+    const unsigned __int128 v = (static_cast<unsigned __int128>(V.w[1]) << 64) | V.w[0];
+    unsigned long long q = static_cast<unsigned long long>(sqrt(static_cast<double>(v)));
+    while (q > 0 && static_cast<unsigned __int128>(q) * q > v) --q;
+    while (static_cast<unsigned __int128>(q + 1) * (q + 1) <= v) ++q;
+    r = U192{{q, 0, 0}};
+  } else {
+    r = isqrt192(V);
+  }
   // flag <=> S/L < sum/(N L) - sqrt(V)/(N L) <=> N*S <= sum - isqrt(V) - 1
   long long s_cut = -1;
   if (r.w[2] == 0 && r.w[1] == 0 && r.w[0] < sum) {
@@ -830,13 +841,15 @@ __global__ void finalize_batch_kernel(uint64_t n, uint32_t tables, DevState* st)
   d_sd += 2.0 * u * sd;
   const double delta = 2.0 * (e_mean + d_sd + 2.0 * u * fabs(thr)) + 4.0 * u * (fabs(mean) + sd);
   const double L = static_cast<double>(tables);
-  st->s_cut = s_cut;
-  st->s_lo = static_cast<long long>(ceil((thr - delta) * L * (1.0 - 4.0 * u)) - 1.0);
-  st->s_hi = static_cast<long long>(floor((thr + delta) * L * (1.0 + 4.0 * u)) + 1.0);
-  if (st->s_lo < 0) st->s_lo = 0;
+  long long s_lo = static_cast<long long>(ceil((thr - delta) * L * (1.0 - 4.0 * u)) - 1.0);
+  long long s_hi = static_cast<long long>(floor((thr + delta) * L * (1.0 + 4.0 * u)) + 1.0);
+  if (s_lo < 0) s_lo = 0;
   // tighten: only integer S whose score can lie within delta of thr
-  while (st->s_lo <= st->s_hi && static_cast<double>(st->s_lo) / L < thr - delta) ++st->s_lo;
-  while (st->s_hi >= st->s_lo && static_cast<double>(st->s_hi) / L > thr + delta) --st->s_hi;
+  while (s_lo <= s_hi && static_cast<double>(s_lo) / L < thr - delta) ++s_lo;
+  while (s_hi >= s_lo && static_cast<double>(s_hi) / L > thr + delta) --s_hi;
+  st->s_cut = s_cut;
+  st->s_lo = s_lo;
+  st->s_hi = s_hi;
   st->mean = mean;
   st->sd = sd;
   st->thr = thr;
