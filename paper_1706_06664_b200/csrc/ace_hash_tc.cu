@@ -1299,17 +1299,21 @@ __global__ void __launch_bounds__(kKsThreads, 1) hash_tck_kernel(const TcArgs a)
   __syncthreads();
   tc_after();
   const uint32_t tmem_base = tmem_base_sh;
-  const uint64_t iters = (n_tiles + gridDim.x - 1) / gridDim.x;
+  // work items (point tile t, direction tile j), j fastest: the CTAs running
+  // side by side share few point tiles, so A chunks are re-read from L2
+  const uint64_t n_items = n_tiles * a.ntiles;
+  const uint64_t iters = (n_items + gridDim.x - 1) / gridDim.x;
   const unsigned long long seg_cap = a.near_cap / gridDim.x;
+  const uint32_t tpt = a.tpt;  // whole tables per direction tile
 
   if (warp == 0) {
     // ---- producer: per (tile, direction tile, K chunk) one A chunk + one W chunk
     if (lane == 0) {
       uint32_t s = 0, ph = 0;
       for (uint64_t it = 0; it < iters; ++it) {
-        const uint64_t t = blockIdx.x + it * gridDim.x;
-        const uint64_t tt = t < n_tiles ? t : n_tiles - 1;
-        for (uint32_t j = 0; j < a.ntiles; ++j)
+        const uint64_t w = min(blockIdx.x + it * gridDim.x, n_items - 1);  // past the end: redo the last item
+        const uint64_t tt = w / a.ntiles;
+        const uint32_t j = static_cast<uint32_t>(w % a.ntiles);
           for (uint32_t kc = 0; kc < nkc; ++kc) {
             mbar_wait_sleepy(&bar_empty[s], ph ^ 1u, nullptr);
             mbar_expect_tx(&bar_full[s], kKsSlot);
@@ -1332,7 +1336,6 @@ __global__ void __launch_bounds__(kKsThreads, 1) hash_tck_kernel(const TcArgs a)
     const uint32_t ta = tmem_base + 256u;  // A buffers: [2][hi 32 | lo 32 columns]
     const uint32_t idesc = idesc_f16(128u);
     for (uint64_t it = 0; it < iters; ++it)
-      for (uint32_t j = 0; j < a.ntiles; ++j)
         for (uint32_t c = 0; c < nch; ++c) {
           mbar_wait(&bar_accempty[ab], abph ^ 1u);
           tc_after();
@@ -1380,15 +1383,18 @@ __global__ void __launch_bounds__(kKsThreads, 1) hash_tck_kernel(const TcArgs a)
     const uint32_t r = q * 32u + lane;
     const uint32_t kmask = (K >= 32u) ? 0xffffffffu : ((1u << K) - 1u);
     uint32_t ab = 0, abph = 0, par = 0;
-    for (uint64_t it = 0; it < iters; ++it) {
-      const uint64_t t = blockIdx.x + it * gridDim.x;
+    for (uint64_t it = 0; it < iters; ++it, par ^= 1u) {
+      const uint64_t w = blockIdx.x + it * gridDim.x;
+      const bool live_item = w < n_items;
+      const uint64_t t = (live_item ? w : n_items - 1) / a.ntiles;
+      const uint32_t j = static_cast<uint32_t>((live_item ? w : n_items - 1) % a.ntiles);
       const uint64_t row = t * kRows + r;
-      const bool valid = row < a.n;
+      const bool valid = live_item && row < a.n;
       const float thr = valid ? a.rowthr[row] : -1.0f;
       const bool zero_row = thr < 0.0f;
-      uint32_t prev3 = 0u;
-      for (uint32_t j = 0; j < a.ntiles; ++j, par ^= 1u) {
-        const uint32_t used = min(128u, R - j * 128u);
+      const uint32_t t0 = j * tpt, t1 = min(a.tables, t0 + tpt);  // tables of this direction tile
+      const uint32_t used = (t1 - t0) * K;
+      {
         float acc[64];
 #pragma unroll
         for (int i = 0; i < 64; ++i) acc[i] = 0.0f;
@@ -1421,24 +1427,21 @@ __global__ void __launch_bounds__(kKsThreads, 1) hash_tck_kernel(const TcArgs a)
             if (used - cc < 32u) nm &= (1u << (used - cc)) - 1u;
             if (nm)
               push_near_mask(a.st, a.near_list + blockIdx.x * seg_cap, seg_cap, &seg_n, a.overflow_rows, nm, row,
-                             j * 128u + cc);
+                             t0 * K + cc);
           }
           sgbuf[par][2 * h + g2][r] = zero_row ? 0xffffffffu : ~neg;  // bit (31-jj) = column cc+jj >= 0
         }
         asm volatile("bar.sync %0, 64;" ::"r"(1u + q) : "memory");  // the quarter's two warps
-        const uint32_t tb = j == 0 ? 0u : a.tab_end[j - 1], te = a.tab_end[j];
         uint32_t* idp = a.ids + row;
-        for (uint32_t tt = tb + h; tt < te; tt += 2) {
-          const uint32_t s0 = tt * K;
-          const int wi = static_cast<int>(s0 >> 5) - static_cast<int>(4 * j);  // -1 .. 3
-          const uint32_t off = s0 & 31u;
-          const uint32_t hi = wi < 0 ? prev3 : sgbuf[par][wi][r];
+        for (uint32_t tt = t0 + h; tt < t1; tt += 2) {
+          const uint32_t s0 = (tt - t0) * K;  // whole tables: no straddling
+          const uint32_t wi = s0 >> 5, off = s0 & 31u;
+          const uint32_t hi = sgbuf[par][wi][r];
           const uint32_t lo = wi < 3 ? sgbuf[par][wi + 1][r] : 0u;
           const unsigned long long win = (static_cast<unsigned long long>(hi) << 32) | lo;
           const uint32_t bucket = static_cast<uint32_t>(win >> (64u - off - K)) & kmask;
           if (valid) idp[static_cast<uint64_t>(tt) * a.n] = bucket;
         }
-        prev3 = sgbuf[par][3][r];
       }
     }
   }
@@ -1687,8 +1690,11 @@ __global__ void dir_norm_kernel(const double* __restrict__ w64, uint64_t dim, ui
   inv[r] = s > 0.0 ? 16384.0 / sqrt(s) : 0.0;
 }
 
+// Direction tile j holds directions j*dpt .. j*dpt + dpt - 1 in rows 0..dpt-1
+// (dpt = tw: packed densely; dpt = tables-per-tile * K: whole tables per tile,
+// the K-streamed kernel), zero rows beyond.
 __global__ void pack_w16_kernel(const double* __restrict__ w64, const double* __restrict__ inv,
-                                FamilyDev f, uint32_t ntiles, uint32_t nkc, uint32_t tw, uint16_t* w16) {
+                                FamilyDev f, uint32_t ntiles, uint32_t nkc, uint32_t tw, uint32_t dpt, uint16_t* w16) {
   const uint64_t total = static_cast<uint64_t>(ntiles) * tw * nkc * kChunk;
   const uint32_t wblk = tw * 128u;
   for (uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
@@ -1697,9 +1703,9 @@ __global__ void pack_w16_kernel(const double* __restrict__ w64, const double* __
     const uint32_t rr = (idx / (nkc * kChunk)) % tw;
     const uint32_t j = static_cast<uint32_t>(idx / (static_cast<uint64_t>(nkc) * kChunk * tw));
     const uint32_t kc = k / kChunk, kk = k % kChunk;
-    const uint64_t dir = static_cast<uint64_t>(j) * tw + rr;  // directions packed densely
+    const uint64_t dir = static_cast<uint64_t>(j) * dpt + rr;
     double w = 0.0;
-    if (dir < f.rows && k < f.dim) w = w64[dir * f.dim + k] * inv[dir];
+    if (rr < dpt && dir < f.rows && k < f.dim) w = w64[dir * f.dim + k] * inv[dir];
     const __half hi = __double2half(w);
     const __half lo = __double2half(w - static_cast<double>(__half2float(hi)));
     uint8_t* blk = reinterpret_cast<uint8_t*>(w16) + ((static_cast<uint64_t>(j) * nkc + kc) * 2) * wblk;
@@ -1744,15 +1750,19 @@ cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc) {
   if ((!tc_kstream(nkc) && L.n_wst < 2) || (tc_kstream(nkc) && kPair != 1)) return cudaSuccess;
   tc->nkc = nkc;
   tc->tw = tw;
-  tc->ntiles = (f.rows + tw - 1) / tw;
-  if (tc->ntiles > 64) return cudaSuccess;  // TcArgs::tab_end
+  // K-streamed kernel: whole tables per direction tile (no table straddles
+  // two tiles, so (point tile, direction tile) items are independent)
+  const uint32_t tpt = 128u / f.k_bits;
+  const uint32_t dpt = tc_kstream(nkc) ? tpt * f.k_bits : tw;
+  tc->ntiles = tc_kstream(nkc) ? (f.tables + tpt - 1) / tpt : (f.rows + tw - 1) / tw;
+  if (tc->ntiles > 64 && !tc_kstream(nkc)) return cudaSuccess;  // TcArgs::tab_end
   const size_t bytes = static_cast<size_t>(tc->ntiles) * nkc * 2 * tw * 128u;
   cudaError_t e = cudaMalloc(&tc->w16, bytes);
   if (e != cudaSuccess) return e;
   double* inv = nullptr;
   if ((e = cudaMalloc(&inv, sizeof(double) * f.rows)) != cudaSuccess) return e;
   dir_norm_kernel<<<(f.rows + 127) / 128, 128>>>(f.w64, f.dim, f.rows, inv);
-  pack_w16_kernel<<<1024, 256>>>(f.w64, inv, f, tc->ntiles, nkc, tw, tc->w16);
+  pack_w16_kernel<<<1024, 256>>>(f.w64, inv, f, tc->ntiles, nkc, tw, dpt, tc->w16);
   count_launch(2);
   e = cudaDeviceSynchronize();
   cudaFree(inv);
