@@ -224,6 +224,20 @@ __device__ __forceinline__ void fence_mbar_init() {
 }
 __device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// Fences inside the MMA <-> epilogue pipeline, as the PTX memory model asks
+// for thread-synchronised tcgen05 accesses.  (CUTLASS's SM100 pipelines omit
+// them; removing them measured no difference here: the ~250 cycles the
+// after_thread_sync fence holds the issuing warp are hidden by the queued
+// MMAs.)  ACE_TC_FENCES=0 drops them.
+#ifndef ACE_TC_FENCES
+#define ACE_TC_FENCES 1
+#endif
+__device__ __forceinline__ void pipe_before() {
+  if (ACE_TC_FENCES) tc_before();
+}
+__device__ __forceinline__ void pipe_after() {
+  if (ACE_TC_FENCES) tc_after();
+}
 
 // K-major SWIZZLE_128B shared-memory matrix descriptor (sm_100 version 1).
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
@@ -785,6 +799,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
     {
       uint32_t s = 0, wph = 0, acc = 0, accph = 0;
       unsigned long long pmi = 0, pmn = 0, pcp = 0;  // instrumentation: MMA-group issue cycles / groups, A copies
+      unsigned long long pfence = 0;
       const long long ploop = clock64();
       const uint32_t nacc = tc_acc_bufs(a.nkc, TW);
       const uint32_t ta_hi = tmem_base + nacc * TW, ta_lo = ta_hi + a.nkc * 32u;  // dpad/2 columns each
@@ -792,7 +807,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
       const uint32_t half = kPair == 2 ? kBlockBytes / kPair : wblk;  // bytes of one W block (hi or lo) per CTA
       for (uint64_t it = 0; it < iters; ++it) {
         mbar_wait_t(&bar_afull[0], static_cast<uint32_t>(it) & 1u, (prof && lane == 0) ? &pw[2] : nullptr);
-        tc_after();
+        pipe_after();
         const long long pc0 = prof ? clock64() : 0;
         // copies execute in issue order after this CTA's earlier MMAs, so the
         // previous tile's reads of TMEM A are complete before it is replaced
@@ -819,7 +834,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
             const uint32_t nmma = kPair == 2 ? 128u : ((min(TW, R - j * TW) + 15u) & ~15u);
             const uint32_t idesc = idesc_f16(nmma);
             mbar_wait(&bar_accempty[ac], acph ^ 1u);
-            tc_after();
+            pipe_after();
             const uint32_t dt = tmem_base + ac * TW;
             for (uint32_t kc = 0; kc < a.nkc; ++kc) {
               mbar_wait(&bar_wfull[ss], ph);
@@ -867,7 +882,9 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
           const uint32_t nmma = kPair == 2 ? 128u : ((min(TW, R - j * TW) + 15u) & ~15u);
           const uint32_t idesc = idesc_f16(nmma);
           mbar_wait_t(&bar_accempty[acc], accph ^ 1u, (prof && lane == 0) ? &pw[3] : nullptr);
-          tc_after();
+          const long long pf0 = prof ? clock64() : 0;
+          pipe_after();
+          if (prof) pfence += static_cast<unsigned long long>(clock64() - pf0);
           const uint32_t dt = tmem_base + acc * TW;
           // one elected burst per direction tile: the issuing lane waits for
           // each stage itself (no warp-wide syncs between the MMA groups, so
@@ -920,6 +937,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
         atomicAdd(&a.prof[22], pcp);
         atomicAdd(&a.prof[23], static_cast<unsigned long long>(clock64() - ploop));
         atomicAdd(&a.prof[24], pw[2] + pw[3] + pw[4]);
+        atomicAdd(&a.prof[25], pfence);
       }
     }
   } else if (kFuse && warp >= 10) {
@@ -1054,7 +1072,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
           const uint32_t used = min(TW, R - j * TW);
           const uint32_t col0 = j * TW;
           mbar_wait_sleepy(&bar_accfull[acc], accph, (prof && lane == 0) ? &pw[5] : nullptr);
-          tc_after();
+          pipe_after();
           long long pc0 = prof ? clock64() : 0, pc1 = 0, pc2 = 0;
           uint32_t wd0 = 0xffffffffu, wd1 = 0xffffffffu, wd2 = 0xffffffffu, wd3 = 0xffffffffu;
           uint32_t wd4 = 0xffffffffu, wd5 = 0xffffffffu;
@@ -1114,7 +1132,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
               }
             }
           }
-          tc_before();
+          pipe_before();
           __syncwarp();
           if (prof) pc2 = clock64();
           if (lane == 0) {
@@ -1338,7 +1356,7 @@ __global__ void __launch_bounds__(kKsThreads, 1) hash_tck_kernel(const TcArgs a)
     for (uint64_t it = 0; it < iters; ++it)
         for (uint32_t c = 0; c < nch; ++c) {
           mbar_wait(&bar_accempty[ab], abph ^ 1u);
-          tc_after();
+          pipe_after();
           const uint32_t k0 = c * kKsSc, k1 = min(nkc, k0 + kKsSc);
           const uint32_t dt = tmem_base + ab * 128u;
           if (elect_one()) {
@@ -1400,14 +1418,14 @@ __global__ void __launch_bounds__(kKsThreads, 1) hash_tck_kernel(const TcArgs a)
         for (int i = 0; i < 64; ++i) acc[i] = 0.0f;
         for (uint32_t c = 0; c < nch; ++c) {
           mbar_wait_sleepy(&bar_accfull[ab], abph, nullptr);
-          tc_after();
+          pipe_after();
           uint32_t v[64];
           ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + ab * 128u + 64u * h, v);
           ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + ab * 128u + 64u * h + 32u, (v + 32));
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 64; ++i) acc[i] += __uint_as_float(v[i]);
-          tc_before();
+          pipe_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&bar_accempty[ab]);
           ab ^= 1u;
