@@ -249,7 +249,7 @@ def run_stream(args, w, ws, rank, local):
         "vs_baseline": None, "dtype": "f32", "data": f"synthetic (datagen cfg {w.cfg}, seed {w.data_seed})",
         "config": {"workload": f"cfg{w.cfg} {w.name}: streaming score -> flag (mean - alpha) -> insert",
                    "N": n, "d": w.dim, "K": w.k_bits, "L": w.num_tables, "batch": w.batch,
-                   "hash_group_batches": int(os.environ.get("ACE_STREAM_GROUP", "8")),
+                   "hash_group_batches": int(os.environ.get("ACE_STREAM_GROUP", "4")),
                    "alpha": w.alpha, "counter_width": 32,
                    "l2": f"inputs {n * w.dim * 4 / 1e9:.1f} GB > 126 MB L2",
                    "parallelism": f"replicas x{ws}"},

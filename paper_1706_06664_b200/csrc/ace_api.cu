@@ -999,7 +999,7 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
   static int group_env = -1;
   if (group_env < 0) {
     const char* e = getenv("ACE_STREAM_GROUP");
-    group_env = e ? std::max(1, atoi(e)) : 8;
+    group_env = e ? std::max(1, atoi(e)) : 4;
   }
   const uint64_t G = static_cast<uint64_t>(group_env);
   for (uint64_t g0 = 0; g0 < nb; g0 += G) {
