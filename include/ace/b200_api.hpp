@@ -11,6 +11,7 @@
 // row-major fp32 matrices, the north-star input format.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <memory>
 #include <optional>
@@ -122,9 +123,28 @@ class SrpFamily {
   // Device handle (created on first use; shared by copies).
   ::AceFamily* device() const;
 
+  // Noisy variant (noise_scale > 0, srp.cpp:93-104): reserves `count` ticks of
+  // this family's noise stream and returns the terms noise_scale * N(0,1).
+  std::vector<double> draw_noise(std::size_t count) const;
+  // Bucket ids (table-major, nt x n) of n points with a noisy family, bits
+  // [b0, b0+nb) of tables [t0, t0+nt), ticks in point / table / bit order.
+  std::vector<std::uint32_t> noisy_ids(const void* x, int dtype, std::size_t n, std::size_t t0, std::size_t nt,
+                                       std::size_t b0, std::size_t nb) const;
+
  private:
+  struct NoiseCounter {  // the reference's atomic tick counter; copies take the current value
+    std::atomic<std::uint64_t> v{0};
+    NoiseCounter() = default;
+    NoiseCounter(const NoiseCounter& o) : v(o.v.load(std::memory_order_relaxed)) {}
+    NoiseCounter& operator=(const NoiseCounter& o) {
+      v.store(o.v.load(std::memory_order_relaxed), std::memory_order_relaxed);
+      return *this;
+    }
+  };
   void check(std::size_t table, std::size_t b, std::span<const double> x) const;
   SrpConfig cfg_;
+  mutable std::uint64_t noise_seed_ = 0;
+  mutable NoiseCounter noise_ctr_;
   std::shared_ptr<const std::vector<double>> w_;  // (K*L) x d, host copy
   std::shared_ptr<std::shared_ptr<::AceFamily>> dev_;  // created on first use, shared by copies
 };

@@ -106,6 +106,19 @@ ace_status ace_family_buckets(AceFamily* fam, const void* x, int dtype,
                               uint64_t n, uint64_t ld, int x_where,
                               uint32_t* ids, int ids_where, AceHashStats* stats);
 
+/* Noisy (private) hashing, SrpFamily::bit with noise_scale > 0
+ * (srp.cpp:93-104), exact: for tables [t0, t0+nt) and bits [b0, b0+nb) of
+ * each, value = RN(p + noise[(i*nt + t-t0)*nb + b-b0]) with p the binary64
+ * left fold and noise the pre-scaled terms noise_scale * N(0,1) drawn on the
+ * host in tick order (ace_noise_terms, include/ace_host.h); bit = value >= 0,
+ * packed MSB-first into ids[(t-t0)*n + i].  The regular hashing entry points
+ * return ACE_E_UNSUPPORTED for a noisy family. */
+ace_status ace_family_buckets_noisy(AceFamily* fam, const void* x, int dtype,
+                                    uint64_t n, uint64_t ld, int x_where,
+                                    uint32_t t0, uint32_t nt, uint32_t b0, uint32_t nb,
+                                    const double* noise, int noise_where,
+                                    uint32_t* ids, int ids_where);
+
 /* ---- AceSketch (sketch.hpp:25-84) -------------------------------------- */
 /* counter_width 16 or 32 (CounterWidth, sketch.hpp:11). */
 ace_status ace_sketch_create(AceFamily* fam, uint32_t counter_width,
@@ -121,6 +134,12 @@ ace_status ace_sketch_set_stream(AceSketch* sk, void* cuda_stream);
 /* AceSketch::insert (sketch.cpp:50-72) for n rows, in row order. */
 ace_status ace_sketch_insert(AceSketch* sk, const void* x, int dtype, uint64_t n,
                              uint64_t ld, int x_where, AceHashStats* stats);
+/* Insert / score n points given by their bucket ids (L x n, table-major,
+ * ids < 2^K; host ids are validated): the counter, mean and score logic of
+ * AceSketch::insert / score without hashing (the noisy variant's path). */
+ace_status ace_sketch_insert_ids(AceSketch* sk, const uint32_t* ids, uint64_t n, int where);
+ace_status ace_sketch_score_ids(AceSketch* sk, const uint32_t* ids, uint64_t n, int where,
+                                double* scores, uint64_t* sums, int out_where);
 /* AceSketch::remove (sketch.cpp:74-106) for n rows.  The batch is
  * all-or-nothing: if any target counter would reach below zero the call
  * returns ACE_E_INCONSISTENT and the sketch is unchanged. */

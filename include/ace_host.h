@@ -21,6 +21,12 @@ int ace_generate_directions(uint64_t seed, uint64_t dim, uint32_t k_bits, uint32
 int ace_load_dataset_csv(const char* path, int has_label, int label_column, double** values, uint64_t* rows,
                          uint64_t* cols, uint8_t** labels);
 const char* ace_host_last_error(void);
+
+/* Noise terms of the noisy hash variant for ticks tick0 .. tick0+count-1
+ * (reference srp.cpp:97-101): noise_scale * NormalStream(mix_seed(noise_seed,
+ * tick)).next() with glibc libm, as the reference draws them; input to
+ * ace_family_buckets_noisy.  0 ok. */
+int ace_noise_terms(uint64_t noise_seed, uint64_t tick0, uint64_t count, double noise_scale, double* out);
 void ace_free(void* p);
 
 #ifdef __cplusplus

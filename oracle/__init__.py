@@ -202,6 +202,13 @@ class Reference:
         L.ref_load_sketch.restype = _vp
         L.ref_load_sketch.argtypes = [C.c_char_p, _P(_i)]
         L.ref_sketch_config.argtypes = [_vp, _P(_u64), _P(_u32), _P(_u32), _P(_u64), _P(_u32)]
+        L.ref_sketch_new_noisy.restype = _vp
+        L.ref_sketch_new_noisy.argtypes = [_u64, _u64, _u32, _u32, _u32, _d]
+        L.ref_sketch_reset_noise.argtypes = [_vp, _u64]
+        L.ref_noisy_calls.restype = _i
+        L.ref_noisy_calls.argtypes = [_u64, _u64, _u32, _u32, _d, _i, _u64, _vp, _u64, _u32, _u32, _i, _vp]
+        L.ref_noisy_sequence.restype = _i
+        L.ref_noisy_sequence.argtypes = [_u64, _u64, _u32, _u32, _d, _u64, _vp, _vp, _u64, _vp]
         L.ref_load_dataset.restype = _i
         L.ref_load_dataset.argtypes = [C.c_char_p, _i, _i, _vp, _vp, _vp, _vp]
         L.ref_free.argtypes = [_vp]
@@ -228,6 +235,36 @@ class Reference:
             self.L.ref_free(labs)
         self.L.ref_free(vals)
         return v, lab
+
+    def noisy_calls(self, seed, dim, k, l, noise, x, t0, nt, b=-1, aux=None):
+        """A noisy family's bucket (b < 0) or bit(t, b) calls, rows in order,
+        tables t0..t0+nt-1; ids (nt, n)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        n = x.shape[0]
+        ids = np.empty((nt, n), dtype=np.uint32)
+        self._ok(self.L.ref_noisy_calls(seed, dim, k, l, noise, int(aux is not None), aux or 0, x.ctypes.data, n,
+                                        t0, nt, b, ids.ctypes.data))
+        return ids
+
+    def noisy_sequence(self, seed, dim, k, l, noise, aux, x, ops):
+        """Calls (row, table, b) on one noisy family after reset_noise_stream(aux);
+        b < 0 is bucket(table, x[row]), else bit(table, b, x[row])."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        o = np.ascontiguousarray(np.asarray(ops, dtype=np.int32).reshape(-1, 3))
+        out = np.empty(o.shape[0], dtype=np.uint32)
+        self._ok(self.L.ref_noisy_sequence(seed, dim, k, l, noise, aux, x.ctypes.data, o.ctypes.data, o.shape[0],
+                                           out.ctypes.data))
+        return out
+
+    def noisy_sketch(self, seed, dim, k, l, noise, width=32, aux=None) -> "RefSketch":
+        r = RefSketch.__new__(RefSketch)
+        r.r, r.dim, r.k, r.l = self, dim, k, l
+        r.h = self.L.ref_sketch_new_noisy(seed, dim, k, l, width, noise)
+        if not r.h:
+            raise RuntimeError(self.L.ref_last_error().decode())
+        if aux is not None:
+            self.L.ref_sketch_reset_noise(r.h, aux)
+        return r
 
     def load_sketch(self, path) -> "RefSketch":
         """ace::io::load_sketch (io.cpp:213-244); DataError -> ValueError."""

@@ -13,6 +13,7 @@
 #include <cstring>
 #include <optional>
 #include <exception>
+#include <span>
 #include <string>
 #include <thread>
 #include <vector>
@@ -108,6 +109,66 @@ void* ref_sketch_new(uint64_t seed, uint64_t dim, uint32_t k, uint32_t l, uint32
 }
 
 void ref_sketch_free(void* h) { delete static_cast<RefSketch*>(h); }
+
+// Noisy variant (srp.cpp:93-104): a sketch over a noisy family; its family
+// copy's aux stream can be re-seeded (reset_noise_stream, srp.cpp:126-129).
+void* ref_sketch_new_noisy(uint64_t seed, uint64_t dim, uint32_t k, uint32_t l, uint32_t width, double noise) {
+  try {
+    auto c = make_cfg(dim, k, l, seed);
+    c.noise_scale = noise;
+    const ace::SrpFamily fam(c);
+    return new RefSketch(fam, width == 16 ? ace::CounterWidth::k16 : ace::CounterWidth::k32);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+void ref_sketch_reset_noise(void* h, uint64_t aux) {
+  static_cast<RefSketch*>(h)->sketch.family().reset_noise_stream(aux);
+}
+
+// A noisy family's bucket calls in order: for each row i, tables t0..t0+nt-1
+// (bucket) or, with b >= 0, the single bit (t, b) of each table.  ids[t*n+i].
+// A sequence of calls on one noisy family: op j = (row, table, b), b < 0
+// meaning bucket(table, row) and b >= 0 bit(table, b, row).
+int ref_noisy_sequence(uint64_t seed, uint64_t dim, uint32_t k, uint32_t l, double noise, uint64_t aux,
+                       const double* x, const int32_t* ops, uint64_t nops, uint32_t* out) {
+  try {
+    auto c = make_cfg(dim, k, l, seed);
+    c.noise_scale = noise;
+    const ace::SrpFamily fam(c);
+    fam.reset_noise_stream(aux);
+    for (uint64_t j = 0; j < nops; ++j) {
+      std::span<const double> row(x + static_cast<uint64_t>(ops[3 * j]) * dim, dim);
+      const auto t = static_cast<std::size_t>(ops[3 * j + 1]);
+      out[j] = ops[3 * j + 2] < 0 ? fam.bucket(t, row) : fam.bit(t, static_cast<std::size_t>(ops[3 * j + 2]), row);
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+int ref_noisy_calls(uint64_t seed, uint64_t dim, uint32_t k, uint32_t l, double noise, int reset, uint64_t aux,
+                    const double* x, uint64_t n, uint32_t t0, uint32_t nt, int b, uint32_t* ids) {
+  try {
+    auto c = make_cfg(dim, k, l, seed);
+    c.noise_scale = noise;
+    const ace::SrpFamily fam(c);
+    if (reset) fam.reset_noise_stream(aux);
+    for (uint64_t i = 0; i < n; ++i) {
+      std::span<const double> row(x + i * dim, dim);
+      for (uint32_t t = 0; t < nt; ++t)
+        ids[static_cast<uint64_t>(t) * n + i] = b < 0 ? fam.bucket(t0 + t, row) : fam.bit(t0 + t, b, row);
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
 
 // AceSketch::insert (sketch.cpp:50-72) for each row in order.
 int ref_sketch_insert(void* h, const float* x, uint64_t n, uint64_t dim) {

@@ -80,11 +80,18 @@ ABI = {
     "ace_sketch_timings": (_i, [_vp, _vp]),
 }
 
+ABI.update({
+    "ace_family_buckets_noisy": (_i, [_vp, _vp, _i, _u64, _u64, _i, _u32, _u32, _u32, _u32, _vp, _i, _vp, _i]),
+    "ace_sketch_insert_ids": (_i, [_vp, _vp, _u64, _i]),
+    "ace_sketch_score_ids": (_i, [_vp, _vp, _u64, _i, _vp, _vp, _i]),
+})
+
 HOST_ABI = {
     "ace_generate_directions": (_i, [_u64, _u64, _u32, _u32, _vp]),
     "ace_load_dataset_csv": (_i, [C.c_char_p, _i, _i, _vp, _vp, _vp, _vp]),
     "ace_host_last_error": (C.c_char_p, []),
     "ace_free": (None, [_vp]),
+    "ace_noise_terms": (_i, [_u64, _u64, _u64, _d, _vp]),
 }
 
 DATAGEN_ABI = {

@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import math
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -119,6 +120,17 @@ def generate_directions(seed: int, dim: int, k_bits: int, num_tables: int) -> np
     return w
 
 
+_M64 = (1 << 64) - 1
+
+
+def mix_seed(seed: int, index: int) -> int:
+    """rng::mix_seed (rng.hpp:19-22): splitmix64 of seed ^ golden * (index + 1)."""
+    z = ((seed ^ ((0x9e3779b97f4a7c15 * (index + 1)) & _M64)) + 0x9e3779b97f4a7c15) & _M64
+    z = ((z ^ (z >> 30)) * 0xbf58476d1ce4e5b9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94d049bb133111eb) & _M64
+    return z ^ (z >> 31)
+
+
 def _bits_to_bool(bits: np.ndarray, n: int) -> np.ndarray:
     return np.unpackbits(bits.view(np.uint8), bitorder="little")[:n].astype(bool)
 
@@ -157,10 +169,25 @@ class SrpFamily:
         self._cfg = SrpConfig(**cfg.__dict__)
         self._w = generate_directions(cfg.seed, cfg.dim, cfg.k_bits, cfg.num_tables)
         self._dev: Optional[C.c_void_p] = None
+        self._owner = True
+        # noisy variant (srp.cpp:34, 97-101): aux stream seed and tick counter
+        self._noise_seed = mix_seed(cfg.seed, 0x6e6f697365)
+        self._noise_ctr = 0
+
+    def _copy(self) -> "SrpFamily":
+        """Copy semantics of the reference (srp.cpp:51-64): same W (device
+        handle shared), own noise counter starting at the current value."""
+        o = SrpFamily.__new__(SrpFamily)
+        o.__dict__.update(self.__dict__)
+        o._owner = False
+        o._parent = self if self._owner else self._parent  # keeps the shared device handle alive
+        return o
 
     # device handle, created on first use
     @property
     def handle(self) -> C.c_void_p:
+        if not self._owner:
+            return self._parent.handle
         if self._dev is None:
             h = C.c_void_p()
             _check(N.dev().ace_family_create(self._cfg.dim, self._cfg.k_bits, self._cfg.num_tables,
@@ -170,7 +197,7 @@ class SrpFamily:
 
     def __del__(self):
         try:
-            if self._dev is not None:
+            if self._owner and self._dev is not None:
                 N.dev().ace_family_destroy(self._dev)
         except Exception:
             pass
@@ -202,11 +229,36 @@ class SrpFamily:
         return self._w.nbytes if self._cfg.cache_projections else 0
 
     def reset_noise_stream(self, aux_seed: int) -> None:
-        if self._cfg.noise_scale > 0:
-            raise UnsupportedOperation("SrpFamily: the noisy hash variant has no device path")
+        """srp.cpp:126-129."""
+        self._noise_seed = int(aux_seed) & _M64
+        self._noise_ctr = 0
+
+    def draw_noise(self, count: int) -> np.ndarray:
+        """Reserve `count` ticks; the terms noise_scale * N(0,1) (glibc libm, libace.so)."""
+        out = np.empty(count, dtype=np.float64)
+        tick0 = self._noise_ctr
+        self._noise_ctr += count
+        if count and N.host().ace_noise_terms(self._noise_seed, tick0, count, self._cfg.noise_scale,
+                                              out.ctypes.data) != 0:
+            raise ContractViolation("ace_noise_terms failed")
+        return out
+
+    def noisy_ids(self, x, t0: int, nt: int, b0: int, nb: int) -> np.ndarray:
+        """Noisy bucket ids (nt, n): bits [b0, b0+nb) of tables [t0, t0+nt),
+        ticks in point / table / bit order (srp.cpp:93-104)."""
+        p = _Points(x, self._cfg.dim)
+        noise = self.draw_noise(p.n * nt * nb)
+        ids = np.empty((nt, p.n), dtype=np.uint32)
+        if p.n and nt:
+            _check(N.dev().ace_family_buckets_noisy(self.handle, p.ptr, p.dtype, p.n, p.ld, p.where, t0, nt, b0,
+                                                    nb, noise.ctypes.data, N.ACE_HOST, ids.ctypes.data,
+                                                    N.ACE_HOST))
+        return ids
 
     def buckets(self, x, stats: Optional[N.AceHashStats] = None) -> np.ndarray:
         """Bucket ids, shape (L, n) uint32 (batched SrpFamily::bucket)."""
+        if self._cfg.noise_scale > 0:
+            return self.noisy_ids(x, 0, self._cfg.num_tables, 0, self._cfg.k_bits)
         p = _Points(x, self._cfg.dim)
         ids = np.empty((self._cfg.num_tables, p.n), dtype=np.uint32)
         st = stats if stats is not None else N.AceHashStats()
@@ -217,10 +269,14 @@ class SrpFamily:
 
     def bucket(self, table: int, x) -> int:
         self._check_indices(table, 0, x)
+        if self._cfg.noise_scale > 0:
+            return int(self.noisy_ids(np.asarray(x, dtype=np.float64), table, 1, 0, self._cfg.k_bits)[0, 0])
         return int(self.buckets(np.asarray(x, dtype=np.float64))[table, 0])
 
     def bit(self, table: int, b: int, x) -> int:
         self._check_indices(table, b, x)
+        if self._cfg.noise_scale > 0:  # one tick
+            return int(self.noisy_ids(np.asarray(x, dtype=np.float64), table, 1, b, 1)[0, 0])
         return (self.bucket(table, x) >> (self._cfg.k_bits - 1 - b)) & 1
 
     def _check_indices(self, table: int, b: int, x) -> None:
@@ -259,7 +315,7 @@ class AceSketch:
     kHeaderBytes = 53
 
     def __init__(self, family: SrpFamily, width: CounterWidth = CounterWidth.k16):
-        self._family = family
+        self._family = family._copy()  # by value, as the reference (sketch.hpp:77)
         self._width = CounterWidth(width)
         h = C.c_void_p()
         _check(N.dev().ace_sketch_create(family.handle, int(self._width), C.byref(h)))
@@ -299,8 +355,15 @@ class AceSketch:
     def _dim(self) -> int:
         return self._family.config().dim
 
+    def _noisy(self) -> bool:
+        return self._family.config().noise_scale > 0
+
     def insert(self, x) -> None:
         """AceSketch::insert (sketch.cpp:50-72); 2-D input inserts rows in order."""
+        if self._noisy():
+            ids = np.ascontiguousarray(self._family.buckets(x))
+            _check(N.dev().ace_sketch_insert_ids(self._h, ids.ctypes.data, ids.shape[1], N.ACE_HOST))
+            return
         p = _Points(x, self._dim())
         _check(N.dev().ace_sketch_insert(self._h, p.ptr, p.dtype, p.n, p.ld, p.where,
                                          C.byref(self.last_stats)))
@@ -326,6 +389,13 @@ class AceSketch:
     def score_batch(self, x, out=None, sums=None):
         """Scores S_i / L of every row (float64).  With `out`/`sums` CUDA
         tensors the results stay on the device."""
+        if self._noisy():
+            ids = np.ascontiguousarray(self._family.buckets(x))
+            res = np.empty(ids.shape[1], dtype=np.float64)
+            if ids.shape[1]:
+                _check(N.dev().ace_sketch_score_ids(self._h, ids.ctypes.data, ids.shape[1], N.ACE_HOST,
+                                                    res.ctypes.data, None, N.ACE_HOST))
+            return res
         p = _Points(x, self._dim())
         if out is not None or sums is not None:
             _check(N.dev().ace_sketch_score(
@@ -506,6 +576,8 @@ def _detect(sketch: AceSketch, data, build: bool, flags_out=None, scores_out=Non
     p = _Points(values, sketch._dim())
     if p.n == 0:
         raise ContractViolation("detect_batch: empty dataset")
+    if sketch._noisy():
+        return _detect_noisy(sketch, values, labels, build, want_scores)
     rep = N.AceBatchReport()
     st = N.AceHashStats()
     fn = N.dev().ace_sketch_build_detect if build else N.dev().ace_sketch_detect_batch
@@ -533,6 +605,37 @@ def _detect(sketch: AceSketch, data, build: bool, flags_out=None, scores_out=Non
         out.correctly_reported = int((flags & lab).sum())
         out.missed = int((~flags & lab).sum())
     sketch.last_stats = st
+    return out
+
+
+def _detect_noisy(sketch: AceSketch, values, labels, build: bool, want_scores: bool) -> DetectionReport:
+    """Noisy variant: device scores with fresh noise (ticks in row order, the
+    reference's threads=1 order), then the reference's own statistics
+    (detect.cpp:44-60: sequential binary64 sums, population sigma, s < thr)."""
+    import time
+    t0 = time.perf_counter()
+    if build:
+        sketch.insert(values)
+    sc = sketch.score_batch(values)
+    total = 0.0
+    for v in sc:
+        total += float(v)
+    mean = total / len(sc)
+    var = 0.0
+    for v in sc:
+        var += (float(v) - mean) * (float(v) - mean)
+    sd = math.sqrt(var / len(sc))
+    thr = mean - sd
+    flags = sc < thr
+    out = DetectionReport(reported=int(flags.sum()), threshold=thr, score_mean=mean, score_stddev=sd,
+                          elapsed_seconds=time.perf_counter() - t0, flags=flags,
+                          scores=sc if want_scores else None, stats=N.AceHashStats())
+    if labels is not None:
+        lab = np.asarray(labels) != 0
+        out.has_labels = True
+        out.total_labeled_anomalies = int(lab.sum())
+        out.correctly_reported = int((flags & lab).sum())
+        out.missed = int((~flags & lab).sum())
     return out
 
 

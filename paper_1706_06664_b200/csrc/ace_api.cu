@@ -9,6 +9,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -71,12 +72,20 @@ struct DevBuf {
 
 }  // namespace
 
+struct AceSketch;
+
 struct AceFamily {
   FamilyDev d{};
+  double noise_scale = 0.0;  // > 0: noisy variant, hashed only through the *_noisy / *_ids entry points
   TcFamily tc{};
   int kernel = 0;  // 0 auto, 1 SIMT, 2 tcgen05
   float margin_c = 0.f;
   std::atomic<int> refs{1};
+  // scratch state of the family-level hashing calls (ace_family_buckets*):
+  // stream, staging and id buffers reused across calls, no counters; it
+  // holds no reference on the family (family_release frees it)
+  std::mutex scratch_mu;
+  AceSketch* scratch = nullptr;
   bool use_tc() const { return tc.enabled && kernel != 1; }
 };
 
@@ -141,6 +150,13 @@ namespace {
 void family_release(AceFamily* f) {
   if (!f) return;
   if (f->refs.fetch_sub(1) == 1) {
+    if (f->scratch) {  // its destroy releases the family once more
+      AceSketch* s = f->scratch;
+      f->scratch = nullptr;
+      f->refs.store(1);
+      ace_sketch_destroy(s);
+      return;
+    }
     cudaFree(f->d.w64);
     cudaFree(f->d.w32t);
     cudaFree(f->d.wnorm);
@@ -150,7 +166,11 @@ void family_release(AceFamily* f) {
 }
 
 ace_status check_x(const AceFamily* f, const void* x, int dtype, uint64_t n, uint64_t ld,
-                   int where) {
+                   int where, bool noisy_ok = false) {
+  if (f->noise_scale > 0.0 && !noisy_ok)
+    return fail(ACE_E_UNSUPPORTED,
+                "ace: a noisy family hashes through ace_family_buckets_noisy (noise terms drawn in tick order on "
+                "the host) and the ids entry points");
   if (dtype != ACE_F32 && dtype != ACE_F64) return fail(ACE_E_CONTRACT, "ace: dtype must be ACE_F32 or ACE_F64");
   if (where != ACE_HOST && where != ACE_DEVICE) return fail(ACE_E_CONTRACT, "ace: bad memory location");
   if (n > 0 && !x) return fail(ACE_E_CONTRACT, "ace: null point matrix");
@@ -494,13 +514,11 @@ ace_status ace_family_create(uint64_t dim, uint32_t k_bits, uint32_t num_tables,
     return fail(ACE_E_CONTRACT, "SrpFamily: k_bits must be in [1, " + std::to_string(kMaxKBits) + "]");
   if (num_tables < 1) return fail(ACE_E_CONTRACT, "SrpFamily: num_tables must be >= 1");
   if (noise_scale < 0.0) return fail(ACE_E_CONTRACT, "SrpFamily: noise_scale must be >= 0");
-  if (noise_scale > 0.0)
-    return fail(ACE_E_UNSUPPORTED,
-                "SrpFamily: the noisy (private) hash variant has no device path");
   if (!w_host) return fail(ACE_E_CONTRACT, "ace_family_create: null W");
   if (!ace_device_available()) return fail(ACE_E_CUDA, "ace: no CUDA device available");
 
   AceFamily* f = new AceFamily();
+  f->noise_scale = noise_scale;
   FamilyDev& d = f->d;
   d.dim = dim;
   d.k_bits = k_bits;
@@ -568,15 +586,46 @@ ace_status ace_family_destroy(AceFamily* fam) {
   return ACE_OK;
 }
 
+ace_status sketch_create(AceFamily* fam, uint32_t counter_width, AceSketch** out, bool counters);
+
+// The family's scratch state for one hashing call: the shared one when free,
+// else (a concurrent caller holds it) a private one for this call.
+struct ScratchLease {
+  AceFamily* f = nullptr;
+  AceSketch* sk = nullptr;
+  bool shared = false;
+  ~ScratchLease() {
+    if (shared) f->scratch_mu.unlock();
+    else if (sk) ace_sketch_destroy(sk);
+  }
+};
+
+ace_status lease_scratch(AceFamily* f, ScratchLease& l) {
+  l.f = f;
+  if (f->scratch_mu.try_lock()) {
+    l.shared = true;
+    if (!f->scratch) {
+      ace_status r = sketch_create(f, 32, &f->scratch, false);
+      if (r != ACE_OK) return r;
+      f->refs.fetch_sub(1);  // held by the family itself
+    }
+    l.sk = f->scratch;
+    ACE_CUDA(zero_call_fields(l.sk));
+    return ACE_OK;
+  }
+  return sketch_create(f, 32, &l.sk, false);
+}
+
 // SrpFamily::bucket (srp.cpp:106-113) for every row and table.
 ace_status ace_family_buckets(AceFamily* fam, const void* x, int dtype, uint64_t n, uint64_t ld,
                               int x_where, uint32_t* ids, int ids_where, AceHashStats* stats) {
   if (!fam) return fail(ACE_E_CONTRACT, "ace_family_buckets: null family");
   ace_status r = check_x(fam, x, dtype, n, ld, x_where);
   if (r != ACE_OK) return r;
-  AceSketch* sk = nullptr;
-  r = ace_sketch_create(fam, 32, &sk);
+  ScratchLease lease;
+  r = lease_scratch(fam, lease);
   if (r != ACE_OK) return r;
+  AceSketch* sk = lease.sk;
   const void* xd;
   uint64_t ldd;
   r = stage_x(sk, sk->stage, sk->stream, x, dtype, n, ld, x_where, &xd, &ldd);
@@ -586,12 +635,55 @@ ace_status ace_family_buckets(AceFamily* fam, const void* x, int dtype, uint64_t
                  ids_where, sk->stream);
   if (r == ACE_OK) r = pull_state(sk);
   if (r == ACE_OK) fill_stats(stats, *sk->hst, n, fam);
-  ace_sketch_destroy(sk);
+  return r;
+}
+
+// Noisy hashing (SrpFamily::bit with noise_scale > 0, srp.cpp:93-104): the
+// host draws the noise terms in tick order, the device folds exactly.
+ace_status ace_family_buckets_noisy(AceFamily* fam, const void* x, int dtype, uint64_t n, uint64_t ld, int x_where,
+                                    uint32_t t0, uint32_t nt, uint32_t b0, uint32_t nb, const double* noise,
+                                    int noise_where, uint32_t* ids, int ids_where) {
+  if (!fam) return fail(ACE_E_CONTRACT, "ace_family_buckets_noisy: null family");
+  ace_status r = check_x(fam, x, dtype, n, ld, x_where, true);
+  if (r != ACE_OK) return r;
+  if (t0 + nt > fam->d.tables || b0 + nb > fam->d.k_bits || nb == 0)
+    return fail(ACE_E_CONTRACT, "ace_family_buckets_noisy: table or bit range out of range");
+  if (n == 0 || nt == 0) return ACE_OK;
+  if (!noise || !ids) return fail(ACE_E_CONTRACT, "ace_family_buckets_noisy: null noise or ids");
+  ScratchLease lease;
+  r = lease_scratch(fam, lease);
+  if (r != ACE_OK) return r;
+  AceSketch* sk = lease.sk;
+  const void* xd;
+  uint64_t ldd;
+  r = stage_x(sk, sk->stage, sk->stream, x, dtype, n, ld, x_where, &xd, &ldd);
+  const double* nd = noise;
+  const size_t nbytes = static_cast<size_t>(n) * nt * nb * sizeof(double);
+  if (r == ACE_OK && noise_where == ACE_HOST) {
+    cudaError_t e = sk->scores.ensure(nbytes);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(sk->scores.p, noise, nbytes, cudaMemcpyHostToDevice, sk->stream);
+    if (e != cudaSuccess) r = fail(ACE_E_CUDA, cudaGetErrorString(e));
+    nd = sk->scores.as<double>();
+  }
+  if (r == ACE_OK) {
+    cudaError_t e = sk->ids.ensure(static_cast<size_t>(n) * nt * sizeof(uint32_t));
+    if (e == cudaSuccess)
+      e = launch_noisy_buckets(xd, dtype == ACE_F64, n, ldd, fam->d.dim, fam->d.w64, fam->d.k_bits, t0, nt, b0, nb, nd,
+                               sk->ids.as<uint32_t>(), sk->stream);
+    if (e != cudaSuccess) r = fail(ACE_E_CUDA, cudaGetErrorString(e));
+  }
+  if (r == ACE_OK)
+    r = copy_out(ids, sk->ids.p, static_cast<size_t>(n) * nt * sizeof(uint32_t), ids_where, sk->stream);
+  if (r == ACE_OK && cudaStreamSynchronize(sk->stream) != cudaSuccess) r = fail(ACE_E_CUDA, "ace_family_buckets_noisy");
   return r;
 }
 
 // AceSketch::AceSketch (sketch.cpp:10-17): zeroed table-major counters.
 ace_status ace_sketch_create(AceFamily* fam, uint32_t counter_width, AceSketch** out) {
+  return sketch_create(fam, counter_width, out, true);
+}
+
+ace_status sketch_create(AceFamily* fam, uint32_t counter_width, AceSketch** out, bool counters) {
   if (!out || !fam) return fail(ACE_E_CONTRACT, "ace_sketch_create: null argument");
   *out = nullptr;
   if (counter_width != 16 && counter_width != 32)
@@ -601,10 +693,10 @@ ace_status ace_sketch_create(AceFamily* fam, uint32_t counter_width, AceSketch**
   fam->refs.fetch_add(1);
   sk->width = counter_width;
   sk->cap = counter_width == 16 ? 0xffffu : 0xffffffffu;
-  sk->num_counters = static_cast<uint64_t>(fam->d.tables) << fam->d.k_bits;
+  sk->num_counters = counters ? static_cast<uint64_t>(fam->d.tables) << fam->d.k_bits : 0;
   cudaError_t e;
   if ((e = cudaStreamCreateWithFlags(&sk->own, cudaStreamNonBlocking)) != cudaSuccess ||
-      (e = cudaMalloc(&sk->counters, sk->num_counters * sizeof(uint32_t))) != cudaSuccess ||
+      (counters && (e = cudaMalloc(&sk->counters, sk->num_counters * sizeof(uint32_t))) != cudaSuccess) ||
       (e = cudaMalloc(&sk->st, sizeof(DevState))) != cudaSuccess ||
       (e = cudaMallocHost(&sk->hst, sizeof(DevState))) != cudaSuccess) {
     ace_sketch_destroy(sk);
@@ -627,7 +719,7 @@ ace_status ace_sketch_create(AceFamily* fam, uint32_t counter_width, AceSketch**
 ace_status ace_sketch_reset(AceSketch* sk) {
   if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_reset: null sketch");
   sk->mean_pinned = false;
-  ACE_CUDA(cudaMemsetAsync(sk->counters, 0, sk->num_counters * sizeof(uint32_t), sk->stream));
+  if (sk->num_counters) ACE_CUDA(cudaMemsetAsync(sk->counters, 0, sk->num_counters * sizeof(uint32_t), sk->stream));
   ACE_CUDA(cudaMemsetAsync(sk->st, 0, sizeof(DevState), sk->stream));
   memset(sk->hst, 0, sizeof(DevState));
   return ACE_OK;
@@ -696,6 +788,77 @@ ace_status ace_sketch_insert(AceSketch* sk, const void* x, int dtype, uint64_t n
   if (r == ACE_OK) r = pull_state(sk);
   if (r == ACE_OK) fill_stats(stats, *sk->hst, n, sk->fam);
   return r;
+}
+
+namespace {
+ace_status stage_ids(AceSketch* sk, const uint32_t* ids, uint64_t n, int where, const uint32_t** out) {
+  const AceFamily* f = sk->fam;
+  if (where != ACE_HOST && where != ACE_DEVICE) return fail(ACE_E_CONTRACT, "ace: bad memory location");
+  if (n > 0 && !ids) return fail(ACE_E_CONTRACT, "ace: null ids");
+  const uint64_t total = n * f->d.tables;
+  if (where == ACE_HOST) {
+    const uint32_t lim = f->d.k_bits >= 32 ? 0xffffffffu : (1u << f->d.k_bits) - 1u;
+    for (uint64_t i = 0; i < total; ++i)
+      if (ids[i] > lim) return fail(ACE_E_CONTRACT, "ace: bucket id out of range [0, 2^K)");
+    ACE_CUDA(sk->ids.ensure(total * sizeof(uint32_t)));
+    ACE_CUDA(cudaMemcpyAsync(sk->ids.p, ids, total * sizeof(uint32_t), cudaMemcpyHostToDevice, sk->stream));
+    *out = sk->ids.as<uint32_t>();
+  } else {
+    *out = ids;  // device ids are taken as valid
+  }
+  return ACE_OK;
+}
+}  // namespace
+
+// Insert n points given by their bucket ids (L x n, table-major; e.g. from
+// ace_family_buckets_noisy): AceSketch::insert's counter and mean update
+// (sketch.cpp:55-71) without hashing.
+ace_status ace_sketch_insert_ids(AceSketch* sk, const uint32_t* ids, uint64_t n, int where) {
+  if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_insert_ids: null sketch");
+  if (n == 0) return ACE_OK;
+  const uint32_t* d = nullptr;
+  ace_status r = stage_ids(sk, ids, n, where, &d);
+  if (r != ACE_OK) return r;
+  sk->mean_pinned = false;
+  ACE_CUDA(zero_call_fields(sk));
+  ACE_CUDA(launch_apply_ids(d, n, sk->fam->d.tables, sk->fam->d.k_bits, sk->counters, sk->cap, +1, sk->st,
+                            sk->stream, !fire_and_forget_ok(sk, n)));
+  if (sk->width == 16) ACE_CUDA(launch_cap(sk->counters, sk->num_counters, sk->cap, sk->st, sk->stream));
+  return pull_state(sk);
+}
+
+// Scores of n points given by their bucket ids (AceSketch::score's gather,
+// sketch.cpp:108-116).
+ace_status ace_sketch_score_ids(AceSketch* sk, const uint32_t* ids, uint64_t n, int where, double* scores,
+                                uint64_t* sums, int out_where) {
+  if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_score_ids: null sketch");
+  if (n == 0) return ACE_OK;
+  const uint32_t* d = nullptr;
+  ace_status r = stage_ids(sk, ids, n, where, &d);
+  if (r != ACE_OK) return r;
+  ACE_CUDA(zero_call_fields(sk));
+  double* dsc = nullptr;
+  uint64_t* dsum = nullptr;
+  if (scores) {
+    if (out_where == ACE_DEVICE) dsc = scores;
+    else {
+      ACE_CUDA(sk->scores.ensure(n * sizeof(double)));
+      dsc = sk->scores.as<double>();
+    }
+  }
+  if (sums) {
+    if (out_where == ACE_DEVICE) dsum = sums;
+    else {
+      ACE_CUDA(sk->sums.ensure(n * sizeof(uint64_t)));
+      dsum = sk->sums.as<uint64_t>();
+    }
+  }
+  ACE_CUDA(launch_score(d, n, n, sk->fam->d.tables, sk->fam->d.k_bits, sk->counters, dsum, dsc, sk->st, sk->stream));
+  if (out_where == ACE_HOST) {
+    if (scores && (r = copy_out(scores, dsc, n * sizeof(double), ACE_HOST, sk->stream)) != ACE_OK) return r;
+    if (sums && (r = copy_out(sums, dsum, n * sizeof(uint64_t), ACE_HOST, sk->stream)) != ACE_OK) return r;
+  }
+  return pull_state(sk);
 }
 
 // AceSketch::remove (sketch.cpp:74-106), all-or-nothing over the batch.

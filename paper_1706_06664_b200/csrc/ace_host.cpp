@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <iterator>
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <numbers>
@@ -99,6 +100,25 @@ SrpFamily::SrpFamily(const SrpConfig& cfg) : cfg_(cfg) {
   if (cfg_.noise_scale < 0.0) throw ContractViolation("SrpFamily: noise_scale must be >= 0");
   w_ = std::make_shared<const std::vector<double>>(generate_w(cfg_));
   dev_ = std::make_shared<std::shared_ptr<::AceFamily>>();
+  noise_seed_ = rng::mix_seed(cfg_.seed, 0x6e6f697365ULL);  // srp.cpp:34, the aux stream
+}
+
+std::vector<double> SrpFamily::draw_noise(std::size_t count) const {
+  const std::uint64_t tick0 = noise_ctr_.v.fetch_add(count, std::memory_order_relaxed);
+  std::vector<double> out(count);
+  if (count) ace_noise_terms(noise_seed_, tick0, count, cfg_.noise_scale, out.data());
+  return out;
+}
+
+std::vector<std::uint32_t> SrpFamily::noisy_ids(const void* x, int dtype, std::size_t n, std::size_t t0,
+                                                std::size_t nt, std::size_t b0, std::size_t nb) const {
+  const auto noise = draw_noise(n * nt * nb);
+  std::vector<std::uint32_t> ids(n * nt);
+  if (n && nt)
+    ok(ace_family_buckets_noisy(device(), x, dtype, n, cfg_.dim, ACE_HOST, static_cast<std::uint32_t>(t0),
+                                static_cast<std::uint32_t>(nt), static_cast<std::uint32_t>(b0),
+                                static_cast<std::uint32_t>(nb), noise.data(), ACE_HOST, ids.data(), ACE_HOST));
+  return ids;
 }
 
 ::AceFamily* SrpFamily::device() const {
@@ -121,6 +141,7 @@ void SrpFamily::check(std::size_t table, std::size_t b, std::span<const double> 
 
 std::uint32_t SrpFamily::bucket(std::size_t table, std::span<const double> x) const {
   check(table, 0, x);
+  if (cfg_.noise_scale > 0.0) return noisy_ids(x.data(), ACE_F64, 1, table, 1, 0, cfg_.k_bits)[0];
   std::vector<std::uint32_t> ids(cfg_.num_tables);
   ok(ace_family_buckets(device(), x.data(), ACE_F64, 1, cfg_.dim, ACE_HOST, ids.data(), ACE_HOST,
                         nullptr));
@@ -129,11 +150,13 @@ std::uint32_t SrpFamily::bucket(std::size_t table, std::span<const double> x) co
 
 std::uint32_t SrpFamily::bit(std::size_t table, std::size_t b, std::span<const double> x) const {
   check(table, b, x);
+  if (cfg_.noise_scale > 0.0) return noisy_ids(x.data(), ACE_F64, 1, table, 1, b, 1)[0];  // one tick
   return (bucket(table, x) >> (cfg_.k_bits - 1 - b)) & 1u;
 }
 
 std::vector<std::uint32_t> SrpFamily::buckets(std::span<const float> rows, std::size_t n) const {
   if (rows.size() != n * cfg_.dim) throw ContractViolation("SrpFamily::buckets: rows size != n * dim");
+  if (cfg_.noise_scale > 0.0) return noisy_ids(rows.data(), ACE_F32, n, 0, cfg_.num_tables, 0, cfg_.k_bits);
   std::vector<std::uint32_t> ids(n * cfg_.num_tables);
   if (n)
     ok(ace_family_buckets(device(), rows.data(), ACE_F32, n, cfg_.dim, ACE_HOST, ids.data(),
@@ -148,9 +171,10 @@ std::vector<double> SrpFamily::direction(std::size_t table, std::size_t b) const
   return std::vector<double>(row, row + cfg_.dim);
 }
 
-void SrpFamily::reset_noise_stream(std::uint64_t) const {
-  if (cfg_.noise_scale > 0.0)
-    throw UnsupportedOperation("SrpFamily: the noisy hash variant has no device path");
+void SrpFamily::reset_noise_stream(std::uint64_t aux_seed) const {
+  // srp.cpp:126-129
+  noise_seed_ = aux_seed;
+  noise_ctr_.v.store(0, std::memory_order_relaxed);
 }
 
 // collision_probability (srp.cpp:130-146): closed-form statistic, not on the
@@ -217,6 +241,12 @@ void AceSketch::check_dim(std::span<const double> x) const {
 
 void AceSketch::insert(std::span<const double> x) {
   check_dim(x);
+  if (family_.config().noise_scale > 0.0) {
+    const auto ids = family_.noisy_ids(x.data(), ACE_F64, 1, 0, family_.config().num_tables, 0,
+                                       family_.config().k_bits);
+    ok(ace_sketch_insert_ids(dev_, ids.data(), 1, ACE_HOST));
+    return;
+  }
   ok(ace_sketch_insert(dev_, x.data(), ACE_F64, 1, x.size(), ACE_HOST, nullptr));
 }
 
@@ -231,6 +261,12 @@ void AceSketch::remove(std::span<const double> x) {
 ScoreEstimate AceSketch::score(std::span<const double> q) const {
   check_dim(q);
   double v = 0.0;
+  if (family_.config().noise_scale > 0.0) {
+    const auto ids = family_.noisy_ids(q.data(), ACE_F64, 1, 0, family_.config().num_tables, 0,
+                                       family_.config().k_bits);
+    ok(ace_sketch_score_ids(dev_, ids.data(), 1, ACE_HOST, &v, nullptr, ACE_HOST));
+    return {v, family_.config().k_bits, family_.config().num_tables};
+  }
   ok(ace_sketch_score(dev_, q.data(), ACE_F64, 1, q.size(), ACE_HOST, &v, nullptr, ACE_HOST,
                       nullptr));
   return {v, family_.config().k_bits, family_.config().num_tables};
@@ -239,6 +275,11 @@ ScoreEstimate AceSketch::score(std::span<const double> q) const {
 void AceSketch::insert_batch(std::span<const float> rows, std::size_t n) {
   const auto d = family_.config().dim;
   if (rows.size() != n * d) throw ContractViolation("AceSketch::insert_batch: rows size != n * dim");
+  if (n && family_.config().noise_scale > 0.0) {
+    const auto ids = family_.buckets(rows, n);  // noisy: ticks in row order
+    ok(ace_sketch_insert_ids(dev_, ids.data(), n, ACE_HOST));
+    return;
+  }
   if (n) ok(ace_sketch_insert(dev_, rows.data(), ACE_F32, n, d, ACE_HOST, nullptr));
 }
 
@@ -246,6 +287,11 @@ std::vector<double> AceSketch::score_batch(std::span<const float> rows, std::siz
   const auto d = family_.config().dim;
   if (rows.size() != n * d) throw ContractViolation("AceSketch::score_batch: rows size != n * dim");
   std::vector<double> out(n);
+  if (n && family_.config().noise_scale > 0.0) {
+    const auto ids = family_.buckets(rows, n);
+    ok(ace_sketch_score_ids(dev_, ids.data(), n, ACE_HOST, out.data(), nullptr, ACE_HOST));
+    return out;
+  }
   if (n)
     ok(ace_sketch_score(dev_, rows.data(), ACE_F32, n, d, ACE_HOST, out.data(), nullptr, ACE_HOST,
                         nullptr));
@@ -302,8 +348,35 @@ DetectionReport detect_batch(const AceSketch& sketch, const Dataset& data, unsig
     throw ContractViolation("detect_batch: data dimension mismatch");
   std::vector<std::uint32_t> bits((data.rows + 31) / 32);
   AceBatchReport r{};
-  ok(ace_sketch_detect_batch(sketch.device(), data.values.data(), ACE_F64, data.rows, data.cols,
-                             ACE_HOST, bits.data(), nullptr, ACE_HOST, &r, nullptr));
+  if (sketch.family().config().noise_scale > 0.0) {
+    // noisy variant: scores with fresh noise (ticks in row order: the
+    // reference's threads=1 order), then the reference's own statistics
+    // (detect.cpp:44-60, sequential binary64 sums over the N scores)
+    const auto t0 = std::chrono::steady_clock::now();
+    const auto ids = sketch.family().noisy_ids(data.values.data(), ACE_F64, data.rows, 0,
+                                               sketch.family().config().num_tables, 0,
+                                               sketch.family().config().k_bits);
+    std::vector<double> sc(data.rows);
+    ok(ace_sketch_score_ids(sketch.device(), ids.data(), data.rows, ACE_HOST, sc.data(), nullptr, ACE_HOST));
+    double sum = 0.0;
+    for (double v : sc) sum += v;
+    const double mean = sum / static_cast<double>(data.rows);
+    double var = 0.0;
+    for (double v : sc) var += (v - mean) * (v - mean);
+    const double sd = std::sqrt(var / static_cast<double>(data.rows));
+    r.score_mean = mean;
+    r.score_stddev = sd;
+    r.threshold = mean - sd;
+    for (std::size_t i = 0; i < data.rows; ++i)
+      if (sc[i] < r.threshold) {
+        bits[i >> 5] |= 1u << (i & 31);
+        ++r.reported;
+      }
+    r.elapsed_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  } else {
+    ok(ace_sketch_detect_batch(sketch.device(), data.values.data(), ACE_F64, data.rows, data.cols,
+                               ACE_HOST, bits.data(), nullptr, ACE_HOST, &r, nullptr));
+  }
   DetectionReport rep;
   rep.reported = r.reported;
   rep.threshold = r.threshold;
@@ -355,6 +428,11 @@ AceSketch build_sketch(const Dataset& data, std::uint32_t k_bits, std::uint32_t 
   cfg.seed = seed;
   cfg.noise_scale = noise_scale;
   AceSketch sketch{SrpFamily(cfg), width};
+  if (noise_scale > 0.0) {  // rows in index order, ticks in row / table / bit order
+    const auto ids = sketch.family().noisy_ids(data.values.data(), ACE_F64, data.rows, 0, num_tables, 0, k_bits);
+    ok(ace_sketch_insert_ids(sketch.device(), ids.data(), data.rows, ACE_HOST));
+    return sketch;
+  }
   ok(ace_sketch_insert(sketch.device(), data.values.data(), ACE_F64, data.rows, data.cols, ACE_HOST,
                        nullptr));
   return sketch;
@@ -593,6 +671,26 @@ extern "C" int ace_load_dataset_csv(const char* path, int has_label, int label_c
     g_host_err = e.what();
     return ACE_E_CONTRACT;
   }
+}
+
+// Noise terms of the noisy variant, ticks tick0 .. tick0+count-1 (srp.cpp:97-101):
+// noise_scale * NormalStream(mix_seed(noise_seed, tick)).next(), glibc libm,
+// computed on all host threads (each term is independent of the others).
+extern "C" int ace_noise_terms(uint64_t noise_seed, uint64_t tick0, uint64_t count, double noise_scale,
+                               double* out) {
+  if (count && !out) return ACE_E_CONTRACT;
+  const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(),
+                                                      static_cast<unsigned>(count / 65536 + 1)));
+  std::vector<std::thread> pool;
+  for (unsigned w = 0; w < nt; ++w)
+    pool.emplace_back([=] {
+      for (uint64_t i = w; i < count; i += nt) {
+        ace::rng::NormalStream g(ace::rng::mix_seed(noise_seed, tick0 + i));
+        out[i] = noise_scale * g.next();
+      }
+    });
+  for (auto& t : pool) t.join();
+  return 0;
 }
 
 // W generation for non-C++ hosts (the Python mirror): the same generator as

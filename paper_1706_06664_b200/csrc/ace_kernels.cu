@@ -630,6 +630,38 @@ __global__ void __launch_bounds__(1024) apply_gather_kernel(const uint32_t* ids,
   }
 }
 
+// Noisy (private) hashing, srp.cpp:93-104: for point i, table t0+tt, bit b
+// in [b0, b0+nb): value = RN(p + noise) with p the reference's binary64 left
+// fold (srp.cpp:78-91) and noise the pre-scaled term cfg.noise_scale * N(0,1)
+// drawn on the host in tick order, noise[(i*nt + tt)*nb + (b-b0)]; bit =
+// value >= 0, packed MSB-first into ids[tt*n + i].  Exact by construction
+// (no fast path: the noise changes every call, so nothing is reused).
+__global__ void noisy_buckets_kernel(const void* __restrict__ x, int x_f64, uint64_t n, uint64_t ld, uint64_t dim,
+                                     const double* __restrict__ w64, uint32_t k_bits, uint32_t t0, uint32_t nt,
+                                     uint32_t b0, uint32_t nb, const double* __restrict__ noise,
+                                     uint32_t* __restrict__ ids) {
+  for (uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < n * nt;
+       idx += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t i = idx / nt;
+    const uint32_t tt = static_cast<uint32_t>(idx % nt);
+    uint32_t bucket = 0;
+    for (uint32_t b = b0; b < b0 + nb; ++b) {
+      const double* w = w64 + (static_cast<uint64_t>(t0 + tt) * k_bits + b) * dim;
+      double acc = 0.0;
+      if (x_f64) {
+        const double* xr = static_cast<const double*>(x) + i * ld;
+        for (uint64_t k = 0; k < dim; ++k) acc = __dadd_rn(acc, __dmul_rn(w[k], xr[k]));
+      } else {
+        const float* xr = static_cast<const float*>(x) + i * ld;
+        for (uint64_t k = 0; k < dim; ++k) acc = __dadd_rn(acc, __dmul_rn(w[k], static_cast<double>(xr[k])));
+      }
+      const double v = __dadd_rn(acc, noise[(i * nt + tt) * nb + (b - b0)]);
+      bucket = (bucket << 1) | (v >= 0.0 ? 1u : 0u);
+    }
+    ids[static_cast<uint64_t>(tt) * n + i] = bucket;
+  }
+}
+
 __global__ void remove_demand_kernel(const uint32_t* __restrict__ ids, uint64_t n, uint32_t tables,
                                      uint32_t k_bits, uint32_t* demand) {
   const uint64_t total = n * tables;
@@ -1134,6 +1166,16 @@ cudaError_t launch_apply_gather(uint32_t* ids, uint32_t* gout, uint64_t n, uint3
                                   smem, s);
   count_launch();
   return e;
+}
+
+cudaError_t launch_noisy_buckets(const void* x, int x_f64, uint64_t n, uint64_t ld, uint64_t dim, const double* w64,
+                                 uint32_t k_bits, uint32_t t0, uint32_t nt, uint32_t b0, uint32_t nb,
+                                 const double* noise, uint32_t* ids, cudaStream_t s) {
+  if (n == 0 || nt == 0) return cudaSuccess;
+  noisy_buckets_kernel<<<grid_for(n * nt, 128), 128, 0, s>>>(x, x_f64, n, ld, dim, w64, k_bits, t0, nt, b0, nb, noise,
+                                                             ids);
+  count_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t launch_remove_check(const uint32_t* ids, uint64_t n, uint32_t tables, uint32_t k_bits,

@@ -37,6 +37,11 @@ cudaError_t launch_apply_ids(const uint32_t* ids, uint64_t n, uint32_t tables,
 // count in `gout` (== ids when K <= 15); score with counters == nullptr.
 cudaError_t launch_apply_gather(uint32_t* ids, uint32_t* gout, uint64_t n, uint32_t tables, uint32_t k_bits,
                                 uint32_t* counters, DevState* st, cudaStream_t s);
+// Noisy hashing (srp.cpp:93-104), exact: tables [t0, t0+nt), bits [b0, b0+nb)
+// of each; noise[(i*nt + tt)*nb + (b-b0)] pre-scaled terms in tick order.
+cudaError_t launch_noisy_buckets(const void* x, int x_f64, uint64_t n, uint64_t ld, uint64_t dim, const double* w64,
+                                 uint32_t k_bits, uint32_t t0, uint32_t nt, uint32_t b0, uint32_t nb,
+                                 const double* noise, uint32_t* ids, cudaStream_t s);
 // Remove validation: counts, per counter, how many removals target it and
 // flags underflow (any count < demand).  scratch: L x 2^K u32, zeroed here.
 cudaError_t launch_remove_check(const uint32_t* ids, uint64_t n, uint32_t tables,

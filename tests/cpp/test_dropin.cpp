@@ -239,13 +239,38 @@ int main() {
     b.insert(normals(3, 2));
     check(a.size() == 1 && b.size() == 2, "AceSketch copy is deep");
   }
-  // noisy variant: no device path
+  // test_srp.cpp:169-194 / test_sketch.cpp:118-126: the noisy variant
   {
-    auto c = cfg(4, 3, 2, 1);
-    c.noise_scale = 1.0;
+    auto c = cfg(6, 4, 2, 1);
+    c.noise_scale = 1.5;
     const ace::SrpFamily f{c};
-    expect_throw<ace::UnsupportedOperation>([&] { f.bucket(0, normals(4, 1)); },
-                                            "noisy hashing reports UnsupportedOperation");
+    const auto x = normals(6, 3);
+    f.reset_noise_stream(99);
+    const auto first = f.bucket(0, x);
+    f.reset_noise_stream(99);
+    check(f.bucket(0, x) == first, "noisy bucket reproducible after reset_noise_stream");
+    const std::size_t m = 4000;
+    const auto y = normals(10, 9);
+    double previous = 1.0;
+    bool below = true, falling = true;
+    for (const double noise : {0.5, 2.0, 8.0}) {
+      auto cn = cfg(10, 1, m, 77);
+      cn.noise_scale = noise;
+      const ace::SrpFamily g{cn};
+      g.reset_noise_stream(4242);
+      std::size_t hits = 0;
+      for (std::size_t j = 0; j < m; ++j) hits += g.bit(j, 0, y) == g.bit(j, 0, y);
+      const double rate = static_cast<double>(hits) / m;
+      below = below && rate < 1.0;
+      falling = falling && rate < previous;
+      previous = rate;
+    }
+    check(below && falling, "noisy self-collision rate < 1 and decreasing in noise");
+    ace::AceSketch s{f};
+    s.insert(std::vector<double>{1, 2, 3, 4, 5, 6});
+    check(s.size() == 1, "noisy insert counts the point");
+    expect_throw<ace::UnsupportedOperation>([&] { s.remove(std::vector<double>{1, 2, 3, 4, 5, 6}); },
+                                            "noisy remove reports UnsupportedOperation");
   }
   // test_io.cpp: ACE1 save/load round-trips state and scores bit-exactly
   {
