@@ -99,7 +99,7 @@ struct AceSketch {
   DevState* hst = nullptr;   // pinned host mirror
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
-  DevBuf ids, sums, stage, flags, scores, demand, near, overflow, x16, rowthr, segc, gbuf;
+  DevBuf ids, sums, stage, flags, scores, demand, near, overflow, x16, rowthr, segc, gbuf, lomask;
   // build + detect over the same rows: run_hash leaves the insert to the
   // fused count-and-gather pass of the detect tail (apply_gather_kernel)
   bool defer_insert = false, insert_deferred = false;
@@ -126,9 +126,9 @@ struct AceSketch {
     uint64_t n = 0, ld = 0;
     int dtype = 0, where = 0, out_where = 0, build = 0, ff = 0;
     cudaStream_t stream = nullptr;
-    const void* bufs[12] = {};  // the sketch's scratch buffers (a reallocation invalidates the graph)
+    const void* bufs[13] = {};  // the sketch's scratch buffers (a reallocation invalidates the graph)
     bool operator==(const GraphKey& o) const {
-      for (int i = 0; i < 12; ++i)
+      for (int i = 0; i < 13; ++i)
         if (bufs[i] != o.bufs[i]) return false;
       return x == o.x && flags == o.flags && scores == o.scores && n == o.n && ld == o.ld && dtype == o.dtype &&
              where == o.where && out_where == o.out_where && build == o.build && ff == o.ff && stream == o.stream;
@@ -359,7 +359,20 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
       return ACE_OK;
     }
     sk->mark(4);
-    if (!t.fuse_convert) ACE_CUDA(launch_convert_x(t, sk->stream));
+    if (!t.fuse_convert) {
+      // per point tile: K16 steps whose x lo parts are not all zero
+      static int lomask_env = -2;
+      if (lomask_env == -2) {
+        const char* e = getenv("ACE_LO_SKIP");
+        lomask_env = e ? atoi(e) : 1;
+      }
+      if (lomask_env) {
+        ACE_CUDA(sk->lomask.ensure(tiles * sizeof(uint32_t)));
+        ACE_CUDA(cudaMemsetAsync(sk->lomask.p, 0, tiles * sizeof(uint32_t), sk->stream));
+        t.lomask = sk->lomask.as<uint32_t>();
+      }
+      ACE_CUDA(launch_convert_x(t, sk->stream));
+    }
     sk->mark(6);
     // Fused epilogue insert (global REDs) only where the separate insert would
     // use global atomics too (K > 20); otherwise the shared-memory histogram
@@ -755,6 +768,7 @@ ace_status ace_sketch_destroy(AceSketch* sk) {
   sk->rowthr.release();
   sk->segc.release();
   sk->gbuf.release();
+  sk->lomask.release();
   if (sk->counters) cudaFree(sk->counters);
   if (sk->st) cudaFree(sk->st);
   if (sk->hst) cudaFreeHost(sk->hst);
@@ -977,9 +991,9 @@ ace_status batch_detect(AceSketch* sk, const void* x, int dtype, uint64_t n, uin
   key.build = build;
   key.ff = build ? (fire_and_forget_ok(sk, n) ? 1 : 0) : 2;
   key.stream = sk->stream;
-  const DevBuf* bufs[12] = {&sk->ids, &sk->sums, &sk->stage, &sk->flags, &sk->scores, &sk->demand,
-                            &sk->near, &sk->overflow, &sk->x16, &sk->rowthr, &sk->segc, &sk->gbuf};
-  for (int i = 0; i < 12; ++i) key.bufs[i] = bufs[i]->p;
+  const DevBuf* bufs[13] = {&sk->ids, &sk->sums, &sk->stage, &sk->flags, &sk->scores, &sk->demand, &sk->near,
+                            &sk->overflow, &sk->x16, &sk->rowthr, &sk->segc, &sk->gbuf, &sk->lomask};
+  for (int i = 0; i < 13; ++i) key.bufs[i] = bufs[i]->p;
   static int graphs_env = -2;
   if (graphs_env == -2) {
     const char* e = getenv("ACE_GRAPHS");

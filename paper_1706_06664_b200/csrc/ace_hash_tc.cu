@@ -45,6 +45,12 @@ constexpr int kMaxWStages = 12;
 #ifndef ACE_SLEEPY
 #define ACE_SLEEPY 64  // ns back-off of off-critical-path barrier waits (0: spin)
 #endif
+#ifndef ACE_SPLIT
+// epilogue: 1 = both warps of a lane quarter on every direction tile (halves
+// of its columns; measured slower: the halves' TMEM loads and barriers cost
+// more than the earlier accumulator release gains), 0 = alternate tiles
+#define ACE_SPLIT 0
+#endif
 #ifndef ACE_TILE_BURST
 #define ACE_TILE_BURST 0  // MMA issuer: 1 = one elected burst per point tile (measured slower), 0 = per direction tile
 #endif
@@ -393,10 +399,14 @@ __device__ __forceinline__ float load_x(const TcArgs& a, uint64_t row, uint64_t 
 // the row's 128-row tile (`tile`: [kc][hi | lo][16 KB]), and the row's error
 // threshold thr = c * ||x~|| * 2^14 + abs (-1: exact zero row or padding,
 // +inf: recheck every projection).
+// Returns this lane's lo-step bits: bit s set iff a lo part it wrote in K16
+// step s is nonzero (an x exactly representable in fp16 after scaling, e.g.
+// one-hot columns, has a zero lo part and its lo x hi MMAs can be skipped).
 template <uint32_t kG>
-__device__ __forceinline__ void convert_row(float (&v)[kG][4], uint32_t l8, bool live, uint32_t groups, uint32_t nkc,
-                                            uint64_t dim, float margin_c, uint8_t* tile, uint32_t r, float* thr_dst) {
-  uint32_t mb = 0u;
+__device__ __forceinline__ uint32_t convert_row(float (&v)[kG][4], uint32_t l8, bool live, uint32_t groups,
+                                                uint32_t nkc, uint64_t dim, float margin_c, uint8_t* tile, uint32_t r,
+                                                float* thr_dst) {
+  uint32_t mb = 0u, lobits = 0u;
 #pragma unroll
   for (uint32_t g = 0; g < kG; ++g)
 #pragma unroll
@@ -428,6 +438,7 @@ __device__ __forceinline__ void convert_row(float (&v)[kG][4], uint32_t l8, bool
       hi[i] = pack_h2(h0, h1);
       lo[i] = pack_h2(x0 - h0, x1 - h1);
     }
+    if ((lo[0] | lo[1]) != 0u) lobits |= 1u << (k0 >> 4);
     uint8_t* blk = tile + kc * 2u * kBlockBytes;
     const uint32_t off = sw128_off(r, kk);
     *reinterpret_cast<uint2*>(blk + off) = make_uint2(hi[0], hi[1]);
@@ -448,6 +459,7 @@ __device__ __forceinline__ void convert_row(float (&v)[kG][4], uint32_t l8, bool
     }
     *thr_dst = thr;
   }
+  return lobits;
 }
 
 // Pre-pass: eight lanes per row (four rows per warp, values in registers),
@@ -484,9 +496,16 @@ __global__ void __launch_bounds__(256) convert_x_kernel(const TcArgs a, uint64_t
     }
     if (!inb) continue;  // (row-uniform per 8-lane group; shuffles stay within the group)
     const uint64_t tile = row / kRows;
-    convert_row<kG>(v, l8, live, groups, a.nkc, a.dim, a.margin_c,
-                    reinterpret_cast<uint8_t*>(a.x16) + tile * a.nkc * 2u * kBlockBytes, static_cast<uint32_t>(row % kRows),
-                &a.rowthr[row]);
+    uint32_t lob = convert_row<kG>(v, l8, live, groups, a.nkc, a.dim, a.margin_c,
+                                   reinterpret_cast<uint8_t*>(a.x16) + tile * a.nkc * 2u * kBlockBytes,
+                                   static_cast<uint32_t>(row % kRows), &a.rowthr[row]);
+    // the 4 rows of a warp lie in one point tile (kRows % 4 == 0)
+    lob |= __shfl_xor_sync(0xffffffffu, lob, 1);
+    lob |= __shfl_xor_sync(0xffffffffu, lob, 2);
+    lob |= __shfl_xor_sync(0xffffffffu, lob, 4);
+    lob |= __shfl_xor_sync(0xffffffffu, lob, 8);
+    lob |= __shfl_xor_sync(0xffffffffu, lob, 16);
+    if (a.lomask && lane == 0 && lob) atomicOr(&a.lomask[tile], lob);
   }
 }
 
@@ -641,6 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
   __shared__ __align__(8) uint64_t bar_accfull[kAccBufs], bar_accempty[kAccBufs];
   __shared__ uint32_t tmem_base_sh;
   __shared__ uint32_t lastw[4][2][32];  // epilogue: last sign word of a direction tile, per quarter / parity
+  __shared__ uint32_t xw[4][2][2][32];  // split epilogue: last word of each half, per quarter / half / parity
   __shared__ uint32_t seg_n;                        // near ties pushed by this CTA
   __shared__ uint32_t tiles_done;                   // epilogue warps x tiles completed (ids stored)
   __shared__ uint32_t min_next;                     // first list slot the recheck warps left over
@@ -684,7 +704,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
     mbar_init(&bar_rawempty, 2);
     for (int b = 0; b < kAccBufs; ++b) {
       mbar_init(&bar_accfull[b], 1);
-      mbar_init(&bar_accempty[b], 4 * kPair);  // one epilogue warp per lane quarter, per CTA
+      mbar_init(&bar_accempty[b], (ACE_SPLIT ? 8 : 4) * kPair);  // epilogue warps per tile, per CTA
     }
     fence_mbar_init();
   }
@@ -756,12 +776,16 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
           const uint32_t hblk = kPair == 2 ? half : wblk;  // stage layout: hi block, then lo block
           for (uint32_t kc = 0; kc < a.nkc; ++kc) {
             mbar_wait_sleepy(&bar_wempty[s], ph ^ 1u, prof ? &pw[1] : nullptr);
+            if ((a.dbg & 256) && it > 0) {  // experiment: W stages loaded for the first point tile only
+              mbar_arrive(&bar_wfull[s]);
+            } else {
             mbar_expect_tx(&bar_wfull[s], 2u * bytes);
             const uint8_t* src = reinterpret_cast<const uint8_t*>(a.w16) +
                                  (static_cast<uint64_t>(j) * a.nkc + kc) * 2u * wblk + rank * share;
             uint8_t* dst = Wsm + static_cast<size_t>(s) * 2u * hblk;
             bulk_g2s(dst, src, bytes, &bar_wfull[s]);
             bulk_g2s(dst + hblk, src + wblk, bytes, &bar_wfull[s]);
+            }
             if (++s == L.n_wst) {
               s = 0;
               ph ^= 1u;
@@ -799,13 +823,18 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
     {
       uint32_t s = 0, wph = 0, acc = 0, accph = 0;
       unsigned long long pmi = 0, pmn = 0, pcp = 0;  // instrumentation: MMA-group issue cycles / groups, A copies
-      unsigned long long pfence = 0;
+      unsigned long long pfence = 0, pwf = 0, pcm = 0;  // instrumentation: W-full waits, commits (issuing lane)
       const long long ploop = clock64();
       const uint32_t nacc = tc_acc_bufs(a.nkc, TW);
       const uint32_t ta_hi = tmem_base + nacc * TW, ta_lo = ta_hi + a.nkc * 32u;  // dpad/2 columns each
       const uint32_t a_base = smem_u32(Asm), w_base = smem_u32(Wsm);
       const uint32_t half = kPair == 2 ? kBlockBytes / kPair : wblk;  // bytes of one W block (hi or lo) per CTA
+      // K16 steps past dim hold zero padding: none of their MMAs run
+      const uint32_t nsteps = static_cast<uint32_t>((a.dim + 15u) / 16u);
       for (uint64_t it = 0; it < iters; ++it) {
+        // lo x hi MMAs of the steps whose x lo parts are all zero in this tile
+        // are skipped (the pre-pass sets the bits; they add exact zeros)
+        const uint32_t lm = (kPair == 1 && a.lomask && !kFuse) ? __ldcg(a.lomask + min(tile_of(it), n_tiles - 1)) : 0xffffffffu;
         mbar_wait_t(&bar_afull[0], static_cast<uint32_t>(it) & 1u, (prof && lane == 0) ? &pw[2] : nullptr);
         pipe_after();
         const long long pc0 = prof ? clock64() : 0;
@@ -893,26 +922,34 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
           if (elect_one()) {
             uint32_t ss = s, ph = wph;
             for (uint32_t kc = 0; kc < a.nkc; ++kc) {
+              const long long pq0 = prof ? clock64() : 0;
               mbar_wait(&bar_wfull[ss], ph);
+              if (prof) pwf += static_cast<unsigned long long>(clock64() - pq0);
               const uint32_t b_hi = w_base + ss * 2u * half;
               const uint64_t dbh = sw128_desc(b_hi), dbl = sw128_desc(b_hi + half);
               if (!(a.dbg & 2)) {
 #pragma unroll
                 for (uint32_t kk = 0; kk < 4; ++kk) {
-                  const uint32_t acol = (kc * 4u + kk) * 8u;  // 16 fp16 = 8 TMEM columns
-                  const uint64_t off = kk * 2u;                // 32 B along K in SW128, >> 4
-                  mma_f16_ts(dt, ta_hi + acol, dbh + off, idesc, (kc | kk) != 0u);
-                  mma_f16_ts(dt, ta_lo + acol, dbh + off, idesc, 1u);
+                  const uint32_t step = kc * 4u + kk;
+                  if (step >= nsteps) break;
+                  const uint32_t acol = step * 8u;  // 16 fp16 = 8 TMEM columns
+                  const uint64_t off = kk * 2u;     // 32 B along K in SW128, >> 4
+                  mma_f16_ts(dt, ta_hi + acol, dbh + off, idesc, step != 0u);
+                  if ((lm >> step) & 1u) mma_f16_ts(dt, ta_lo + acol, dbh + off, idesc, 1u);
                   mma_f16_ts(dt, ta_hi + acol, dbl + off, idesc, 1u);
                 }
               }
+              const long long pq1 = prof ? clock64() : 0;
               mma_commit(&bar_wempty[ss]);
+              if (prof) pcm += static_cast<unsigned long long>(clock64() - pq1);
               if (++ss == L.n_wst) {
                 ss = 0;
                 ph ^= 1u;
               }
             }
+            const long long pq2 = prof ? clock64() : 0;
             mma_commit(&bar_accfull[acc]);
+            if (prof) pcm += static_cast<unsigned long long>(clock64() - pq2);
           }
           __syncwarp();
           for (uint32_t kc = 0; kc < a.nkc; ++kc)
@@ -938,6 +975,13 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
         atomicAdd(&a.prof[23], static_cast<unsigned long long>(clock64() - ploop));
         atomicAdd(&a.prof[24], pw[2] + pw[3] + pw[4]);
         atomicAdd(&a.prof[25], pfence);
+      }
+      if (prof && pmn) {
+        const unsigned long long wf = warp_sum_u64_tc(pwf), cm = warp_sum_u64_tc(pcm);
+        if (lane == 0) {
+          atomicAdd(&a.prof[26], wf);
+          atomicAdd(&a.prof[27], cm);
+        }
       }
     }
   } else if (kFuse && warp >= 10) {
@@ -970,7 +1014,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
             v[g][0] = v[g][1] = v[g][2] = v[g][3] = 0.0f;
           }
         }
-        convert_row<8>(v, l8, live, groups, a.nkc, a.dim, a.margin_c, Asm, r, &thr_sm[p][r]);
+        (void)convert_row<8>(v, l8, live, groups, a.nkc, a.dim, a.margin_c, Asm, r, &thr_sm[p][r]);
       }
       fence_proxy_async();  // A image (generic stores) -> tcgen05.cp (async proxy)
       __syncwarp();
@@ -1031,6 +1075,166 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
     }
     atomicMin(&min_next, i);
   } else {
+#if ACE_SPLIT
+    // ---------------- epilogue (warps 2-9), split direction tiles ----------------
+    // Both warps of a TMEM lane quarter (q = warp % 4) work on every direction
+    // tile: half h takes columns [h*TW/2, (h+1)*TW/2) in 64-column rounds
+    // (two 32-column loads in flight, one for the 96-column half's last
+    // round).  Per 32 columns: sign bits packed MSB-first, near ties by one
+    // unsigned min over |v| (bits << 1), four independent chains for ILP.  The
+    // tile's accumulator is released after half the per-warp work of the
+    // whole-tile scheme, so the next MMA into it starts that much sooner.
+    // Each half cuts the buckets of the tables ending in its columns; a table
+    // straddling the halves needs half 0's last word, a table straddling the
+    // previous tile that tile's last word (half 1): both are published in
+    // shared memory around one 64-thread pair barrier (1+q) per tile.
+    const uint32_t q = warp & 3, h = (warp - 2) >> 2;
+    const uint32_t r = q * 32u + lane;
+    const uint32_t kmask = (K >= 32u) ? 0xffffffffu : ((1u << K) - 1u);
+    const uint32_t nacc = tc_acc_bufs(a.nkc, TW);
+    const uint32_t hw = TW / 2u;      // columns per half (64 or 96)
+    const uint32_t nwh = hw / 32u;    // sign words per half (2 or 3)
+    const uint32_t nwords = TW / 32u;
+    uint32_t acc = 0, accph = 0;
+    uint64_t g = 0;
+    long long pc_ext = 0;
+    for (uint64_t it = 0; it < iters; ++it) {
+      const uint64_t t = tile_of(it);
+      const uint64_t row = t * kRows + r;
+      const bool valid = row < a.n;
+      float thr;
+      if (kFuse) {
+        const uint32_t p = static_cast<uint32_t>(it) & 1u;
+        mbar_wait_sleepy(&bar_thrfull[p], static_cast<uint32_t>(it >> 1) & 1u, nullptr);
+        thr = valid ? thr_sm[p][r] : -1.0f;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_threempty[p]);
+      } else {
+        thr = valid ? a.rowthr[row] : -1.0f;
+      }
+      const bool zero_row = thr < 0.0f;
+      const uint32_t thr_u = zero_row ? 0u : (isinf(thr) ? 0xffffffffu : (__float_as_uint(thr) << 1));
+      for (uint32_t j = 0; j < a.ntiles; ++j, ++g) {
+        const uint32_t used = min(TW, R - j * TW);
+        const uint32_t hbase = h * hw;
+        const uint32_t hused = used > hbase ? min(hw, used - hbase) : 0u;
+        const uint32_t col0 = j * TW + hbase;
+        // half 0: the previous tile's last word (half 1 wrote it before the
+        // previous pair barrier and rewrites the slot only after this one)
+        uint32_t prev = 0u;
+        if (h == 0u && g > 0) prev = xw[q][1][(g - 1) & 1u][lane];
+        mbar_wait_sleepy(&bar_accfull[acc], accph, (prof && lane == 0) ? &pw[5] : nullptr);
+        pipe_after();
+        long long pc0 = prof ? clock64() : 0, pc1 = 0, pc2 = 0;
+        uint32_t wd0 = 0xffffffffu, wd1 = 0xffffffffu, wd2 = 0xffffffffu;
+        if (!(a.dbg & 1)) {
+#pragma unroll 1
+          for (uint32_t hr = 0; hr < (nwh + 1u) / 2u; ++hr) {
+            const uint32_t c0 = 64u * hr;
+            if (c0 >= hused) break;
+            const bool two = c0 + 32u < hw;  // the round's second 32-column group lies in this half
+            uint32_t v[64];
+            const uint32_t ta = tmem_base + ((q * 32u) << 16) + acc * TW + hbase + c0;
+            ACE_TMEM_LD32(ta, v);
+            if (two) ACE_TMEM_LD32(ta + 32u, (v + 32));
+            tmem_wait_ld();
+            if (prof && hr == 0) pc1 = clock64();
+            uint32_t w2[2] = {0xffffffffu, 0xffffffffu};
+#pragma unroll
+            for (uint32_t g2 = 0; g2 < 2; ++g2) {
+              if (g2 == 1u && !two) break;
+              const uint32_t cc = c0 + 32u * g2;
+              const uint32_t* vv = v + 32 * g2;
+              uint32_t n4[4] = {0u, 0u, 0u, 0u}, m4[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+#pragma unroll
+              for (int jj = 0; jj < 8; ++jj)
+#pragma unroll
+                for (int gq = 0; gq < 4; ++gq) {
+                  n4[gq] = (n4[gq] << 1) | (vv[gq * 8 + jj] >> 31);
+                  m4[gq] = min(m4[gq], vv[gq * 8 + jj] << 1);
+                }
+              const uint32_t neg = (n4[0] << 24) | (n4[1] << 16) | (n4[2] << 8) | n4[3];
+              const uint32_t mn = min(min(m4[0], m4[1]), min(m4[2], m4[3]));
+              // columns past `used` (padding / stale) are masked here, off the hot path
+              if (!zero_row && valid && mn <= thr_u && cc < hused) {
+                const uint32_t ncol = min(32u, hused - cc);
+                uint32_t nm = 0u;
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) nm |= (((vv[jj] << 1) <= thr_u) ? 1u : 0u) << jj;
+                if (ncol < 32u) nm &= (1u << ncol) - 1u;
+                if (nm)
+                  push_near_mask(a.st, a.near_list + blockIdx.x * seg_cap, seg_cap, &seg_n, a.overflow_rows, nm, row,
+                                 col0 + cc);
+              }
+              w2[g2] = zero_row ? 0xffffffffu : ~neg;  // bit (31-jj) = column cc+jj >= 0
+            }
+            if (hr == 0) {
+              wd0 = w2[0];
+              wd1 = w2[1];
+            } else {
+              wd2 = w2[0];
+            }
+          }
+        }
+        pipe_before();
+        __syncwarp();
+        if (prof) pc2 = clock64();
+        if (lane == 0) {
+          if (rank == 0)
+            mbar_arrive(&bar_accempty[acc]);
+          else
+            mbar_arrive_remote(&bar_accempty[acc], 0);  // the leader's MMA reuses our accumulator too
+        }
+        xw[q][h][g & 1u][lane] = nwh == 2u ? wd1 : wd2;  // this half's last word
+        asm volatile("bar.sync %0, 64;" ::"r"(1u + q) : "memory");
+        if (prof && lane == 0 && warp == 2) {
+          const long long pc3 = clock64();
+          atomicAdd(&a.prof[16], static_cast<unsigned long long>(pc1 - pc0));  // TMEM load + wait
+          atomicAdd(&a.prof[17], static_cast<unsigned long long>(pc2 - pc1));  // sign / near processing
+          atomicAdd(&a.prof[18], static_cast<unsigned long long>(pc3 - pc2));  // arrive + pair barrier
+          pc_ext = pc3;
+        }
+        // buckets of the tables whose last column lies in this half
+        const uint32_t tb = j == 0 ? 0u : a.tab_end[j - 1], te = a.tab_end[j];
+        const uint32_t tm = min(max((j * TW + hw) / K, tb), te);  // tables ending before half 1
+        const uint32_t t0 = h == 0u ? tb : tm, t1 = h == 0u ? tm : te;
+        if (t0 < t1) {
+          // word stream: the word before this half, then its own words; the
+          // first table starts in one of the first two (K <= 32)
+          const uint32_t s0 = t0 * K;
+          uint32_t w0 = h == 0u ? prev : xw[q][0][g & 1u][lane], w1 = wd0, w2 = wd1, w3 = wd2, w4 = 0u;
+          if (static_cast<int>(s0 >> 5) - static_cast<int>(j * nwords + h * nwh) >= 0) {
+            w0 = w1; w1 = w2; w2 = w3; w3 = w4;
+          }
+          uint32_t off = s0 & 31u;
+          uint32_t* idp = a.ids + row;
+          for (uint32_t tt = t0; tt < t1; ++tt) {
+            const unsigned long long win = (static_cast<unsigned long long>(w0) << 32) | w1;
+            const uint32_t bucket = static_cast<uint32_t>(win >> (64u - off - K)) & kmask;
+            if (valid) idp[static_cast<uint64_t>(tt) * a.n] = bucket;
+            if (a.fused_insert) insert_bucket_warp(a.counters + (static_cast<uint64_t>(tt) << K), bucket, valid, lane);
+            off += K;
+            if (off >= 32u) {
+              off -= 32u;
+              w0 = w1; w1 = w2; w2 = w3; w3 = 0u;
+            }
+          }
+        }
+        if (prof && lane == 0 && warp == 2) atomicAdd(&a.prof[19], static_cast<unsigned long long>(clock64() - pc_ext));
+        if (++acc == nacc) {
+          acc = 0;
+          accph ^= 1u;
+        }
+      }
+      // this tile's ids (and near-list entries) are written: publish to the
+      // recheck warps
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        atomicAdd(&tiles_done, 1u);
+      }
+    }
+#else
     // ---------------- epilogue (warps 2-9) ----------------
     // Two warps per TMEM lane quarter (q = warp % 4) take alternate direction
     // tiles (global tile counter g, owner h = g & 1), all 128 columns each, in
@@ -1164,28 +1368,29 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
           // stream, words nwords*j-1 (prev) .. nwords*j+nwords-1 (wd)
           const uint32_t tb = j == 0 ? 0u : a.tab_end[j - 1], te = a.tab_end[j];
           uint32_t* idp = a.ids + row;
-          for (uint32_t tt = tb; tt < te; ++tt) {
-            const uint32_t s0 = tt * K;
-            const int wi = static_cast<int>(s0 >> 5) - static_cast<int>(nwords * j);  // -1 .. nwords-1
-            const uint32_t off = s0 & 31u;
-            const uint32_t hi = wi < 0    ? prev
-                                : wi == 0 ? wd0
-                                : wi == 1 ? wd1
-                                : wi == 2 ? wd2
-                                : wi == 3 ? wd3
-                                : wi == 4 ? wd4
-                                          : wd5;
-            const uint32_t lo = wi < 0    ? wd0
-                                : wi == 0 ? wd1
-                                : wi == 1 ? wd2
-                                : wi == 2 ? wd3
-                                : wi == 3 ? wd4
-                                : wi == 4 ? wd5
-                                          : 0u;
-            const unsigned long long win = (static_cast<unsigned long long>(hi) << 32) | lo;
-            const uint32_t bucket = static_cast<uint32_t>(win >> (64u - off - K)) & kmask;
-            if (valid && (!(a.dbg & 128) || bucket == 0xffffffffu)) idp[static_cast<uint64_t>(tt) * a.n] = bucket;
-            if (a.fused_insert) insert_bucket_warp(a.counters + (static_cast<uint64_t>(tt) << K), bucket, valid, lane);
+          if (tb < te) {
+            // a window over the word stream prev, wd0, wd1, ...: the first
+            // table starts in prev or wd0 (it ends in this tile, K <= 32);
+            // each table reads the top two words, and the stream moves down
+            // a word whenever the bit offset passes 32 (no dynamic indexing)
+            const uint32_t s0 = tb * K;
+            uint32_t w0 = prev, w1 = wd0, w2 = wd1, w3 = wd2, w4 = wd3, w5 = nwords == 4u ? 0u : wd4,
+                     w6 = nwords == 4u ? 0u : wd5;
+            if (static_cast<int>(s0 >> 5) - static_cast<int>(nwords * j) >= 0) {
+              w0 = w1; w1 = w2; w2 = w3; w3 = w4; w4 = w5; w5 = w6; w6 = 0u;
+            }
+            uint32_t off = s0 & 31u;
+            for (uint32_t tt = tb; tt < te; ++tt) {
+              const unsigned long long win = (static_cast<unsigned long long>(w0) << 32) | w1;
+              const uint32_t bucket = static_cast<uint32_t>(win >> (64u - off - K)) & kmask;
+              if (valid && (!(a.dbg & 128) || bucket == 0xffffffffu)) idp[static_cast<uint64_t>(tt) * a.n] = bucket;
+              if (a.fused_insert) insert_bucket_warp(a.counters + (static_cast<uint64_t>(tt) << K), bucket, valid, lane);
+              off += K;
+              if (off >= 32u) {
+                off -= 32u;
+                w0 = w1; w1 = w2; w2 = w3; w3 = w4; w4 = w5; w5 = w6; w6 = 0u;
+              }
+            }
           }
           if (prof && lane == 0 && warp == 2) atomicAdd(&a.prof[19], static_cast<unsigned long long>(clock64() - pc_ext));
         }
@@ -1202,6 +1407,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
         atomicAdd(&tiles_done, 1u);
       }
     }
+#endif
   }
 
   if (warp >= 2) {

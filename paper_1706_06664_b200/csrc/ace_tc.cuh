@@ -28,6 +28,8 @@ struct TcArgs {
   const uint16_t* w16;
   uint16_t* x16;              // converted x tiles (pre-pass output), SW128 image
   float* rowthr;              // per-row error threshold (pre-pass output)
+  uint32_t* lomask;           // per point tile: bit s set iff some x lo part of K16 step s is nonzero
+                              // (pre-pass output, zeroed before it; null = all steps need the lo pass)
   float margin_c;             // relative error bound
   uint32_t* ids;              // table-major, stride n
   unsigned long long* near_list;  // (row << 32) | direction; one segment per CTA

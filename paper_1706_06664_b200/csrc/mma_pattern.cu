@@ -11,10 +11,15 @@
 //          commits an empty barrier; a producer warp re-arms (4 stages)
 //   bit 6: the producer also bulk-copies 32 KB from global into the stage
 //   bit 7: whole warp walks the MMA loop (elect + __syncwarp), as the kernel
+//   bit 8: warps 4-7 drain accumulators with tcgen05.ld 32x32b.x32 (all 128
+//          lanes) the whole time, as the epilogue does; reports LDTM B/cycle
+//   bit 9: with bit 8, the loads use 32x32b.x64 (64 registers per load)
+//   bit 10: with bit 8, 16x256b.x8 shape instead
 // Prints cycles per MMA for each mode.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -39,6 +44,7 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
 }
 
 __global__ void mma_pattern(int n_tiles, int mode, const uint8_t* gsrc, unsigned long long* out) {
+  __shared__ volatile int done;
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint32_t tbase;
@@ -61,6 +67,7 @@ __global__ void mma_pattern(int n_tiles, int mode, const uint8_t* gsrc, unsigned
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[i])));
     }
     asm volatile("fence.mbarrier_init.release.cluster;");
+    done = 0;
   }
   asm volatile("fence.proxy.async.shared::cta;");
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -130,7 +137,67 @@ __global__ void mma_pattern(int n_tiles, int mode, const uint8_t* gsrc, unsigned
     __syncwarp();
     asm volatile("{\n.reg .pred p;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra W;\n}\n" ::"r"(smem_u32(&bar)));
     t1 = clock64();
-    if (threadIdx.x == 0) atomicAdd(out, static_cast<unsigned long long>(t1 - t0));
+    if (threadIdx.x == 0) {
+      atomicAdd(out, static_cast<unsigned long long>(t1 - t0));
+      done = 1;
+    }
+  }
+  if ((mode & 256) && threadIdx.x >= 128) {
+    const uint32_t lane_base = ((threadIdx.x / 32) & 3u) * 32u;
+    uint32_t acc = 0;
+    unsigned long long bytes = 0;
+    const long long s0 = clock64();
+    uint32_t col = 0;
+    while (!done) {
+      const uint32_t addr = t + (lane_base << 16) + col;
+      uint32_t r[64];
+      if (mode & 1024) {
+        asm volatile("tcgen05.ld.sync.aligned.16x256b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                     "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                       "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                       "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                       "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                       "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                     : "r"(addr));
+        for (int i = 32; i < 64; ++i) r[i] = 0;
+        bytes += 16 * 32 * 4;  // per warp: 16 lanes x 64 cols... counted as 32 regs x 32 threads x 4 B
+        bytes += 0;
+      } else {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                     "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                       "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                       "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                       "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                       "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                     : "r"(addr));
+        if (mode & 512) {
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                       "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                       : "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]),
+                         "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]),
+                         "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]),
+                         "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]),
+                         "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+                       : "r"(addr + 32u));
+          bytes += 32 * 32 * 4;
+        } else {
+          for (int i = 32; i < 64; ++i) r[i] = 0;
+        }
+        bytes += 32 * 32 * 4;
+      }
+      asm volatile("tcgen05.wait::ld.sync.aligned;");
+      #pragma unroll
+      for (int i = 0; i < 64; ++i) acc += r[i];
+      col = (col + 64u) % 384u;
+    }
+    const long long s1 = clock64();
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(out + 1, bytes);
+      atomicAdd(out + 2, static_cast<unsigned long long>(s1 - s0));
+    }
+    if (acc == 0x12345678u) out[3] = acc;
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -142,22 +209,35 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   cudaFuncSetAttribute(mma_pattern, cudaFuncAttributeMaxDynamicSharedMemorySize, 130 * 1024);
   unsigned long long* d;
-  cudaMalloc(&d, 8);
+  cudaMalloc(&d, 32);
   uint8_t* src;
   cudaMalloc(&src, 64 << 15);
   cudaMemset(src, 0, 64 << 15);
   const int n_tiles = 2000;  // x 24 MMAs
-  for (int mode : {0, 16, 15, 31, 15 | 32, 31 | 32, 15 | 32 | 64 | 128, 31 | 32 | 64 | 128, 0, 31}) {
-    double per = 0;
-    for (int rep = 0; rep < 2; ++rep) {
-      cudaMemset(d, 0, 8);
-      mma_pattern<<<sms, 128, 130 * 1024>>>(n_tiles, mode, src, d);
-      cudaDeviceSynchronize();
-      unsigned long long cyc = 0;
-      cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
-      per = static_cast<double>(cyc) / sms / (n_tiles * 24.0);
+  int modes[32], nm = 0;
+  if (getenv("MODES")) {
+    for (char* p = getenv("MODES"); *p && nm < 32;) {
+      modes[nm++] = static_cast<int>(strtol(p, &p, 0));
+      while (*p == ',') ++p;
     }
-    printf("mode %2d: %.1f cycles/MMA\n", mode, per);
+  } else {
+    const int def[] = {31, 31 | 256, 31 | 256 | 512, 31 | 256 | 1024, 31 | 32 | 64 | 128, 31 | 32 | 64 | 128 | 256,
+                       31 | 32 | 64 | 128 | 256 | 512};
+    for (int m : def) modes[nm++] = m;
+  }
+  for (int mi = 0; mi < nm; ++mi) {
+    const int mode = modes[mi];
+    double per = 0, ldb = 0;
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaMemset(d, 0, 32);
+      mma_pattern<<<sms, (mode & 256) ? 256 : 128, 130 * 1024>>>(n_tiles, mode, src, d);
+      cudaDeviceSynchronize();
+      unsigned long long h[4] = {0, 0, 0, 0};
+      cudaMemcpy(h, d, 32, cudaMemcpyDeviceToHost);
+      per = static_cast<double>(h[0]) / sms / (n_tiles * 24.0);
+      ldb = h[2] ? static_cast<double>(h[1]) / (static_cast<double>(h[2]) / 4.0) : 0.0;  // per SM: 4 warps
+    }
+    printf("mode %4d: %.1f cycles/MMA, LDTM %.1f B/cycle/SM\n", mode, per, ldb);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) fprintf(stderr, "%s\n", cudaGetErrorString(e));

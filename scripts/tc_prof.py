@@ -39,3 +39,6 @@ if out[21]:
     print("  MMA warp: %d groups of 12 MMAs per CTA, %.0f cycles issue time per group (%.1f per MMA)" % (out[21] / grid, out[20] / out[21], out[20] / out[21] / 12))
 print("  MMA lane per CTA: loop %.0f = issue %.0f + A copies %.0f + waits %.0f + other %.0f" % (out[23] / grid, out[20] / grid, out[22] / grid, out[24] / grid, (out[23] - out[20] - out[22] - out[24]) / grid))
 print("  MMA lane per CTA: tcgen05 fence after acc_empty %.0f" % (out[25] / grid))
+if out[21]:
+    print("  MMA issuing lane per CTA: W-full waits %.0f  commits %.0f  (per group: %.0f / %.0f)" % (
+        out[26] / grid, out[27] / grid, out[26] / out[21], out[27] / out[21]))
