@@ -99,6 +99,11 @@ struct AceSketch {
   DevState* hst = nullptr;   // pinned host mirror
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
+  // chunked host-input pipeline (batch_detect): H2D copies on their own
+  // stream, one event per chunk
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t cstart = nullptr;
+  std::vector<cudaEvent_t> cev;
   DevBuf ids, sums, stage, flags, scores, demand, near, overflow, x16, rowthr, segc, gbuf, lomask;
   // build + detect over the same rows: run_hash leaves the insert to the
   // fused count-and-gather pass of the detect tail (apply_gather_kernel)
@@ -258,9 +263,16 @@ bool fire_and_forget_ok(const AceSketch* sk, uint64_t n) {
 }
 
 // hash n rows into sk->ids (table-major, stride n); optional fused insert.
-ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64_t ld, int insert) {
+// Chunk mode (ids_out != null): the rows are rows [r0, r0 + n) of a longer
+// batch whose ids (stride ids_ld) the caller has sized.
+ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64_t ld, int insert,
+                    uint32_t* ids_out = nullptr, uint64_t ids_ld = 0) {
   const AceFamily* f = sk->fam;
-  ACE_CUDA(sk->ids.ensure(static_cast<size_t>(n) * f->d.tables * sizeof(uint32_t)));
+  if (!ids_out) {
+    ACE_CUDA(sk->ids.ensure(static_cast<size_t>(n) * f->d.tables * sizeof(uint32_t)));
+    ids_out = sk->ids.as<uint32_t>();
+    ids_ld = n;
+  }
   for (bool& u : sk->ev_used) u = false;
   sk->mark(0);
   if (f->use_tc()) {
@@ -283,7 +295,8 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
     t.margin_c = kstream ? tck_margin(f->tc.nkc, t.x_f64 != 0)
                          : static_cast<float>(2.0 * (4.0 * 0x1.0p-22 + 0x1.0p-23 * (12.0 * f->tc.nkc + 16.0) * 1.01 +
                                                      (t.x_f64 ? 0x1.0p-23 : 0.0)));
-    t.ids = sk->ids.as<uint32_t>();
+    t.ids = ids_out;
+    t.ids_ld = ids_ld;
     // near-tie list: the K-streamed path's bound (large d, dense data) leaves
     // far more near ties per row, size its list accordingly
     uint64_t cap = tc_kstream(f->tc.nkc) ? n * f->d.rows / 48 : n * f->d.rows / 1024;
@@ -351,8 +364,8 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
       if (insert && sk->defer_insert)
         sk->insert_deferred = true;
       else if (insert)
-        ACE_CUDA(launch_apply_ids(sk->ids.as<uint32_t>(), n, f->d.tables, f->d.k_bits, sk->counters, sk->cap,
-                                  +1, sk->st, sk->stream, !fire_and_forget_ok(sk, n)));
+        ACE_CUDA(launch_apply_ids(ids_out, n, f->d.tables, f->d.k_bits, sk->counters, sk->cap, +1, sk->st,
+                                  sk->stream, !fire_and_forget_ok(sk, n), ids_ld));
       if (insert && sk->width == 16)
         ACE_CUDA(launch_cap(sk->counters, sk->num_counters, sk->cap, sk->st, sk->stream));
       sk->mark(1);
@@ -397,11 +410,11 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
     } else if (insert && sk->defer_insert) {
       sk->insert_deferred = true;
     } else if (insert) {
-      ACE_CUDA(launch_apply_ids(sk->ids.as<uint32_t>(), n, f->d.tables, f->d.k_bits, sk->counters, sk->cap,
-                                +1, sk->st, sk->stream, !fire_and_forget_ok(sk, n)));
+      ACE_CUDA(launch_apply_ids(ids_out, n, f->d.tables, f->d.k_bits, sk->counters, sk->cap, +1, sk->st,
+                                sk->stream, !fire_and_forget_ok(sk, n), ids_ld));
     }
   } else {
-    HashArgs a = make_hash_args(f, xd, dtype, n, ld, sk->ids.as<uint32_t>(), n, sk->st);
+    HashArgs a = make_hash_args(f, xd, dtype, n, ld, ids_out, ids_ld, sk->st);
     a.insert = insert;
     a.counters = sk->counters;
     a.cap = sk->cap;
@@ -773,6 +786,10 @@ ace_status ace_sketch_destroy(AceSketch* sk) {
   if (sk->st) cudaFree(sk->st);
   if (sk->hst) cudaFreeHost(sk->hst);
   if (sk->own) cudaStreamDestroy(sk->own);
+  if (sk->cstream) cudaStreamDestroy(sk->cstream);
+  if (sk->cstart) cudaEventDestroy(sk->cstart);
+  for (cudaEvent_t e : sk->cev)
+    if (e) cudaEventDestroy(e);
   for (cudaEvent_t& e : sk->ev)
     if (e) cudaEventDestroy(e);
   family_release(sk->fam);
@@ -999,11 +1016,57 @@ ace_status batch_detect(AceSketch* sk, const void* x, int dtype, uint64_t n, uin
     const char* e = getenv("ACE_GRAPHS");
     graphs_env = e ? atoi(e) : 1;
   }
-  const bool eligible = graphs_env != 0 && !sk->timing && (x_where == ACE_DEVICE || host_pinned(x));
+  const bool pinned = x_where == ACE_HOST && host_pinned(x);
+  const bool eligible = graphs_env != 0 && !sk->timing && (x_where == ACE_DEVICE || pinned);
   const void* xd = nullptr;
   uint64_t ldd = 0;
   uint32_t* dflags = nullptr;
   double* dscores = nullptr;
+  // Pinned host rows of a large batch: the H2D copy runs in chunks on a copy
+  // stream and each chunk is converted and hashed as it lands, so the hashing
+  // hides behind the transfer (ACE_H2D_CHUNKS; 0 = one copy, then the work).
+  static int chunks_env = -2;
+  if (chunks_env == -2) {
+    const char* e = getenv("ACE_H2D_CHUNKS");
+    chunks_env = e ? atoi(e) : 8;
+  }
+  if (pinned && chunks_env > 1 && !sk->timing && sk->fam->use_tc() && !tc_kstream(sk->fam->tc.nkc) &&
+      n >= static_cast<uint64_t>(chunks_env) * 16384u) {
+    const uint64_t rows_c = ((n + chunks_env - 1) / chunks_env + 127) / 128 * 128;
+    const size_t esz = dtype == ACE_F64 ? 8 : 4;
+    ACE_CUDA(zero_call_fields(sk));
+    ACE_CUDA(sk->stage.ensure(n * ld * esz));
+    ACE_CUDA(sk->ids.ensure(static_cast<size_t>(n) * sk->fam->d.tables * sizeof(uint32_t)));
+    if (!sk->cstream) ACE_CUDA(cudaStreamCreateWithFlags(&sk->cstream, cudaStreamNonBlocking));
+    if (!sk->cstart) ACE_CUDA(cudaEventCreateWithFlags(&sk->cstart, cudaEventDisableTiming));
+    const uint64_t nch = (n + rows_c - 1) / rows_c;
+    while (sk->cev.size() < nch) {
+      cudaEvent_t e;
+      ACE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      sk->cev.push_back(e);
+    }
+    // the copies overwrite the staging buffer: after earlier work on the stream
+    ACE_CUDA(cudaEventRecord(sk->cstart, sk->stream));
+    ACE_CUDA(cudaStreamWaitEvent(sk->cstream, sk->cstart, 0));
+    for (uint64_t c = 0; c < nch; ++c) {
+      const uint64_t r0 = c * rows_c, rows = std::min(rows_c, n - r0);
+      ACE_CUDA(cudaMemcpyAsync(static_cast<char*>(sk->stage.p) + r0 * ld * esz,
+                               static_cast<const char*>(x) + r0 * ld * esz, rows * ld * esz, cudaMemcpyHostToDevice,
+                               sk->cstream));
+      ACE_CUDA(cudaEventRecord(sk->cev[c], sk->cstream));
+    }
+    for (uint64_t c = 0; c < nch; ++c) {
+      const uint64_t r0 = c * rows_c, rows = std::min(rows_c, n - r0);
+      ACE_CUDA(cudaStreamWaitEvent(sk->stream, sk->cev[c], 0));
+      ace_status r = run_hash(sk, static_cast<const char*>(sk->stage.p) + r0 * ld * esz, dtype, rows, ld, build,
+                              sk->ids.as<uint32_t>() + r0, n);
+      if (r != ACE_OK) return r;
+    }
+    ace_status r = run_detect_device(sk, n, flag_bits, scores, out_where, &dflags, &dscores);
+    sk->defer_insert = false;
+    if (r != ACE_OK) return r;
+    return finish_detect(sk, n, flag_bits, scores, out_where, dflags, dscores, report);
+  }
   auto device_work = [&]() -> ace_status {
     ACE_CUDA(zero_call_fields(sk));
     ace_status r = stage_x(sk, sk->stage, sk->stream, x, dtype, n, ld, x_where, &xd, &ldd);

@@ -871,10 +871,12 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
               const uint64_t dbh = sw128_desc(b_hi), dbl = sw128_desc(b_hi + half);
 #pragma unroll
               for (uint32_t kk = 0; kk < 4; ++kk) {
-                const uint32_t acol = (kc * 4u + kk) * 8u;
+                const uint32_t step = kc * 4u + kk;
+                if (step >= nsteps) break;
+                const uint32_t acol = step * 8u;
                 const uint64_t off = kk * 2u;
-                mma_f16_ts(dt, ta_hi + acol, dbh + off, idesc, (kc | kk) != 0u);
-                mma_f16_ts(dt, ta_lo + acol, dbh + off, idesc, 1u);
+                mma_f16_ts(dt, ta_hi + acol, dbh + off, idesc, step != 0u);
+                if ((lm >> step) & 1u) mma_f16_ts(dt, ta_lo + acol, dbh + off, idesc, 1u);
                 mma_f16_ts(dt, ta_hi + acol, dbl + off, idesc, 1u);
               }
               mma_commit(&bar_wempty[ss]);
@@ -1057,7 +1059,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
         const bool abandoned = !exact_proj_until(a.w64 + static_cast<uint64_t>(dir) * a.dim, a.x, a.x_f64, row, a.ld,
                                                  static_cast<uint32_t>(a.dim), &tiles_done, total_done, &p);
         if (abandoned) break;
-        uint32_t* id = &a.ids[static_cast<uint64_t>(table) * a.n + row];
+        uint32_t* id = &a.ids[static_cast<uint64_t>(table) * a.ids_ld + row];
         const uint32_t exact = p >= 0.0 ? 1u : 0u;
         if (((__ldcg(id) >> bpos) & 1u) != exact) {
           const uint32_t old = atomicXor(id, 1u << bpos);
@@ -1211,7 +1213,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
           for (uint32_t tt = t0; tt < t1; ++tt) {
             const unsigned long long win = (static_cast<unsigned long long>(w0) << 32) | w1;
             const uint32_t bucket = static_cast<uint32_t>(win >> (64u - off - K)) & kmask;
-            if (valid) idp[static_cast<uint64_t>(tt) * a.n] = bucket;
+            if (valid) idp[static_cast<uint64_t>(tt) * a.ids_ld] = bucket;
             if (a.fused_insert) insert_bucket_warp(a.counters + (static_cast<uint64_t>(tt) << K), bucket, valid, lane);
             off += K;
             if (off >= 32u) {
@@ -1383,7 +1385,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
             for (uint32_t tt = tb; tt < te; ++tt) {
               const unsigned long long win = (static_cast<unsigned long long>(w0) << 32) | w1;
               const uint32_t bucket = static_cast<uint32_t>(win >> (64u - off - K)) & kmask;
-              if (valid && (!(a.dbg & 128) || bucket == 0xffffffffu)) idp[static_cast<uint64_t>(tt) * a.n] = bucket;
+              if (valid && (!(a.dbg & 128) || bucket == 0xffffffffu)) idp[static_cast<uint64_t>(tt) * a.ids_ld] = bucket;
               if (a.fused_insert) insert_bucket_warp(a.counters + (static_cast<uint64_t>(tt) << K), bucket, valid, lane);
               off += K;
               if (off >= 32u) {
@@ -1420,7 +1422,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
     const uint32_t et = threadIdx.x - 64u;
     const uint32_t cnt = static_cast<uint32_t>(min(static_cast<unsigned long long>(seg_n), seg_cap));
     if (!(a.dbg & 32))
-      recheck_tail(a.x, a.x_f64, a.ld, static_cast<uint32_t>(a.dim), a.w64, a.ids, a.n, a.counters, a.fused_insert,
+      recheck_tail(a.x, a.x_f64, a.ld, static_cast<uint32_t>(a.dim), a.w64, a.ids, a.ids_ld, a.counters, a.fused_insert,
                    K, base, L.a_bytes + L.w_bytes, a.near_list + blockIdx.x * seg_cap, min(min_next, cnt), cnt, et,
                    rr_own, ff_own);
     rr_own = warp_sum_u64_tc(rr_own);
@@ -1664,7 +1666,7 @@ __global__ void __launch_bounds__(kKsThreads, 1) hash_tck_kernel(const TcArgs a)
           const uint32_t lo = wi < 3 ? sgbuf[par][wi + 1][r] : 0u;
           const unsigned long long win = (static_cast<unsigned long long>(hi) << 32) | lo;
           const uint32_t bucket = static_cast<uint32_t>(win >> (64u - off - K)) & kmask;
-          if (valid) idp[static_cast<uint64_t>(tt) * a.n] = bucket;
+          if (valid) idp[static_cast<uint64_t>(tt) * a.ids_ld] = bucket;
         }
       }
     }
@@ -1859,7 +1861,7 @@ __global__ void __launch_bounds__(256) recheck_segs_kernel(const TcArgs a, uint3
       }
       if (lane == 0) {
         const uint32_t table = dir / K, bpos = K - 1u - dir % K;
-        uint32_t* id = &a.ids[static_cast<uint64_t>(table) * a.n + row];
+        uint32_t* id = &a.ids[static_cast<uint64_t>(table) * a.ids_ld + row];
         if (static_cast<int>((*id >> bpos) & 1u) != bit) {
           atomicXor(id, 1u << bpos);
           ++ff;
@@ -1892,7 +1894,7 @@ __global__ void recheck_rows_kernel(const TcArgs a, const double* __restrict__ w
                                   a.ld, a.dim);
       bucket = (bucket << 1) | (p >= 0.0 ? 1u : 0u);
     }
-    uint32_t* id = &a.ids[static_cast<uint64_t>(table) * a.n + row];
+    uint32_t* id = &a.ids[static_cast<uint64_t>(table) * a.ids_ld + row];
     const uint32_t old = *id;
     *id = bucket;
     if (a.fused_insert && old != bucket) {

@@ -31,7 +31,8 @@ struct TcArgs {
   uint32_t* lomask;           // per point tile: bit s set iff some x lo part of K16 step s is nonzero
                               // (pre-pass output, zeroed before it; null = all steps need the lo pass)
   float margin_c;             // relative error bound
-  uint32_t* ids;              // table-major, stride n
+  uint32_t* ids;              // table-major, stride ids_ld
+  uint64_t ids_ld;            // ids row stride per table (>= n; a chunk of a longer batch writes into it)
   unsigned long long* near_list;  // (row << 32) | direction; one segment per CTA
   unsigned long long near_cap;    // total entries (the kernel uses near_cap / grid per CTA)
   const double* w64;              // the reference's W (binary64) for the exact recheck

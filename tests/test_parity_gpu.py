@@ -320,3 +320,53 @@ print(json.dumps(out))
         assert got[cfg][0] == e["counters_sha256"], cfg
         assert got[cfg][1] == e["flags_sha256"], cfg
         assert got[cfg][2] == e["reported"], cfg
+
+
+@pytest.mark.parametrize("chunks", [3, 16])
+def test_chunked_h2d_pipeline(cuda, golden, chunks):
+    """Pinned host rows of a large batch are copied in chunks on a copy
+    stream and hashed as each chunk lands (ACE_H2D_CHUNKS, read once: a
+    subprocess).  Uneven chunk counts on configs 1 and 2: reference counters,
+    flags and report."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    code = r'''
+import hashlib, json, sys
+import numpy as np, torch
+sys.path.insert(0, %r)
+from paper_1706_06664_b200 import ace
+from paper_1706_06664_b200 import workloads as W
+g = json.loads(open(%r).read())
+out = {}
+for cfg in (1, 2):
+    e = g["configs"][str(cfg)]
+    w = W.CONFIGS[cfg]
+    x, _ = W.host_rows(cfg, 0, e["n"])
+    xp = torch.from_numpy(x).pin_memory()
+    fam = ace.SrpFamily(ace.SrpConfig(dim=w.dim, k_bits=w.k_bits, num_tables=w.num_tables, seed=w.w_seed))
+    res = []
+    for width in (ace.CounterWidth.k32, ace.CounterWidth.k16):
+        sk = ace.AceSketch(fam, width)
+        for _ in range(2):
+            sk.reset()
+            rep = sk.build_detect(xp.numpy())
+        res.append([hashlib.sha256(sk.counters_u32().tobytes()).hexdigest(),
+                    hashlib.sha256(np.packbits(rep.flags, bitorder="little").tobytes()).hexdigest(),
+                    int(rep.reported)])
+    out[cfg] = res
+print(json.dumps(out))
+''' % (str(root), str(root / "tests" / "golden" / "golden.json"))
+    env = dict(os.environ, ACE_H2D_CHUNKS=str(chunks))
+    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    got = json.loads(res.stdout.strip().splitlines()[-1])
+    for cfg in ("1", "2"):
+        e = golden["configs"][cfg]
+        for width_res in got[cfg]:
+            assert width_res[0] == e["counters_sha256"], cfg
+            assert width_res[1] == e["flags_sha256"], cfg
+            assert width_res[2] == e["reported"], cfg
