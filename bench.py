@@ -44,6 +44,36 @@ def peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
 
 
+def step_roofline(w, value, pk, tensor=True):
+    """The metric's binding roofline for the whole step:
+    points/s = min(projection peak / (2 d K L), HBM / (4 d), L2 RED rate / L),
+    with the tcgen05 bf16 dense peak (or FP32 FFMA for the SIMT kernel), the
+    measured HBM copy bandwidth and the measured random-address L2 RED rate
+    (profiles/r1_peaks_probe.json) for this counter array.  This design counts
+    in shared-memory histograms (one RED per touched bucket per block), so
+    the L2-atomic term is the metric's definition rather than a limit of the
+    implementation; the binding term without it is reported beside it."""
+    probe = ROOT / "profiles" / "r1_peaks_probe.json"
+    red = None
+    if probe.exists():
+        d = json.loads(probe.read_text())
+        rates = {int(k): v for k, v in d.get("l2_red_u32_gops", {}).items()}
+        if rates:
+            size = w.num_tables * (4 << w.k_bits)
+            red = rates[min(rates, key=lambda k: abs(k - size))] * 1e9
+    f = 2.0 * w.dim * w.k_bits * w.num_tables
+    proj = (pk["bf16_tflops"] * 1e12 if tensor else 148 * 128 * 2 * 1.965e9) / f
+    hbm = pk["hbm_gbs"] * 1e9 / (4.0 * w.dim)
+    terms = {"projection_pts_s": proj, "hbm_x_read_pts_s": hbm}
+    if red:
+        terms["l2_atomic_pts_s"] = red / w.num_tables
+    bind = min(terms, key=terms.get)
+    no_atomic = min(proj, hbm)
+    return {"binding": bind.replace("_pts_s", ""), "binding_pts_s": terms[bind], "frac": value / terms[bind],
+            "terms": terms, "frac_without_atomic_term": value / no_atomic,
+            "source": "SURVEY.md 8(d); peaks from MEASURED_PEAKS.json and profiles/r1_peaks_probe.json"}
+
+
 class Clocks:
     """nvidia-smi sampling during the timed region."""
 
@@ -257,6 +287,7 @@ def run_stream(args, w, ws, rank, local):
                              "p99": float(np.percentile(lat_all, 99)),
                              "max": float(lat_all.max()), "batches_per_step": int(len(lats[0]))},
         "gpu_launches": int(launches), "clocks": clk,
+        "step_roofline": step_roofline(w, value, peaks()[0]),
         "exactness": {"rechecked": int(sk.last_stats.rechecked), "flipped": int(sk.last_stats.flipped),
                       "ambiguous": int(rep.ambiguous), "reported": int(rep.reported)},
     }
@@ -429,6 +460,7 @@ def main():
                    "l2": f"inputs {n * w.dim * 4 / 1e6:.0f} MB > 126 MB L2 (no flush needed)",
                    "parallelism": f"replicas x{ws}"},
         "roofline": roofline,
+        "step_roofline": step_roofline(w, value, pk, tensor=kernel == 2),
         "phases_ms": {"hash_insert": phase[0], "score": phase[1], "threshold_flags": phase[2],
                       "convert_x": phase[3], "projection_kernel": phase[4]},
         "kernels": kernels,
