@@ -104,9 +104,9 @@ struct AceSketch {
   cudaStream_t cstream = nullptr;
   cudaEvent_t cstart = nullptr;
   std::vector<cudaEvent_t> cev;
-  DevBuf ids, sums, stage, flags, scores, demand, near, overflow, x16, rowthr, segc, gbuf, lomask;
+  DevBuf ids, sums, stage, flags, scores, demand, near, overflow, x16, rowthr, segc, lomask;
   // build + detect over the same rows: run_hash leaves the insert to the
-  // fused count-and-gather pass of the detect tail (apply_gather_kernel)
+  // fused count-and-gather pass of the detect tail (detect_tail_kernel)
   bool defer_insert = false, insert_deferred = false;
   // restore (e.g. an ACE1 file) reports the restored mean exactly until the
   // next update, as the reference does (its mean is a stored recurrence)
@@ -448,29 +448,14 @@ ace_status run_detect_device(AceSketch* sk, uint64_t n, uint32_t* flag_bits, dou
     }
   }
   uint32_t* dflags = (flag_bits && out_where == ACE_DEVICE) ? flag_bits : sk->flags.as<uint32_t>();
-  if (sk->insert_deferred) {
-    // counts, then every id replaced by its final count (gathers from shared
-    // memory), then per-row sums of counts
-    sk->insert_deferred = false;
-    uint32_t* gout = sk->ids.as<uint32_t>();
-    if (f->d.k_bits > 15) {
-      ACE_CUDA(sk->gbuf.ensure(static_cast<size_t>(n) * f->d.tables * sizeof(uint32_t)));
-      gout = sk->gbuf.as<uint32_t>();
-    }
-    ACE_CUDA(launch_apply_gather(sk->ids.as<uint32_t>(), gout, n, f->d.tables, f->d.k_bits, sk->counters, sk->st,
-                                 sk->stream));
-    sk->mark(1);
-    ACE_CUDA(launch_score(gout, n, n, f->d.tables, f->d.k_bits, nullptr, sk->sums.as<uint64_t>(), dscores, sk->st,
-                          sk->stream));
-  } else {
-    ACE_CUDA(launch_score(sk->ids.as<uint32_t>(), n, n, f->d.tables, f->d.k_bits, sk->counters,
-                          sk->sums.as<uint64_t>(), dscores, sk->st, sk->stream));
-  }
+  // one cooperative launch: (deferred insert: counts, ids replaced by their
+  // final counts,) scores, exact threshold, flags (+ replay when ambiguous)
+  const int gather = sk->insert_deferred ? 1 : 0;
+  sk->insert_deferred = false;
+  sk->mark(1);
   sk->mark(2);
-  ACE_CUDA(launch_finalize_batch(n, f->d.tables, sk->st, sk->stream));
-  ACE_CUDA(launch_flags(sk->sums.as<uint64_t>(), n, dflags, sk->st, 0, sk->stream));
-  ACE_CUDA(launch_replay(sk->sums.as<uint64_t>(), n, f->d.tables, sk->st, sk->stream));
-  ACE_CUDA(launch_flags(sk->sums.as<uint64_t>(), n, dflags, sk->st, 1, sk->stream));
+  ACE_CUDA(launch_detect_tail(sk->ids.as<uint32_t>(), n, f->d.tables, f->d.k_bits, sk->counters, gather,
+                              sk->sums.as<uint64_t>(), dscores, dflags, sk->st, sk->stream));
   sk->mark(3);
   *dflags_out = dflags;
   *dscores_out = dscores;
@@ -528,6 +513,14 @@ int ace_debug_tc_prof(unsigned long long* out32) {
   if (!g_tc_prof) return -1;
   cudaDeviceSynchronize();
   return cudaMemcpy(out32, g_tc_prof, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : -2;
+}
+
+// Instrumentation: %globaltimer stamps of the last detect tail (ACE_TAIL_PROF=1):
+// [0] start [1] counts done [2] gather done [3] scores + threshold done [4] flags done.
+int ace_debug_tail_prof(unsigned long long* out8) {
+  if (!g_tail_prof) return -1;
+  cudaDeviceSynchronize();
+  return cudaMemcpy(out8, g_tail_prof, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : -2;
 }
 
 // SrpFamily::SrpFamily (srp.cpp:24-49): validation + W upload.
@@ -780,7 +773,6 @@ ace_status ace_sketch_destroy(AceSketch* sk) {
   sk->x16.release();
   sk->rowthr.release();
   sk->segc.release();
-  sk->gbuf.release();
   sk->lomask.release();
   if (sk->counters) cudaFree(sk->counters);
   if (sk->st) cudaFree(sk->st);
@@ -993,8 +985,8 @@ ace_status batch_detect(AceSketch* sk, const void* x, int dtype, uint64_t n, uin
   // gathers dominate (cfg 2: 0.541 -> 0.525 ms); a loss on small batches
   // (cfg 1) and even on cfg 3 (K = 16, two parts)
   sk->defer_insert = gather_env != 0 && build && sk->width == 32 && sk->fam->use_tc() &&
-                     (gather_env == 2 || (sk->fam->d.k_bits <= 15 && n * sk->fam->d.tables >= (16ull << 20))) &&
-                     sk->fam->d.k_bits <= 20 && fire_and_forget_ok(sk, n);
+                     (gather_env == 2 || (sk->fam->d.k_bits <= 16 && n * sk->fam->d.tables >= (16ull << 20))) &&
+                     sk->fam->d.k_bits <= 16 && fire_and_forget_ok(sk, n);
   sk->insert_deferred = false;
   AceSketch::GraphKey key;
   key.x = x;
@@ -1008,9 +1000,9 @@ ace_status batch_detect(AceSketch* sk, const void* x, int dtype, uint64_t n, uin
   key.build = build;
   key.ff = build ? (fire_and_forget_ok(sk, n) ? 1 : 0) : 2;
   key.stream = sk->stream;
-  const DevBuf* bufs[13] = {&sk->ids, &sk->sums, &sk->stage, &sk->flags, &sk->scores, &sk->demand, &sk->near,
-                            &sk->overflow, &sk->x16, &sk->rowthr, &sk->segc, &sk->gbuf, &sk->lomask};
-  for (int i = 0; i < 13; ++i) key.bufs[i] = bufs[i]->p;
+  const DevBuf* bufs[12] = {&sk->ids, &sk->sums, &sk->stage, &sk->flags, &sk->scores, &sk->demand, &sk->near,
+                            &sk->overflow, &sk->x16, &sk->rowthr, &sk->segc, &sk->lomask};
+  for (int i = 0; i < 12; ++i) key.bufs[i] = bufs[i]->p;
   static int graphs_env = -2;
   if (graphs_env == -2) {
     const char* e = getenv("ACE_GRAPHS");

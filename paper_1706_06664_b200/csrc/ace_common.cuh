@@ -23,6 +23,7 @@ struct DevState {
   unsigned long long near_count;     // tc path: near-tie items pushed
   unsigned long long near_overflow;  // tc path: list overflowed (rows rechecked in full)
   unsigned long long batch_sum;      // stream: sum of the batch's pre-insert S_i
+  unsigned int ticket_a, ticket_b;   // detect tail: blocks done with the score / flag phases
   unsigned long long underflow;  // remove: counters that would go negative
   int saturated;
   int replayed;

@@ -11,6 +11,9 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
+
+#include <algorithm>
 
 #include "ace_kernels.cuh"
 
@@ -574,35 +577,18 @@ __global__ void __launch_bounds__(1024) apply_ids_smem_kernel(const uint32_t* __
   }
 }
 
-// build_sketch + detect_batch over the same rows, fused: phase 1 is
-// apply_ids_smem_kernel<false> (shared histograms, RED merge); after a grid
-// barrier every block stages the FINAL counts of its (table, part) into shared
-// memory and replaces each of its ids by that count (gathers from shared
-// memory instead of random L2 gathers), and the block whose range holds a
-// table's first row adds that (table, part)'s sum of squares to T.
-// score_kernel then sums the counts per row (counters == nullptr).
-// gout == ids when the table is one part (each position is read and written
-// by the same thread); with several parts a separate buffer (the partner
-// block still reads the ids).  Cooperative launch, one block per SM.
-__global__ void __launch_bounds__(1024) apply_gather_kernel(const uint32_t* ids, uint32_t* gout, uint64_t n,
-                                                            uint32_t tables, uint32_t k_bits, uint32_t part_bits,
-                                                            uint64_t per, uint32_t* counters, DevState* st) {
-  extern __shared__ uint32_t hist[];
-  __shared__ unsigned long long blk;
+// Phase 1 of the fused passes: counts of the block's id range [i0, i1)
+// (flattened table-major ids), bins of `part` only, merged into `counters`
+// with fire-and-forget REDs (32-bit, unsaturable sketches).
+__device__ void count_range(const uint32_t* ids, uint64_t n, uint32_t k_bits, uint32_t part_bits, uint32_t part,
+                            uint64_t i0, uint64_t i1, uint32_t* counters, uint32_t* hist, DevState* st) {
   const uint32_t nb = 1u << part_bits;
   const uint32_t pshift = k_bits - part_bits;
-  const uint32_t part = blockIdx.x & ((1u << pshift) - 1u);
-  const uint64_t total = n * tables;
-  const uint64_t i0 = static_cast<uint64_t>(blockIdx.x >> pshift) * per;
-  const uint64_t i1 = min(total, i0 + per);
-  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
-  if (threadIdx.x == 0) blk = 0ull;
   const int lane = threadIdx.x & 31;
   unsigned long long dT = 0ull;
   constexpr int kDepth = 8;
   constexpr int kVec = 4;  // 16-byte vectors per thread in flight (one-part path)
   const uint32_t step = blockDim.x * kDepth;
-  // ---- phase 1: counts
   for (uint64_t seg = i0; seg < i1;) {
     const uint64_t t = seg / n;
     const uint64_t seg_end = min(i1, (t + 1) * n);
@@ -646,61 +632,86 @@ __global__ void __launch_bounds__(1024) apply_gather_kernel(const uint32_t* ids,
                       st, dT);
     seg = seg_end;
   }
-  __threadfence();
-  cg::this_grid().sync();
-  // ---- phase 2: final counts per id
-  for (uint64_t seg = i0; seg < i1;) {
+}
+
+// Phase 2 of the fused passes: ids [g0, g1) replaced in place by their
+// final counts, looked up in a shared-memory copy of each table (staged once
+// per table segment).  TS = uint32_t holds a table of 2^K <= 2^15 counts;
+// TS = uint16_t holds 2^16 counts saturated at 0xffff, whose exact value is
+// then read from global memory.  The block whose range holds a table's first
+// row returns that table's sum of squared counts (T = sum c^2).
+template <typename TS>
+__device__ unsigned long long gather_range(uint32_t* ids, uint64_t n, uint32_t k_bits, uint64_t g0, uint64_t g1,
+                                           const uint32_t* counters, TS* tab) {
+  constexpr uint32_t kMax = sizeof(TS) == 2 ? 0xffffu : 0xffffffffu;
+  constexpr int kVec = 8;
+  const uint32_t nb = 1u << k_bits;
+  unsigned long long dT = 0ull;
+  for (uint64_t seg = g0; seg < g1;) {
     const uint64_t t = seg / n;
-    const uint64_t seg_end = min(i1, (t + 1) * n);
-    const uint32_t* ct = counters + (t << k_bits) + (static_cast<uint64_t>(part) << part_bits);
+    const uint64_t seg_end = min(g1, (t + 1) * n);
+    const uint32_t* ct = counters + (t << k_bits);
+    const bool owner = g0 <= t * n && t * n < g1;
     __syncthreads();
-    const bool owner = i0 <= t * n && t * n < i1;  // this block's range holds the table's first row
-    for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
-      const uint32_t c = __ldcg(ct + b);
-      hist[b] = c;
-      if (owner) dT += static_cast<unsigned long long>(c) * c;
-    }
-    __syncthreads();
-    if (pshift == 0) {
-      // one part (gout == ids): 16-byte loads and stores, scalar head / tail
-      const uint64_t a = min(seg_end, static_cast<uint64_t>((seg + 3u) & ~static_cast<uint64_t>(3))), nv = (seg_end - a) >> 2, z = a + (nv << 2);
-      for (uint64_t i = seg + threadIdx.x; i < a; i += blockDim.x) gout[i] = hist[ids[i]];
-      for (uint64_t i = z + threadIdx.x; i < seg_end; i += blockDim.x) gout[i] = hist[ids[i]];
-      const uint4* v4 = reinterpret_cast<const uint4*>(ids + a);
-      uint4* o4 = reinterpret_cast<uint4*>(gout + a);
-      for (uint64_t base = 0; base < nv; base += kVec * blockDim.x) {
-        uint4 q[kVec];
+    // stage the table: 16-byte loads, kStage per thread in flight
+    {
+      constexpr int kStage = 8;
+      const uint32_t nv4 = nb >> 2;
+      const uint4* c4 = reinterpret_cast<const uint4*>(ct);
+      for (uint32_t b0 = threadIdx.x; b0 < nv4; b0 += kStage * blockDim.x) {
+        uint4 c[kStage];
 #pragma unroll
-        for (int u = 0; u < kVec; ++u) q[u] = v4[min(base + u * blockDim.x + threadIdx.x, nv - 1u)];
+        for (int u = 0; u < kStage; ++u) c[u] = __ldcg(c4 + min(b0 + u * blockDim.x, nv4 - 1u));
 #pragma unroll
-        for (int u = 0; u < kVec; ++u) {
-          const uint64_t j = base + u * blockDim.x + threadIdx.x;
-          if (j < nv) o4[j] = make_uint4(hist[q[u].x], hist[q[u].y], hist[q[u].z], hist[q[u].w]);
+        for (int u = 0; u < kStage; ++u) {
+          const uint32_t b = b0 + u * blockDim.x;
+          if (b < nv4) {
+            const uint32_t v[4] = {c[u].x, c[u].y, c[u].z, c[u].w};
+            TS o[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              o[e] = static_cast<TS>(v[e] < kMax ? v[e] : kMax);
+              if (owner) dT += static_cast<unsigned long long>(v[e]) * v[e];
+            }
+            if constexpr (sizeof(TS) == 4)
+              *reinterpret_cast<uint4*>(tab + 4u * b) = make_uint4(o[0], o[1], o[2], o[3]);
+            else
+              *reinterpret_cast<uint2*>(tab + 4u * b) =
+                  make_uint2(static_cast<uint32_t>(o[0]) | (static_cast<uint32_t>(o[1]) << 16),
+                             static_cast<uint32_t>(o[2]) | (static_cast<uint32_t>(o[3]) << 16));
+          }
         }
       }
-    } else {
-      for (uint64_t base = seg; base < seg_end; base += step) {
-        const uint32_t len = static_cast<uint32_t>(min(seg_end - base, static_cast<uint64_t>(step)));
-        const uint32_t* src = ids + base;
-        uint32_t idv[kDepth];
+      for (uint32_t b = 4u * nv4 + threadIdx.x; b < nb; b += blockDim.x) {  // K < 2
+        const uint32_t c = __ldcg(ct + b);
+        tab[b] = static_cast<TS>(c < kMax ? c : kMax);
+        if (owner) dT += static_cast<unsigned long long>(c) * c;
+      }
+    }
+    __syncthreads();
+    auto look = [&](uint32_t id) -> uint32_t {
+      const uint32_t v = tab[id];
+      if constexpr (sizeof(TS) == 2) return v == kMax ? __ldcg(ct + id) : v;
+      return v;
+    };
+    const uint64_t a = min(seg_end, static_cast<uint64_t>((seg + 3u) & ~static_cast<uint64_t>(3)));
+    const uint64_t nv = (seg_end - a) >> 2, z = a + (nv << 2);
+    for (uint64_t i = seg + threadIdx.x; i < a; i += blockDim.x) ids[i] = look(ids[i]);
+    for (uint64_t i = z + threadIdx.x; i < seg_end; i += blockDim.x) ids[i] = look(ids[i]);
+    uint4* v4 = reinterpret_cast<uint4*>(ids + a);
+    for (uint64_t base = 0; base < nv; base += kVec * blockDim.x) {
+      uint4 q[kVec];
 #pragma unroll
-        for (int u = 0; u < kDepth; ++u) idv[u] = src[min(u * blockDim.x + threadIdx.x, len - 1u)];
+      for (int u = 0; u < kVec; ++u) q[u] = v4[min(base + u * blockDim.x + threadIdx.x, nv - 1u)];
 #pragma unroll
-        for (int u = 0; u < kDepth; ++u) {
-          const uint32_t i = u * blockDim.x + threadIdx.x;
-          if (i < len && (idv[u] >> part_bits) == part) gout[base + i] = hist[idv[u] & (nb - 1u)];
-        }
+      for (int u = 0; u < kVec; ++u) {
+        const uint64_t j = base + u * blockDim.x + threadIdx.x;
+        if (j < nv) v4[j] = make_uint4(look(q[u].x), look(q[u].y), look(q[u].z), look(q[u].w));
       }
     }
     seg = seg_end;
   }
-  dT = warp_sum_u64(dT);
-  if (lane == 0 && dT) atomicAdd(&blk, dT);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (blk) atomicAdd(&st->T, blk);
-    if (blockIdx.x == 0) atomicAdd(&st->n, n);
-  }
+  return dT;
 }
 
 // Noisy (private) hashing, srp.cpp:93-104: for point i, table t0+tt, bit b
@@ -771,13 +782,54 @@ __global__ void cap_kernel(uint32_t* counters, uint64_t num, uint32_t cap, DevSt
 
 // ---- scoring -----------------------------------------------------------------
 
-__global__ void score_kernel(const uint32_t* __restrict__ ids, uint64_t ids_stride, uint64_t n,
-                             uint32_t tables, uint32_t k_bits, const uint32_t* __restrict__ counters,
-                             uint64_t* __restrict__ sums, double* __restrict__ scores,
-                             DevState* st) {
+// Rows first, first + stride, ... of the batch: S_i (integer), optional
+// sums / scores, and the block's exact sum S and sum S^2 (u128) added to st
+// by thread 0.  Called by every thread of the block (block-wide reduction).
+__device__ void score_rows(const uint32_t* __restrict__ ids, uint64_t ids_stride, uint64_t n, uint32_t tables,
+                           uint32_t k_bits, const uint32_t* __restrict__ counters, uint64_t* __restrict__ sums,
+                           double* __restrict__ scores, DevState* st, uint64_t first, uint64_t stride) {
   unsigned long long acc = 0ull, sq_lo = 0ull, sq_hi = 0ull;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+  auto account = [&](uint64_t i, unsigned long long S) {
+    if (sums) sums[i] = S;
+    if (scores) scores[i] = __ddiv_rn(static_cast<double>(S), static_cast<double>(tables));
+    acc += S;
+    const unsigned long long lo = S * S, hi = __umul64hi(S, S);
+    const unsigned long long nlo = sq_lo + lo;
+    sq_hi += hi + (nlo < sq_lo ? 1ull : 0ull);
+    sq_lo = nlo;
+  };
+  if (!counters && ids_stride % 4 == 0 && (reinterpret_cast<uintptr_t>(ids) & 15) == 0) {
+    // counts in place of the ids: four rows per thread, 16-byte loads of 8
+    // tables in flight (128 B per thread)
+    const uint64_t n4 = n / 4;
+    for (uint64_t g = first; g < n4; g += stride) {
+      unsigned long long S[4] = {0ull, 0ull, 0ull, 0ull};
+      uint32_t t = 0;
+      for (; t + 8 <= tables; t += 8) {
+        uint4 c[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) c[u] = __ldcs(reinterpret_cast<const uint4*>(ids + (uint64_t)(t + u) * ids_stride) + g);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          S[0] += c[u].x;
+          S[1] += c[u].y;
+          S[2] += c[u].z;
+          S[3] += c[u].w;
+        }
+      }
+      for (; t < tables; ++t) {
+        const uint4 c = __ldcs(reinterpret_cast<const uint4*>(ids + (uint64_t)t * ids_stride) + g);
+        S[0] += c.x;
+        S[1] += c.y;
+        S[2] += c.z;
+        S[3] += c.w;
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) account(4 * g + e, S[e]);
+    }
+    first += 4 * n4;  // the last n % 4 rows: scalar
+  }
+  for (uint64_t i = first; i < n; i += stride) {
     unsigned long long S = 0ull;
     uint32_t t = 0;
     for (; t + 8 <= tables; t += 8) {
@@ -798,13 +850,7 @@ __global__ void score_kernel(const uint32_t* __restrict__ ids, uint64_t ids_stri
       const uint32_t b = ids[(uint64_t)t * ids_stride + i];
       S += counters ? counters[((uint64_t)t << k_bits) + b] : b;
     }
-    if (sums) sums[i] = S;
-    if (scores) scores[i] = __ddiv_rn(static_cast<double>(S), static_cast<double>(tables));
-    acc += S;
-    const unsigned long long lo = S * S, hi = __umul64hi(S, S);
-    const unsigned long long nlo = sq_lo + lo;
-    sq_hi += hi + (nlo < sq_lo ? 1ull : 0ull);
-    sq_lo = nlo;
+    account(i, S);
   }
   // warp reductions, then thread 0 folds the warps and issues the global atomics
   __shared__ unsigned long long w_s[32], w_qlo[32], w_qhi[32];
@@ -828,6 +874,14 @@ __global__ void score_kernel(const uint32_t* __restrict__ ids, uint64_t ids_stri
     atomic_add_u128(&st->sum_lo, &st->sum_hi, ts, 0ull);
     atomic_add_u128(&st->sq_lo, &st->sq_hi, tlo, thi);
   }
+}
+
+__global__ void score_kernel(const uint32_t* __restrict__ ids, uint64_t ids_stride, uint64_t n,
+                             uint32_t tables, uint32_t k_bits, const uint32_t* __restrict__ counters,
+                             uint64_t* __restrict__ sums, double* __restrict__ scores,
+                             DevState* st) {
+  score_rows(ids, ids_stride, n, tables, k_bits, counters, sums, scores, st,
+             static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x, static_cast<uint64_t>(gridDim.x) * blockDim.x);
 }
 
 // ---- detect_batch threshold (1 thread) -------------------------------------
@@ -904,11 +958,13 @@ __device__ U192 isqrt192(U192 v) {
   return res;
 }
 
-__global__ void finalize_batch_kernel(uint64_t n, uint32_t tables, DevState* st) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const unsigned long long sum = st->sum_lo;  // sum_hi == 0 checked on host
+// One thread.  The sums are read through volatile loads: in the fused tail
+// they were accumulated by other blocks' atomics (L2) during this launch.
+__device__ void finalize_batch_dev(uint64_t n, uint32_t tables, DevState* st) {
+  const volatile DevState* vs = st;
+  const unsigned long long sum = vs->sum_lo;  // sum_hi == 0 checked on host
   // V = N * sum S^2 - (sum S)^2  (exact, >= 0)
-  const U192 a = mul_u128_u64(st->sq_lo, st->sq_hi, n);
+  const U192 a = mul_u128_u64(vs->sq_lo, vs->sq_hi, n);
   U192 b;
   b.w[0] = sum * sum;
   b.w[1] = __umul64hi(sum, sum);
@@ -963,18 +1019,17 @@ __global__ void finalize_batch_kernel(uint64_t n, uint32_t tables, DevState* st)
   st->ambiguous = 0;
 }
 
-__global__ void flags_kernel(const uint64_t* __restrict__ sums, uint64_t n,
-                             uint32_t* __restrict__ flag_bits, DevState* st, int pass) {
-  if (pass == 1 && !st->replayed) return;
-  const long long cut = st->s_cut, lo = st->s_lo, hi = st->s_hi;
+__device__ void flags_rows(const uint64_t* __restrict__ sums, uint64_t n, uint32_t* __restrict__ flag_bits,
+                           DevState* st, int pass, uint64_t bi, uint64_t nb) {
+  const volatile DevState* vs = st;
+  const long long cut = vs->s_cut, lo = vs->s_lo, hi = vs->s_hi;
   unsigned long long rep = 0, amb = 0;
   const uint64_t words = (n + 31) / 32;
-  for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x; base < words * 32;
-       base += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+  for (uint64_t base = bi * blockDim.x; base < words * 32; base += nb * blockDim.x) {
     const uint64_t i = base + threadIdx.x;
     bool f = false;
     if (i < n) {
-      const long long S = static_cast<long long>(sums[i]);
+      const long long S = static_cast<long long>(__ldcg(sums + i));
       f = S <= cut;
       if (pass == 0 && S >= lo && S <= hi) ++amb;
     }
@@ -993,21 +1048,21 @@ __global__ void flags_kernel(const uint64_t* __restrict__ sums, uint64_t n,
 }
 
 // Sequential replay of detect.cpp:44-50 in binary64 (one block, thread 0 folds).
-__global__ void replay_kernel(const uint64_t* __restrict__ sums, uint64_t n, uint32_t tables,
-                              DevState* st) {
-  if (st->ambiguous == 0) return;
-  __shared__ double buf[1024];
+// One block (all threads), buf: blockDim.x doubles of shared memory.
+__device__ void replay_dev(const uint64_t* __restrict__ sums, uint64_t n, uint32_t tables, DevState* st,
+                           double* buf) {
   __shared__ double s_sum, s_mean, s_sq;
   const double L = static_cast<double>(tables);
+  const uint32_t B = blockDim.x;
   if (threadIdx.x == 0) s_sum = 0.0;
-  for (uint64_t base = 0; base < n; base += 1024) {
+  for (uint64_t base = 0; base < n; base += B) {
     __syncthreads();
     const uint64_t i = base + threadIdx.x;
-    if (i < n) buf[threadIdx.x] = __ddiv_rn(static_cast<double>(sums[i]), L);
+    if (i < n) buf[threadIdx.x] = __ddiv_rn(static_cast<double>(__ldcg(sums + i)), L);
     __syncthreads();
     if (threadIdx.x == 0) {
       double s = s_sum;
-      const uint64_t m = n - base < 1024 ? n - base : 1024;
+      const uint64_t m = n - base < B ? n - base : B;
       for (uint64_t j = 0; j < m; ++j) s = __dadd_rn(s, buf[j]);
       s_sum = s;
     }
@@ -1017,15 +1072,15 @@ __global__ void replay_kernel(const uint64_t* __restrict__ sums, uint64_t n, uin
     s_mean = __ddiv_rn(s_sum, static_cast<double>(n));
     s_sq = 0.0;
   }
-  for (uint64_t base = 0; base < n; base += 1024) {
+  for (uint64_t base = 0; base < n; base += B) {
     __syncthreads();
     const uint64_t i = base + threadIdx.x;
-    if (i < n) buf[threadIdx.x] = __ddiv_rn(static_cast<double>(sums[i]), L);
+    if (i < n) buf[threadIdx.x] = __ddiv_rn(static_cast<double>(__ldcg(sums + i)), L);
     __syncthreads();
     if (threadIdx.x == 0) {
       double q = s_sq;
       const double mu = s_mean;
-      const uint64_t m = n - base < 1024 ? n - base : 1024;
+      const uint64_t m = n - base < B ? n - base : B;
       for (uint64_t j = 0; j < m; ++j) {
         const double t = __dsub_rn(buf[j], mu);
         q = __dadd_rn(q, __dmul_rn(t, t));
@@ -1051,6 +1106,112 @@ __global__ void replay_kernel(const uint64_t* __restrict__ sums, uint64_t n, uin
     st->thr = thr;
     st->reported = 0;
     st->replayed = 1;
+  }
+  __syncthreads();
+}
+
+// ---- fused detect tail ------------------------------------------------------
+//
+// build_sketch's deferred insert + detect_batch in one cooperative launch
+// (estimators.cpp:79-92 then detect.cpp:12-74), phases separated by grid
+// barriers instead of kernel boundaries:
+//   gather mode (build, 32-bit, K <= 16): counts of each block's id range in
+//     a shared histogram (count_range), grid barrier, every id replaced by its
+//     final count from a shared-memory copy of its table (gather_range), grid
+//     barrier;
+//   scores: S_i summed from the counts (gather mode) or gathered from the
+//     L2-resident counters; exact sum S and sum S^2;
+//   the last block to finish the scores computes the exact threshold
+//     (finalize_batch_dev); grid barrier; flags of every row (pass 0);
+//   the last block to finish the flags replays the reference's sequential
+//     statistics when the ambiguity band is not empty, and re-flags.
+struct TailArgs {
+  uint32_t* ids;  // table-major [tables][n]: bucket ids (counts in place after the gather)
+  uint64_t n;
+  uint32_t tables, k_bits, part_bits;
+  uint64_t per;  // gather mode: ids per block range
+  uint32_t* counters;
+  int gather;
+  uint64_t* sums;
+  double* scores;
+  uint32_t* flag_bits;
+  DevState* st;
+  unsigned long long* prof;  // instrumentation: %globaltimer at the phase boundaries (block 0), or null
+};
+
+__device__ __forceinline__ void tail_stamp(const TailArgs& a, int i) {
+  if (a.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    a.prof[i] = g;
+  }
+}
+
+__global__ void __launch_bounds__(1024) detect_tail_kernel(const TailArgs a) {
+  extern __shared__ __align__(16) uint32_t hist[];  // gather: 2^min(K,15) u32 / 2^16 u16; else blockDim doubles
+  __shared__ unsigned long long blk;
+  __shared__ int last;
+  cg::grid_group grid = cg::this_grid();
+  DevState* st = a.st;
+  const int lane = threadIdx.x & 31;
+  tail_stamp(a, 0);
+  if (a.gather) {
+    const uint32_t pshift = a.k_bits - a.part_bits, parts = 1u << pshift;
+    const uint32_t part = blockIdx.x & (parts - 1u);
+    const uint64_t total = a.n * a.tables;
+    const uint64_t i0 = min(total, static_cast<uint64_t>(blockIdx.x >> pshift) * a.per);
+    const uint64_t i1 = min(total, i0 + a.per);
+    for (uint32_t b = threadIdx.x; b < (1u << a.part_bits); b += blockDim.x) hist[b] = 0u;
+    if (threadIdx.x == 0) blk = 0ull;
+    count_range(a.ids, a.n, a.k_bits, a.part_bits, part, i0, i1, a.counters, hist, st);
+    __threadfence();
+    grid.sync();
+    tail_stamp(a, 1);
+    // the range's parts split it by position for the gather (whole tables in
+    // shared memory): each id is read and rewritten by one thread
+    const uint64_t len = i1 - i0;
+    const uint64_t g0 = i0 + len * part / parts, g1 = i0 + len * (part + 1) / parts;
+    unsigned long long dT = a.k_bits <= 15
+                                ? gather_range<uint32_t>(a.ids, a.n, a.k_bits, g0, g1, a.counters, hist)
+                                : gather_range<uint16_t>(a.ids, a.n, a.k_bits, g0, g1, a.counters,
+                                                         reinterpret_cast<uint16_t*>(hist));
+    dT = warp_sum_u64(dT);
+    if (lane == 0 && dT) atomicAdd(&blk, dT);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (blk) atomicAdd(&st->T, blk);
+      if (blockIdx.x == 0) atomicAdd(&st->n, a.n);
+    }
+    __threadfence();
+    grid.sync();
+    tail_stamp(a, 2);
+  }
+  score_rows(a.ids, a.n, a.n, a.tables, a.k_bits, a.gather ? nullptr : a.counters, a.sums, a.scores, st,
+             static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x,
+             static_cast<uint64_t>(gridDim.x) * blockDim.x);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&st->ticket_a, 1u) == gridDim.x - 1u;
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    finalize_batch_dev(a.n, a.tables, st);
+  }
+  __threadfence();
+  grid.sync();
+  tail_stamp(a, 3);
+  flags_rows(a.sums, a.n, a.flag_bits, st, 0, blockIdx.x, gridDim.x);
+  tail_stamp(a, 4);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&st->ticket_b, 1u) == gridDim.x - 1u;
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    if (*reinterpret_cast<volatile unsigned long long*>(&st->ambiguous) != 0ull) {
+      replay_dev(a.sums, a.n, a.tables, st, reinterpret_cast<double*>(hist));
+      flags_rows(a.sums, a.n, a.flag_bits, st, 1, 0, 1);
+    }
   }
 }
 
@@ -1205,9 +1366,12 @@ cudaError_t launch_apply_ids(const uint32_t* ids, uint64_t n, uint32_t tables, u
   return cudaGetLastError();
 }
 
-cudaError_t launch_apply_gather(uint32_t* ids, uint32_t* gout, uint64_t n, uint32_t tables, uint32_t k_bits,
-                                uint32_t* counters, DevState* st, cudaStream_t s) {
-  if (n == 0 || k_bits > 20) return cudaErrorInvalidValue;
+unsigned long long* g_tail_prof = nullptr;
+
+cudaError_t launch_detect_tail(uint32_t* ids, uint64_t n, uint32_t tables, uint32_t k_bits, uint32_t* counters,
+                               int gather, uint64_t* sums, double* scores, uint32_t* flag_bits, DevState* st,
+                               cudaStream_t s) {
+  if (n == 0 || (gather && k_bits > 16)) return cudaErrorInvalidValue;
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -1216,27 +1380,49 @@ cudaError_t launch_apply_gather(uint32_t* ids, uint32_t* gout, uint64_t n, uint3
   }
   static bool configured = false;
   if (!configured) {
-    const cudaError_t e = cudaFuncSetAttribute(apply_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const cudaError_t e = cudaFuncSetAttribute(detect_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(sizeof(uint32_t) << 15));
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  uint32_t part_bits = k_bits < 15 ? k_bits : 15;
-  const uint32_t parts = 1u << (k_bits - part_bits);
-  const uint64_t total = n * tables;
-  uint64_t ranges = static_cast<uint64_t>(sms) / parts;
-  if (ranges < 1) ranges = 1;
-  if (ranges > total / 4096) ranges = total / 4096 > 0 ? total / 4096 : 1;
-  uint64_t per = (total + ranges - 1) / ranges;
-  const unsigned grid = static_cast<unsigned>((total + per - 1) / per) * parts;
-  const size_t smem = sizeof(uint32_t) << part_bits;
-  // T = sum c^2 is accumulated from zero by the kernel (32-bit, unsaturated)
-  cudaError_t e = cudaMemsetAsync(&st->T, 0, sizeof(unsigned long long), s);
-  if (e != cudaSuccess) return e;
-  const uint32_t* ids_c = ids;
-  void* args[] = {&ids_c, &gout, &n, &tables, &k_bits, &part_bits, &per, &counters, &st};
-  e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(apply_gather_kernel), dim3(grid), dim3(1024), args,
-                                  smem, s);
+  TailArgs a{};
+  a.ids = ids;
+  a.n = n;
+  a.tables = tables;
+  a.k_bits = k_bits;
+  a.counters = counters;
+  a.gather = gather;
+  a.sums = sums;
+  a.scores = scores;
+  a.flag_bits = flag_bits;
+  a.st = st;
+  static int prof_env = -1;
+  if (prof_env < 0) prof_env = getenv("ACE_TAIL_PROF") ? 1 : 0;
+  if (prof_env) {
+    if (!g_tail_prof) cudaMalloc(&g_tail_prof, 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(g_tail_prof, 0, 8 * sizeof(unsigned long long), s);
+    a.prof = g_tail_prof;
+  }
+  unsigned grid = static_cast<unsigned>(sms);
+  size_t smem = 1024 * sizeof(double);
+  if (gather) {
+    a.part_bits = k_bits < 15 ? k_bits : 15;
+    const uint32_t parts = 1u << (k_bits - a.part_bits);
+    const uint64_t total = n * tables;
+    uint64_t ranges = static_cast<uint64_t>(sms) / parts;
+    if (ranges < 1) ranges = 1;
+    if (ranges > total / 4096) ranges = total / 4096 > 0 ? total / 4096 : 1;
+    a.per = (total + ranges - 1) / ranges;
+    grid = static_cast<unsigned>((total + a.per - 1) / a.per) * parts;
+    smem = std::max<size_t>(smem, sizeof(uint32_t) << a.part_bits);
+    if (k_bits == 16) smem = std::max<size_t>(smem, sizeof(uint16_t) << 16);
+    // T = sum c^2 is accumulated from zero (32-bit, unsaturated)
+    const cudaError_t e = cudaMemsetAsync(&st->T, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+  }
+  void* args[] = {&a};
+  const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(detect_tail_kernel), dim3(grid),
+                                                    dim3(1024), args, smem, s);
   count_launch();
   return e;
 }
@@ -1276,26 +1462,6 @@ cudaError_t launch_score(const uint32_t* ids, uint64_t ids_stride, uint64_t n, u
   if (n == 0) return cudaSuccess;
   score_kernel<<<grid_for(n, 256), 256, 0, s>>>(ids, ids_stride, n, tables, k_bits, counters, sums,
                                                 scores, st);
-  count_launch();
-  return cudaGetLastError();
-}
-
-cudaError_t launch_finalize_batch(uint64_t n, uint32_t tables, DevState* st, cudaStream_t s) {
-  finalize_batch_kernel<<<1, 32, 0, s>>>(n, tables, st);
-  count_launch();
-  return cudaGetLastError();
-}
-
-cudaError_t launch_flags(const uint64_t* sums, uint64_t n, uint32_t* flag_bits, DevState* st,
-                         int pass, cudaStream_t s) {
-  flags_kernel<<<grid_for(n, 256), 256, 0, s>>>(sums, n, flag_bits, st, pass);
-  count_launch();
-  return cudaGetLastError();
-}
-
-cudaError_t launch_replay(const uint64_t* sums, uint64_t n, uint32_t tables, DevState* st,
-                          cudaStream_t s) {
-  replay_kernel<<<1, 1024, 0, s>>>(sums, n, tables, st);
   count_launch();
   return cudaGetLastError();
 }

@@ -32,11 +32,14 @@ cudaError_t launch_apply_ids(const uint32_t* ids, uint64_t n, uint32_t tables,
                              uint32_t k_bits, uint32_t* counters, uint32_t cap,
                              int sign, DevState* st, cudaStream_t s, bool track_t = true,
                              uint64_t ids_stride = 0);  // 0: n
-// build + detect over the same rows (32-bit, unsaturable, K <= 20): counts
-// into `counters` (T = sum c^2 recomputed) and every id replaced by its final
-// count in `gout` (== ids when K <= 15); score with counters == nullptr.
-cudaError_t launch_apply_gather(uint32_t* ids, uint32_t* gout, uint64_t n, uint32_t tables, uint32_t k_bits,
-                                uint32_t* counters, DevState* st, cudaStream_t s);
+// build (deferred insert, gather = 1: 32-bit, K <= 16) + detect_batch tail in
+// one cooperative launch: counts, ids replaced by final counts, scores, exact
+// threshold, flags, sequential replay when ambiguous.  gather = 0: scores
+// gathered from the final counters, then threshold and flags.
+cudaError_t launch_detect_tail(uint32_t* ids, uint64_t n, uint32_t tables, uint32_t k_bits, uint32_t* counters,
+                               int gather, uint64_t* sums, double* scores, uint32_t* flag_bits, DevState* st,
+                               cudaStream_t s);
+extern unsigned long long* g_tail_prof;  // ACE_TAIL_PROF=1: phase timestamps of the last tail launch
 // Noisy hashing (srp.cpp:93-104), exact: tables [t0, t0+nt), bits [b0, b0+nb)
 // of each; noise[(i*nt + tt)*nb + (b-b0)] pre-scaled terms in tick order.
 cudaError_t launch_noisy_buckets(const void* x, int x_f64, uint64_t n, uint64_t ld, uint64_t dim, const double* w64,
@@ -57,17 +60,6 @@ cudaError_t launch_cap(uint32_t* counters, uint64_t num, uint32_t cap, DevState*
 cudaError_t launch_score(const uint32_t* ids, uint64_t ids_stride, uint64_t n,
                          uint32_t tables, uint32_t k_bits, const uint32_t* counters,
                          uint64_t* sums, double* scores, DevState* st, cudaStream_t s);
-
-// detect_batch threshold: exact integer cut + rigorous ambiguity band.
-cudaError_t launch_finalize_batch(uint64_t n, uint32_t tables, DevState* st,
-                                  cudaStream_t s);
-// flags from sums (pass 0: exact cut, counts ambiguity; pass 1: only if
-// the sequential replay ran).
-cudaError_t launch_flags(const uint64_t* sums, uint64_t n, uint32_t* flag_bits,
-                         DevState* st, int pass, cudaStream_t s);
-// Sequential replay of detect.cpp:44-50 when the band is not empty.
-cudaError_t launch_replay(const uint64_t* sums, uint64_t n, uint32_t tables,
-                          DevState* st, cudaStream_t s);
 
 // Streaming: score against current counts, flag score <= mean - alpha.
 cudaError_t launch_stream_score(const uint32_t* ids, uint64_t n, uint32_t tables,
