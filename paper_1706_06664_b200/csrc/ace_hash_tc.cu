@@ -1147,18 +1147,21 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
               if (g2 == 1u && !two) break;
               const uint32_t cc = c0 + 32u * g2;
               const uint32_t* vv = v + 32 * g2;
-              uint32_t n4[4] = {0u, 0u, 0u, 0u}, m4[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+              // near-tie test on |v| as a float min (FMNMX3 with |.| operands: half an
+              // instruction per column); NaN (non-finite rows, thr = inf) fails `mn > thr`
+              uint32_t n4[4] = {0u, 0u, 0u, 0u};
+              float m4[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
 #pragma unroll
               for (int jj = 0; jj < 8; ++jj)
 #pragma unroll
                 for (int gq = 0; gq < 4; ++gq) {
                   n4[gq] = (n4[gq] << 1) | (vv[gq * 8 + jj] >> 31);
-                  m4[gq] = min(m4[gq], vv[gq * 8 + jj] << 1);
+                  m4[gq] = fminf(m4[gq], fabsf(__uint_as_float(vv[gq * 8 + jj])));
                 }
               const uint32_t neg = (n4[0] << 24) | (n4[1] << 16) | (n4[2] << 8) | n4[3];
-              const uint32_t mn = min(min(m4[0], m4[1]), min(m4[2], m4[3]));
+              const float mn = fminf(fminf(m4[0], m4[1]), fminf(m4[2], m4[3]));
               // columns past `used` (padding / stale) are masked here, off the hot path
-              if (!zero_row && valid && mn <= thr_u && cc < hused) {
+              if (!zero_row && valid && !(mn > thr) && cc < hused) {
                 const uint32_t ncol = min(32u, hused - cc);
                 uint32_t nm = 0u;
 #pragma unroll
@@ -1302,18 +1305,21 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
                 for (uint32_t g2 = 0; g2 < 2; ++g2) {
                   const uint32_t cc = c0 + 32u * g2;
                   const uint32_t* vv = v + 32 * g2;
-                  uint32_t n4[4] = {0u, 0u, 0u, 0u}, m4[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+                  // near-tie test on |v| as a float min (FMNMX3 with |.| operands: half an
+                  // instruction per column); NaN (non-finite rows, thr = inf) fails `mn > thr`
+                  uint32_t n4[4] = {0u, 0u, 0u, 0u};
+                  float m4[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
 #pragma unroll
                   for (int jj = 0; jj < 8; ++jj)
 #pragma unroll
                     for (int gq = 0; gq < 4; ++gq) {
                       n4[gq] = (n4[gq] << 1) | (vv[gq * 8 + jj] >> 31);
-                      m4[gq] = min(m4[gq], vv[gq * 8 + jj] << 1);
+                      m4[gq] = fminf(m4[gq], fabsf(__uint_as_float(vv[gq * 8 + jj])));
                     }
                   const uint32_t neg = (n4[0] << 24) | (n4[1] << 16) | (n4[2] << 8) | n4[3];
-                  const uint32_t mn = min(min(m4[0], m4[1]), min(m4[2], m4[3]));
+                  const float mn = fminf(fminf(m4[0], m4[1]), fminf(m4[2], m4[3]));
                   // columns past `used` (padding / stale) are masked here, off the hot path
-                  if (!zero_row && valid && mn <= thr_u && cc < used) {
+                  if (!zero_row && valid && !(mn > thr) && cc < used) {
                     const uint32_t ncol = min(32u, used - cc);
                     uint32_t nm = 0u;
 #pragma unroll
