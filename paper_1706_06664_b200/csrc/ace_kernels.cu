@@ -782,6 +782,32 @@ __global__ void cap_kernel(uint32_t* counters, uint64_t num, uint32_t cap, DevSt
 
 // ---- scoring -----------------------------------------------------------------
 
+// S = sum_t counters[t * 2^K + ids[t * stride + i]] (sketch.cpp:108-116):
+// ids in groups of G, the next group's ids loaded while the current group's
+// counters are gathered (two dependent L2 round trips per group otherwise).
+template <uint32_t G>
+__device__ __forceinline__ unsigned long long gather_sum(const uint32_t* __restrict__ ids, uint64_t stride, uint64_t i,
+                                                         uint32_t tables, uint32_t k_bits,
+                                                         const uint32_t* __restrict__ counters) {
+  unsigned long long S = 0ull;
+  uint32_t b[G];
+#pragma unroll
+  for (uint32_t u = 0; u < G; ++u) b[u] = u < tables ? __ldg(ids + (uint64_t)u * stride + i) : 0u;
+  for (uint32_t t = 0; t < tables; t += G) {
+    uint32_t c[G], nb[G];
+#pragma unroll
+    for (uint32_t u = 0; u < G; ++u) c[u] = t + u < tables ? __ldg(counters + ((uint64_t)(t + u) << k_bits) + b[u]) : 0u;
+#pragma unroll
+    for (uint32_t u = 0; u < G; ++u) nb[u] = t + G + u < tables ? __ldg(ids + (uint64_t)(t + G + u) * stride + i) : 0u;
+#pragma unroll
+    for (uint32_t u = 0; u < G; ++u) {
+      S += c[u];
+      b[u] = nb[u];
+    }
+  }
+  return S;
+}
+
 // Rows first, first + stride, ... of the batch: S_i (integer), optional
 // sums / scores, and the block's exact sum S and sum S^2 (u128) added to st
 // by thread 0.  Called by every thread of the block (block-wide reduction).
@@ -830,26 +856,21 @@ __device__ void score_rows(const uint32_t* __restrict__ ids, uint64_t ids_stride
     first += 4 * n4;  // the last n % 4 rows: scalar
   }
   for (uint64_t i = first; i < n; i += stride) {
+    if (counters) {
+      account(i, gather_sum<8>(ids, ids_stride, i, tables, k_bits, counters));  // (64-register kernel)
+      continue;
+    }
+    // the ids were replaced by their final counts (detect_tail_kernel gather)
     unsigned long long S = 0ull;
     uint32_t t = 0;
     for (; t + 8 <= tables; t += 8) {
-      uint32_t b[8], c[8];
+      uint32_t c[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) b[u] = ids[(uint64_t)(t + u) * ids_stride + i];
-      if (counters) {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) c[u] = counters[((uint64_t)(t + u) << k_bits) + b[u]];
-      } else {  // the ids were replaced by their final counts (apply_gather_kernel)
-#pragma unroll
-        for (int u = 0; u < 8; ++u) c[u] = b[u];
-      }
+      for (int u = 0; u < 8; ++u) c[u] = __ldcg(ids + (uint64_t)(t + u) * ids_stride + i);
 #pragma unroll
       for (int u = 0; u < 8; ++u) S += c[u];
     }
-    for (; t < tables; ++t) {
-      const uint32_t b = ids[(uint64_t)t * ids_stride + i];
-      S += counters ? counters[((uint64_t)t << k_bits) + b] : b;
-    }
+    for (; t < tables; ++t) S += __ldcg(ids + (uint64_t)t * ids_stride + i);
     account(i, S);
   }
   // warp reductions, then thread 0 folds the warps and issues the global atomics
@@ -1252,18 +1273,7 @@ __global__ void stream_score_kernel(const uint32_t* __restrict__ ids, uint64_t n
     const uint64_t i = base + threadIdx.x;
     bool f = false;
     if (i < n) {
-      unsigned long long S = 0ull;
-      uint32_t t = 0;
-      for (; t + 8 <= tables; t += 8) {
-        uint32_t b[8], c[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) b[u] = ids[(uint64_t)(t + u) * ids_stride + i];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) c[u] = counters[((uint64_t)(t + u) << k_bits) + b[u]];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) S += c[u];
-      }
-      for (; t < tables; ++t) S += counters[((uint64_t)t << k_bits) + ids[(uint64_t)t * ids_stride + i]];
+      const unsigned long long S = gather_sum<16>(ids, ids_stride, i, tables, k_bits, counters);
       bsum += S;
       const double sc = __ddiv_rn(static_cast<double>(S), L);
       if (scores) scores[i] = sc;
