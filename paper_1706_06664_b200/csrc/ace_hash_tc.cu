@@ -284,6 +284,17 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uin
       "}\n" ::"r"(tmem_d),
       "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate));
 }
+// A and B both from shared memory (K-major SW128 descriptors), one CTA.
+__device__ __forceinline__ void mma_f16_ss(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
 // Commit: the barrier at this offset in every CTA of the pair gets one arrival
 // once all earlier tcgen05 operations of the issuing thread have completed.
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -1491,6 +1502,9 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
 // bound at (12 kKsSc + nchunks + 16) ulp instead of growing with d, so near
 // ties stay rare; they are rechecked by recheck_segs_kernel afterwards.
 
+#ifndef ACE_KS_TS
+#define ACE_KS_TS 0  // K-streamed MMAs: 1 = A chunks copied into TMEM (TS), 0 = A from shared memory (SS)
+#endif
 constexpr uint32_t kKsSc = 2;                  // K chunks per accumulation pass
 constexpr uint32_t kKsSlot = 4u * kBlockBytes;  // ring slot: A chunk (hi | lo) + W chunk (hi | lo)
 constexpr uint32_t kKsSlots = 3;
@@ -1563,9 +1577,11 @@ __global__ void __launch_bounds__(kKsThreads, 1) hash_tck_kernel(const TcArgs a)
       }
     }
   } else if (warp == 1) {
-    // ---- MMA issuer: A chunk -> TMEM (double-buffered), 12 TS MMAs per K chunk
+    // ---- MMA issuer: 12 MMAs per K chunk (SS, or TS with the A chunk copied
+    // into a double-buffered TMEM region)
     uint32_t s = 0, ph = 0, ab = 0, abph = 0;
-    const uint32_t ta = tmem_base + 256u;  // A buffers: [2][hi 32 | lo 32 columns]
+    const uint32_t ta = tmem_base + 256u;  // TS: A buffers [2][hi 32 | lo 32 columns]
+    (void)ta;
     const uint32_t idesc = idesc_f16(128u);
     for (uint64_t it = 0; it < iters; ++it)
         for (uint32_t c = 0; c < nch; ++c) {
@@ -1578,13 +1594,14 @@ __global__ void __launch_bounds__(kKsThreads, 1) hash_tck_kernel(const TcArgs a)
             for (uint32_t kc = k0; kc < k1; ++kc) {
               mbar_wait(&bar_full[ss], pp);
               const uint32_t sa = smem_u32(base + static_cast<size_t>(ss) * kKsSlot);
+              const uint64_t dbh = sw128_desc(sa + 2u * kBlockBytes), dbl = sw128_desc(sa + 3u * kBlockBytes);
+#if ACE_KS_TS
               const uint32_t tb = ta + (kc & 1u) * 64u;
 #pragma unroll
               for (uint32_t kk = 0; kk < 4; ++kk) {
                 tmem_cp_128x256b(tb + kk * 8u, sw128_desc(sa + kk * 32u));
                 tmem_cp_128x256b(tb + 32u + kk * 8u, sw128_desc(sa + kBlockBytes + kk * 32u));
               }
-              const uint64_t dbh = sw128_desc(sa + 2u * kBlockBytes), dbl = sw128_desc(sa + 3u * kBlockBytes);
 #pragma unroll
               for (uint32_t kk = 0; kk < 4; ++kk) {
                 const uint64_t off = kk * 2u;
@@ -1592,6 +1609,17 @@ __global__ void __launch_bounds__(kKsThreads, 1) hash_tck_kernel(const TcArgs a)
                 mma_f16_ts(dt, tb + 32u + kk * 8u, dbh + off, idesc, 1u);
                 mma_f16_ts(dt, tb + kk * 8u, dbl + off, idesc, 1u);
               }
+#else
+              // A read from the slot by the MMAs themselves (no copy into TMEM)
+              const uint64_t dah = sw128_desc(sa), dal = sw128_desc(sa + kBlockBytes);
+#pragma unroll
+              for (uint32_t kk = 0; kk < 4; ++kk) {
+                const uint64_t off = kk * 2u;
+                mma_f16_ss(dt, dah + off, dbh + off, idesc, (kc != k0 || kk != 0u) ? 1u : 0u);
+                mma_f16_ss(dt, dal + off, dbh + off, idesc, 1u);
+                mma_f16_ss(dt, dah + off, dbl + off, idesc, 1u);
+              }
+#endif
               mma_commit(&bar_empty[ss]);
               if (++ss == kKsSlots) {
                 ss = 0;
