@@ -284,7 +284,7 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
     t.dim = f->d.dim;
     t.k_bits = f->d.k_bits;
     t.tables = f->d.tables;
-    t.tpt = f->d.tpt;
+    t.tpt = f->tc.tpt ? f->tc.tpt : f->d.tpt;
     t.ntiles = f->tc.ntiles;
     t.nkc = f->tc.nkc;
     t.tw = f->tc.tw;

@@ -1506,18 +1506,33 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
 #define ACE_KS_TS 0  // K-streamed MMAs: 1 = A chunks copied into TMEM (TS), 0 = A from shared memory (SS)
 #endif
 constexpr uint32_t kKsSc = 2;                  // K chunks per accumulation pass
-constexpr uint32_t kKsSlot = 4u * kBlockBytes;  // ring slot: A chunk (hi | lo) + W chunk (hi | lo)
-constexpr uint32_t kKsSlots = 3;
 constexpr int kKsThreads = 320;                // producer, MMA, 8 epilogue warps
+// Direction tile width kTW (MMA N): 256 (SS MMAs, two 256-column TMEM
+// accumulators, ring of two 96 KB slots) or 128 (three 64 KB slots).  A ring
+// slot holds one A chunk (hi | lo, 2 x 16 KB) and one W chunk (hi | lo).
+template <uint32_t kTW>
+struct KsCfg {
+  static constexpr uint32_t kSlot = 2u * kBlockBytes + 2u * kTW * 128u;
+  static constexpr uint32_t kSlots = kTW == 256 ? 2u : 3u;
+  static constexpr uint32_t kCols = kTW / 2u;  // accumulator columns per epilogue warp (two per lane quarter)
+  static constexpr uint32_t kWords = kTW / 32u;
+};
 
 __host__ __device__ inline uint32_t ks_chunks(uint32_t nkc) { return (nkc + kKsSc - 1) / kKsSc; }
-__host__ inline size_t ks_smem_bytes() { return static_cast<size_t>(kKsSlots) * kKsSlot + 1024; }
+__host__ inline size_t ks_smem_bytes(uint32_t tw) {
+  return tw == 256 ? static_cast<size_t>(KsCfg<256>::kSlots) * KsCfg<256>::kSlot + 1024
+                   : static_cast<size_t>(KsCfg<128>::kSlots) * KsCfg<128>::kSlot + 1024;
+}
 
+template <uint32_t kTW>
 __global__ void __launch_bounds__(kKsThreads, 1) hash_tck_kernel(const TcArgs a) {
+  using C = KsCfg<kTW>;
+  constexpr uint32_t kKsSlot = C::kSlot, kKsSlots = C::kSlots, kCW = C::kCols;
+  static_assert(!(ACE_KS_TS && kTW != 128), "TS K-streamed MMAs need 128-direction tiles");
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t bar_full[kKsSlots], bar_empty[kKsSlots], bar_accfull[2], bar_accempty[2];
   __shared__ uint32_t tmem_base_sh;
-  __shared__ uint32_t sgbuf[2][4][kRows];  // sign words of a direction tile, by tile parity
+  __shared__ uint32_t sgbuf[2][C::kWords][kRows];  // sign words of a direction tile, by tile parity
   __shared__ uint32_t seg_n;
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1567,8 +1582,8 @@ __global__ void __launch_bounds__(kKsThreads, 1) hash_tck_kernel(const TcArgs a)
             bulk_g2s(dst, reinterpret_cast<const uint8_t*>(a.x16) + (tt * nkc + kc) * 2u * kBlockBytes,
                      2u * kBlockBytes, &bar_full[s]);
             bulk_g2s(dst + 2u * kBlockBytes,
-                     reinterpret_cast<const uint8_t*>(a.w16) + (static_cast<uint64_t>(j) * nkc + kc) * 2u * kBlockBytes,
-                     2u * kBlockBytes, &bar_full[s]);
+                     reinterpret_cast<const uint8_t*>(a.w16) + (static_cast<uint64_t>(j) * nkc + kc) * 2u * kTW * 128u,
+                     2u * kTW * 128u, &bar_full[s]);
             if (++s == kKsSlots) {
               s = 0;
               ph ^= 1u;
@@ -1582,19 +1597,19 @@ __global__ void __launch_bounds__(kKsThreads, 1) hash_tck_kernel(const TcArgs a)
     uint32_t s = 0, ph = 0, ab = 0, abph = 0;
     const uint32_t ta = tmem_base + 256u;  // TS: A buffers [2][hi 32 | lo 32 columns]
     (void)ta;
-    const uint32_t idesc = idesc_f16(128u);
+    const uint32_t idesc = idesc_f16(kTW);
     for (uint64_t it = 0; it < iters; ++it)
         for (uint32_t c = 0; c < nch; ++c) {
           mbar_wait(&bar_accempty[ab], abph ^ 1u);
           pipe_after();
           const uint32_t k0 = c * kKsSc, k1 = min(nkc, k0 + kKsSc);
-          const uint32_t dt = tmem_base + ab * 128u;
+          const uint32_t dt = tmem_base + ab * kTW;
           if (elect_one()) {
             uint32_t ss = s, pp = ph;
             for (uint32_t kc = k0; kc < k1; ++kc) {
               mbar_wait(&bar_full[ss], pp);
               const uint32_t sa = smem_u32(base + static_cast<size_t>(ss) * kKsSlot);
-              const uint64_t dbh = sw128_desc(sa + 2u * kBlockBytes), dbl = sw128_desc(sa + 3u * kBlockBytes);
+              const uint64_t dbh = sw128_desc(sa + 2u * kBlockBytes), dbl = sw128_desc(sa + 2u * kBlockBytes + kTW * 128u);
 #if ACE_KS_TS
               const uint32_t tb = ta + (kc & 1u) * 64u;
 #pragma unroll
@@ -1638,7 +1653,7 @@ __global__ void __launch_bounds__(kKsThreads, 1) hash_tck_kernel(const TcArgs a)
           if (ab == 0) abph ^= 1u;
         }
   } else {
-    // ---- epilogue (warps 2-9): two warps per lane quarter, 64 columns each
+    // ---- epilogue (warps 2-9): two warps per lane quarter, kCW columns each
     const uint32_t q = warp & 3, h = (warp - 2) >> 2;
     const uint32_t r = q * 32u + lane;
     const uint32_t kmask = (K >= 32u) ? 0xffffffffu : ((1u << K) - 1u);
@@ -1655,27 +1670,36 @@ __global__ void __launch_bounds__(kKsThreads, 1) hash_tck_kernel(const TcArgs a)
       const uint32_t t0 = j * tpt, t1 = min(a.tables, t0 + tpt);  // tables of this direction tile
       const uint32_t used = (t1 - t0) * K;
       {
-        float acc[64];
+        float acc[kCW];
 #pragma unroll
-        for (int i = 0; i < 64; ++i) acc[i] = 0.0f;
+        for (int i = 0; i < static_cast<int>(kCW); ++i) acc[i] = 0.0f;
         for (uint32_t c = 0; c < nch; ++c) {
           mbar_wait_sleepy(&bar_accfull[ab], abph, nullptr);
           pipe_after();
-          uint32_t v[64];
-          ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + ab * 128u + 64u * h, v);
-          ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + ab * 128u + 64u * h + 32u, (v + 32));
-          tmem_wait_ld();
+          // kR columns per round (kR / 32 loads in flight; 32 when the
+          // running sums take 128 registers)
+          constexpr uint32_t kR = kCW > 64u ? 32u : 64u;
 #pragma unroll
-          for (int i = 0; i < 64; ++i) acc[i] += __uint_as_float(v[i]);
+          for (uint32_t p0 = 0; p0 < kCW; p0 += kR) {
+            uint32_t v[kR];
+            const uint32_t ta = tmem_base + ((q * 32u) << 16) + ab * kTW + kCW * h + p0;
+            ACE_TMEM_LD32(ta, v);
+            if constexpr (kR == 64u) ACE_TMEM_LD32(ta + 32u, (v + 32));
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < static_cast<int>(kR); ++i) acc[p0 + i] += __uint_as_float(v[i]);
+          }
           pipe_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&bar_accempty[ab]);
           ab ^= 1u;
           if (ab == 0) abph ^= 1u;
         }
+        // sign words and near masks of all columns first (the running sums
+        // are dead before the out-of-line pushes: no registers to save)
+        uint32_t nms[kCW / 32u];
 #pragma unroll
-        for (uint32_t g2 = 0; g2 < 2; ++g2) {
-          const uint32_t cc = 64u * h + 32u * g2;
+        for (uint32_t g2 = 0; g2 < kCW / 32u; ++g2) {
           uint32_t neg = 0u, nm = 0u;
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) {
@@ -1683,13 +1707,19 @@ __global__ void __launch_bounds__(kKsThreads, 1) hash_tck_kernel(const TcArgs a)
             neg = (neg << 1) | (__float_as_uint(p) >> 31);
             nm |= ((!(fabsf(p) > thr)) ? 1u : 0u) << jj;  // NaN projections (wild rows) count as near
           }
+          nms[g2] = nm;
+          sgbuf[par][(kCW / 32u) * h + g2][r] = zero_row ? 0xffffffffu : ~neg;  // bit (31-jj) = column cc+jj >= 0
+        }
+#pragma unroll
+        for (uint32_t g2 = 0; g2 < kCW / 32u; ++g2) {
+          const uint32_t cc = kCW * h + 32u * g2;
+          uint32_t nm = nms[g2];
           if (cc < used && !zero_row && valid) {
             if (used - cc < 32u) nm &= (1u << (used - cc)) - 1u;
             if (nm)
               push_near_mask(a.st, a.near_list + blockIdx.x * seg_cap, seg_cap, &seg_n, a.overflow_rows, nm, row,
                              t0 * K + cc);
           }
-          sgbuf[par][2 * h + g2][r] = zero_row ? 0xffffffffu : ~neg;  // bit (31-jj) = column cc+jj >= 0
         }
         asm volatile("bar.sync %0, 64;" ::"r"(1u + q) : "memory");  // the quarter's two warps
         uint32_t* idp = a.ids + row;
@@ -1697,7 +1727,7 @@ __global__ void __launch_bounds__(kKsThreads, 1) hash_tck_kernel(const TcArgs a)
           const uint32_t s0 = (tt - t0) * K;  // whole tables: no straddling
           const uint32_t wi = s0 >> 5, off = s0 & 31u;
           const uint32_t hi = sgbuf[par][wi][r];
-          const uint32_t lo = wi < 3 ? sgbuf[par][wi + 1][r] : 0u;
+          const uint32_t lo = wi + 1u < C::kWords ? sgbuf[par][wi + 1][r] : 0u;
           const unsigned long long win = (static_cast<unsigned long long>(hi) << 32) | lo;
           const uint32_t bucket = static_cast<uint32_t>(win >> (64u - off - K)) & kmask;
           if (valid) idp[static_cast<uint64_t>(tt) * a.ids_ld] = bucket;
@@ -2012,24 +2042,38 @@ cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc) {
   tc->tw = tw;
   // K-streamed kernel: whole tables per direction tile (no table straddles
   // two tiles, so (point tile, direction tile) items are independent)
-  const uint32_t tpt = 128u / f.k_bits;
+  // 256-direction tiles (SS MMAs with N = 256) unless ACE_KS_TW=128
+  static int kstw_env = -1;
+  if (kstw_env < 0) {
+    const char* e = getenv("ACE_KS_TW");
+    kstw_env = e ? atoi(e) : 256;
+  }
+  const uint32_t ktw = (ACE_KS_TS || kstw_env == 128) ? 128u : 256u;
+  const uint32_t wtw = tc_kstream(nkc) ? ktw : tw;  // W tile rows
+  const uint32_t tpt = wtw / f.k_bits;
+  if (tc_kstream(nkc)) {
+    tc->tw = wtw;
+    tc->tpt = tpt;
+  }
   const uint32_t dpt = tc_kstream(nkc) ? tpt * f.k_bits : tw;
   tc->ntiles = tc_kstream(nkc) ? (f.tables + tpt - 1) / tpt : (f.rows + tw - 1) / tw;
   if (tc->ntiles > 64 && !tc_kstream(nkc)) return cudaSuccess;  // TcArgs::tab_end
-  const size_t bytes = static_cast<size_t>(tc->ntiles) * nkc * 2 * tw * 128u;
+  const size_t bytes = static_cast<size_t>(tc->ntiles) * nkc * 2 * wtw * 128u;
   cudaError_t e = cudaMalloc(&tc->w16, bytes);
   if (e != cudaSuccess) return e;
   double* inv = nullptr;
   if ((e = cudaMalloc(&inv, sizeof(double) * f.rows)) != cudaSuccess) return e;
   dir_norm_kernel<<<(f.rows + 127) / 128, 128>>>(f.w64, f.dim, f.rows, inv);
-  pack_w16_kernel<<<1024, 256>>>(f.w64, inv, f, tc->ntiles, nkc, tw, dpt, tc->w16);
+  pack_w16_kernel<<<1024, 256>>>(f.w64, inv, f, tc->ntiles, nkc, wtw, dpt, tc->w16);
   count_launch(2);
   e = cudaDeviceSynchronize();
   cudaFree(inv);
   if (e != cudaSuccess) return e;
   if (tc_kstream(nkc)) {
-    e = cudaFuncSetAttribute(hash_tck_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(ks_smem_bytes()));
+    e = wtw == 256 ? cudaFuncSetAttribute(hash_tck_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(ks_smem_bytes(256)))
+                   : cudaFuncSetAttribute(hash_tck_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(ks_smem_bytes(128)));
     if (e != cudaSuccess) return e;
     e = cudaMalloc(&tc->w32, sizeof(float) * f.rows * f.dim);
     if (e != cudaSuccess) return e;
@@ -2138,7 +2182,10 @@ cudaError_t launch_convert_x_wide(const TcArgs& a, cudaStream_t s) {
 
 cudaError_t launch_hash_tck(const TcArgs& a, cudaStream_t s) {
   if (a.n == 0) return cudaSuccess;
-  hash_tck_kernel<<<tck_grid(a.n), kKsThreads, ks_smem_bytes(), s>>>(a);
+  if (a.tw == 256)
+    hash_tck_kernel<256><<<tck_grid(a.n), kKsThreads, ks_smem_bytes(256), s>>>(a);
+  else
+    hash_tck_kernel<128><<<tck_grid(a.n), kKsThreads, ks_smem_bytes(128), s>>>(a);
   count_launch();
   return cudaGetLastError();
 }

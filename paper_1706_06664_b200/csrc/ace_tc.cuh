@@ -15,7 +15,8 @@ struct TcFamily {
   float* w32 = nullptr;      // K-streamed recheck: W rounded to fp32, [rows][dim]
   uint32_t nkc = 0;          // K-chunks of 64: dpad64 / 64
   uint32_t ntiles = 0;       // direction tiles of tw directions (packed densely)
-  uint32_t tw = 128;         // direction tile width: 192 (d <= 128) or 128
+  uint32_t tw = 128;         // direction tile width: 192 (d <= 128) or 128; K-streamed: 256 or 128
+  uint32_t tpt = 0;          // K-streamed: whole tables per direction tile (tw / K)
   int enabled = 0;
 };
 
