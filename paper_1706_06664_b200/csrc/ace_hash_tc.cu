@@ -1498,8 +1498,8 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
 // is streamed in 64-wide K chunks next to the W chunks, one direction tile at
 // a time.  Accumulation is chunked: kKsSc K chunks go into a TMEM accumulator
 // (double-buffered), the epilogue adds the chunk results into fp32 running
-// sums in registers (64 columns per thread).  That keeps the rigorous error
-// bound at (12 kKsSc + nchunks + 16) ulp instead of growing with d, so near
+// sums in registers (kTW / 2 columns per thread).  That keeps the rigorous error
+// bound at (12 kKsSc + 16 + nchunks / 2) ulp instead of growing with d, so near
 // ties stay rare; they are rechecked by recheck_segs_kernel afterwards.
 
 #ifndef ACE_KS_TS
@@ -2198,8 +2198,13 @@ cudaError_t launch_recheck_segs(const TcArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// The chunk results are added in fp32 registers with round-to-nearest (the
+// epilogue's FADD): each partial sum is bounded by ||x~|| ||w^|| (Cauchy-
+// Schwarz over the chunks), so each add errs by at most 2^-24 of it, half the
+// 2^-23 allowed for each (truncating) tensor-core accumulation step.
 float tck_margin(uint32_t nkc, bool x_f64) {
-  return static_cast<float>(2.0 * (4.0 * 0x1.0p-22 + 0x1.0p-23 * (12.0 * kKsSc + ks_chunks(nkc) + 16.0) * 1.01 +
+  return static_cast<float>(2.0 * (4.0 * 0x1.0p-22 +
+                                   (0x1.0p-23 * (12.0 * kKsSc + 16.0) + 0x1.0p-24 * ks_chunks(nkc)) * 1.01 +
                                    (x_f64 ? 0x1.0p-23 : 0.0)));
 }
 
