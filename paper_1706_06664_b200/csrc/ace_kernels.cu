@@ -634,6 +634,66 @@ __device__ void count_range(const uint32_t* ids, uint64_t n, uint32_t k_bits, ui
   }
 }
 
+// Counts of 2^16 bins in 32768 shared words, two u16 bins per word (K = 16 in
+// one part: each id read once).  A half that wraps (65536 hits within the
+// block's range) spills 65536 to the global counter; a wrapped low half also
+// carried into the high half, which is undone (and a wrap of the high half in
+// either direction spilled too).  Every wrap is seen by the atomic that caused
+// it (its returned old value), so value + 65536 * spills is exact per bin.
+__device__ __forceinline__ void hist16_add(uint32_t* hist, uint32_t b, uint32_t* ct) {
+  const uint32_t wd = b >> 1, sh = (b & 1u) << 4;
+  const uint32_t old = atomicAdd(&hist[wd], 1u << sh);
+  if (((old >> sh) & 0xffffu) == 0xffffu) {
+    atomicAdd(&ct[b], 65536u);
+    if (sh == 0u) {
+      if ((old >> 16) == 0xffffu) atomicAdd(&ct[b + 1], 65536u);   // the carry wrapped the high half
+      const uint32_t o2 = atomicAdd(&hist[wd], 0xffff0000u);      // undo the carry: high half - 1
+      if ((o2 >> 16) == 0u) atomicSub(&ct[b + 1], 65536u);          // ... wrapping it backwards
+    }
+  }
+}
+
+__device__ void count_range16(const uint32_t* ids, uint64_t n, uint64_t i0, uint64_t i1, uint32_t* counters,
+                              uint32_t* hist) {
+  constexpr int kVec = 4;
+  for (uint64_t seg = i0; seg < i1;) {
+    const uint64_t t = seg / n;
+    const uint64_t seg_end = min(i1, (t + 1) * n);
+    uint32_t* ct = counters + (t << 16);
+    __syncthreads();
+    const uint64_t a = min(seg_end, static_cast<uint64_t>((seg + 3u) & ~static_cast<uint64_t>(3))), nv = (seg_end - a) >> 2,
+                   z = a + (nv << 2);
+    for (uint64_t i = seg + threadIdx.x; i < a; i += blockDim.x) hist16_add(hist, __ldg(ids + i), ct);
+    for (uint64_t i = z + threadIdx.x; i < seg_end; i += blockDim.x) hist16_add(hist, __ldg(ids + i), ct);
+    const uint4* v4 = reinterpret_cast<const uint4*>(ids + a);
+    for (uint64_t base = 0; base < nv; base += kVec * blockDim.x) {
+      uint4 q[kVec];
+#pragma unroll
+      for (int u = 0; u < kVec; ++u) q[u] = __ldg(v4 + min(base + u * blockDim.x + threadIdx.x, nv - 1u));
+#pragma unroll
+      for (int u = 0; u < kVec; ++u)
+        if (base + u * blockDim.x + threadIdx.x < nv) {
+          hist16_add(hist, q[u].x, ct);
+          hist16_add(hist, q[u].y, ct);
+          hist16_add(hist, q[u].z, ct);
+          hist16_add(hist, q[u].w, ct);
+        }
+    }
+    // merge: two bins per word, fire-and-forget
+    __syncthreads();
+    for (uint32_t wd = threadIdx.x; wd < 32768u; wd += blockDim.x) {
+      const uint32_t v = hist[wd];
+      if (v) {
+        hist[wd] = 0u;
+        if (v & 0xffffu) atomicAdd(&ct[2u * wd], v & 0xffffu);
+        if (v >> 16) atomicAdd(&ct[2u * wd + 1u], v >> 16);
+      }
+    }
+    __syncthreads();
+    seg = seg_end;
+  }
+}
+
 // Phase 2 of the fused passes: ids [g0, g1) replaced in place by their
 // final counts, looked up in a shared-memory copy of each table (staged once
 // per table segment).  TS = uint32_t holds a table of 2^K <= 2^15 counts;
@@ -1182,9 +1242,12 @@ __global__ void __launch_bounds__(1024) detect_tail_kernel(const TailArgs a) {
     const uint64_t total = a.n * a.tables;
     const uint64_t i0 = min(total, static_cast<uint64_t>(blockIdx.x >> pshift) * a.per);
     const uint64_t i1 = min(total, i0 + a.per);
-    for (uint32_t b = threadIdx.x; b < (1u << a.part_bits); b += blockDim.x) hist[b] = 0u;
+    for (uint32_t b = threadIdx.x; b < (1u << min(a.part_bits, 15u)); b += blockDim.x) hist[b] = 0u;
     if (threadIdx.x == 0) blk = 0ull;
-    count_range(a.ids, a.n, a.k_bits, a.part_bits, part, i0, i1, a.counters, hist, st);
+    if (a.part_bits == 16)
+      count_range16(a.ids, a.n, i0, i1, a.counters, hist);
+    else
+      count_range(a.ids, a.n, a.k_bits, a.part_bits, part, i0, i1, a.counters, hist, st);
     __threadfence();
     grid.sync();
     tail_stamp(a, 1);
@@ -1416,7 +1479,13 @@ cudaError_t launch_detect_tail(uint32_t* ids, uint64_t n, uint32_t tables, uint3
   unsigned grid = static_cast<unsigned>(sms);
   size_t smem = 1024 * sizeof(double);
   if (gather) {
-    a.part_bits = k_bits < 15 ? k_bits : 15;
+    // K = 16: one part of packed u16 bins (count_range16); 2 parts of u32 bins with ACE_HIST16=0
+    static int h16_env = -1;
+    if (h16_env < 0) {
+      const char* e = getenv("ACE_HIST16");
+      h16_env = e ? atoi(e) : 1;
+    }
+    a.part_bits = k_bits < 15 ? k_bits : (k_bits == 16 && h16_env ? 16u : 15u);
     const uint32_t parts = 1u << (k_bits - a.part_bits);
     const uint64_t total = n * tables;
     uint64_t ranges = static_cast<uint64_t>(sms) / parts;
@@ -1424,7 +1493,7 @@ cudaError_t launch_detect_tail(uint32_t* ids, uint64_t n, uint32_t tables, uint3
     if (ranges > total / 4096) ranges = total / 4096 > 0 ? total / 4096 : 1;
     a.per = (total + ranges - 1) / ranges;
     grid = static_cast<unsigned>((total + a.per - 1) / a.per) * parts;
-    smem = std::max<size_t>(smem, sizeof(uint32_t) << a.part_bits);
+    smem = std::max<size_t>(smem, sizeof(uint32_t) << std::min(a.part_bits, 15u));
     if (k_bits == 16) smem = std::max<size_t>(smem, sizeof(uint16_t) << 16);
     // T = sum c^2 is accumulated from zero (32-bit, unsaturated)
     const cudaError_t e = cudaMemsetAsync(&st->T, 0, sizeof(unsigned long long), s);

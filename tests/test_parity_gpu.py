@@ -370,3 +370,46 @@ print(json.dumps(out))
             assert width_res[0] == e["counters_sha256"], cfg
             assert width_res[1] == e["flags_sha256"], cfg
             assert width_res[2] == e["reported"], cfg
+
+
+def test_hist16_hot_bins_wrap(cuda):
+    """K = 16 deferred insert counts 2^16 bins packed two per shared word
+    (count_range16): bins hit 65536+ times within one block's id range wrap
+    their u16 half and spill to the global counter, a wrapped low half's carry
+    into its neighbour is undone.  Two points whose table-0 buckets differ only
+    in the last bit (the two halves of one word) alternate over 6M rows (24M
+    ids: ~81k hits per bin per block range); the other tables get one or two
+    hot bins.  Counters, mean and scores equal the exact counts."""
+    torch = cuda
+    fam = ace.SrpFamily(ace.SrpConfig(dim=2, k_bits=16, num_tables=4, seed=7))
+    w = np.asarray(fam.direction(0, 15), dtype=np.float64)
+    perp = np.array([-w[1], w[0]]) / np.linalg.norm(w)
+    u = w / np.linalg.norm(w)
+    pair = None
+    for delta in (1e-2, 1e-3, 1e-4, 1e-5):
+        pts = np.stack([perp + delta * u, perp - delta * u]).astype(np.float32)
+        b = fam.buckets(pts.astype(np.float64))
+        if int(b[0, 0]) ^ int(b[0, 1]) == 1:
+            pair = pts
+            break
+    assert pair is not None, "no point pair straddling only the last hyperplane of table 0"
+    n = 6_000_000
+    x = np.empty((n, 2), dtype=np.float32)
+    x[0::2] = pair[0]
+    x[1::2] = pair[1]
+    ids = fam.buckets(pair.astype(np.float64))  # (L, 2)
+    L, K = 4, 16
+    expect = np.zeros((L, 1 << K), dtype=np.uint64)
+    for t in range(L):
+        expect[t, ids[t, 0]] += n // 2
+        expect[t, ids[t, 1]] += n // 2
+    sk = ace.AceSketch(fam, ace.CounterWidth.k32)
+    rep = sk.build_detect(torch.from_numpy(x).cuda())
+    got = sk.counters_u32().reshape(L, 1 << K).astype(np.uint64)
+    assert np.array_equal(got, expect)
+    sq = int((expect.astype(object) ** 2).sum())
+    assert sk.size() == n
+    assert abs(sk.mean() - sq / (n * L)) <= 1e-12 * sq / (n * L)
+    s0 = int(sum(expect[t, ids[t, 0]] for t in range(L)))
+    s1 = int(sum(expect[t, ids[t, 1]] for t in range(L)))
+    assert abs(rep.score_mean - (s0 + s1) / (2 * L)) <= 1e-9 * max(s0, s1)
