@@ -400,7 +400,24 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
     t.w64 = f->d.w64;
     t.counters = sk->counters;
     t.fused_insert = fused ? 1 : 0;
+    // ACE_EXT_RECHECK=1: near ties rechecked by a separate warp-per-item pass
+    // (recheck_segs_kernel) instead of inside the projection kernel (recheck
+    // warps and shared tail; not with the fused insert, whose recheck also
+    // moves counts).  Measured: cfg 2 0.463 (in-kernel) vs 0.472 ms per step,
+    // cfg 3 15.69 vs 15.59 ms, so off by default.
+    static int ext_env = -1;
+    if (ext_env < 0) {
+      const char* e = getenv("ACE_EXT_RECHECK");
+      ext_env = e ? atoi(e) : 0;
+    }
+    t.ext_recheck = (ext_env && !fused && !t.fuse_convert) ? 1 : 0;
+    if (t.ext_recheck) {
+      ACE_CUDA(sk->segc.ensure(static_cast<size_t>(tck_grid(n)) * sizeof(uint32_t)));
+      t.seg_counts = sk->segc.as<uint32_t>();
+      t.w32 = f->tc.w32;
+    }
     ACE_CUDA(launch_hash_tc(t, sk->stream));
+    if (t.ext_recheck) ACE_CUDA(launch_recheck_segs(t, sk->stream));
     sk->mark(5);
     ACE_CUDA(launch_recheck(t, f->d.w64, sk->stream));
     if (fused) {

@@ -1048,7 +1048,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
     const uint32_t total_done = 8u * static_cast<uint32_t>(iters);
     unsigned long long* seg = a.near_list + blockIdx.x * seg_cap;
     uint32_t i = (warp - 10u) * 32u + lane;
-    if (!(a.dbg & 32)) {
+    if (!(a.dbg & 32) && !a.ext_recheck) {
       while (true) {
         unsigned long long item = ~0ull;
         while (true) {
@@ -1438,7 +1438,11 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
     if (prof && warp == 2) pw[8] = static_cast<unsigned long long>(clock64() - t_start);
     const uint32_t et = threadIdx.x - 64u;
     const uint32_t cnt = static_cast<uint32_t>(min(static_cast<unsigned long long>(seg_n), seg_cap));
-    if (!(a.dbg & 32))
+    if (prof && et == 0) {
+      atomicAdd(&a.prof[28], static_cast<unsigned long long>(min(min_next, cnt)));  // slots reached by the recheck warps
+      atomicAdd(&a.prof[29], static_cast<unsigned long long>(cnt));                 // slots pushed
+    }
+    if (!(a.dbg & 32) && !a.ext_recheck)
       recheck_tail(a.x, a.x_f64, a.ld, static_cast<uint32_t>(a.dim), a.w64, a.ids, a.ids_ld, a.counters, a.fused_insert,
                    K, base, L.a_bytes + L.w_bytes, a.near_list + blockIdx.x * seg_cap, min(min_next, cnt), cnt, et,
                    rr_own, ff_own);
@@ -1453,6 +1457,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
       if (blk_rech) atomicAdd(&a.st->rechecked, blk_rech);
       if (blk_flip) atomicAdd(&a.st->flipped, blk_flip);
       if (seg_n) atomicAdd(&a.st->near_count, static_cast<unsigned long long>(seg_n));
+      if (a.ext_recheck) a.seg_counts[blockIdx.x] = seg_n;
       if (a.fused_insert && blockIdx.x == 0) atomicAdd(&a.st->n, a.n);
     }
   }
@@ -2069,16 +2074,17 @@ cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc) {
   e = cudaDeviceSynchronize();
   cudaFree(inv);
   if (e != cudaSuccess) return e;
+  e = cudaMalloc(&tc->w32, sizeof(float) * f.rows * f.dim);
+  if (e != cudaSuccess) return e;
+  w32_round_kernel<<<1024, 256>>>(f.w64, static_cast<uint64_t>(f.rows) * f.dim, tc->w32);
+  count_launch();
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return e;
   if (tc_kstream(nkc)) {
     e = wtw == 256 ? cudaFuncSetAttribute(hash_tck_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(ks_smem_bytes(256)))
                    : cudaFuncSetAttribute(hash_tck_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(ks_smem_bytes(128)));
-    if (e != cudaSuccess) return e;
-    e = cudaMalloc(&tc->w32, sizeof(float) * f.rows * f.dim);
-    if (e != cudaSuccess) return e;
-    w32_round_kernel<<<1024, 256>>>(f.w64, static_cast<uint64_t>(f.rows) * f.dim, tc->w32);
-    e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return e;
     tc->enabled = 1;
     return cudaSuccess;

@@ -12,7 +12,7 @@ namespace ace_dev {
 //   so one cp.async.bulk per block lands them ready for tcgen05.mma.
 struct TcFamily {
   uint16_t* w16 = nullptr;   // [ntiles][nkc][2][128*64] fp16 (swizzled)
-  float* w32 = nullptr;      // K-streamed recheck: W rounded to fp32, [rows][dim]
+  float* w32 = nullptr;      // near-tie recheck (recheck_segs_kernel): W rounded to fp32, [rows][dim]
   uint32_t nkc = 0;          // K-chunks of 64: dpad64 / 64
   uint32_t ntiles = 0;       // direction tiles of tw directions (packed densely)
   uint32_t tw = 128;         // direction tile width: 192 (d <= 128) or 128; K-streamed: 256 or 128
@@ -40,8 +40,9 @@ struct TcArgs {
   uint32_t* counters;             // fused insert target (fused_insert != 0)
   int fused_insert;               // 32-bit sketch: insert buckets in the epilogue
   int fuse_convert;               // convert X inside the projection kernel (no pre-pass)
-  uint32_t* seg_counts;           // K-streamed kernel: near ties pushed per CTA
-  const float* w32;               // K-streamed recheck: W rounded to fp32 [rows][dim]
+  uint32_t* seg_counts;           // near ties pushed per CTA (K-streamed kernel, ext_recheck)
+  const float* w32;               // recheck_segs_kernel: W rounded to fp32 [rows][dim]
+  int ext_recheck;                // hash_tc_kernel: leave the near-tie list to recheck_segs_kernel
   uint32_t* overflow_rows;    // bitmap over rows; rows rechecked in full
   DevState* st;
   uint16_t tab_end[64];      // tables completed by the end of direction tile j

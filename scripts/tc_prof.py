@@ -42,3 +42,4 @@ print("  MMA lane per CTA: tcgen05 fence after acc_empty %.0f" % (out[25] / grid
 if out[21]:
     print("  MMA issuing lane per CTA: W-full waits %.0f  commits %.0f  (per group: %.0f / %.0f)" % (
         out[26] / grid, out[27] / grid, out[26] / out[21], out[27] / out[21]))
+print("  near-tie slots per CTA: pushed %.0f, reached by the recheck warps during the main loop %.0f" % (out[29] / grid, out[28] / grid))
