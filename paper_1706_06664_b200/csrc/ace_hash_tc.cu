@@ -11,14 +11,19 @@
 // (recheck kernel).  Buckets are packed MSB-first (srp.cpp:106-113) straight
 // from the accumulator columns: one thread owns one point (TMEM lane).
 //
-// Warp roles (256 threads, one CTA per SM, persistent over point tiles):
-//   warp 0      W producer: cp.async.bulk of pre-swizzled W blocks (TMA engine)
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (A from TMEM)
-//   warps 2-5   X converters: one point row per thread, fp32 -> scaled fp16
-//               hi/lo, tcgen05.st into the TMEM A operand
-//   warps 6-9   epilogue: tcgen05.ld accumulators -> signs, near ties, buckets
-// Pipelines (mbarriers): W smem stages full/empty, TMEM A buffers full/empty,
-// 2 TMEM accumulator buffers of 128 columns full/empty.
+// Warp roles (384 threads, one CTA per SM, persistent over point tiles):
+//   warp 0      producer: cp.async.bulk (TMA engine) of the point tile's A
+//               image (fp16 hi | lo, written by convert_x_kernel) and a ring
+//               of pre-swizzled W stages
+//   warp 1      TMEM allocator; copies A into TMEM (tcgen05.cp) and issues the
+//               TS MMAs from one elected lane, one burst per direction tile
+//   warps 2-9   epilogue: two warps per TMEM lane quarter on alternate
+//               direction tiles; tcgen05.ld -> sign words, near ties, buckets
+//   warps 10-11 exact recheck of near ties while the main loop runs; leftovers
+//               go to a shared tail after it
+// Pipelines (mbarriers): W stages full/empty, A full/empty, two TMEM
+// accumulators (192 columns for d <= 128, else 128) full/empty.
+// hash_tck_kernel (further down) is the K-streamed variant for d > 256.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>

@@ -9,7 +9,7 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/b
 if [ "${NCU:-1}" = "1" ]; then
   ./scripts/launches.sh gpurun_out/launches.csv > gpurun_out/launches.txt 2>&1; cat gpurun_out/launches.txt
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/b_plain.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"hash_tc|convert_x|apply_ids|score_kernel" -s 8 -c 4 \
+  ncu --set full --clock-control none --import-source on -k regex:"hash_tc|convert_x|detect_tail" -s 6 -c 3 \
       -f -o gpurun_out/prof_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full.log 2>&1
   echo "ncu rc=$?"
 fi
