@@ -413,3 +413,31 @@ def test_hist16_hot_bins_wrap(cuda):
     s0 = int(sum(expect[t, ids[t, 0]] for t in range(L)))
     s1 = int(sum(expect[t, ids[t, 1]] for t in range(L)))
     assert abs(rep.score_mean - (s0 + s1) / (2 * L)) <= 1e-9 * max(s0, s1)
+
+
+@pytest.mark.parametrize("gather", [False, True])
+def test_tied_scores_replay(cuda, oracle_c, gather):
+    """Every row's score sits exactly on the exact threshold (two points, m
+    copies each: all scores equal, sd = 0), so the ambiguity band holds every
+    row and the detect tail's last block replays the reference's sequential
+    binary64 statistics (detect.cpp:44-60).  The flags must be the
+    reference's, whichever way its rounding falls; the run with N*L >= 16M
+    takes the deferred-insert (gather) path of the tail."""
+    torch = cuda
+    L = 50 if gather else 4
+    fam = ace.SrpFamily(ace.SrpConfig(dim=8, k_bits=15, num_tables=L, seed=11))
+    rng = np.random.default_rng(5)
+    pts = rng.standard_normal((2, 8)).astype(np.float32)
+    m = 200_000 if gather else 3_001
+    x = np.repeat(pts, m, axis=0)
+    rng.shuffle(x, axis=0)
+    sk = ace.AceSketch(fam, ace.CounterWidth.k32)
+    rep = sk.build_detect(torch.from_numpy(x).cuda())
+    assert rep.ambiguous == 2 * m and rep.replayed
+    ids = fam.buckets(x.astype(np.float64))                      # (L, n)
+    cnt = sk.counters_u32().reshape(L, -1)
+    S = cnt[np.arange(L)[:, None], ids].astype(np.int64).sum(axis=0)
+    _, _, thr, flags = detect_from_scores(oracle_c, S / float(L))
+    assert np.array_equal(rep.flags, flags)
+    assert rep.reported == int(flags.sum())
+    assert rep.threshold == thr
