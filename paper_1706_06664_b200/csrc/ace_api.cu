@@ -262,6 +262,18 @@ bool fire_and_forget_ok(const AceSketch* sk, uint64_t n) {
   return sk->width == 32 && !sk->hst->saturated && sk->hst->n + n < 0xffffffffull;
 }
 
+// One cooperative launch per streaming batch (launch_stream_step): 32-bit
+// unsaturable sketches with K <= 15 (a whole table's histogram in shared
+// memory); ACE_STREAM_FUSED=0 keeps the score / insert / sum-of-squares kernels.
+bool stream_fused_ok(const AceSketch* sk, bool ff) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("ACE_STREAM_FUSED");
+    env = e ? atoi(e) : 1;
+  }
+  return env != 0 && ff && sk->width == 32 && sk->fam->d.k_bits <= 15;
+}
+
 // hash n rows into sk->ids (table-major, stride n); optional fused insert.
 // Chunk mode (ids_out != null): the rows are rows [r0, r0 + n) of a longer
 // batch whose ids (stride ids_ld) the caller has sized.
@@ -1191,13 +1203,19 @@ ace_status ace_sketch_stream_batch(AceSketch* sk, const void* x, int dtype, uint
     }
   }
   uint32_t* dflags = (flag_bits && out_where == ACE_DEVICE) ? flag_bits : sk->flags.as<uint32_t>();
-  ACE_CUDA(cudaMemsetAsync(&sk->st->batch_sum, 0, sizeof(unsigned long long), sk->stream));
-  ACE_CUDA(launch_stream_score(sk->ids.as<uint32_t>(), n, f->d.tables, f->d.k_bits, sk->counters,
-                               alpha, dflags, dsc, sk->st, sk->stream));
-  sk->mark(2);
-  ACE_CUDA(launch_apply_ids(sk->ids.as<uint32_t>(), n, f->d.tables, f->d.k_bits, sk->counters,
-                            sk->cap, +1, sk->st, sk->stream, !fire_and_forget_ok(sk, n)));
-  if (sk->width == 16) ACE_CUDA(launch_cap(sk->counters, sk->num_counters, sk->cap, sk->st, sk->stream));
+  if (stream_fused_ok(sk, fire_and_forget_ok(sk, n))) {
+    ACE_CUDA(launch_stream_step(sk->ids.as<uint32_t>(), n, n, f->d.tables, f->d.k_bits, sk->counters, alpha, dflags,
+                                dsc, sk->st, sk->stream));
+    sk->mark(2);
+  } else {
+    ACE_CUDA(cudaMemsetAsync(&sk->st->batch_sum, 0, sizeof(unsigned long long), sk->stream));
+    ACE_CUDA(launch_stream_score(sk->ids.as<uint32_t>(), n, f->d.tables, f->d.k_bits, sk->counters,
+                                 alpha, dflags, dsc, sk->st, sk->stream));
+    sk->mark(2);
+    ACE_CUDA(launch_apply_ids(sk->ids.as<uint32_t>(), n, f->d.tables, f->d.k_bits, sk->counters,
+                              sk->cap, +1, sk->st, sk->stream, !fire_and_forget_ok(sk, n)));
+    if (sk->width == 16) ACE_CUDA(launch_cap(sk->counters, sk->num_counters, sk->cap, sk->st, sk->stream));
+  }
   sk->mark(3);
   if (out_where == ACE_HOST) {
     if (flag_bits &&
@@ -1264,6 +1282,11 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
       const uint64_t r0 = b * batch, rows = std::min(batch, n - r0);
       if (batch_ms && b != g0) ACE_CUDA(cudaEventRecord(ev[b], sk->stream));
       const uint32_t* ids = sk->ids.as<uint32_t>() + (r0 - gr0);
+      if (stream_fused_ok(sk, ff)) {
+        ACE_CUDA(launch_stream_step(ids, rows, grows, f->d.tables, f->d.k_bits, sk->counters, alpha, dflags + r0 / 32,
+                                    nullptr, sk->st, sk->stream));
+        continue;
+      }
       ACE_CUDA(cudaMemsetAsync(&sk->st->batch_sum, 0, sizeof(unsigned long long), sk->stream));
       ACE_CUDA(launch_stream_score(ids, rows, f->d.tables, f->d.k_bits, sk->counters, alpha, dflags + r0 / 32,
                                    nullptr, sk->st, sk->stream, grows));

@@ -1360,6 +1360,125 @@ __global__ void stream_score_kernel(const uint32_t* __restrict__ ids, uint64_t n
 }
 
 
+// One streaming batch in one cooperative launch (detect_stream, detect.cpp:
+// 76-84, then the insert, ace_cli.cpp:177-183): every row scored against the
+// counts at batch start and flagged (score <= mu - alpha, warps dealt
+// round-robin over the blocks); grid barrier; then each block owns whole
+// tables (32-bit sketch, K <= 15): it counts the batch's ids of its table in
+// a shared histogram and adds each touched bin with a plain read-modify-write
+// (no other block writes the table), accumulating T += (c + m)^2 - c^2 =
+// 2 c m + m^2 exactly, so no sum-of-squares pass follows.
+struct StreamArgs {
+  const uint32_t* ids;  // table-major, ids[t * stride + i]
+  uint64_t n, stride;
+  uint32_t tables, k_bits;
+  uint32_t* counters;
+  double alpha;
+  uint32_t* flag_bits;
+  double* scores;
+  DevState* st;
+};
+
+__global__ void __launch_bounds__(1024) stream_step_kernel(const StreamArgs a) {
+  extern __shared__ uint32_t hist[];
+  __shared__ double s_cut, s_band;
+  __shared__ int s_live;
+  __shared__ unsigned long long s_dT;
+  DevState* st = a.st;
+  const uint32_t lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    const double mu = sketch_mean(st, a.tables);
+    s_cut = mu - a.alpha;
+    s_live = st->n > 0;
+    s_band = 0x1.0p-30 * fmax(1.0, fabs(mu));
+    s_dT = 0ull;
+    if (blockIdx.x == 0) {
+      st->cut = s_cut;
+      st->mean_before = mu;
+    }
+  }
+  __syncthreads();
+  {
+    const double cut = s_cut, band = s_band;
+    const int live = s_live;
+    const double L = static_cast<double>(a.tables);
+    unsigned long long rep = 0, amb = 0;
+    const uint64_t words = (a.n + 31) / 32;
+    const uint64_t wstride = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (uint64_t wd = static_cast<uint64_t>(threadIdx.x >> 5) * gridDim.x + blockIdx.x; wd < words; wd += wstride) {
+      const uint64_t i = wd * 32 + lane;
+      bool f = false;
+      if (i < a.n) {
+        const unsigned long long S = gather_sum<8>(a.ids, a.stride, i, a.tables, a.k_bits, a.counters);
+        const double sc = __ddiv_rn(static_cast<double>(S), L);
+        if (a.scores) a.scores[i] = sc;
+        f = live && sc <= cut;
+        if (live && fabs(sc - cut) <= band) ++amb;
+      }
+      const unsigned w = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) {
+        if (a.flag_bits) a.flag_bits[wd] = w;
+        rep += __popc(w);
+      }
+    }
+    rep = warp_sum_u64(rep);
+    amb = warp_sum_u64(amb);
+    if (lane == 0) {
+      if (rep) atomicAdd(&st->reported, rep);
+      if (amb) atomicAdd(&st->ambiguous, amb);
+    }
+  }
+  __threadfence();
+  cg::this_grid().sync();
+  // ---- insert: block b owns tables b, b + gridDim.x, ...
+  const uint32_t nb = 1u << a.k_bits;
+  unsigned long long dT = 0ull;
+  for (uint32_t t = blockIdx.x; t < a.tables; t += gridDim.x) {
+    for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
+    __syncthreads();
+    const uint32_t* src = a.ids + static_cast<uint64_t>(t) * a.stride;
+    constexpr int kDepth = 8;
+    for (uint64_t i0 = 0; i0 < a.n; i0 += kDepth * blockDim.x) {
+      uint32_t idv[kDepth];
+#pragma unroll
+      for (int u = 0; u < kDepth; ++u) {
+        const uint64_t i = i0 + u * blockDim.x + threadIdx.x;
+        idv[u] = i < a.n ? __ldg(src + i) : 0xffffffffu;
+      }
+#pragma unroll
+      for (int u = 0; u < kDepth; ++u)
+        if (idv[u] != 0xffffffffu) atomicAdd(&hist[idv[u]], 1u);
+    }
+    __syncthreads();
+    uint32_t* ct = a.counters + (static_cast<uint64_t>(t) << a.k_bits);
+    for (uint32_t b0 = threadIdx.x; b0 < nb; b0 += kDepth * blockDim.x) {
+      uint32_t m[kDepth], o[kDepth];
+#pragma unroll
+      for (int u = 0; u < kDepth; ++u) {
+        const uint32_t b = b0 + u * blockDim.x;
+        m[u] = b < nb ? hist[b] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < kDepth; ++u) o[u] = m[u] ? ct[b0 + u * blockDim.x] : 0u;
+#pragma unroll
+      for (int u = 0; u < kDepth; ++u)
+        if (m[u]) {
+          ct[b0 + u * blockDim.x] = o[u] + m[u];
+          dT += 2ull * o[u] * m[u] + static_cast<unsigned long long>(m[u]) * m[u];
+        }
+    }
+    __syncthreads();
+  }
+  dT = warp_sum_u64(dT);
+  if (lane == 0 && dT) atomicAdd(&s_dT, dT);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_dT) atomicAdd(&st->T, s_dT);
+    if (blockIdx.x == 0) atomicAdd(&st->n, a.n);
+  }
+}
+
+
 int grid_for(uint64_t work, int threads, int max_blocks = 148 * 16) {
   uint64_t b = (work + threads - 1) / threads;
   if (b < 1) b = 1;
@@ -1553,6 +1672,42 @@ cudaError_t launch_stream_score(const uint32_t* ids, uint64_t n, uint32_t tables
                                                        counters, alpha, flag_bits, scores, st);
   count_launch();
   return cudaGetLastError();
+}
+
+cudaError_t launch_stream_step(const uint32_t* ids, uint64_t n, uint64_t ids_stride, uint32_t tables, uint32_t k_bits,
+                               uint32_t* counters, double alpha, uint32_t* flag_bits, double* scores, DevState* st,
+                               cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  if (k_bits > 15) return cudaErrorInvalidValue;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  static bool configured = false;
+  if (!configured) {
+    const cudaError_t e = cudaFuncSetAttribute(stream_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(sizeof(uint32_t) << 15));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  StreamArgs a{};
+  a.ids = ids;
+  a.n = n;
+  a.stride = ids_stride ? ids_stride : n;
+  a.tables = tables;
+  a.k_bits = k_bits;
+  a.counters = counters;
+  a.alpha = alpha;
+  a.flag_bits = flag_bits;
+  a.scores = scores;
+  a.st = st;
+  void* args[] = {&a};
+  const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(stream_step_kernel), dim3(sms),
+                                                    dim3(1024), args, sizeof(uint32_t) << k_bits, s);
+  count_launch();
+  return e;
 }
 
 cudaError_t launch_sum_squares(const uint32_t* counters, uint64_t num, unsigned long long* out,

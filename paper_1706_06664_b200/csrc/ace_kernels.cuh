@@ -67,6 +67,13 @@ cudaError_t launch_stream_score(const uint32_t* ids, uint64_t n, uint32_t tables
                                 double alpha, uint32_t* flag_bits, double* scores,
                                 DevState* st, cudaStream_t s, uint64_t ids_stride = 0);  // 0: n
 
+// One streaming batch (32-bit, unsaturable, K <= 15) in one cooperative
+// launch: score + flag against the counts at batch start, then insert with T
+// updated exactly (no sum-of-squares pass).
+cudaError_t launch_stream_step(const uint32_t* ids, uint64_t n, uint64_t ids_stride, uint32_t tables, uint32_t k_bits,
+                               uint32_t* counters, double alpha, uint32_t* flag_bits, double* scores, DevState* st,
+                               cudaStream_t s);
+
 // Sum of squares of all counters (T after restore with exact state).
 cudaError_t launch_sum_squares(const uint32_t* counters, uint64_t num,
                                unsigned long long* out, cudaStream_t s);
