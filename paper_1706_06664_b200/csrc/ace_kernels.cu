@@ -577,6 +577,12 @@ __global__ void __launch_bounds__(1024) apply_ids_smem_kernel(const uint32_t* __
   }
 }
 
+#ifndef ACE_COUNT_DBG
+#define ACE_COUNT_DBG 0
+#endif
+#ifndef ACE_COUNT_VEC
+#define ACE_COUNT_VEC 4  // 16-byte id vectors per thread in flight in the one-part count
+#endif
 // Phase 1 of the fused passes: counts of the block's id range [i0, i1)
 // (flattened table-major ids), bins of `part` only, merged into `counters`
 // with fire-and-forget REDs (32-bit, unsaturable sketches).
@@ -587,7 +593,7 @@ __device__ void count_range(const uint32_t* ids, uint64_t n, uint32_t k_bits, ui
   const int lane = threadIdx.x & 31;
   unsigned long long dT = 0ull;
   constexpr int kDepth = 8;
-  constexpr int kVec = 4;  // 16-byte vectors per thread in flight (one-part path)
+  constexpr int kVec = ACE_COUNT_VEC;  // 16-byte vectors per thread in flight (one-part path)
   const uint32_t step = blockDim.x * kDepth;
   for (uint64_t seg = i0; seg < i1;) {
     const uint64_t t = seg / n;
@@ -606,10 +612,14 @@ __device__ void count_range(const uint32_t* ids, uint64_t n, uint32_t k_bits, ui
 #pragma unroll
         for (int u = 0; u < kVec; ++u)
           if (base + u * blockDim.x + threadIdx.x < nv) {
+#if ACE_COUNT_DBG & 1  // timing experiment: no atomics (wrong counts)
+            if ((q[u].x ^ q[u].y ^ q[u].z ^ q[u].w) == 0xffffffffu) hist[0] = 1u;
+#else
             atomicAdd(&hist[q[u].x], 1u);
             atomicAdd(&hist[q[u].y], 1u);
             atomicAdd(&hist[q[u].z], 1u);
             atomicAdd(&hist[q[u].w], 1u);
+#endif
           }
       }
     } else {
@@ -628,8 +638,12 @@ __device__ void count_range(const uint32_t* ids, uint64_t n, uint32_t k_bits, ui
         }
       }
     }
+#if ACE_COUNT_DBG & 2  // timing experiment: no merge (wrong counts)
+    __syncthreads();
+#else
     flush_hist<false>(hist, nb, counters + (t << k_bits) + (static_cast<uint64_t>(part) << part_bits), 0xffffffffu,
                       st, dT);
+#endif
     seg = seg_end;
   }
 }
@@ -842,18 +856,18 @@ __global__ void cap_kernel(uint32_t* counters, uint64_t num, uint32_t cap, DevSt
 
 // ---- scoring -----------------------------------------------------------------
 
-// S = sum_t counters[t * 2^K + ids[t * stride + i]] (sketch.cpp:108-116):
+// S = sum_{t0 <= t < tables} counters[t * 2^K + ids[t * stride + i]] (sketch.cpp:108-116):
 // ids in groups of G, the next group's ids loaded while the current group's
 // counters are gathered (two dependent L2 round trips per group otherwise).
 template <uint32_t G>
 __device__ __forceinline__ unsigned long long gather_sum(const uint32_t* __restrict__ ids, uint64_t stride, uint64_t i,
                                                          uint32_t tables, uint32_t k_bits,
-                                                         const uint32_t* __restrict__ counters) {
+                                                         const uint32_t* __restrict__ counters, uint32_t t0 = 0) {
   unsigned long long S = 0ull;
   uint32_t b[G];
 #pragma unroll
-  for (uint32_t u = 0; u < G; ++u) b[u] = u < tables ? __ldg(ids + (uint64_t)u * stride + i) : 0u;
-  for (uint32_t t = 0; t < tables; t += G) {
+  for (uint32_t u = 0; u < G; ++u) b[u] = t0 + u < tables ? __ldg(ids + (uint64_t)(t0 + u) * stride + i) : 0u;
+  for (uint32_t t = t0; t < tables; t += G) {
     uint32_t c[G], nb[G];
 #pragma unroll
     for (uint32_t u = 0; u < G; ++u) c[u] = t + u < tables ? __ldg(counters + ((uint64_t)(t + u) << k_bits) + b[u]) : 0u;
@@ -1191,6 +1205,88 @@ __device__ void replay_dev(const uint64_t* __restrict__ sums, uint64_t n, uint32
   __syncthreads();
 }
 
+// build_sketch's deferred insert for K <= 15 without grid barriers: each
+// table is owned by a cluster of two CTAs.  CTA r counts rows [r n/2,
+// (r+1) n/2) of the table into its shared histogram; after a cluster barrier
+// it merges bins [r 2^K/2, (r+1) 2^K/2) with the peer's histogram (distributed
+// shared memory) and the sketch's existing counts, writes the final counts
+// (plain stores: no other CTA touches the table) and adds their squares to T;
+// after a second barrier it copies the peer's final half, so each CTA holds
+// the whole final table, and replaces its rows' ids by their counts in place.
+// The detect tail then scores from the counts (gather = 2).
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024)
+    count_gather_pair_kernel(uint32_t* ids, uint64_t n, uint32_t k_bits, uint32_t* counters, DevState* st) {
+  extern __shared__ __align__(16) uint32_t hist[];
+  __shared__ unsigned long long blk;
+  cg::cluster_group cl = cg::this_cluster();
+  const uint32_t r = cl.block_rank();
+  const uint64_t t = blockIdx.x >> 1;
+  const uint32_t nb = 1u << k_bits, half = (nb + 1u) / 2u;
+  uint32_t* tids = ids + t * n;
+  const uint64_t row0 = n * r / 2, row1 = n * (r + 1) / 2;
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
+  if (threadIdx.x == 0) blk = 0ull;
+  __syncthreads();
+  // rows [row0, row1) of the flattened ids: scalar head and tail, 16-byte body
+  const uint64_t g0 = t * n + row0, g1 = t * n + row1;
+  const uint64_t va = min(g1, (g0 + 3u) & ~static_cast<uint64_t>(3)), nv = (g1 - va) >> 2, vz = va + (nv << 2);
+  constexpr int kVec = 4;
+  for (uint64_t i = g0 + threadIdx.x; i < va; i += blockDim.x) atomicAdd(&hist[ids[i]], 1u);
+  for (uint64_t i = vz + threadIdx.x; i < g1; i += blockDim.x) atomicAdd(&hist[ids[i]], 1u);
+  const uint4* v4 = reinterpret_cast<const uint4*>(ids + va);
+  for (uint64_t base = 0; base < nv; base += kVec * blockDim.x) {
+    uint4 q[kVec];
+#pragma unroll
+    for (int u = 0; u < kVec; ++u) q[u] = __ldg(v4 + min(base + u * blockDim.x + threadIdx.x, nv - 1u));
+#pragma unroll
+    for (int u = 0; u < kVec; ++u)
+      if (base + u * blockDim.x + threadIdx.x < nv) {
+        atomicAdd(&hist[q[u].x], 1u);
+        atomicAdd(&hist[q[u].y], 1u);
+        atomicAdd(&hist[q[u].z], 1u);
+        atomicAdd(&hist[q[u].w], 1u);
+      }
+  }
+  cl.sync();
+  // merge this CTA's half of the bins: existing + own + peer
+  uint32_t* peer = cl.map_shared_rank(hist, r ^ 1u);
+  uint32_t* ct = counters + (t << k_bits);
+  unsigned long long dT = 0ull;
+  const uint32_t b0 = r * half, b1 = min(nb, b0 + half);
+  for (uint32_t b = b0 + threadIdx.x; b < b1; b += blockDim.x) {
+    const uint32_t c = ct[b] + hist[b] + peer[b];
+    ct[b] = c;
+    hist[b] = c;
+    dT += static_cast<unsigned long long>(c) * c;
+  }
+  cl.sync();
+  // the peer's final half
+  const uint32_t p0 = (r ^ 1u) * half, p1 = min(nb, p0 + half);
+  for (uint32_t b = p0 + threadIdx.x; b < p1; b += blockDim.x) hist[b] = peer[b];
+  cl.sync();  // the peer has read our half: it may leave, we may rewrite ids
+  for (uint64_t i = g0 + threadIdx.x; i < va; i += blockDim.x) ids[i] = hist[ids[i]];
+  for (uint64_t i = vz + threadIdx.x; i < g1; i += blockDim.x) ids[i] = hist[ids[i]];
+  uint4* w4 = reinterpret_cast<uint4*>(ids + va);
+  for (uint64_t base = 0; base < nv; base += 8 * blockDim.x) {
+    uint4 q[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) q[u] = w4[min(base + u * blockDim.x + threadIdx.x, nv - 1u)];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint64_t j = base + u * blockDim.x + threadIdx.x;
+      if (j < nv) w4[j] = make_uint4(hist[q[u].x], hist[q[u].y], hist[q[u].z], hist[q[u].w]);
+    }
+  }
+  (void)tids;
+  dT = warp_sum_u64(dT);
+  if ((threadIdx.x & 31) == 0 && dT) atomicAdd(&blk, dT);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (blk) atomicAdd(&st->T, blk);
+    if (blockIdx.x == 0) atomicAdd(&st->n, n);
+  }
+}
+
 // ---- fused detect tail ------------------------------------------------------
 //
 // build_sketch's deferred insert + detect_batch in one cooperative launch
@@ -1236,7 +1332,7 @@ __global__ void __launch_bounds__(1024) detect_tail_kernel(const TailArgs a) {
   DevState* st = a.st;
   const int lane = threadIdx.x & 31;
   tail_stamp(a, 0);
-  if (a.gather) {
+  if (a.gather == 1) {
     const uint32_t pshift = a.k_bits - a.part_bits, parts = 1u << pshift;
     const uint32_t part = blockIdx.x & (parts - 1u);
     const uint64_t total = a.n * a.tables;
@@ -1403,21 +1499,31 @@ __global__ void __launch_bounds__(1024) stream_step_kernel(const StreamArgs a) {
     const int live = s_live;
     const double L = static_cast<double>(a.tables);
     unsigned long long rep = 0, amb = 0;
-    const uint64_t words = (a.n + 31) / 32;
+    // two lanes per row (tables split in halves: half the dependent gather
+    // rounds per lane), 16 rows per warp, half flag words dealt round-robin
+    const uint64_t hwords = (a.n + 15) / 16;
     const uint64_t wstride = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
-    for (uint64_t wd = static_cast<uint64_t>(threadIdx.x >> 5) * gridDim.x + blockIdx.x; wd < words; wd += wstride) {
-      const uint64_t i = wd * 32 + lane;
+    const uint32_t th = (a.tables + 1) / 2, hl = lane & 1u;
+    for (uint64_t hw = static_cast<uint64_t>(threadIdx.x >> 5) * gridDim.x + blockIdx.x; hw < hwords; hw += wstride) {
+      const uint64_t i = hw * 16 + (lane >> 1);
+      unsigned long long S = 0ull;
+      if (i < a.n)
+        S = gather_sum<8>(a.ids, a.stride, i, hl ? a.tables : th, a.k_bits, a.counters, hl ? th : 0u);
+      S += __shfl_xor_sync(0xffffffffu, S, 1);
       bool f = false;
-      if (i < a.n) {
-        const unsigned long long S = gather_sum<8>(a.ids, a.stride, i, a.tables, a.k_bits, a.counters);
+      if (i < a.n && hl == 0u) {
         const double sc = __ddiv_rn(static_cast<double>(S), L);
         if (a.scores) a.scores[i] = sc;
         f = live && sc <= cut;
         if (live && fabs(sc - cut) <= band) ++amb;
       }
-      const unsigned w = __ballot_sync(0xffffffffu, f);
+      unsigned w = __ballot_sync(0xffffffffu, f) & 0x55555555u;  // even lanes: rows 16 hw + lane / 2
+      w = (w | (w >> 1)) & 0x33333333u;
+      w = (w | (w >> 2)) & 0x0f0f0f0fu;
+      w = (w | (w >> 4)) & 0x00ff00ffu;
+      w = (w | (w >> 8)) & 0x0000ffffu;
       if (lane == 0) {
-        if (a.flag_bits) a.flag_bits[wd] = w;
+        if (a.flag_bits) reinterpret_cast<uint16_t*>(a.flag_bits)[hw] = static_cast<uint16_t>(w);
         rep += __popc(w);
       }
     }
@@ -1563,7 +1669,7 @@ unsigned long long* g_tail_prof = nullptr;
 cudaError_t launch_detect_tail(uint32_t* ids, uint64_t n, uint32_t tables, uint32_t k_bits, uint32_t* counters,
                                int gather, uint64_t* sums, double* scores, uint32_t* flag_bits, DevState* st,
                                cudaStream_t s) {
-  if (n == 0 || (gather && k_bits > 16)) return cudaErrorInvalidValue;
+  if (n == 0 || (gather && k_bits > 16)) return cudaErrorInvalidValue;  // gather: 1 = counts + gather here
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -1597,7 +1703,32 @@ cudaError_t launch_detect_tail(uint32_t* ids, uint64_t n, uint32_t tables, uint3
   }
   unsigned grid = static_cast<unsigned>(sms);
   size_t smem = 1024 * sizeof(double);
-  if (gather) {
+  // ACE_PAIR_GATHER=1, K <= 15: count and gather by table-owning CTA pairs (no
+  // grid barriers), then the tail scores from the counts.  Measured slower on
+  // cfg 2 (tail 0.130 vs 0.109 ms): 100 SMs count instead of 148, and the
+  // shared atomics bound the count.
+  static int pair_env = -1;
+  if (pair_env < 0) {
+    const char* e = getenv("ACE_PAIR_GATHER");
+    pair_env = e ? atoi(e) : 0;
+  }
+  if (gather == 1 && k_bits <= 15 && pair_env) {
+    static bool pcfg = false;
+    if (!pcfg) {
+      const cudaError_t e = cudaFuncSetAttribute(count_gather_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(sizeof(uint32_t) << 15));
+      if (e != cudaSuccess) return e;
+      pcfg = true;
+    }
+    cudaError_t e = cudaMemsetAsync(&st->T, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+    count_gather_pair_kernel<<<2 * tables, 1024, sizeof(uint32_t) << k_bits, s>>>(ids, n, k_bits, counters, st);
+    count_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    gather = 2;
+    a.gather = 2;
+  }
+  if (gather == 1) {
     // K = 16: one part of packed u16 bins (count_range16); 2 parts of u32 bins with ACE_HIST16=0
     static int h16_env = -1;
     if (h16_env < 0) {
