@@ -427,6 +427,12 @@ def main():
             "algorithmic_flops_per_launch": flops,
             "kernel_ms": kern_ms,
             "kernel_share_of_step": kern_ms / ms if ms else None,
+            # the exact-sign split runs 3 fp16 MMA passes per projection
+            # (x_hi w_hi, x_lo w_hi, x_hi w_lo): peak / 3 is this kernel's
+            # ceiling in algorithmic flops (zero-lo and past-d steps skipped
+            # make the issued work smaller, so this fraction is conservative)
+            "split_passes": 3,
+            "frac_of_split_ceiling": (3.0 * flops / (kern_ms * 1e-3) / 1e12) / peak if kern_ms > 0 else None,
         }
     else:
         kern_ms = phase[0]

@@ -262,6 +262,18 @@ bool fire_and_forget_ok(const AceSketch* sk, uint64_t n) {
   return sk->width == 32 && !sk->hst->saturated && sk->hst->n + n < 0xffffffffull;
 }
 
+// Two blocks per table in the stream step's insert (ACE_STREAM_SPLIT=1; measured
+// slower on cfg 5: 7.9e8 vs 8.6e8 points/s, the second grid barrier and the
+// scratch round trip cost more than the halved count saves).
+bool stream_split_env() {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("ACE_STREAM_SPLIT");
+    env = e ? atoi(e) : 0;
+  }
+  return env != 0;
+}
+
 // One cooperative launch per streaming batch (launch_stream_step): 32-bit
 // unsaturable sketches with K <= 15 (a whole table's histogram in shared
 // memory); ACE_STREAM_FUSED=0 keeps the score / insert / sum-of-squares kernels.
@@ -1204,8 +1216,9 @@ ace_status ace_sketch_stream_batch(AceSketch* sk, const void* x, int dtype, uint
   }
   uint32_t* dflags = (flag_bits && out_where == ACE_DEVICE) ? flag_bits : sk->flags.as<uint32_t>();
   if (stream_fused_ok(sk, fire_and_forget_ok(sk, n))) {
+    ACE_CUDA(sk->demand.ensure(sk->num_counters * sizeof(uint32_t)));
     ACE_CUDA(launch_stream_step(sk->ids.as<uint32_t>(), n, n, f->d.tables, f->d.k_bits, sk->counters, alpha, dflags,
-                                dsc, sk->st, sk->stream));
+                                dsc, sk->st, sk->stream, stream_split_env() ? sk->demand.as<uint32_t>() : nullptr));
     sk->mark(2);
   } else {
     ACE_CUDA(cudaMemsetAsync(&sk->st->batch_sum, 0, sizeof(unsigned long long), sk->stream));
@@ -1283,8 +1296,9 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
       if (batch_ms && b != g0) ACE_CUDA(cudaEventRecord(ev[b], sk->stream));
       const uint32_t* ids = sk->ids.as<uint32_t>() + (r0 - gr0);
       if (stream_fused_ok(sk, ff)) {
+        ACE_CUDA(sk->demand.ensure(sk->num_counters * sizeof(uint32_t)));
         ACE_CUDA(launch_stream_step(ids, rows, grows, f->d.tables, f->d.k_bits, sk->counters, alpha, dflags + r0 / 32,
-                                    nullptr, sk->st, sk->stream));
+                                    nullptr, sk->st, sk->stream, stream_split_env() ? sk->demand.as<uint32_t>() : nullptr));
         continue;
       }
       ACE_CUDA(cudaMemsetAsync(&sk->st->batch_sum, 0, sizeof(unsigned long long), sk->stream));

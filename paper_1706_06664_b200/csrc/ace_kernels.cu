@@ -1473,7 +1473,15 @@ struct StreamArgs {
   uint32_t* flag_bits;
   double* scores;
   DevState* st;
+  uint32_t* scratch;         // L x 2^K u32 (second halves' histograms), or null
+  unsigned long long* prof;  // instrumentation (ACE_TAIL_PROF=1): [5] start [6] scores done [7] max end
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long g;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+  return g;
+}
 
 __global__ void __launch_bounds__(1024) stream_step_kernel(const StreamArgs a) {
   extern __shared__ uint32_t hist[];
@@ -1482,6 +1490,7 @@ __global__ void __launch_bounds__(1024) stream_step_kernel(const StreamArgs a) {
   __shared__ unsigned long long s_dT;
   DevState* st = a.st;
   const uint32_t lane = threadIdx.x & 31;
+  if (a.prof && blockIdx.x == 0 && threadIdx.x == 0) a.prof[5] = gtimer();
   if (threadIdx.x == 0) {
     const double mu = sketch_mean(st, a.tables);
     s_cut = mu - a.alpha;
@@ -1536,33 +1545,39 @@ __global__ void __launch_bounds__(1024) stream_step_kernel(const StreamArgs a) {
   }
   __threadfence();
   cg::this_grid().sync();
-  // ---- insert: block b owns tables b, b + gridDim.x, ...
+  if (a.prof && blockIdx.x == 0 && threadIdx.x == 0) a.prof[6] = gtimer();
+  // ---- insert.  With 2 L <= grid (and a scratch table per table) two blocks
+  // share a table: the second counts half the rows and publishes its
+  // histogram, and after a second grid barrier the owner merges it; else
+  // block b owns tables b, b + gridDim.x, ... alone.
   const uint32_t nb = 1u << a.k_bits;
+  const uint32_t parts = (a.scratch && 2u * a.tables <= gridDim.x) ? 2u : 1u;
   unsigned long long dT = 0ull;
-  for (uint32_t t = blockIdx.x; t < a.tables; t += gridDim.x) {
+  constexpr int kDepth = 8;
+  auto count_rows = [&](const uint32_t* src, uint64_t r0, uint64_t r1) {
     for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
     __syncthreads();
-    const uint32_t* src = a.ids + static_cast<uint64_t>(t) * a.stride;
-    constexpr int kDepth = 8;
-    for (uint64_t i0 = 0; i0 < a.n; i0 += kDepth * blockDim.x) {
+    for (uint64_t i0 = r0; i0 < r1; i0 += kDepth * blockDim.x) {
       uint32_t idv[kDepth];
 #pragma unroll
       for (int u = 0; u < kDepth; ++u) {
         const uint64_t i = i0 + u * blockDim.x + threadIdx.x;
-        idv[u] = i < a.n ? __ldg(src + i) : 0xffffffffu;
+        idv[u] = i < r1 ? __ldg(src + i) : 0xffffffffu;
       }
 #pragma unroll
       for (int u = 0; u < kDepth; ++u)
         if (idv[u] != 0xffffffffu) atomicAdd(&hist[idv[u]], 1u);
     }
     __syncthreads();
+  };
+  auto merge = [&](uint32_t t, const uint32_t* other) {
     uint32_t* ct = a.counters + (static_cast<uint64_t>(t) << a.k_bits);
     for (uint32_t b0 = threadIdx.x; b0 < nb; b0 += kDepth * blockDim.x) {
       uint32_t m[kDepth], o[kDepth];
 #pragma unroll
       for (int u = 0; u < kDepth; ++u) {
         const uint32_t b = b0 + u * blockDim.x;
-        m[u] = b < nb ? hist[b] : 0u;
+        m[u] = b < nb ? hist[b] + (other ? __ldcg(other + b) : 0u) : 0u;
       }
 #pragma unroll
       for (int u = 0; u < kDepth; ++u) o[u] = m[u] ? ct[b0 + u * blockDim.x] : 0u;
@@ -1574,6 +1589,25 @@ __global__ void __launch_bounds__(1024) stream_step_kernel(const StreamArgs a) {
         }
     }
     __syncthreads();
+  };
+  if (parts == 2) {
+    const uint32_t t = blockIdx.x >> 1, p = blockIdx.x & 1u;
+    const bool live = t < a.tables;
+    if (live) {
+      count_rows(a.ids + static_cast<uint64_t>(t) * a.stride, p ? a.n / 2 : 0, p ? a.n : a.n / 2);
+      if (p == 1u) {
+        uint32_t* sc = a.scratch + (static_cast<uint64_t>(t) << a.k_bits);
+        for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) sc[b] = hist[b];
+      }
+    }
+    __threadfence();
+    cg::this_grid().sync();
+    if (live && p == 0u) merge(t, a.scratch + (static_cast<uint64_t>(t) << a.k_bits));
+  } else {
+    for (uint32_t t = blockIdx.x; t < a.tables; t += gridDim.x) {
+      count_rows(a.ids + static_cast<uint64_t>(t) * a.stride, 0, a.n);
+      merge(t, nullptr);
+    }
   }
   dT = warp_sum_u64(dT);
   if (lane == 0 && dT) atomicAdd(&s_dT, dT);
@@ -1581,6 +1615,7 @@ __global__ void __launch_bounds__(1024) stream_step_kernel(const StreamArgs a) {
   if (threadIdx.x == 0) {
     if (s_dT) atomicAdd(&st->T, s_dT);
     if (blockIdx.x == 0) atomicAdd(&st->n, a.n);
+    if (a.prof) atomicMax(&a.prof[7], gtimer());
   }
 }
 
@@ -1807,7 +1842,7 @@ cudaError_t launch_stream_score(const uint32_t* ids, uint64_t n, uint32_t tables
 
 cudaError_t launch_stream_step(const uint32_t* ids, uint64_t n, uint64_t ids_stride, uint32_t tables, uint32_t k_bits,
                                uint32_t* counters, double alpha, uint32_t* flag_bits, double* scores, DevState* st,
-                               cudaStream_t s) {
+                               cudaStream_t s, uint32_t* scratch) {
   if (n == 0) return cudaSuccess;
   if (k_bits > 15) return cudaErrorInvalidValue;
   static int sms = 0;
@@ -1834,6 +1869,14 @@ cudaError_t launch_stream_step(const uint32_t* ids, uint64_t n, uint64_t ids_str
   a.flag_bits = flag_bits;
   a.scores = scores;
   a.st = st;
+  a.scratch = scratch;
+  static int prof_env = -1;
+  if (prof_env < 0) prof_env = getenv("ACE_TAIL_PROF") ? 1 : 0;
+  if (prof_env) {
+    if (!g_tail_prof) cudaMalloc(&g_tail_prof, 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(g_tail_prof, 0, 8 * sizeof(unsigned long long), s);
+    a.prof = g_tail_prof;
+  }
   void* args[] = {&a};
   const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(stream_step_kernel), dim3(sms),
                                                     dim3(1024), args, sizeof(uint32_t) << k_bits, s);

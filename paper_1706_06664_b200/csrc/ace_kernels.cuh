@@ -70,9 +70,10 @@ cudaError_t launch_stream_score(const uint32_t* ids, uint64_t n, uint32_t tables
 // One streaming batch (32-bit, unsaturable, K <= 15) in one cooperative
 // launch: score + flag against the counts at batch start, then insert with T
 // updated exactly (no sum-of-squares pass).
+// scratch: L x 2^K u32 lets two blocks share each table's insert (or null).
 cudaError_t launch_stream_step(const uint32_t* ids, uint64_t n, uint64_t ids_stride, uint32_t tables, uint32_t k_bits,
                                uint32_t* counters, double alpha, uint32_t* flag_bits, double* scores, DevState* st,
-                               cudaStream_t s);
+                               cudaStream_t s, uint32_t* scratch = nullptr);
 
 // Sum of squares of all counters (T after restore with exact state).
 cudaError_t launch_sum_squares(const uint32_t* counters, uint64_t num,
