@@ -1216,7 +1216,7 @@ ace_status ace_sketch_stream_batch(AceSketch* sk, const void* x, int dtype, uint
   }
   uint32_t* dflags = (flag_bits && out_where == ACE_DEVICE) ? flag_bits : sk->flags.as<uint32_t>();
   if (stream_fused_ok(sk, fire_and_forget_ok(sk, n))) {
-    ACE_CUDA(sk->demand.ensure(sk->num_counters * sizeof(uint32_t)));
+    if (stream_split_env()) ACE_CUDA(sk->demand.ensure(sk->num_counters * sizeof(uint32_t)));
     ACE_CUDA(launch_stream_step(sk->ids.as<uint32_t>(), n, n, f->d.tables, f->d.k_bits, sk->counters, alpha, dflags,
                                 dsc, sk->st, sk->stream, stream_split_env() ? sk->demand.as<uint32_t>() : nullptr));
     sk->mark(2);
@@ -1296,7 +1296,7 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
       if (batch_ms && b != g0) ACE_CUDA(cudaEventRecord(ev[b], sk->stream));
       const uint32_t* ids = sk->ids.as<uint32_t>() + (r0 - gr0);
       if (stream_fused_ok(sk, ff)) {
-        ACE_CUDA(sk->demand.ensure(sk->num_counters * sizeof(uint32_t)));
+        if (stream_split_env()) ACE_CUDA(sk->demand.ensure(sk->num_counters * sizeof(uint32_t)));
         ACE_CUDA(launch_stream_step(ids, rows, grows, f->d.tables, f->d.k_bits, sk->counters, alpha, dflags + r0 / 32,
                                     nullptr, sk->st, sk->stream, stream_split_env() ? sk->demand.as<uint32_t>() : nullptr));
         continue;
