@@ -1025,16 +1025,8 @@ ace_status batch_detect(AceSketch* sk, const void* x, int dtype, uint64_t n, uin
   // measured: a gain where the tables fit one shared-memory histogram and the
   // gathers dominate (cfg 2: 0.541 -> 0.525 ms); a loss on small batches
   // (cfg 1) and even on cfg 3 (K = 16, two parts)
-  // ACE_OWNER_ROWS (off): small batches counted by the tail's table-owning
-  // blocks (n <= ACE_OWNER_ROWS, L <= SMs, K <= 15)
-  static int owner_rows = -1;
-  if (owner_rows < 0) {
-    const char* e = getenv("ACE_OWNER_ROWS");
-    owner_rows = e ? atoi(e) : 0;
-  }
-  const bool owner_ok = sk->fam->d.k_bits <= 15 && sk->fam->d.tables <= 148 && n <= static_cast<uint64_t>(owner_rows);
   sk->defer_insert = gather_env != 0 && build && sk->width == 32 && sk->fam->use_tc() &&
-                     (gather_env == 2 || owner_ok || (sk->fam->d.k_bits <= 16 && n * sk->fam->d.tables >= (16ull << 20))) &&
+                     (gather_env == 2 || (sk->fam->d.k_bits <= 16 && n * sk->fam->d.tables >= (16ull << 20))) &&
                      sk->fam->d.k_bits <= 16 && fire_and_forget_ok(sk, n);
   sk->insert_deferred = false;
   AceSketch::GraphKey key;

@@ -1332,79 +1332,6 @@ __global__ void __launch_bounds__(1024) detect_tail_kernel(const TailArgs a) {
   DevState* st = a.st;
   const int lane = threadIdx.x & 31;
   tail_stamp(a, 0);
-  if (a.gather == 3) {
-    // table-owning blocks (small batches): count the table's ids, merge with
-    // the existing counts by plain read-modify-write (no other block writes
-    // the table), T += c^2, and replace the ids by their counts from the same
-    // shared table; no cross-block merge, one grid barrier
-    const uint32_t nb = 1u << a.k_bits;
-    unsigned long long dT = 0ull;
-    if (threadIdx.x == 0) blk = 0ull;
-    for (uint32_t t = blockIdx.x; t < a.tables; t += gridDim.x) {
-      for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
-      __syncthreads();
-      const uint64_t g0 = static_cast<uint64_t>(t) * a.n, g1 = g0 + a.n;
-      const uint64_t va = min(g1, (g0 + 3u) & ~static_cast<uint64_t>(3)), nv = (g1 - va) >> 2, vz = va + (nv << 2);
-      for (uint64_t i = g0 + threadIdx.x; i < va; i += blockDim.x) atomicAdd(&hist[a.ids[i]], 1u);
-      for (uint64_t i = vz + threadIdx.x; i < g1; i += blockDim.x) atomicAdd(&hist[a.ids[i]], 1u);
-      const uint4* v4 = reinterpret_cast<const uint4*>(a.ids + va);
-      for (uint64_t base = 0; base < nv; base += 4u * blockDim.x) {
-        uint4 q[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) q[u] = v4[min(base + u * blockDim.x + threadIdx.x, nv - 1u)];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (base + u * blockDim.x + threadIdx.x < nv) {
-            atomicAdd(&hist[q[u].x], 1u);
-            atomicAdd(&hist[q[u].y], 1u);
-            atomicAdd(&hist[q[u].z], 1u);
-            atomicAdd(&hist[q[u].w], 1u);
-          }
-      }
-      __syncthreads();
-      uint32_t* ct = a.counters + (static_cast<uint64_t>(t) << a.k_bits);
-      for (uint32_t b0 = threadIdx.x; b0 < nb; b0 += 8u * blockDim.x) {
-        uint32_t o[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) o[u] = b0 + u * blockDim.x < nb ? ct[b0 + u * blockDim.x] : 0u;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t b = b0 + u * blockDim.x;
-          if (b < nb) {
-            const uint32_t c = o[u] + hist[b];
-            if (c != o[u]) ct[b] = c;
-            hist[b] = c;
-            dT += static_cast<unsigned long long>(c) * c;
-          }
-        }
-      }
-      __syncthreads();
-      for (uint64_t i = g0 + threadIdx.x; i < va; i += blockDim.x) a.ids[i] = hist[a.ids[i]];
-      for (uint64_t i = vz + threadIdx.x; i < g1; i += blockDim.x) a.ids[i] = hist[a.ids[i]];
-      uint4* w4 = reinterpret_cast<uint4*>(a.ids + va);
-      for (uint64_t base = 0; base < nv; base += 4u * blockDim.x) {
-        uint4 q[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) q[u] = w4[min(base + u * blockDim.x + threadIdx.x, nv - 1u)];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint64_t j = base + u * blockDim.x + threadIdx.x;
-          if (j < nv) w4[j] = make_uint4(hist[q[u].x], hist[q[u].y], hist[q[u].z], hist[q[u].w]);
-        }
-      }
-      __syncthreads();
-    }
-    dT = warp_sum_u64(dT);
-    if (lane == 0 && dT) atomicAdd(&blk, dT);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      if (blk) atomicAdd(&st->T, blk);
-      if (blockIdx.x == 0) atomicAdd(&st->n, a.n);
-    }
-    __threadfence();
-    grid.sync();
-    tail_stamp(a, 2);
-  }
   if (a.gather == 1) {
     const uint32_t pshift = a.k_bits - a.part_bits, parts = 1u << pshift;
     const uint32_t part = blockIdx.x & (parts - 1u);
@@ -1819,22 +1746,6 @@ cudaError_t launch_detect_tail(uint32_t* ids, uint64_t n, uint32_t tables, uint3
   if (pair_env < 0) {
     const char* e = getenv("ACE_PAIR_GATHER");
     pair_env = e ? atoi(e) : 0;
-  }
-  // ACE_OWNER_ROWS=n: batches of up to n rows counted by table-owning blocks
-  // in the tail itself (gather = 3).  Measured slower on cfg 1 (0.175 vs
-  // 0.153 ms per step): one SM per table serialises the clustered data's
-  // same-bucket shared atomics.
-  static int owner_env = -1;
-  if (owner_env < 0) {
-    const char* e = getenv("ACE_OWNER_ROWS");
-    owner_env = e ? atoi(e) : 0;
-  }
-  if (gather == 1 && k_bits <= 15 && tables <= static_cast<uint32_t>(sms) && n <= static_cast<uint64_t>(owner_env)) {
-    gather = 3;
-    a.gather = 3;
-    smem = std::max<size_t>(smem, sizeof(uint32_t) << k_bits);
-    const cudaError_t e = cudaMemsetAsync(&st->T, 0, sizeof(unsigned long long), s);
-    if (e != cudaSuccess) return e;
   }
   if (gather == 1 && k_bits <= 15 && pair_env) {
     static bool pcfg = false;
