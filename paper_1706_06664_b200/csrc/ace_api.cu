@@ -1065,7 +1065,9 @@ ace_status batch_detect(AceSketch* sk, const void* x, int dtype, uint64_t n, uin
   }
   if (pinned && chunks_env > 1 && !sk->timing && sk->fam->use_tc() && !tc_kstream(sk->fam->tc.nkc) &&
       n >= static_cast<uint64_t>(chunks_env) * 16384u) {
-    const uint64_t rows_c = ((n + chunks_env - 1) / chunks_env + 127) / 128 * 128;
+    // chunk boundaries: chunks_env - 1 equal chunks and a last one of a quarter
+    // of their size (only the last chunk's hashing follows the transfer)
+    const uint64_t rows_c = ((n * 4 + (4 * chunks_env - 3) - 1) / (4 * chunks_env - 3) + 127) / 128 * 128;
     const size_t esz = dtype == ACE_F64 ? 8 : 4;
     ACE_CUDA(zero_call_fields(sk));
     ACE_CUDA(sk->stage.ensure(n * ld * esz));

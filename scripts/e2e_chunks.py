@@ -35,3 +35,21 @@ for _ in range(15):
 ts.sort()
 print(f"chunks={os.environ.get('ACE_H2D_CHUNKS', '8')} cfg{cfg} e2e median {ts[len(ts)//2]*1e3:.3f} ms "
       f"min {ts[0]*1e3:.3f} ms -> {n / ts[len(ts)//2]:.4g} points/s")
+
+# the C-ABI call alone (host rows in, host flag bitmap out), as a C/C++ caller makes it
+import ctypes as C
+import numpy as np
+from paper_1706_06664_b200 import _native as N
+p = ace._Points(xnp, w.dim)
+bits = np.zeros((n + 31) // 32, dtype=np.uint32)
+rep = N.AceBatchReport()
+st = N.AceHashStats()
+fn = N.dev().ace_sketch_build_detect
+ts = []
+for _ in range(15):
+    t0 = time.perf_counter()
+    sk.reset()
+    assert fn(sk._h, p.ptr, p.dtype, p.n, p.ld, p.where, bits.ctypes.data, None, N.ACE_HOST, C.byref(rep), C.byref(st)) == 0
+    ts.append(time.perf_counter() - t0)
+ts.sort()
+print(f"C-ABI call: median {ts[len(ts)//2]*1e3:.3f} ms min {ts[0]*1e3:.3f} ms -> {n / ts[len(ts)//2]:.4g} points/s")
