@@ -861,8 +861,12 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a) {
             const uint32_t ah = a_base + kc * 2u * kBlockBytes;
 #pragma unroll
             for (uint32_t kk = 0; kk < 4; ++kk) {
-              tmem_cp_128x256b(ta_hi + (kc * 4u + kk) * 8u, sw128_desc(ah + kk * 32u));
-              tmem_cp_128x256b(ta_lo + (kc * 4u + kk) * 8u, sw128_desc(ah + kBlockBytes + kk * 32u));
+              // one copy per K16 step and operand; steps whose MMAs are all
+              // skipped (past d, or a zero x lo part) are not copied either
+              const uint32_t step = kc * 4u + kk;
+              if (step >= nsteps) break;
+              tmem_cp_128x256b(ta_hi + step * 8u, sw128_desc(ah + kk * 32u));
+              if ((lm >> step) & 1u) tmem_cp_128x256b(ta_lo + step * 8u, sw128_desc(ah + kBlockBytes + kk * 32u));
             }
           }
           mma_commit(&bar_aempty[0]);  // shared-memory A free once the copies land
