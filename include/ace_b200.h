@@ -54,6 +54,9 @@ typedef struct {
   uint64_t rechecked;   /* projections inside the fast-path error margin,
                            recomputed as the reference's FP64 fold        */
   uint64_t flipped;     /* rechecked projections whose fast sign was wrong */
+  uint64_t near_ties;   /* projections with |<x,w>| < 1e-6 |x| |w| (the
+                           BASELINE.json near-tie measure, evaluated on the
+                           exact fold as the oracle does)                  */
 } AceHashStats;
 
 /* detect_batch result (detect.hpp:12-22 DetectionReport + exactness info). */
@@ -208,7 +211,8 @@ uint64_t ace_kernel_launches(void);
 /* Phase timing with CUDA events on the sketch's stream (off by default):
  * after each call, ms[0] = hash (+ recheck + insert), ms[1] = score,
  * ms[2] = threshold + flags (batch) or stream flags + insert (stream),
- * ms[3] = x conversion pre-pass, ms[4] = tcgen05 projection kernel. */
+ * ms[3] = x conversion pre-pass (0 where the projection kernel converts the
+ * raw rows itself, d <= 256), ms[4] = tcgen05 projection kernel. */
 ace_status ace_sketch_set_timing(AceSketch* sk, int enable);
 ace_status ace_sketch_timings(const AceSketch* sk, double* ms5);
 

@@ -53,6 +53,8 @@ class Oracle:
         L.ora_project.argtypes = [_vp, _vp, _u64]
         L.ora_buckets.restype = _u64
         L.ora_buckets.argtypes = [_vp, _u64, _u32, _u32, _vp, _i, _u64, _vp, _i, _d]
+        L.ora_buckets_fast.restype = _u64
+        L.ora_buckets_fast.argtypes = [_vp, _u64, _u32, _u32, _vp, _i, _u64, _vp, _i, _d]
         L.ora_sketch_new.restype = _vp
         L.ora_sketch_new.argtypes = [_u32, _u32, _u32]
         L.ora_sketch_free.argtypes = [_vp]
@@ -78,16 +80,18 @@ class Oracle:
         self.L.ora_directions(seed, dim, k, l, w.ctypes.data)
         return w
 
-    def buckets(self, w, x, k, l, threads=None, rel_eps=0.0):
-        """(ids (L, n) uint32, near-tie count below rel_eps)."""
+    def buckets(self, w, x, k, l, threads=None, rel_eps=0.0, fast=True):
+        """(ids (L, n) uint32, near-tie count below rel_eps).  fast: the
+        row-blocked fold (ora_buckets_fast, same bits); else the scalar one."""
         x = np.ascontiguousarray(x)
         is64 = x.dtype == np.float64
         if not is64:
             x = _f32(x)
         n, dim = x.shape
         ids = np.empty((l, n), dtype=np.uint32)
-        near = self.L.ora_buckets(np.ascontiguousarray(w).ctypes.data, dim, k, l, x.ctypes.data,
-                                  int(is64), n, ids.ctypes.data, threads or _threads(), rel_eps)
+        fn = self.L.ora_buckets_fast if fast else self.L.ora_buckets
+        near = fn(np.ascontiguousarray(w).ctypes.data, dim, k, l, x.ctypes.data,
+                  int(is64), n, ids.ctypes.data, threads or _threads(), rel_eps)
         return ids, int(near)
 
     def project(self, wrow, x) -> float:

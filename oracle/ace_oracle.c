@@ -9,7 +9,7 @@
  * It restates, in plain C, the algorithm of the reference C++ sources under
  * /root/reference/proj (cited file:line per function).  It is pinned against
  * the compiled reference itself (oracle/_ref/libaceref.so, built by
- * oracle/Makefile from the reference sources) by tests/test_oracle_pin.py and
+ * oracle/Makefile from the reference sources) by tests/test_cpu_oracle.py and
  * against the committed golden digests in tests/golden/.
  *
  * Build: gcc -O2 -ffp-contract=off -fPIC -shared (see oracle/Makefile).  The
@@ -97,17 +97,16 @@ uint32_t ora_bucket(const double* w, uint64_t dim, uint32_t k_bits,
   return idx;
 }
 
-/* Relative projection magnitude |p| / (|x| |w|) — the BASELINE.json near-tie
- * measure (|<x,w>| < 1e-6 |x||w|).  Not a reference function. */
-double ora_rel_margin(const double* wrow, const double* x, uint64_t dim) {
+/* The BASELINE.json near-tie predicate |<x,w>| < eps |x| |w| (strict, so an
+ * all-zero row is not a near tie).  Not a reference function. */
+int ora_near_tie(const double* wrow, const double* x, uint64_t dim, double eps) {
   double nx = 0.0, nw = 0.0;
   for (uint64_t i = 0; i < dim; ++i) {
     nx += x[i] * x[i];
     nw += wrow[i] * wrow[i];
   }
   const double p = ora_project(wrow, x, dim);
-  const double den = sqrt(nx) * sqrt(nw);
-  return den > 0 ? fabs(p) / den : 0.0;
+  return fabs(p) < eps * (sqrt(nx) * sqrt(nw));
 }
 
 /* Bucket ids of rows X (n x dim, fp32 or fp64) for every table, table-major
@@ -137,18 +136,116 @@ static void* ora_bucket_worker(void* arg) {
       j->ids[t * j->n + i] = ora_bucket(j->w, j->dim, j->k_bits, t, xd);
       if (j->rel_eps > 0)
         for (uint64_t b = 0; b < j->k_bits; ++b)
-          if (ora_rel_margin(j->w + (t * j->k_bits + b) * j->dim, xd, j->dim) <
-              j->rel_eps)
-            ++j->near;
+          j->near += ora_near_tie(j->w + (t * j->k_bits + b) * j->dim, xd, j->dim,
+                                  j->rel_eps);
     }
   }
   free(xd);
   return NULL;
 }
 
+/* The same ids, faster: ORA_RB rows at a time, each (row, direction) still
+ * the sequential left fold of srp.cpp:84 (one independent accumulator per row,
+ * mul then add, never fused: -ffp-contract=off), so the bits are those of
+ * ora_bucket; the rows only run side by side as vector lanes.  Used to pin
+ * the full-size configurations (tests/golden/make_golden_full.py), where the
+ * scalar fold would take hours. */
+#define ORA_RB 64
+typedef double ora_v4 __attribute__((vector_size(64)));
+
+__attribute__((target_clones("avx512f", "avx2", "default")))
+static void ora_block_project(const double* w, uint64_t dim, uint64_t ndir,
+                              const double* xt, double* p) {
+  for (uint64_t r = 0; r < ndir; ++r) {
+    const double* wr = w + r * dim;
+    ora_v4 a[ORA_RB / 8];
+    for (int v = 0; v < ORA_RB / 8; ++v) a[v] = (ora_v4){0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (uint64_t i = 0; i < dim; ++i) {
+      const double s = wr[i];
+      const ora_v4 wb = {s, s, s, s, s, s, s, s};
+      const ora_v4* xv = (const ora_v4*)(xt + i * ORA_RB);
+      for (int v = 0; v < ORA_RB / 8; ++v) {
+        const ora_v4 prod = wb * xv[v];
+        a[v] = a[v] + prod;
+      }
+    }
+    ora_v4* pv = (ora_v4*)(p + r * ORA_RB);
+    for (int v = 0; v < ORA_RB / 8; ++v) pv[v] = a[v];
+  }
+}
+
+static void* ora_bucket_worker_fast(void* arg) {
+  ora_bucket_job* j = (ora_bucket_job*)arg;
+  const uint64_t ndir = (uint64_t)j->k_bits * j->tables;
+  double* xt = (double*)aligned_alloc(64, sizeof(double) * j->dim * ORA_RB);
+  double* p = (double*)aligned_alloc(64, sizeof(double) * j->k_bits * ORA_RB);
+  double* wn = NULL;
+  double xn[ORA_RB];
+  if (j->rel_eps > 0) { /* |w| per direction, as ora_near_tie computes it */
+    wn = (double*)malloc(sizeof(double) * ndir);
+    for (uint64_t r = 0; r < ndir; ++r) {
+      double s = 0.0;
+      for (uint64_t i = 0; i < j->dim; ++i) s += j->w[r * j->dim + i] * j->w[r * j->dim + i];
+      wn[r] = sqrt(s);
+    }
+  }
+  for (uint64_t i0 = j->row0; i0 < j->row1; i0 += ORA_RB) {
+    const uint64_t m = j->row1 - i0 < ORA_RB ? j->row1 - i0 : ORA_RB;
+    for (uint64_t k = 0; k < ORA_RB; ++k) {
+      const uint64_t row = i0 + (k < m ? k : 0);
+      for (uint64_t c = 0; c < j->dim; ++c)
+        xt[c * ORA_RB + k] = j->x_is_f64 ? ((const double*)j->x)[row * j->dim + c]
+                                         : (double)((const float*)j->x)[row * j->dim + c];
+    }
+    if (wn)
+      for (uint64_t k = 0; k < m; ++k) {
+        double s = 0.0;
+        for (uint64_t c = 0; c < j->dim; ++c) s += xt[c * ORA_RB + k] * xt[c * ORA_RB + k];
+        xn[k] = sqrt(s);
+      }
+    for (uint64_t t = 0; t < j->tables; ++t) {
+      ora_block_project(j->w + t * j->k_bits * j->dim, j->dim, j->k_bits, xt, p);
+      for (uint64_t k = 0; k < m; ++k) {
+        uint32_t idx = 0;
+        for (uint64_t b = 0; b < j->k_bits; ++b) {
+          const uint64_t r = t * j->k_bits + b;
+          const double v = p[b * ORA_RB + k];
+          idx = (idx << 1) | (v >= 0.0 ? 1u : 0u);
+          if (wn) j->near += fabs(v) < j->rel_eps * (xn[k] * wn[r]);
+        }
+        j->ids[t * j->n + i0 + k] = idx;
+      }
+    }
+  }
+  free(xt);
+  free(p);
+  free(wn);
+  return NULL;
+}
+
+static uint64_t ora_buckets_run(void* (*worker)(void*), const double* w, uint64_t dim,
+                                uint32_t k_bits, uint32_t tables, const void* x,
+                                int x_is_f64, uint64_t n, uint32_t* ids, int threads,
+                                double rel_eps);
+
 uint64_t ora_buckets(const double* w, uint64_t dim, uint32_t k_bits,
                      uint32_t tables, const void* x, int x_is_f64, uint64_t n,
                      uint32_t* ids, int threads, double rel_eps) {
+  return ora_buckets_run(ora_bucket_worker, w, dim, k_bits, tables, x, x_is_f64, n, ids,
+                         threads, rel_eps);
+}
+
+uint64_t ora_buckets_fast(const double* w, uint64_t dim, uint32_t k_bits,
+                          uint32_t tables, const void* x, int x_is_f64, uint64_t n,
+                          uint32_t* ids, int threads, double rel_eps) {
+  return ora_buckets_run(ora_bucket_worker_fast, w, dim, k_bits, tables, x, x_is_f64, n,
+                         ids, threads, rel_eps);
+}
+
+static uint64_t ora_buckets_run(void* (*worker)(void*), const double* w, uint64_t dim,
+                                uint32_t k_bits, uint32_t tables, const void* x,
+                                int x_is_f64, uint64_t n, uint32_t* ids, int threads,
+                                double rel_eps) {
   if (threads < 1) threads = 1;
   pthread_t* tid = (pthread_t*)malloc(sizeof(pthread_t) * threads);
   ora_bucket_job* jobs = (ora_bucket_job*)malloc(sizeof(ora_bucket_job) * threads);
@@ -159,7 +256,7 @@ uint64_t ora_buckets(const double* w, uint64_t dim, uint32_t k_bits,
     if (b > n) b = n;
     ora_bucket_job j = {w, x, x_is_f64, dim, n, a, b, k_bits, tables, ids, rel_eps, 0};
     jobs[t] = j;
-    pthread_create(&tid[t], NULL, ora_bucket_worker, &jobs[t]);
+    pthread_create(&tid[t], NULL, worker, &jobs[t]);
   }
   uint64_t near = 0;
   for (int t = 0; t < threads; ++t) {

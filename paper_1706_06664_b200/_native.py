@@ -17,7 +17,8 @@ ACE_HOST, ACE_DEVICE = 0, 1
 
 
 class AceHashStats(C.Structure):
-    _fields_ = [("projections", C.c_uint64), ("rechecked", C.c_uint64), ("flipped", C.c_uint64)]
+    _fields_ = [("projections", C.c_uint64), ("rechecked", C.c_uint64), ("flipped", C.c_uint64),
+                ("near_ties", C.c_uint64)]
 
 
 class AceBatchReport(C.Structure):

@@ -44,7 +44,7 @@ def _stale(out: Path, deps: list[Path]) -> bool:
 
 def build_dev(force: bool = False) -> Path:
     out = LIB / "libace_dev.so"
-    srcs = [CSRC / "ace_api.cu", CSRC / "ace_kernels.cu", CSRC / "ace_hash_tc.cu"]
+    srcs = [CSRC / "ace_api.cu", CSRC / "ace_kernels.cu", CSRC / "ace_hash_tc.cu", CSRC / "ace_hash_tck.cu"]
     deps = srcs + list(CSRC.glob("*.cuh")) + [INC / "ace_b200.h"]
     if force or _stale(out, deps):
         _run([_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
@@ -71,14 +71,6 @@ def build_datagen(force: bool = False) -> Path:
     return out
 
 
-def build_probe(force: bool = False) -> Path:
-    out = LIB / "ace_probe"
-    src = CSRC / "probe.cu"
-    if force or _stale(out, [src]):
-        _run([_nvcc(), *ARCH, "-O3", "-o", str(out), str(src)])
-    return out
-
-
 def build_cpp_test(force: bool = False) -> Path:
     """The drop-in C++ test program (tests/cpp/test_dropin.cpp) against
     include/ace/*.hpp + libace.so; run on the GPU by tests/test_cpp_dropin_gpu.py."""
@@ -102,7 +94,6 @@ def build_all(force: bool = False) -> None:
     build_dev(force)
     build_host(force)
     build_datagen(force)
-    build_probe(force)
     build_cpp_test(force)
     build_oracle()
 

@@ -28,7 +28,6 @@ void set_error(const std::string& msg) { g_err = msg; }
 using namespace ace_dev;
 
 namespace {
-unsigned long long* g_tc_prof = nullptr;
 
 constexpr uint32_t kMaxKBits = 30;  // srp.cpp:15
 
@@ -104,7 +103,7 @@ struct AceSketch {
   cudaStream_t cstream = nullptr;
   cudaEvent_t cstart = nullptr;
   std::vector<cudaEvent_t> cev;
-  DevBuf ids, sums, stage, flags, scores, demand, near, overflow, x16, rowthr, segc, lomask;
+  DevBuf ids, sums, stage, flags, scores, demand, near, overflow, x16, rowthr, segc, xf32;
   // build + detect over the same rows: run_hash leaves the insert to the
   // fused count-and-gather pass of the detect tail (detect_tail_kernel)
   bool defer_insert = false, insert_deferred = false;
@@ -165,6 +164,7 @@ void family_release(AceFamily* f) {
     cudaFree(f->d.w64);
     cudaFree(f->d.w32t);
     cudaFree(f->d.wnorm);
+    cudaFree(f->d.wnorm64);
     tc_free_family(&f->tc);
     delete f;
   }
@@ -238,8 +238,7 @@ ace_status pull_state(AceSketch* sk) {
 
 double host_mean(const DevState& s, uint32_t tables) {
   if (s.n == 0) return 0.0;
-  const unsigned long long den = s.n * tables;
-  return static_cast<double>(s.T / den) + static_cast<double>(s.T % den) / static_cast<double>(den);
+  return ace_div_rn(s.T, s.n * tables);
 }
 
 void fill_stats(AceHashStats* stats, const DevState& s, uint64_t n, const AceFamily* f) {
@@ -247,6 +246,7 @@ void fill_stats(AceHashStats* stats, const DevState& s, uint64_t n, const AceFam
   stats->projections = n * f->d.rows;
   stats->rechecked = s.rechecked;
   stats->flipped = s.flipped;
+  stats->near_ties = s.near_ties;
 }
 
 ace_status copy_out(void* dst, const void* src, size_t bytes, int where, cudaStream_t s) {
@@ -300,6 +300,7 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
   for (bool& u : sk->ev_used) u = false;
   sk->mark(0);
   if (f->use_tc()) {
+    const bool kstream = tc_kstream(f->tc.nkc);
     TcArgs t{};
     t.x = xd;
     t.x_f64 = dtype == ACE_F64;
@@ -308,23 +309,19 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
     t.dim = f->d.dim;
     t.k_bits = f->d.k_bits;
     t.tables = f->d.tables;
-    t.tpt = f->tc.tpt ? f->tc.tpt : f->d.tpt;
+    t.tpt = f->tc.tpt;
     t.ntiles = f->tc.ntiles;
     t.nkc = f->tc.nkc;
     t.tw = f->tc.tw;
     t.w16 = f->tc.w16;
     tc_fill_tables(&t);
-    // error bound of the fp16x3 split relative to ||x~|| ||w^||
-    const bool kstream = tc_kstream(f->tc.nkc);
-    t.margin_c = kstream ? tck_margin(f->tc.nkc, t.x_f64 != 0)
-                         : static_cast<float>(2.0 * (4.0 * 0x1.0p-22 + 0x1.0p-23 * (12.0 * f->tc.nkc + 16.0) * 1.01 +
-                                                     (t.x_f64 ? 0x1.0p-23 : 0.0)));
+    t.margin_c = kstream ? tck_margin(f->tc.nkc, t.x_f64 != 0) : tc_margin(f->tc.nkc, t.x_f64 != 0);
     t.ids = ids_out;
     t.ids_ld = ids_ld;
     // near-tie list: the K-streamed path's bound (large d, dense data) leaves
     // far more near ties per row, size its list accordingly
-    uint64_t cap = tc_kstream(f->tc.nkc) ? n * f->d.rows / 48 : n * f->d.rows / 1024;
-    cap = std::min<uint64_t>(std::max<uint64_t>(cap, 1u << 20), tc_kstream(f->tc.nkc) ? (1u << 27) : (1u << 25));
+    uint64_t cap = kstream ? n * f->d.rows / 48 : n * f->d.rows / 1024;
+    cap = std::min<uint64_t>(std::max<uint64_t>(cap, 1u << 20), kstream ? (1u << 27) : (1u << 25));
     {
       // the kernel's near-tie list is all ~0 between launches (entries are
       // reset as they are rechecked); fill a newly allocated one
@@ -335,46 +332,20 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
     ACE_CUDA(sk->overflow.ensure(((n + 31) / 32) * sizeof(uint32_t)));
     ACE_CUDA(cudaMemsetAsync(sk->overflow.p, 0, ((n + 31) / 32) * sizeof(uint32_t), sk->stream));
     ACE_CUDA(cudaMemsetAsync(&sk->st->near_count, 0, 2 * sizeof(unsigned long long), sk->stream));
-    const uint64_t tiles = (n + 127) / 128;
-    ACE_CUDA(sk->x16.ensure(tiles * f->tc.nkc * 2 * 16384));
-    ACE_CUDA(sk->rowthr.ensure(tiles * 128 * sizeof(float)));
-    t.x16 = sk->x16.as<uint16_t>();
-    t.rowthr = sk->rowthr.as<float>();
     t.near_list = sk->near.as<unsigned long long>();
     t.near_cap = sk->near.bytes / sizeof(unsigned long long);
     t.overflow_rows = sk->overflow.as<uint32_t>();
     t.st = sk->st;
-    {
-      static int dbg = -1;
-      if (dbg < 0) {
-        const char* e = getenv("ACE_TC_DBG");
-        dbg = e ? atoi(e) : 0;
-      }
-      t.dbg = dbg;
-      static unsigned long long* prof = nullptr;
-      if (getenv("ACE_TC_PROF")) {
-        if (!prof) cudaMalloc(&prof, 32 * sizeof(unsigned long long));
-        cudaMemsetAsync(prof, 0, 32 * sizeof(unsigned long long), sk->stream);
-        cudaMemsetAsync(prof + 10, 0xff, sizeof(unsigned long long), sk->stream);  // min start
-      }
-      t.prof = prof;
-      g_tc_prof = prof;
-    }
-    // X conversion inside the projection kernel (opt-in, ACE_FUSE_CONVERT=1:
-    // two converter warps per CTA are slower than the pre-pass on cfg 2/3,
-    // 0.60 vs 0.27 + 0.11 ms) when the rows are plain contiguous fp32
-    static int fuse_env = -2;
-    if (fuse_env == -2) {
-      const char* e = getenv("ACE_FUSE_CONVERT");
-      fuse_env = e ? atoi(e) : 0;
-    }
-    t.fuse_convert = fuse_env != 0 && t.tw == 128 && !t.x_f64 && ld == f->d.dim && (reinterpret_cast<uintptr_t>(xd) & 15) == 0 &&
-                     tc_fuse_ok_dim(f->d.dim, f->tc.nkc);
+    t.w64 = f->d.w64;
+    t.wnorm64 = f->d.wnorm64;
+    t.counters = sk->counters;
     if (kstream) {
       // d > 256: K-streamed kernel with its own conversion and recheck
-      t.fuse_convert = 0;
-      t.fused_insert = 0;
-      t.w64 = f->d.w64;
+      const uint64_t tiles = (n + 127) / 128;
+      ACE_CUDA(sk->x16.ensure(tiles * f->tc.nkc * 2 * 16384));
+      ACE_CUDA(sk->rowthr.ensure(tiles * 128 * sizeof(float)));
+      t.x16 = sk->x16.as<uint16_t>();
+      t.rowthr = sk->rowthr.as<float>();
       ACE_CUDA(sk->segc.ensure(static_cast<size_t>(tck_grid(n)) * sizeof(uint32_t)));
       t.seg_counts = sk->segc.as<uint32_t>();
       t.w32 = f->tc.w32;
@@ -384,7 +355,7 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
       ACE_CUDA(launch_hash_tck(t, sk->stream));
       sk->mark(5);
       ACE_CUDA(launch_recheck_segs(t, sk->stream));
-      ACE_CUDA(launch_recheck(t, f->d.w64, sk->stream));
+      ACE_CUDA(launch_recheck(t, sk->stream));
       if (insert && sk->defer_insert)
         sk->insert_deferred = true;
       else if (insert)
@@ -395,55 +366,17 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
       sk->mark(1);
       return ACE_OK;
     }
-    sk->mark(4);
-    if (!t.fuse_convert) {
-      // per point tile: K16 steps whose x lo parts are not all zero
-      static int lomask_env = -2;
-      if (lomask_env == -2) {
-        const char* e = getenv("ACE_LO_SKIP");
-        lomask_env = e ? atoi(e) : 1;
-      }
-      if (lomask_env) {
-        ACE_CUDA(sk->lomask.ensure(tiles * sizeof(uint32_t)));
-        ACE_CUDA(cudaMemsetAsync(sk->lomask.p, 0, tiles * sizeof(uint32_t), sk->stream));
-        t.lomask = sk->lomask.as<uint32_t>();
-      }
-      ACE_CUDA(launch_convert_x(t, sk->stream));
-    }
-    sk->mark(6);
     // Fused epilogue insert (global REDs) only where the separate insert would
     // use global atomics too (K > 20); otherwise the shared-memory histogram
     // (split into 2^15-bin parts for K > 15) absorbs hot buckets far better.
-    static int fused_env = -2;
-    if (fused_env == -2) {
-      const char* e = getenv("ACE_FUSED_INSERT");
-      fused_env = e ? atoi(e) : -1;
-    }
-    const bool fused = insert && sk->width == 32 && fire_and_forget_ok(sk, n) &&
-                       (fused_env >= 0 ? fused_env == 1 : f->d.k_bits > 20);
-    t.w64 = f->d.w64;
-    t.counters = sk->counters;
+    const bool fused = insert && sk->width == 32 && fire_and_forget_ok(sk, n) && f->d.k_bits > 20;
     t.fused_insert = fused ? 1 : 0;
-    // ACE_EXT_RECHECK=1: near ties rechecked by a separate warp-per-item pass
-    // (recheck_segs_kernel) instead of inside the projection kernel (recheck
-    // warps and shared tail; not with the fused insert, whose recheck also
-    // moves counts).  Measured: cfg 2 0.463 (in-kernel) vs 0.472 ms per step,
-    // cfg 3 15.69 vs 15.59 ms, so off by default.
-    static int ext_env = -1;
-    if (ext_env < 0) {
-      const char* e = getenv("ACE_EXT_RECHECK");
-      ext_env = e ? atoi(e) : 0;
-    }
-    t.ext_recheck = (ext_env && !fused && !t.fuse_convert) ? 1 : 0;
-    if (t.ext_recheck) {
-      ACE_CUDA(sk->segc.ensure(static_cast<size_t>(tck_grid(n)) * sizeof(uint32_t)));
-      t.seg_counts = sk->segc.as<uint32_t>();
-      t.w32 = f->tc.w32;
-    }
-    ACE_CUDA(launch_hash_tc(t, sk->stream));
-    if (t.ext_recheck) ACE_CUDA(launch_recheck_segs(t, sk->stream));
+    if (!tc_direct_ok(xd, t.x_f64, ld)) ACE_CUDA(sk->xf32.ensure(tc_stage_bytes(n, f->d.dim)));
+    sk->mark(4);
+    sk->mark(6);
+    ACE_CUDA(launch_hash_tc(t, sk->xf32.p, sk->stream));
     sk->mark(5);
-    ACE_CUDA(launch_recheck(t, f->d.w64, sk->stream));
+    ACE_CUDA(launch_recheck(t, sk->stream));
     if (fused) {
       // T = sum of squared counters (exact: 32-bit, unsaturated)
       ACE_CUDA(cudaMemsetAsync(&sk->st->T, 0, sizeof(unsigned long long), sk->stream));
@@ -547,15 +480,6 @@ int ace_device_available(void) {
 
 uint64_t ace_kernel_launches(void) { return g_launches.load(); }
 
-// Instrumentation readout (ACE_TC_PROF set): wait cycles per barrier kind of
-// the last tcgen05 projection launch, summed over CTAs.  Not part of the ABI
-// contract in include/ace_b200.h.
-int ace_debug_tc_prof(unsigned long long* out32) {
-  if (!g_tc_prof) return -1;
-  cudaDeviceSynchronize();
-  return cudaMemcpy(out32, g_tc_prof, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : -2;
-}
-
 // Instrumentation: %globaltimer stamps of the last detect tail (ACE_TAIL_PROF=1):
 // [0] start [1] counts done [2] gather done [3] scores + threshold done [4] flags done.
 int ace_debug_tail_prof(unsigned long long* out8) {
@@ -590,7 +514,9 @@ ace_status ace_family_create(uint64_t dim, uint32_t k_bits, uint32_t num_tables,
   d.dpad = (dim + 31) / 32 * 32;
   // fast-path error bound: fp32 FMA fold of fp32-rounded W and x against
   // the binary64 fold, relative to ||w|| ||x||.
-  f->margin_c = static_cast<float>((static_cast<double>(dim) + 6.0) * 0x1.0p-24 * 1.01);
+  // (at least 2e-6: every projection below the BASELINE near-tie measure
+  // 1e-6 |x| |w| is then rechecked and counted)
+  f->margin_c = static_cast<float>(std::max((static_cast<double>(dim) + 6.0) * 0x1.0p-24 * 1.01, 2e-6));
 
   std::vector<float> w32t(static_cast<size_t>(d.dpad) * d.ncols, 0.0f);
   std::vector<float> wn(d.ncols, 0.0f);
@@ -614,12 +540,17 @@ ace_status ace_family_create(uint64_t dim, uint32_t k_bits, uint32_t num_tables,
   if ((e = cudaMalloc(&d.w64, sizeof(double) * d.rows * dim)) != cudaSuccess ||
       (e = cudaMalloc(&d.w32t, sizeof(float) * w32t.size())) != cudaSuccess ||
       (e = cudaMalloc(&d.wnorm, sizeof(float) * wn.size())) != cudaSuccess ||
+      (e = cudaMalloc(&d.wnorm64, sizeof(double) * d.rows)) != cudaSuccess ||
       (e = cudaMemcpy(d.w64, w_host, sizeof(double) * d.rows * dim, cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemcpy(d.w32t, w32t.data(), sizeof(float) * w32t.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemcpy(d.wnorm, wn.data(), sizeof(float) * wn.size(), cudaMemcpyHostToDevice)) != cudaSuccess) {
     cleanup();
     return fail(e == cudaErrorMemoryAllocation ? ACE_E_NOMEM : ACE_E_CUDA,
                 std::string("ace_family_create: ") + cudaGetErrorString(e));
+  }
+  if ((e = launch_wnorm64(d.w64, d.dim, d.rows, d.wnorm64)) != cudaSuccess) {
+    cleanup();
+    return fail(ACE_E_CUDA, std::string("ace_family_create: ") + cudaGetErrorString(e));
   }
   if ((e = tc_prepare_family(d, &f->tc)) != cudaSuccess) {
     cleanup();
@@ -814,7 +745,7 @@ ace_status ace_sketch_destroy(AceSketch* sk) {
   sk->x16.release();
   sk->rowthr.release();
   sk->segc.release();
-  sk->lomask.release();
+  sk->xf32.release();
   if (sk->counters) cudaFree(sk->counters);
   if (sk->st) cudaFree(sk->st);
   if (sk->hst) cudaFreeHost(sk->hst);
@@ -1042,7 +973,7 @@ ace_status batch_detect(AceSketch* sk, const void* x, int dtype, uint64_t n, uin
   key.ff = build ? (fire_and_forget_ok(sk, n) ? 1 : 0) : 2;
   key.stream = sk->stream;
   const DevBuf* bufs[12] = {&sk->ids, &sk->sums, &sk->stage, &sk->flags, &sk->scores, &sk->demand, &sk->near,
-                            &sk->overflow, &sk->x16, &sk->rowthr, &sk->segc, &sk->lomask};
+                            &sk->overflow, &sk->x16, &sk->rowthr, &sk->segc, &sk->xf32};
   for (int i = 0; i < 12; ++i) key.bufs[i] = bufs[i]->p;
   static int graphs_env = -2;
   if (graphs_env == -2) {

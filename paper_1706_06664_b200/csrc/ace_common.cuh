@@ -1,6 +1,7 @@
 // Shared definitions of the ACE device library (libace_dev.so).
 #pragma once
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdint.h>
 
 #include <atomic>
@@ -20,6 +21,7 @@ struct DevState {
   unsigned long long ambiguous;
   unsigned long long rechecked;
   unsigned long long flipped;
+  unsigned long long near_ties;      // |p| < 1e-6 |x| |w| (BASELINE.json near-tie measure), exact
   unsigned long long near_count;     // tc path: near-tie items pushed
   unsigned long long near_overflow;  // tc path: list overflowed (rows rechecked in full)
   unsigned long long batch_sum;      // stream: sum of the batch's pre-insert S_i
@@ -33,6 +35,52 @@ struct DevState {
   double cut;                    // stream cut (mean - alpha)
   double mean_before;
 };
+
+// T / den correctly rounded to binary64 (round half to even), T, den < 2^64:
+// the exact sketch mean T / (n L) with a single rounding.  Long division
+// produces 53 mantissa bits plus a round bit; the remainder is the sticky bit.
+__host__ __device__ inline int ace_bits64(uint64_t v) {
+#ifdef __CUDA_ARCH__
+  return 64 - __clzll(static_cast<long long>(v));
+#else
+  return v ? 64 - __builtin_clzll(v) : 0;
+#endif
+}
+__host__ __device__ inline double ace_div_rn(uint64_t T, uint64_t den) {
+  if (T == 0 || den == 0) return 0.0;
+  const uint64_t q = T / den;
+  uint64_t r = T % den;  // < den
+  uint64_t m;
+  int e;
+  bool sticky;
+  const int bq = ace_bits64(q);
+  if (bq >= 54) {
+    const int sh = bq - 54;
+    sticky = (sh > 0 && (q & ((1ull << sh) - 1ull)) != 0) || r != 0;
+    m = q >> sh;
+    e = sh;
+  } else {
+    m = q;
+    e = 0;
+    while (ace_bits64(m) < 54) {
+      // r < den < 2^64: 2r may need 65 bits
+      const bool carry = (r >> 63) != 0;
+      r <<= 1;
+      const uint64_t bit = (carry || r >= den) ? 1ull : 0ull;
+      if (bit) r -= den;
+      m = (m << 1) | bit;
+      --e;
+    }
+    sticky = r != 0;
+  }
+  uint64_t mant = m >> 1;
+  if ((m & 1ull) && (sticky || (mant & 1ull))) ++mant;
+  if (mant == (1ull << 53)) {
+    mant >>= 1;
+    ++e;
+  }
+  return ldexp(static_cast<double>(mant), e + 1);
+}
 
 // Fast-path projection operands of a family (SIMT tile layout).
 //   Columns are grouped in tiles of kTileCols; tile j holds tables
@@ -48,6 +96,7 @@ struct FamilyDev {
   double* w64;       // rows x dim, binary64 (the reference's W)
   float* w32t;       // dpad x ncols, fp32, zero padded
   float* wnorm;      // ncols, upper bound of ||w|| (0 on pad columns)
+  double* wnorm64;   // rows, ||w|| as the oracle computes it (sequential binary64 fold, IEEE sqrt)
 };
 
 void set_error(const std::string& msg);

@@ -107,6 +107,31 @@ __device__ __forceinline__ double exact_projection(const double* __restrict__ w,
   return acc;
 }
 
+// The reference's fold plus the oracle's sequential |x|^2 (near-tie measure).
+__device__ __forceinline__ double exact_projection_nx(const double* __restrict__ w, const void* x, int x_f64,
+                                                      uint64_t row, uint64_t ld, uint64_t dim, double* nx_out) {
+  double acc = 0.0, nx = 0.0;
+  for (uint64_t i = 0; i < dim; ++i) {
+    const double xv = x_f64 ? static_cast<const double*>(x)[row * ld + i]
+                            : static_cast<double>(static_cast<const float*>(x)[row * ld + i]);
+    acc = __dadd_rn(acc, __dmul_rn(w[i], xv));
+    nx = __dadd_rn(nx, __dmul_rn(xv, xv));
+  }
+  *nx_out = nx;
+  return acc;
+}
+__device__ __forceinline__ bool near_tie_1e6_simt(double p, double nx, double wn) {
+  return fabs(p) < __dmul_rn(1e-6, __dmul_rn(__dsqrt_rn(nx), wn));
+}
+
+__global__ void wnorm64_kernel(const double* __restrict__ w64, uint64_t dim, uint32_t rows, double* out) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  double s = 0.0;
+  for (uint64_t i = 0; i < dim; ++i) s = __dadd_rn(s, __dmul_rn(w64[r * dim + i], w64[r * dim + i]));
+  out[r] = __dsqrt_rn(s);
+}
+
 // ---- hash (SIMT FP32 + FP64 recheck) --------------------------------------
 
 struct HashSmem {
@@ -121,7 +146,7 @@ __global__ void __launch_bounds__(NT, 2) hash_simt_kernel(const HashArgs a) {
   __shared__ uint32_t bits[BM][4];
   __shared__ uint32_t nt_list[NT_CAP];
   __shared__ int nt_count;
-  __shared__ unsigned long long blk_T, blk_rechk, blk_flip;
+  __shared__ unsigned long long blk_T, blk_rechk, blk_flip, blk_near;
 
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
@@ -138,6 +163,7 @@ __global__ void __launch_bounds__(NT, 2) hash_simt_kernel(const HashArgs a) {
     blk_T = 0;
     blk_rechk = 0;
     blk_flip = 0;
+    blk_near = 0;
   }
 
   // loader mapping: rows lrow + 32*i (i<4), k = 4*lkq + e (e<4)
@@ -258,8 +284,10 @@ __global__ void __launch_bounds__(NT, 2) hash_simt_kernel(const HashArgs a) {
           nt_list[slot] = (static_cast<uint32_t>(pt) << 8) | col;
         } else {
           const uint32_t table = tile * a.fam.tpt + col / K, b = col % K;
-          const double p = exact_projection(a.fam.w64 + (static_cast<uint64_t>(table) * K + b) * dim,
-                                            a.x, a.x_f64, row, a.ld, dim);
+          double nx = 0.0;
+          const double p = exact_projection_nx(a.fam.w64 + (static_cast<uint64_t>(table) * K + b) * dim,
+                                               a.x, a.x_f64, row, a.ld, dim, &nx);
+          if (near_tie_1e6_simt(p, nx, a.fam.wnorm64[table * K + b])) atomicAdd(&blk_near, 1ull);
           const int bit = p >= 0.0;
           if (bit != (acc[i][j] >= 0.0f)) atomicAdd(&blk_flip, 1ull);
           atomicAdd(&blk_rechk, 1ull);
@@ -297,8 +325,10 @@ __global__ void __launch_bounds__(NT, 2) hash_simt_kernel(const HashArgs a) {
     const int pt = static_cast<int>(e >> 8);
     const uint32_t col = e & 0xffu;
     const uint32_t table = tile * a.fam.tpt + col / K, b = col % K;
-    const double p = exact_projection(a.fam.w64 + (static_cast<uint64_t>(table) * K + b) * dim, a.x,
-                                      a.x_f64, m0 + pt, a.ld, dim);
+    double nx = 0.0;
+    const double p = exact_projection_nx(a.fam.w64 + (static_cast<uint64_t>(table) * K + b) * dim, a.x,
+                                         a.x_f64, m0 + pt, a.ld, dim, &nx);
+    if (near_tie_1e6_simt(p, nx, a.fam.wnorm64[table * K + b])) atomicAdd(&blk_near, 1ull);
     const uint32_t mask = 1u << (col & 31);
     const bool fast = (bits[pt][col >> 5] & mask) != 0u;
     const bool exact = p >= 0.0;
@@ -353,6 +383,7 @@ __global__ void __launch_bounds__(NT, 2) hash_simt_kernel(const HashArgs a) {
     if (blk_T) atomicAdd(&a.st->T, blk_T);
     if (blk_rechk) atomicAdd(&a.st->rechecked, blk_rechk);
     if (blk_flip) atomicAdd(&a.st->flipped, blk_flip);
+    if (blk_near) atomicAdd(&a.st->near_ties, blk_near);
     if (a.insert && blockIdx.x == 0 && blockIdx.y == 0) atomicAdd(&a.st->n, a.n);
   }
 }
@@ -1400,9 +1431,7 @@ __global__ void __launch_bounds__(1024) detect_tail_kernel(const TailArgs a) {
 __device__ double sketch_mean(const DevState* st, uint32_t tables) {
   const unsigned long long n = st->n;
   if (n == 0) return 0.0;
-  const unsigned long long den = n * tables;
-  const unsigned long long q = st->T / den, r = st->T % den;
-  return static_cast<double>(q) + static_cast<double>(r) / static_cast<double>(den);
+  return ace_div_rn(st->T, n * tables);
 }
 
 __global__ void stream_score_kernel(const uint32_t* __restrict__ ids, uint64_t n, uint64_t ids_stride, uint32_t tables,
@@ -1630,6 +1659,12 @@ int grid_for(uint64_t work, int threads, int max_blocks = 148 * 16) {
 }  // namespace
 
 size_t hash_simt_smem_bytes() { return sizeof(HashSmem); }
+
+cudaError_t launch_wnorm64(const double* w64, uint64_t dim, uint32_t rows, double* out) {
+  wnorm64_kernel<<<(rows + 127) / 128, 128>>>(w64, dim, rows, out);
+  count_launch();
+  return cudaDeviceSynchronize();
+}
 
 cudaError_t launch_hash_simt(const HashArgs& a, cudaStream_t s) {
   static bool configured = false;

@@ -20,6 +20,10 @@ struct HashArgs {
   DevState* st;
 };
 
+// ||w|| per direction as the oracle computes it (sequential binary64 fold of
+// w*w, IEEE sqrt): the near-tie measure |p| < 1e-6 |x| |w|.  Synchronous.
+cudaError_t launch_wnorm64(const double* w64, uint64_t dim, uint32_t rows, double* out);
+
 // SIMT FP32 projection + FP64 near-tie recheck + bucket packing (+ insert).
 cudaError_t launch_hash_simt(const HashArgs& a, cudaStream_t s);
 size_t hash_simt_smem_bytes();

@@ -104,6 +104,7 @@ def test_near_tie_stress_exact(cuda, oracle_c, dtype, kernel):
     ref_ids, near = oracle_c.buckets(w, x, k, l, rel_eps=1e-6)
     assert np.array_equal(ids, ref_ids)
     assert st.rechecked >= near  # every sub-1e-6 projection went to the recheck
+    assert st.near_ties == near  # the BASELINE near-tie measure, counted as the oracle counts it
 
 
 @pytest.mark.parametrize("kernel", ["tc", "simt"])
