@@ -2,22 +2,28 @@
 """ACE hot-path benchmark (BASELINE.json metric: ACE points/sec, hash + insert
 + score, on 1 B200; roofline fraction reported beside it).
 
-One step = one pass of the batch pipeline over the workload: reset the sketch,
-build_sketch (hash + insert every row) then detect_batch (score every row,
-mu - sigma threshold, flags) — ace_sketch_build_detect through the C ABI.
-Default workload: BASELINE config 2 (configs[1]: N=500,000, d=120, K=15,
-L=50), inputs resident in HBM (240 MB > the 126 MB L2, so no flush needed).
+Prints one JSON line per BASELINE configuration, configs 1-4 first and the
+headline last: config 5, the largest single-GPU workload (100M points,
+streamed in 65,536-point batches: score against the counts at batch start,
+flag score <= mean - alpha, insert; ace_cli.cpp:173-186 / detect.cpp:76-84).
+A batch-config step is reset + build_sketch + detect_batch over the config's
+rows (ace_sketch_build_detect); the stream step is the whole 100M-row stream
+from an empty sketch (ace_sketch_stream_run).  Inputs are resident in HBM
+(all larger than the 126 MB L2, so no flush is needed) for `value`; `e2e`
+is the same call with the rows in pinned host memory and the flags returned to
+the host.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C ...]
   python bench.py --impl reference ...   # the reference's CPU implementation
 
-Multi-GPU (torchrun): replicas only — each rank runs the full workload on its
+Multi-GPU (torchrun): replicas only -- each rank runs the full workload on its
 own GPU (the north star is single-GPU, no inter-GPU exchange); value = total
 points of all ranks / max-over-ranks time.
 """
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import os
 import statistics
@@ -34,6 +40,12 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "ACE points/sec (hash+insert+score) on 1 B200; % of binding FP32/HBM/L2-atomic roofline"
 UNIT = "points/s"
+ORDER = [1, 2, 3, 4, 5]  # the headline (config 5) last
+
+# bounded CPU samples (rows): cpu_baseline leg (~10 s of reference CPU work
+# per config) and the --impl reference arm (~1 s per step)
+CPU_SAMPLE = {1: 100_000, 2: 150_000, 3: 40_000, 4: 1_500, 5: 3 * 65_536}
+REF_SAMPLE = {1: 20_000, 2: 10_000, 3: 4_000, 4: 160, 5: 16_384}
 
 
 def peaks():
@@ -44,13 +56,12 @@ def peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
 
 
-def step_roofline(w, value, pk, tensor=True):
+def step_roofline(w, value, pk):
     """The metric's binding roofline for the whole step:
     points/s = min(projection peak / (2 d K L), HBM / (4 d), L2 RED rate / L),
-    with the tcgen05 bf16 dense peak (or FP32 FFMA for the SIMT kernel), the
-    measured HBM copy bandwidth and the measured random-address L2 RED rate
-    (profiles/r1_peaks_probe.json) for this counter array.  This design counts
-    in shared-memory histograms (one RED per touched bucket per block), so
+    with the tcgen05 bf16 dense peak, the measured HBM copy bandwidth and the
+    measured random-address L2 RED rate (profiles/r1_peaks_probe.json) for
+    this counter array.  This design counts in shared-memory histograms, so
     the L2-atomic term is the metric's definition rather than a limit of the
     implementation; the binding term without it is reported beside it."""
     probe = ROOT / "profiles" / "r1_peaks_probe.json"
@@ -62,7 +73,7 @@ def step_roofline(w, value, pk, tensor=True):
             size = w.num_tables * (4 << w.k_bits)
             red = rates[min(rates, key=lambda k: abs(k - size))] * 1e9
     f = 2.0 * w.dim * w.k_bits * w.num_tables
-    proj = (pk["bf16_tflops"] * 1e12 if tensor else 148 * 128 * 2 * 1.965e9) / f
+    proj = pk["bf16_tflops"] * 1e12 / f
     hbm = pk["hbm_gbs"] * 1e9 / (4.0 * w.dim)
     terms = {"projection_pts_s": proj, "hbm_x_read_pts_s": hbm}
     if red:
@@ -131,7 +142,7 @@ class Clocks:
 
 def _profiled_traffic(kernel: str, cfg: int):
     """DRAM bytes per launch of `kernel` from the committed ncu --set full
-    summary (profiles/traffic.json), or None."""
+    summaries (profiles/traffic.json), or None."""
     p = ROOT / "profiles" / "traffic.json"
     if not p.exists():
         return None
@@ -164,179 +175,120 @@ def replica_value(points_per_rank: int, ws: int, ms_max: float) -> float:
     return points_per_rank * ws / (ms_max * 1e-3)
 
 
-def cpu_baseline(cfg: int, sample: int):
-    """The compiled reference (oracle/_ref) on a bounded sample: insert on one
-    core (single writer, sketch.hpp:23-24), detect_batch on all cores."""
+def sample_rows(cfg: int, rows: int):
+    """Host rows of a bounded CPU sample, generated in this process only for
+    the compiled reference (the reference arm does not load the repo's
+    generator library: see ref_rows)."""
+    from paper_1706_06664_b200 import workloads as W
+    return W.host_rows(cfg, 0, rows)[0]
+
+
+def cpu_baseline(cfg: int, x) -> dict:
+    """The compiled reference (oracle/_ref) on a bounded sample of the
+    workload on the host cores: batch configs insert on one core (single
+    writer, sketch.hpp:23-24) then detect_batch on all cores; config 5 in
+    stream order (per 65,536-row batch: detect_stream on all cores, then the
+    inserts on one core).  The C restatement (oracle/) if the reference was
+    not built."""
     from oracle import REF_SO, Oracle, Reference
     from paper_1706_06664_b200 import workloads as W
     w = W.CONFIGS[cfg]
-    x, _ = W.host_rows(cfg, 0, sample)
+    n = x.shape[0]
     cores = os.cpu_count() or 1
     if REF_SO.exists():
         ref = Reference()
-        ti, td, _rep = ref.time_build_detect(w.w_seed, x, w.k_bits, w.num_tables, 0)
+        if w.mode == "stream":
+            ts, ti, _ = ref.time_stream(w.w_seed, x, w.k_bits, w.num_tables, w.batch, w.alpha)
+            what = (f"first {n} rows of config {cfg} in {w.batch}-row batches: detect_stream on {cores} threads "
+                    f"({ts:.2f} s), inserts on 1 core ({ti:.2f} s)")
+            secs = ts + ti
+        else:
+            ti, td, _ = ref.time_build_detect(w.w_seed, x, w.k_bits, w.num_tables, 0)
+            what = f"first {n} rows of config {cfg}: insert on 1 core ({ti:.2f} s), detect_batch on {cores} threads ({td:.2f} s)"
+            secs = ti + td
         kind = "reference"
-    else:  # the C restatement (same algorithm), single thread throughout
+    else:
         o = Oracle()
         t0 = time.perf_counter()
         wm = o.directions(w.w_seed, w.dim, w.k_bits, w.num_tables)
-        ids, _ = o.buckets(wm, x, w.k_bits, w.num_tables, threads=1)
+        ids, _ = o.buckets(wm, x, w.k_bits, w.num_tables, threads=1, fast=False)
         sk = o.sketch(w.k_bits, w.num_tables, 32)
         sk.insert_ids(ids)
-        ti = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        o.buckets(wm, x, w.k_bits, w.num_tables, threads=cores)
         sk.score_ids(ids)
-        td = time.perf_counter() - t0
-        kind = "port"
-    return {"value": sample / (ti + td), "unit": UNIT, "cores": cores, "kind": kind,
-            "sample": f"first {sample} rows of config {cfg}: insert on 1 core ({ti:.2f} s), "
-                      f"detect_batch on {cores} threads ({td:.2f} s)"}
+        secs = time.perf_counter() - t0
+        kind, cores = "port", 1
+        what = f"first {n} rows of config {cfg}, the C restatement on one core"
+    return {"value": n / secs, "unit": UNIT, "cores": cores, "kind": kind, "sample": what}
+
+
+def ref_rows(cfg: int, rows: int):
+    """Reference-arm input rows, generated by a separate process into a .npy
+    file so this process loads only the compiled reference (oracle/_ref)."""
+    out = Path("/tmp") / f"ace_ref_rows_cfg{cfg}_{rows}.npy"
+    if not out.exists():
+        code = ("import sys, numpy as np; sys.path.insert(0, %r); "
+                "from paper_1706_06664_b200 import workloads as W; "
+                "np.save(%r, W.host_rows(%d, 0, %d)[0])") % (str(ROOT), str(out), cfg, rows)
+        subprocess.run([sys.executable, "-c", code], check=True)
+    return np.load(out)
 
 
 def run_reference(args):
+    """--impl reference: the reference's own CPU implementation of the path
+    (oracle/_ref, compiled from the unmodified sources) on the box's host
+    cores, each step a bounded sample of the config's workload."""
     ws, rank, _ = dist_setup()
     if rank != 0:
         return
     from paper_1706_06664_b200 import workloads as W
-    w = W.CONFIGS[args.config]
-    sample = args.ref_sample
-    times = []
-    for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(args.config, sample)
-        if i >= args.warmup:
-            times.append(sample / cb["value"])
-    t = statistics.mean(times)
-    value = sample / t
-    line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": f"cfg{args.config} {w.name} sample={sample} rows",
-                                        "N": sample, "d": w.dim, "K": w.k_bits, "L": w.num_tables},
-        "cpu_baseline": {**cb, "value": value},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-
-
-def run_stream(args, w, ws, rank, local):
-    """Config 5: the streaming driver over N rows in batches (score against the
-    counts at batch start, flag score <= mean - alpha, insert), one step = the
-    whole stream from an empty sketch.  Reports points/s and p50/p99 of the
-    per-batch device latency."""
-    import ctypes as C
-
-    import torch
-    import torch.distributed as dist
-
-    from paper_1706_06664_b200 import _native as N
-    from paper_1706_06664_b200 import ace
-    from paper_1706_06664_b200 import workloads as W
-
-    n = w.n if args.rows is None else min(w.n, args.rows)
-    x = torch.empty((n, w.dim), dtype=torch.float32, device="cuda")
-    chunk = 8 * 1024 * 1024
-    for r0 in range(0, n, chunk):
-        m = min(chunk, n - r0)
-        W.device_rows(w.cfg, r0, m, x[r0:r0 + m].data_ptr())
-    torch.cuda.synchronize()
-    fam = ace.SrpFamily(ace.SrpConfig(dim=w.dim, k_bits=w.k_bits, num_tables=w.num_tables, seed=w.w_seed))
-    sk = ace.AceSketch(fam, ace.CounterWidth.k32)
-    stream = torch.cuda.current_stream()
-    sk.set_stream(stream.cuda_stream)
-    flags = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
-
-    def step():
-        sk.reset()
-        return sk.stream_run(x, w.batch, w.alpha, flags_out=flags)
-
-    for _ in range(max(3, args.warmup)):
-        _, lat, rep = step()
-    torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    clocks = Clocks(local)
-    clocks.start()
-    launches0 = N.dev().ace_kernel_launches()
-    lats = []
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        _, lat, rep = step()
-        lats.append(lat)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    launches = N.dev().ace_kernel_launches() - launches0
-    clk = clocks.stop()
-    ms = e0.elapsed_time(e1) / args.steps
-    ms = max_over_ranks(ms, ws)
-    lat_all = np.concatenate(lats)
-    value = replica_value(n, ws, ms)
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": f"synthetic (datagen cfg {w.cfg}, seed {w.data_seed})",
-        "config": {"workload": f"cfg{w.cfg} {w.name}: streaming score -> flag (mean - alpha) -> insert",
-                   "N": n, "d": w.dim, "K": w.k_bits, "L": w.num_tables, "batch": w.batch,
-                   "hash_group_batches": int(os.environ.get("ACE_STREAM_GROUP", "4")),
-                   "alpha": w.alpha, "counter_width": 32,
-                   "l2": f"inputs {n * w.dim * 4 / 1e9:.1f} GB > 126 MB L2",
-                   "parallelism": f"replicas x{ws}"},
-        "batch_latency_ms": {"p50": float(np.percentile(lat_all, 50)),
-                             "p99": float(np.percentile(lat_all, 99)),
-                             "max": float(lat_all.max()), "batches_per_step": int(len(lats[0]))},
-        "gpu_launches": int(launches), "clocks": clk,
-        "step_roofline": step_roofline(w, value, peaks()[0]),
-        "exactness": {"rechecked": int(sk.last_stats.rechecked), "flipped": int(sk.last_stats.flipped),
-                      "ambiguous": int(rep.ambiguous), "reported": int(rep.reported)},
-    }
-    if rank == 0:
+    for cfg in args.config:
+        w = W.CONFIGS[cfg]
+        x = ref_rows(cfg, REF_SAMPLE[cfg])
+        times = []
+        cb = None
+        for i in range(args.warmup + args.steps):
+            cb = cpu_baseline(cfg, x)
+            if i >= args.warmup:
+                times.append(x.shape[0] / cb["value"])
+        t = statistics.mean(times)
+        value = x.shape[0] / t
+        line = {
+            "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": f"synthetic (datagen cfg {cfg}, seed {w.data_seed})",
+            "config": {"workload": f"cfg{cfg} {w.name}: {'stream' if w.mode == 'stream' else 'build_sketch + detect_batch'}"
+                                   f" (reference CPU, sample of {x.shape[0]} rows per step)",
+                       "N": x.shape[0], "d": w.dim, "K": w.k_bits, "L": w.num_tables},
+            "cpu_baseline": {**cb, "value": value},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
         print(json.dumps(line), flush=True)
-    if ws > 1:
-        dist.destroy_process_group()
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--impl", default="ace", choices=["ace", "reference"])
-    ap.add_argument("--ref-sample", type=int, default=20_000,
-                    help="rows per step of the --impl reference arm")
-    ap.add_argument("--cpu-sample", type=int, default=150_000,
-                    help="rows of the cpu_baseline leg (10-30 s of CPU work)")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--rows", type=int, default=None, help="stream mode: limit N (smoke runs)")
-    args = ap.parse_args()
-    if args.impl == "reference":
-        return run_reference(args)
+def roofline_of(kernel_ms, flops, pk, pk_src, w, cfg, ms_step, kname, desc):
+    peak = pk["bf16_tflops"]
+    ach = flops / (kernel_ms * 1e-3) / 1e12 if kernel_ms > 0 else None
+    return {
+        "bound": "tensor", "kernel": f"{kname} ({desc})", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+        "frac": ach / peak if ach else None, "traffic": _profiled_traffic(kname, cfg),
+        "peak_source": f"bf16 dense {pk_src} (burst); algorithmic flops = 2*d*K*L per point, "
+                       "the 3 split passes count against achieved",
+        "algorithmic_flops_per_launch": flops, "kernel_ms": kernel_ms,
+        "kernel_share_of_step": kernel_ms / ms_step if ms_step else None,
+        # the exact-sign split runs 3 fp16 MMA passes per projection: peak / 3
+        # is the kernel's ceiling in algorithmic flops
+        "split_passes": 3, "frac_of_split_ceiling": 3.0 * ach / peak if ach else None,
+    }
 
-    import ctypes as C
 
-    import torch
-    import torch.distributed as dist
-
-    from paper_1706_06664_b200 import _native as N
-    from paper_1706_06664_b200 import ace
-    from paper_1706_06664_b200 import workloads as W
-
-    ws, rank, local = dist_setup()
-    torch.cuda.set_device(local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    w = W.CONFIGS[args.config]
-    if w.mode == "stream":
-        return run_stream(args, w, ws, rank, local)
+def run_batch(args, cfg, ws, rank, local, torch, N, ace, W):
+    w = W.CONFIGS[cfg]
     n = w.n
     x = torch.empty((n, w.dim), dtype=torch.float32, device="cuda")
-    W.device_rows(args.config, 0, n, x.data_ptr())
+    W.device_rows(cfg, 0, n, x.data_ptr())
     torch.cuda.synchronize()
-    fam = ace.SrpFamily(ace.SrpConfig(dim=w.dim, k_bits=w.k_bits, num_tables=w.num_tables,
-                                      seed=w.w_seed))
+    fam = ace.SrpFamily(ace.SrpConfig(dim=w.dim, k_bits=w.k_bits, num_tables=w.num_tables, seed=w.w_seed))
     sk = ace.AceSketch(fam, ace.CounterWidth.k32)
     stream = torch.cuda.current_stream()
     sk.set_stream(stream.cuda_stream)
@@ -350,6 +302,7 @@ def main():
         rep = step()
     torch.cuda.synchronize()
     if ws > 1:
+        import torch.distributed as dist
         dist.barrier()
     clocks = Clocks(local)
     clocks.start()
@@ -361,15 +314,11 @@ def main():
         rep = step()
     e1.record(stream)
     torch.cuda.synchronize()
-    launches = N.dev().ace_kernel_launches() - launches0
+    launches = (N.dev().ace_kernel_launches() - launches0) / args.steps
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1) / args.steps
-    if ws > 1:
-        ms = max_over_ranks(ms, ws)
-        dist.barrier()
-    # per-phase breakdown: a separate pass with per-phase CUDA events (outside
-    # the timed region, so the events do not perturb the headline number)
-    import ctypes as C
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, ws)
+    # per-phase breakdown: a separate pass with per-phase CUDA events on the
+    # sketch's stream (outside the timed region)
     N.dev().ace_sketch_set_timing(sk.handle, 1)
     phase = np.zeros(5)
     ms5 = (C.c_double * 5)()
@@ -382,8 +331,6 @@ def main():
     phase /= phase_steps
     value = replica_value(n, ws, ms)
 
-    # e2e: same metric through the public API from pinned host memory (H2D of
-    # the rows and D2H of the flag bitmap inside the timed region)
     e2e = None
     if not args.no_e2e:
         xh = torch.empty((n, w.dim), dtype=torch.float32, pin_memory=True)
@@ -391,8 +338,6 @@ def main():
         xnp = xh.numpy()
         sk_e = ace.AceSketch(fam, ace.CounterWidth.k32)
         sk_e.set_stream(stream.cuda_stream)
-        # the drop-in boundary itself: ace_sketch_build_detect (C ABI) with the
-        # host rows in pinned memory and the flag bitmap returned to host memory
         bits = np.zeros((n + 31) // 32, dtype=np.uint32)
         rep_e, st_e = N.AceBatchReport(), N.AceHashStats()
         fn = N.dev().ace_sketch_build_detect
@@ -407,94 +352,207 @@ def main():
         for _ in range(2):
             e2e_call()
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
         reps = max(3, args.steps // 2)
+        t0 = time.perf_counter()
         for _ in range(reps):
             e2e_call()
         torch.cuda.synchronize()
-        te = (time.perf_counter() - t0) / reps
-        te = max_over_ranks(te, ws)
+        te = max_over_ranks((time.perf_counter() - t0) / reps, ws)
         e2e = {"value": replica_value(n, ws, te * 1e3), "unit": UNIT, "h2d_bytes_per_step": n * w.dim * 4,
                "d2h_bytes_per_step": ((n + 31) // 32) * 4 + 200,
                "note": "wall clock around the C-ABI call ace_sketch_build_detect (+ sketch reset) with pinned host "
-                       "rows in and the flag bitmap out to host memory"}
+                       "rows in (copied in chunks, each hashed as it lands) and the flag bitmap out to host memory"}
+        del xh, xnp, sk_e
 
     pk, pk_src = peaks()
-    flops = 2.0 * w.dim * w.k_bits * w.num_tables * n  # one fp32 projection pass
-    kernel = N.dev().ace_family_kernel(fam.handle)
-    if kernel == 2:
-        kern_ms = phase[4]
-        peak = pk["bf16_tflops"]
-        kname = "hash_tck_kernel" if w.dim > 256 else "hash_tc_kernel"
-        traffic = _profiled_traffic(kname, args.config)
-        roofline = {
-            "bound": "tensor",
-            "kernel": (kname + " (tcgen05 fp16x3-split projection, TMEM accumulators, sign/near-tie/bucket epilogue"
-                       + (", A and W streamed in K chunks)" if w.dim > 256 else ")")),
-            "achieved": flops / (kern_ms * 1e-3) / 1e12 if kern_ms > 0 else None,
-            "peak": peak,
-            "unit": "TFLOP/s",
-            "frac": (flops / (kern_ms * 1e-3) / 1e12) / peak if kern_ms > 0 else None,
-            "traffic": traffic,
-            "peak_source": f"bf16 dense {pk_src} (burst); algorithmic flops = 2*d*K*L per point, "
-                           "the 3 split passes count against achieved",
-            "algorithmic_flops_per_launch": flops,
-            "kernel_ms": kern_ms,
-            "kernel_share_of_step": kern_ms / ms if ms else None,
-            # the exact-sign split runs 3 fp16 MMA passes per projection
-            # (x_hi w_hi, x_lo w_hi, x_hi w_lo): peak / 3 is this kernel's
-            # ceiling in algorithmic flops (zero-lo and past-d steps skipped
-            # make the issued work smaller, so this fraction is conservative)
-            "split_passes": 3,
-            "frac_of_split_ceiling": (3.0 * flops / (kern_ms * 1e-3) / 1e12) / peak if kern_ms > 0 else None,
-        }
-    else:
-        kern_ms = phase[0]
-        fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
-        roofline = {
-            "bound": "fp32",
-            "kernel": "hash_simt_kernel (SIMT FP32 projection + FP64 near-tie recheck + packing + fused insert)",
-            "achieved": flops / (kern_ms * 1e-3) / 1e12 if kern_ms > 0 else None,
-            "peak": fp32_peak, "unit": "TFLOP/s",
-            "frac": (flops / (kern_ms * 1e-3) / 1e12) / fp32_peak if kern_ms > 0 else None,
-            "traffic": None, "peak_source": "spec FP32 FFMA (148 SM x 128 x 2 x 1.965 GHz)",
-            "algorithmic_flops_per_launch": flops, "kernel_ms": kern_ms,
-            "kernel_share_of_step": kern_ms / ms if ms else None,
-        }
-    x_bytes = n * w.dim * 4
-    conv_ms = phase[3]
-    kernels = {
-        "convert_x (hbm)": {"ms": conv_ms, "GB/s": x_bytes / (conv_ms * 1e-3) / 1e9 if conv_ms else None,
-                            "frac_hbm": (x_bytes / (conv_ms * 1e-3) / 1e9) / pk["hbm_gbs"] if conv_ms else None},
-        "hash_tc (tensor)": {"ms": phase[4]},
-        "recheck+insert": {"ms": phase[0] - phase[3] - phase[4]},
-        "score": {"ms": phase[1]},
-        "threshold+flags": {"ms": phase[2]},
-    }
+    flops = 2.0 * w.dim * w.k_bits * w.num_tables * n
+    kstream = w.dim > 256
+    kname = "hash_tck_kernel" if kstream else "hash_tc_kernel"
+    desc = ("tcgen05 fp16x3-split projection, TMEM accumulators, A and W streamed in K chunks" if kstream else
+            "tcgen05 fp16x3-split projection of raw fp32 rows loaded by tensor-map TMA, split in-kernel into a "
+            "TMEM A operand; sign / near-tie epilogue; bucket packing")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": f"synthetic (datagen cfg {args.config}, seed {w.data_seed})",
-        "config": {"workload": f"cfg{args.config} {w.name}: build_sketch + detect_batch",
+        "vs_baseline": None, "dtype": "f32", "data": f"synthetic (datagen cfg {cfg}, seed {w.data_seed})",
+        "config": {"workload": f"cfg{cfg} {w.name}: build_sketch + detect_batch",
                    "N": n, "d": w.dim, "K": w.k_bits, "L": w.num_tables, "counter_width": 32,
                    "l2": f"inputs {n * w.dim * 4 / 1e6:.0f} MB > 126 MB L2 (no flush needed)",
                    "parallelism": f"replicas x{ws}"},
-        "roofline": roofline,
-        "step_roofline": step_roofline(w, value, pk, tensor=kernel == 2),
+        "roofline": roofline_of(phase[4], flops, pk, pk_src, w, cfg, ms, kname, desc),
+        "step_roofline": step_roofline(w, value, pk),
         "phases_ms": {"hash_insert": phase[0], "score": phase[1], "threshold_flags": phase[2],
                       "convert_x": phase[3], "projection_kernel": phase[4]},
-        "kernels": kernels,
-        "gpu_launches": int(launches),
+        "gpu_launches": int(round(launches)),
         "clocks": clk,
         "e2e": e2e,
-        "exactness": {"rechecked": int(rep.stats.rechecked), "flipped": int(rep.stats.flipped),
-                      "ambiguous": int(rep.ambiguous), "replayed": bool(rep.replayed),
-                      "reported": int(rep.reported)},
+        "exactness": {"near_ties_1e-6": int(rep.stats.near_ties), "rechecked": int(rep.stats.rechecked),
+                      "flipped": int(rep.stats.flipped), "ambiguous": int(rep.ambiguous),
+                      "replayed": bool(rep.replayed), "reported": int(rep.reported)},
     }
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.config, min(args.cpu_sample, n))
-    if rank == 0:
-        print(json.dumps(line), flush=True)
+    del x, flags, sk
+    torch.cuda.empty_cache()
+    return line
+
+
+def run_stream(args, cfg, ws, rank, local, torch, N, ace, W):
+    """Config 5: the streaming driver over the 100M rows in 65,536-row
+    batches; one step = the whole stream from an empty sketch.  Reports
+    points/s and p50/p99 of the per-batch latency (start of the batch's work
+    to the end of the launch that writes its flags)."""
+    w = W.CONFIGS[cfg]
+    n = w.n if args.rows is None else min(w.n, args.rows)
+    x = torch.empty((n, w.dim), dtype=torch.float32, device="cuda")
+    chunk = 8 * 1024 * 1024
+    for r0 in range(0, n, chunk):
+        m = min(chunk, n - r0)
+        W.device_rows(w.cfg, r0, m, x[r0:r0 + m].data_ptr())
+    torch.cuda.synchronize()
+    fam = ace.SrpFamily(ace.SrpConfig(dim=w.dim, k_bits=w.k_bits, num_tables=w.num_tables, seed=w.w_seed))
+    sk = ace.AceSketch(fam, ace.CounterWidth.k32)
+    stream = torch.cuda.current_stream()
+    sk.set_stream(stream.cuda_stream)
+    flags = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
+
+    def step(lat=True):
+        sk.reset()
+        return sk.stream_run(x, w.batch, w.alpha, flags_out=flags, latencies=lat)
+
+    for _ in range(max(3, args.warmup)):
+        _, lat, rep = step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    launches0 = N.dev().ace_kernel_launches()
+    lats = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        _, lat, rep = step()
+        lats.append(lat)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = (N.dev().ace_kernel_launches() - launches0) / args.steps
+    clk = clocks.stop()
+    st = sk.last_stats
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, ws)
+    lat_all = np.concatenate(lats)
+    value = replica_value(n, ws, ms)
+    # phase totals of one more run (events around every launch group)
+    N.dev().ace_sketch_set_timing(sk.handle, 1)
+    step(lat=False)
+    ms5 = (C.c_double * 5)()
+    N.dev().ace_sketch_timings(sk.handle, ms5)
+    N.dev().ace_sketch_set_timing(sk.handle, 0)
+    hash_ms, apply_ms = ms5[4], ms5[2]
+
+    e2e = None
+    if not args.no_e2e:
+        # the same call with the rows in pinned host memory (the next hashing
+        # group's H2D copy overlaps this group's work) and the flag bitmap
+        # returned to host memory
+        xh = torch.empty((n, w.dim), dtype=torch.float32, pin_memory=True)
+        xh.copy_(x)
+        bits = np.zeros((n + 31) // 32, dtype=np.uint32)
+        rep_e = N.AceStreamReport()
+        st_e = N.AceHashStats()
+        fn = N.dev().ace_sketch_stream_run
+        sk_e = ace.AceSketch(fam, ace.CounterWidth.k32)
+        sk_e.set_stream(stream.cuda_stream)
+
+        def e2e_call():
+            sk_e.reset()
+            rc = fn(sk_e._h, xh.data_ptr(), N.ACE_F32, n, w.dim, N.ACE_HOST, w.batch, float(w.alpha),
+                    bits.ctypes.data, N.ACE_HOST, None, C.byref(rep_e), C.byref(st_e))
+            if rc != 0:
+                raise RuntimeError(N.dev().ace_last_error().decode())
+
+        e2e_call()
+        torch.cuda.synchronize()
+        reps = 3
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            e2e_call()
+        torch.cuda.synchronize()
+        te = max_over_ranks((time.perf_counter() - t0) / reps, ws)
+        e2e = {"value": replica_value(n, ws, te * 1e3), "unit": UNIT, "h2d_bytes_per_step": n * w.dim * 4,
+               "d2h_bytes_per_step": ((n + 31) // 32) * 4 + 200,
+               "note": "wall clock around the C-ABI call ace_sketch_stream_run (+ sketch reset) with pinned host "
+                       "rows in and the flag bitmap out to host memory"}
+        del xh, sk_e
+
+    pk, pk_src = peaks()
+    nb = -(-n // w.batch)
+    groups = -(-nb // 2)  # hashing launches of 2 batches each
+    flops_per_launch = 2.0 * w.dim * w.k_bits * w.num_tables * (n / groups)
+    roof = roofline_of(hash_ms / groups, flops_per_launch, pk, pk_src, w, cfg, ms / groups, "hash_tc_kernel",
+                       "tcgen05 fp16x3-split projection of raw fp32 rows loaded by tensor-map TMA, split in-kernel; "
+                       "per launch: one 2-batch hashing group (131,072 rows) with its near-tie pass")
+    roof["kernel_share_of_step"] = hash_ms / ms if ms else None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": f"synthetic (datagen cfg {cfg}, seed {w.data_seed})",
+        "config": {"workload": f"cfg{cfg} {w.name}: streaming score -> flag (mean - alpha) -> insert",
+                   "N": n, "d": w.dim, "K": w.k_bits, "L": w.num_tables, "batch": w.batch,
+                   "hash_group_batches": 2, "alpha": w.alpha, "counter_width": 32,
+                   "l2": f"inputs {n * w.dim * 4 / 1e9:.1f} GB > 126 MB L2",
+                   "parallelism": f"replicas x{ws}"},
+        "roofline": roof,
+        "step_roofline": step_roofline(w, value, pk),
+        "phases_ms": {"hashing": hash_ms, "stream_kernels": apply_ms},
+        "batch_latency_ms": {"p50": float(np.percentile(lat_all, 50)),
+                             "p99": float(np.percentile(lat_all, 99)),
+                             "max": float(lat_all.max()), "batches_per_step": int(len(lats[0])),
+                             "definition": "start of the batch's work (its group's hashing for a group's first "
+                                           "batch) to the end of the launch that writes its flags"},
+        "gpu_launches": int(round(launches)), "clocks": clk, "e2e": e2e,
+        "exactness": {"near_ties_1e-6": int(st.near_ties), "rechecked": int(st.rechecked),
+                      "flipped": int(st.flipped), "ambiguous": int(rep.ambiguous), "reported": int(rep.reported)},
+    }
+    del x, flags, sk
+    torch.cuda.empty_cache()
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, nargs="+", default=ORDER,
+                    help="configurations to run, in order (default: 1 2 3 4 5, the headline last)")
+    ap.add_argument("--impl", default="ace", choices=["ace", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--rows", type=int, default=None, help="stream mode: limit N (smoke runs)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1706_06664_b200 import _native as N
+    from paper_1706_06664_b200 import ace
+    from paper_1706_06664_b200 import workloads as W
+
+    ws, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    for cfg in args.config:
+        w = W.CONFIGS[cfg]
+        run = run_stream if w.mode == "stream" else run_batch
+        line = run(args, cfg, ws, rank, local, torch, N, ace, W)
+        if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+            n_cpu = min(CPU_SAMPLE[cfg], line["config"]["N"])
+            line["cpu_baseline"] = cpu_baseline(cfg, sample_rows(cfg, n_cpu))
+        if rank == 0:
+            print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
 

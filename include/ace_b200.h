@@ -133,6 +133,16 @@ ace_status ace_sketch_reset(AceSketch* sk);
 /* Use an external CUDA stream (cudaStream_t) instead of the sketch's own;
  * NULL restores the private stream. */
 ace_status ace_sketch_set_stream(AceSketch* sk, void* cuda_stream);
+/* Per-sketch execution options (results are identical under every setting):
+ *   ACE_OPT_H2D_CHUNKS    pinned host rows of a large batch are copied in this
+ *                         many chunks, each hashed as it lands (default 8;
+ *                         1 = one copy, then the work);
+ *   ACE_OPT_DEFER_INSERT  build + detect: fuse the insert into the detect
+ *                         tail's count-and-gather pass: 0 = when the batch is
+ *                         large enough (default), 1 = whenever the sketch
+ *                         allows it (32-bit, K <= 16), -1 = never. */
+enum { ACE_OPT_H2D_CHUNKS = 1, ACE_OPT_DEFER_INSERT = 2 };
+ace_status ace_sketch_set_option(AceSketch* sk, int option, int64_t value);
 
 /* AceSketch::insert (sketch.cpp:50-72) for n rows, in row order. */
 ace_status ace_sketch_insert(AceSketch* sk, const void* x, int dtype, uint64_t n,
@@ -212,7 +222,9 @@ uint64_t ace_kernel_launches(void);
  * after each call, ms[0] = hash (+ recheck + insert), ms[1] = score,
  * ms[2] = threshold + flags (batch) or stream flags + insert (stream),
  * ms[3] = x conversion pre-pass (0 where the projection kernel converts the
- * raw rows itself, d <= 256), ms[4] = tcgen05 projection kernel. */
+ * raw rows itself, d <= 256), ms[4] = tcgen05 projection kernel.  After
+ * ace_sketch_stream_run: ms[0] = ms[4] = all hashing (projection launches
+ * with their near-tie passes), ms[2] = all stream kernels (phases A and B). */
 ace_status ace_sketch_set_timing(AceSketch* sk, int enable);
 ace_status ace_sketch_timings(const AceSketch* sk, double* ms5);
 

@@ -201,6 +201,9 @@ class Reference:
         L.ref_time_build_detect.restype = _i
         L.ref_time_build_detect.argtypes = [_u64, _vp, _u64, _u64, _u32, _u32, C.c_uint, _P(_d),
                                             _P(_d), _P(_u64)]
+        L.ref_time_stream.restype = _i
+        L.ref_time_stream.argtypes = [_u64, _vp, _u64, _u64, _u32, _u32, _u64, _d, C.c_uint, _P(_d), _P(_d),
+                                      _P(_u64)]
         L.ref_save_sketch.restype = _i
         L.ref_save_sketch.argtypes = [_vp, C.c_char_p]
         L.ref_load_sketch.restype = _vp
@@ -308,6 +311,17 @@ class Reference:
         self._ok(self.L.ref_time_build_detect(seed, x.ctypes.data, n, dim, k, l, threads,
                                               C.byref(ti), C.byref(td), C.byref(rep)))
         return ti.value, td.value, rep.value
+
+
+    def time_stream(self, seed, x, k, l, batch, alpha, threads=0):
+        """(seconds scoring on `threads` cores, seconds inserting on one core,
+        reported) of the stream-ordered reference loop over the rows."""
+        x = _f32(x)
+        n, dim = x.shape
+        ts, ti, rep = _d(), _d(), _u64()
+        self._ok(self.L.ref_time_stream(seed, x.ctypes.data, n, dim, k, l, batch, alpha, threads, C.byref(ts),
+                                        C.byref(ti), C.byref(rep)))
+        return ts.value, ti.value, rep.value
 
 
 class RefSketch:

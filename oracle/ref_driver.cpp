@@ -311,6 +311,60 @@ int ref_time_build_detect(uint64_t seed, const float* x, uint64_t n, uint64_t di
   }
 }
 
+// CPU baseline of the streaming driver in config 5's order: per batch, every
+// row scored by detect_stream (detect.cpp:76-84) against the counts at batch
+// start on `threads` cores (the sketch is only read: const, thread-safe), then
+// the batch inserted in row order on one core (single writer, sketch.hpp:
+// 23-24), as ace_cli.cpp:173-186 does per query with the insert deferred to
+// the batch end.  Seconds of scoring and of inserting over all n rows.
+int ref_time_stream(uint64_t seed, const float* x, uint64_t n, uint64_t dim, uint32_t k, uint32_t l,
+                    uint64_t batch, double alpha, unsigned threads, double* t_score, double* t_insert,
+                    uint64_t* reported) {
+  try {
+    const ace::SrpFamily fam(make_cfg(dim, k, l, seed));
+    ace::AceSketch s(fam, ace::CounterWidth::k32);
+    if (threads == 0) threads = std::max(1u, std::thread::hardware_concurrency());
+    std::vector<double> xd(n * dim);
+    for (uint64_t i = 0; i < n * dim; ++i) xd[i] = static_cast<double>(x[i]);
+    double ts = 0.0, ti = 0.0;
+    uint64_t rep = 0;
+    std::vector<uint64_t> rep_t(threads);
+    for (uint64_t b0 = 0; b0 < n; b0 += batch) {
+      const uint64_t m = std::min(batch, n - b0);
+      const auto t0 = std::chrono::steady_clock::now();
+      std::vector<std::thread> pool;
+      for (unsigned t = 0; t < threads; ++t) {
+        rep_t[t] = 0;
+        pool.emplace_back([&, t] {
+          for (uint64_t i = b0 + t; i < b0 + m; i += threads) {
+            std::span<const double> r(xd.data() + i * dim, dim);
+            if (s.size() == 0) {
+              (void)s.score(r);
+            } else {
+              const auto res = ace::detect_stream(s, r, alpha);
+              rep_t[t] += res.second ? 1 : 0;
+            }
+          }
+        });
+      }
+      for (auto& th : pool) th.join();
+      const auto t1 = std::chrono::steady_clock::now();
+      for (uint64_t i = b0; i < b0 + m; ++i) s.insert(std::span<const double>(xd.data() + i * dim, dim));
+      const auto t2 = std::chrono::steady_clock::now();
+      ts += std::chrono::duration<double>(t1 - t0).count();
+      ti += std::chrono::duration<double>(t2 - t1).count();
+      for (unsigned t = 0; t < threads; ++t) rep += rep_t[t];
+    }
+    *t_score = ts;
+    *t_insert = ti;
+    *reported = rep;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // ACE1 sketch files through the reference's io (io.cpp:184-244): 0 ok,
 // -3 DataError (message in ref_last_error), -1 other.
 int ref_save_sketch(void* h, const char* path) {

@@ -14,6 +14,7 @@ LIB_DIR = Path(__file__).resolve().parent / "lib"
 ACE_OK, ACE_E_CONTRACT, ACE_E_UNSUPPORTED, ACE_E_INCONSISTENT, ACE_E_DATA, ACE_E_CUDA, ACE_E_NOMEM = range(7)
 ACE_F32, ACE_F64 = 0, 1
 ACE_HOST, ACE_DEVICE = 0, 1
+ACE_OPT_H2D_CHUNKS, ACE_OPT_DEFER_INSERT = 1, 2
 
 
 class AceHashStats(C.Structure):
@@ -61,6 +62,7 @@ ABI = {
     "ace_sketch_destroy": (_i, [_vp]),
     "ace_sketch_reset": (_i, [_vp]),
     "ace_sketch_set_stream": (_i, [_vp, _vp]),
+    "ace_sketch_set_option": (_i, [_vp, _i, C.c_int64]),
     "ace_sketch_insert": (_i, [_vp, _vp, _i, _u64, _u64, _i, _P(AceHashStats)]),
     "ace_sketch_remove": (_i, [_vp, _vp, _i, _u64, _u64, _i, _P(AceHashStats)]),
     "ace_sketch_score": (_i, [_vp, _vp, _i, _u64, _u64, _i, _vp, _vp, _i, _P(AceHashStats)]),

@@ -349,6 +349,10 @@ class AceSketch:
     def reset(self) -> None:
         _check(N.dev().ace_sketch_reset(self._h))
 
+    def set_option(self, option: int, value: int) -> None:
+        """Per-sketch execution option (N.ACE_OPT_*); results do not change."""
+        _check(N.dev().ace_sketch_set_option(self._h, int(option), int(value)))
+
     def set_stream(self, stream_ptr: int) -> None:
         _check(N.dev().ace_sketch_set_stream(self._h, stream_ptr))
 

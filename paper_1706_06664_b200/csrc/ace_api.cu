@@ -103,7 +103,15 @@ struct AceSketch {
   cudaStream_t cstream = nullptr;
   cudaEvent_t cstart = nullptr;
   std::vector<cudaEvent_t> cev;
+  // stream driver with pinned host rows: two staging halves, copied on
+  // cstream; copy-done and hash-done events per half
+  DevBuf sstage[2];
+  cudaEvent_t s_copied[2] = {nullptr, nullptr}, s_used[2] = {nullptr, nullptr};
   DevBuf ids, sums, stage, flags, scores, demand, near, overflow, x16, rowthr, segc, xf32;
+  DevBuf cnt[2], dts;       // stream: counts at batch start (double-buffered), phase-A increments
+  uint64_t stream_seq = 0;  // stream batches so far (cut slot = seq & 1)
+  int h2d_chunks = 8;       // pinned host rows of a large batch: copy chunks hashed as they land
+  int defer_mode = 0;       // ACE_OPT_DEFER_INSERT
   // build + detect over the same rows: run_hash leaves the insert to the
   // fused count-and-gather pass of the detect tail (detect_tail_kernel)
   bool defer_insert = false, insert_deferred = false;
@@ -114,6 +122,10 @@ struct AceSketch {
   // phase timing (ace_sketch_set_timing)
   bool timing = false;
   cudaEvent_t ev[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  // stream driver phase totals (timing on): [0] hashing (projection + near-tie
+  // rows + memsets), [1] stream kernels (phases A / B); valid after a stream_run
+  double stream_ms[2] = {0.0, 0.0};
+  bool stream_timed = false;
   bool ev_used[7] = {false, false, false, false, false, false, false};
   void mark(int i) {
     if (timing) {
@@ -257,33 +269,29 @@ ace_status copy_out(void* dst, const void* src, size_t bytes, int where, cudaStr
 }
 
 // 32-bit sketches cannot saturate while n stays below 2^32 - 1, so their
-// insert merge may skip the pre-add values and recompute T = sum c^2.
+// insert merge may skip the pre-add values and recompute T = sum c^2; T (a
+// u64, at most L n^2 when every point shares one bucket) must not wrap either.
 bool fire_and_forget_ok(const AceSketch* sk, uint64_t n) {
-  return sk->width == 32 && !sk->hst->saturated && sk->hst->n + n < 0xffffffffull;
+  const unsigned long long tot = sk->hst->n + n;
+  const unsigned __int128 worst = static_cast<unsigned __int128>(tot) * tot * sk->fam->d.tables;
+  return sk->width == 32 && !sk->hst->saturated && tot < 0xffffffffull && (worst >> 64) == 0;
 }
 
-// Two blocks per table in the stream step's insert (ACE_STREAM_SPLIT=1; measured
-// slower on cfg 5: 7.9e8 vs 8.6e8 points/s, the second grid barrier and the
-// scratch round trip cost more than the halved count saves).
-bool stream_split_env() {
-  static int env = -1;
-  if (env < 0) {
-    const char* e = getenv("ACE_STREAM_SPLIT");
-    env = e ? atoi(e) : 0;
-  }
-  return env != 0;
-}
+// The barrier-free stream kernel (stream_apply_kernel): 32-bit unsaturable
+// sketches with K <= 16; others score, insert and cap with separate kernels.
+bool stream_apply_ok(const AceSketch* sk, bool ff) { return ff && sk->width == 32 && sk->fam->d.k_bits <= 16; }
 
-// One cooperative launch per streaming batch (launch_stream_step): 32-bit
-// unsaturable sketches with K <= 15 (a whole table's histogram in shared
-// memory); ACE_STREAM_FUSED=0 keeps the score / insert / sum-of-squares kernels.
-bool stream_fused_ok(const AceSketch* sk, bool ff) {
-  static int env = -1;
-  if (env < 0) {
-    const char* e = getenv("ACE_STREAM_FUSED");
-    env = e ? atoi(e) : 1;
-  }
-  return env != 0 && ff && sk->width == 32 && sk->fam->d.k_bits <= 15;
+// Batches of the stream driver hashed by one projection launch (hashing does
+// not depend on the counts): amortises the persistent kernel's fill and
+// drain over more point tiles.
+constexpr uint64_t kStreamGroup = 2;
+
+ace_status ensure_stream_bufs(AceSketch* sk, uint64_t rows) {
+  const size_t cnt_bytes = static_cast<size_t>(rows) * sk->fam->d.tables * sizeof(uint32_t);
+  ACE_CUDA(sk->cnt[0].ensure(cnt_bytes));
+  ACE_CUDA(sk->cnt[1].ensure(cnt_bytes));
+  ACE_CUDA(sk->dts.ensure(stream_phase_a_blocks(sk->fam->d.tables, sk->fam->d.k_bits) * sizeof(unsigned long long)));
+  return ACE_OK;
 }
 
 // hash n rows into sk->ids (table-major, stride n); optional fused insert.
@@ -298,6 +306,7 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
     ids_ld = n;
   }
   for (bool& u : sk->ev_used) u = false;
+  sk->stream_timed = false;
   sk->mark(0);
   if (f->use_tc()) {
     const bool kstream = tc_kstream(f->tc.nkc);
@@ -314,7 +323,6 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
     t.nkc = f->tc.nkc;
     t.tw = f->tc.tw;
     t.w16 = f->tc.w16;
-    tc_fill_tables(&t);
     t.margin_c = kstream ? tck_margin(f->tc.nkc, t.x_f64 != 0) : tc_margin(f->tc.nkc, t.x_f64 != 0);
     t.ids = ids_out;
     t.ids_ld = ids_ld;
@@ -479,14 +487,6 @@ int ace_device_available(void) {
 }
 
 uint64_t ace_kernel_launches(void) { return g_launches.load(); }
-
-// Instrumentation: %globaltimer stamps of the last detect tail (ACE_TAIL_PROF=1):
-// [0] start [1] counts done [2] gather done [3] scores + threshold done [4] flags done.
-int ace_debug_tail_prof(unsigned long long* out8) {
-  if (!g_tail_prof) return -1;
-  cudaDeviceSynchronize();
-  return cudaMemcpy(out8, g_tail_prof, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : -2;
-}
 
 // SrpFamily::SrpFamily (srp.cpp:24-49): validation + W upload.
 ace_status ace_family_create(uint64_t dim, uint32_t k_bits, uint32_t num_tables, double noise_scale,
@@ -746,10 +746,19 @@ ace_status ace_sketch_destroy(AceSketch* sk) {
   sk->rowthr.release();
   sk->segc.release();
   sk->xf32.release();
+  sk->cnt[0].release();
+  sk->cnt[1].release();
+  sk->dts.release();
   if (sk->counters) cudaFree(sk->counters);
   if (sk->st) cudaFree(sk->st);
   if (sk->hst) cudaFreeHost(sk->hst);
   if (sk->own) cudaStreamDestroy(sk->own);
+  sk->sstage[0].release();
+  sk->sstage[1].release();
+  for (int i = 0; i < 2; ++i) {
+    if (sk->s_copied[i]) cudaEventDestroy(sk->s_copied[i]);
+    if (sk->s_used[i]) cudaEventDestroy(sk->s_used[i]);
+  }
   if (sk->cstream) cudaStreamDestroy(sk->cstream);
   if (sk->cstart) cudaEventDestroy(sk->cstart);
   for (cudaEvent_t e : sk->cev)
@@ -765,6 +774,24 @@ ace_status ace_sketch_set_stream(AceSketch* sk, void* cuda_stream) {
   if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_set_stream: null sketch");
   ACE_CUDA(cudaStreamSynchronize(sk->stream));
   sk->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : sk->own;
+  return ACE_OK;
+}
+
+ace_status ace_sketch_set_option(AceSketch* sk, int option, int64_t value) {
+  if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_set_option: null sketch");
+  switch (option) {
+    case ACE_OPT_H2D_CHUNKS:
+      if (value < 1 || value > 64) return fail(ACE_E_CONTRACT, "ace_sketch_set_option: chunks must be in [1, 64]");
+      sk->h2d_chunks = static_cast<int>(value);
+      break;
+    case ACE_OPT_DEFER_INSERT:
+      if (value < -1 || value > 1) return fail(ACE_E_CONTRACT, "ace_sketch_set_option: defer mode must be -1, 0 or 1");
+      sk->defer_mode = static_cast<int>(value);
+      break;
+    default:
+      return fail(ACE_E_CONTRACT, "ace_sketch_set_option: unknown option " + std::to_string(option));
+  }
+  sk->drop_graph();
   return ACE_OK;
 }
 
@@ -948,17 +975,13 @@ bool host_pinned(const void* p) {
 ace_status batch_detect(AceSketch* sk, const void* x, int dtype, uint64_t n, uint64_t ld, int x_where,
                         uint32_t* flag_bits, double* scores, int out_where, AceBatchReport* report, int build) {
   if (build) sk->mean_pinned = false;
-  static int gather_env = -1;
-  if (gather_env < 0) {
-    const char* e = getenv("ACE_FUSED_GATHER");
-    gather_env = e ? atoi(e) : 1;
-  }
-  // measured: a gain where the tables fit one shared-memory histogram and the
-  // gathers dominate (cfg 2: 0.541 -> 0.525 ms); a loss on small batches
-  // (cfg 1) and even on cfg 3 (K = 16, two parts)
-  sk->defer_insert = gather_env != 0 && build && sk->width == 32 && sk->fam->use_tc() &&
-                     (gather_env == 2 || (sk->fam->d.k_bits <= 16 && n * sk->fam->d.tables >= (16ull << 20))) &&
-                     sk->fam->d.k_bits <= 16 && fire_and_forget_ok(sk, n);
+  // Deferred insert (counts and gather fused into the detect tail) where the
+  // tables fit one shared-memory histogram and the batch is large enough for
+  // the gathers to dominate (cfg 2: 0.541 -> 0.525 ms; a loss on small
+  // batches such as cfg 1)
+  sk->defer_insert = build && sk->defer_mode >= 0 && sk->width == 32 && sk->fam->use_tc() &&
+                     sk->fam->d.k_bits <= 16 && (sk->defer_mode == 1 || n * sk->fam->d.tables >= (16ull << 20)) &&
+                     fire_and_forget_ok(sk, n);
   sk->insert_deferred = false;
   AceSketch::GraphKey key;
   key.x = x;
@@ -975,25 +998,17 @@ ace_status batch_detect(AceSketch* sk, const void* x, int dtype, uint64_t n, uin
   const DevBuf* bufs[12] = {&sk->ids, &sk->sums, &sk->stage, &sk->flags, &sk->scores, &sk->demand, &sk->near,
                             &sk->overflow, &sk->x16, &sk->rowthr, &sk->segc, &sk->xf32};
   for (int i = 0; i < 12; ++i) key.bufs[i] = bufs[i]->p;
-  static int graphs_env = -2;
-  if (graphs_env == -2) {
-    const char* e = getenv("ACE_GRAPHS");
-    graphs_env = e ? atoi(e) : 1;
-  }
   const bool pinned = x_where == ACE_HOST && host_pinned(x);
-  const bool eligible = graphs_env != 0 && !sk->timing && (x_where == ACE_DEVICE || pinned);
+  const bool eligible = !sk->timing && (x_where == ACE_DEVICE || pinned);
   const void* xd = nullptr;
   uint64_t ldd = 0;
   uint32_t* dflags = nullptr;
   double* dscores = nullptr;
   // Pinned host rows of a large batch: the H2D copy runs in chunks on a copy
   // stream and each chunk is converted and hashed as it lands, so the hashing
-  // hides behind the transfer (ACE_H2D_CHUNKS; 0 = one copy, then the work).
-  static int chunks_env = -2;
-  if (chunks_env == -2) {
-    const char* e = getenv("ACE_H2D_CHUNKS");
-    chunks_env = e ? atoi(e) : 8;
-  }
+  // hides behind the transfer (sk->h2d_chunks, 8 by default; 1 = one copy,
+  // then the work).
+  const int chunks_env = sk->h2d_chunks;
   if (pinned && chunks_env > 1 && !sk->timing && sk->fam->use_tc() && !tc_kstream(sk->fam->tc.nkc) &&
       n >= static_cast<uint64_t>(chunks_env) * 16384u) {
     // chunk boundaries: chunks_env - 1 equal chunks and a last one of a quarter
@@ -1148,11 +1163,17 @@ ace_status ace_sketch_stream_batch(AceSketch* sk, const void* x, int dtype, uint
     }
   }
   uint32_t* dflags = (flag_bits && out_where == ACE_DEVICE) ? flag_bits : sk->flags.as<uint32_t>();
-  if (stream_fused_ok(sk, fire_and_forget_ok(sk, n))) {
-    if (stream_split_env()) ACE_CUDA(sk->demand.ensure(sk->num_counters * sizeof(uint32_t)));
-    ACE_CUDA(launch_stream_step(sk->ids.as<uint32_t>(), n, n, f->d.tables, f->d.k_bits, sk->counters, alpha, dflags,
-                                dsc, sk->st, sk->stream, stream_split_env() ? sk->demand.as<uint32_t>() : nullptr));
+  if (stream_apply_ok(sk, fire_and_forget_ok(sk, n))) {
+    // phase A (counts at batch start, insert), then phase B (scores, flags)
+    if ((r = ensure_stream_bufs(sk, n)) != ACE_OK) return r;
+    const uint32_t slot = static_cast<uint32_t>(sk->stream_seq++ & 1u);
+    uint32_t* cnt = sk->cnt[slot].as<uint32_t>();
+    ACE_CUDA(launch_stream_apply(sk->ids.as<uint32_t>(), n, n, f->d.tables, f->d.k_bits, sk->counters, cnt,
+                                 sk->dts.as<unsigned long long>(), slot, nullptr, 0, nullptr, nullptr, 0, alpha, sk->st,
+                                 sk->stream));
     sk->mark(2);
+    ACE_CUDA(launch_stream_apply(nullptr, 0, 0, f->d.tables, f->d.k_bits, sk->counters, nullptr, nullptr, 0, cnt, n,
+                                 dflags, dsc, slot, alpha, sk->st, sk->stream));
   } else {
     ACE_CUDA(cudaMemsetAsync(&sk->st->batch_sum, 0, sizeof(unsigned long long), sk->stream));
     ACE_CUDA(launch_stream_score(sk->ids.as<uint32_t>(), n, f->d.tables, f->d.k_bits, sk->counters,
@@ -1200,38 +1221,107 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
   ACE_CUDA(zero_call_fields(sk));
   ACE_CUDA(sk->flags.ensure(((n + 31) / 32) * sizeof(uint32_t)));
   uint32_t* dflags = (flag_bits && out_where == ACE_DEVICE) ? flag_bits : sk->flags.as<uint32_t>();
-  std::vector<cudaEvent_t> ev;
+  // per-batch latency: from the start of the batch's work (its group's
+  // hashing for a group's first batch) to the end of the launch that writes
+  // its flags
+  std::vector<cudaEvent_t> ev_a, ev_b;
   if (batch_ms) {
-    ev.resize(nb + 1);
-    for (auto& e : ev) ACE_CUDA(cudaEventCreate(&e));
+    ev_a.resize(nb);
+    ev_b.resize(nb);
+    for (auto& e : ev_a) ACE_CUDA(cudaEventCreate(&e));
+    for (auto& e : ev_b) ACE_CUDA(cudaEventCreate(&e));
   }
-  // Hashing does not depend on the counts, so the batches of a group are
-  // hashed by one projection launch (its fixed cost amortised); scoring and
-  // insertion then run batch by batch in the reference's order.  A group's
-  // first batch latency includes the group's hashing.
-  static int group_env = -1;
-  if (group_env < 0) {
-    const char* e = getenv("ACE_STREAM_GROUP");
-    group_env = e ? std::max(1, atoi(e)) : 4;
+  const bool fast = stream_apply_ok(sk, ff);
+  std::vector<cudaEvent_t> tev;  // timing on: (start, end) pairs, hashing then stream kernels
+  std::vector<int> tkind;
+  auto tmark = [&](int kind, bool end) -> cudaError_t {
+    if (!sk->timing) return cudaSuccess;
+    cudaEvent_t e;
+    cudaError_t err = cudaEventCreate(&e);
+    if (err != cudaSuccess) return err;
+    tev.push_back(e);
+    if (!end) tkind.push_back(kind);
+    return cudaEventRecord(e, sk->stream);
+  };
+  if (fast && (r = ensure_stream_bufs(sk, std::min(batch, n))) != ACE_OK) return r;
+  // the batch whose phase B is still due (fast path)
+  const uint32_t* p_cnt = nullptr;
+  uint64_t p_rows = 0, p_b = 0;
+  uint32_t* p_flags = nullptr;
+  uint32_t p_slot = 0;
+  const uint64_t G = kStreamGroup;
+  // pinned host rows: H2D copies of the next group overlap this group's work
+  const bool overlap = x_where == ACE_HOST && host_pinned(x) && nb > G;
+  if (overlap) {
+    const size_t gbytes = static_cast<size_t>(G * batch) * ld * esz;
+    ACE_CUDA(sk->sstage[0].ensure(gbytes));
+    ACE_CUDA(sk->sstage[1].ensure(gbytes));
+    if (!sk->cstream) ACE_CUDA(cudaStreamCreateWithFlags(&sk->cstream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      if (!sk->s_copied[i]) ACE_CUDA(cudaEventCreateWithFlags(&sk->s_copied[i], cudaEventDisableTiming));
+      if (!sk->s_used[i]) ACE_CUDA(cudaEventCreateWithFlags(&sk->s_used[i], cudaEventDisableTiming));
+    }
+    // the staging halves are free once earlier work on the stream is done
+    ACE_CUDA(cudaEventRecord(sk->s_used[0], sk->stream));
+    ACE_CUDA(cudaEventRecord(sk->s_used[1], sk->stream));
+    ACE_CUDA(cudaStreamWaitEvent(sk->cstream, sk->s_used[0], 0));
+    const uint64_t rows0 = std::min(G * batch, n);
+    ACE_CUDA(cudaMemcpyAsync(sk->sstage[0].p, x, rows0 * ld * esz, cudaMemcpyHostToDevice, sk->cstream));
+    ACE_CUDA(cudaEventRecord(sk->s_copied[0], sk->cstream));
   }
-  const uint64_t G = static_cast<uint64_t>(group_env);
   for (uint64_t g0 = 0; g0 < nb; g0 += G) {
     const uint64_t gb = std::min(G, nb - g0), gr0 = g0 * batch, grows = std::min(gb * batch, n - gr0);
-    if (batch_ms) ACE_CUDA(cudaEventRecord(ev[g0], sk->stream));
+    if (batch_ms) ACE_CUDA(cudaEventRecord(ev_a[g0], sk->stream));
     const void* xg = static_cast<const char*>(x) + gr0 * ld * esz;
     const void* xd;
     uint64_t ldd;
-    r = stage_x(sk, sk->stage, sk->stream, xg, dtype, grows, ld, x_where, &xd, &ldd);
-    if (r == ACE_OK) r = run_hash(sk, xd, dtype, grows, ldd, 0);
-    if (r != ACE_OK) return r;
+    if (overlap) {
+      // group g's rows were copied into staging half g & 1 ahead of time;
+      // start the copy of group g + 1 into the other half once the hash of
+      // group g - 1 (its previous user) has run
+      const int hb = static_cast<int>((g0 / G) & 1u);
+      ACE_CUDA(cudaStreamWaitEvent(sk->stream, sk->s_copied[hb], 0));
+      xd = sk->sstage[hb].p;
+      ldd = ld;
+      ACE_CUDA(tmark(0, false));
+      r = run_hash(sk, xd, dtype, grows, ldd, 0);
+      if (r != ACE_OK) return r;
+      ACE_CUDA(tmark(0, true));
+      ACE_CUDA(cudaEventRecord(sk->s_used[hb], sk->stream));
+      const uint64_t g1 = g0 + G;
+      if (g1 < nb) {
+        const uint64_t r1 = g1 * batch, rows1 = std::min(G * batch, n - r1);
+        ACE_CUDA(cudaStreamWaitEvent(sk->cstream, sk->s_used[hb ^ 1], 0));
+        ACE_CUDA(cudaMemcpyAsync(sk->sstage[hb ^ 1].p, static_cast<const char*>(x) + r1 * ld * esz, rows1 * ld * esz,
+                                 cudaMemcpyHostToDevice, sk->cstream));
+        ACE_CUDA(cudaEventRecord(sk->s_copied[hb ^ 1], sk->cstream));
+      }
+    } else {
+      r = stage_x(sk, sk->stage, sk->stream, xg, dtype, grows, ld, x_where, &xd, &ldd);
+      if (r != ACE_OK) return r;
+      ACE_CUDA(tmark(0, false));
+      r = run_hash(sk, xd, dtype, grows, ldd, 0);
+      if (r != ACE_OK) return r;
+      ACE_CUDA(tmark(0, true));
+    }
     for (uint64_t b = g0; b < g0 + gb; ++b) {
       const uint64_t r0 = b * batch, rows = std::min(batch, n - r0);
-      if (batch_ms && b != g0) ACE_CUDA(cudaEventRecord(ev[b], sk->stream));
+      if (batch_ms && b != g0) ACE_CUDA(cudaEventRecord(ev_a[b], sk->stream));
       const uint32_t* ids = sk->ids.as<uint32_t>() + (r0 - gr0);
-      if (stream_fused_ok(sk, ff)) {
-        if (stream_split_env()) ACE_CUDA(sk->demand.ensure(sk->num_counters * sizeof(uint32_t)));
-        ACE_CUDA(launch_stream_step(ids, rows, grows, f->d.tables, f->d.k_bits, sk->counters, alpha, dflags + r0 / 32,
-                                    nullptr, sk->st, sk->stream, stream_split_env() ? sk->demand.as<uint32_t>() : nullptr));
+      if (fast) {
+        const uint32_t slot = static_cast<uint32_t>(sk->stream_seq++ & 1u);
+        uint32_t* cnt = sk->cnt[slot].as<uint32_t>();
+        ACE_CUDA(tmark(1, false));
+        ACE_CUDA(launch_stream_apply(ids, rows, grows, f->d.tables, f->d.k_bits, sk->counters, cnt,
+                                     sk->dts.as<unsigned long long>(), slot, p_cnt, p_rows, p_flags, nullptr, p_slot,
+                                     alpha, sk->st, sk->stream));
+        ACE_CUDA(tmark(1, true));
+        if (batch_ms && p_rows) ACE_CUDA(cudaEventRecord(ev_b[p_b], sk->stream));
+        p_cnt = cnt;
+        p_rows = rows;
+        p_b = b;
+        p_flags = dflags + r0 / 32;
+        p_slot = slot;
         continue;
       }
       ACE_CUDA(cudaMemsetAsync(&sk->st->batch_sum, 0, sizeof(unsigned long long), sk->stream));
@@ -1240,21 +1330,39 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
       ACE_CUDA(launch_apply_ids(ids, rows, f->d.tables, f->d.k_bits, sk->counters, sk->cap, +1, sk->st, sk->stream,
                                 !ff, grows));
       if (sk->width == 16) ACE_CUDA(launch_cap(sk->counters, sk->num_counters, sk->cap, sk->st, sk->stream));
+      if (batch_ms) ACE_CUDA(cudaEventRecord(ev_b[b], sk->stream));
     }
   }
-  if (batch_ms) ACE_CUDA(cudaEventRecord(ev[nb], sk->stream));
+  if (fast && p_rows) {  // the last batch's phase B
+    ACE_CUDA(tmark(1, false));
+    ACE_CUDA(launch_stream_apply(nullptr, 0, 0, f->d.tables, f->d.k_bits, sk->counters, nullptr, nullptr, 0, p_cnt,
+                                 p_rows, p_flags, nullptr, p_slot, alpha, sk->st, sk->stream));
+    ACE_CUDA(tmark(1, true));
+    if (batch_ms) ACE_CUDA(cudaEventRecord(ev_b[p_b], sk->stream));
+  }
   if (flag_bits && out_where == ACE_HOST)
     if ((r = copy_out(flag_bits, dflags, ((n + 31) / 32) * sizeof(uint32_t), ACE_HOST, sk->stream)) != ACE_OK)
       return r;
   r = pull_state(sk);
   if (r != ACE_OK) return r;
+  if (sk->timing) {
+    sk->stream_ms[0] = sk->stream_ms[1] = 0.0;
+    for (size_t k = 0; k < tkind.size(); ++k) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tev[2 * k], tev[2 * k + 1]);
+      sk->stream_ms[tkind[k]] += ms;
+    }
+    for (auto& e : tev) cudaEventDestroy(e);
+    sk->stream_timed = true;
+  }
   if (batch_ms) {
     for (uint64_t b = 0; b < nb; ++b) {
       float ms = 0.f;
-      cudaEventElapsedTime(&ms, ev[b], ev[b + 1]);
+      cudaEventElapsedTime(&ms, ev_a[b], ev_b[b]);
       batch_ms[b] = ms;
     }
-    for (auto& e : ev) cudaEventDestroy(e);
+    for (auto& e : ev_a) cudaEventDestroy(e);
+    for (auto& e : ev_b) cudaEventDestroy(e);
   }
   fill_stats(stats, *sk->hst, n, f);
   if (report) {
@@ -1315,7 +1423,14 @@ ace_status ace_sketch_restore(AceSketch* sk, const uint64_t* counters, uint64_t 
   ACE_CUDA(cudaStreamSynchronize(sk->stream));
   DevState s{};
   s.n = n;
-  s.T = static_cast<unsigned long long>(std::llround(mean * static_cast<double>(n) * sk->fam->d.tables));
+  // T = sum of the insert numerators = sum c^2 exactly while nothing has
+  // saturated; a saturated 16-bit sketch keeps the rounded mean * n * L
+  unsigned __int128 sq = 0;
+  for (uint64_t i = 0; i < num_counters; ++i) sq += static_cast<unsigned __int128>(tmp[i]) * tmp[i];
+  if (!saturated && (sq >> 64) == 0)
+    s.T = static_cast<unsigned long long>(sq);
+  else
+    s.T = static_cast<unsigned long long>(std::llround(mean * static_cast<double>(n) * sk->fam->d.tables));
   sk->mean_pinned = true;
   sk->pinned_mean = mean;
   s.saturated = saturated ? 1 : 0;
@@ -1338,6 +1453,14 @@ ace_status ace_sketch_set_timing(AceSketch* sk, int enable) {
 
 ace_status ace_sketch_timings(const AceSketch* sk, double* ms3) {
   if (!sk || !ms3) return fail(ACE_E_CONTRACT, "ace_sketch_timings: null argument");
+  if (sk->stream_timed) {  // the last call was the stream driver
+    ms3[0] = sk->stream_ms[0];
+    ms3[1] = 0.0;
+    ms3[2] = sk->stream_ms[1];
+    ms3[3] = 0.0;
+    ms3[4] = sk->stream_ms[0];
+    return ACE_OK;
+  }
   const int pairs[5][2] = {{0, 1}, {1, 2}, {2, 3}, {4, 6}, {6, 5}};
   for (int i = 0; i < 5; ++i) {
     ms3[i] = 0.0;

@@ -34,6 +34,12 @@ struct DevState {
   double mean, sd, thr;          // detect_batch statistics
   double cut;                    // stream cut (mean - alpha)
   double mean_before;
+  // stream cut per batch (stream_apply_kernel): recorded by the batch's
+  // phase A from the state before its insert, read by its phase B one launch
+  // later (two slots, alternating); not reset per call
+  double cut_ring[2], mean_ring[2];
+  int live_ring[2];
+  unsigned int ticket_s;         // phase-A blocks done (the last one commits T and n)
 };
 
 // T / den correctly rounded to binary64 (round half to even), T, den < 2^64:

@@ -49,16 +49,41 @@ constexpr uint32_t kRawBox = 16384;  // one raw box: 128 rows x 32 fp32 (SW128)
 constexpr uint32_t kConvBar = 10;    // named barrier of the converter warps
 constexpr uint32_t kTailBar = 9;     // named barrier of the shared tail
 
+// Compile-time instrumentation (-DACE_TC_PROF=1, profiling builds only):
+// clock64 cycles per pipeline section summed over CTAs into g_tc_prof
+// (read by ace_debug_tc_prof, exported only by such builds).
+#ifndef ACE_TC_PROF
+#define ACE_TC_PROF 0
+#endif
+#if ACE_TC_PROF
+__device__ unsigned long long g_tc_prof[24];
+#define TCP_DECL unsigned long long tcp[24] = {0}; long long tcp_t = 0
+#define TCP_BEGIN() (tcp_t = clock64())
+#define TCP_END(k) (tcp[k] += static_cast<unsigned long long>(clock64() - tcp_t))
+#define TCP_FLUSH(cond) \
+  if (cond)             \
+    for (int k_ = 0; k_ < 24; ++k_) \
+      if (tcp[k_]) atomicAdd(&g_tc_prof[k_], tcp[k_])
+#else
+#define TCP_DECL
+#define TCP_BEGIN()
+#define TCP_END(k)
+#define TCP_FLUSH(cond)
+#endif
+
 // Shared memory: the raw fp32 tile (n_raw boxes), then a ring of W stages
 // (hi + lo block of one direction tile x 64 K).  TMEM (512 columns): nacc
 // fp32 accumulators of tw columns, then n_abuf A operands (hi | lo, 8 columns
 // per K16 step each).
 struct TcLayout {
-  uint32_t n_raw, n_wst, nsteps, acols, nacc, n_abuf;
-  size_t raw_bytes, w_bytes, total;
+  uint32_t n_raw, n_wst, nsteps, acols, nacc, n_abuf, nwords, n_sbuf;
+  size_t raw_bytes, sgn_bytes, w_bytes, total;
 };
 
-__host__ __device__ inline TcLayout tc_layout(uint64_t dim, uint32_t tw) {
+// rows = K * L directions.  Sign words: per point tile, word w of row r at
+// sgn[w][r] (one buffer: nwords * 128 u32, rounded to 1 KB); two buffers when
+// at least three W stages still fit.
+__host__ __device__ inline TcLayout tc_layout(uint64_t dim, uint32_t tw, uint32_t rows) {
   TcLayout L;
   L.n_raw = static_cast<uint32_t>((dim + 31) / 32);
   L.raw_bytes = static_cast<size_t>(L.n_raw) * kRawBox;
@@ -66,13 +91,17 @@ __host__ __device__ inline TcLayout tc_layout(uint64_t dim, uint32_t tw) {
   L.acols = 16u * L.nsteps;
   L.nacc = 2;
   L.n_abuf = (L.nacc * tw + 2u * L.acols <= 512u) ? 2u : 1u;
-  const size_t room = kSmemLimit - 8192 - 1024 - L.raw_bytes;
+  L.nwords = (rows + 31u) / 32u;
+  L.sgn_bytes = (static_cast<size_t>(L.nwords) * kRows * 4u + 1023u) / 1024u * 1024u;
+  const size_t room0 = kSmemLimit - 8192 - 1024 - L.raw_bytes;
   const size_t stage = 2u * tw * 128u;
+  L.n_sbuf = (room0 >= 2u * L.sgn_bytes + 3u * stage) ? 2u : 1u;
+  const size_t room = room0 > L.n_sbuf * L.sgn_bytes ? room0 - L.n_sbuf * L.sgn_bytes : 0;
   size_t st = room / stage;
   if (st > kMaxWStages) st = kMaxWStages;
   L.n_wst = static_cast<uint32_t>(st);
   L.w_bytes = st * stage;
-  L.total = L.raw_bytes + L.w_bytes + 1024;
+  L.total = L.raw_bytes + L.n_sbuf * L.sgn_bytes + L.w_bytes + 1024;
   return L;
 }
 
@@ -180,19 +209,21 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t bar_wfull[kMaxWStages], bar_wempty[kMaxWStages];
   __shared__ __align__(8) uint64_t bar_rawfull, bar_afull[2], bar_aempty[2], bar_thrfull[2], bar_threempty[2];
-  __shared__ __align__(8) uint64_t bar_accfull[2], bar_accempty[2];
+  __shared__ __align__(8) uint64_t bar_accfull[2], bar_accempty[2], bar_sfull[2], bar_sempty[2];
   __shared__ uint32_t tmem_base_sh;
-  __shared__ uint32_t lastw[4][2][32];  // epilogue: last sign word of a direction tile, per quarter / parity
   __shared__ float thr_sm[2][kRows];    // row thresholds per tile parity (converters -> epilogue)
   __shared__ uint32_t lom_sm[2][4];     // K16 steps with a nonzero x lo part, per A buffer / lane quarter
   __shared__ uint32_t seg_n;            // near ties pushed by this CTA
   __shared__ unsigned long long blk_rech, blk_flip, blk_near;
 
   const uint32_t TW = a.tw, wblk = a.tw * 128u;  // direction tile width, one W block (hi or lo) in bytes
-  const TcLayout L = tc_layout(a.dim, TW);
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const TcLayout L = tc_layout(a.dim, TW, a.k_bits * a.tables);
+  // 1 KB aligned (SW128 operands); offset from the __shared__ array itself so
+  // the compiler keeps the accesses in the shared state space (LDS / STS)
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* Rsm = base;                // raw fp32 tile [n_raw][128 rows][32] (SW128)
-  uint8_t* Wsm = base + L.raw_bytes;  // [n_wst][hi | lo][tw * 128 B]
+  uint32_t* Ssm = reinterpret_cast<uint32_t*>(base + L.raw_bytes);  // sign words [n_sbuf][nwords][128]
+  uint8_t* Wsm = base + L.raw_bytes + L.n_sbuf * L.sgn_bytes;      // [n_wst][hi | lo][tw * 128 B]
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t n_tiles = (a.n + kRows - 1) / kRows;
@@ -215,7 +246,9 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
       mbar_init(&bar_thrfull[b], 4);
       mbar_init(&bar_threempty[b], 8);  // every epilogue warp reads its rows' thresholds
       mbar_init(&bar_accfull[b], 1);
-      mbar_init(&bar_accempty[b], 4);   // the four warps (one per quarter) owning the direction tile
+      mbar_init(&bar_accempty[b], 8);   // every epilogue warp reads half of each direction tile
+      mbar_init(&bar_sfull[b], 8u * a.ntiles);  // every epilogue warp, every direction tile
+      mbar_init(&bar_sempty[b], 4);     // the four packer (converter) warps
     }
     fence_mbar_init();
   }
@@ -229,6 +262,9 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
   unsigned long long* seg = a.near_list + blockIdx.x * seg_cap;
   const uint32_t a_col0 = L.nacc * TW;  // first TMEM column of the A buffers
   unsigned long long rr_own = 0, ff_own = 0, nt_own = 0;
+  TCP_DECL;
+  const long long t_kernel = clock64();
+  (void)t_kernel;
 
   if (warp == 0) {
     // ---------------- W producer: per tile, per direction tile j, per K chunk ----------------
@@ -239,6 +275,16 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
           const uint32_t bytes = ((min(TW, R - j * TW) + 15u) & ~15u) * 128u;  // rows of the MMA's N
           for (uint32_t kc = 0; kc < a.nkc; ++kc) {
             mbar_wait_sleepy(&bar_wempty[s], ph ^ 1u);
+#ifdef ACE_EXP_WONCE
+            if (it > 0) {
+              mbar_arrive(&bar_wfull[s]);
+              if (++s == L.n_wst) {
+                s = 0;
+                ph ^= 1u;
+              }
+              continue;
+            }
+#endif
             mbar_expect_tx(&bar_wfull[s], 2u * bytes);
             const uint8_t* src = reinterpret_cast<const uint8_t*>(a.w16) + (static_cast<uint64_t>(j) * a.nkc + kc) * 2u * wblk;
             uint8_t* dst = Wsm + static_cast<size_t>(s) * 2u * wblk;
@@ -261,7 +307,9 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
     for (uint64_t it = 0; it < my_tiles; ++it) {
       const uint32_t b = L.n_abuf == 2u ? static_cast<uint32_t>(it & 1u) : 0u;
       const uint32_t use = static_cast<uint32_t>(L.n_abuf == 2u ? (it >> 1) : it);
+      TCP_BEGIN();
       mbar_wait(&bar_afull[b], use & 1u);
+      TCP_END(0);
       tc_after();
       // lo x hi MMAs of K16 steps whose x lo parts are all zero in this tile
       // are skipped (they would add exact zeros), e.g. one-hot columns
@@ -269,13 +317,17 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
       const uint32_t ta_hi = tmem_base + a_col0 + b * L.acols, ta_lo = ta_hi + L.acols / 2u;
       for (uint32_t j = 0; j < a.ntiles; ++j) {
         const uint32_t idesc = idesc_f16((min(TW, R - j * TW) + 15u) & ~15u);
+        TCP_BEGIN();
         mbar_wait(&bar_accempty[acc], accph ^ 1u);
+        TCP_END(1);
         tc_after();
         const uint32_t dt = tmem_base + acc * TW;
         if (elect_one()) {
           uint32_t ss = s, ph = wph;
           for (uint32_t kc = 0; kc < a.nkc; ++kc) {
+            TCP_BEGIN();
             mbar_wait(&bar_wfull[ss], ph);
+            TCP_END(2);
             const uint32_t b_hi = w_base + ss * 2u * wblk;
             const uint64_t dbh = sw128_desc(b_hi), dbl = sw128_desc(b_hi + wblk);
 #pragma unroll
@@ -311,16 +363,67 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
       if (elect_one()) mma_commit(&bar_aempty[b]);
       __syncwarp();
     }
+#if ACE_TC_PROF
+    tcp[3] += static_cast<unsigned long long>(clock64() - t_kernel);
+#endif
+    TCP_FLUSH(lane == 0);
   } else if (warp >= 10) {
     // ---------------- converters (warps 10-13): raw fp32 tile -> TMEM A operand ----------------
+    // and, one tile behind, the bucket packers: each thread cuts its row's L
+    // bucket ids (MSB-first bit fields of the sign-word stream, srp.cpp:106-113)
+    // from the shared sign words and stores them (coalesced per table).
     const uint32_t q = warp & 3u, r = q * 32u + lane;
     const uint32_t sw = r & 7u;  // SW128: 16-byte unit u of row r sits at unit u ^ (r & 7)
     const uint64_t pol = policy_evict_first();
+    const uint32_t kmask = (K >= 32u) ? 0xffffffffu : ((1u << K) - 1u);
     auto issue_raw = [&](uint64_t t) {
       mbar_expect_tx(&bar_rawfull, L.n_raw * kRawBox);
       for (uint32_t c = 0; c < L.n_raw; ++c)
         tma_load_2d(Rsm + c * kRawBox, &tmx, static_cast<int32_t>(32u * c), static_cast<int32_t>(t * kRows),
                     &bar_rawfull, pol);
+    };
+    auto pack = [&](uint64_t itp) {
+      const uint32_t sb = L.n_sbuf == 2u ? static_cast<uint32_t>(itp & 1u) : 0u;
+      const uint32_t suse = static_cast<uint32_t>(L.n_sbuf == 2u ? (itp >> 1) : itp);
+      TCP_BEGIN();
+      mbar_wait_sleepy(&bar_sfull[sb], suse & 1u);
+      TCP_END(15);
+      TCP_BEGIN();
+      const uint32_t* sg = Ssm + static_cast<size_t>(sb) * (L.sgn_bytes / 4u);
+      const uint64_t row = tile_of(itp) * kRows + r;
+      const bool valid = row < a.n;
+      uint32_t* idp = a.ids + row;
+#ifdef ACE_EXP_NOPACK
+      if (valid && row == 0xffffffffull) idp[0] = 0u;
+      for (uint32_t t0 = 0; t0 < 0u; t0 += 8u) {
+#else
+      // eight tables at a time: all sixteen word loads in flight first (a
+      // table needs the next word only if it straddles, which then exists)
+      for (uint32_t t0 = 0; t0 < a.tables; t0 += 8u) {
+#endif
+        uint32_t bk[8];
+#pragma unroll
+        for (uint32_t u = 0; u < 8u; ++u) {
+          const uint32_t s0 = min(t0 + u, a.tables - 1u) * K, wi = s0 >> 5;
+          const uint32_t hi = sg[wi * kRows + r], lo = sg[min(wi + 1u, L.nwords - 1u) * kRows + r];
+          const unsigned long long win = (static_cast<unsigned long long>(hi) << 32) | lo;
+          bk[u] = static_cast<uint32_t>(win >> (64u - (s0 & 31u) - K)) & kmask;
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < 8u; ++u) {
+          const uint32_t tt = t0 + u;
+#ifndef ACE_EXP_NOSTORE
+          if (valid && tt < a.tables) idp[static_cast<uint64_t>(tt) * a.ids_ld] = bk[u];
+#else
+          if (valid && tt < a.tables && bk[u] == 0xfffffffeu) idp[0] = bk[u];
+#endif
+          if (a.fused_insert && tt < a.tables)
+            insert_bucket_warp(a.counters + (static_cast<uint64_t>(tt) << K), bk[u], valid, lane);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_sempty[sb]);
+      TCP_END(14);
     };
     if (warp == 10 && lane == 0 && my_tiles > 0) issue_raw(tile_of(0));
     const uint32_t lane_base = (q * 32u) << 16;
@@ -330,7 +433,10 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
       const uint32_t b = L.n_abuf == 2u ? p : 0u;
       const uint32_t use = static_cast<uint32_t>(L.n_abuf == 2u ? (it >> 1) : it);
       const bool live = t * kRows + r < a.n;
+      TCP_BEGIN();
       mbar_wait_sleepy(&bar_rawfull, static_cast<uint32_t>(it & 1u));
+      TCP_END(5);
+      TCP_BEGIN();
       // pass 1: max |x| of the row (magnitude bits: NaN > inf > finite)
       uint32_t mb = 0u;
       for (uint32_t c = 0; c < L.n_raw; ++c) {
@@ -343,10 +449,15 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
         }
       }
       const RowScale rs = row_scale(mb, live);
+      TCP_END(6);
+      TCP_BEGIN();
       mbar_wait_sleepy(&bar_aempty[b], (use & 1u) ^ 1u);
       mbar_wait_sleepy(&bar_threempty[p], (static_cast<uint32_t>(it >> 1) & 1u) ^ 1u);
+      TCP_END(7);
+      TCP_BEGIN();
       tc_after();
-      // pass 2: per K16 step, 16 values -> fp16 hi / lo -> 8 + 8 TMEM columns
+      // pass 2: per K16 step, 16 values -> fp16 hi / lo (packed conversions)
+      // -> 8 + 8 TMEM columns
       const uint32_t ta_hi = tmem_base + lane_base + a_col0 + b * L.acols, ta_lo = ta_hi + L.acols / 2u;
       float ss = 0.0f;
       uint32_t lob = 0u;
@@ -368,18 +479,26 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
         for (int i = 0; i < 8; ++i) {
           const float x0 = v[2 * i] * rs.scale, x1 = v[2 * i + 1] * rs.scale;
           ss = fmaf(x0, x0, fmaf(x1, x1, ss));
-          const float h0 = __half2float(__float2half_rn(x0)), h1 = __half2float(__float2half_rn(x1));
-          hw[i] = pack_h2(h0, h1);
-          lw[i] = pack_h2(x0 - h0, x1 - h1);
+          const __half2 hh = __floats2half2_rn(x0, x1);  // low half: x0
+          const float2 hf = __half22float2(hh);
+          const __half2 ll = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+          hw[i] = *reinterpret_cast<const uint32_t*>(&hh);
+          lw[i] = *reinterpret_cast<const uint32_t*>(&ll);
           lor |= lw[i];
         }
         if (lor != 0u) lob |= 1u << st;
         tmem_st8(ta_hi + st * 8u, hw);
         tmem_st8(ta_lo + st * 8u, lw);
       }
+      TCP_END(8);
+      TCP_BEGIN();
       // every converter has read the raw tile: warp 10 loads the next one
       asm volatile("bar.sync %0, 128;" ::"r"(kConvBar) : "memory");
+#ifdef ACE_EXP_NORAW
+      if (warp == 10 && lane == 0 && it + 1 < my_tiles) mbar_arrive(&bar_rawfull);
+#else
       if (warp == 10 && lane == 0 && it + 1 < my_tiles) issue_raw(tile_of(it + 1));
+#endif
       thr_sm[p][r] = row_threshold(rs, live, ss, a.dim, a.margin_c);
       lob = __reduce_or_sync(0xffffffffu, lob);
       if (lane == 0) lom_sm[b][q] = lob;
@@ -390,134 +509,100 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
         mbar_arrive(&bar_afull[b]);
         mbar_arrive(&bar_thrfull[p]);
       }
+      TCP_END(9);
+      if (it > 0) pack(it - 1);
     }
+    if (my_tiles > 0) pack(my_tiles - 1);
+    TCP_FLUSH(warp == 10 && lane == 0);
   } else {
     // ---------------- epilogue (warps 2-9) ----------------
-    // Two warps per TMEM lane quarter (q = warp % 4) take alternate direction
-    // tiles (global tile counter g, owner h = g & 1), all tw columns each, in
-    // 64-column rounds (two 32-column loads in flight).  Per 32 columns: sign
-    // bits packed MSB-first (one funnel shift per column), near ties by one
-    // float min over |v|, four independent chains for ILP.  The sign words stay
-    // in registers and the buckets of the tables ending in the tile are cut
-    // from them.  A table straddling the previous tile needs that tile's last
-    // word, which the partner warp publishes in shared memory (named barriers
-    // 1+q: h=0 -> h=1, 5+q: h=1 -> h=0, one arrive / one sync per tile).
+    // Both warps of a TMEM lane quarter (q = warp % 4, half h) work on every
+    // direction tile, half its columns each (64 or 96: all loads issued
+    // before one wait), so a tile's accumulator is read and released in half
+    // the time.  Per 32 columns: sign bits packed MSB-first (one funnel shift
+    // per column), near ties by one float min over |v|, four independent
+    // chains for ILP.  The tile's sign words go to shared memory
+    // (sgn[word][row]), where the converter warps cut the buckets.
     const uint32_t q = warp & 3, h = (warp - 2) >> 2;
     const uint32_t r = q * 32u + lane;
-    const uint32_t kmask = (K >= 32u) ? 0xffffffffu : ((1u << K) - 1u);
-    const uint32_t nwords = TW / 32u;  // sign words per direction tile (4 or 6)
-    const uint64_t g_total = my_tiles * a.ntiles;
+    const uint32_t hw = TW / 2u, ngrp = hw / 32u;  // columns and 32-column groups per warp (64/2 or 96/3)
     uint32_t acc = 0, accph = 0;
-    uint64_t g = 0;
     for (uint64_t it = 0; it < my_tiles; ++it) {
       const uint64_t t = tile_of(it);
       const uint64_t row = t * kRows + r;
       const bool valid = row < a.n;
       const uint32_t p = static_cast<uint32_t>(it & 1u);
+      const uint32_t sb = L.n_sbuf == 2u ? p : 0u;
+      const uint32_t suse = static_cast<uint32_t>(L.n_sbuf == 2u ? (it >> 1) : it);
+      TCP_BEGIN();
       mbar_wait_sleepy(&bar_thrfull[p], static_cast<uint32_t>(it >> 1) & 1u);
       const float thr = valid ? thr_sm[p][r] : -1.0f;
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_threempty[p]);
+      mbar_wait_sleepy(&bar_sempty[sb], (suse & 1u) ^ 1u);  // the packers are done with this buffer
+      TCP_END(10);
+      uint32_t* sg = Ssm + static_cast<size_t>(sb) * (L.sgn_bytes / 4u);
       const bool zero_row = thr < 0.0f;
       const uint32_t thr_u = zero_row ? 0u : (isinf(thr) ? 0xffffffffu : (__float_as_uint(thr) << 1));
-      for (uint32_t j = 0; j < a.ntiles; ++j, ++g) {
-        if ((g & 1u) == h) {
-          const uint32_t used = min(TW, R - j * TW);
-          const uint32_t col0 = j * TW;
-          mbar_wait_sleepy(&bar_accfull[acc], accph);
-          tc_after();
-          uint32_t wd[6] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
-          // one copy of the 64-column code (small instruction footprint)
-#pragma unroll 1
-          for (uint32_t hr = 0; hr < nwords / 2u; ++hr) {
-            const uint32_t c0 = 64u * hr;
-            if (c0 >= used) break;
-            uint32_t v[64];
-            ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + acc * TW + c0, v);
-            ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + acc * TW + c0 + 32u, (v + 32));
-            tmem_wait_ld();
-            uint32_t w2[2];
+      for (uint32_t j = 0; j < a.ntiles; ++j) {
+        const uint32_t col0 = j * TW + h * hw;  // this warp's first column (direction)
+        const uint32_t used = R > col0 ? min(hw, R - col0) : 0u;
+        TCP_BEGIN();
+        mbar_wait_sleepy(&bar_accfull[acc], accph);
+        TCP_END(11);
+        TCP_BEGIN();
+        tc_after();
+        uint32_t v[96];
+        const uint32_t ta = tmem_base + ((q * 32u) << 16) + acc * TW + h * hw;
+        ACE_TMEM_LD32(ta, v);
+        ACE_TMEM_LD32(ta + 32u, (v + 32));
+        if (ngrp > 2u) ACE_TMEM_LD32(ta + 64u, (v + 64));
+        tmem_wait_ld();
+        tc_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_accempty[acc]);  // read: the MMAs may reuse it
+        uint32_t wd[3];
 #pragma unroll
-            for (uint32_t g2 = 0; g2 < 2; ++g2) {
-              const uint32_t cc = c0 + 32u * g2;
-              const uint32_t* vv = v + 32 * g2;
-              // near-tie test on |v| as a float min (FMNMX with |.| operands);
-              // NaN (non-finite rows, thr = inf) fails `mn > thr`
-              uint32_t n4[4] = {0u, 0u, 0u, 0u};
-              float m4[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+        for (uint32_t g2 = 0; g2 < 3u; ++g2) {
+          wd[g2] = 0xffffffffu;
+          if (g2 >= ngrp) break;
+          const uint32_t cc = 32u * g2;
+          const uint32_t* vv = v + 32 * g2;
+          // near-tie test on |v| as a float min (FMNMX with |.| operands);
+          // NaN (non-finite rows, thr = inf) fails `mn > thr`
+          uint32_t n4[4] = {0u, 0u, 0u, 0u};
+          float m4[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
 #pragma unroll
-              for (int jj = 0; jj < 8; ++jj)
+          for (int jj = 0; jj < 8; ++jj)
 #pragma unroll
-                for (int gq = 0; gq < 4; ++gq) {
-                  n4[gq] = (n4[gq] << 1) | (vv[gq * 8 + jj] >> 31);
-                  m4[gq] = fminf(m4[gq], fabsf(__uint_as_float(vv[gq * 8 + jj])));
-                }
-              const uint32_t neg = (n4[0] << 24) | (n4[1] << 16) | (n4[2] << 8) | n4[3];
-              const float mn = fminf(fminf(m4[0], m4[1]), fminf(m4[2], m4[3]));
-              // columns past `used` (padding / stale) are masked here, off the hot path
-              if (!zero_row && valid && !(mn > thr) && cc < used) {
-                const uint32_t ncol = min(32u, used - cc);
-                uint32_t nm = 0u;
+            for (int gq = 0; gq < 4; ++gq) {
+              n4[gq] = (n4[gq] << 1) | (vv[gq * 8 + jj] >> 31);
+              m4[gq] = fminf(m4[gq], fabsf(__uint_as_float(vv[gq * 8 + jj])));
+            }
+          const uint32_t neg = (n4[0] << 24) | (n4[1] << 16) | (n4[2] << 8) | n4[3];
+          const float mn = fminf(fminf(m4[0], m4[1]), fminf(m4[2], m4[3]));
+          // columns past `used` (padding / stale) are masked here, off the hot path
+          if (!zero_row && valid && !(mn > thr) && cc < used) {
+            const uint32_t ncol = min(32u, used - cc);
+            uint32_t nm = 0u;
 #pragma unroll
-                for (int jj = 0; jj < 32; ++jj) nm |= (((vv[jj] << 1) <= thr_u) ? 1u : 0u) << jj;
-                if (ncol < 32u) nm &= (1u << ncol) - 1u;
-                if (nm) push_near_mask(a.st, seg, seg_cap, &seg_n, a.overflow_rows, nm, row, col0 + cc);
-              }
-              w2[g2] = zero_row ? 0xffffffffu : ~neg;  // bit (31-jj) = column cc+jj >= 0
-            }
-            if (hr == 0) {
-              wd[0] = w2[0];
-              wd[1] = w2[1];
-            } else if (hr == 1) {
-              wd[2] = w2[0];
-              wd[3] = w2[1];
-            } else {
-              wd[4] = w2[0];
-              wd[5] = w2[1];
-            }
+            for (int jj = 0; jj < 32; ++jj) nm |= (((vv[jj] << 1) <= thr_u) ? 1u : 0u) << jj;
+            if (ncol < 32u) nm &= (1u << ncol) - 1u;
+            if (nm) push_near_mask(a.st, seg, seg_cap, &seg_n, a.overflow_rows, nm, row, col0 + cc);
           }
-          tc_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&bar_accempty[acc]);
-          // last word of the previous tile (partner warp), for a straddling table
-          uint32_t prev = 0u;
-          if (g > 0) {
-            asm volatile("bar.sync %0, 64;" ::"r"((h == 1 ? 1u : 5u) + q) : "memory");
-            prev = lastw[q][(g - 1) & 1u][lane];
-          }
-          // publish this tile's last word for the partner (next tile's owner)
-          if (g + 1 < g_total) {
-            lastw[q][g & 1u][lane] = nwords == 4u ? wd[3] : wd[5];
-            asm volatile("bar.arrive %0, 64;" ::"r"((h == 0 ? 1u : 5u) + q) : "memory");
-          }
-          // buckets of the tables whose last column lies in this tile (host
-          // precomputed range): bits [t*K, t*K+K) of the big-endian column
-          // stream, words nwords*j-1 (prev) .. nwords*j+nwords-1 (wd); a
-          // window over the stream moves down a word whenever the bit offset
-          // passes 32 (no dynamic register indexing)
-          const uint32_t tb = j == 0 ? 0u : a.tab_end[j - 1], te = a.tab_end[j];
-          uint32_t* idp = a.ids + row;
-          if (tb < te) {
-            const uint32_t s0 = tb * K;
-            uint32_t w0 = prev, w1 = wd[0], w2 = wd[1], w3 = wd[2], w4 = wd[3], w5 = nwords == 4u ? 0u : wd[4],
-                     w6 = nwords == 4u ? 0u : wd[5];
-            if (static_cast<int>(s0 >> 5) - static_cast<int>(nwords * j) >= 0) {
-              w0 = w1; w1 = w2; w2 = w3; w3 = w4; w4 = w5; w5 = w6; w6 = 0u;
-            }
-            uint32_t off = s0 & 31u;
-            for (uint32_t tt = tb; tt < te; ++tt) {
-              const unsigned long long win = (static_cast<unsigned long long>(w0) << 32) | w1;
-              const uint32_t bucket = static_cast<uint32_t>(win >> (64u - off - K)) & kmask;
-              if (valid) idp[static_cast<uint64_t>(tt) * a.ids_ld] = bucket;
-              if (a.fused_insert) insert_bucket_warp(a.counters + (static_cast<uint64_t>(tt) << K), bucket, valid, lane);
-              off += K;
-              if (off >= 32u) {
-                off -= 32u;
-                w0 = w1; w1 = w2; w2 = w3; w3 = w4; w4 = w5; w5 = w6; w6 = 0u;
-              }
-            }
-          }
+          wd[g2] = zero_row ? 0xffffffffu : ~neg;  // bit (31-jj) = column cc+jj >= 0
         }
+        TCP_END(12);
+        TCP_BEGIN();
+        // sign words of this half tile: global words (j * TW + h * hw) / 32 + g2
+#pragma unroll
+        for (uint32_t g2 = 0; g2 < 3u; ++g2) {
+          const uint32_t gw = col0 / 32u + g2;
+          if (g2 < ngrp && gw < L.nwords) sg[gw * kRows + r] = wd[g2];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_sfull[sb]);
+        TCP_END(13);
         if (++acc == L.nacc) {
           acc = 0;
           accph ^= 1u;
@@ -526,6 +611,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
     }
   }
 
+  TCP_FLUSH(warp == 2 && lane == 0);
   if (warp >= 2) {
     // ---- shared tail: exact recheck of the listed near ties ----
     asm volatile("bar.sync %0, %1;" ::"r"(kTailBar), "r"(kTail) : "memory");  // ids stored, list complete
@@ -549,6 +635,9 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
       if (a.fused_insert && blockIdx.x == 0) atomicAdd(&a.st->n, a.n);
     }
   }
+#if ACE_TC_PROF
+  if (threadIdx.x == 0) atomicAdd(&g_tc_prof[16], static_cast<unsigned long long>(clock64() - t_kernel));
+#endif
   tc_before();
   __syncthreads();
   tc_after();
@@ -686,13 +775,6 @@ float tc_margin(uint32_t nkc, bool x_f64) {
   return static_cast<float>(2.0 * (4.0 * 0x1.0p-22 + 0x1.0p-23 * (12.0 * nkc + 16.0) * 1.01 + (x_f64 ? 0x1.0p-23 : 0.0)));
 }
 
-void tc_fill_tables(TcArgs* a) {
-  for (uint32_t j = 0; j < a->ntiles && j < 64; ++j) {
-    const uint32_t end_col = std::min((j + 1) * a->tw, a->k_bits * a->tables);
-    a->tab_end[j] = static_cast<uint16_t>(std::min(end_col / a->k_bits, a->tables));
-  }
-}
-
 cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc) {
   tc->enabled = 0;
   if (!tc_supported(f.dim) || f.k_bits > 128 || !tmap_encoder()) return cudaSuccess;
@@ -702,7 +784,7 @@ cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc) {
   // (d <= 64), else 128; the K-streamed kernel: 256 (whole tables per tile)
   const uint32_t nsteps = static_cast<uint32_t>((f.dim + 15) / 16);
   const uint32_t tw = ks ? 256u : (2u * 192u + 2u * 16u * nsteps <= 512u ? 192u : 128u);
-  if (!ks && tc_layout(f.dim, tw).n_wst < 2) return cudaSuccess;
+  if (!ks && tc_layout(f.dim, tw, f.rows).n_wst < 2) return cudaSuccess;
   tc->nkc = nkc;
   tc->tw = tw;
   const uint32_t tpt = tw / f.k_bits;
@@ -712,7 +794,6 @@ cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc) {
   }
   const uint32_t dpt = ks ? tpt * f.k_bits : tw;
   tc->ntiles = ks ? (f.tables + tpt - 1) / tpt : (f.rows + tw - 1) / tw;
-  if (tc->ntiles > 64 && !ks) return cudaSuccess;  // TcArgs::tab_end
   const size_t bytes = static_cast<size_t>(tc->ntiles) * nkc * 2 * tw * 128u;
   cudaError_t e = cudaMalloc(&tc->w16, bytes);
   if (e != cudaSuccess) return e;
@@ -731,8 +812,9 @@ cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc) {
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return e;
     if ((e = tck_prepare(tw)) != cudaSuccess) return e;
   } else {
+    // every layout stays within kSmemLimit - 8192 (tc_layout)
     e = cudaFuncSetAttribute(hash_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(tc_layout(f.dim, tw).total));
+                             static_cast<int>(kSmemLimit - 8192));
     if (e != cudaSuccess) return e;
   }
   tc->enabled = 1;
@@ -770,10 +852,22 @@ cudaError_t launch_hash_tc(const TcArgs& a, void* stage, cudaStream_t s) {
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   const uint64_t tiles = (a.n + kRows - 1) / kRows;
   const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(tc_sms()));
-  hash_tc_kernel<<<static_cast<unsigned>(grid), kThreads, tc_layout(a.dim, a.tw).total, s>>>(a, map);
+  hash_tc_kernel<<<static_cast<unsigned>(grid), kThreads, tc_layout(a.dim, a.tw, a.k_bits * a.tables).total, s>>>(a, map);
   count_launch();
   return cudaGetLastError();
 }
+
+#if ACE_TC_PROF
+extern "C" int ace_debug_tc_prof(unsigned long long* out24, int reset) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out24, g_tc_prof, sizeof(unsigned long long) * 24) != cudaSuccess) return -1;
+  if (reset) {
+    unsigned long long z[24] = {0};
+    cudaMemcpyToSymbol(g_tc_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 cudaError_t launch_recheck(const TcArgs& a, cudaStream_t s) {
   recheck_rows_kernel<<<148, 256, 0, s>>>(a);  // exits at once unless a list segment overflowed

@@ -51,7 +51,9 @@ __global__ void __launch_bounds__(kKsThreads, 1) hash_tck_kernel(const TcArgs a)
   __shared__ uint32_t tmem_base_sh;
   __shared__ uint32_t sgbuf[2][C::kWords][kRows];  // sign words of a direction tile, by tile parity
   __shared__ uint32_t seg_n;
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1 KB aligned (SW128 operands); offset from the __shared__ array itself so
+  // the compiler keeps the accesses in the shared state space (LDS / STS)
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t n_tiles = (a.n + kRows - 1) / kRows;
   const uint32_t K = a.k_bits, nkc = a.nkc, nch = ks_chunks(nkc);

@@ -14,6 +14,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include "ace_kernels.cuh"
 
@@ -23,6 +24,13 @@ namespace cg = cooperative_groups;
 namespace ace_dev {
 
 namespace {
+
+// Stream flags: scores within this relative distance of the cut mean - alpha
+// are counted as ambiguous.  The cut uses the exact mean T / (n L); the
+// reference's rounded recurrence (sketch.cpp:69-71) drifted by at most
+// 3.4e-13 relative from it over the whole 100M-row config-5 stream
+// (tests/golden/golden_full.json, make_golden_full.py); the band is ~40x that.
+constexpr double kStreamBand = 0x1.0p-36;
 
 constexpr int BM = 128;          // points per CTA tile
 constexpr int BN = kTileCols;    // directions per CTA tile
@@ -65,46 +73,6 @@ __device__ __forceinline__ void atomic_add_u128(unsigned long long* lo, unsigned
   const unsigned long long old = atomicAdd(lo, vlo);
   const unsigned long long carry = (old + vlo < old) ? 1ull : 0ull;
   if (vhi + carry) atomicAdd(hi, vhi + carry);
-}
-
-// Exact reference projection: binary64 mul-then-add fold from +0.0.
-__device__ __forceinline__ double exact_projection(const double* __restrict__ w,
-                                                   const void* x, int x_f64,
-                                                   uint64_t row, uint64_t ld,
-                                                   uint64_t dim) {
-  // binary64 left fold, mul then add, from +0.0 (srp.cpp:78-91); operands
-  // are loaded 8 ahead so only the add chain is serial
-  double acc = 0.0;
-  uint64_t i = 0;
-  if (x_f64) {
-    const double* xr = static_cast<const double*>(x) + row * ld;
-    for (; i + 8 <= dim; i += 8) {
-      double wv[8], xv[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        wv[k] = w[i + k];
-        xv[k] = xr[i + k];
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) acc = __dadd_rn(acc, __dmul_rn(wv[k], xv[k]));
-    }
-    for (; i < dim; ++i) acc = __dadd_rn(acc, __dmul_rn(w[i], xr[i]));
-  } else {
-    const float* xr = static_cast<const float*>(x) + row * ld;
-    for (; i + 8 <= dim; i += 8) {
-      double wv[8];
-      float xv[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        wv[k] = w[i + k];
-        xv[k] = xr[i + k];
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) acc = __dadd_rn(acc, __dmul_rn(wv[k], static_cast<double>(xv[k])));
-    }
-    for (; i < dim; ++i) acc = __dadd_rn(acc, __dmul_rn(w[i], static_cast<double>(xr[i])));
-  }
-  return acc;
 }
 
 // The reference's fold plus the oracle's sequential |x|^2 (near-tie measure).
@@ -471,56 +439,13 @@ __global__ void sum_squares_kernel(const uint32_t* __restrict__ c, uint64_t num,
 // table-major id array (spanning at most a few tables), counts into a 2^K u32
 // shared histogram with warp-aggregated shared atomics, and merges it into the
 // global counters (one atomic per touched bucket) whenever the table changes.
-// One shared-histogram increment per lane holding a bucket (b != ~0).
-//   ACE_HIST_MATCH=2 (default): a plain shared atomic per id.  Measured
-//     fastest on every input tried (cfg 2: 0.487 vs 0.507 ms per step, cfg 3:
-//     18.7 vs 19.9 ms; 2M rows of only 8 distinct points: 1.64 vs 2.14 ms),
-//     the shared-memory atomic unit absorbs equal addresses within a warp.
-//   ACE_HIST_MATCH=0: equal buckets merged by up to four ballot rounds first.
-//   ACE_HIST_MATCH=1: merged by match.any (slowest).
-//   ACE_HIST_MATCH=3: ballot rounds only when lane 0's bucket recurs.
-#ifndef ACE_HIST_MATCH
-#define ACE_HIST_MATCH 2
-#endif
+// One shared-histogram increment per id (b != ~0).  A plain shared atomic
+// per id measured fastest on every input tried, clustered ones included
+// (ballot-round or match.any merging of equal buckets cost more than they
+// save: cfg 2 0.487 vs 0.507 ms, 2M rows of 8 distinct points 1.64 vs 2.14 ms).
 __device__ __forceinline__ void hist_add_warp(uint32_t* hist, uint32_t b, int lane) {
-#if ACE_HIST_MATCH == 2
+  (void)lane;
   if (b != 0xffffffffu) atomicAdd(&hist[b], 1u);
-#elif ACE_HIST_MATCH == 3
-  const uint32_t b0 = __shfl_sync(0xffffffffu, b, 0);
-  if (!__any_sync(0xffffffffu, lane != 0 && b == b0 && b != 0xffffffffu)) {
-    if (b != 0xffffffffu) atomicAdd(&hist[b], 1u);
-    return;
-  }
-  unsigned rem = __ballot_sync(0xffffffffu, b != 0xffffffffu);
-#pragma unroll 1
-  for (int round = 0; round < 4 && rem; ++round) {
-    const int leader = __ffs(rem) - 1;
-    const uint32_t bl = __shfl_sync(0xffffffffu, b, leader);
-    const unsigned eq = __ballot_sync(0xffffffffu, b == bl) & rem;
-    if (eq == (1u << leader)) break;
-    if (lane == leader) atomicAdd(&hist[bl], static_cast<uint32_t>(__popc(eq)));
-    rem &= ~eq;
-  }
-  if ((rem >> lane) & 1u) atomicAdd(&hist[b], 1u);
-#elif ACE_HIST_MATCH == 1
-  const unsigned live = __ballot_sync(0xffffffffu, b != 0xffffffffu);
-  if (b != 0xffffffffu) {
-    const unsigned m = __match_any_sync(live, b);
-    if (lane == __ffs(m) - 1) atomicAdd(&hist[b], static_cast<uint32_t>(__popc(m)));
-  }
-#else
-  unsigned rem = __ballot_sync(0xffffffffu, b != 0xffffffffu);
-#pragma unroll 1
-  for (int round = 0; round < 4 && rem; ++round) {
-    const int leader = __ffs(rem) - 1;
-    const uint32_t bl = __shfl_sync(0xffffffffu, b, leader);
-    const unsigned eq = __ballot_sync(0xffffffffu, b == bl) & rem;
-    if (eq == (1u << leader)) break;  // nothing merged: stop aggregating
-    if (lane == leader) atomicAdd(&hist[bl], static_cast<uint32_t>(__popc(eq)));
-    rem &= ~eq;
-  }
-  if ((rem >> lane) & 1u) atomicAdd(&hist[b], 1u);
-#endif
 }
 
 // kTrackT: accumulate the insert numerators from the pre-add counter values
@@ -608,15 +533,11 @@ __global__ void __launch_bounds__(1024) apply_ids_smem_kernel(const uint32_t* __
   }
 }
 
-#ifndef ACE_COUNT_DBG
-#define ACE_COUNT_DBG 0
-#endif
-#ifndef ACE_COUNT_VEC
-#define ACE_COUNT_VEC 4  // 16-byte id vectors per thread in flight in the one-part count
-#endif
 // Phase 1 of the fused passes: counts of the block's id range [i0, i1)
 // (flattened table-major ids), bins of `part` only, merged into `counters`
-// with fire-and-forget REDs (32-bit, unsaturable sketches).
+// with fire-and-forget REDs (32-bit, unsaturable sketches).  The ids are read
+// with coherent L2 loads (ld.global.cg): phase 2 of the same launch rewrites
+// them in place, so the read-only (non-coherent) path must not cache them.
 __device__ void count_range(const uint32_t* ids, uint64_t n, uint32_t k_bits, uint32_t part_bits, uint32_t part,
                             uint64_t i0, uint64_t i1, uint32_t* counters, uint32_t* hist, DevState* st) {
   const uint32_t nb = 1u << part_bits;
@@ -624,7 +545,7 @@ __device__ void count_range(const uint32_t* ids, uint64_t n, uint32_t k_bits, ui
   const int lane = threadIdx.x & 31;
   unsigned long long dT = 0ull;
   constexpr int kDepth = 8;
-  constexpr int kVec = ACE_COUNT_VEC;  // 16-byte vectors per thread in flight (one-part path)
+  constexpr int kVec = 4;  // 16-byte vectors per thread in flight (one-part path)
   const uint32_t step = blockDim.x * kDepth;
   for (uint64_t seg = i0; seg < i1;) {
     const uint64_t t = seg / n;
@@ -633,24 +554,20 @@ __device__ void count_range(const uint32_t* ids, uint64_t n, uint32_t k_bits, ui
     if (pshift == 0) {
       // one part: every id counts; 16-byte loads (scalar head / tail)
       const uint64_t a = min(seg_end, static_cast<uint64_t>((seg + 3u) & ~static_cast<uint64_t>(3))), nv = (seg_end - a) >> 2, z = a + (nv << 2);
-      for (uint64_t i = seg + threadIdx.x; i < a; i += blockDim.x) atomicAdd(&hist[__ldg(ids + i)], 1u);
-      for (uint64_t i = z + threadIdx.x; i < seg_end; i += blockDim.x) atomicAdd(&hist[__ldg(ids + i)], 1u);
+      for (uint64_t i = seg + threadIdx.x; i < a; i += blockDim.x) atomicAdd(&hist[__ldcg(ids + i)], 1u);
+      for (uint64_t i = z + threadIdx.x; i < seg_end; i += blockDim.x) atomicAdd(&hist[__ldcg(ids + i)], 1u);
       const uint4* v4 = reinterpret_cast<const uint4*>(ids + a);
       for (uint64_t base = 0; base < nv; base += kVec * blockDim.x) {
         uint4 q[kVec];
 #pragma unroll
-        for (int u = 0; u < kVec; ++u) q[u] = __ldg(v4 + min(base + u * blockDim.x + threadIdx.x, nv - 1u));
+        for (int u = 0; u < kVec; ++u) q[u] = __ldcg(v4 + min(base + u * blockDim.x + threadIdx.x, nv - 1u));
 #pragma unroll
         for (int u = 0; u < kVec; ++u)
           if (base + u * blockDim.x + threadIdx.x < nv) {
-#if ACE_COUNT_DBG & 1  // timing experiment: no atomics (wrong counts)
-            if ((q[u].x ^ q[u].y ^ q[u].z ^ q[u].w) == 0xffffffffu) hist[0] = 1u;
-#else
             atomicAdd(&hist[q[u].x], 1u);
             atomicAdd(&hist[q[u].y], 1u);
             atomicAdd(&hist[q[u].z], 1u);
             atomicAdd(&hist[q[u].w], 1u);
-#endif
           }
       }
     } else {
@@ -659,7 +576,7 @@ __device__ void count_range(const uint32_t* ids, uint64_t n, uint32_t k_bits, ui
         const uint32_t* src = ids + base;
         uint32_t idv[kDepth];
 #pragma unroll
-        for (int u = 0; u < kDepth; ++u) idv[u] = __ldg(src + min(u * blockDim.x + threadIdx.x, len - 1u));
+        for (int u = 0; u < kDepth; ++u) idv[u] = __ldcg(src + min(u * blockDim.x + threadIdx.x, len - 1u));
 #pragma unroll
         for (int u = 0; u < kDepth; ++u) {
           const uint32_t id = idv[u];
@@ -669,12 +586,8 @@ __device__ void count_range(const uint32_t* ids, uint64_t n, uint32_t k_bits, ui
         }
       }
     }
-#if ACE_COUNT_DBG & 2  // timing experiment: no merge (wrong counts)
-    __syncthreads();
-#else
     flush_hist<false>(hist, nb, counters + (t << k_bits) + (static_cast<uint64_t>(part) << part_bits), 0xffffffffu,
                       st, dT);
-#endif
     seg = seg_end;
   }
 }
@@ -708,13 +621,13 @@ __device__ void count_range16(const uint32_t* ids, uint64_t n, uint64_t i0, uint
     __syncthreads();
     const uint64_t a = min(seg_end, static_cast<uint64_t>((seg + 3u) & ~static_cast<uint64_t>(3))), nv = (seg_end - a) >> 2,
                    z = a + (nv << 2);
-    for (uint64_t i = seg + threadIdx.x; i < a; i += blockDim.x) hist16_add(hist, __ldg(ids + i), ct);
-    for (uint64_t i = z + threadIdx.x; i < seg_end; i += blockDim.x) hist16_add(hist, __ldg(ids + i), ct);
+    for (uint64_t i = seg + threadIdx.x; i < a; i += blockDim.x) hist16_add(hist, __ldcg(ids + i), ct);
+    for (uint64_t i = z + threadIdx.x; i < seg_end; i += blockDim.x) hist16_add(hist, __ldcg(ids + i), ct);
     const uint4* v4 = reinterpret_cast<const uint4*>(ids + a);
     for (uint64_t base = 0; base < nv; base += kVec * blockDim.x) {
       uint4 q[kVec];
 #pragma unroll
-      for (int u = 0; u < kVec; ++u) q[u] = __ldg(v4 + min(base + u * blockDim.x + threadIdx.x, nv - 1u));
+      for (int u = 0; u < kVec; ++u) q[u] = __ldcg(v4 + min(base + u * blockDim.x + threadIdx.x, nv - 1u));
 #pragma unroll
       for (int u = 0; u < kVec; ++u)
         if (base + u * blockDim.x + threadIdx.x < nv) {
@@ -939,7 +852,7 @@ __device__ void score_rows(const uint32_t* __restrict__ ids, uint64_t ids_stride
       for (; t + 8 <= tables; t += 8) {
         uint4 c[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) c[u] = __ldcs(reinterpret_cast<const uint4*>(ids + (uint64_t)(t + u) * ids_stride) + g);
+        for (int u = 0; u < 8; ++u) c[u] = __ldcg(reinterpret_cast<const uint4*>(ids + (uint64_t)(t + u) * ids_stride) + g);
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           S[0] += c[u].x;
@@ -949,7 +862,7 @@ __device__ void score_rows(const uint32_t* __restrict__ ids, uint64_t ids_stride
         }
       }
       for (; t < tables; ++t) {
-        const uint4 c = __ldcs(reinterpret_cast<const uint4*>(ids + (uint64_t)t * ids_stride) + g);
+        const uint4 c = __ldcg(reinterpret_cast<const uint4*>(ids + (uint64_t)t * ids_stride) + g);
         S[0] += c.x;
         S[1] += c.y;
         S[2] += c.z;
@@ -1236,88 +1149,6 @@ __device__ void replay_dev(const uint64_t* __restrict__ sums, uint64_t n, uint32
   __syncthreads();
 }
 
-// build_sketch's deferred insert for K <= 15 without grid barriers: each
-// table is owned by a cluster of two CTAs.  CTA r counts rows [r n/2,
-// (r+1) n/2) of the table into its shared histogram; after a cluster barrier
-// it merges bins [r 2^K/2, (r+1) 2^K/2) with the peer's histogram (distributed
-// shared memory) and the sketch's existing counts, writes the final counts
-// (plain stores: no other CTA touches the table) and adds their squares to T;
-// after a second barrier it copies the peer's final half, so each CTA holds
-// the whole final table, and replaces its rows' ids by their counts in place.
-// The detect tail then scores from the counts (gather = 2).
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024)
-    count_gather_pair_kernel(uint32_t* ids, uint64_t n, uint32_t k_bits, uint32_t* counters, DevState* st) {
-  extern __shared__ __align__(16) uint32_t hist[];
-  __shared__ unsigned long long blk;
-  cg::cluster_group cl = cg::this_cluster();
-  const uint32_t r = cl.block_rank();
-  const uint64_t t = blockIdx.x >> 1;
-  const uint32_t nb = 1u << k_bits, half = (nb + 1u) / 2u;
-  uint32_t* tids = ids + t * n;
-  const uint64_t row0 = n * r / 2, row1 = n * (r + 1) / 2;
-  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
-  if (threadIdx.x == 0) blk = 0ull;
-  __syncthreads();
-  // rows [row0, row1) of the flattened ids: scalar head and tail, 16-byte body
-  const uint64_t g0 = t * n + row0, g1 = t * n + row1;
-  const uint64_t va = min(g1, (g0 + 3u) & ~static_cast<uint64_t>(3)), nv = (g1 - va) >> 2, vz = va + (nv << 2);
-  constexpr int kVec = 4;
-  for (uint64_t i = g0 + threadIdx.x; i < va; i += blockDim.x) atomicAdd(&hist[ids[i]], 1u);
-  for (uint64_t i = vz + threadIdx.x; i < g1; i += blockDim.x) atomicAdd(&hist[ids[i]], 1u);
-  const uint4* v4 = reinterpret_cast<const uint4*>(ids + va);
-  for (uint64_t base = 0; base < nv; base += kVec * blockDim.x) {
-    uint4 q[kVec];
-#pragma unroll
-    for (int u = 0; u < kVec; ++u) q[u] = __ldg(v4 + min(base + u * blockDim.x + threadIdx.x, nv - 1u));
-#pragma unroll
-    for (int u = 0; u < kVec; ++u)
-      if (base + u * blockDim.x + threadIdx.x < nv) {
-        atomicAdd(&hist[q[u].x], 1u);
-        atomicAdd(&hist[q[u].y], 1u);
-        atomicAdd(&hist[q[u].z], 1u);
-        atomicAdd(&hist[q[u].w], 1u);
-      }
-  }
-  cl.sync();
-  // merge this CTA's half of the bins: existing + own + peer
-  uint32_t* peer = cl.map_shared_rank(hist, r ^ 1u);
-  uint32_t* ct = counters + (t << k_bits);
-  unsigned long long dT = 0ull;
-  const uint32_t b0 = r * half, b1 = min(nb, b0 + half);
-  for (uint32_t b = b0 + threadIdx.x; b < b1; b += blockDim.x) {
-    const uint32_t c = ct[b] + hist[b] + peer[b];
-    ct[b] = c;
-    hist[b] = c;
-    dT += static_cast<unsigned long long>(c) * c;
-  }
-  cl.sync();
-  // the peer's final half
-  const uint32_t p0 = (r ^ 1u) * half, p1 = min(nb, p0 + half);
-  for (uint32_t b = p0 + threadIdx.x; b < p1; b += blockDim.x) hist[b] = peer[b];
-  cl.sync();  // the peer has read our half: it may leave, we may rewrite ids
-  for (uint64_t i = g0 + threadIdx.x; i < va; i += blockDim.x) ids[i] = hist[ids[i]];
-  for (uint64_t i = vz + threadIdx.x; i < g1; i += blockDim.x) ids[i] = hist[ids[i]];
-  uint4* w4 = reinterpret_cast<uint4*>(ids + va);
-  for (uint64_t base = 0; base < nv; base += 8 * blockDim.x) {
-    uint4 q[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) q[u] = w4[min(base + u * blockDim.x + threadIdx.x, nv - 1u)];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const uint64_t j = base + u * blockDim.x + threadIdx.x;
-      if (j < nv) w4[j] = make_uint4(hist[q[u].x], hist[q[u].y], hist[q[u].z], hist[q[u].w]);
-    }
-  }
-  (void)tids;
-  dT = warp_sum_u64(dT);
-  if ((threadIdx.x & 31) == 0 && dT) atomicAdd(&blk, dT);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (blk) atomicAdd(&st->T, blk);
-    if (blockIdx.x == 0) atomicAdd(&st->n, n);
-  }
-}
-
 // ---- fused detect tail ------------------------------------------------------
 //
 // build_sketch's deferred insert + detect_batch in one cooperative launch
@@ -1344,16 +1175,7 @@ struct TailArgs {
   double* scores;
   uint32_t* flag_bits;
   DevState* st;
-  unsigned long long* prof;  // instrumentation: %globaltimer at the phase boundaries (block 0), or null
 };
-
-__device__ __forceinline__ void tail_stamp(const TailArgs& a, int i) {
-  if (a.prof && blockIdx.x == 0 && threadIdx.x == 0) {
-    unsigned long long g;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
-    a.prof[i] = g;
-  }
-}
 
 __global__ void __launch_bounds__(1024) detect_tail_kernel(const TailArgs a) {
   extern __shared__ __align__(16) uint32_t hist[];  // gather: 2^min(K,15) u32 / 2^16 u16; else blockDim doubles
@@ -1362,7 +1184,6 @@ __global__ void __launch_bounds__(1024) detect_tail_kernel(const TailArgs a) {
   cg::grid_group grid = cg::this_grid();
   DevState* st = a.st;
   const int lane = threadIdx.x & 31;
-  tail_stamp(a, 0);
   if (a.gather == 1) {
     const uint32_t pshift = a.k_bits - a.part_bits, parts = 1u << pshift;
     const uint32_t part = blockIdx.x & (parts - 1u);
@@ -1377,7 +1198,6 @@ __global__ void __launch_bounds__(1024) detect_tail_kernel(const TailArgs a) {
       count_range(a.ids, a.n, a.k_bits, a.part_bits, part, i0, i1, a.counters, hist, st);
     __threadfence();
     grid.sync();
-    tail_stamp(a, 1);
     // the range's parts split it by position for the gather (whole tables in
     // shared memory): each id is read and rewritten by one thread
     const uint64_t len = i1 - i0;
@@ -1395,7 +1215,6 @@ __global__ void __launch_bounds__(1024) detect_tail_kernel(const TailArgs a) {
     }
     __threadfence();
     grid.sync();
-    tail_stamp(a, 2);
   }
   score_rows(a.ids, a.n, a.n, a.tables, a.k_bits, a.gather ? nullptr : a.counters, a.sums, a.scores, st,
              static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x,
@@ -1410,9 +1229,7 @@ __global__ void __launch_bounds__(1024) detect_tail_kernel(const TailArgs a) {
   }
   __threadfence();
   grid.sync();
-  tail_stamp(a, 3);
   flags_rows(a.sums, a.n, a.flag_bits, st, 0, blockIdx.x, gridDim.x);
-  tail_stamp(a, 4);
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(&st->ticket_b, 1u) == gridDim.x - 1u;
@@ -1444,7 +1261,7 @@ __global__ void stream_score_kernel(const uint32_t* __restrict__ ids, uint64_t n
     const double mu = sketch_mean(st, tables);
     s_cut = mu - alpha;
     s_live = st->n > 0;
-    s_band = 0x1.0p-30 * fmax(1.0, fabs(mu));
+    s_band = kStreamBand * fmax(1.0, fabs(mu));
     if (blockIdx.x == 0) {
       st->cut = s_cut;
       st->mean_before = mu;
@@ -1485,166 +1302,241 @@ __global__ void stream_score_kernel(const uint32_t* __restrict__ ids, uint64_t n
 }
 
 
-// One streaming batch in one cooperative launch (detect_stream, detect.cpp:
-// 76-84, then the insert, ace_cli.cpp:177-183): every row scored against the
-// counts at batch start and flagged (score <= mu - alpha, warps dealt
-// round-robin over the blocks); grid barrier; then each block owns whole
-// tables (32-bit sketch, K <= 15): it counts the batch's ids of its table in
-// a shared histogram and adds each touched bin with a plain read-modify-write
-// (no other block writes the table), accumulating T += (c + m)^2 - c^2 =
-// 2 c m + m^2 exactly, so no sum-of-squares pass follows.
-struct StreamArgs {
-  const uint32_t* ids;  // table-major, ids[t * stride + i]
+// One streaming batch, in the reference's streaming order (detect.cpp:76-84
+// on the counts at batch start, then the insert, ace_cli.cpp:177-183 with the
+// insert deferred to the batch end), without a grid barrier.  One launch does
+// phase A of batch b and phase B of the batch before it:
+//   phase A (blocks [0, L * parts)): block (t, p) owns bins [p, p+1) * 2^pb
+//     of table t.  It stages them in shared memory, reads all n ids of table
+//     t, and for the ids in its bins writes the count at batch start into
+//     cnt_out[t][i] and counts the id into a shared histogram; then it adds the
+//     histogram to its bins (plain stores: no other block writes them) and
+//     computes T += (c + m)^2 - c^2 = 2 c m + m^2 exactly.  Block 0 first
+//     records the cut mean - alpha of batch b from the state before the
+//     batch; the last phase-A block commits T and n.
+//   phase B (the other blocks): batch b-1's scores S_i = sum_t cnt[t][i]
+//     (coalesced rows), flags score <= cut (the cut recorded when its phase A
+//     ran), optional scores, reported / ambiguous counts.
+// The counts of a batch are final when its launch ends, so phase B of batch
+// b-1 overlaps phase A of batch b; a one-batch call runs A, then B alone.
+struct StreamApplyArgs {
+  const uint32_t* ids;  // batch b, table-major, ids[t * stride + i]; n = 0: no phase A
   uint64_t n, stride;
-  uint32_t tables, k_bits;
+  uint32_t tables, k_bits, part_bits;
   uint32_t* counters;
+  uint32_t* cnt_out;             // [tables][n]
+  unsigned long long* dT_slots;  // one per phase-A block
+  uint32_t slot_a;               // cut slot of batch b
+  const uint32_t* cnt_in;        // batch b-1: [tables][n_prev]; n_prev = 0: no phase B
+  uint64_t n_prev;
+  uint32_t* flag_bits;           // batch b-1's flag words
+  double* scores;                // batch b-1's scores or null
+  uint32_t slot_b;               // cut slot of batch b-1
   double alpha;
-  uint32_t* flag_bits;
-  double* scores;
   DevState* st;
-  uint32_t* scratch;         // L x 2^K u32 (second halves' histograms), or null
-  unsigned long long* prof;  // instrumentation (ACE_TAIL_PROF=1): [5] start [6] scores done [7] max end
 };
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long g;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
-  return g;
-}
-
-__global__ void __launch_bounds__(1024) stream_step_kernel(const StreamArgs a) {
-  extern __shared__ uint32_t hist[];
-  __shared__ double s_cut, s_band;
-  __shared__ int s_live;
-  __shared__ unsigned long long s_dT;
+__global__ void __launch_bounds__(1024) stream_apply_kernel(const StreamApplyArgs a) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  __shared__ unsigned long long red[32];
+  __shared__ unsigned long long red2[32];
   DevState* st = a.st;
-  const uint32_t lane = threadIdx.x & 31;
-  if (a.prof && blockIdx.x == 0 && threadIdx.x == 0) a.prof[5] = gtimer();
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t parts = 1u << (a.k_bits - a.part_bits);
+  const uint32_t nA = a.n ? a.tables * parts : 0u;
+  if (blockIdx.x < nA) {
+    // ---------------- phase A: counts at batch start, then the insert ----------------
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      const unsigned long long n0 = st->n;
+      const double mu = n0 ? ace_div_rn(st->T, n0 * a.tables) : 0.0;
+      st->cut_ring[a.slot_a] = mu - a.alpha;
+      st->mean_ring[a.slot_a] = mu;
+      st->live_ring[a.slot_a] = n0 > 0 ? 1 : 0;
+    }
+    const uint32_t t = blockIdx.x / parts, p = blockIdx.x % parts;
+    const uint32_t nbp = 1u << a.part_bits, base = p << a.part_bits;
+    uint32_t* cs = sm;        // counts at batch start (read-only during the batch)
+    uint32_t* ms = sm + nbp;  // this batch's histogram
+    uint32_t* ct = a.counters + (static_cast<uint64_t>(t) << a.k_bits) + base;
+    {  // 16-byte staging (nbp is a multiple of 4, the bins 16-byte aligned)
+      const uint4* c4 = reinterpret_cast<const uint4*>(ct);
+      for (uint32_t b = threadIdx.x; b < nbp / 4; b += blockDim.x) {
+        reinterpret_cast<uint4*>(cs)[b] = c4[b];
+        reinterpret_cast<uint4*>(ms)[b] = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+    __syncthreads();
+    const uint32_t* idt = a.ids + static_cast<uint64_t>(t) * a.stride;
+    uint32_t* co = a.cnt_out + static_cast<uint64_t>(t) * a.n;
+    auto take = [&](uint64_t i, uint32_t id) {
+      const uint32_t rel = id - base;
+      if (rel < nbp) {
+#ifndef ACE_EXP_NOGATHER
+        co[i] = cs[rel];
+#endif
+#ifndef ACE_EXP_NOATOM
+        atomicAdd(&ms[rel], 1u);
+#endif
+      }
+    };
+    if (a.stride % 4 == 0 && a.n % 4 == 0 && (reinterpret_cast<uintptr_t>(a.ids) & 15) == 0) {
+      // 16-byte id loads, kDepth per thread in flight (the ids are L2-resident:
+      // memory-level parallelism, not bandwidth, bounds this loop)
+      constexpr int kDepth = 8;
+      const uint4* id4 = reinterpret_cast<const uint4*>(idt);
+      const uint64_t n4 = a.n / 4;
+      for (uint64_t g0 = 0; g0 < n4; g0 += kDepth * blockDim.x) {
+        uint4 q[kDepth];
+#pragma unroll
+        for (int u = 0; u < kDepth; ++u) q[u] = __ldg(id4 + min(g0 + u * blockDim.x + threadIdx.x, n4 - 1));
+#pragma unroll
+        for (int u = 0; u < kDepth; ++u) {
+          const uint64_t j = g0 + u * blockDim.x + threadIdx.x;
+          if (j < n4) {
+            take(4 * j, q[u].x);
+            take(4 * j + 1, q[u].y);
+            take(4 * j + 2, q[u].z);
+            take(4 * j + 3, q[u].w);
+          }
+        }
+      }
+    } else {
+      constexpr int kDepth = 16;
+      for (uint64_t i0 = 0; i0 < a.n; i0 += kDepth * blockDim.x) {
+        uint32_t idv[kDepth];
+#pragma unroll
+        for (int u = 0; u < kDepth; ++u) idv[u] = __ldg(idt + min(i0 + u * blockDim.x + threadIdx.x, a.n - 1));
+#pragma unroll
+        for (int u = 0; u < kDepth; ++u) {
+          const uint64_t i = i0 + u * blockDim.x + threadIdx.x;
+          if (i < a.n) take(i, idv[u]);
+        }
+      }
+    }
+    __syncthreads();
+    unsigned long long dT = 0ull;
+    for (uint32_t b = threadIdx.x; b < nbp; b += blockDim.x) {
+      const uint32_t m = ms[b];
+      if (m) {
+        const uint32_t c = cs[b];
+        ct[b] = c + m;
+        dT += 2ull * c * m + static_cast<unsigned long long>(m) * m;
+      }
+    }
+    dT = warp_sum_u64(dT);
+    if (lane == 0) red[wid] = dT;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long sum = 0ull;
+      for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) sum += red[w];
+      a.dT_slots[blockIdx.x] = sum;
+      __threadfence();
+      if (atomicAdd(&st->ticket_s, 1u) == nA - 1u) {
+        // every phase-A block has recorded its increment (and block 0 its cut)
+        __threadfence();
+        unsigned long long tot = 0ull;
+        for (uint32_t k = 0; k < nA; ++k) tot += __ldcg(a.dT_slots + k);
+        st->T += tot;
+        st->n += a.n;
+        st->ticket_s = 0u;
+      }
+    }
+    return;
+  }
+  // ---------------- phase B: scores and flags of the previous batch ----------------
+  if (a.n_prev == 0) return;
+  const uint32_t bb = blockIdx.x - nA, nB = gridDim.x - nA;
+  const double cut = st->cut_ring[a.slot_b], mu = st->mean_ring[a.slot_b];
+  const int live = st->live_ring[a.slot_b];
+  const double band = kStreamBand * fmax(1.0, fabs(mu));
+  const double L = static_cast<double>(a.tables);
+  unsigned long long rep = 0ull, amb = 0ull;
+  auto score_flag = [&](uint64_t i, unsigned long long S) -> bool {
+    const double sc = __ddiv_rn(static_cast<double>(S), L);
+    if (a.scores) a.scores[i] = sc;
+    if (live && fabs(sc - cut) <= band) ++amb;
+    return live && sc <= cut;
+  };
+  if (a.n_prev % 128 == 0) {
+    // four rows per thread (16-byte loads of 16 tables in flight), a warp
+    // covers 128 rows = 4 flag words
+    const uint64_t quads = a.n_prev / 4;
+    const uint4* c4 = reinterpret_cast<const uint4*>(a.cnt_in);
+    const uint64_t q4 = a.n_prev / 4;  // uint4 per table row
+    // warps dealt round-robin over the blocks (a short batch still spreads
+    // over every SM)
+    const uint64_t nwarps = static_cast<uint64_t>(nB) * (blockDim.x >> 5);
+    for (uint64_t qd = (static_cast<uint64_t>(wid) * nB + bb) * 32 + lane; qd < quads; qd += nwarps * 32) {
+      unsigned long long S[4] = {0ull, 0ull, 0ull, 0ull};
+      for (uint32_t t0 = 0; t0 < a.tables; t0 += 16) {
+        uint4 c[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) c[u] = __ldcg(c4 + static_cast<uint64_t>(min(t0 + u, a.tables - 1)) * q4 + qd);
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (t0 + u < a.tables) {
+            S[0] += c[u].x;
+            S[1] += c[u].y;
+            S[2] += c[u].z;
+            S[3] += c[u].w;
+          }
+      }
+      uint32_t nib = 0u;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) nib |= (score_flag(4 * qd + e, S[e]) ? 1u : 0u) << e;
+      // lane l holds rows 4 l .. 4 l + 3 of the warp's 128: word l / 8, bits 4 (l % 8) ..
+      uint32_t word = nib << (4 * (lane & 7));
+      word |= __shfl_xor_sync(0xffffffffu, word, 1);
+      word |= __shfl_xor_sync(0xffffffffu, word, 2);
+      word |= __shfl_xor_sync(0xffffffffu, word, 4);
+      if ((lane & 7) == 0) {
+        a.flag_bits[qd / 8] = word;
+        rep += __popc(word);
+      }
+    }
+  } else {
+    const uint64_t words = (a.n_prev + 31) / 32;
+    for (uint64_t w = static_cast<uint64_t>(wid) * nB + bb; w < words; w += static_cast<uint64_t>(nB) * (blockDim.x >> 5)) {
+      const uint64_t i = w * 32 + lane;
+      bool f = false;
+      if (i < a.n_prev) {
+        unsigned long long S = 0ull;
+        for (uint32_t t0 = 0; t0 < a.tables; t0 += 16) {
+          uint32_t c[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) c[u] = __ldcg(a.cnt_in + static_cast<uint64_t>(min(t0 + u, a.tables - 1)) * a.n_prev + i);
+#pragma unroll
+          for (int u = 0; u < 16; ++u)
+            if (t0 + u < a.tables) S += c[u];
+        }
+        f = score_flag(i, S);
+      }
+      const unsigned word = __ballot_sync(0xffffffffu, f);  // whole words: rows past n_prev are 0
+      if (lane == 0) {
+        a.flag_bits[w] = word;
+        rep += __popc(word);
+      }
+    }
+  }
+  rep = warp_sum_u64(rep);
+  amb = warp_sum_u64(amb);
+  if (lane == 0) {
+    red[wid] = rep;
+    red2[wid] = amb;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    const double mu = sketch_mean(st, a.tables);
-    s_cut = mu - a.alpha;
-    s_live = st->n > 0;
-    s_band = 0x1.0p-30 * fmax(1.0, fabs(mu));
-    s_dT = 0ull;
-    if (blockIdx.x == 0) {
-      st->cut = s_cut;
+    unsigned long long r = 0ull, m = 0ull;
+    for (uint32_t k = 0; k < (blockDim.x >> 5); ++k) {
+      r += red[k];
+      m += red2[k];
+    }
+    if (r) atomicAdd(&st->reported, r);
+    if (m) atomicAdd(&st->ambiguous, m);
+    if (bb == 0) {
+      st->cut = cut;
       st->mean_before = mu;
     }
-  }
-  __syncthreads();
-  {
-    const double cut = s_cut, band = s_band;
-    const int live = s_live;
-    const double L = static_cast<double>(a.tables);
-    unsigned long long rep = 0, amb = 0;
-    // two lanes per row (tables split in halves: half the dependent gather
-    // rounds per lane), 16 rows per warp, half flag words dealt round-robin
-    const uint64_t hwords = (a.n + 15) / 16;
-    const uint64_t wstride = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
-    const uint32_t th = (a.tables + 1) / 2, hl = lane & 1u;
-    for (uint64_t hw = static_cast<uint64_t>(threadIdx.x >> 5) * gridDim.x + blockIdx.x; hw < hwords; hw += wstride) {
-      const uint64_t i = hw * 16 + (lane >> 1);
-      unsigned long long S = 0ull;
-      if (i < a.n)
-        S = gather_sum<8>(a.ids, a.stride, i, hl ? a.tables : th, a.k_bits, a.counters, hl ? th : 0u);
-      S += __shfl_xor_sync(0xffffffffu, S, 1);
-      bool f = false;
-      if (i < a.n && hl == 0u) {
-        const double sc = __ddiv_rn(static_cast<double>(S), L);
-        if (a.scores) a.scores[i] = sc;
-        f = live && sc <= cut;
-        if (live && fabs(sc - cut) <= band) ++amb;
-      }
-      unsigned w = __ballot_sync(0xffffffffu, f) & 0x55555555u;  // even lanes: rows 16 hw + lane / 2
-      w = (w | (w >> 1)) & 0x33333333u;
-      w = (w | (w >> 2)) & 0x0f0f0f0fu;
-      w = (w | (w >> 4)) & 0x00ff00ffu;
-      w = (w | (w >> 8)) & 0x0000ffffu;
-      if (lane == 0) {
-        if (a.flag_bits) reinterpret_cast<uint16_t*>(a.flag_bits)[hw] = static_cast<uint16_t>(w);
-        rep += __popc(w);
-      }
-    }
-    rep = warp_sum_u64(rep);
-    amb = warp_sum_u64(amb);
-    if (lane == 0) {
-      if (rep) atomicAdd(&st->reported, rep);
-      if (amb) atomicAdd(&st->ambiguous, amb);
-    }
-  }
-  __threadfence();
-  cg::this_grid().sync();
-  if (a.prof && blockIdx.x == 0 && threadIdx.x == 0) a.prof[6] = gtimer();
-  // ---- insert.  With 2 L <= grid (and a scratch table per table) two blocks
-  // share a table: the second counts half the rows and publishes its
-  // histogram, and after a second grid barrier the owner merges it; else
-  // block b owns tables b, b + gridDim.x, ... alone.
-  const uint32_t nb = 1u << a.k_bits;
-  const uint32_t parts = (a.scratch && 2u * a.tables <= gridDim.x) ? 2u : 1u;
-  unsigned long long dT = 0ull;
-  constexpr int kDepth = 8;
-  auto count_rows = [&](const uint32_t* src, uint64_t r0, uint64_t r1) {
-    for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
-    __syncthreads();
-    for (uint64_t i0 = r0; i0 < r1; i0 += kDepth * blockDim.x) {
-      uint32_t idv[kDepth];
-#pragma unroll
-      for (int u = 0; u < kDepth; ++u) {
-        const uint64_t i = i0 + u * blockDim.x + threadIdx.x;
-        idv[u] = i < r1 ? __ldg(src + i) : 0xffffffffu;
-      }
-#pragma unroll
-      for (int u = 0; u < kDepth; ++u)
-        if (idv[u] != 0xffffffffu) atomicAdd(&hist[idv[u]], 1u);
-    }
-    __syncthreads();
-  };
-  auto merge = [&](uint32_t t, const uint32_t* other) {
-    uint32_t* ct = a.counters + (static_cast<uint64_t>(t) << a.k_bits);
-    for (uint32_t b0 = threadIdx.x; b0 < nb; b0 += kDepth * blockDim.x) {
-      uint32_t m[kDepth], o[kDepth];
-#pragma unroll
-      for (int u = 0; u < kDepth; ++u) {
-        const uint32_t b = b0 + u * blockDim.x;
-        m[u] = b < nb ? hist[b] + (other ? __ldcg(other + b) : 0u) : 0u;
-      }
-#pragma unroll
-      for (int u = 0; u < kDepth; ++u) o[u] = m[u] ? ct[b0 + u * blockDim.x] : 0u;
-#pragma unroll
-      for (int u = 0; u < kDepth; ++u)
-        if (m[u]) {
-          ct[b0 + u * blockDim.x] = o[u] + m[u];
-          dT += 2ull * o[u] * m[u] + static_cast<unsigned long long>(m[u]) * m[u];
-        }
-    }
-    __syncthreads();
-  };
-  if (parts == 2) {
-    const uint32_t t = blockIdx.x >> 1, p = blockIdx.x & 1u;
-    const bool live = t < a.tables;
-    if (live) {
-      count_rows(a.ids + static_cast<uint64_t>(t) * a.stride, p ? a.n / 2 : 0, p ? a.n : a.n / 2);
-      if (p == 1u) {
-        uint32_t* sc = a.scratch + (static_cast<uint64_t>(t) << a.k_bits);
-        for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) sc[b] = hist[b];
-      }
-    }
-    __threadfence();
-    cg::this_grid().sync();
-    if (live && p == 0u) merge(t, a.scratch + (static_cast<uint64_t>(t) << a.k_bits));
-  } else {
-    for (uint32_t t = blockIdx.x; t < a.tables; t += gridDim.x) {
-      count_rows(a.ids + static_cast<uint64_t>(t) * a.stride, 0, a.n);
-      merge(t, nullptr);
-    }
-  }
-  dT = warp_sum_u64(dT);
-  if (lane == 0 && dT) atomicAdd(&s_dT, dT);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (s_dT) atomicAdd(&st->T, s_dT);
-    if (blockIdx.x == 0) atomicAdd(&st->n, a.n);
-    if (a.prof) atomicMax(&a.prof[7], gtimer());
   }
 }
 
@@ -1654,6 +1546,33 @@ int grid_for(uint64_t work, int threads, int max_blocks = 148 * 16) {
   if (b < 1) b = 1;
   if (b > static_cast<uint64_t>(max_blocks)) b = max_blocks;
   return static_cast<int>(b);
+}
+
+// SM count of the current device, cached per device ordinal (a process may
+// drive several GPUs).
+int dev_sms() {
+  static int sms[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) {
+    int v = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }
+  if (!sms[dev]) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+  return sms[dev];
+}
+
+// The dynamic shared-memory opt-in of kernel `id`, once per device ordinal.
+cudaError_t set_smem_once(const void* fn, int bytes, int id) {
+  static std::atomic<unsigned long long> done[8];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const bool track = dev >= 0 && dev < 64;
+  if (track && ((done[id].load() >> dev) & 1ull)) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && track) done[id].fetch_or(1ull << dev);
+  return e;
 }
 
 }  // namespace
@@ -1667,13 +1586,8 @@ cudaError_t launch_wnorm64(const double* w64, uint64_t dim, uint32_t rows, doubl
 }
 
 cudaError_t launch_hash_simt(const HashArgs& a, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(hash_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(sizeof(HashSmem)));
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  cudaError_t e = set_smem_once(reinterpret_cast<const void*>(hash_simt_kernel), static_cast<int>(sizeof(HashSmem)), 0);
+  if (e != cudaSuccess) return e;
   if (a.n == 0) return cudaSuccess;
   const dim3 grid(static_cast<unsigned>((a.n + BM - 1) / BM), a.fam.ntiles);
   hash_simt_kernel<<<grid, NT, sizeof(HashSmem), s>>>(a);
@@ -1687,22 +1601,13 @@ cudaError_t launch_apply_ids(const uint32_t* ids, uint64_t n, uint32_t tables, u
   if (n == 0) return cudaSuccess;
   if (ids_stride == 0) ids_stride = n;
   if (sign > 0 && k_bits <= 20 && n >= 4096) {
-    static bool configured = false;
-    if (!configured) {
-      cudaError_t e = cudaFuncSetAttribute(apply_ids_smem_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(sizeof(uint32_t) << 15));
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(apply_ids_smem_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(sizeof(uint32_t) << 15));
-      if (e != cudaSuccess) return e;
-      configured = true;
-    }
-    static int sms = 0;
-    if (!sms) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    cudaError_t e = set_smem_once(reinterpret_cast<const void*>(apply_ids_smem_kernel<true>),
+                                  static_cast<int>(sizeof(uint32_t) << 15), 2);
+    if (e == cudaSuccess)
+      e = set_smem_once(reinterpret_cast<const void*>(apply_ids_smem_kernel<false>),
+                        static_cast<int>(sizeof(uint32_t) << 15), 3);
+    if (e != cudaSuccess) return e;
+    const int sms = dev_sms();
     const uint32_t part_bits = k_bits < 15 ? k_bits : 15;
     const uint32_t parts = 1u << (k_bits - part_bits);
     const uint64_t total = n * tables;
@@ -1734,24 +1639,16 @@ cudaError_t launch_apply_ids(const uint32_t* ids, uint64_t n, uint32_t tables, u
   return cudaGetLastError();
 }
 
-unsigned long long* g_tail_prof = nullptr;
 
 cudaError_t launch_detect_tail(uint32_t* ids, uint64_t n, uint32_t tables, uint32_t k_bits, uint32_t* counters,
                                int gather, uint64_t* sums, double* scores, uint32_t* flag_bits, DevState* st,
                                cudaStream_t s) {
   if (n == 0 || (gather && k_bits > 16)) return cudaErrorInvalidValue;  // gather: 1 = counts + gather here
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  static bool configured = false;
-  if (!configured) {
-    const cudaError_t e = cudaFuncSetAttribute(detect_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(sizeof(uint32_t) << 15));
+  const int sms = dev_sms();
+  {
+    const cudaError_t e = set_smem_once(reinterpret_cast<const void*>(detect_tail_kernel),
+                                        static_cast<int>(sizeof(uint32_t) << 15), 4);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   TailArgs a{};
   a.ids = ids;
@@ -1764,48 +1661,12 @@ cudaError_t launch_detect_tail(uint32_t* ids, uint64_t n, uint32_t tables, uint3
   a.scores = scores;
   a.flag_bits = flag_bits;
   a.st = st;
-  static int prof_env = -1;
-  if (prof_env < 0) prof_env = getenv("ACE_TAIL_PROF") ? 1 : 0;
-  if (prof_env) {
-    if (!g_tail_prof) cudaMalloc(&g_tail_prof, 8 * sizeof(unsigned long long));
-    cudaMemsetAsync(g_tail_prof, 0, 8 * sizeof(unsigned long long), s);
-    a.prof = g_tail_prof;
-  }
   unsigned grid = static_cast<unsigned>(sms);
   size_t smem = 1024 * sizeof(double);
-  // ACE_PAIR_GATHER=1, K <= 15: count and gather by table-owning CTA pairs (no
-  // grid barriers), then the tail scores from the counts.  Measured slower on
-  // cfg 2 (tail 0.130 vs 0.109 ms): 100 SMs count instead of 148, and the
-  // shared atomics bound the count.
-  static int pair_env = -1;
-  if (pair_env < 0) {
-    const char* e = getenv("ACE_PAIR_GATHER");
-    pair_env = e ? atoi(e) : 0;
-  }
-  if (gather == 1 && k_bits <= 15 && pair_env) {
-    static bool pcfg = false;
-    if (!pcfg) {
-      const cudaError_t e = cudaFuncSetAttribute(count_gather_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(sizeof(uint32_t) << 15));
-      if (e != cudaSuccess) return e;
-      pcfg = true;
-    }
-    cudaError_t e = cudaMemsetAsync(&st->T, 0, sizeof(unsigned long long), s);
-    if (e != cudaSuccess) return e;
-    count_gather_pair_kernel<<<2 * tables, 1024, sizeof(uint32_t) << k_bits, s>>>(ids, n, k_bits, counters, st);
-    count_launch();
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    gather = 2;
-    a.gather = 2;
-  }
   if (gather == 1) {
-    // K = 16: one part of packed u16 bins (count_range16); 2 parts of u32 bins with ACE_HIST16=0
-    static int h16_env = -1;
-    if (h16_env < 0) {
-      const char* e = getenv("ACE_HIST16");
-      h16_env = e ? atoi(e) : 1;
-    }
-    a.part_bits = k_bits < 15 ? k_bits : (k_bits == 16 && h16_env ? 16u : 15u);
+    // K = 16: one part of packed u16 bins (count_range16: each id read once;
+    // two parts of u32 bins measured 2.07 vs 0.85 ms for the cfg 3 count)
+    a.part_bits = k_bits < 15 ? k_bits : (k_bits == 16 ? 16u : 15u);
     const uint32_t parts = 1u << (k_bits - a.part_bits);
     const uint64_t total = n * tables;
     uint64_t ranges = static_cast<uint64_t>(sms) / parts;
@@ -1875,48 +1736,55 @@ cudaError_t launch_stream_score(const uint32_t* ids, uint64_t n, uint32_t tables
   return cudaGetLastError();
 }
 
-cudaError_t launch_stream_step(const uint32_t* ids, uint64_t n, uint64_t ids_stride, uint32_t tables, uint32_t k_bits,
-                               uint32_t* counters, double alpha, uint32_t* flag_bits, double* scores, DevState* st,
-                               cudaStream_t s, uint32_t* scratch) {
-  if (n == 0) return cudaSuccess;
-  if (k_bits > 15) return cudaErrorInvalidValue;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  static bool configured = false;
-  if (!configured) {
-    const cudaError_t e = cudaFuncSetAttribute(stream_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(sizeof(uint32_t) << 15));
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  StreamArgs a{};
+uint32_t stream_part_bits(uint32_t tables, uint32_t k_bits) {
+  // bins per phase-A block: two u32 arrays of 2^pb in shared memory (<= 128
+  // KB); split tables further while fewer than ~96 blocks would insert
+  uint32_t pb = k_bits < 14 ? k_bits : 14u;
+  while (pb > 8 && (static_cast<uint64_t>(tables) << (k_bits - pb)) < 96) --pb;
+#ifdef ACE_EXP_PB
+  pb = ACE_EXP_PB;
+#endif
+  return pb;
+}
+
+uint32_t stream_phase_a_blocks(uint32_t tables, uint32_t k_bits) {
+  return tables << (k_bits - stream_part_bits(tables, k_bits));
+}
+
+cudaError_t launch_stream_apply(const uint32_t* ids, uint64_t n, uint64_t ids_stride, uint32_t tables, uint32_t k_bits,
+                                uint32_t* counters, uint32_t* cnt_out, unsigned long long* dT_slots, uint32_t slot_a,
+                                const uint32_t* cnt_in, uint64_t n_prev, uint32_t* flag_bits, double* scores,
+                                uint32_t slot_b, double alpha, DevState* st, cudaStream_t s) {
+  if (n == 0 && n_prev == 0) return cudaSuccess;
+  if (k_bits > 16) return cudaErrorInvalidValue;
+  StreamApplyArgs a{};
   a.ids = ids;
   a.n = n;
   a.stride = ids_stride ? ids_stride : n;
   a.tables = tables;
   a.k_bits = k_bits;
+  a.part_bits = stream_part_bits(tables, k_bits);
   a.counters = counters;
-  a.alpha = alpha;
+  a.cnt_out = cnt_out;
+  a.dT_slots = dT_slots;
+  a.slot_a = slot_a;
+  a.cnt_in = cnt_in;
+  a.n_prev = n_prev;
   a.flag_bits = flag_bits;
   a.scores = scores;
+  a.slot_b = slot_b;
+  a.alpha = alpha;
   a.st = st;
-  a.scratch = scratch;
-  static int prof_env = -1;
-  if (prof_env < 0) prof_env = getenv("ACE_TAIL_PROF") ? 1 : 0;
-  if (prof_env) {
-    if (!g_tail_prof) cudaMalloc(&g_tail_prof, 8 * sizeof(unsigned long long));
-    cudaMemsetAsync(g_tail_prof, 0, 8 * sizeof(unsigned long long), s);
-    a.prof = g_tail_prof;
-  }
-  void* args[] = {&a};
-  const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(stream_step_kernel), dim3(sms),
-                                                    dim3(1024), args, sizeof(uint32_t) << k_bits, s);
+  const int sms = dev_sms();
+  const uint32_t nA = n ? stream_phase_a_blocks(tables, k_bits) : 0u;
+  uint32_t nB = 0;
+  if (n_prev) nB = nA == 0 ? static_cast<uint32_t>(sms) : std::max<uint32_t>(nA < static_cast<uint32_t>(sms) ? sms - nA : 0u, 32u);
+  const size_t smem = n ? (sizeof(uint32_t) << (a.part_bits + 1)) : 0;
+  cudaError_t e = set_smem_once(reinterpret_cast<const void*>(stream_apply_kernel), 128 * 1024, 1);
+  if (e != cudaSuccess) return e;
+  stream_apply_kernel<<<nA + nB, 1024, smem, s>>>(a);
   count_launch();
-  return e;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_sum_squares(const uint32_t* counters, uint64_t num, unsigned long long* out,

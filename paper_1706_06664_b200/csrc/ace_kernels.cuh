@@ -43,7 +43,6 @@ cudaError_t launch_apply_ids(const uint32_t* ids, uint64_t n, uint32_t tables,
 cudaError_t launch_detect_tail(uint32_t* ids, uint64_t n, uint32_t tables, uint32_t k_bits, uint32_t* counters,
                                int gather, uint64_t* sums, double* scores, uint32_t* flag_bits, DevState* st,
                                cudaStream_t s);
-extern unsigned long long* g_tail_prof;  // ACE_TAIL_PROF=1: phase timestamps of the last tail launch
 // Noisy hashing (srp.cpp:93-104), exact: tables [t0, t0+nt), bits [b0, b0+nb)
 // of each; noise[(i*nt + tt)*nb + (b-b0)] pre-scaled terms in tick order.
 cudaError_t launch_noisy_buckets(const void* x, int x_f64, uint64_t n, uint64_t ld, uint64_t dim, const double* w64,
@@ -71,13 +70,17 @@ cudaError_t launch_stream_score(const uint32_t* ids, uint64_t n, uint32_t tables
                                 double alpha, uint32_t* flag_bits, double* scores,
                                 DevState* st, cudaStream_t s, uint64_t ids_stride = 0);  // 0: n
 
-// One streaming batch (32-bit, unsaturable, K <= 15) in one cooperative
-// launch: score + flag against the counts at batch start, then insert with T
-// updated exactly (no sum-of-squares pass).
-// scratch: L x 2^K u32 lets two blocks share each table's insert (or null).
-cudaError_t launch_stream_step(const uint32_t* ids, uint64_t n, uint64_t ids_stride, uint32_t tables, uint32_t k_bits,
-                               uint32_t* counters, double alpha, uint32_t* flag_bits, double* scores, DevState* st,
-                               cudaStream_t s, uint32_t* scratch = nullptr);
+// Streaming (32-bit, unsaturable, K <= 16), no grid barrier: one launch runs
+// phase A of batch b (counts at batch start into cnt_out [L][n], insert, T
+// exact; the cut of batch b recorded in slot_a) and phase B of the batch
+// before it (scores from cnt_in [L][n_prev], flags against slot_b's cut).
+// n = 0: phase B only; n_prev = 0: phase A only.  dT_slots: one u64 per
+// phase-A block (stream_phase_a_blocks).
+uint32_t stream_phase_a_blocks(uint32_t tables, uint32_t k_bits);
+cudaError_t launch_stream_apply(const uint32_t* ids, uint64_t n, uint64_t ids_stride, uint32_t tables, uint32_t k_bits,
+                                uint32_t* counters, uint32_t* cnt_out, unsigned long long* dT_slots, uint32_t slot_a,
+                                const uint32_t* cnt_in, uint64_t n_prev, uint32_t* flag_bits, double* scores,
+                                uint32_t slot_b, double alpha, DevState* st, cudaStream_t s);
 
 // Sum of squares of all counters (T after restore with exact state).
 cudaError_t launch_sum_squares(const uint32_t* counters, uint64_t num,

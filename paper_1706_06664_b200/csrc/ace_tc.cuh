@@ -47,12 +47,9 @@ struct TcArgs {
   const float* w32;               // K-streamed recheck: W rounded to fp32 [rows][dim]
   uint32_t* overflow_rows;        // bitmap over rows; rows rechecked in full
   DevState* st;
-  uint16_t tab_end[64];           // tables completed by the end of direction tile j
 };
 
 cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc);
-// per-tile table ranges (TcArgs::tab_end) from k_bits, tables, ntiles
-void tc_fill_tables(TcArgs* a);
 void tc_free_family(TcFamily* tc);
 bool tc_supported(uint64_t dim);
 // d <= 256: the projection kernel reads raw fp32 rows through a tensor map

@@ -50,7 +50,7 @@ from paper_1706_06664_b200 import workloads as W  # noqa: E402
 
 OUT = ROOT / "tests" / "golden" / "golden_full.json"
 CHUNK = 1 << 20          # rows per ids digest chunk (batch configs)
-STREAM_CHUNK_BATCHES = 16  # batches per ids digest chunk (stream)
+STREAM_CHUNK_BATCHES = 16  # batches per device generation chunk of the GPU test (ids digested per batch)
 NEAR_EPS = 1e-6          # BASELINE.json near-tie measure |<x,w>| < 1e-6 |x||w|
 
 

@@ -97,9 +97,10 @@ def test_full_stream_config5_matches_oracle(cuda):
     for c0 in range(0, w.n, chunk):
         m = min(chunk, w.n - c0)
         W.device_rows(5, c0, m, xd.data_ptr())
-        st = N.AceHashStats()
-        h_ids.update(fam.buckets(xd[:m], stats=st).tobytes())
-        near += st.near_ties
+        for b0 in range(0, m, w.batch):  # ids digested batch by batch, as the fixture
+            st = N.AceHashStats()
+            h_ids.update(fam.buckets(xd[b0:min(m, b0 + w.batch)], stats=st).tobytes())
+            near += st.near_ties
         for b0 in range(0, m, w.batch):
             fl, sc, rep = sk.stream_batch(xd[b0:min(m, b0 + w.batch)], w.alpha, scores=True)
             fsha, frep, mean_after = g["per_batch"][b]
@@ -123,3 +124,35 @@ def test_full_stream_config5_matches_oracle(cuda):
     # stream's ambiguity band
     assert g["exact_vs_reference_mean"]["rows_flagged_differently_under_exact_cut"] == 0
     assert ambiguous == 0
+
+
+def test_full_stream_run_config5_matches_oracle(cuda):
+    """The streaming driver (ace_sketch_stream_run: 2-batch hashing groups,
+    phase B of each batch in the next batch's launch) over all 100M rows at
+    once: per-batch flag digests, counters and n as the oracle's."""
+    torch = cuda
+    g = GOLD["5"]
+    w = W.CONFIGS[5]
+    sk = ace.AceSketch(family(5), ace.CounterWidth.k32)
+    xd = torch.empty((w.n, w.dim), dtype=torch.float32, device="cuda")
+    chunk = 8 * 1024 * 1024
+    for r0 in range(0, w.n, chunk):
+        m = min(chunk, w.n - r0)
+        W.device_rows(5, r0, m, xd[r0:r0 + m].data_ptr())
+    flags = torch.zeros((w.n + 31) // 32, dtype=torch.int32, device="cuda")
+    _, lat, rep = sk.stream_run(xd, w.batch, w.alpha, flags_out=flags)
+    del xd
+    torch.cuda.empty_cache()
+    bits = flags.cpu().numpy().view(np.uint32)
+    words = w.batch // 32
+    for b in range(g["batches"]):
+        wb = bits[b * words:(b + 1) * words]
+        rows = min(w.batch, w.n - b * w.batch)
+        fl = ((wb[:, None] >> np.arange(32, dtype=np.uint32)) & 1).astype(bool).reshape(-1)[:rows]
+        assert sha(np.packbits(fl, bitorder="little"))[:16] == g["per_batch"][b][0], f"batch {b}"
+    assert rep.reported == g["reported"]
+    assert rep.ambiguous == 0
+    assert sha(sk.counters_u32()) == g["counters_sha256"]
+    assert sk.size() == g["size"]
+    assert sk.mean() == float.fromhex(g["mean_exact"])
+    assert len(lat) == g["batches"] and float(np.max(lat)) > 0.0

@@ -284,93 +284,46 @@ def test_repeated_calls_replay_graph(cuda, golden, cfg):
 
 
 def test_fused_gather_path_all_shapes(cuda, golden):
-    """The fused count-and-gather pass (forced on with ACE_FUSED_GATHER=2, in
-    a subprocess: the switch is read once) on configs 1, 2 and the K = 16
-    prefix of 3 (two histogram parts): reference counters and flags."""
-    import json
-    import os
-    import subprocess
-    import sys
-    from pathlib import Path
-    root = Path(__file__).resolve().parents[1]
-    code = r'''
-import hashlib, json, sys
-import numpy as np, torch
-sys.path.insert(0, %r)
-from paper_1706_06664_b200 import ace
-from paper_1706_06664_b200 import workloads as W
-g = json.loads(open(%r).read())
-out = {}
-for cfg in (1, 2, 3):
-    e = g["configs"][str(cfg)]
-    w = W.CONFIGS[cfg]
-    x, _ = W.host_rows(cfg, 0, e["n"])
-    fam = ace.SrpFamily(ace.SrpConfig(dim=w.dim, k_bits=w.k_bits, num_tables=w.num_tables, seed=w.w_seed))
-    sk = ace.AceSketch(fam, ace.CounterWidth.k32)
-    rep = sk.build_detect(torch.from_numpy(x).cuda())
-    out[cfg] = [hashlib.sha256(sk.counters_u32().tobytes()).hexdigest(),
-                hashlib.sha256(np.packbits(rep.flags, bitorder="little").tobytes()).hexdigest(), int(rep.reported)]
-print(json.dumps(out))
-''' % (str(root), str(root / "tests" / "golden" / "golden.json"))
-    env = dict(os.environ, ACE_FUSED_GATHER="2")
-    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-    assert res.returncode == 0, res.stderr[-2000:]
-    got = json.loads(res.stdout.strip().splitlines()[-1])
-    for cfg in ("1", "2", "3"):
-        e = golden["configs"][cfg]
-        assert got[cfg][0] == e["counters_sha256"], cfg
-        assert got[cfg][1] == e["flags_sha256"], cfg
-        assert got[cfg][2] == e["reported"], cfg
+    """The fused count-and-gather pass forced on (ACE_OPT_DEFER_INSERT = 1)
+    for configs 1, 2 and the K = 16 prefix of 3 (packed u16 bins), and forced
+    off (-1): reference counters and flags either way."""
+    torch = cuda
+    for cfg in (1, 2, 3):
+        e = golden["configs"][str(cfg)]
+        w = W.CONFIGS[cfg]
+        x, _ = W.host_rows(cfg, 0, e["n"])
+        fam = ace.SrpFamily(ace.SrpConfig(dim=w.dim, k_bits=w.k_bits, num_tables=w.num_tables, seed=w.w_seed))
+        for mode in (1, -1):
+            sk = ace.AceSketch(fam, ace.CounterWidth.k32)
+            sk.set_option(N.ACE_OPT_DEFER_INSERT, mode)
+            rep = sk.build_detect(torch.from_numpy(x).cuda())
+            assert sha(sk.counters_u32()) == e["counters_sha256"], (cfg, mode)
+            assert sha(np.packbits(rep.flags, bitorder="little")) == e["flags_sha256"], (cfg, mode)
+            assert rep.reported == e["reported"], (cfg, mode)
 
 
-@pytest.mark.parametrize("chunks", [3, 16])
+@pytest.mark.parametrize("chunks", [1, 3, 16])
 def test_chunked_h2d_pipeline(cuda, golden, chunks):
     """Pinned host rows of a large batch are copied in chunks on a copy
-    stream and hashed as each chunk lands (ACE_H2D_CHUNKS, read once: a
-    subprocess).  Uneven chunk counts on configs 1 and 2: reference counters,
-    flags and report."""
-    import json
-    import os
-    import subprocess
-    import sys
-    from pathlib import Path
-    root = Path(__file__).resolve().parents[1]
-    code = r'''
-import hashlib, json, sys
-import numpy as np, torch
-sys.path.insert(0, %r)
-from paper_1706_06664_b200 import ace
-from paper_1706_06664_b200 import workloads as W
-g = json.loads(open(%r).read())
-out = {}
-for cfg in (1, 2):
-    e = g["configs"][str(cfg)]
-    w = W.CONFIGS[cfg]
-    x, _ = W.host_rows(cfg, 0, e["n"])
-    xp = torch.from_numpy(x).pin_memory()
-    fam = ace.SrpFamily(ace.SrpConfig(dim=w.dim, k_bits=w.k_bits, num_tables=w.num_tables, seed=w.w_seed))
-    res = []
-    for width in (ace.CounterWidth.k32, ace.CounterWidth.k16):
-        sk = ace.AceSketch(fam, width)
-        for _ in range(2):
-            sk.reset()
-            rep = sk.build_detect(xp.numpy())
-        res.append([hashlib.sha256(sk.counters_u32().tobytes()).hexdigest(),
-                    hashlib.sha256(np.packbits(rep.flags, bitorder="little").tobytes()).hexdigest(),
-                    int(rep.reported)])
-    out[cfg] = res
-print(json.dumps(out))
-''' % (str(root), str(root / "tests" / "golden" / "golden.json"))
-    env = dict(os.environ, ACE_H2D_CHUNKS=str(chunks))
-    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-    assert res.returncode == 0, res.stderr[-2000:]
-    got = json.loads(res.stdout.strip().splitlines()[-1])
-    for cfg in ("1", "2"):
-        e = golden["configs"][cfg]
-        for width_res in got[cfg]:
-            assert width_res[0] == e["counters_sha256"], cfg
-            assert width_res[1] == e["flags_sha256"], cfg
-            assert width_res[2] == e["reported"], cfg
+    stream and hashed as each chunk lands (ACE_OPT_H2D_CHUNKS).  Uneven chunk
+    counts on configs 1 and 2, both counter widths, repeated calls (graph
+    replay): reference counters, flags and report."""
+    torch = cuda
+    for cfg in (1, 2):
+        e = golden["configs"][str(cfg)]
+        w = W.CONFIGS[cfg]
+        x, _ = W.host_rows(cfg, 0, e["n"])
+        xp = torch.from_numpy(x).pin_memory()
+        fam = ace.SrpFamily(ace.SrpConfig(dim=w.dim, k_bits=w.k_bits, num_tables=w.num_tables, seed=w.w_seed))
+        for width in (ace.CounterWidth.k32, ace.CounterWidth.k16):
+            sk = ace.AceSketch(fam, width)
+            sk.set_option(N.ACE_OPT_H2D_CHUNKS, chunks)
+            for _ in range(2):
+                sk.reset()
+                rep = sk.build_detect(xp.numpy())
+            assert sha(sk.counters_u32()) == e["counters_sha256"], (cfg, width)
+            assert sha(np.packbits(rep.flags, bitorder="little")) == e["flags_sha256"], (cfg, width)
+            assert rep.reported == e["reported"], (cfg, width)
 
 
 def test_hist16_hot_bins_wrap(cuda):
