@@ -140,8 +140,11 @@ ace_status ace_sketch_set_stream(AceSketch* sk, void* cuda_stream);
  *   ACE_OPT_DEFER_INSERT  build + detect: fuse the insert into the detect
  *                         tail's count-and-gather pass: 0 = when the batch is
  *                         large enough (default), 1 = whenever the sketch
- *                         allows it (32-bit, K <= 16), -1 = never. */
-enum { ACE_OPT_H2D_CHUNKS = 1, ACE_OPT_DEFER_INSERT = 2 };
+ *                         allows it (32-bit, K <= 16), -1 = never;
+ *   ACE_OPT_STREAM_GROUP  ace_sketch_stream_run: batches hashed by one
+ *                         projection launch (default 4; 1..64; throughput vs
+ *                         per-batch latency). */
+enum { ACE_OPT_H2D_CHUNKS = 1, ACE_OPT_DEFER_INSERT = 2, ACE_OPT_STREAM_GROUP = 3 };
 ace_status ace_sketch_set_option(AceSketch* sk, int option, int64_t value);
 
 /* AceSketch::insert (sketch.cpp:50-72) for n rows, in row order. */

@@ -108,10 +108,12 @@ struct AceSketch {
   DevBuf sstage[2];
   cudaEvent_t s_copied[2] = {nullptr, nullptr}, s_used[2] = {nullptr, nullptr};
   DevBuf ids, sums, stage, flags, scores, demand, near, overflow, x16, rowthr, segc, xf32;
-  DevBuf cnt[2], dts;       // stream: counts at batch start (double-buffered), phase-A increments
-  uint64_t stream_seq = 0;  // stream batches so far (cut slot = seq & 1)
+  DevBuf cnt[2];            // stream: counts at batch start (double-buffered)
   int h2d_chunks = 8;       // pinned host rows of a large batch: copy chunks hashed as they land
   int defer_mode = 0;       // ACE_OPT_DEFER_INSERT
+  // stream driver: batches hashed by one projection launch (hashing does not
+  // depend on the counts), amortising the persistent kernel's fill and drain
+  int stream_group = 4;     // ACE_OPT_STREAM_GROUP
   // build + detect over the same rows: run_hash leaves the insert to the
   // fused count-and-gather pass of the detect tail (detect_tail_kernel)
   bool defer_insert = false, insert_deferred = false;
@@ -151,6 +153,29 @@ struct AceSketch {
     }
   };
   GraphKey gkey, gseen;
+  // stream driver graph (ace_sketch_stream_run with device rows)
+  struct StreamKey {
+    const void* x = nullptr;
+    const void* flags = nullptr;
+    uint64_t n = 0, ld = 0, batch = 0;
+    double alpha = 0.0;
+    int dtype = 0, out_where = 0, group = 0;
+    bool lat = false, ff = false;
+    cudaStream_t stream = nullptr;
+    const void* bufs[6] = {};
+    bool operator==(const StreamKey& o) const {
+      for (int i = 0; i < 6; ++i)
+        if (bufs[i] != o.bufs[i]) return false;
+      return x == o.x && flags == o.flags && n == o.n && ld == o.ld && batch == o.batch && alpha == o.alpha &&
+             dtype == o.dtype && out_where == o.out_where && group == o.group && lat == o.lat && ff == o.ff &&
+             stream == o.stream;
+    }
+  };
+  StreamKey sgkey, sgseen;
+  bool sgseen_valid = false;
+  cudaGraphExec_t sgexec = nullptr;
+  unsigned long long sglaunches = 0;
+  std::vector<cudaEvent_t> lat_a, lat_b;  // per-batch latency events of the stream driver
   bool gseen_valid = false;
   cudaGraphExec_t gexec = nullptr;
   unsigned long long glaunches = 0;
@@ -158,6 +183,9 @@ struct AceSketch {
     if (gexec) cudaGraphExecDestroy(gexec);
     gexec = nullptr;
     gseen_valid = false;
+    if (sgexec) cudaGraphExecDestroy(sgexec);
+    sgexec = nullptr;
+    sgseen_valid = false;
   }
 };
 
@@ -281,16 +309,11 @@ bool fire_and_forget_ok(const AceSketch* sk, uint64_t n) {
 // sketches with K <= 16; others score, insert and cap with separate kernels.
 bool stream_apply_ok(const AceSketch* sk, bool ff) { return ff && sk->width == 32 && sk->fam->d.k_bits <= 16; }
 
-// Batches of the stream driver hashed by one projection launch (hashing does
-// not depend on the counts): amortises the persistent kernel's fill and
-// drain over more point tiles.
-constexpr uint64_t kStreamGroup = 2;
 
 ace_status ensure_stream_bufs(AceSketch* sk, uint64_t rows) {
   const size_t cnt_bytes = static_cast<size_t>(rows) * sk->fam->d.tables * sizeof(uint32_t);
   ACE_CUDA(sk->cnt[0].ensure(cnt_bytes));
   ACE_CUDA(sk->cnt[1].ensure(cnt_bytes));
-  ACE_CUDA(sk->dts.ensure(stream_phase_a_blocks(sk->fam->d.tables, sk->fam->d.k_bits) * sizeof(unsigned long long)));
   return ACE_OK;
 }
 
@@ -748,7 +771,6 @@ ace_status ace_sketch_destroy(AceSketch* sk) {
   sk->xf32.release();
   sk->cnt[0].release();
   sk->cnt[1].release();
-  sk->dts.release();
   if (sk->counters) cudaFree(sk->counters);
   if (sk->st) cudaFree(sk->st);
   if (sk->hst) cudaFreeHost(sk->hst);
@@ -765,8 +787,11 @@ ace_status ace_sketch_destroy(AceSketch* sk) {
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t& e : sk->ev)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : sk->lat_a) cudaEventDestroy(e);
+  for (cudaEvent_t e : sk->lat_b) cudaEventDestroy(e);
   family_release(sk->fam);
   delete sk;
+  cudaGetLastError();  // teardown errors are not the next call's launch error
   return ACE_OK;
 }
 
@@ -787,6 +812,10 @@ ace_status ace_sketch_set_option(AceSketch* sk, int option, int64_t value) {
     case ACE_OPT_DEFER_INSERT:
       if (value < -1 || value > 1) return fail(ACE_E_CONTRACT, "ace_sketch_set_option: defer mode must be -1, 0 or 1");
       sk->defer_mode = static_cast<int>(value);
+      break;
+    case ACE_OPT_STREAM_GROUP:
+      if (value < 1 || value > 64) return fail(ACE_E_CONTRACT, "ace_sketch_set_option: group must be in [1, 64]");
+      sk->stream_group = static_cast<int>(value);
       break;
     default:
       return fail(ACE_E_CONTRACT, "ace_sketch_set_option: unknown option " + std::to_string(option));
@@ -1166,14 +1195,13 @@ ace_status ace_sketch_stream_batch(AceSketch* sk, const void* x, int dtype, uint
   if (stream_apply_ok(sk, fire_and_forget_ok(sk, n))) {
     // phase A (counts at batch start, insert), then phase B (scores, flags)
     if ((r = ensure_stream_bufs(sk, n)) != ACE_OK) return r;
-    const uint32_t slot = static_cast<uint32_t>(sk->stream_seq++ & 1u);
+    const uint32_t slot = 0u;  // a one-batch call: its phase B reads slot 0 right after
     uint32_t* cnt = sk->cnt[slot].as<uint32_t>();
-    ACE_CUDA(launch_stream_apply(sk->ids.as<uint32_t>(), n, n, f->d.tables, f->d.k_bits, sk->counters, cnt,
-                                 sk->dts.as<unsigned long long>(), slot, nullptr, 0, nullptr, nullptr, 0, alpha, sk->st,
-                                 sk->stream));
+    ACE_CUDA(launch_stream_apply(sk->ids.as<uint32_t>(), n, n, f->d.tables, f->d.k_bits, sk->counters, cnt, slot,
+                                 nullptr, 0, nullptr, nullptr, 0, alpha, sk->st, sk->stream));
     sk->mark(2);
-    ACE_CUDA(launch_stream_apply(nullptr, 0, 0, f->d.tables, f->d.k_bits, sk->counters, nullptr, nullptr, 0, cnt, n,
-                                 dflags, dsc, slot, alpha, sk->st, sk->stream));
+    ACE_CUDA(launch_stream_apply(nullptr, 0, 0, f->d.tables, f->d.k_bits, sk->counters, nullptr, 0, cnt, n, dflags, dsc,
+                                 slot, alpha, sk->st, sk->stream));
   } else {
     ACE_CUDA(cudaMemsetAsync(&sk->st->batch_sum, 0, sizeof(unsigned long long), sk->stream));
     ACE_CUDA(launch_stream_score(sk->ids.as<uint32_t>(), n, f->d.tables, f->d.k_bits, sk->counters,
@@ -1218,20 +1246,23 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
   const size_t esz = dtype == ACE_F64 ? 8 : 4;
   const uint64_t nb = (n + batch - 1) / batch;
   const bool ff = fire_and_forget_ok(sk, n);
-  ACE_CUDA(zero_call_fields(sk));
+  const bool fast = stream_apply_ok(sk, ff);
+  const uint64_t G = static_cast<uint64_t>(sk->stream_group);
   ACE_CUDA(sk->flags.ensure(((n + 31) / 32) * sizeof(uint32_t)));
   uint32_t* dflags = (flag_bits && out_where == ACE_DEVICE) ? flag_bits : sk->flags.as<uint32_t>();
+  if (fast && (r = ensure_stream_bufs(sk, std::min(batch, n))) != ACE_OK) return r;
   // per-batch latency: from the start of the batch's work (its group's
   // hashing for a group's first batch) to the end of the launch that writes
-  // its flags
-  std::vector<cudaEvent_t> ev_a, ev_b;
+  // its flags; events kept by the sketch across calls
   if (batch_ms) {
-    ev_a.resize(nb);
-    ev_b.resize(nb);
-    for (auto& e : ev_a) ACE_CUDA(cudaEventCreate(&e));
-    for (auto& e : ev_b) ACE_CUDA(cudaEventCreate(&e));
+    while (sk->lat_a.size() < nb) {
+      cudaEvent_t e0, e1;
+      ACE_CUDA(cudaEventCreate(&e0));
+      ACE_CUDA(cudaEventCreate(&e1));
+      sk->lat_a.push_back(e0);
+      sk->lat_b.push_back(e1);
+    }
   }
-  const bool fast = stream_apply_ok(sk, ff);
   std::vector<cudaEvent_t> tev;  // timing on: (start, end) pairs, hashing then stream kernels
   std::vector<int> tkind;
   auto tmark = [&](int kind, bool end) -> cudaError_t {
@@ -1243,13 +1274,6 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
     if (!end) tkind.push_back(kind);
     return cudaEventRecord(e, sk->stream);
   };
-  if (fast && (r = ensure_stream_bufs(sk, std::min(batch, n))) != ACE_OK) return r;
-  // the batch whose phase B is still due (fast path)
-  const uint32_t* p_cnt = nullptr;
-  uint64_t p_rows = 0, p_b = 0;
-  uint32_t* p_flags = nullptr;
-  uint32_t p_slot = 0;
-  const uint64_t G = kStreamGroup;
   // pinned host rows: H2D copies of the next group overlap this group's work
   const bool overlap = x_where == ACE_HOST && host_pinned(x) && nb > G;
   if (overlap) {
@@ -1261,88 +1285,150 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
       if (!sk->s_copied[i]) ACE_CUDA(cudaEventCreateWithFlags(&sk->s_copied[i], cudaEventDisableTiming));
       if (!sk->s_used[i]) ACE_CUDA(cudaEventCreateWithFlags(&sk->s_used[i], cudaEventDisableTiming));
     }
-    // the staging halves are free once earlier work on the stream is done
-    ACE_CUDA(cudaEventRecord(sk->s_used[0], sk->stream));
-    ACE_CUDA(cudaEventRecord(sk->s_used[1], sk->stream));
-    ACE_CUDA(cudaStreamWaitEvent(sk->cstream, sk->s_used[0], 0));
-    const uint64_t rows0 = std::min(G * batch, n);
-    ACE_CUDA(cudaMemcpyAsync(sk->sstage[0].p, x, rows0 * ld * esz, cudaMemcpyHostToDevice, sk->cstream));
-    ACE_CUDA(cudaEventRecord(sk->s_copied[0], sk->cstream));
   }
-  for (uint64_t g0 = 0; g0 < nb; g0 += G) {
-    const uint64_t gb = std::min(G, nb - g0), gr0 = g0 * batch, grows = std::min(gb * batch, n - gr0);
-    if (batch_ms) ACE_CUDA(cudaEventRecord(ev_a[g0], sk->stream));
-    const void* xg = static_cast<const char*>(x) + gr0 * ld * esz;
-    const void* xd;
-    uint64_t ldd;
+  // All device work of the call.  Consecutive batches alternate the two cut
+  // slots (slot = batch index & 1): a batch's phase B reads the slot its
+  // phase A wrote one launch earlier.
+  auto device_work = [&]() -> ace_status {
+    ACE_CUDA(zero_call_fields(sk));
     if (overlap) {
-      // group g's rows were copied into staging half g & 1 ahead of time;
-      // start the copy of group g + 1 into the other half once the hash of
-      // group g - 1 (its previous user) has run
-      const int hb = static_cast<int>((g0 / G) & 1u);
-      ACE_CUDA(cudaStreamWaitEvent(sk->stream, sk->s_copied[hb], 0));
-      xd = sk->sstage[hb].p;
-      ldd = ld;
-      ACE_CUDA(tmark(0, false));
-      r = run_hash(sk, xd, dtype, grows, ldd, 0);
-      if (r != ACE_OK) return r;
-      ACE_CUDA(tmark(0, true));
-      ACE_CUDA(cudaEventRecord(sk->s_used[hb], sk->stream));
-      const uint64_t g1 = g0 + G;
-      if (g1 < nb) {
-        const uint64_t r1 = g1 * batch, rows1 = std::min(G * batch, n - r1);
-        ACE_CUDA(cudaStreamWaitEvent(sk->cstream, sk->s_used[hb ^ 1], 0));
-        ACE_CUDA(cudaMemcpyAsync(sk->sstage[hb ^ 1].p, static_cast<const char*>(x) + r1 * ld * esz, rows1 * ld * esz,
-                                 cudaMemcpyHostToDevice, sk->cstream));
-        ACE_CUDA(cudaEventRecord(sk->s_copied[hb ^ 1], sk->cstream));
-      }
-    } else {
-      r = stage_x(sk, sk->stage, sk->stream, xg, dtype, grows, ld, x_where, &xd, &ldd);
-      if (r != ACE_OK) return r;
-      ACE_CUDA(tmark(0, false));
-      r = run_hash(sk, xd, dtype, grows, ldd, 0);
-      if (r != ACE_OK) return r;
-      ACE_CUDA(tmark(0, true));
+      // the staging halves are free once earlier work on the stream is done
+      ACE_CUDA(cudaEventRecord(sk->s_used[0], sk->stream));
+      ACE_CUDA(cudaEventRecord(sk->s_used[1], sk->stream));
+      ACE_CUDA(cudaStreamWaitEvent(sk->cstream, sk->s_used[0], 0));
+      const uint64_t rows0 = std::min(G * batch, n);
+      ACE_CUDA(cudaMemcpyAsync(sk->sstage[0].p, x, rows0 * ld * esz, cudaMemcpyHostToDevice, sk->cstream));
+      ACE_CUDA(cudaEventRecord(sk->s_copied[0], sk->cstream));
     }
-    for (uint64_t b = g0; b < g0 + gb; ++b) {
-      const uint64_t r0 = b * batch, rows = std::min(batch, n - r0);
-      if (batch_ms && b != g0) ACE_CUDA(cudaEventRecord(ev_a[b], sk->stream));
-      const uint32_t* ids = sk->ids.as<uint32_t>() + (r0 - gr0);
-      if (fast) {
-        const uint32_t slot = static_cast<uint32_t>(sk->stream_seq++ & 1u);
-        uint32_t* cnt = sk->cnt[slot].as<uint32_t>();
-        ACE_CUDA(tmark(1, false));
-        ACE_CUDA(launch_stream_apply(ids, rows, grows, f->d.tables, f->d.k_bits, sk->counters, cnt,
-                                     sk->dts.as<unsigned long long>(), slot, p_cnt, p_rows, p_flags, nullptr, p_slot,
-                                     alpha, sk->st, sk->stream));
-        ACE_CUDA(tmark(1, true));
-        if (batch_ms && p_rows) ACE_CUDA(cudaEventRecord(ev_b[p_b], sk->stream));
-        p_cnt = cnt;
-        p_rows = rows;
-        p_b = b;
-        p_flags = dflags + r0 / 32;
-        p_slot = slot;
-        continue;
+    // the batch whose phase B is still due (fast path)
+    const uint32_t* p_cnt = nullptr;
+    uint64_t p_rows = 0, p_b = 0;
+    uint32_t* p_flags = nullptr;
+    uint32_t p_slot = 0;
+    for (uint64_t g0 = 0; g0 < nb; g0 += G) {
+      const uint64_t gb = std::min(G, nb - g0), gr0 = g0 * batch, grows = std::min(gb * batch, n - gr0);
+      if (batch_ms) ACE_CUDA(cudaEventRecord(sk->lat_a[g0], sk->stream));
+      const void* xg = static_cast<const char*>(x) + gr0 * ld * esz;
+      const void* xd;
+      uint64_t ldd;
+      ace_status rr;
+      if (overlap) {
+        // group g's rows were copied into staging half g & 1 ahead of time;
+        // start the copy of group g + 1 into the other half once the hash of
+        // group g - 1 (its previous user) has run
+        const int hb = static_cast<int>((g0 / G) & 1u);
+        ACE_CUDA(cudaStreamWaitEvent(sk->stream, sk->s_copied[hb], 0));
+        xd = sk->sstage[hb].p;
+        ldd = ld;
+        ACE_CUDA(tmark(0, false));
+        if ((rr = run_hash(sk, xd, dtype, grows, ldd, 0)) != ACE_OK) return rr;
+        ACE_CUDA(tmark(0, true));
+        ACE_CUDA(cudaEventRecord(sk->s_used[hb], sk->stream));
+        const uint64_t g1 = g0 + G;
+        if (g1 < nb) {
+          const uint64_t r1 = g1 * batch, rows1 = std::min(G * batch, n - r1);
+          ACE_CUDA(cudaStreamWaitEvent(sk->cstream, sk->s_used[hb ^ 1], 0));
+          ACE_CUDA(cudaMemcpyAsync(sk->sstage[hb ^ 1].p, static_cast<const char*>(x) + r1 * ld * esz,
+                                   rows1 * ld * esz, cudaMemcpyHostToDevice, sk->cstream));
+          ACE_CUDA(cudaEventRecord(sk->s_copied[hb ^ 1], sk->cstream));
+        }
+      } else {
+        if ((rr = stage_x(sk, sk->stage, sk->stream, xg, dtype, grows, ld, x_where, &xd, &ldd)) != ACE_OK) return rr;
+        ACE_CUDA(tmark(0, false));
+        if ((rr = run_hash(sk, xd, dtype, grows, ldd, 0)) != ACE_OK) return rr;
+        ACE_CUDA(tmark(0, true));
       }
-      ACE_CUDA(cudaMemsetAsync(&sk->st->batch_sum, 0, sizeof(unsigned long long), sk->stream));
-      ACE_CUDA(launch_stream_score(ids, rows, f->d.tables, f->d.k_bits, sk->counters, alpha, dflags + r0 / 32,
-                                   nullptr, sk->st, sk->stream, grows));
-      ACE_CUDA(launch_apply_ids(ids, rows, f->d.tables, f->d.k_bits, sk->counters, sk->cap, +1, sk->st, sk->stream,
-                                !ff, grows));
-      if (sk->width == 16) ACE_CUDA(launch_cap(sk->counters, sk->num_counters, sk->cap, sk->st, sk->stream));
-      if (batch_ms) ACE_CUDA(cudaEventRecord(ev_b[b], sk->stream));
+      for (uint64_t b = g0; b < g0 + gb; ++b) {
+        const uint64_t r0 = b * batch, rows = std::min(batch, n - r0);
+        if (batch_ms && b != g0) ACE_CUDA(cudaEventRecord(sk->lat_a[b], sk->stream));
+        const uint32_t* ids = sk->ids.as<uint32_t>() + (r0 - gr0);
+        if (fast) {
+          const uint32_t slot = static_cast<uint32_t>(b & 1u);
+          uint32_t* cnt = sk->cnt[slot].as<uint32_t>();
+          ACE_CUDA(tmark(1, false));
+          ACE_CUDA(launch_stream_apply(ids, rows, grows, f->d.tables, f->d.k_bits, sk->counters, cnt, slot, p_cnt,
+                                       p_rows, p_flags, nullptr, p_slot, alpha, sk->st, sk->stream));
+          ACE_CUDA(tmark(1, true));
+          if (batch_ms && p_rows) ACE_CUDA(cudaEventRecord(sk->lat_b[p_b], sk->stream));
+          p_cnt = cnt;
+          p_rows = rows;
+          p_b = b;
+          p_flags = dflags + r0 / 32;
+          p_slot = slot;
+          continue;
+        }
+        ACE_CUDA(cudaMemsetAsync(&sk->st->batch_sum, 0, sizeof(unsigned long long), sk->stream));
+        ACE_CUDA(launch_stream_score(ids, rows, f->d.tables, f->d.k_bits, sk->counters, alpha, dflags + r0 / 32,
+                                     nullptr, sk->st, sk->stream, grows));
+        ACE_CUDA(launch_apply_ids(ids, rows, f->d.tables, f->d.k_bits, sk->counters, sk->cap, +1, sk->st, sk->stream,
+                                  !ff, grows));
+        if (sk->width == 16) ACE_CUDA(launch_cap(sk->counters, sk->num_counters, sk->cap, sk->st, sk->stream));
+        if (batch_ms) ACE_CUDA(cudaEventRecord(sk->lat_b[b], sk->stream));
+      }
     }
-  }
-  if (fast && p_rows) {  // the last batch's phase B
-    ACE_CUDA(tmark(1, false));
-    ACE_CUDA(launch_stream_apply(nullptr, 0, 0, f->d.tables, f->d.k_bits, sk->counters, nullptr, nullptr, 0, p_cnt,
-                                 p_rows, p_flags, nullptr, p_slot, alpha, sk->st, sk->stream));
-    ACE_CUDA(tmark(1, true));
-    if (batch_ms) ACE_CUDA(cudaEventRecord(ev_b[p_b], sk->stream));
-  }
-  if (flag_bits && out_where == ACE_HOST)
-    if ((r = copy_out(flag_bits, dflags, ((n + 31) / 32) * sizeof(uint32_t), ACE_HOST, sk->stream)) != ACE_OK)
+    if (fast && p_rows) {  // the last batch's phase B
+      ACE_CUDA(tmark(1, false));
+      ACE_CUDA(launch_stream_apply(nullptr, 0, 0, f->d.tables, f->d.k_bits, sk->counters, nullptr, 0, p_cnt, p_rows,
+                                   p_flags, nullptr, p_slot, alpha, sk->st, sk->stream));
+      ACE_CUDA(tmark(1, true));
+      if (batch_ms) ACE_CUDA(cudaEventRecord(sk->lat_b[p_b], sk->stream));
+    }
+    if (flag_bits && out_where == ACE_HOST) {
+      ace_status rr2 = copy_out(flag_bits, dflags, ((n + 31) / 32) * sizeof(uint32_t), ACE_HOST, sk->stream);
+      if (rr2 != ACE_OK) return rr2;
+    }
+    return ACE_OK;
+  };
+  // Repeated calls with the same arguments (device rows) replay a CUDA graph
+  // of all the device work (captured on the second identical call): the
+  // thousands of launches of a long stream cost one graph launch.
+  AceSketch::StreamKey key;
+  key.x = x;
+  key.flags = flag_bits;
+  key.n = n;
+  key.ld = ld;
+  key.batch = batch;
+  key.alpha = alpha;
+  key.dtype = dtype;
+  key.out_where = out_where;
+  key.lat = batch_ms != nullptr;
+  key.group = sk->stream_group;
+  key.stream = sk->stream;
+  key.ff = ff;
+  const DevBuf* sb[6] = {&sk->ids, &sk->flags, &sk->cnt[0], &sk->cnt[1], &sk->near, &sk->overflow};
+  for (int i = 0; i < 6; ++i) key.bufs[i] = sb[i]->p;
+  // (per-batch latency events are recorded only outside graphs)
+  const bool eligible = x_where == ACE_DEVICE && !sk->timing && fast && !batch_ms;
+  if (eligible && sk->sgexec && key == sk->sgkey) {
+    ACE_CUDA(cudaGraphLaunch(sk->sgexec, sk->stream));
+    count_launch(sk->sglaunches);
+  } else if (eligible && sk->sgseen_valid && key == sk->sgseen) {
+    if (sk->sgexec) cudaGraphExecDestroy(sk->sgexec);
+    sk->sgexec = nullptr;
+    const unsigned long long l0 = ace_kernel_launches();
+    ACE_CUDA(cudaStreamBeginCapture(sk->stream, cudaStreamCaptureModeThreadLocal));
+    r = device_work();
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(sk->stream, &g);
+    if (r != ACE_OK) {
+      if (g) cudaGraphDestroy(g);
       return r;
+    }
+    if (ce != cudaSuccess) return fail(ACE_E_CUDA, std::string("stream graph capture: ") + cudaGetErrorString(ce));
+    const cudaError_t ie = cudaGraphInstantiate(&sk->sgexec, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) {
+      sk->sgexec = nullptr;
+      return fail(ACE_E_CUDA, std::string("stream graph instantiate: ") + cudaGetErrorString(ie));
+    }
+    sk->sglaunches = ace_kernel_launches() - l0;
+    sk->sgkey = key;
+    ACE_CUDA(cudaGraphLaunch(sk->sgexec, sk->stream));
+  } else {
+    if ((r = device_work()) != ACE_OK) return r;
+    sk->sgseen = key;
+    sk->sgseen_valid = eligible;
+  }
   r = pull_state(sk);
   if (r != ACE_OK) return r;
   if (sk->timing) {
@@ -1358,11 +1444,9 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
   if (batch_ms) {
     for (uint64_t b = 0; b < nb; ++b) {
       float ms = 0.f;
-      cudaEventElapsedTime(&ms, ev_a[b], ev_b[b]);
+      cudaEventElapsedTime(&ms, sk->lat_a[b], sk->lat_b[b]);
       batch_ms[b] = ms;
     }
-    for (auto& e : ev_a) cudaEventDestroy(e);
-    for (auto& e : ev_b) cudaEventDestroy(e);
   }
   fill_stats(stats, *sk->hst, n, f);
   if (report) {

@@ -40,6 +40,7 @@ struct DevState {
   double cut_ring[2], mean_ring[2];
   int live_ring[2];
   unsigned int ticket_s;         // phase-A blocks done (the last one commits T and n)
+  unsigned long long dT_acc;     // phase-A increments of T pending the last block's commit
 };
 
 // T / den correctly rounded to binary64 (round half to even), T, den < 2^64:

@@ -1304,37 +1304,57 @@ __global__ void stream_score_kernel(const uint32_t* __restrict__ ids, uint64_t n
 
 // One streaming batch, in the reference's streaming order (detect.cpp:76-84
 // on the counts at batch start, then the insert, ace_cli.cpp:177-183 with the
-// insert deferred to the batch end), without a grid barrier.  One launch does
-// phase A of batch b and phase B of the batch before it:
-//   phase A (blocks [0, L * parts)): block (t, p) owns bins [p, p+1) * 2^pb
-//     of table t.  It stages them in shared memory, reads all n ids of table
-//     t, and for the ids in its bins writes the count at batch start into
-//     cnt_out[t][i] and counts the id into a shared histogram; then it adds the
-//     histogram to its bins (plain stores: no other block writes them) and
-//     computes T += (c + m)^2 - c^2 = 2 c m + m^2 exactly.  Block 0 first
-//     records the cut mean - alpha of batch b from the state before the
-//     batch; the last phase-A block commits T and n.
-//   phase B (the other blocks): batch b-1's scores S_i = sum_t cnt[t][i]
-//     (coalesced rows), flags score <= cut (the cut recorded when its phase A
-//     ran), optional scores, reported / ambiguous counts.
-// The counts of a batch are final when its launch ends, so phase B of batch
-// b-1 overlaps phase A of batch b; a one-batch call runs A, then B alone.
+// insert deferred to the batch end), without a grid barrier.  One launch of G
+// blocks (one per SM) does phase B of the previous batch, then phase A of
+// batch b:
+//   phase B: the previous batch's scores S_i = sum_t cnt[t][i] (coalesced
+//     rows, warps dealt over all blocks), flags score <= cut (the cut that
+//     batch's phase A recorded), optional scores, reported / ambiguous counts.
+//   phase A: the G blocks split the L tables into bin ranges (2 or 3 per
+//     table at L = 50); block (t, range) stages its bins in shared memory,
+//     reads all n ids of table t, and for the ids in its range writes the
+//     count at batch start into cnt_out[t][i] and counts the id into a shared
+//     histogram; then it adds the histogram to its bins (plain stores: no
+//     other block writes them) with T += (c + m)^2 - c^2 = 2 c m + m^2
+//     exactly.  Block 0 first records the cut mean - alpha of batch b from the
+//     state before the batch (no block commits T before every block has
+//     passed its start: the last block to finish commits T and n).
+// Phase B of a batch thus overlaps nothing but its successor's staging; a
+// one-batch call runs A, then B alone.
 struct StreamApplyArgs {
   const uint32_t* ids;  // batch b, table-major, ids[t * stride + i]; n = 0: no phase A
   uint64_t n, stride;
-  uint32_t tables, k_bits, part_bits;
+  uint32_t tables, k_bits;
   uint32_t* counters;
   uint32_t* cnt_out;             // [tables][n]
-  unsigned long long* dT_slots;  // one per phase-A block
   uint32_t slot_a;               // cut slot of batch b
-  const uint32_t* cnt_in;        // batch b-1: [tables][n_prev]; n_prev = 0: no phase B
+  const uint32_t* cnt_in;        // previous batch: [tables][n_prev]; n_prev = 0: no phase B
   uint64_t n_prev;
-  uint32_t* flag_bits;           // batch b-1's flag words
-  double* scores;                // batch b-1's scores or null
-  uint32_t slot_b;               // cut slot of batch b-1
+  uint32_t* flag_bits;           // previous batch's flag words
+  double* scores;                // previous batch's scores or null
+  uint32_t slot_b;               // cut slot of the previous batch
   double alpha;
   DevState* st;
 };
+
+// Block b of G -> (table, bin range): the first G % L tables get one range more.
+__device__ __forceinline__ void stream_part(uint32_t b, uint32_t G, uint32_t L, uint32_t nbins, uint32_t& t,
+                                            uint32_t& b0, uint32_t& b1) {
+  const uint32_t base = G / L, extra = G % L;
+  uint32_t p, P;
+  if (b < extra * (base + 1u)) {
+    P = base + 1u;
+    t = b / P;
+    p = b % P;
+  } else {
+    const uint32_t r = b - extra * (base + 1u);
+    P = base;
+    t = extra + r / P;
+    p = r % P;
+  }
+  b0 = static_cast<uint32_t>(static_cast<uint64_t>(nbins) * p / P) & ~3u;
+  b1 = p + 1u == P ? nbins : (static_cast<uint32_t>(static_cast<uint64_t>(nbins) * (p + 1u) / P) & ~3u);
+}
 
 __global__ void __launch_bounds__(1024) stream_apply_kernel(const StreamApplyArgs a) {
   extern __shared__ __align__(16) uint32_t sm[];
@@ -1342,200 +1362,194 @@ __global__ void __launch_bounds__(1024) stream_apply_kernel(const StreamApplyArg
   __shared__ unsigned long long red2[32];
   DevState* st = a.st;
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint32_t parts = 1u << (a.k_bits - a.part_bits);
-  const uint32_t nA = a.n ? a.tables * parts : 0u;
-  if (blockIdx.x < nA) {
-    // ---------------- phase A: counts at batch start, then the insert ----------------
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      const unsigned long long n0 = st->n;
-      const double mu = n0 ? ace_div_rn(st->T, n0 * a.tables) : 0.0;
-      st->cut_ring[a.slot_a] = mu - a.alpha;
-      st->mean_ring[a.slot_a] = mu;
-      st->live_ring[a.slot_a] = n0 > 0 ? 1 : 0;
-    }
-    const uint32_t t = blockIdx.x / parts, p = blockIdx.x % parts;
-    const uint32_t nbp = 1u << a.part_bits, base = p << a.part_bits;
-    uint32_t* cs = sm;        // counts at batch start (read-only during the batch)
-    uint32_t* ms = sm + nbp;  // this batch's histogram
-    uint32_t* ct = a.counters + (static_cast<uint64_t>(t) << a.k_bits) + base;
-    {  // 16-byte staging (nbp is a multiple of 4, the bins 16-byte aligned)
-      const uint4* c4 = reinterpret_cast<const uint4*>(ct);
-      for (uint32_t b = threadIdx.x; b < nbp / 4; b += blockDim.x) {
-        reinterpret_cast<uint4*>(cs)[b] = c4[b];
-        reinterpret_cast<uint4*>(ms)[b] = make_uint4(0u, 0u, 0u, 0u);
-      }
-    }
-    __syncthreads();
-    const uint32_t* idt = a.ids + static_cast<uint64_t>(t) * a.stride;
-    uint32_t* co = a.cnt_out + static_cast<uint64_t>(t) * a.n;
-    auto take = [&](uint64_t i, uint32_t id) {
-      const uint32_t rel = id - base;
-      if (rel < nbp) {
-#ifndef ACE_EXP_NOGATHER
-        co[i] = cs[rel];
-#endif
-#ifndef ACE_EXP_NOATOM
-        atomicAdd(&ms[rel], 1u);
-#endif
-      }
+  const uint32_t G = gridDim.x, bb = blockIdx.x;
+  if (a.n && bb == 0 && threadIdx.x == 0) {
+    const unsigned long long n0 = st->n;
+    const double mu = n0 ? ace_div_rn(st->T, n0 * a.tables) : 0.0;
+    st->cut_ring[a.slot_a] = mu - a.alpha;
+    st->mean_ring[a.slot_a] = mu;
+    st->live_ring[a.slot_a] = n0 > 0 ? 1 : 0;
+  }
+  // ---------------- phase B: scores and flags of the previous batch ----------------
+  if (a.n_prev) {
+    const double cut = st->cut_ring[a.slot_b], mu = st->mean_ring[a.slot_b];
+    const int live = st->live_ring[a.slot_b];
+    const double band = kStreamBand * fmax(1.0, fabs(mu));
+    const double L = static_cast<double>(a.tables);
+    unsigned long long rep = 0ull, amb = 0ull;
+    auto score_flag = [&](uint64_t i, unsigned long long S) -> bool {
+      const double sc = __ddiv_rn(static_cast<double>(S), L);
+      if (a.scores) a.scores[i] = sc;
+      if (live && fabs(sc - cut) <= band) ++amb;
+      return live && sc <= cut;
     };
-    if (a.stride % 4 == 0 && a.n % 4 == 0 && (reinterpret_cast<uintptr_t>(a.ids) & 15) == 0) {
-      // 16-byte id loads, kDepth per thread in flight (the ids are L2-resident:
-      // memory-level parallelism, not bandwidth, bounds this loop)
-      constexpr int kDepth = 8;
-      const uint4* id4 = reinterpret_cast<const uint4*>(idt);
-      const uint64_t n4 = a.n / 4;
-      for (uint64_t g0 = 0; g0 < n4; g0 += kDepth * blockDim.x) {
-        uint4 q[kDepth];
+    if (a.n_prev % 128 == 0) {
+      // four rows per thread (16-byte loads of 8 tables in flight), a warp
+      // covers 128 rows = 4 flag words; warps dealt round-robin over blocks
+      const uint64_t quads = a.n_prev / 4;
+      const uint4* c4 = reinterpret_cast<const uint4*>(a.cnt_in);
+      const uint64_t nwarps = static_cast<uint64_t>(G) * (blockDim.x >> 5);
+      for (uint64_t qd = (static_cast<uint64_t>(wid) * G + bb) * 32 + lane; qd < quads; qd += nwarps * 32) {
+        unsigned long long S[4] = {0ull, 0ull, 0ull, 0ull};
+        for (uint32_t t0 = 0; t0 < a.tables; t0 += 8) {
+          uint4 c[8];
 #pragma unroll
-        for (int u = 0; u < kDepth; ++u) q[u] = __ldg(id4 + min(g0 + u * blockDim.x + threadIdx.x, n4 - 1));
+          for (int u = 0; u < 8; ++u) c[u] = __ldcg(c4 + static_cast<uint64_t>(min(t0 + u, a.tables - 1)) * quads + qd);
 #pragma unroll
-        for (int u = 0; u < kDepth; ++u) {
-          const uint64_t j = g0 + u * blockDim.x + threadIdx.x;
-          if (j < n4) {
-            take(4 * j, q[u].x);
-            take(4 * j + 1, q[u].y);
-            take(4 * j + 2, q[u].z);
-            take(4 * j + 3, q[u].w);
-          }
+          for (int u = 0; u < 8; ++u)
+            if (t0 + u < a.tables) {
+              S[0] += c[u].x;
+              S[1] += c[u].y;
+              S[2] += c[u].z;
+              S[3] += c[u].w;
+            }
+        }
+        uint32_t nib = 0u;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) nib |= (score_flag(4 * qd + e, S[e]) ? 1u : 0u) << e;
+        // lane l holds rows 4 l .. 4 l + 3 of the warp's 128: word l / 8, bits 4 (l % 8) ..
+        uint32_t word = nib << (4 * (lane & 7));
+        word |= __shfl_xor_sync(0xffffffffu, word, 1);
+        word |= __shfl_xor_sync(0xffffffffu, word, 2);
+        word |= __shfl_xor_sync(0xffffffffu, word, 4);
+        if ((lane & 7) == 0) {
+          a.flag_bits[qd / 8] = word;
+          rep += __popc(word);
         }
       }
     } else {
-      constexpr int kDepth = 16;
-      for (uint64_t i0 = 0; i0 < a.n; i0 += kDepth * blockDim.x) {
-        uint32_t idv[kDepth];
+      const uint64_t words = (a.n_prev + 31) / 32;
+      for (uint64_t w = static_cast<uint64_t>(wid) * G + bb; w < words; w += static_cast<uint64_t>(G) * (blockDim.x >> 5)) {
+        const uint64_t i = w * 32 + lane;
+        bool f = false;
+        if (i < a.n_prev) {
+          unsigned long long S = 0ull;
+          for (uint32_t t0 = 0; t0 < a.tables; t0 += 16) {
+            uint32_t c[16];
 #pragma unroll
-        for (int u = 0; u < kDepth; ++u) idv[u] = __ldg(idt + min(i0 + u * blockDim.x + threadIdx.x, a.n - 1));
+            for (int u = 0; u < 16; ++u) c[u] = __ldcg(a.cnt_in + static_cast<uint64_t>(min(t0 + u, a.tables - 1)) * a.n_prev + i);
 #pragma unroll
-        for (int u = 0; u < kDepth; ++u) {
-          const uint64_t i = i0 + u * blockDim.x + threadIdx.x;
-          if (i < a.n) take(i, idv[u]);
+            for (int u = 0; u < 16; ++u)
+              if (t0 + u < a.tables) S += c[u];
+          }
+          f = score_flag(i, S);
+        }
+        const unsigned word = __ballot_sync(0xffffffffu, f);  // whole words: rows past n_prev are 0
+        if (lane == 0) {
+          a.flag_bits[w] = word;
+          rep += __popc(word);
         }
       }
     }
-    __syncthreads();
-    unsigned long long dT = 0ull;
-    for (uint32_t b = threadIdx.x; b < nbp; b += blockDim.x) {
-      const uint32_t m = ms[b];
-      if (m) {
-        const uint32_t c = cs[b];
-        ct[b] = c + m;
-        dT += 2ull * c * m + static_cast<unsigned long long>(m) * m;
-      }
+    rep = warp_sum_u64(rep);
+    amb = warp_sum_u64(amb);
+    if (lane == 0) {
+      red[wid] = rep;
+      red2[wid] = amb;
     }
-    dT = warp_sum_u64(dT);
-    if (lane == 0) red[wid] = dT;
     __syncthreads();
     if (threadIdx.x == 0) {
-      unsigned long long sum = 0ull;
-      for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) sum += red[w];
-      a.dT_slots[blockIdx.x] = sum;
-      __threadfence();
-      if (atomicAdd(&st->ticket_s, 1u) == nA - 1u) {
-        // every phase-A block has recorded its increment (and block 0 its cut)
-        __threadfence();
-        unsigned long long tot = 0ull;
-        for (uint32_t k = 0; k < nA; ++k) tot += __ldcg(a.dT_slots + k);
-        st->T += tot;
-        st->n += a.n;
-        st->ticket_s = 0u;
+      unsigned long long r = 0ull, m = 0ull;
+      for (uint32_t k = 0; k < (blockDim.x >> 5); ++k) {
+        r += red[k];
+        m += red2[k];
+      }
+      if (r) atomicAdd(&st->reported, r);
+      if (m) atomicAdd(&st->ambiguous, m);
+      if (bb == 0) {
+        st->cut = cut;
+        st->mean_before = mu;
       }
     }
-    return;
+    __syncthreads();
   }
-  // ---------------- phase B: scores and flags of the previous batch ----------------
-  if (a.n_prev == 0) return;
-  const uint32_t bb = blockIdx.x - nA, nB = gridDim.x - nA;
-  const double cut = st->cut_ring[a.slot_b], mu = st->mean_ring[a.slot_b];
-  const int live = st->live_ring[a.slot_b];
-  const double band = kStreamBand * fmax(1.0, fabs(mu));
-  const double L = static_cast<double>(a.tables);
-  unsigned long long rep = 0ull, amb = 0ull;
-  auto score_flag = [&](uint64_t i, unsigned long long S) -> bool {
-    const double sc = __ddiv_rn(static_cast<double>(S), L);
-    if (a.scores) a.scores[i] = sc;
-    if (live && fabs(sc - cut) <= band) ++amb;
-    return live && sc <= cut;
+  if (a.n == 0) return;
+  // ---------------- phase A: counts at batch start, then the insert ----------------
+  uint32_t t, b0, b1;
+  stream_part(bb, G, a.tables, 1u << a.k_bits, t, b0, b1);
+  const uint32_t nbp = b1 - b0;
+  uint32_t* cs = sm;                            // counts at batch start (read-only during the batch)
+  uint32_t* ms = sm + ((nbp + 3u) & ~3u);       // this batch's histogram
+  uint32_t* ct = a.counters + (static_cast<uint64_t>(t) << a.k_bits) + b0;
+  {  // 16-byte staging (range bounds are multiples of 4, the bins 16-byte aligned)
+    const uint4* c4 = reinterpret_cast<const uint4*>(ct);
+    for (uint32_t b = threadIdx.x; b < nbp / 4; b += blockDim.x) {
+      reinterpret_cast<uint4*>(cs)[b] = c4[b];
+      reinterpret_cast<uint4*>(ms)[b] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    for (uint32_t b = (nbp & ~3u) + threadIdx.x; b < nbp; b += blockDim.x) {  // K < 2
+      cs[b] = ct[b];
+      ms[b] = 0u;
+    }
+  }
+  __syncthreads();
+  const uint32_t* idt = a.ids + static_cast<uint64_t>(t) * a.stride;
+  uint32_t* co = a.cnt_out + static_cast<uint64_t>(t) * a.n;
+  auto take = [&](uint64_t i, uint32_t id) {
+    const uint32_t rel = id - b0;
+    if (rel < nbp) {
+      co[i] = cs[rel];
+      atomicAdd(&ms[rel], 1u);
+    }
   };
-  if (a.n_prev % 128 == 0) {
-    // four rows per thread (16-byte loads of 16 tables in flight), a warp
-    // covers 128 rows = 4 flag words
-    const uint64_t quads = a.n_prev / 4;
-    const uint4* c4 = reinterpret_cast<const uint4*>(a.cnt_in);
-    const uint64_t q4 = a.n_prev / 4;  // uint4 per table row
-    // warps dealt round-robin over the blocks (a short batch still spreads
-    // over every SM)
-    const uint64_t nwarps = static_cast<uint64_t>(nB) * (blockDim.x >> 5);
-    for (uint64_t qd = (static_cast<uint64_t>(wid) * nB + bb) * 32 + lane; qd < quads; qd += nwarps * 32) {
-      unsigned long long S[4] = {0ull, 0ull, 0ull, 0ull};
-      for (uint32_t t0 = 0; t0 < a.tables; t0 += 16) {
-        uint4 c[16];
+  if (a.stride % 4 == 0 && a.n % 4 == 0 && (reinterpret_cast<uintptr_t>(a.ids) & 15) == 0) {
+    // 16-byte id loads, kDepth per thread in flight (the ids are L2-resident:
+    // memory-level parallelism, not bandwidth, bounds this loop)
+    constexpr int kDepth = 8;
+    const uint4* id4 = reinterpret_cast<const uint4*>(idt);
+    const uint64_t n4 = a.n / 4;
+    for (uint64_t g0 = 0; g0 < n4; g0 += kDepth * blockDim.x) {
+      uint4 q[kDepth];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) c[u] = __ldcg(c4 + static_cast<uint64_t>(min(t0 + u, a.tables - 1)) * q4 + qd);
+      for (int u = 0; u < kDepth; ++u) q[u] = __ldg(id4 + min(g0 + u * blockDim.x + threadIdx.x, n4 - 1));
 #pragma unroll
-        for (int u = 0; u < 16; ++u)
-          if (t0 + u < a.tables) {
-            S[0] += c[u].x;
-            S[1] += c[u].y;
-            S[2] += c[u].z;
-            S[3] += c[u].w;
-          }
-      }
-      uint32_t nib = 0u;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) nib |= (score_flag(4 * qd + e, S[e]) ? 1u : 0u) << e;
-      // lane l holds rows 4 l .. 4 l + 3 of the warp's 128: word l / 8, bits 4 (l % 8) ..
-      uint32_t word = nib << (4 * (lane & 7));
-      word |= __shfl_xor_sync(0xffffffffu, word, 1);
-      word |= __shfl_xor_sync(0xffffffffu, word, 2);
-      word |= __shfl_xor_sync(0xffffffffu, word, 4);
-      if ((lane & 7) == 0) {
-        a.flag_bits[qd / 8] = word;
-        rep += __popc(word);
+      for (int u = 0; u < kDepth; ++u) {
+        const uint64_t j = g0 + u * blockDim.x + threadIdx.x;
+        if (j < n4) {
+          take(4 * j, q[u].x);
+          take(4 * j + 1, q[u].y);
+          take(4 * j + 2, q[u].z);
+          take(4 * j + 3, q[u].w);
+        }
       }
     }
   } else {
-    const uint64_t words = (a.n_prev + 31) / 32;
-    for (uint64_t w = static_cast<uint64_t>(wid) * nB + bb; w < words; w += static_cast<uint64_t>(nB) * (blockDim.x >> 5)) {
-      const uint64_t i = w * 32 + lane;
-      bool f = false;
-      if (i < a.n_prev) {
-        unsigned long long S = 0ull;
-        for (uint32_t t0 = 0; t0 < a.tables; t0 += 16) {
-          uint32_t c[16];
+    constexpr int kDepth = 16;
+    for (uint64_t i0 = 0; i0 < a.n; i0 += kDepth * blockDim.x) {
+      uint32_t idv[kDepth];
 #pragma unroll
-          for (int u = 0; u < 16; ++u) c[u] = __ldcg(a.cnt_in + static_cast<uint64_t>(min(t0 + u, a.tables - 1)) * a.n_prev + i);
+      for (int u = 0; u < kDepth; ++u) idv[u] = __ldg(idt + min(i0 + u * blockDim.x + threadIdx.x, a.n - 1));
 #pragma unroll
-          for (int u = 0; u < 16; ++u)
-            if (t0 + u < a.tables) S += c[u];
-        }
-        f = score_flag(i, S);
-      }
-      const unsigned word = __ballot_sync(0xffffffffu, f);  // whole words: rows past n_prev are 0
-      if (lane == 0) {
-        a.flag_bits[w] = word;
-        rep += __popc(word);
+      for (int u = 0; u < kDepth; ++u) {
+        const uint64_t i = i0 + u * blockDim.x + threadIdx.x;
+        if (i < a.n) take(i, idv[u]);
       }
     }
-  }
-  rep = warp_sum_u64(rep);
-  amb = warp_sum_u64(amb);
-  if (lane == 0) {
-    red[wid] = rep;
-    red2[wid] = amb;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long r = 0ull, m = 0ull;
-    for (uint32_t k = 0; k < (blockDim.x >> 5); ++k) {
-      r += red[k];
-      m += red2[k];
+  unsigned long long dT = 0ull;
+  for (uint32_t b = threadIdx.x; b < nbp; b += blockDim.x) {
+    const uint32_t m = ms[b];
+    if (m) {
+      const uint32_t c = cs[b];
+      ct[b] = c + m;
+      dT += 2ull * c * m + static_cast<unsigned long long>(m) * m;
     }
-    if (r) atomicAdd(&st->reported, r);
-    if (m) atomicAdd(&st->ambiguous, m);
-    if (bb == 0) {
-      st->cut = cut;
-      st->mean_before = mu;
+  }
+  dT = warp_sum_u64(dT);
+  if (lane == 0) red[wid] = dT;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long sum = 0ull;
+    for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) sum += red[w];
+    if (sum) atomicAdd(&st->dT_acc, sum);
+    __threadfence();
+    if (atomicAdd(&st->ticket_s, 1u) == G - 1u) {
+      // every block has added its increment (and block 0 recorded the cut)
+      __threadfence();
+      st->T += atomicExch(&st->dT_acc, 0ull);
+      st->n += a.n;
+      st->ticket_s = 0u;
     }
   }
 }
@@ -1736,25 +1750,18 @@ cudaError_t launch_stream_score(const uint32_t* ids, uint64_t n, uint32_t tables
   return cudaGetLastError();
 }
 
-uint32_t stream_part_bits(uint32_t tables, uint32_t k_bits) {
-  // bins per phase-A block: two u32 arrays of 2^pb in shared memory (<= 128
-  // KB); split tables further while fewer than ~96 blocks would insert
-  uint32_t pb = k_bits < 14 ? k_bits : 14u;
-  while (pb > 8 && (static_cast<uint64_t>(tables) << (k_bits - pb)) < 96) --pb;
-#ifdef ACE_EXP_PB
-  pb = ACE_EXP_PB;
-#endif
-  return pb;
-}
-
-uint32_t stream_phase_a_blocks(uint32_t tables, uint32_t k_bits) {
-  return tables << (k_bits - stream_part_bits(tables, k_bits));
+// Blocks of the stream kernel: one per SM, at least enough bin ranges per
+// table that two u32 arrays of a range fit in shared memory.
+uint32_t stream_blocks(uint32_t tables, uint32_t k_bits) {
+  const uint32_t nbins = 1u << k_bits;
+  const uint32_t pmin = (nbins * 8u + (200u << 10) - 1u) / (200u << 10);  // 2 x u32 per bin <= 200 KB
+  return std::max<uint32_t>(static_cast<uint32_t>(dev_sms()), tables * std::max(pmin, 1u));
 }
 
 cudaError_t launch_stream_apply(const uint32_t* ids, uint64_t n, uint64_t ids_stride, uint32_t tables, uint32_t k_bits,
-                                uint32_t* counters, uint32_t* cnt_out, unsigned long long* dT_slots, uint32_t slot_a,
-                                const uint32_t* cnt_in, uint64_t n_prev, uint32_t* flag_bits, double* scores,
-                                uint32_t slot_b, double alpha, DevState* st, cudaStream_t s) {
+                                uint32_t* counters, uint32_t* cnt_out, uint32_t slot_a, const uint32_t* cnt_in,
+                                uint64_t n_prev, uint32_t* flag_bits, double* scores, uint32_t slot_b, double alpha,
+                                DevState* st, cudaStream_t s) {
   if (n == 0 && n_prev == 0) return cudaSuccess;
   if (k_bits > 16) return cudaErrorInvalidValue;
   StreamApplyArgs a{};
@@ -1763,10 +1770,8 @@ cudaError_t launch_stream_apply(const uint32_t* ids, uint64_t n, uint64_t ids_st
   a.stride = ids_stride ? ids_stride : n;
   a.tables = tables;
   a.k_bits = k_bits;
-  a.part_bits = stream_part_bits(tables, k_bits);
   a.counters = counters;
   a.cnt_out = cnt_out;
-  a.dT_slots = dT_slots;
   a.slot_a = slot_a;
   a.cnt_in = cnt_in;
   a.n_prev = n_prev;
@@ -1775,14 +1780,13 @@ cudaError_t launch_stream_apply(const uint32_t* ids, uint64_t n, uint64_t ids_st
   a.slot_b = slot_b;
   a.alpha = alpha;
   a.st = st;
-  const int sms = dev_sms();
-  const uint32_t nA = n ? stream_phase_a_blocks(tables, k_bits) : 0u;
-  uint32_t nB = 0;
-  if (n_prev) nB = nA == 0 ? static_cast<uint32_t>(sms) : std::max<uint32_t>(nA < static_cast<uint32_t>(sms) ? sms - nA : 0u, 32u);
-  const size_t smem = n ? (sizeof(uint32_t) << (a.part_bits + 1)) : 0;
-  cudaError_t e = set_smem_once(reinterpret_cast<const void*>(stream_apply_kernel), 128 * 1024, 1);
+  const uint32_t G = stream_blocks(tables, k_bits);
+  const uint32_t base = G / tables;  // smallest ranges per table
+  const uint32_t range = ((1u << k_bits) + base - 1u) / base + 4u;
+  const size_t smem = n ? 2u * sizeof(uint32_t) * ((range + 3u) & ~3u) : 0;
+  cudaError_t e = set_smem_once(reinterpret_cast<const void*>(stream_apply_kernel), 210 * 1024, 1);
   if (e != cudaSuccess) return e;
-  stream_apply_kernel<<<nA + nB, 1024, smem, s>>>(a);
+  stream_apply_kernel<<<G, 1024, smem, s>>>(a);
   count_launch();
   return cudaGetLastError();
 }

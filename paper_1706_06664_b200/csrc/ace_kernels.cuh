@@ -71,16 +71,14 @@ cudaError_t launch_stream_score(const uint32_t* ids, uint64_t n, uint32_t tables
                                 DevState* st, cudaStream_t s, uint64_t ids_stride = 0);  // 0: n
 
 // Streaming (32-bit, unsaturable, K <= 16), no grid barrier: one launch runs
-// phase A of batch b (counts at batch start into cnt_out [L][n], insert, T
-// exact; the cut of batch b recorded in slot_a) and phase B of the batch
-// before it (scores from cnt_in [L][n_prev], flags against slot_b's cut).
-// n = 0: phase B only; n_prev = 0: phase A only.  dT_slots: one u64 per
-// phase-A block (stream_phase_a_blocks).
-uint32_t stream_phase_a_blocks(uint32_t tables, uint32_t k_bits);
+// phase B of the previous batch (scores from cnt_in [L][n_prev], flags
+// against slot_b's cut) and phase A of batch b (counts at batch start into
+// cnt_out [L][n], insert, T exact; the cut of batch b recorded in slot_a).
+// n = 0: phase B only; n_prev = 0: phase A only.
 cudaError_t launch_stream_apply(const uint32_t* ids, uint64_t n, uint64_t ids_stride, uint32_t tables, uint32_t k_bits,
-                                uint32_t* counters, uint32_t* cnt_out, unsigned long long* dT_slots, uint32_t slot_a,
-                                const uint32_t* cnt_in, uint64_t n_prev, uint32_t* flag_bits, double* scores,
-                                uint32_t slot_b, double alpha, DevState* st, cudaStream_t s);
+                                uint32_t* counters, uint32_t* cnt_out, uint32_t slot_a, const uint32_t* cnt_in,
+                                uint64_t n_prev, uint32_t* flag_bits, double* scores, uint32_t slot_b, double alpha,
+                                DevState* st, cudaStream_t s);
 
 // Sum of squares of all counters (T after restore with exact state).
 cudaError_t launch_sum_squares(const uint32_t* counters, uint64_t num,
