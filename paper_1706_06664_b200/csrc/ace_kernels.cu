@@ -1356,22 +1356,14 @@ __device__ __forceinline__ void stream_part(uint32_t b, uint32_t G, uint32_t L, 
   b1 = p + 1u == P ? nbins : (static_cast<uint32_t>(static_cast<uint64_t>(nbins) * (p + 1u) / P) & ~3u);
 }
 
-__global__ void __launch_bounds__(1024) stream_apply_kernel(const StreamApplyArgs a) {
-  extern __shared__ __align__(16) uint32_t sm[];
-  __shared__ unsigned long long red[32];
-  __shared__ unsigned long long red2[32];
+// Phase B of the stream kernels: the previous batch's scores S_i = sum_t
+// cnt[t][i] (coalesced rows, warps dealt over blocks bb of G), flags score <=
+// cut (the cut that batch's phase A recorded), optional scores, reported /
+// ambiguous counts.  Every thread of the block calls it.
+__device__ void stream_phase_b(const StreamApplyArgs& a, uint32_t bb, uint32_t G, unsigned long long* red,
+                               unsigned long long* red2) {
   DevState* st = a.st;
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint32_t G = gridDim.x, bb = blockIdx.x;
-  if (a.n && bb == 0 && threadIdx.x == 0) {
-    const unsigned long long n0 = st->n;
-    const double mu = n0 ? ace_div_rn(st->T, n0 * a.tables) : 0.0;
-    st->cut_ring[a.slot_a] = mu - a.alpha;
-    st->mean_ring[a.slot_a] = mu;
-    st->live_ring[a.slot_a] = n0 > 0 ? 1 : 0;
-  }
-  // ---------------- phase B: scores and flags of the previous batch ----------------
-  if (a.n_prev) {
     const double cut = st->cut_ring[a.slot_b], mu = st->mean_ring[a.slot_b];
     const int live = st->live_ring[a.slot_b];
     const double band = kStreamBand * fmax(1.0, fabs(mu));
@@ -1463,6 +1455,22 @@ __global__ void __launch_bounds__(1024) stream_apply_kernel(const StreamApplyArg
     }
     __syncthreads();
   }
+
+__global__ void __launch_bounds__(1024) stream_apply_kernel(const StreamApplyArgs a) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  __shared__ unsigned long long red[32];
+  __shared__ unsigned long long red2[32];
+  DevState* st = a.st;
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t G = gridDim.x, bb = blockIdx.x;
+  if (a.n && bb == 0 && threadIdx.x == 0) {
+    const unsigned long long n0 = st->n;
+    const double mu = n0 ? ace_div_rn(st->T, n0 * a.tables) : 0.0;
+    st->cut_ring[a.slot_a] = mu - a.alpha;
+    st->mean_ring[a.slot_a] = mu;
+    st->live_ring[a.slot_a] = n0 > 0 ? 1 : 0;
+  }
+  if (a.n_prev) stream_phase_b(a, bb, G, red, red2);
   if (a.n == 0) return;
   // ---------------- phase A: counts at batch start, then the insert ----------------
   uint32_t t, b0, b1;
@@ -1546,6 +1554,113 @@ __global__ void __launch_bounds__(1024) stream_apply_kernel(const StreamApplyArg
     __threadfence();
     if (atomicAdd(&st->ticket_s, 1u) == G - 1u) {
       // every block has added its increment (and block 0 recorded the cut)
+      __threadfence();
+      st->T += atomicExch(&st->dT_acc, 0ull);
+      st->n += a.n;
+      st->ticket_s = 0u;
+    }
+  }
+}
+
+
+// The stream kernel for K <= 15 and batches of at most 2 x 65,535 rows:
+// table t is owned by a cluster of two CTAs.  Both stage the whole table's
+// counts at batch start (u32, 128 KB at K = 15); CTA r takes rows
+// [r n/2, (r+1) n/2) of the batch with full warps (no out-of-range lanes):
+// each row's count at batch start goes to cnt_out[t][i] and the row is
+// counted into the CTA's u16-pair histogram (at most 65,535 per bin: no
+// wrap).  After a cluster barrier CTA r merges bins [r, r+1) * 2^K / 2 of
+// both histograms (its peer's through distributed shared memory) into the
+// table with plain stores (no other CTA writes them) and T += 2 c m + m^2.
+// The CTAs of the clusters past the tables do phase B of the previous batch.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_pair_kernel(const StreamApplyArgs a) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  __shared__ unsigned long long red[32];
+  __shared__ unsigned long long red2[32];
+  DevState* st = a.st;
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t nA = a.n ? 2u * a.tables : 0u;  // phase-A CTAs (one cluster per table)
+  if (blockIdx.x >= nA) {
+    if (a.n_prev) stream_phase_b(a, blockIdx.x - nA, gridDim.x - nA, red, red2);
+    return;
+  }
+  cg::cluster_group cl = cg::this_cluster();
+  const uint32_t r = cl.block_rank(), t = blockIdx.x >> 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // the cut of batch b, from the state before it
+    const unsigned long long n0 = st->n;
+    const double mu = n0 ? ace_div_rn(st->T, n0 * a.tables) : 0.0;
+    st->cut_ring[a.slot_a] = mu - a.alpha;
+    st->mean_ring[a.slot_a] = mu;
+    st->live_ring[a.slot_a] = n0 > 0 ? 1 : 0;
+  }
+  const uint32_t nb = 1u << a.k_bits, nw = (nb + 1u) / 2u;  // bins, histogram words (two u16 bins each)
+  uint32_t* cs = sm;       // counts at batch start [nb]
+  uint32_t* hs = sm + nb;  // this CTA's histogram [nw]
+  uint32_t* ct = a.counters + (static_cast<uint64_t>(t) << a.k_bits);
+  if (nb >= 4) {
+    const uint4* c4 = reinterpret_cast<const uint4*>(ct);
+    for (uint32_t b = threadIdx.x; b < nb / 4; b += blockDim.x) reinterpret_cast<uint4*>(cs)[b] = c4[b];
+  } else {
+    for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) cs[b] = ct[b];
+  }
+  for (uint32_t w = threadIdx.x; w < nw; w += blockDim.x) hs[w] = 0u;
+  __syncthreads();
+  const uint64_t i0 = a.n * r / 2, i1 = a.n * (r + 1) / 2;
+  const uint32_t* idt = a.ids + static_cast<uint64_t>(t) * a.stride;
+  uint32_t* co = a.cnt_out + static_cast<uint64_t>(t) * a.n;
+  auto take = [&](uint64_t i, uint32_t id) {
+    co[i] = cs[id];
+    atomicAdd(&hs[id >> 1], 1u << ((id & 1u) << 4));
+  };
+  if (a.stride % 4 == 0 && i0 % 4 == 0 && i1 % 4 == 0 && (reinterpret_cast<uintptr_t>(a.ids) & 15) == 0) {
+    constexpr int kDepth = 4;  // 16-byte id loads in flight per thread
+    const uint4* id4 = reinterpret_cast<const uint4*>(idt + i0);
+    const uint64_t n4 = (i1 - i0) / 4;
+    for (uint64_t g0 = 0; g0 < n4; g0 += kDepth * blockDim.x) {
+      uint4 q[kDepth];
+#pragma unroll
+      for (int u = 0; u < kDepth; ++u) q[u] = __ldg(id4 + min(g0 + u * blockDim.x + threadIdx.x, n4 - 1));
+#pragma unroll
+      for (int u = 0; u < kDepth; ++u) {
+        const uint64_t j = g0 + u * blockDim.x + threadIdx.x;
+        if (j < n4) {
+          const uint64_t i = i0 + 4 * j;
+          take(i, q[u].x);
+          take(i + 1, q[u].y);
+          take(i + 2, q[u].z);
+          take(i + 3, q[u].w);
+        }
+      }
+    }
+  } else {
+    for (uint64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) take(i, __ldg(idt + i));
+  }
+  cl.sync();  // both histograms complete
+  const uint32_t* peer = cl.map_shared_rank(hs, r ^ 1u);
+  unsigned long long dT = 0ull;
+  const uint32_t w0 = nw * r / 2, w1 = nw * (r + 1) / 2;
+  for (uint32_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) {
+    const uint32_t ow = hs[w], pw = peer[w];
+#pragma unroll
+    for (uint32_t h = 0; h < 2; ++h) {
+      const uint32_t b = 2u * w + h;
+      const uint32_t m = ((ow >> (16 * h)) & 0xffffu) + ((pw >> (16 * h)) & 0xffffu);
+      if (m && b < nb) {
+        const uint32_t c = cs[b];
+        ct[b] = c + m;
+        dT += 2ull * c * m + static_cast<unsigned long long>(m) * m;
+      }
+    }
+  }
+  dT = warp_sum_u64(dT);
+  if (lane == 0) red[wid] = dT;
+  cl.sync();  // the peer has read this CTA's histogram
+  if (threadIdx.x == 0) {
+    unsigned long long sum = 0ull;
+    for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) sum += red[w];
+    if (sum) atomicAdd(&st->dT_acc, sum);
+    __threadfence();
+    if (atomicAdd(&st->ticket_s, 1u) == nA - 1u) {
       __threadfence();
       st->T += atomicExch(&st->dT_acc, 0ull);
       st->n += a.n;
@@ -1780,12 +1895,24 @@ cudaError_t launch_stream_apply(const uint32_t* ids, uint64_t n, uint64_t ids_st
   a.slot_b = slot_b;
   a.alpha = alpha;
   a.st = st;
+  cudaError_t e;
+  if (k_bits <= 15 && (n + 1) / 2 <= 65535u && (n == 0 || 2u * tables <= static_cast<uint32_t>(dev_sms()))) {
+    // one cluster of two CTAs per table; the remaining CTAs (at least 16
+    // clusters) do phase B
+    const uint32_t nA = n ? 2u * tables : 0u;
+    uint32_t grid = std::max<uint32_t>(static_cast<uint32_t>(dev_sms()) & ~1u, nA + 32u);
+    if (n_prev == 0) grid = nA;
+    const size_t smem = n ? sizeof(uint32_t) * ((1u << k_bits) + (1u << k_bits) / 2u + 4u) : 0;
+    if ((e = set_smem_once(reinterpret_cast<const void*>(stream_pair_kernel), 200 * 1024, 5)) != cudaSuccess) return e;
+    stream_pair_kernel<<<grid, 1024, smem, s>>>(a);
+    count_launch();
+    return cudaGetLastError();
+  }
   const uint32_t G = stream_blocks(tables, k_bits);
   const uint32_t base = G / tables;  // smallest ranges per table
   const uint32_t range = ((1u << k_bits) + base - 1u) / base + 4u;
   const size_t smem = n ? 2u * sizeof(uint32_t) * ((range + 3u) & ~3u) : 0;
-  cudaError_t e = set_smem_once(reinterpret_cast<const void*>(stream_apply_kernel), 210 * 1024, 1);
-  if (e != cudaSuccess) return e;
+  if ((e = set_smem_once(reinterpret_cast<const void*>(stream_apply_kernel), 210 * 1024, 1)) != cudaSuccess) return e;
   stream_apply_kernel<<<G, 1024, smem, s>>>(a);
   count_launch();
   return cudaGetLastError();
