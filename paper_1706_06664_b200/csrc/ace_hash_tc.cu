@@ -275,16 +275,6 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
           const uint32_t bytes = ((min(TW, R - j * TW) + 15u) & ~15u) * 128u;  // rows of the MMA's N
           for (uint32_t kc = 0; kc < a.nkc; ++kc) {
             mbar_wait_sleepy(&bar_wempty[s], ph ^ 1u);
-#ifdef ACE_EXP_WONCE
-            if (it > 0) {
-              mbar_arrive(&bar_wfull[s]);
-              if (++s == L.n_wst) {
-                s = 0;
-                ph ^= 1u;
-              }
-              continue;
-            }
-#endif
             mbar_expect_tx(&bar_wfull[s], 2u * bytes);
             const uint8_t* src = reinterpret_cast<const uint8_t*>(a.w16) + (static_cast<uint64_t>(j) * a.nkc + kc) * 2u * wblk;
             uint8_t* dst = Wsm + static_cast<size_t>(s) * 2u * wblk;
@@ -393,14 +383,9 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
       const uint64_t row = tile_of(itp) * kRows + r;
       const bool valid = row < a.n;
       uint32_t* idp = a.ids + row;
-#ifdef ACE_EXP_NOPACK
-      if (valid && row == 0xffffffffull) idp[0] = 0u;
-      for (uint32_t t0 = 0; t0 < 0u; t0 += 8u) {
-#else
       // eight tables at a time: all sixteen word loads in flight first (a
       // table needs the next word only if it straddles, which then exists)
       for (uint32_t t0 = 0; t0 < a.tables; t0 += 8u) {
-#endif
         uint32_t bk[8];
 #pragma unroll
         for (uint32_t u = 0; u < 8u; ++u) {
@@ -412,11 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
 #pragma unroll
         for (uint32_t u = 0; u < 8u; ++u) {
           const uint32_t tt = t0 + u;
-#ifndef ACE_EXP_NOSTORE
           if (valid && tt < a.tables) idp[static_cast<uint64_t>(tt) * a.ids_ld] = bk[u];
-#else
-          if (valid && tt < a.tables && bk[u] == 0xfffffffeu) idp[0] = bk[u];
-#endif
           if (a.fused_insert && tt < a.tables)
             insert_bucket_warp(a.counters + (static_cast<uint64_t>(tt) << K), bk[u], valid, lane);
         }
@@ -494,11 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
       TCP_BEGIN();
       // every converter has read the raw tile: warp 10 loads the next one
       asm volatile("bar.sync %0, 128;" ::"r"(kConvBar) : "memory");
-#ifdef ACE_EXP_NORAW
-      if (warp == 10 && lane == 0 && it + 1 < my_tiles) mbar_arrive(&bar_rawfull);
-#else
       if (warp == 10 && lane == 0 && it + 1 < my_tiles) issue_raw(tile_of(it + 1));
-#endif
       thr_sm[p][r] = row_threshold(rs, live, ss, a.dim, a.margin_c);
       lob = __reduce_or_sync(0xffffffffu, lob);
       if (lane == 0) lom_sm[b][q] = lob;
