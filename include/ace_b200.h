@@ -147,7 +147,11 @@ ace_status ace_sketch_set_stream(AceSketch* sk, void* cuda_stream);
 enum { ACE_OPT_H2D_CHUNKS = 1, ACE_OPT_DEFER_INSERT = 2, ACE_OPT_STREAM_GROUP = 3 };
 ace_status ace_sketch_set_option(AceSketch* sk, int option, int64_t value);
 
-/* AceSketch::insert (sketch.cpp:50-72) for n rows, in row order. */
+/* AceSketch::insert (sketch.cpp:50-72) for n rows, in row order.
+ * A few host rows (n <= 32, n * dim * size <= 3 KB) of a 32-bit sketch with
+ * stats == NULL take the per-point path: one kernel launch carrying the rows
+ * by value, and the call returns without waiting (every later call on the
+ * sketch is ordered after it; x may be reused at once). */
 ace_status ace_sketch_insert(AceSketch* sk, const void* x, int dtype, uint64_t n,
                              uint64_t ld, int x_where, AceHashStats* stats);
 /* Insert / score n points given by their bucket ids (L x n, table-major,
@@ -166,6 +170,16 @@ ace_status ace_sketch_remove(AceSketch* sk, const void* x, int dtype, uint64_t n
 ace_status ace_sketch_score(AceSketch* sk, const void* x, int dtype, uint64_t n,
                             uint64_t ld, int x_where, double* scores,
                             uint64_t* sums, int out_where, AceHashStats* stats);
+/* detect_stream (detect.cpp:76-84) for each of n queries against the
+ * current sketch (nothing inserted): scores[i] (host, may be NULL) and
+ * flags[i] = scores[i] <= mean - alpha (host bytes, may be NULL).
+ * alpha < 0 or an empty sketch is ACE_E_CONTRACT, checked in the
+ * reference's order.  A few host queries take the per-point path (one
+ * launch, results in mapped host memory, one wait). */
+ace_status ace_sketch_detect_stream(AceSketch* sk, const void* q, int dtype,
+                                    uint64_t n, uint64_t ld, int q_where,
+                                    double alpha, double* scores,
+                                    uint8_t* flags);
 /* detect_batch (detect.cpp:12-74): score every row against the current
  * counts, mean / population stddev, flag score < mean - stddev.
  * flag_bits ((n+31)/32 words) and scores may be NULL. */
@@ -209,6 +223,9 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype,
 /* State (sketch.hpp:44-69). */
 ace_status ace_sketch_info(const AceSketch* sk, uint64_t* n, double* mean,
                            int* saturated);
+/* One counter (AceSketch::counter): a 4-byte device read. */
+ace_status ace_sketch_counter(const AceSketch* sk, uint32_t table,
+                              uint64_t bucket, uint64_t* value);
 /* counters: L * 2^K values, array-major (counters_flat), host memory. */
 ace_status ace_sketch_counters(const AceSketch* sk, uint64_t* counters);
 ace_status ace_sketch_counters_u32(const AceSketch* sk, uint32_t* counters,

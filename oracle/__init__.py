@@ -201,6 +201,8 @@ class Reference:
         L.ref_time_build_detect.restype = _i
         L.ref_time_build_detect.argtypes = [_u64, _vp, _u64, _u64, _u32, _u32, C.c_uint, _P(_d),
                                             _P(_d), _P(_u64)]
+        L.ref_time_point.restype = _i
+        L.ref_time_point.argtypes = [_u64, _vp, _u64, _u64, _u64, _u32, _u32, _d, _P(_d), _P(_u64), _vp, _vp]
         L.ref_time_stream.restype = _i
         L.ref_time_stream.argtypes = [_u64, _vp, _u64, _u64, _u32, _u32, _u64, _d, C.c_uint, _P(_d), _P(_d),
                                       _P(_u64)]
@@ -322,6 +324,20 @@ class Reference:
         self._ok(self.L.ref_time_stream(seed, x.ctypes.data, n, dim, k, l, batch, alpha, threads, C.byref(ts),
                                         C.byref(ti), C.byref(rep)))
         return ts.value, ti.value, rep.value
+
+    def time_point(self, seed, x, n_build, k, l, alpha, outputs=False):
+        """(seconds, reported[, scores, flags]) of the per-point loop
+        detect_stream + insert over rows n_build.. of x (ace_cli stream
+        --adapt), after an untimed build from the first n_build rows."""
+        x = _f32(x)
+        n, dim = x.shape
+        q = n - n_build
+        sec, rep = _d(), _u64()
+        sc = np.empty(q, dtype=np.float64) if outputs else None
+        fl = np.empty(q, dtype=np.uint8) if outputs else None
+        self._ok(self.L.ref_time_point(seed, x.ctypes.data, n_build, q, dim, k, l, alpha, C.byref(sec), C.byref(rep),
+                                       sc.ctypes.data if outputs else None, fl.ctypes.data if outputs else None))
+        return (sec.value, rep.value, sc, fl) if outputs else (sec.value, rep.value)
 
 
 class RefSketch:

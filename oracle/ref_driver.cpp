@@ -365,6 +365,39 @@ int ref_time_stream(uint64_t seed, const float* x, uint64_t n, uint64_t dim, uin
   }
 }
 
+// Per-point API baseline in ace_cli stream --adapt's order (ace_cli.cpp:
+// 173-183): a sketch built from the first n_build rows (untimed), then for
+// each of the next n_query rows detect_stream (detect.cpp:76-84) followed by
+// insert (sketch.cpp:50-72), one call at a time on one core.  Seconds of the
+// query loop; scores / flags optional.
+int ref_time_point(uint64_t seed, const float* x, uint64_t n_build, uint64_t n_query, uint64_t dim,
+                   uint32_t k, uint32_t l, double alpha, double* seconds, uint64_t* reported,
+                   double* scores, uint8_t* flags) {
+  try {
+    const ace::SrpFamily fam(make_cfg(dim, k, l, seed));
+    ace::AceSketch s(fam, ace::CounterWidth::k32);
+    std::vector<double> xd((n_build + n_query) * dim);
+    for (uint64_t i = 0; i < xd.size(); ++i) xd[i] = static_cast<double>(x[i]);
+    for (uint64_t i = 0; i < n_build; ++i) s.insert(std::span<const double>(xd.data() + i * dim, dim));
+    uint64_t rep = 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (uint64_t i = n_build; i < n_build + n_query; ++i) {
+      std::span<const double> r(xd.data() + i * dim, dim);
+      const auto [est, flag] = ace::detect_stream(s, r, alpha);
+      if (scores) scores[i - n_build] = est.value;
+      if (flags) flags[i - n_build] = flag ? 1 : 0;
+      rep += flag ? 1 : 0;
+      s.insert(r);
+    }
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *reported = rep;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // ACE1 sketch files through the reference's io (io.cpp:184-244): 0 ok,
 // -3 DataError (message in ref_last_error), -1 other.
 int ref_save_sketch(void* h, const char* path) {

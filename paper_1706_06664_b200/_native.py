@@ -74,6 +74,8 @@ ABI = {
                                      _P(AceStreamReport), _P(AceHashStats)]),
     "ace_sketch_stream_run": (_i, [_vp, _vp, _i, _u64, _u64, _i, _u64, _d, _vp, _i, _vp,
                                    _P(AceStreamReport), _P(AceHashStats)]),
+    "ace_sketch_detect_stream": (_i, [_vp, _vp, _i, _u64, _u64, _i, _d, _vp, _vp]),
+    "ace_sketch_counter": (_i, [_vp, _u32, _u64, _P(_u64)]),
     "ace_sketch_info": (_i, [_vp, _P(_u64), _P(_d), _P(_i)]),
     "ace_sketch_counters": (_i, [_vp, _vp]),
     "ace_sketch_counters_u32": (_i, [_vp, _vp, _i]),

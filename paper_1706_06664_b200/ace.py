@@ -65,6 +65,9 @@ def _check(status: int) -> None:
 
 # ------------------------------------------------------------- helpers ------
 
+POINT_MAX_ROWS = 32  # per-point path (include/ace_b200.h, ace_sketch_insert)
+
+
 class _Points:
     """A point matrix as (pointer, dtype, n, ld, where) + keepalive."""
 
@@ -369,6 +372,11 @@ class AceSketch:
             _check(N.dev().ace_sketch_insert_ids(self._h, ids.ctypes.data, ids.shape[1], N.ACE_HOST))
             return
         p = _Points(x, self._dim())
+        if p.n <= POINT_MAX_ROWS and p.where == N.ACE_HOST:
+            # a few host rows: the per-point path (one launch, no wait; no stats)
+            self.last_stats = N.AceHashStats()
+            _check(N.dev().ace_sketch_insert(self._h, p.ptr, p.dtype, p.n, p.ld, p.where, None))
+            return
         _check(N.dev().ace_sketch_insert(self._h, p.ptr, p.dtype, p.n, p.ld, p.where,
                                          C.byref(self.last_stats)))
 
@@ -466,7 +474,9 @@ class AceSketch:
         cfg = self._family.config()
         if table >= cfg.num_tables or bucket >= (1 << cfg.k_bits) or table < 0 or bucket < 0:
             raise ContractViolation("AceSketch: counter index out of range")
-        return int(self.counters_u32()[(table << cfg.k_bits) + bucket])
+        v = C.c_uint64()
+        _check(N.dev().ace_sketch_counter(self._h, table, bucket, C.byref(v)))
+        return int(v.value)
 
     @classmethod
     def restore(cls, family: SrpFamily, width: CounterWidth, counters, n: int, mean: float,
@@ -655,10 +665,18 @@ def detect_stream(sketch: AceSketch, q, alpha: float):
     """detect_stream (detect.cpp:76-84): (ScoreEstimate, score <= mean - alpha)."""
     if alpha < 0.0:
         raise ContractViolation("detect_stream: alpha must be >= 0")
-    if sketch.size() == 0:
-        raise ContractViolation("detect_stream: empty sketch")
-    est = sketch.score(q)
-    return est, est.value <= sketch.mean() - alpha
+    cfg = sketch.family().config()
+    qa = np.asarray(q)
+    if cfg.noise_scale > 0 or qa.ndim != 1 or qa.shape[0] != cfg.dim:
+        if sketch.size() == 0:
+            raise ContractViolation("detect_stream: empty sketch")
+        est = sketch.score(q)
+        return est, est.value <= sketch.mean() - alpha
+    p = _Points(qa, cfg.dim)
+    v, f = C.c_double(), C.c_uint8()
+    _check(N.dev().ace_sketch_detect_stream(sketch._h, p.ptr, p.dtype, 1, p.ld, p.where, float(alpha),
+                                            C.byref(v), C.byref(f)))
+    return ScoreEstimate(v.value, cfg.k_bits, cfg.num_tables), bool(f.value)
 
 
 # ------------------------------------------------------------ estimators -----

@@ -82,6 +82,17 @@ def build_cpp_test(force: bool = False) -> Path:
     return out
 
 
+def build_point_bench(force: bool = False) -> Path:
+    """The per-point API timing program (tests/cpp/point_bench.cpp) against
+    include/ace/*.hpp + libace.so; driven by bench.py --api point."""
+    out = LIB / "ace_point_bench"
+    src = ROOT / "tests" / "cpp" / "point_bench.cpp"
+    if src.exists() and (force or _stale(out, [src, LIB / "libace.so", *INC.glob("ace/*.hpp")])):
+        _run(["g++", "-std=c++20", "-O2", f"-I{INC}", "-o", str(out), str(src), f"-L{LIB}", "-lace",
+              "-lace_dev", "-Wl,-rpath,$ORIGIN"])
+    return out
+
+
 def build_oracle() -> None:
     """C restatement always; the reference build only where its sources exist."""
     _run(["make", "-C", str(ROOT / "oracle"), "oracle"])
@@ -95,6 +106,7 @@ def build_all(force: bool = False) -> None:
     build_host(force)
     build_datagen(force)
     build_cpp_test(force)
+    build_point_bench(force)
     build_oracle()
 
 

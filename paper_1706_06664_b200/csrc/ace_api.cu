@@ -77,6 +77,7 @@ struct AceFamily {
   FamilyDev d{};
   double noise_scale = 0.0;  // > 0: noisy variant, hashed only through the *_noisy / *_ids entry points
   TcFamily tc{};
+  double* w64t = nullptr;  // per-point path: W transposed (dim x rows), dims the point kernel takes
   int kernel = 0;  // 0 auto, 1 SIMT, 2 tcgen05
   float margin_c = 0.f;
   std::atomic<int> refs{1};
@@ -96,6 +97,26 @@ struct AceSketch {
   uint32_t* counters = nullptr;
   DevState* st = nullptr;    // device
   DevState* hst = nullptr;   // pinned host mirror
+  // per-point path (point_kernel): host-mapped results, the ids of the last
+  // point score (kPointMaxRows x L words), and the rows inserted
+  // asynchronously since the host mirror was last refreshed
+  struct PointHost {
+    double scores[kPointMaxRows];
+    unsigned long long sums[kPointMaxRows];
+    unsigned long long snap[2];
+    uint32_t counter;  // ace_sketch_counter
+  };
+  PointHost* pth = nullptr;
+  uint32_t* pbits = nullptr;  // [kPointMaxRows * L] ids of the last point score
+  unsigned long long pending_rows = 0;
+  std::vector<unsigned char> pcache_x;  // rows (dense) whose ids the last point score left in the cache
+  uint64_t pcache_n = 0;
+  int pcache_dtype = 0;
+  bool pcache_valid = false;
+  // insert(q) right after a point score of q: deferred (no launch) and
+  // applied from the cached ids by the next point kernel, or by
+  // flush_point() before any other work is queued on the sketch
+  uint32_t pins_pend = 0;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   // chunked host-input pipeline (batch_detect): H2D copies on their own
@@ -205,6 +226,7 @@ void family_release(AceFamily* f) {
     cudaFree(f->d.w32t);
     cudaFree(f->d.wnorm);
     cudaFree(f->d.wnorm64);
+    cudaFree(f->w64t);
     tc_free_family(&f->tc);
     delete f;
   }
@@ -270,9 +292,18 @@ cudaError_t zero_call_fields(AceSketch* sk) {
   return cudaMemsetAsync(base + off, 0, end - off, sk->stream);
 }
 
+ace_status flush_point(const AceSketch* sk);
+#define ACE_FLUSH(sk)                       \
+  do {                                      \
+    const ace_status fr_ = flush_point(sk); \
+    if (fr_ != ACE_OK) return fr_;          \
+  } while (0)
+
 ace_status pull_state(AceSketch* sk) {
+  ACE_FLUSH(sk);
   ACE_CUDA(cudaMemcpyAsync(sk->hst, sk->st, sizeof(DevState), cudaMemcpyDeviceToHost, sk->stream));
   ACE_CUDA(cudaStreamSynchronize(sk->stream));
+  sk->pending_rows = 0;
   return ACE_OK;
 }
 
@@ -300,7 +331,7 @@ ace_status copy_out(void* dst, const void* src, size_t bytes, int where, cudaStr
 // insert merge may skip the pre-add values and recompute T = sum c^2; T (a
 // u64, at most L n^2 when every point shares one bucket) must not wrap either.
 bool fire_and_forget_ok(const AceSketch* sk, uint64_t n) {
-  const unsigned long long tot = sk->hst->n + n;
+  const unsigned long long tot = sk->hst->n + sk->pending_rows + n;
   const unsigned __int128 worst = static_cast<unsigned __int128>(tot) * tot * sk->fam->d.tables;
   return sk->width == 32 && !sk->hst->saturated && tot < 0xffffffffull && (worst >> 64) == 0;
 }
@@ -308,6 +339,108 @@ bool fire_and_forget_ok(const AceSketch* sk, uint64_t n) {
 // The barrier-free stream kernel (stream_apply_kernel): 32-bit unsaturable
 // sketches with K <= 16; others score, insert and cap with separate kernels.
 bool stream_apply_ok(const AceSketch* sk, bool ff) { return ff && sk->width == 32 && sk->fam->d.k_bits <= 16; }
+
+// The per-point kernel takes up to kPointMaxRows host rows of a noise-free
+// family by value in its launch parameters.
+bool point_ok(const AceSketch* sk, int dtype, uint64_t n, int where) {
+  const size_t esz = dtype == ACE_F64 ? 8 : 4;
+  return sk->pth && sk->fam->w64t && where == ACE_HOST && n >= 1 && n <= kPointMaxRows &&
+         sk->fam->noise_scale == 0.0 && n * sk->fam->d.dim * esz <= kPointXBytes &&
+         n * sk->fam->d.tables <= 12288;  // the ids fit CTA 0's default shared memory
+}
+
+// The last point score hashed exactly these rows (its ids are in the cache).
+bool point_cached(const AceSketch* sk, const void* x, int dtype, uint64_t n, uint64_t ld) {
+  if (!sk->pcache_valid || sk->pcache_dtype != dtype || sk->pcache_n != n) return false;
+  const size_t esz = dtype == ACE_F64 ? 8 : 4, row = sk->fam->d.dim * esz;
+  for (uint64_t i = 0; i < n; ++i)
+    if (memcmp(sk->pcache_x.data() + i * row, static_cast<const unsigned char*>(x) + i * ld * esz, row) != 0)
+      return false;
+  return true;
+}
+
+template <uint32_t XB>
+ace_status run_point_t(AceSketch* sk, const void* x, int dtype, uint64_t n, uint64_t ld, int insert) {
+  const AceFamily* f = sk->fam;
+  PointArgs<XB> a;
+  PointHdr& h = a.h;
+  h.w64t = f->w64t;
+  h.dim = f->d.dim;
+  h.k_bits = f->d.k_bits;
+  h.tables = f->d.tables;
+  h.rows = f->d.rows;
+  h.n = static_cast<uint32_t>(n);
+  h.x_f64 = dtype == ACE_F64;
+  h.counters = sk->counters;
+  h.st = sk->st;
+  h.cache = sk->pbits;
+  h.scores = sk->pth->scores;
+  h.sums = sk->pth->sums;
+  h.snap = sk->pth->snap;
+  const size_t esz = h.x_f64 ? 8 : 4, row = f->d.dim * esz, bytes = n * row;
+  for (uint64_t i = 0; i < n; ++i)
+    memcpy(a.x + i * row, static_cast<const unsigned char*>(x) + i * ld * esz, row);
+  // an insert of the rows the last score hashed reuses their ids (the
+  // per-point loop detect_stream(q); insert(q)): bucket ids depend on the
+  // rows and the family only
+  const bool cached = insert && !sk->pins_pend && point_cached(sk, x, dtype, n, ld);
+  h.mode = insert ? (cached ? kPointInsertCached : kPointInsert) : kPointScore;
+  h.pend_n = 0;
+  if (!insert) {  // a deferred insert rides along, applied before the gather
+    h.pend_n = sk->pins_pend;
+    sk->pins_pend = 0;
+  } else {
+    ACE_FLUSH(sk);
+  }
+  sk->pcache_valid = false;
+  ACE_CUDA(launch_point(a, sk->stream));
+  if (!insert) {
+    sk->pcache_x.assign(a.x, a.x + bytes);
+    sk->pcache_n = n;
+    sk->pcache_dtype = dtype;
+    sk->pcache_valid = true;
+  }
+  return ACE_OK;
+}
+
+// One point_kernel launch over host rows x (insert: 32-bit unsaturable
+// sketches, see fire_and_forget_ok).  Asynchronous; results land in sk->pth.
+ace_status run_point(AceSketch* sk, const void* x, int dtype, uint64_t n, uint64_t ld, int insert) {
+  const size_t esz = dtype == ACE_F64 ? 8 : 4;
+  if (n * sk->fam->d.dim * esz <= kPointXSmall) return run_point_t<kPointXSmall>(sk, x, dtype, n, ld, insert);
+  return run_point_t<kPointXBytes>(sk, x, dtype, n, ld, insert);
+}
+
+// Apply a deferred point insert before other work is queued on the sketch.
+ace_status flush_point(const AceSketch* csk) {
+  AceSketch* sk = const_cast<AceSketch*>(csk);
+  if (!sk->pins_pend) return ACE_OK;
+  PointArgs<kPointXSmall> a;
+  PointHdr& h = a.h;
+  h = PointHdr{};
+  h.k_bits = sk->fam->d.k_bits;
+  h.tables = sk->fam->d.tables;
+  h.rows = sk->fam->d.rows;
+  h.n = sk->pins_pend;
+  h.mode = kPointInsertCached;
+  h.counters = sk->counters;
+  h.st = sk->st;
+  h.cache = sk->pbits;
+  h.snap = sk->pth->snap;
+  sk->pins_pend = 0;
+  ACE_CUDA(launch_point(a, sk->stream));
+  return ACE_OK;
+}
+
+// Wait for a point_kernel score; the host mirror takes its n and T (the only
+// state an unsaturable insert changes).
+ace_status finish_point_score(AceSketch* sk) {
+  ACE_CUDA(cudaStreamSynchronize(sk->stream));
+  sk->hst->n = sk->pth->snap[0];
+  sk->hst->T = sk->pth->snap[1];
+  sk->pending_rows = 0;
+  return ACE_OK;
+}
 
 
 ace_status ensure_stream_bufs(AceSketch* sk, uint64_t rows) {
@@ -571,6 +704,17 @@ ace_status ace_family_create(uint64_t dim, uint32_t k_bits, uint32_t num_tables,
     return fail(e == cudaErrorMemoryAllocation ? ACE_E_NOMEM : ACE_E_CUDA,
                 std::string("ace_family_create: ") + cudaGetErrorString(e));
   }
+  if (dim * sizeof(float) <= kPointXBytes) {  // a row fits the per-point kernel's parameters
+    std::vector<double> wt(static_cast<size_t>(d.rows) * dim);
+    for (uint64_t r = 0; r < d.rows; ++r)
+      for (uint64_t i = 0; i < dim; ++i) wt[i * d.rows + r] = w_host[r * dim + i];
+    if ((e = cudaMalloc(&f->w64t, sizeof(double) * wt.size())) != cudaSuccess ||
+        (e = cudaMemcpy(f->w64t, wt.data(), sizeof(double) * wt.size(), cudaMemcpyHostToDevice)) != cudaSuccess) {
+      cleanup();
+      return fail(e == cudaErrorMemoryAllocation ? ACE_E_NOMEM : ACE_E_CUDA,
+                  std::string("ace_family_create: ") + cudaGetErrorString(e));
+    }
+  }
   if ((e = launch_wnorm64(d.w64, d.dim, d.rows, d.wnorm64)) != cudaSuccess) {
     cleanup();
     return fail(ACE_E_CUDA, std::string("ace_family_create: ") + cudaGetErrorString(e));
@@ -712,13 +856,21 @@ ace_status sketch_create(AceFamily* fam, uint32_t counter_width, AceSketch** out
   if ((e = cudaStreamCreateWithFlags(&sk->own, cudaStreamNonBlocking)) != cudaSuccess ||
       (counters && (e = cudaMalloc(&sk->counters, sk->num_counters * sizeof(uint32_t))) != cudaSuccess) ||
       (e = cudaMalloc(&sk->st, sizeof(DevState))) != cudaSuccess ||
-      (e = cudaMallocHost(&sk->hst, sizeof(DevState))) != cudaSuccess) {
+      (e = cudaMallocHost(&sk->hst, sizeof(DevState))) != cudaSuccess ||
+      (counters && (e = cudaHostAlloc(&sk->pth, sizeof(AceSketch::PointHost), cudaHostAllocMapped)) != cudaSuccess) ||
+      (counters && (e = cudaMalloc(&sk->pbits, kPointMaxRows * fam->d.tables * sizeof(uint32_t))) != cudaSuccess)) {
     ace_sketch_destroy(sk);
     return fail(e == cudaErrorMemoryAllocation ? ACE_E_NOMEM : ACE_E_CUDA,
                 std::string("ace_sketch_create: ") + cudaGetErrorString(e));
   }
   sk->stream = sk->own;
   memset(sk->hst, 0, sizeof(DevState));
+  if (sk->pbits &&
+      (e = cudaMemsetAsync(sk->pbits, 0, kPointMaxRows * fam->d.tables * sizeof(uint32_t), sk->stream)) !=
+          cudaSuccess) {
+    ace_sketch_destroy(sk);
+    return fail(ACE_E_CUDA, std::string("ace_sketch_create: ") + cudaGetErrorString(e));
+  }
   ace_status r = ace_sketch_reset(sk);
   if (r != ACE_OK) {
     ace_sketch_destroy(sk);
@@ -736,11 +888,14 @@ ace_status ace_sketch_reset(AceSketch* sk) {
   if (sk->num_counters) ACE_CUDA(cudaMemsetAsync(sk->counters, 0, sk->num_counters * sizeof(uint32_t), sk->stream));
   ACE_CUDA(cudaMemsetAsync(sk->st, 0, sizeof(DevState), sk->stream));
   memset(sk->hst, 0, sizeof(DevState));
+  sk->pending_rows = 0;
+  sk->pins_pend = 0;
   return ACE_OK;
 }
 
 ace_status ace_sketch_clone(const AceSketch* src, AceSketch** out) {
   if (!src || !out) return fail(ACE_E_CONTRACT, "ace_sketch_clone: null argument");
+  ACE_FLUSH(src);
   ace_status r = ace_sketch_create(src->fam, src->width, out);
   if (r != ACE_OK) return r;
   AceSketch* d = *out;
@@ -774,6 +929,8 @@ ace_status ace_sketch_destroy(AceSketch* sk) {
   if (sk->counters) cudaFree(sk->counters);
   if (sk->st) cudaFree(sk->st);
   if (sk->hst) cudaFreeHost(sk->hst);
+  if (sk->pth) cudaFreeHost(sk->pth);
+  if (sk->pbits) cudaFree(sk->pbits);
   if (sk->own) cudaStreamDestroy(sk->own);
   sk->sstage[0].release();
   sk->sstage[1].release();
@@ -797,6 +954,7 @@ ace_status ace_sketch_destroy(AceSketch* sk) {
 
 ace_status ace_sketch_set_stream(AceSketch* sk, void* cuda_stream) {
   if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_set_stream: null sketch");
+  ACE_FLUSH(sk);
   ACE_CUDA(cudaStreamSynchronize(sk->stream));
   sk->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : sk->own;
   return ACE_OK;
@@ -831,6 +989,21 @@ ace_status ace_sketch_insert(AceSketch* sk, const void* x, int dtype, uint64_t n
   ace_status r = check_x(sk->fam, x, dtype, n, ld, x_where);
   if (r != ACE_OK) return r;
   sk->mean_pinned = false;
+  if (!stats && point_ok(sk, dtype, n, x_where) && fire_and_forget_ok(sk, n)) {
+    // a few host rows, no stats asked: one launch, no wait (stream-ordered
+    // before every later call on the sketch; the rows travel by value) --
+    // or none, when the last point score hashed exactly these rows
+    if (!sk->pins_pend && point_cached(sk, x, dtype, n, ld)) {
+      sk->pins_pend = static_cast<uint32_t>(n);
+      sk->pcache_valid = false;
+      sk->pending_rows += n;
+      return ACE_OK;
+    }
+    r = run_point(sk, x, dtype, n, ld, 1);
+    if (r == ACE_OK) sk->pending_rows += n;
+    return r;
+  }
+  ACE_FLUSH(sk);
   ACE_CUDA(zero_call_fields(sk));
   const void* xd;
   uint64_t ldd;
@@ -866,6 +1039,7 @@ ace_status stage_ids(AceSketch* sk, const uint32_t* ids, uint64_t n, int where, 
 // (sketch.cpp:55-71) without hashing.
 ace_status ace_sketch_insert_ids(AceSketch* sk, const uint32_t* ids, uint64_t n, int where) {
   if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_insert_ids: null sketch");
+  ACE_FLUSH(sk);
   if (n == 0) return ACE_OK;
   const uint32_t* d = nullptr;
   ace_status r = stage_ids(sk, ids, n, where, &d);
@@ -883,6 +1057,7 @@ ace_status ace_sketch_insert_ids(AceSketch* sk, const uint32_t* ids, uint64_t n,
 ace_status ace_sketch_score_ids(AceSketch* sk, const uint32_t* ids, uint64_t n, int where, double* scores,
                                 uint64_t* sums, int out_where) {
   if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_score_ids: null sketch");
+  ACE_FLUSH(sk);
   if (n == 0) return ACE_OK;
   const uint32_t* d = nullptr;
   ace_status r = stage_ids(sk, ids, n, where, &d);
@@ -916,6 +1091,7 @@ ace_status ace_sketch_score_ids(AceSketch* sk, const uint32_t* ids, uint64_t n, 
 ace_status ace_sketch_remove(AceSketch* sk, const void* x, int dtype, uint64_t n, uint64_t ld,
                              int x_where, AceHashStats* stats) {
   if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_remove: null sketch");
+  ACE_FLUSH(sk);
   ace_status r = check_x(sk->fam, x, dtype, n, ld, x_where);
   if (r != ACE_OK) return r;
   if (n == 0) return ACE_OK;
@@ -951,6 +1127,13 @@ ace_status ace_sketch_score(AceSketch* sk, const void* x, int dtype, uint64_t n,
   ace_status r = check_x(sk->fam, x, dtype, n, ld, x_where);
   if (r != ACE_OK) return r;
   if (n == 0) return ACE_OK;
+  if (!stats && out_where == ACE_HOST && point_ok(sk, dtype, n, x_where)) {
+    if ((r = run_point(sk, x, dtype, n, ld, 0)) != ACE_OK || (r = finish_point_score(sk)) != ACE_OK) return r;
+    if (scores) memcpy(scores, sk->pth->scores, n * sizeof(double));
+    if (sums) memcpy(sums, sk->pth->sums, n * sizeof(uint64_t));
+    return ACE_OK;
+  }
+  ACE_FLUSH(sk);
   ACE_CUDA(zero_call_fields(sk));
   const void* xd;
   uint64_t ldd;
@@ -1131,6 +1314,7 @@ ace_status ace_sketch_detect_batch(AceSketch* sk, const void* x, int dtype, uint
                                    int x_where, uint32_t* flag_bits, double* scores, int out_where,
                                    AceBatchReport* report, AceHashStats* stats) {
   if (!sk) return fail(ACE_E_CONTRACT, "detect_batch: null sketch");
+  ACE_FLUSH(sk);
   if (n == 0) return fail(ACE_E_CONTRACT, "detect_batch: empty dataset");
   if (ld < sk->fam->d.dim) return fail(ACE_E_CONTRACT, "detect_batch: data dimension mismatch");
   ace_status r = check_x(sk->fam, x, dtype, n, ld, x_where);
@@ -1151,6 +1335,7 @@ ace_status ace_sketch_build_detect(AceSketch* sk, const void* x, int dtype, uint
                                    int x_where, uint32_t* flag_bits, double* scores, int out_where,
                                    AceBatchReport* report, AceHashStats* stats) {
   if (!sk) return fail(ACE_E_CONTRACT, "build_sketch: null sketch");
+  ACE_FLUSH(sk);
   if (n == 0) return fail(ACE_E_CONTRACT, "build_sketch: empty dataset");
   ace_status r = check_x(sk->fam, x, dtype, n, ld, x_where);
   if (r != ACE_OK) return r;
@@ -1170,6 +1355,7 @@ ace_status ace_sketch_stream_batch(AceSketch* sk, const void* x, int dtype, uint
                                    int x_where, double alpha, uint32_t* flag_bits, double* scores,
                                    int out_where, AceStreamReport* report, AceHashStats* stats) {
   if (!sk) return fail(ACE_E_CONTRACT, "detect_stream: null sketch");
+  ACE_FLUSH(sk);
   if (!(alpha >= 0.0)) return fail(ACE_E_CONTRACT, "detect_stream: alpha must be >= 0");
   ace_status r = check_x(sk->fam, x, dtype, n, ld, x_where);
   if (r != ACE_OK) return r;
@@ -1236,6 +1422,7 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
                                  uint64_t batch, double alpha, uint32_t* flag_bits, int out_where,
                                  float* batch_ms, AceStreamReport* report, AceHashStats* stats) {
   if (!sk) return fail(ACE_E_CONTRACT, "detect_stream: null sketch");
+  ACE_FLUSH(sk);
   if (!(alpha >= 0.0)) return fail(ACE_E_CONTRACT, "detect_stream: alpha must be >= 0");
   if (batch == 0 || batch % 32 != 0) return fail(ACE_E_CONTRACT, "stream_run: batch must be a positive multiple of 32");
   ace_status r = check_x(sk->fam, x, dtype, n, ld, x_where);
@@ -1458,6 +1645,53 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
   return ACE_OK;
 }
 
+// detect_stream (detect.cpp:76-84) for each of n queries against the current
+// sketch: score, flag = score <= mean - alpha.  Host outputs.
+ace_status ace_sketch_detect_stream(AceSketch* sk, const void* q, int dtype, uint64_t n, uint64_t ld, int q_where,
+                                    double alpha, double* scores, uint8_t* flags) {
+  if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_detect_stream: null sketch");
+  if (alpha < 0.0) return fail(ACE_E_CONTRACT, "detect_stream: alpha must be >= 0");
+  ace_status r = check_x(sk->fam, q, dtype, n, ld, q_where);
+  if (r != ACE_OK) {
+    // the reference reports an empty sketch before it scores (detect.cpp:80-81)
+    const std::string msg = g_err;
+    if (pull_state(sk) == ACE_OK && sk->hst->n == 0) return fail(ACE_E_CONTRACT, "detect_stream: empty sketch");
+    return fail(r, msg);
+  }
+  if (n == 0) return ACE_OK;
+  std::vector<double> tmp;
+  double* sc = scores;
+  if (!sc) {
+    tmp.resize(n);
+    sc = tmp.data();
+  }
+  if (point_ok(sk, dtype, n, q_where)) {
+    if ((r = run_point(sk, q, dtype, n, ld, 0)) != ACE_OK || (r = finish_point_score(sk)) != ACE_OK) return r;
+    memcpy(sc, sk->pth->scores, n * sizeof(double));
+  } else if ((r = ace_sketch_score(sk, q, dtype, n, ld, q_where, sc, nullptr, ACE_HOST, nullptr)) != ACE_OK) {
+    return r;
+  }
+  if (sk->hst->n == 0) return fail(ACE_E_CONTRACT, "detect_stream: empty sketch");
+  const double mean = sk->mean_pinned ? sk->pinned_mean : host_mean(*sk->hst, sk->fam->d.tables);
+  if (flags)
+    for (uint64_t i = 0; i < n; ++i) flags[i] = sc[i] <= mean - alpha ? 1 : 0;
+  return ACE_OK;
+}
+
+// One counter (AceSketch::counter, sketch.hpp): a 4-byte read into pinned
+// memory, not the whole array.
+ace_status ace_sketch_counter(const AceSketch* sk, uint32_t table, uint64_t bucket, uint64_t* value) {
+  if (!sk || !value) return fail(ACE_E_CONTRACT, "ace_sketch_counter: null argument");
+  ACE_FLUSH(sk);
+  if (!sk->pth || table >= sk->fam->d.tables || bucket >= (1ull << sk->fam->d.k_bits))
+    return fail(ACE_E_CONTRACT, "AceSketch: counter index out of range");
+  const uint32_t* src = sk->counters + (static_cast<uint64_t>(table) << sk->fam->d.k_bits) + bucket;
+  ACE_CUDA(cudaMemcpyAsync(&sk->pth->counter, src, sizeof(uint32_t), cudaMemcpyDeviceToHost, sk->stream));
+  ACE_CUDA(cudaStreamSynchronize(sk->stream));
+  *value = sk->pth->counter;
+  return ACE_OK;
+}
+
 // size / mean / saturated (sketch.hpp:44-46).
 ace_status ace_sketch_info(const AceSketch* sk, uint64_t* n, double* mean, int* saturated) {
   if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_info: null sketch");
@@ -1473,6 +1707,7 @@ ace_status ace_sketch_info(const AceSketch* sk, uint64_t* n, double* mean, int* 
 // counters_flat (sketch.cpp:126-130).
 ace_status ace_sketch_counters(const AceSketch* sk, uint64_t* counters) {
   if (!sk || !counters) return fail(ACE_E_CONTRACT, "ace_sketch_counters: null argument");
+  ACE_FLUSH(sk);
   std::vector<uint32_t> tmp(sk->num_counters);
   ACE_CUDA(cudaMemcpyAsync(tmp.data(), sk->counters, sk->num_counters * sizeof(uint32_t),
                            cudaMemcpyDeviceToHost, sk->stream));
@@ -1483,6 +1718,7 @@ ace_status ace_sketch_counters(const AceSketch* sk, uint64_t* counters) {
 
 ace_status ace_sketch_counters_u32(const AceSketch* sk, uint32_t* counters, int where) {
   if (!sk || !counters) return fail(ACE_E_CONTRACT, "ace_sketch_counters_u32: null argument");
+  ACE_FLUSH(sk);
   ACE_CUDA(cudaMemcpyAsync(counters, sk->counters, sk->num_counters * sizeof(uint32_t),
                            where == ACE_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
                            sk->stream));
@@ -1494,6 +1730,7 @@ ace_status ace_sketch_counters_u32(const AceSketch* sk, uint32_t* counters, int 
 ace_status ace_sketch_restore(AceSketch* sk, const uint64_t* counters, uint64_t num_counters,
                               uint64_t n, double mean, int saturated) {
   if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_restore: null sketch");
+  ACE_FLUSH(sk);
   if (num_counters != sk->num_counters)
     return fail(ACE_E_CONTRACT, "AceSketch::restore: counter payload size " + std::to_string(num_counters) +
                                     " does not match L * 2^K = " + std::to_string(sk->num_counters));
@@ -1524,7 +1761,11 @@ ace_status ace_sketch_restore(AceSketch* sk, const uint64_t* counters, uint64_t 
   return ACE_OK;
 }
 
-const uint32_t* ace_sketch_device_counters(const AceSketch* sk) { return sk ? sk->counters : nullptr; }
+const uint32_t* ace_sketch_device_counters(const AceSketch* sk) {
+  if (!sk) return nullptr;
+  if (flush_point(sk) != ACE_OK) return nullptr;  // counters complete in the sketch's stream order
+  return sk->counters;
+}
 
 ace_status ace_sketch_set_timing(AceSketch* sk, int enable) {
   if (!sk) return fail(ACE_E_CONTRACT, "ace_sketch_set_timing: null sketch");

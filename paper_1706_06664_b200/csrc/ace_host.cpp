@@ -323,7 +323,9 @@ std::size_t AceSketch::counter_bytes() const {
 std::uint64_t AceSketch::counter(std::size_t table, std::size_t bucket) const {
   if (table >= family_.config().num_tables || bucket >= family_.num_buckets())
     throw ContractViolation("AceSketch: counter index out of range");
-  return counters_flat()[table * family_.num_buckets() + bucket];
+  std::uint64_t v = 0;
+  ok(ace_sketch_counter(dev_, static_cast<std::uint32_t>(table), bucket, &v));
+  return v;
 }
 
 std::vector<std::uint64_t> AceSketch::counters_flat() const {
@@ -399,9 +401,17 @@ std::pair<ScoreEstimate, bool> detect_stream(const AceSketch& sketch, std::span<
                                              double alpha) {
   // detect.cpp:79-83
   if (alpha < 0.0) throw ContractViolation("detect_stream: alpha must be >= 0");
-  if (sketch.size() == 0) throw ContractViolation("detect_stream: empty sketch");
-  const ScoreEstimate e = sketch.score(q);
-  return {e, e.value <= sketch.mean() - alpha};
+  const auto& c = sketch.family().config();
+  if (c.noise_scale > 0.0 || q.size() != c.dim) {
+    if (sketch.size() == 0) throw ContractViolation("detect_stream: empty sketch");
+    const ScoreEstimate e = sketch.score(q);
+    return {e, e.value <= sketch.mean() - alpha};
+  }
+  // one call: score on the device, flag against the state it saw
+  double v = 0.0;
+  std::uint8_t f = 0;
+  ok(ace_sketch_detect_stream(sketch.device(), q.data(), ACE_F64, 1, q.size(), ACE_HOST, alpha, &v, &f));
+  return {ScoreEstimate{v, c.k_bits, c.num_tables}, f != 0};
 }
 
 std::vector<std::uint8_t> stream_batch(AceSketch& sketch, std::span<const float> rows, std::size_t n,

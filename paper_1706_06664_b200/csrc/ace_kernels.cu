@@ -1918,6 +1918,181 @@ cudaError_t launch_stream_apply(const uint32_t* ids, uint64_t n, uint64_t ids_st
   return cudaGetLastError();
 }
 
+// ---- per-point path ----------------------------------------------------------
+
+// One cluster of kPointCtas CTAs: the (row, direction) folds spread over the
+// cluster, bucket bits OR-ed into CTA 0's shared memory over DSMEM, one
+// cluster barrier, then CTA 0 gathers / inserts.  No global ticket, no
+// bucket round trip through L2.
+constexpr uint32_t kPointCtas = 8;
+constexpr uint32_t kPointMaxThreads = 256;
+
+__device__ __forceinline__ void cluster_arrive_release() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait_acquire() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// The reference's left fold (srp.cpp:84) of one direction over a row held in
+// the launch parameters; W transposed so a warp's loads coalesce, up to 32
+// in flight ahead of the dependent adds.
+template <class X>
+__device__ __forceinline__ double point_fold(const double* __restrict__ wt, uint32_t rows, uint64_t dim,
+                                             const X* x) {
+  constexpr uint32_t U = 32;
+  double acc = 0.0;
+  uint64_t j = 0;
+  for (; j + U <= dim; j += U) {
+    double wv[U];
+#pragma unroll
+    for (uint32_t u = 0; u < U; ++u) wv[u] = __ldg(wt + (j + u) * rows);
+    __syncwarp();  // all U loads issued ahead of the dependent adds (one wait, not U)
+#pragma unroll
+    for (uint32_t u = 0; u < U; ++u) acc = __dadd_rn(acc, __dmul_rn(wv[u], static_cast<double>(x[j + u])));
+  }
+  if (j < dim) {  // remainder: loads clamped in range, folded under a predicate
+    double wv[U];
+#pragma unroll
+    for (uint32_t u = 0; u < U; ++u) wv[u] = __ldg(wt + min(j + u, dim - 1u) * rows);
+    __syncwarp();
+#pragma unroll
+    for (uint32_t u = 0; u < U; ++u)
+      if (j + u < dim) acc = __dadd_rn(acc, __dmul_rn(wv[u], static_cast<double>(x[j + u])));
+  }
+  return acc;
+}
+
+template <uint32_t XB>
+__global__ void __cluster_dims__(kPointCtas, 1, 1) __launch_bounds__(kPointMaxThreads)
+    point_kernel(const __grid_constant__ PointArgs<XB> a) {
+  extern __shared__ uint32_t sbits[];  // n x tables bucket ids (CTA 0's are the cluster's)
+  __shared__ unsigned long long S[kPointMaxRows];
+  __shared__ unsigned long long dT;
+  const PointHdr& h = a.h;
+  const uint32_t K = h.k_bits;
+  const uint32_t rank = blockIdx.x;  // one cluster: block index = rank
+  const uint32_t ne = h.n * h.tables;
+  const bool fold = h.mode != kPointInsertCached;
+  if (!fold && rank != 0) return;
+  // CTA 0: clear the ids, prefetch the state and the deferred insert's ids
+  unsigned long long n0 = 0, T0 = 0;
+  uint32_t pend_b = 0;
+  const bool fused = h.mode == kPointScore && h.pend_n == 1 && h.n == 1;  // detect_stream(q); insert(q); ...
+  if (rank == 0) {
+    for (uint32_t e = threadIdx.x; e < ne; e += blockDim.x) sbits[e] = 0u;
+    if (threadIdx.x < kPointMaxRows) S[threadIdx.x] = 0ull;
+    if (threadIdx.x == 0) {
+      dT = 0ull;
+      n0 = h.st->n;
+      T0 = h.st->T;
+    }
+    if (fused && threadIdx.x < h.tables) pend_b = h.cache[threadIdx.x];
+  }
+  if (fold) {
+    cluster_arrive_release();  // CTA 0's cleared ids, visible after the wait below
+    const uint32_t per = blockDim.x * kPointCtas;
+    uint32_t* dst = cg::this_cluster().map_shared_rank(sbits, 0u);
+    const uint32_t total = h.n * h.rows;
+    // warp-uniform trip count; every lane folds (a spare lane folds row 0,
+    // direction 0 and drops it): the fold's __syncwarp needs the whole warp
+    for (uint32_t q0 = rank * blockDim.x + (threadIdx.x & ~31u), first = 1; q0 < total || first; q0 += per) {
+      const uint32_t q = q0 + (threadIdx.x & 31u);
+      const bool live = q < total;
+      const uint32_t qq = live ? q : 0u;
+      const uint32_t i = qq / h.rows, r = qq - i * h.rows;
+      const double p = h.x_f64 ? point_fold(h.w64t + r, h.rows, h.dim,
+                                            reinterpret_cast<const double*>(a.x) + static_cast<uint64_t>(i) * h.dim)
+                               : point_fold(h.w64t + r, h.rows, h.dim,
+                                            reinterpret_cast<const float*>(a.x) + static_cast<uint64_t>(i) * h.dim);
+      if (first) {
+        cluster_wait_acquire();
+        first = 0;
+      }
+      if (live && p >= 0.0) {
+        const uint32_t t = r / K, b = r - t * K;
+        atomicOr(dst + i * h.tables + t, 1u << (K - 1u - b));  // MSB first, srp.cpp:86-90
+      }
+    }
+    cluster_arrive_release();
+    cluster_wait_acquire();
+    if (rank != 0) return;
+  } else {
+    __syncthreads();
+  }
+  // ---- CTA 0: deferred insert, gather (score) or insert, state
+  if (fused) {
+    // the deferred insert (ids in the cache) and this query's gather in one
+    // pass: a table whose two buckets coincide takes one atomic
+    if (threadIdx.x < h.tables) {
+      const uint32_t t = threadIdx.x, bn = sbits[t];
+      uint32_t* base = h.counters + (static_cast<uint64_t>(t) << K);
+      unsigned long long s;
+      uint32_t old;
+      if (bn == pend_b) {
+        old = atomicAdd(base + bn, 1u);
+        s = static_cast<unsigned long long>(old) + 1ull;
+      } else {
+        old = atomicAdd(base + pend_b, 1u);
+        s = __ldcg(base + bn);
+      }
+      h.cache[t] = bn;
+      atomicAdd(&dT, 2ull * old + 1ull);
+      atomicAdd(&S[0], s);
+    }
+  } else {
+    if (h.mode == kPointScore && h.pend_n) {  // the deferred insert, ahead of this score's gather
+      for (uint32_t e = threadIdx.x; e < h.pend_n * h.tables; e += blockDim.x) {
+        const uint32_t t = e % h.tables;
+        const uint32_t old = atomicAdd(h.counters + (static_cast<uint64_t>(t) << K) + h.cache[e], 1u);
+        atomicAdd(&dT, 2ull * old + 1ull);
+      }
+      __syncthreads();
+    }
+    for (uint32_t e = threadIdx.x; e < ne; e += blockDim.x) {
+      const uint32_t i = e / h.tables, t = e - i * h.tables;
+      const uint32_t bkt = h.mode == kPointInsertCached ? h.cache[e] : sbits[e];
+      if (h.mode == kPointScore) h.cache[e] = bkt;
+      uint32_t* c = h.counters + (static_cast<uint64_t>(t) << K) + bkt;
+      if (h.mode == kPointScore) {
+        atomicAdd(&S[i], static_cast<unsigned long long>(__ldcg(c)));
+      } else {
+        const uint32_t old = atomicAdd(c, 1u);  // sketch.cpp:55-71: T gains (c+1)^2 - c^2
+        atomicAdd(&dT, 2ull * old + 1ull);
+      }
+    }
+  }
+  __syncthreads();
+  if (h.mode == kPointScore && threadIdx.x < h.n) {
+    const unsigned long long v = S[threadIdx.x];
+    h.sums[threadIdx.x] = v;
+    h.scores[threadIdx.x] = __ddiv_rn(static_cast<double>(v), static_cast<double>(h.tables));  // sketch.cpp:108-116
+  }
+  if (threadIdx.x == 0) {
+    const uint32_t added = h.mode == kPointScore ? h.pend_n : h.n;
+    const unsigned long long n1 = n0 + added, T1 = T0 + dT;
+    if (added) {
+      h.st->T = T1;
+      h.st->n = n1;
+    }
+    h.snap[0] = n1;
+    h.snap[1] = T1;
+  }
+}
+
+template <uint32_t XB>
+cudaError_t launch_point(const PointArgs<XB>& a, cudaStream_t s) {
+  const uint32_t work = (a.h.n * a.h.rows + kPointCtas - 1u) / kPointCtas;
+  const uint32_t threads = std::max<uint32_t>(std::min<uint32_t>((work + 31u) & ~31u, kPointMaxThreads),
+                                              std::max<uint32_t>((a.h.tables + 31u) & ~31u, 64u));
+  const size_t smem = static_cast<size_t>(a.h.n) * a.h.tables * sizeof(uint32_t);
+  point_kernel<XB><<<kPointCtas, threads, smem, s>>>(a);
+  count_launch();
+  return cudaGetLastError();
+}
+template cudaError_t launch_point<kPointXSmall>(const PointArgs<kPointXSmall>&, cudaStream_t);
+template cudaError_t launch_point<kPointXBytes>(const PointArgs<kPointXBytes>&, cudaStream_t);
+
 cudaError_t launch_sum_squares(const uint32_t* counters, uint64_t num, unsigned long long* out,
                                cudaStream_t s) {
   sum_squares_kernel<<<grid_for(num, 256), 256, 0, s>>>(counters, num, out);

@@ -80,6 +80,41 @@ cudaError_t launch_stream_apply(const uint32_t* ids, uint64_t n, uint64_t ids_st
                                 uint64_t n_prev, uint32_t* flag_bits, double* scores, uint32_t slot_b, double alpha,
                                 DevState* st, cudaStream_t s);
 
+// Per-point path (AceSketch::insert / score / detect_stream one query at a
+// time, sketch.hpp:33,42, detect.hpp:34-36): up to kPointMaxRows rows passed
+// by value in the launch parameters (no staging copy); one cluster of CTAs
+// runs the exact binary64 folds (srp.cpp:78-113, one thread per (row,
+// direction), W transposed so loads coalesce) and ORs the bucket bits into
+// CTA 0's shared memory; CTA 0 then gathers (score: S_i into host-mapped
+// memory, the ids kept for an insert of the same rows) or inserts (c += 1,
+// T += 2c + 1, n += rows; 32-bit unsaturable sketches only) and snapshots n
+// and T into host-mapped memory.  One launch per call.
+constexpr uint32_t kPointMaxRows = 32;
+constexpr uint32_t kPointXBytes = 3072;   // rows by value: n * dim * sizeof(elem)
+constexpr uint32_t kPointXSmall = 512;    // a smaller parameter block when the rows fit
+enum { kPointScore = 0, kPointInsert = 1, kPointInsertCached = 2 };
+struct PointHdr {
+  const double* w64t;           // dim x rows: W transposed (binary64)
+  uint64_t dim;
+  uint32_t k_bits, tables, rows, n;
+  int x_f64;
+  int mode;                     // kPointScore / kPointInsert / kPointInsertCached
+  uint32_t pend_n;              // kPointScore: a deferred insert of the cached ids (rows) applied first
+  uint32_t* counters;
+  DevState* st;
+  uint32_t* cache;              // n x tables: ids of the last score (read by kPointInsertCached)
+  double* scores;               // host-mapped [n] (score)
+  unsigned long long* sums;     // host-mapped [n] (score)
+  unsigned long long* snap;     // host-mapped: n, T after the call
+};
+template <uint32_t XB>
+struct PointArgs {
+  PointHdr h;
+  alignas(16) unsigned char x[XB];  // n x dim, dense, fp32 or fp64
+};
+template <uint32_t XB>
+cudaError_t launch_point(const PointArgs<XB>& a, cudaStream_t s);
+
 // Sum of squares of all counters (T after restore with exact state).
 cudaError_t launch_sum_squares(const uint32_t* counters, uint64_t num,
                                unsigned long long* out, cudaStream_t s);
