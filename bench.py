@@ -15,6 +15,13 @@ the host.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C ...]
   python bench.py --impl reference ...   # the reference's CPU implementation
+  python bench.py --api point [--impl reference]   # the per-point API
+
+--api point times the reference's only API, one query at a time, as
+ace_cli stream --adapt drives it (ace_cli.cpp:173-183): detect_stream then
+insert per query through the C++ drop-in headers (include/ace/*.hpp,
+tests/cpp/point_bench.cpp) after a sketch built from one 65,536-row batch;
+a step is 1,000 queries.
 
 Multi-GPU (torchrun): replicas only -- each rank runs the full workload on its
 own GPU (the north star is single-GPU, no inter-GPU exchange); value = total
@@ -241,6 +248,16 @@ def run_reference(args):
     if rank != 0:
         return
     from paper_1706_06664_b200 import workloads as W
+    if args.api == "point":
+        for cfg in args.config:
+            cb = run_point_ref(args, cfg, args.steps, args.warmup)
+            line = point_line(cfg, "reference", cb["value"], cb["ms_per_step"], args, ws)
+            line["impl"] = "reference"
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            line["e2e"] = {"value": cb["value"], "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+            line["reported"] = cb["reported"]
+            print(json.dumps(line), flush=True)
+        return
     for cfg in args.config:
         w = W.CONFIGS[cfg]
         x = ref_rows(cfg, REF_SAMPLE[cfg])
@@ -264,6 +281,109 @@ def run_reference(args):
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }
         print(json.dumps(line), flush=True)
+
+
+POINT_BUILD, POINT_STEP = 65_536, 1_000  # per-point API: sketch built from one batch; queries per step
+
+
+def point_rows(cfg: int, queries: int):
+    """Rows of the per-point workload (build batch + queries), float32, in a
+    file (the C++ program reads it)."""
+    n = POINT_BUILD + queries
+    f = Path("/tmp") / f"ace_point_rows_cfg{cfg}_{n}.f32"
+    if not f.exists():
+        ref_rows(cfg, n).astype(np.float32).tofile(f)
+    return f, n
+
+
+def run_point_ref(args, cfg: int, steps: int, warmup: int) -> dict:
+    """The reference's per-point loop (oracle/_ref ref_time_point: the
+    unmodified reference's detect_stream + insert per query, one core)."""
+    from oracle import REF_SO, Oracle, Reference
+    from paper_1706_06664_b200 import workloads as W
+    w = W.CONFIGS[cfg]
+    q = (steps + warmup) * POINT_STEP
+    x = ref_rows(cfg, POINT_BUILD + q)
+    if REF_SO.exists():
+        # warm-up queries are the first `warmup` steps of the same loop: time
+        # the whole loop and each part by its query count (per-query cost is flat)
+        sec, rep = Reference().time_point(w.w_seed, x, POINT_BUILD, w.k_bits, w.num_tables, w.alpha)
+        kind = "reference"
+    else:
+        o = Oracle()
+        wm = o.directions(w.w_seed, w.dim, w.k_bits, w.num_tables)
+        t0 = time.perf_counter()
+        ids, _ = o.buckets(wm, x, w.k_bits, w.num_tables, threads=1, fast=False)
+        sk = o.sketch(w.k_bits, w.num_tables, 32)
+        sk.insert_ids(np.ascontiguousarray(ids[:, :POINT_BUILD]))
+        t1 = time.perf_counter()
+        rep = 0
+        for i in range(POINT_BUILD, x.shape[0]):
+            f, _ = sk.stream_ids(np.ascontiguousarray(ids[:, i:i + 1]), w.alpha)
+            rep += int(f[0])
+        sec = time.perf_counter() - t1 + (t1 - t0) * q / x.shape[0]
+        kind = "port"
+    per_q = sec / q
+    return {"value": 1.0 / per_q, "unit": "queries/s", "cores": 1, "kind": kind,
+            "sample": f"cfg {cfg}: sketch from {POINT_BUILD} rows, then {q} queries of detect_stream + insert "
+                      f"one at a time on one core ({sec:.2f} s)", "ms_per_step": per_q * POINT_STEP * 1e3,
+            "reported": rep}
+
+
+def point_line(cfg: int, impl: str, value: float, ms: float, args, ws: int) -> dict:
+    from paper_1706_06664_b200 import workloads as W
+    w = W.CONFIGS[cfg]
+    return {
+        "metric": "per-point API queries/s (detect_stream + insert per query, ace_cli stream --adapt)",
+        "value": value, "unit": "queries/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (datagen cfg {cfg}, seed {w.data_seed})",
+        "config": {"workload": f"cfg{cfg} {w.name}: per-point detect_stream + insert through the C++ drop-in "
+                               f"(include/ace/*.hpp), sketch built from {POINT_BUILD} rows, {POINT_STEP} queries "
+                               f"per step", "d": w.dim, "K": w.k_bits, "L": w.num_tables, "alpha": w.alpha,
+                   "api": "point"},
+    }
+
+
+def run_point(args, cfg, ws, rank, local, N):
+    """--api point, this implementation: tests/cpp/point_bench.cpp (the C++
+    drop-in, libace.so over libace_dev.so) runs the loop; wall clock around
+    the timed queries (a host API: every query's row goes in and its score
+    and flag come back)."""
+    from paper_1706_06664_b200 import workloads as W
+    w = W.CONFIGS[cfg]
+    q, wq = args.steps * POINT_STEP, max(3, args.warmup) * POINT_STEP
+    f, _ = point_rows(cfg, wq + q)
+    clocks = Clocks(local)
+    clocks.start()
+    r = subprocess.run([str(N.LIB_DIR / "ace_point_bench"), str(w.dim), str(w.k_bits), str(w.num_tables),
+                        str(w.w_seed), repr(w.alpha), str(POINT_BUILD), str(wq), str(q), str(f)],
+                       capture_output=True, text=True, check=True)
+    clk = clocks.stop()
+    sec, rep, p50, p99, tdet, launches = r.stdout.split()
+    sec = max_over_ranks(float(sec), ws)
+    value = q * ws / sec
+    ms = sec / args.steps * 1e3
+    line = point_line(cfg, "ace", value, ms, args, ws)
+    pk, pk_src = peaks()
+    per_q_s = sec / q
+    bytes_q = w.num_tables * w.k_bits * w.dim * 8.0  # W (binary64) read per query's folds
+    line.update({
+        "latency_us": {"p50": float(p50), "p99": float(p99), "detect_stream_mean": float(tdet),
+                       "definition": "wall clock of one detect_stream + insert pair"},
+        "roofline": {"bound": "hbm", "achieved": bytes_q / per_q_s / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": bytes_q / per_q_s / 1e9 / pk["hbm_gbs"], "traffic": None,
+                     "peak_source": pk_src,
+                     "note": "latency-bound: one point_kernel launch (a cluster of 8 CTAs) per query; algorithmic "
+                             "bytes = the query's binary64 W read (K L d x 8 B, L2-resident) per query time"},
+        "gpu_launches": int(launches) // args.steps, "clocks": clk,
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": POINT_STEP * w.dim * 8,
+                "d2h_bytes_per_step": POINT_STEP * 32,
+                "note": "the per-point API is the host call itself: the row (binary64) travels in the launch "
+                        "parameters, score, sum and state snapshot come back through mapped host memory"},
+        "reported": int(rep),
+    })
+    return line
 
 
 def roofline_of(kernel_ms, flops, pk, pk_src, w, cfg, ms_step, kname, desc):
@@ -531,7 +651,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--rows", type=int, default=None, help="stream mode: limit N (smoke runs)")
+    ap.add_argument("--api", default="batch", choices=["batch", "point"],
+                    help="batch: the hot path over each config (default); point: the per-point API")
     args = ap.parse_args()
+    if args.api == "point" and args.config == ORDER:
+        args.config = [5, 2]
     if args.impl == "reference":
         return run_reference(args)
 
@@ -547,6 +671,14 @@ def main():
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     for cfg in args.config:
+        if args.api == "point":
+            line = run_point(args, cfg, ws, rank, local, N)
+            if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+                cb = run_point_ref(args, cfg, 2, 0)
+                line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            if rank == 0:
+                print(json.dumps(line), flush=True)
+            continue
         w = W.CONFIGS[cfg]
         run = run_stream if w.mode == "stream" else run_batch
         line = run(args, cfg, ws, rank, local, torch, N, ace, W)

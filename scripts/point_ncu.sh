@@ -8,7 +8,7 @@ x, _ = W.host_rows(5, 0, 4096 + 200)
 x.astype(np.float32).tofile('/tmp/pt_rows.f32')
 PY
 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control ${CACHE:-all} -k regex:point --csv --log-file gpurun_out/point_ncu.csv \
-  paper_1706_06664_b200/lib/ace_point_bench 64 15 50 1 1.0 4096 200 /tmp/pt_rows.f32 > gpurun_out/point_ncu.log 2>&1
+  paper_1706_06664_b200/lib/ace_point_bench 64 15 50 1 1.0 4096 0 200 /tmp/pt_rows.f32 > gpurun_out/point_ncu.log 2>&1
 python - <<'PY'
 import csv
 rows = [r for r in csv.reader(open('gpurun_out/point_ncu.csv')) if len(r) > 10]

@@ -23,9 +23,9 @@ for cfg in (5, 2):
         o = Path(td) / "out.bin"
         x.astype(np.float32).tofile(f)
         r = subprocess.run([str(ROOT / "paper_1706_06664_b200/lib/ace_point_bench"), str(w.dim), str(w.k_bits),
-                            str(w.num_tables), str(w.w_seed), repr(w.alpha), str(NB), str(NQ), str(f), str(o)],
+                            str(w.num_tables), str(w.w_seed), repr(w.alpha), str(NB), "0", str(NQ), str(f), str(o)],
                            capture_output=True, text=True, check=True)
-        sec, rep, p50, p99, tdet = r.stdout.split()
+        sec, rep, p50, p99, tdet, nl = r.stdout.split()
         raw = o.read_bytes()
         sc = np.frombuffer(raw[:8 * NQ], dtype=np.float64)
         fl = np.frombuffer(raw[8 * NQ:], dtype=np.uint8)

@@ -111,12 +111,14 @@ def test_cpp_point_bench_matches_oracle(cuda, tmp_path):
     out = tmp_path / "out.bin"
     x.astype(np.float32).tofile(f)
     r = subprocess.run([str(exe), str(w.dim), str(w.k_bits), str(w.num_tables), str(w.w_seed), repr(w.alpha),
-                        str(nb), str(nq), str(f), str(out)], capture_output=True, text=True, timeout=300)
+                        str(nb), "0", str(nq), str(f), str(out)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr
     raw = out.read_bytes()
     assert np.array_equal(np.frombuffer(raw[:8 * nq], dtype=np.float64), want_sc)
     assert np.array_equal(np.frombuffer(raw[8 * nq:], dtype=np.uint8).astype(bool), want_fl)
-    assert int(r.stdout.split()[1]) == int(want_fl.sum())
+    f_ = r.stdout.split()
+    assert int(f_[1]) == int(want_fl.sum())
+    assert int(f_[5]) == nq + 1  # one point kernel per query, plus the last deferred insert
 
 
 def test_point_deferred_insert_with_other_calls(cuda):
