@@ -12,20 +12,23 @@
 // Buckets are packed MSB-first (srp.cpp:106-113) straight from the
 // accumulator columns: one thread owns one point (TMEM lane).
 //
-// Warp roles (448 threads, one CTA per SM, persistent over point tiles):
+// Warp roles (576 threads, one CTA per SM, persistent over point tiles):
 //   warp 0      W producer: ring of pre-swizzled W stages (cp.async.bulk)
 //   warp 1      TMEM allocator and MMA issuer (one elected lane, TS MMAs with
 //               the x split as the TMEM A operand)
-//   warps 2-9   epilogue: two warps per TMEM lane quarter on alternate
-//               direction tiles; tcgen05.ld -> sign words, near ties, buckets
-//   warps 10-13 converters, one per lane quarter, one thread per point: the
+//   warps 2-13  epilogue: three warps per TMEM lane quarter, the 32-column
+//               groups of each direction tile dealt round-robin; tcgen05.ld
+//               -> sign words, near ties
+//   warps 14-17 converters, one per lane quarter, one thread per point: the
 //               raw fp32 tile arrives by tensor-map TMA (SWIZZLE_128B boxes
 //               of 32 columns, OOB rows and columns zero-filled); each thread
 //               finds its row's scale, splits into fp16 hi / lo and writes
 //               them into a double-buffered TMEM A operand with tcgen05.st,
-//               plus the row's error threshold for the epilogue.  Warp 10
+//               plus the row's error threshold for the epilogue.  Warp 14
 //               issues the next tile's TMA as soon as the raw tile is read.
-// After the main loop warps 2-13 recheck the listed near ties (shared tail).
+//               One tile behind, the same warps cut the bucket ids from the
+//               sign words and store them.
+// After the main loop warps 2-17 recheck the listed near ties (shared tail).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_fp16.h>
@@ -42,8 +45,10 @@ using namespace tc;
 
 namespace {
 
-constexpr int kThreads = 448;        // 14 warps
-constexpr uint32_t kTail = 384;      // warps 2..13: the shared recheck tail
+constexpr uint32_t kEpiQ = 4;        // epilogue warps per TMEM lane quarter (one 32-column group each)
+constexpr uint32_t kConvW = 2u + 4u * kEpiQ;  // first converter warp
+constexpr int kThreads = 32 * (kConvW + 4);   // 22 warps
+constexpr uint32_t kTail = kThreads - 64;     // warps 2..: the shared recheck tail
 constexpr uint32_t kMaxWStages = 8;
 constexpr uint32_t kRawBox = 16384;  // one raw box: 128 rows x 32 fp32 (SW128)
 constexpr uint32_t kConvBar = 10;    // named barrier of the converter warps
@@ -54,6 +59,12 @@ constexpr uint32_t kTailBar = 9;     // named barrier of the shared tail
 // (read by ace_debug_tc_prof, exported only by such builds).
 #ifndef ACE_TC_PROF
 #define ACE_TC_PROF 0
+#endif
+// Experiment switches (profiling builds only; results are then wrong):
+// 1 = epilogue skips the sign / near-tie work, 2 = no MMAs issued,
+// 4 = packers skip the bucket cut and stores
+#ifndef ACE_TC_DBG
+#define ACE_TC_DBG 0
 #endif
 #if ACE_TC_PROF
 __device__ unsigned long long g_tc_prof[24];
@@ -89,7 +100,8 @@ __host__ __device__ inline TcLayout tc_layout(uint64_t dim, uint32_t tw, uint32_
   L.raw_bytes = static_cast<size_t>(L.n_raw) * kRawBox;
   L.nsteps = static_cast<uint32_t>((dim + 15) / 16);
   L.acols = 16u * L.nsteps;
-  L.nacc = 2;
+  // a third accumulator where it fits beside two A buffers (d <= 64 at tw = 128)
+  L.nacc = (3u * tw + 2u * L.acols <= 512u) ? 3u : 2u;
   L.n_abuf = (L.nacc * tw + 2u * L.acols <= 512u) ? 2u : 1u;
   L.nwords = (rows + 31u) / 32u;
   L.sgn_bytes = (static_cast<size_t>(L.nwords) * kRows * 4u + 1023u) / 1024u * 1024u;
@@ -205,11 +217,40 @@ __device__ __noinline__ void recheck_tail(const TcArgs& a, uint8_t* smem, size_t
   }
 }
 
+// Bucket packing with a compile-time K (KT = 15, 16: the BASELINE shapes):
+// 32 tables span exactly KT sign words, so per group of 32 tables the thread
+// loads its row's KT words once and cuts every bucket with constant shifts
+// (srp.cpp:106-113, bit 0 = MSB); one store per table, coalesced per table.
+template <uint32_t KT>
+__device__ __forceinline__ void pack_row_k(const uint32_t* sg, uint32_t r, uint32_t nwords, uint32_t tables,
+                                           uint32_t* idp, uint64_t ids_ld, bool valid) {
+  constexpr uint32_t kMask = (1u << KT) - 1u;
+  for (uint32_t g = 0; g * 32u < tables; ++g) {
+    uint32_t w[KT + 1];
+#pragma unroll
+    for (uint32_t i = 0; i <= KT; ++i) w[i] = sg[min(g * KT + i, nwords - 1u) * kRows + r];
+    uint32_t* p = idp + static_cast<uint64_t>(g) * 32u * ids_ld;
+    const uint32_t left = tables - g * 32u;
+#pragma unroll
+    for (uint32_t u = 0; u < 32u; ++u) {
+      const uint32_t s = u * KT, i = s >> 5, sh = s & 31u;
+      uint32_t b;
+      if (sh + KT <= 32u)
+        b = (w[i] >> (32u - sh - KT)) & kMask;
+      else
+        b = __funnelshift_l(w[i + 1], w[i], sh + KT - 32u) & kMask;
+      if (valid && u < left) *p = b;
+      p += ids_ld;
+    }
+  }
+}
+
+template <uint32_t KT>
 __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t bar_wfull[kMaxWStages], bar_wempty[kMaxWStages];
   __shared__ __align__(8) uint64_t bar_rawfull, bar_afull[2], bar_aempty[2], bar_thrfull[2], bar_threempty[2];
-  __shared__ __align__(8) uint64_t bar_accfull[2], bar_accempty[2], bar_sfull[2], bar_sempty[2];
+  __shared__ __align__(8) uint64_t bar_accfull[3], bar_accempty[3], bar_sfull[2], bar_sempty[2];
   __shared__ uint32_t tmem_base_sh;
   __shared__ float thr_sm[2][kRows];    // row thresholds per tile parity (converters -> epilogue)
   __shared__ uint32_t lom_sm[2][4];     // K16 steps with a nonzero x lo part, per A buffer / lane quarter
@@ -244,16 +285,18 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
       mbar_init(&bar_afull[b], 4);      // the four converter warps
       mbar_init(&bar_aempty[b], 1);     // MMA commit after the tile's last MMA
       mbar_init(&bar_thrfull[b], 4);
-      mbar_init(&bar_threempty[b], 8);  // every epilogue warp reads its rows' thresholds
-      mbar_init(&bar_accfull[b], 1);
-      mbar_init(&bar_accempty[b], 8);   // every epilogue warp reads half of each direction tile
-      mbar_init(&bar_sfull[b], 8u * a.ntiles);  // every epilogue warp, every direction tile
+      mbar_init(&bar_threempty[b], 4u * kEpiQ);  // every epilogue warp reads its rows' thresholds
+      mbar_init(&bar_sfull[b], 4u * kEpiQ);  // every epilogue warp, once per point tile
       mbar_init(&bar_sempty[b], 4);     // the four packer (converter) warps
+    }
+    for (int b = 0; b < 3; ++b) {
+      mbar_init(&bar_accfull[b], 1);
+      mbar_init(&bar_accempty[b], 4u * kEpiQ);  // every epilogue warp reads its group of each direction tile
     }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(&tmem_base_sh, 512);
-  if (warp == 10 && lane == 0) prefetch_tmap(&tmx);
+  if (warp == kConvW && lane == 0) prefetch_tmap(&tmx);
   tc_before();
   __syncthreads();
   tc_after();
@@ -326,6 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
               if (step >= L.nsteps) break;
               const uint32_t acol = step * 8u;  // 16 fp16 = 8 TMEM columns
               const uint64_t off = kk * 2u;     // 32 B along K in SW128, >> 4
+              if (ACE_TC_DBG & 2) continue;
               mma_f16_ts(dt, ta_hi + acol, dbh + off, idesc, step != 0u);
               if ((lm >> step) & 1u) mma_f16_ts(dt, ta_lo + acol, dbh + off, idesc, 1u);
               mma_f16_ts(dt, ta_hi + acol, dbl + off, idesc, 1u);
@@ -357,8 +401,8 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
     tcp[3] += static_cast<unsigned long long>(clock64() - t_kernel);
 #endif
     TCP_FLUSH(lane == 0);
-  } else if (warp >= 10) {
-    // ---------------- converters (warps 10-13): raw fp32 tile -> TMEM A operand ----------------
+  } else if (warp >= kConvW) {
+    // ---------------- converters (the last four warps): raw fp32 tile -> TMEM A operand ----------------
     // and, one tile behind, the bucket packers: each thread cuts its row's L
     // bucket ids (MSB-first bit fields of the sign-word stream, srp.cpp:106-113)
     // from the shared sign words and stores them (coalesced per table).
@@ -383,6 +427,10 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
       const uint64_t row = tile_of(itp) * kRows + r;
       const bool valid = row < a.n;
       uint32_t* idp = a.ids + row;
+      if constexpr (ACE_TC_DBG & 4) {
+      } else if constexpr (KT != 0) {
+        pack_row_k<KT>(sg, r, L.nwords, a.tables, idp, a.ids_ld, valid);
+      } else {
       // eight tables at a time: all sixteen word loads in flight first (a
       // table needs the next word only if it straddles, which then exists)
       for (uint32_t t0 = 0; t0 < a.tables; t0 += 8u) {
@@ -402,11 +450,12 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
             insert_bucket_warp(a.counters + (static_cast<uint64_t>(tt) << K), bk[u], valid, lane);
         }
       }
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_sempty[sb]);
       TCP_END(14);
     };
-    if (warp == 10 && lane == 0 && my_tiles > 0) issue_raw(tile_of(0));
+    if (warp == kConvW && lane == 0 && my_tiles > 0) issue_raw(tile_of(0));
     const uint32_t lane_base = (q * 32u) << 16;
     for (uint64_t it = 0; it < my_tiles; ++it) {
       const uint64_t t = tile_of(it);
@@ -473,9 +522,9 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
       }
       TCP_END(8);
       TCP_BEGIN();
-      // every converter has read the raw tile: warp 10 loads the next one
+      // every converter has read the raw tile: warp kConvW loads the next one
       asm volatile("bar.sync %0, 128;" ::"r"(kConvBar) : "memory");
-      if (warp == 10 && lane == 0 && it + 1 < my_tiles) issue_raw(tile_of(it + 1));
+      if (warp == kConvW && lane == 0 && it + 1 < my_tiles) issue_raw(tile_of(it + 1));
       thr_sm[p][r] = row_threshold(rs, live, ss, a.dim, a.margin_c);
       lob = __reduce_or_sync(0xffffffffu, lob);
       if (lane == 0) lom_sm[b][q] = lob;
@@ -490,19 +539,17 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
       if (it > 0) pack(it - 1);
     }
     if (my_tiles > 0) pack(my_tiles - 1);
-    TCP_FLUSH(warp == 10 && lane == 0);
+    TCP_FLUSH(warp == kConvW && lane == 0);
   } else {
-    // ---------------- epilogue (warps 2-9) ----------------
-    // Both warps of a TMEM lane quarter (q = warp % 4, half h) work on every
-    // direction tile, half its columns each (64 or 96: all loads issued
-    // before one wait), so a tile's accumulator is read and released in half
-    // the time.  Per 32 columns: sign bits packed MSB-first (one funnel shift
-    // per column), near ties by one float min over |v|, four independent
-    // chains for ILP.  The tile's sign words go to shared memory
-    // (sgn[word][row]), where the converter warps cut the buckets.
-    const uint32_t q = warp & 3, h = (warp - 2) >> 2;
+    // ---------------- epilogue (warps 2 .. 2 + 4 kEpiQ - 1) ----------------
+    // kEpiQ = 4 warps per TMEM lane quarter (q = warp % 4, e = (warp - 2) / 4):
+    // warp e reads 32-column group e of every 128-direction tile, i.e. sign
+    // word G = 4 j + e.  Per group: sign bits packed MSB-first (one funnel
+    // shift per column, four chains) and near ties by one float min over |v|.
+    // The sign words go to shared memory (sgn[word][row]), where the
+    // converter warps cut the buckets.
+    const uint32_t q = warp & 3, e = (warp - 2) >> 2;
     const uint32_t r = q * 32u + lane;
-    const uint32_t hw = TW / 2u, ngrp = hw / 32u;  // columns and 32-column groups per warp (64/2 or 96/3)
     uint32_t acc = 0, accph = 0;
     for (uint64_t it = 0; it < my_tiles; ++it) {
       const uint64_t t = tile_of(it);
@@ -520,31 +567,22 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
       TCP_END(10);
       uint32_t* sg = Ssm + static_cast<size_t>(sb) * (L.sgn_bytes / 4u);
       const bool zero_row = thr < 0.0f;
+      const bool live = !zero_row && valid;
       const uint32_t thr_u = zero_row ? 0u : (isinf(thr) ? 0xffffffffu : (__float_as_uint(thr) << 1));
       for (uint32_t j = 0; j < a.ntiles; ++j) {
-        const uint32_t col0 = j * TW + h * hw;  // this warp's first column (direction)
-        const uint32_t used = R > col0 ? min(hw, R - col0) : 0u;
+        const uint32_t gw = 4u * j + e;  // this warp's sign word (directions 32 gw ..)
         TCP_BEGIN();
         mbar_wait_sleepy(&bar_accfull[acc], accph);
         TCP_END(11);
         TCP_BEGIN();
         tc_after();
-        uint32_t v[96];
-        const uint32_t ta = tmem_base + ((q * 32u) << 16) + acc * TW + h * hw;
-        ACE_TMEM_LD32(ta, v);
-        ACE_TMEM_LD32(ta + 32u, (v + 32));
-        if (ngrp > 2u) ACE_TMEM_LD32(ta + 64u, (v + 64));
+        uint32_t v[32];
+        ACE_TMEM_LD32(tmem_base + ((q * 32u) << 16) + acc * TW + 32u * e, v);
         tmem_wait_ld();
         tc_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar_accempty[acc]);  // read: the MMAs may reuse it
-        uint32_t wd[3];
-#pragma unroll
-        for (uint32_t g2 = 0; g2 < 3u; ++g2) {
-          wd[g2] = 0xffffffffu;
-          if (g2 >= ngrp) break;
-          const uint32_t cc = 32u * g2;
-          const uint32_t* vv = v + 32 * g2;
+        if (!(ACE_TC_DBG & 1) && gw < L.nwords) {
           // near-tie test on |v| as a float min (FMNMX with |.| operands);
           // NaN (non-finite rows, thr = inf) fails `mn > thr`
           uint32_t n4[4] = {0u, 0u, 0u, 0u};
@@ -553,38 +591,32 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
           for (int jj = 0; jj < 8; ++jj)
 #pragma unroll
             for (int gq = 0; gq < 4; ++gq) {
-              n4[gq] = (n4[gq] << 1) | (vv[gq * 8 + jj] >> 31);
-              m4[gq] = fminf(m4[gq], fabsf(__uint_as_float(vv[gq * 8 + jj])));
+              n4[gq] = (n4[gq] << 1) | (v[gq * 8 + jj] >> 31);
+              m4[gq] = fminf(m4[gq], fabsf(__uint_as_float(v[gq * 8 + jj])));
             }
-          const uint32_t neg = (n4[0] << 24) | (n4[1] << 16) | (n4[2] << 8) | n4[3];
           const float mn = fminf(fminf(m4[0], m4[1]), fminf(m4[2], m4[3]));
-          // columns past `used` (padding / stale) are masked here, off the hot path
-          if (!zero_row && valid && !(mn > thr) && cc < used) {
-            const uint32_t ncol = min(32u, used - cc);
+          // bit (31-jj) = direction 32 gw + jj >= 0
+          sg[gw * kRows + r] = zero_row ? 0xffffffffu : ~((n4[0] << 24) | (n4[1] << 16) | (n4[2] << 8) | n4[3]);
+          TCP_END(12);
+          TCP_BEGIN();
+          // columns past R (padding / stale) are masked here, off the hot path
+          if (live && !(mn > thr)) {
+            const uint32_t ncol = min(32u, R - 32u * gw);
             uint32_t nm = 0u;
 #pragma unroll
-            for (int jj = 0; jj < 32; ++jj) nm |= (((vv[jj] << 1) <= thr_u) ? 1u : 0u) << jj;
+            for (int jj = 0; jj < 32; ++jj) nm |= (((v[jj] << 1) <= thr_u) ? 1u : 0u) << jj;
             if (ncol < 32u) nm &= (1u << ncol) - 1u;
-            if (nm) push_near_mask(a.st, seg, seg_cap, &seg_n, a.overflow_rows, nm, row, col0 + cc);
+            if (nm) push_near_mask(a.st, seg, seg_cap, &seg_n, a.overflow_rows, nm, row, 32u * gw);
           }
-          wd[g2] = zero_row ? 0xffffffffu : ~neg;  // bit (31-jj) = column cc+jj >= 0
+          TCP_END(13);
         }
-        TCP_END(12);
-        TCP_BEGIN();
-        // sign words of this half tile: global words (j * TW + h * hw) / 32 + g2
-#pragma unroll
-        for (uint32_t g2 = 0; g2 < 3u; ++g2) {
-          const uint32_t gw = col0 / 32u + g2;
-          if (g2 < ngrp && gw < L.nwords) sg[gw * kRows + r] = wd[g2];
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bar_sfull[sb]);
-        TCP_END(13);
         if (++acc == L.nacc) {
           acc = 0;
           accph ^= 1u;
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_sfull[sb]);
     }
   }
 
@@ -759,8 +791,7 @@ cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc) {
   const bool ks = tc_kstream(nkc);
   // 192-direction tiles where two accumulators and two A buffers fit TMEM
   // (d <= 64), else 128; the K-streamed kernel: 256 (whole tables per tile)
-  const uint32_t nsteps = static_cast<uint32_t>((f.dim + 15) / 16);
-  const uint32_t tw = ks ? 256u : (2u * 192u + 2u * 16u * nsteps <= 512u ? 192u : 128u);
+  const uint32_t tw = ks ? 256u : 128u;  // the d <= 256 kernel's epilogue reads 4 x 32 columns per tile
   if (!ks && tc_layout(f.dim, tw, f.rows).n_wst < 2) return cudaSuccess;
   tc->nkc = nkc;
   tc->tw = tw;
@@ -790,9 +821,11 @@ cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc) {
     if ((e = tck_prepare(tw)) != cudaSuccess) return e;
   } else {
     // every layout stays within kSmemLimit - 8192 (tc_layout)
-    e = cudaFuncSetAttribute(hash_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kSmemLimit - 8192));
-    if (e != cudaSuccess) return e;
+    for (const void* fn : {reinterpret_cast<const void*>(hash_tc_kernel<0>), reinterpret_cast<const void*>(hash_tc_kernel<15>),
+                           reinterpret_cast<const void*>(hash_tc_kernel<16>)})
+      if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kSmemLimit - 8192))) != cudaSuccess)
+        return e;
   }
   tc->enabled = 1;
   return cudaSuccess;
@@ -829,7 +862,14 @@ cudaError_t launch_hash_tc(const TcArgs& a, void* stage, cudaStream_t s) {
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   const uint64_t tiles = (a.n + kRows - 1) / kRows;
   const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(tc_sms()));
-  hash_tc_kernel<<<static_cast<unsigned>(grid), kThreads, tc_layout(a.dim, a.tw, a.k_bits * a.tables).total, s>>>(a, map);
+  const size_t smem = tc_layout(a.dim, a.tw, a.k_bits * a.tables).total;
+  // compile-time K packers for the BASELINE shapes (never with the fused insert, K > 20)
+  if (a.k_bits == 15 && !a.fused_insert)
+    hash_tc_kernel<15><<<static_cast<unsigned>(grid), kThreads, smem, s>>>(a, map);
+  else if (a.k_bits == 16 && !a.fused_insert)
+    hash_tc_kernel<16><<<static_cast<unsigned>(grid), kThreads, smem, s>>>(a, map);
+  else
+    hash_tc_kernel<0><<<static_cast<unsigned>(grid), kThreads, smem, s>>>(a, map);
   count_launch();
   return cudaGetLastError();
 }

@@ -57,7 +57,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 // Waits off the critical MMA path back off between polls so the polling does
-// not compete with the tensor pipe for shared memory.
+// not compete with the busy warps for issue slots.  (A try_wait suspend-time
+// hint instead of the back-off measured slower: 145.7 vs 137.3 us per
+// 262,144-row cfg-5 hashing launch.)
 __device__ __forceinline__ void mbar_wait_sleepy(uint64_t* bar, uint32_t parity) {
   while (!mbar_try(bar, parity)) __nanosleep(64);
 }
