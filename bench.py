@@ -48,6 +48,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "ACE points/sec (hash+insert+score) on 1 B200; % of binding FP32/HBM/L2-atomic roofline"
 UNIT = "points/s"
 ORDER = [1, 2, 3, 4, 5]  # the headline (config 5) last
+STREAM_GROUP = 4  # config 5: batches per hashing / stream-kernel launch
 
 # bounded CPU samples (rows): cpu_baseline leg (~10 s of reference CPU work
 # per config) and the --impl reference arm (~1 s per step)
@@ -529,7 +530,9 @@ def run_stream(args, cfg, ws, rank, local, torch, N, ace, W):
         W.device_rows(w.cfg, r0, m, x[r0:r0 + m].data_ptr())
     torch.cuda.synchronize()
     fam = ace.SrpFamily(ace.SrpConfig(dim=w.dim, k_bits=w.k_bits, num_tables=w.num_tables, seed=w.w_seed))
+    G = args.stream_group
     sk = ace.AceSketch(fam, ace.CounterWidth.k32)
+    sk.set_option(N.ACE_OPT_STREAM_GROUP, G)
     stream = torch.cuda.current_stream()
     sk.set_stream(stream.cuda_stream)
     flags = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
@@ -581,6 +584,7 @@ def run_stream(args, cfg, ws, rank, local, torch, N, ace, W):
         st_e = N.AceHashStats()
         fn = N.dev().ace_sketch_stream_run
         sk_e = ace.AceSketch(fam, ace.CounterWidth.k32)
+        sk_e.set_option(N.ACE_OPT_STREAM_GROUP, G)
         sk_e.set_stream(stream.cuda_stream)
 
         def e2e_call():
@@ -606,11 +610,11 @@ def run_stream(args, cfg, ws, rank, local, torch, N, ace, W):
 
     pk, pk_src = peaks()
     nb = -(-n // w.batch)
-    groups = -(-nb // 4)  # hashing launches of 4 batches each
+    groups = -(-nb // G)  # hashing launches of G batches each
     flops_per_launch = 2.0 * w.dim * w.k_bits * w.num_tables * (n / groups)
     roof = roofline_of(hash_ms / groups, flops_per_launch, pk, pk_src, w, cfg, ms / groups, "hash_tc_kernel",
                        "tcgen05 fp16x3-split projection of raw fp32 rows loaded by tensor-map TMA, split in-kernel; "
-                       "per launch: one 4-batch hashing group (262,144 rows) with its near-tie pass")
+                       f"per launch: one {G}-batch hashing group ({G * w.batch:,} rows) with its near-tie pass")
     roof["kernel_share_of_step"] = hash_ms / ms if ms else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -618,7 +622,7 @@ def run_stream(args, cfg, ws, rank, local, torch, N, ace, W):
         "vs_baseline": None, "dtype": "f32", "data": f"synthetic (datagen cfg {cfg}, seed {w.data_seed})",
         "config": {"workload": f"cfg{cfg} {w.name}: streaming score -> flag (mean - alpha) -> insert",
                    "N": n, "d": w.dim, "K": w.k_bits, "L": w.num_tables, "batch": w.batch,
-                   "hash_group_batches": 4, "graph": "the stream driver's device work replayed as one CUDA graph",
+                   "hash_group_batches": G, "graph": "the stream driver's device work replayed as one CUDA graph",
                    "alpha": w.alpha, "counter_width": 32,
                    "l2": f"inputs {n * w.dim * 4 / 1e9:.1f} GB > 126 MB L2",
                    "parallelism": f"replicas x{ws}"},
@@ -651,6 +655,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--rows", type=int, default=None, help="stream mode: limit N (smoke runs)")
+    ap.add_argument("--stream-group", type=int, default=STREAM_GROUP,
+                    help="stream mode: batches per hashing launch and per stream-kernel launch")
     ap.add_argument("--api", default="batch", choices=["batch", "point"],
                     help="batch: the hot path over each config (default); point: the per-point API")
     args = ap.parse_args()
