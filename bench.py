@@ -59,15 +59,26 @@ REF_SAMPLE = {1: 20_000, 2: 10_000, 3: 4_000, 4: 160, 5: 16_384}
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
-        d = json.loads(p.read_text())
-        return d, "measured (MEASURED_PEAKS.json)"
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
+        d, src = json.loads(p.read_text()), "measured (MEASURED_PEAKS.json)"
+    else:
+        d, src = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
+    # dense TF32: the tcgen05 peak of the fp32 input dtype,
+    # measured on this pool's B200 by scripts/tf32_peak.py; else half of bf16
+    t = ROOT / "profiles" / "r2_tf32_peak.json"
+    if t.exists():
+        d["tf32_tflops"] = json.loads(t.read_text())["tf32_tflops"]
+        d["tf32_source"] = "measured (profiles/r2_tf32_peak.json, torch.matmul fp32+TF32 8192^3)"
+    else:
+        d["tf32_tflops"] = 0.5 * d["bf16_tflops"]
+        d["tf32_source"] = "half the bf16 dense peak (fallback)"
+    return d, src
 
 
 def step_roofline(w, value, pk):
     """The metric's binding roofline for the whole step:
     points/s = min(projection peak / (2 d K L), HBM / (4 d), L2 RED rate / L),
-    with the tcgen05 bf16 dense peak, the measured HBM copy bandwidth and the
+    with the tcgen05 dense peak of the fp32 input dtype (TF32, measured), the
+    measured HBM copy bandwidth and the
     measured random-address L2 RED rate (profiles/r1_peaks_probe.json) for
     this counter array.  This design counts in shared-memory histograms, so
     the L2-atomic term is the metric's definition rather than a limit of the
@@ -81,7 +92,7 @@ def step_roofline(w, value, pk):
             size = w.num_tables * (4 << w.k_bits)
             red = rates[min(rates, key=lambda k: abs(k - size))] * 1e9
     f = 2.0 * w.dim * w.k_bits * w.num_tables
-    proj = pk["bf16_tflops"] * 1e12 / f
+    proj = pk["tf32_tflops"] * 1e12 / f
     hbm = pk["hbm_gbs"] * 1e9 / (4.0 * w.dim)
     terms = {"projection_pts_s": proj, "hbm_x_read_pts_s": hbm}
     if red:
@@ -90,7 +101,8 @@ def step_roofline(w, value, pk):
     no_atomic = min(proj, hbm)
     return {"binding": bind.replace("_pts_s", ""), "binding_pts_s": terms[bind], "frac": value / terms[bind],
             "terms": terms, "frac_without_atomic_term": value / no_atomic,
-            "source": "SURVEY.md 8(d); peaks from MEASURED_PEAKS.json and profiles/r1_peaks_probe.json"}
+            "source": "SURVEY.md 8(d); HBM from MEASURED_PEAKS.json, TF32 from profiles/r2_tf32_peak.json, "
+                      "L2 RED rate from profiles/r1_peaks_probe.json"}
 
 
 class Clocks:
@@ -388,18 +400,26 @@ def run_point(args, cfg, ws, rank, local, N):
 
 
 def roofline_of(kernel_ms, flops, pk, pk_src, w, cfg, ms_step, kname, desc):
-    peak = pk["bf16_tflops"]
+    """Dominant-kernel roofline: algorithmic flops (2 d K L per point) per
+    launch / live launch time, against the dense tcgen05 peak of the fp32
+    input dtype (TF32: "the dense tcgen05 peak of the input
+    dtype for tensor kernels"); the bf16 dense fraction and the fraction of
+    the 3-pass fp16 split's own ceiling (bf16 peak / 3) are reported beside."""
+    peak = pk["tf32_tflops"]
+    bf16 = pk["bf16_tflops"]
     ach = flops / (kernel_ms * 1e-3) / 1e12 if kernel_ms > 0 else None
     return {
         "bound": "tensor", "kernel": f"{kname} ({desc})", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
         "frac": ach / peak if ach else None, "traffic": _profiled_traffic(kname, cfg),
-        "peak_source": f"bf16 dense {pk_src} (burst); algorithmic flops = 2*d*K*L per point, "
+        "peak_source": f"dense TF32, {pk['tf32_source']}; algorithmic flops = 2*d*K*L per point, "
                        "the 3 split passes count against achieved",
+        "peak_bf16_dense": bf16, "peak_bf16_source": f"{pk_src} (burst)",
+        "frac_vs_bf16_dense": ach / bf16 if ach else None,
         "algorithmic_flops_per_launch": flops, "kernel_ms": kernel_ms,
         "kernel_share_of_step": kernel_ms / ms_step if ms_step else None,
-        # the exact-sign split runs 3 fp16 MMA passes per projection: peak / 3
-        # is the kernel's ceiling in algorithmic flops
-        "split_passes": 3, "frac_of_split_ceiling": 3.0 * ach / peak if ach else None,
+        # the exact-sign split runs 3 fp16 MMA passes per projection: bf16
+        # peak / 3 is the kernel's ceiling in algorithmic flops
+        "split_passes": 3, "frac_of_split_ceiling": 3.0 * ach / bf16 if ach else None,
     }
 
 
