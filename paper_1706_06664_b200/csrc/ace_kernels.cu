@@ -1573,17 +1573,44 @@ __global__ void __launch_bounds__(1024) stream_apply_kernel(const StreamApplyArg
 // both histograms (its peer's through distributed shared memory) into the
 // table with plain stores (no other CTA writes them) and T += 2 c m + m^2.
 // The CTAs of the clusters past the tables do phase B of the previous batch.
+#ifndef ACE_SP_PROF
+#define ACE_SP_PROF 0
+#endif
+#if ACE_SP_PROF
+// profiling builds: globaltimer marks per phase, summed over CTAs
+__device__ unsigned long long g_sp_prof[16];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define SPP(k) \
+  if (threadIdx.x == 0) atomicAdd(&g_sp_prof[k], gtime() - sp_t0)
+#define SPC(k) \
+  if (threadIdx.x == 0) atomicAdd(&g_sp_prof[k], 1ull)
+#else
+#define SPP(k)
+#define SPC(k)
+#endif
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_pair_kernel(const StreamApplyArgs a) {
   extern __shared__ __align__(16) uint32_t sm[];
   __shared__ unsigned long long red[32];
   __shared__ unsigned long long red2[32];
+#if ACE_SP_PROF
+  const unsigned long long sp_t0 = gtime();
+#endif
   DevState* st = a.st;
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t nA = a.n ? 2u * a.tables : 0u;  // phase-A CTAs (one cluster per table)
   if (blockIdx.x >= nA) {
+    SPP(8);
     if (a.n_prev) stream_phase_b(a, blockIdx.x - nA, gridDim.x - nA, red, red2);
+    SPP(9);
+    SPC(15);
     return;
   }
+  SPP(0);
+  SPC(14);
   cg::cluster_group cl = cg::this_cluster();
   const uint32_t r = cl.block_rank(), t = blockIdx.x >> 1;
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // the cut of batch b, from the state before it
@@ -1598,22 +1625,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_pair_ke
   uint32_t* hs = sm + nb;  // this CTA's histogram [nw]
   uint32_t* ct = a.counters + (static_cast<uint64_t>(t) << a.k_bits);
   if (nb >= 4) {
+    // 16-byte loads, eight per thread in flight (latency-bound otherwise)
     const uint4* c4 = reinterpret_cast<const uint4*>(ct);
-    for (uint32_t b = threadIdx.x; b < nb / 4; b += blockDim.x) reinterpret_cast<uint4*>(cs)[b] = c4[b];
+    uint4* s4 = reinterpret_cast<uint4*>(cs);
+    constexpr uint32_t kU = 8;
+    const uint32_t n4 = nb / 4, step = kU * blockDim.x;
+    for (uint32_t b0 = 0; b0 < n4; b0 += step) {
+      uint4 v[kU];
+#pragma unroll
+      for (uint32_t u = 0; u < kU; ++u) v[u] = __ldcg(c4 + min(b0 + u * blockDim.x + threadIdx.x, n4 - 1u));
+#pragma unroll
+      for (uint32_t u = 0; u < kU; ++u)
+        if (b0 + u * blockDim.x + threadIdx.x < n4) s4[b0 + u * blockDim.x + threadIdx.x] = v[u];
+    }
   } else {
     for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) cs[b] = ct[b];
   }
   for (uint32_t w = threadIdx.x; w < nw; w += blockDim.x) hs[w] = 0u;
   __syncthreads();
+  SPP(1);
   const uint64_t i0 = a.n * r / 2, i1 = a.n * (r + 1) / 2;
   const uint32_t* idt = a.ids + static_cast<uint64_t>(t) * a.stride;
   uint32_t* co = a.cnt_out + static_cast<uint64_t>(t) * a.n;
+#ifndef ACE_SP_DBG
+#define ACE_SP_DBG 0
+#endif
   auto take = [&](uint64_t i, uint32_t id) {
-    co[i] = cs[id];
+    if (ACE_SP_DBG & 2) co[i] = id; else co[i] = cs[id];
+    if (ACE_SP_DBG & 1) return;
+    if (ACE_SP_DBG & 4) {
+      const unsigned peers = __match_any_sync(__activemask(), id);
+      if ((__ffs(peers) - 1) == static_cast<int>(threadIdx.x & 31u))
+        atomicAdd(&hs[id >> 1], static_cast<uint32_t>(__popc(peers)) << ((id & 1u) << 4));
+      return;
+    }
     atomicAdd(&hs[id >> 1], 1u << ((id & 1u) << 4));
   };
   if (a.stride % 4 == 0 && i0 % 4 == 0 && i1 % 4 == 0 && (reinterpret_cast<uintptr_t>(a.ids) & 15) == 0) {
-    constexpr int kDepth = 4;  // 16-byte id loads in flight per thread
+    constexpr int kDepth = 8;  // 16-byte id loads in flight per thread
     const uint4* id4 = reinterpret_cast<const uint4*>(idt + i0);
     const uint64_t n4 = (i1 - i0) / 4;
     for (uint64_t g0 = 0; g0 < n4; g0 += kDepth * blockDim.x) {
@@ -1635,26 +1684,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_pair_ke
   } else {
     for (uint64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) take(i, __ldg(idt + i));
   }
+  __syncthreads();
+  SPP(2);
   cl.sync();  // both histograms complete
+  SPP(3);
   const uint32_t* peer = cl.map_shared_rank(hs, r ^ 1u);
   unsigned long long dT = 0ull;
   const uint32_t w0 = nw * r / 2, w1 = nw * (r + 1) / 2;
-  for (uint32_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) {
-    const uint32_t ow = hs[w], pw = peer[w];
+  auto merge_word = [&](uint32_t w, uint32_t ow, uint32_t pw) {
 #pragma unroll
     for (uint32_t h = 0; h < 2; ++h) {
       const uint32_t b = 2u * w + h;
       const uint32_t m = ((ow >> (16 * h)) & 0xffffu) + ((pw >> (16 * h)) & 0xffffu);
       if (m && b < nb) {
         const uint32_t c = cs[b];
-        ct[b] = c + m;
+        if (!(ACE_SP_DBG & 16)) ct[b] = c + m;
         dT += 2ull * c * m + static_cast<unsigned long long>(m) * m;
       }
     }
+  };
+  if (w0 % 4 == 0 && w1 % 4 == 0) {
+    // 16-byte words of both histograms (the peer's through distributed shared
+    // memory), two per thread in flight
+    const uint4* o4 = reinterpret_cast<const uint4*>(hs);
+    const uint4* p4 = reinterpret_cast<const uint4*>(peer);
+    constexpr uint32_t kU = 2;
+    const uint32_t q0 = w0 / 4, q1 = w1 / 4, step = kU * blockDim.x;
+    for (uint32_t g = q0; g < q1; g += step) {
+      uint4 ov[kU], pv[kU];
+#pragma unroll
+      for (uint32_t u = 0; u < kU; ++u) {
+        const uint32_t q = min(g + u * blockDim.x + threadIdx.x, q1 - 1u);
+        pv[u] = (ACE_SP_DBG & 8) ? make_uint4(0u, 0u, 0u, 0u) : p4[q];
+        ov[u] = o4[q];
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < kU; ++u) {
+        const uint32_t q = g + u * blockDim.x + threadIdx.x;
+        if (q >= q1) continue;
+        if ((ov[u].x | pv[u].x) != 0u) merge_word(4 * q, ov[u].x, pv[u].x);
+        if ((ov[u].y | pv[u].y) != 0u) merge_word(4 * q + 1, ov[u].y, pv[u].y);
+        if ((ov[u].z | pv[u].z) != 0u) merge_word(4 * q + 2, ov[u].z, pv[u].z);
+        if ((ov[u].w | pv[u].w) != 0u) merge_word(4 * q + 3, ov[u].w, pv[u].w);
+      }
+    }
+  } else {
+    for (uint32_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) merge_word(w, hs[w], peer[w]);
   }
   dT = warp_sum_u64(dT);
   if (lane == 0) red[wid] = dT;
+  __syncthreads();
+  SPP(4);
   cl.sync();  // the peer has read this CTA's histogram
+  SPP(5);
   if (threadIdx.x == 0) {
     unsigned long long sum = 0ull;
     for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) sum += red[w];
@@ -2101,3 +2183,15 @@ cudaError_t launch_sum_squares(const uint32_t* counters, uint64_t num, unsigned 
 }
 
 }  // namespace ace_dev
+
+#if ACE_SP_PROF
+extern "C" int ace_debug_sp_prof(unsigned long long* out16, int reset) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out16, ace_dev::g_sp_prof, sizeof(unsigned long long) * 16) != cudaSuccess) return -1;
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(ace_dev::g_sp_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

@@ -42,5 +42,9 @@ names = {0: "mma wait A", 1: "mma wait acc-empty", 2: "mma wait W", 3: "mma loop
          10: "epi wait thr + sgn free", 11: "epi wait acc-full", 12: "epi TMEM ld + process", 13: "epi sign words",
          14: "pack buckets", 15: "pack wait sgn", 16: "kernel total (thread 0)"}
 print(f"cfg {cfg} n {n}: {tpc:.1f} tiles per CTA; cycles per CTA (per tile)")
+if out[22]:
+    c = out[22]
+    print(f"  per CTA from entry: prologue {out[17] / c:.0f}, first MMA {out[18] / c:.0f}, tail start {out[19] / c:.0f}, "
+          f"tail end {out[20] / c:.0f}, kernel end {out[21] / c:.0f} cycles")
 for k, nm in names.items():
     print(f"  {nm:26s} {per[k]:10.0f} ({per[k] / tpc:7.0f})")
