@@ -1647,18 +1647,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_pair_ke
   const uint64_t i0 = a.n * r / 2, i1 = a.n * (r + 1) / 2;
   const uint32_t* idt = a.ids + static_cast<uint64_t>(t) * a.stride;
   uint32_t* co = a.cnt_out + static_cast<uint64_t>(t) * a.n;
-#ifndef ACE_SP_DBG
-#define ACE_SP_DBG 0
-#endif
   auto take = [&](uint64_t i, uint32_t id) {
-    if (ACE_SP_DBG & 2) co[i] = id; else co[i] = cs[id];
-    if (ACE_SP_DBG & 1) return;
-    if (ACE_SP_DBG & 4) {
-      const unsigned peers = __match_any_sync(__activemask(), id);
-      if ((__ffs(peers) - 1) == static_cast<int>(threadIdx.x & 31u))
-        atomicAdd(&hs[id >> 1], static_cast<uint32_t>(__popc(peers)) << ((id & 1u) << 4));
-      return;
-    }
+    co[i] = cs[id];
     atomicAdd(&hs[id >> 1], 1u << ((id & 1u) << 4));
   };
   if (a.stride % 4 == 0 && i0 % 4 == 0 && i1 % 4 == 0 && (reinterpret_cast<uintptr_t>(a.ids) & 15) == 0) {
@@ -1698,7 +1688,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_pair_ke
       const uint32_t m = ((ow >> (16 * h)) & 0xffffu) + ((pw >> (16 * h)) & 0xffffu);
       if (m && b < nb) {
         const uint32_t c = cs[b];
-        if (!(ACE_SP_DBG & 16)) ct[b] = c + m;
+        ct[b] = c + m;
         dT += 2ull * c * m + static_cast<unsigned long long>(m) * m;
       }
     }
@@ -1715,7 +1705,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_pair_ke
 #pragma unroll
       for (uint32_t u = 0; u < kU; ++u) {
         const uint32_t q = min(g + u * blockDim.x + threadIdx.x, q1 - 1u);
-        pv[u] = (ACE_SP_DBG & 8) ? make_uint4(0u, 0u, 0u, 0u) : p4[q];
+        pv[u] = p4[q];
         ov[u] = o4[q];
       }
 #pragma unroll
