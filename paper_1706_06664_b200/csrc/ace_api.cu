@@ -454,7 +454,7 @@ ace_status ensure_stream_bufs(AceSketch* sk, uint64_t rows) {
 // Chunk mode (ids_out != null): the rows are rows [r0, r0 + n) of a longer
 // batch whose ids (stride ids_ld) the caller has sized.
 ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64_t ld, int insert,
-                    uint32_t* ids_out = nullptr, uint64_t ids_ld = 0) {
+                    uint32_t* ids_out = nullptr, uint64_t ids_ld = 0, bool ids16 = false) {
   const AceFamily* f = sk->fam;
   if (!ids_out) {
     ACE_CUDA(sk->ids.ensure(static_cast<size_t>(n) * f->d.tables * sizeof(uint32_t)));
@@ -482,6 +482,7 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
     t.margin_c = kstream ? tck_margin(f->tc.nkc, t.x_f64 != 0) : tc_margin(f->tc.nkc, t.x_f64 != 0);
     t.ids = ids_out;
     t.ids_ld = ids_ld;
+    t.ids16 = ids16 ? 1 : 0;  // callers ask for u16 ids only on this path (stream driver, K <= 15)
     // near-tie list: the K-streamed path's bound (large d, dense data) leaves
     // far more near ties per row, size its list accordingly
     uint64_t cap = kstream ? n * f->d.rows / 48 : n * f->d.rows / 1024;
@@ -1435,6 +1436,9 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
   const bool ff = fire_and_forget_ok(sk, n);
   const bool fast = stream_apply_ok(sk, ff);
   const uint64_t G = static_cast<uint64_t>(sk->stream_group);
+  // u16 bucket ids between the projection and the pair stream kernel: half
+  // the id traffic (K <= 15, the d <= 256 tensor-core projection)
+  const bool ids16 = fast && stream_pair_ok(f->d.tables, f->d.k_bits, batch) && f->use_tc() && !tc_kstream(f->tc.nkc);
   ACE_CUDA(sk->flags.ensure(((n + 31) / 32) * sizeof(uint32_t)));
   uint32_t* dflags = (flag_bits && out_where == ACE_DEVICE) ? flag_bits : sk->flags.as<uint32_t>();
   if (fast && (r = ensure_stream_bufs(sk, std::min(batch, n))) != ACE_OK) return r;
@@ -1508,7 +1512,7 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
         xd = sk->sstage[hb].p;
         ldd = ld;
         ACE_CUDA(tmark(0, false));
-        if ((rr = run_hash(sk, xd, dtype, grows, ldd, 0)) != ACE_OK) return rr;
+        if ((rr = run_hash(sk, xd, dtype, grows, ldd, 0, nullptr, 0, ids16)) != ACE_OK) return rr;
         ACE_CUDA(tmark(0, true));
         ACE_CUDA(cudaEventRecord(sk->s_used[hb], sk->stream));
         const uint64_t g1 = g0 + G;
@@ -1522,19 +1526,20 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
       } else {
         if ((rr = stage_x(sk, sk->stage, sk->stream, xg, dtype, grows, ld, x_where, &xd, &ldd)) != ACE_OK) return rr;
         ACE_CUDA(tmark(0, false));
-        if ((rr = run_hash(sk, xd, dtype, grows, ldd, 0)) != ACE_OK) return rr;
+        if ((rr = run_hash(sk, xd, dtype, grows, ldd, 0, nullptr, 0, ids16)) != ACE_OK) return rr;
         ACE_CUDA(tmark(0, true));
       }
       for (uint64_t b = g0; b < g0 + gb; ++b) {
         const uint64_t r0 = b * batch, rows = std::min(batch, n - r0);
         if (batch_ms && b != g0) ACE_CUDA(cudaEventRecord(sk->lat_a[b], sk->stream));
-        const uint32_t* ids = sk->ids.as<uint32_t>() + (r0 - gr0);
+        const uint32_t* ids = ids16 ? reinterpret_cast<const uint32_t*>(sk->ids.as<uint16_t>() + (r0 - gr0))
+                                    : sk->ids.as<uint32_t>() + (r0 - gr0);
         if (fast) {
           const uint32_t slot = static_cast<uint32_t>(b & 1u);
           uint32_t* cnt = sk->cnt[slot].as<uint32_t>();
           ACE_CUDA(tmark(1, false));
           ACE_CUDA(launch_stream_apply(ids, rows, grows, f->d.tables, f->d.k_bits, sk->counters, cnt, slot, p_cnt,
-                                       p_rows, p_flags, nullptr, p_slot, alpha, sk->st, sk->stream));
+                                       p_rows, p_flags, nullptr, p_slot, alpha, sk->st, sk->stream, ids16 ? 1 : 0));
           ACE_CUDA(tmark(1, true));
           if (batch_ms && p_rows) ACE_CUDA(cudaEventRecord(sk->lat_b[p_b], sk->stream));
           p_cnt = cnt;

@@ -132,6 +132,25 @@ __device__ __forceinline__ void insert_bucket_warp(uint32_t* ct, uint32_t bucket
   if ((rem >> lane) & 1u) atomicAdd(&ct[bucket], 1u);
 }
 
+// Bucket ids are u32, or u16 for the stream driver (K <= 16): element idx of
+// the table-major id array.
+__device__ __forceinline__ uint32_t id_get(const TcArgs& a, uint64_t idx) {
+  return a.ids16 ? static_cast<uint32_t>(__ldcg(reinterpret_cast<const unsigned short*>(a.ids) + idx)) : __ldcg(a.ids + idx);
+}
+__device__ __forceinline__ void id_put(const TcArgs& a, uint64_t idx, uint32_t v) {
+  if (a.ids16)
+    reinterpret_cast<unsigned short*>(a.ids)[idx] = static_cast<unsigned short>(v);
+  else
+    a.ids[idx] = v;
+}
+// atomic XOR of bits m into id idx (a u16 id through its aligned 32-bit word); the old id
+__device__ __forceinline__ uint32_t id_xor(const TcArgs& a, uint64_t idx, uint32_t m) {
+  if (!a.ids16) return atomicXor(a.ids + idx, m);
+  const uintptr_t p = reinterpret_cast<uintptr_t>(reinterpret_cast<unsigned short*>(a.ids) + idx);
+  const uint32_t sh = (p & 2u) ? 16u : 0u;
+  return (atomicXor(reinterpret_cast<uint32_t*>(p & ~static_cast<uintptr_t>(3)), m << sh) >> sh) & 0xffffu;
+}
+
 // Shared tail of the near-tie recheck, run by the kTail threads once the
 // main loop is over: one group of 8 lanes per listed item (the CTA's list
 // slots [0, cnt)), four items per warp in flight.  The lanes split the d
@@ -192,9 +211,9 @@ __device__ __noinline__ void recheck_tail(const TcArgs& a, unsigned long long* s
       near = near_tie_1e6(e, nx, a.wnorm64[dir]);
     }
     const uint32_t table = dir / K, bpos = K - 1u - dir % K;
-    uint32_t* id = &a.ids[static_cast<uint64_t>(table) * a.ids_ld + row];
-    if (((__ldcg(id) >> bpos) & 1u) != exact) {
-      const uint32_t old = atomicXor(id, 1u << bpos);
+    const uint64_t idx = static_cast<uint64_t>(table) * a.ids_ld + row;
+    if (((id_get(a, idx) >> bpos) & 1u) != exact) {
+      const uint32_t old = id_xor(a, idx, 1u << bpos);
       if (a.fused_insert) {
         uint32_t* ct = a.counters + (static_cast<uint64_t>(table) << K);
         atomicSub(&ct[old], 1u);
@@ -212,15 +231,15 @@ __device__ __noinline__ void recheck_tail(const TcArgs& a, unsigned long long* s
 // 32 tables span exactly KT sign words, so per group of 32 tables the thread
 // loads its row's KT words once and cuts every bucket with constant shifts
 // (srp.cpp:106-113, bit 0 = MSB); one store per table, coalesced per table.
-template <uint32_t KT>
+template <uint32_t KT, class IdT>
 __device__ __forceinline__ void pack_row_k(const uint32_t* sg, uint32_t r, uint32_t nwords, uint32_t tables,
-                                           uint32_t* idp, uint64_t ids_ld, bool valid) {
+                                           IdT* idp, uint64_t ids_ld, bool valid) {
   constexpr uint32_t kMask = (1u << KT) - 1u;
   for (uint32_t g = 0; g * 32u < tables; ++g) {
     uint32_t w[KT + 1];
 #pragma unroll
     for (uint32_t i = 0; i <= KT; ++i) w[i] = sg[min(g * KT + i, nwords - 1u) * kRows + r];
-    uint32_t* p = idp + static_cast<uint64_t>(g) * 32u * ids_ld;
+    IdT* p = idp + static_cast<uint64_t>(g) * 32u * ids_ld;
     const uint32_t left = tables - g * 32u;
 #pragma unroll
     for (uint32_t u = 0; u < 32u; ++u) {
@@ -230,7 +249,7 @@ __device__ __forceinline__ void pack_row_k(const uint32_t* sg, uint32_t r, uint3
         b = (w[i] >> (32u - sh - KT)) & kMask;
       else
         b = __funnelshift_l(w[i + 1], w[i], sh + KT - 32u) & kMask;
-      if (valid && u < left) *p = b;
+      if (valid && u < left) *p = static_cast<IdT>(b);
       p += ids_ld;
     }
   }
@@ -417,10 +436,12 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
       const uint32_t* sg = Ssm + static_cast<size_t>(sb) * (L.sgn_bytes / 4u);
       const uint64_t row = tile_of(itp) * kRows + r;
       const bool valid = row < a.n;
-      uint32_t* idp = a.ids + row;
       if constexpr (ACE_TC_DBG & 4) {
       } else if constexpr (KT != 0) {
-        pack_row_k<KT>(sg, r, L.nwords, a.tables, idp, a.ids_ld, valid);
+        if (a.ids16)
+          pack_row_k<KT>(sg, r, L.nwords, a.tables, reinterpret_cast<unsigned short*>(a.ids) + row, a.ids_ld, valid);
+        else
+          pack_row_k<KT>(sg, r, L.nwords, a.tables, a.ids + row, a.ids_ld, valid);
       } else {
       // eight tables at a time: all sixteen word loads in flight first (a
       // table needs the next word only if it straddles, which then exists)
@@ -436,7 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
 #pragma unroll
         for (uint32_t u = 0; u < 8u; ++u) {
           const uint32_t tt = t0 + u;
-          if (valid && tt < a.tables) idp[static_cast<uint64_t>(tt) * a.ids_ld] = bk[u];
+          if (valid && tt < a.tables) id_put(a, static_cast<uint64_t>(tt) * a.ids_ld + row, bk[u]);
           if (a.fused_insert && tt < a.tables)
             insert_bucket_warp(a.counters + (static_cast<uint64_t>(tt) << K), bk[u], valid, lane);
         }
@@ -678,9 +699,9 @@ __global__ void recheck_rows_kernel(const TcArgs a) {
       bucket = (bucket << 1) | (p >= 0.0 ? 1u : 0u);
       if (near_tie_1e6(p, nx, a.wnorm64[dir])) ++nt;
     }
-    uint32_t* id = &a.ids[static_cast<uint64_t>(table) * a.ids_ld + row];
-    const uint32_t old = *id;
-    *id = bucket;
+    const uint64_t ix = static_cast<uint64_t>(table) * a.ids_ld + row;
+    const uint32_t old = id_get(a, ix);
+    id_put(a, ix, bucket);
     if (a.fused_insert && old != bucket) {
       uint32_t* ct = a.counters + (static_cast<uint64_t>(table) << K);
       atomicSub(&ct[old], 1u);

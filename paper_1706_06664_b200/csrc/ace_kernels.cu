@@ -1335,6 +1335,7 @@ struct StreamApplyArgs {
   uint32_t slot_b;               // cut slot of the previous batch
   double alpha;
   DevState* st;
+  int ids16;                     // ids stored as u16 (stream_pair_kernel only)
 };
 
 // Block b of G -> (table, bin range): the first G % L tables get one range more.
@@ -1646,12 +1647,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_pair_ke
   SPP(1);
   const uint64_t i0 = a.n * r / 2, i1 = a.n * (r + 1) / 2;
   const uint32_t* idt = a.ids + static_cast<uint64_t>(t) * a.stride;
+  const unsigned short* idt16 = reinterpret_cast<const unsigned short*>(a.ids) + static_cast<uint64_t>(t) * a.stride;
   uint32_t* co = a.cnt_out + static_cast<uint64_t>(t) * a.n;
   auto take = [&](uint64_t i, uint32_t id) {
     co[i] = cs[id];
     atomicAdd(&hs[id >> 1], 1u << ((id & 1u) << 4));
   };
-  if (a.stride % 4 == 0 && i0 % 4 == 0 && i1 % 4 == 0 && (reinterpret_cast<uintptr_t>(a.ids) & 15) == 0) {
+  if (a.ids16) {
+    // u16 ids (K <= 15): 16-byte loads of eight ids, four per thread in flight
+    if (a.stride % 8 == 0 && i0 % 8 == 0 && i1 % 8 == 0 && a.n % 4 == 0 && (reinterpret_cast<uintptr_t>(a.ids) & 15) == 0) {
+      constexpr int kDepth = 4;
+      const uint4* id8 = reinterpret_cast<const uint4*>(idt16 + i0);
+      const uint64_t n8 = (i1 - i0) / 8;
+      for (uint64_t g0 = 0; g0 < n8; g0 += kDepth * blockDim.x) {
+        uint4 q[kDepth];
+#pragma unroll
+        for (int u = 0; u < kDepth; ++u) q[u] = __ldcg(id8 + min(g0 + u * blockDim.x + threadIdx.x, n8 - 1));
+#pragma unroll
+        for (int u = 0; u < kDepth; ++u) {
+          const uint64_t j = g0 + u * blockDim.x + threadIdx.x;
+          if (j < n8) {
+            const uint64_t i = i0 + 8 * j;
+            const uint32_t w[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+            uint32_t c[8];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const uint32_t lo = w[e] & 0xffffu, hi = w[e] >> 16;
+              c[2 * e] = cs[lo];
+              c[2 * e + 1] = cs[hi];
+              atomicAdd(&hs[lo >> 1], 1u << ((lo & 1u) << 4));
+              atomicAdd(&hs[hi >> 1], 1u << ((hi & 1u) << 4));
+            }
+            // the eight counts at batch start as two 16-byte stores
+            uint4* c4 = reinterpret_cast<uint4*>(co + i);
+            c4[0] = make_uint4(c[0], c[1], c[2], c[3]);
+            c4[1] = make_uint4(c[4], c[5], c[6], c[7]);
+          }
+        }
+      }
+    } else {
+      for (uint64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) take(i, __ldcg(idt16 + i));
+    }
+  } else if (a.stride % 4 == 0 && i0 % 4 == 0 && i1 % 4 == 0 && a.n % 4 == 0 &&
+             (reinterpret_cast<uintptr_t>(a.ids) & 15) == 0) {
     constexpr int kDepth = 8;  // 16-byte id loads in flight per thread
     const uint4* id4 = reinterpret_cast<const uint4*>(idt + i0);
     const uint64_t n4 = (i1 - i0) / 4;
@@ -1664,10 +1702,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_pair_ke
         const uint64_t j = g0 + u * blockDim.x + threadIdx.x;
         if (j < n4) {
           const uint64_t i = i0 + 4 * j;
-          take(i, q[u].x);
-          take(i + 1, q[u].y);
-          take(i + 2, q[u].z);
-          take(i + 3, q[u].w);
+          const uint32_t w[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+          uint32_t c[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            c[e] = cs[w[e]];
+            atomicAdd(&hs[w[e] >> 1], 1u << ((w[e] & 1u) << 4));
+          }
+          *reinterpret_cast<uint4*>(co + i) = make_uint4(c[0], c[1], c[2], c[3]);  // one 16-byte store
         }
       }
     }
@@ -1945,10 +1987,14 @@ uint32_t stream_blocks(uint32_t tables, uint32_t k_bits) {
   return std::max<uint32_t>(static_cast<uint32_t>(dev_sms()), tables * std::max(pmin, 1u));
 }
 
+bool stream_pair_ok(uint32_t tables, uint32_t k_bits, uint64_t batch) {
+  return k_bits <= 15 && (batch + 1) / 2 <= 65535u && 2u * tables <= static_cast<uint32_t>(dev_sms());
+}
+
 cudaError_t launch_stream_apply(const uint32_t* ids, uint64_t n, uint64_t ids_stride, uint32_t tables, uint32_t k_bits,
                                 uint32_t* counters, uint32_t* cnt_out, uint32_t slot_a, const uint32_t* cnt_in,
                                 uint64_t n_prev, uint32_t* flag_bits, double* scores, uint32_t slot_b, double alpha,
-                                DevState* st, cudaStream_t s) {
+                                DevState* st, cudaStream_t s, int ids16) {
   if (n == 0 && n_prev == 0) return cudaSuccess;
   if (k_bits > 16) return cudaErrorInvalidValue;
   StreamApplyArgs a{};
@@ -1967,6 +2013,7 @@ cudaError_t launch_stream_apply(const uint32_t* ids, uint64_t n, uint64_t ids_st
   a.slot_b = slot_b;
   a.alpha = alpha;
   a.st = st;
+  a.ids16 = ids16;
   cudaError_t e;
   if (k_bits <= 15 && (n + 1) / 2 <= 65535u && (n == 0 || 2u * tables <= static_cast<uint32_t>(dev_sms()))) {
     // one cluster of two CTAs per table; the remaining CTAs (at least 16
@@ -1980,6 +2027,7 @@ cudaError_t launch_stream_apply(const uint32_t* ids, uint64_t n, uint64_t ids_st
     count_launch();
     return cudaGetLastError();
   }
+  if (ids16) return cudaErrorInvalidValue;  // u16 ids: the pair kernel only
   const uint32_t G = stream_blocks(tables, k_bits);
   const uint32_t base = G / tables;  // smallest ranges per table
   const uint32_t range = ((1u << k_bits) + base - 1u) / base + 4u;

@@ -75,10 +75,13 @@ cudaError_t launch_stream_score(const uint32_t* ids, uint64_t n, uint32_t tables
 // against slot_b's cut) and phase A of batch b (counts at batch start into
 // cnt_out [L][n], insert, T exact; the cut of batch b recorded in slot_a).
 // n = 0: phase B only; n_prev = 0: phase A only.
+// The stream driver hashes into u16 ids (ids16) where the pair kernel runs
+// (K <= 15, batches of at most 2 x 65,535 rows, two CTAs per table fit).
+bool stream_pair_ok(uint32_t tables, uint32_t k_bits, uint64_t batch);
 cudaError_t launch_stream_apply(const uint32_t* ids, uint64_t n, uint64_t ids_stride, uint32_t tables, uint32_t k_bits,
                                 uint32_t* counters, uint32_t* cnt_out, uint32_t slot_a, const uint32_t* cnt_in,
                                 uint64_t n_prev, uint32_t* flag_bits, double* scores, uint32_t slot_b, double alpha,
-                                DevState* st, cudaStream_t s);
+                                DevState* st, cudaStream_t s, int ids16 = 0);
 
 // Per-point path (AceSketch::insert / score / detect_stream one query at a
 // time, sketch.hpp:33,42, detect.hpp:34-36): up to kPointMaxRows rows passed

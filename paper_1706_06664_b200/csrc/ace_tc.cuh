@@ -37,6 +37,7 @@ struct TcArgs {
   float margin_c;             // relative error bound
   uint32_t* ids;              // table-major, stride ids_ld
   uint64_t ids_ld;            // ids row stride per table (>= n; a chunk of a longer batch writes into it)
+  int ids16;                  // ids stored as u16 (K <= 16; the stream driver), else u32
   unsigned long long* near_list;  // (row << 32) | direction; one segment per CTA
   unsigned long long near_cap;    // total entries (near_cap / grid per CTA)
   const double* w64;              // the reference's W (binary64) for the exact recheck
