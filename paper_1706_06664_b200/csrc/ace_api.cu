@@ -537,11 +537,13 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
     const bool fused = insert && sk->width == 32 && fire_and_forget_ok(sk, n) && f->d.k_bits > 20;
     t.fused_insert = fused ? 1 : 0;
     if (!tc_direct_ok(xd, t.x_f64, ld)) ACE_CUDA(sk->xf32.ensure(tc_stage_bytes(n, f->d.dim)));
+    ACE_CUDA(sk->segc.ensure(static_cast<size_t>(tc_grid(n)) * sizeof(uint32_t)));
+    t.seg_counts = sk->segc.as<uint32_t>();
     sk->mark(4);
     sk->mark(6);
     ACE_CUDA(launch_hash_tc(t, sk->xf32.p, sk->stream));
     sk->mark(5);
-    ACE_CUDA(launch_recheck(t, sk->stream));
+    ACE_CUDA(launch_recheck_near(t, sk->stream));
     if (fused) {
       // T = sum of squared counters (exact: 32-bit, unsaturated)
       ACE_CUDA(cudaMemsetAsync(&sk->st->T, 0, sizeof(unsigned long long), sk->stream));

@@ -48,11 +48,9 @@ namespace {
 constexpr uint32_t kEpiQ = 4;        // epilogue warps per TMEM lane quarter (one 32-column group each)
 constexpr uint32_t kConvW = 2u + 4u * kEpiQ;  // first converter warp
 constexpr int kThreads = 32 * (kConvW + 4);   // 22 warps
-constexpr uint32_t kTail = kThreads - 64;     // warps 2..: the shared recheck tail
 constexpr uint32_t kMaxWStages = 8;
 constexpr uint32_t kRawBox = 16384;  // one raw box: 128 rows x 32 fp32 (SW128)
 constexpr uint32_t kConvBar = 10;    // named barrier of the converter warps
-constexpr uint32_t kTailBar = 9;     // named barrier of the shared tail
 
 // Compile-time instrumentation (-DACE_TC_PROF=1, profiling builds only):
 // clock64 cycles per pipeline section summed over CTAs into g_tc_prof
@@ -62,7 +60,8 @@ constexpr uint32_t kTailBar = 9;     // named barrier of the shared tail
 #endif
 // Experiment switches (profiling builds only; results are then wrong):
 // 1 = epilogue skips the sign / near-tie work, 2 = no MMAs issued,
-// 4 = packers skip the bucket cut and stores
+// 4 = packers skip the bucket cut and stores, 8 = W loaded for the first
+// point tile only, 64 = near ties not listed
 #ifndef ACE_TC_DBG
 #define ACE_TC_DBG 0
 #endif
@@ -151,80 +150,86 @@ __device__ __forceinline__ uint32_t id_xor(const TcArgs& a, uint64_t idx, uint32
   return (atomicXor(reinterpret_cast<uint32_t*>(p & ~static_cast<uintptr_t>(3)), m << sh) >> sh) & 0xffffu;
 }
 
-// Shared tail of the near-tie recheck, run by the kTail threads once the
-// main loop is over: one group of 8 lanes per listed item (the CTA's list
-// slots [0, cnt)), four items per warp in flight.  The lanes split the d
-// products x_i w_i (binary64: exact for fp32 x, one rounding for fp64 x) and
-// sum them in a tree: p1 and the reference's sequential left fold
+// Exact decision of one listed near tie by a group of kG lanes (all lanes of
+// the warp call it together; `live` false for idle groups).  The lanes split
+// the d products x_i w_i (binary64: exact for fp32 x, one rounding for fp64
+// x) and sum them in a tree: p1 and the reference's sequential left fold
 // (srp.cpp:78-91) are both within gamma_{d+2} A of the exact value (A = sum
 // |x_i w_i|), so |p1| > 2 gamma A decides the reference's sign bit; likewise
 // the BASELINE near-tie measure |p| < 1e-6 |x||w| where p1 is clear of its
 // threshold.  Otherwise (never seen on the BASELINE data) the group's first
 // lane evaluates the reference's fold and the oracle's sequential |x|^2
-// themselves.  Wrong fast bits are flipped in ids (and, with the fused
-// insert, the count moves to the corrected bucket).  Slots are reset to ~0
-// for the next launch.
-__device__ __noinline__ void recheck_tail(const TcArgs& a, unsigned long long* seg, uint32_t cnt, uint32_t et,
-                                          unsigned long long& rr, unsigned long long& ff, unsigned long long& nt) {
-  constexpr uint32_t kG = 8;  // lanes per item
+// themselves.  A wrong fast bit is flipped in the ids (and, with the fused
+// insert, the count moves to the corrected bucket).
+constexpr uint32_t kG = 8;  // lanes per item
+__device__ __forceinline__ void recheck_item(const TcArgs& a, unsigned long long item, bool live, uint32_t gl,
+                                             unsigned long long& rr, unsigned long long& ff, unsigned long long& nt) {
   const uint32_t dim = static_cast<uint32_t>(a.dim), K = a.k_bits;
-  const uint32_t gl = et % kG, grp = et / kG, ngrp = kTail / kG;
   const double gam = static_cast<double>(dim + 2) * 0x1.0p-53 / (1.0 - static_cast<double>(dim + 2) * 0x1.0p-53);
   const double bound_rel = 2.0 * gam * (1.0 + 4.0 * gam);
-  const uint32_t rounds = (cnt + ngrp - 1) / ngrp;  // warp-uniform trip count (shuffles below)
-  for (uint32_t rd = 0; rd < rounds; ++rd) {
-    const uint32_t i = rd * ngrp + grp;
-    const bool live = i < cnt;
-    const unsigned long long item = live ? seg[i] : 0ull;
-    const uint64_t row = item >> 32;
-    const uint32_t dir = static_cast<uint32_t>(item & 0xffffffffu);
-    const double* w = a.w64 + static_cast<uint64_t>(dir) * dim;
-    double p = 0.0, ab = 0.0, xx = 0.0;
-    if (live) {
-      for (uint32_t k = gl; k < dim; k += kG) {
-        const double xv = a.x_f64 ? static_cast<const double*>(a.x)[row * a.ld + k]
-                                  : static_cast<double>(static_cast<const float*>(a.x)[row * a.ld + k]);
-        const double t = xv * __ldg(w + k);
-        p += t;
-        ab += fabs(t);
-        xx += xv * xv;
-      }
-    }
+  const uint64_t row = item >> 32;
+  const uint32_t dir = static_cast<uint32_t>(item & 0xffffffffu);
+  const double* w = a.w64 + static_cast<uint64_t>(dir) * dim;
+  const uint32_t table = dir / K, bpos = K - 1u - dir % K;
+  const uint64_t idx = static_cast<uint64_t>(table) * a.ids_ld + row;
+  // the deciding lane's other loads issued up front, beside the row loads
+  const bool lead = live && gl == 0;
+  const double wn = lead ? __ldg(a.wnorm64 + dir) : 0.0;
+  const uint32_t id0 = lead ? id_get(a, idx) : 0u;
+  double p = 0.0, ab = 0.0, xx = 0.0;
+  if (live) {
+    // eight elements per lane per round, all sixteen loads issued before any
+    // is used (the rows come from HBM: latency bounds this)
+    for (uint32_t k0 = 0; k0 < dim; k0 += 8u * kG) {
+      double xv[8], wv[8];
 #pragma unroll
-    for (uint32_t o = kG / 2; o > 0; o >>= 1) {
-      p += __shfl_xor_sync(0xffffffffu, p, o);
-      ab += __shfl_xor_sync(0xffffffffu, ab, o);
-      xx += __shfl_xor_sync(0xffffffffu, xx, o);
-    }
-    if (!live || gl != 0) continue;
-    const double err = bound_rel * ab + 0x1.0p-1000;
-    const double lim = 1e-6 * (sqrt(xx) * a.wnorm64[dir]);
-    const bool sign_ok = fabs(p) > err;
-    const bool near_sure = fabs(p) + err < lim * (1.0 - 1e-9);
-    const bool far_sure = fabs(p) - err > lim * (1.0 + 1e-9);
-    uint32_t exact = p >= 0.0 ? 1u : 0u;
-    bool near = near_sure;
-    if (!sign_ok || !(near_sure || far_sure)) {
-      double nx = 0.0;
-      const double e = exact_proj_nx(w, a.x, a.x_f64, row, a.ld, dim, &nx);
-      exact = e >= 0.0 ? 1u : 0u;
-      near = near_tie_1e6(e, nx, a.wnorm64[dir]);
-    }
-    const uint32_t table = dir / K, bpos = K - 1u - dir % K;
-    const uint64_t idx = static_cast<uint64_t>(table) * a.ids_ld + row;
-    if (((id_get(a, idx) >> bpos) & 1u) != exact) {
-      const uint32_t old = id_xor(a, idx, 1u << bpos);
-      if (a.fused_insert) {
-        uint32_t* ct = a.counters + (static_cast<uint64_t>(table) << K);
-        atomicSub(&ct[old], 1u);
-        atomicAdd(&ct[old ^ (1u << bpos)], 1u);
+      for (uint32_t u = 0; u < 8u; ++u) {
+        const uint32_t k = min(k0 + u * kG + gl, dim - 1u);
+        xv[u] = a.x_f64 ? static_cast<const double*>(a.x)[row * a.ld + k]
+                        : static_cast<double>(static_cast<const float*>(a.x)[row * a.ld + k]);
+        wv[u] = __ldg(w + k);
       }
-      ++ff;
+#pragma unroll
+      for (uint32_t u = 0; u < 8u; ++u)
+        if (k0 + u * kG + gl < dim) {
+          const double t = xv[u] * wv[u];
+          p += t;
+          ab += fabs(t);
+          xx += xv[u] * xv[u];
+        }
     }
-    if (near) ++nt;
-    ++rr;
-    seg[i] = ~0ull;  // the list is all ~0 between launches
   }
+#pragma unroll
+  for (uint32_t o = kG / 2; o > 0; o >>= 1) {
+    p += __shfl_xor_sync(0xffffffffu, p, o);
+    ab += __shfl_xor_sync(0xffffffffu, ab, o);
+    xx += __shfl_xor_sync(0xffffffffu, xx, o);
+  }
+  if (!lead) return;
+  const double err = bound_rel * ab + 0x1.0p-1000;
+  const double lim = 1e-6 * (sqrt(xx) * wn);
+  const bool sign_ok = fabs(p) > err;
+  const bool near_sure = fabs(p) + err < lim * (1.0 - 1e-9);
+  const bool far_sure = fabs(p) - err > lim * (1.0 + 1e-9);
+  uint32_t exact = p >= 0.0 ? 1u : 0u;
+  bool near = near_sure;
+  if (!sign_ok || !(near_sure || far_sure)) {
+    double nx = 0.0;
+    const double e = exact_proj_nx(w, a.x, a.x_f64, row, a.ld, dim, &nx);
+    exact = e >= 0.0 ? 1u : 0u;
+    near = near_tie_1e6(e, nx, wn);
+  }
+  if (((id0 >> bpos) & 1u) != exact) {
+    const uint32_t old = id_xor(a, idx, 1u << bpos);
+    if (a.fused_insert) {
+      uint32_t* ct = a.counters + (static_cast<uint64_t>(table) << K);
+      atomicSub(&ct[old], 1u);
+      atomicAdd(&ct[old ^ (1u << bpos)], 1u);
+    }
+    ++ff;
+  }
+  if (near) ++nt;
+  ++rr;
 }
 
 // Bucket packing with a compile-time K (KT = 15, 16: the BASELINE shapes):
@@ -265,7 +270,6 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
   __shared__ float thr_sm[2][kRows];    // row thresholds per tile parity (converters -> epilogue)
   __shared__ uint32_t lom_sm[2][4];     // K16 steps with a nonzero x lo part, per A buffer / lane quarter
   __shared__ uint32_t seg_n;            // near ties pushed by this CTA
-  __shared__ unsigned long long blk_rech, blk_flip, blk_near;
 
   const uint32_t TW = a.tw, wblk = a.tw * 128u;  // direction tile width, one W block (hi or lo) in bytes
   const TcLayout L = tc_layout(a.dim, TW, a.k_bits * a.tables);
@@ -285,7 +289,6 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
 
   if (threadIdx.x == 0) {
     seg_n = 0;
-    blk_rech = blk_flip = blk_near = 0;
     for (uint32_t s = 0; s < L.n_wst; ++s) {
       mbar_init(&bar_wfull[s], 1);
       mbar_init(&bar_wempty[s], 1);
@@ -314,7 +317,8 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
   const unsigned long long seg_cap = a.near_cap / gridDim.x;
   unsigned long long* seg = a.near_list + blockIdx.x * seg_cap;
   const uint32_t a_col0 = L.nacc * TW;  // first TMEM column of the A buffers
-  unsigned long long rr_own = 0, ff_own = 0, nt_own = 0;
+  uint32_t dbg_sink = 0;
+  (void)dbg_sink;
   TCP_DECL;
   const long long t_kernel = clock64();
   (void)t_kernel;
@@ -328,6 +332,14 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
           const uint32_t bytes = ((min(TW, R - j * TW) + 15u) & ~15u) * 128u;  // rows of the MMA's N
           for (uint32_t kc = 0; kc < a.nkc; ++kc) {
             mbar_wait_sleepy(&bar_wempty[s], ph ^ 1u);
+            if ((ACE_TC_DBG & 8) && it > 0) {
+              mbar_arrive(&bar_wfull[s]);
+              if (++s == L.n_wst) {
+                s = 0;
+                ph ^= 1u;
+              }
+              continue;
+            }
             mbar_expect_tx(&bar_wfull[s], 2u * bytes);
             const uint8_t* src = reinterpret_cast<const uint8_t*>(a.w16) + (static_cast<uint64_t>(j) * a.nkc + kc) * 2u * wblk;
             uint8_t* dst = Wsm + static_cast<size_t>(s) * 2u * wblk;
@@ -614,11 +626,20 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
           // columns past R (padding / stale) are masked here, off the hot path
           if (live && !(mn > thr)) {
             const uint32_t ncol = min(32u, R - 32u * gw);
+            // only the 8-column chains whose min is inside the bound
             uint32_t nm = 0u;
 #pragma unroll
-            for (int jj = 0; jj < 32; ++jj) nm |= (((v[jj] << 1) <= thr_u) ? 1u : 0u) << jj;
+            for (int gq = 0; gq < 4; ++gq)
+              if (!(m4[gq] > thr)) {
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) nm |= (((v[gq * 8 + jj] << 1) <= thr_u) ? 1u : 0u) << (gq * 8 + jj);
+              }
             if (ncol < 32u) nm &= (1u << ncol) - 1u;
-            if (nm) push_near_mask(a.st, seg, seg_cap, &seg_n, a.overflow_rows, nm, row, 32u * gw);
+            if (ACE_TC_DBG & 128) {
+              dbg_sink += __popc(nm);
+            } else if (nm && !(ACE_TC_DBG & 64)) {
+              push_near_mask(a.st, seg, seg_cap, &seg_n, a.overflow_rows, nm, row, 32u * gw);
+            }
           }
           TCP_END(13);
         }
@@ -633,28 +654,13 @@ __global__ void __launch_bounds__(kThreads, 1) hash_tc_kernel(const TcArgs a, co
   }
 
   TCP_FLUSH(warp == 2 && lane == 0);
-  if (warp >= 2) {
-    // ---- shared tail: exact recheck of the listed near ties ----
-    asm volatile("bar.sync %0, %1;" ::"r"(kTailBar), "r"(kTail) : "memory");  // ids stored, list complete
-    const uint32_t et = threadIdx.x - 64u;
-    const uint32_t cnt = static_cast<uint32_t>(min(static_cast<unsigned long long>(seg_n), seg_cap));
-    recheck_tail(a, seg, cnt, et, rr_own, ff_own, nt_own);
-    rr_own = warp_sum_u64(rr_own);
-    ff_own = warp_sum_u64(ff_own);
-    nt_own = warp_sum_u64(nt_own);
-    if (lane == 0) {
-      if (rr_own) atomicAdd(&blk_rech, rr_own);
-      if (ff_own) atomicAdd(&blk_flip, ff_own);
-      if (nt_own) atomicAdd(&blk_near, nt_own);
-    }
-    asm volatile("bar.sync %0, %1;" ::"r"(kTailBar), "r"(kTail) : "memory");
-    if (et == 0) {
-      if (blk_rech) atomicAdd(&a.st->rechecked, blk_rech);
-      if (blk_flip) atomicAdd(&a.st->flipped, blk_flip);
-      if (blk_near) atomicAdd(&a.st->near_ties, blk_near);
-      if (seg_n) atomicAdd(&a.st->near_count, static_cast<unsigned long long>(seg_n));
-      if (a.fused_insert && blockIdx.x == 0) atomicAdd(&a.st->n, a.n);
-    }
+  // the listed near ties are decided by recheck_near_kernel (next launch,
+  // every SM): publish this CTA's list length
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    a.seg_counts[blockIdx.x] = static_cast<uint32_t>(min(static_cast<unsigned long long>(seg_n), seg_cap));
+    if (seg_n) atomicAdd(&a.st->near_count, static_cast<unsigned long long>(seg_n));
+    if (a.fused_insert && blockIdx.x == 0) atomicAdd(&a.st->n, a.n);
   }
 #if ACE_TC_PROF
   if (threadIdx.x == 0) atomicAdd(&g_tc_prof[16], static_cast<unsigned long long>(clock64() - t_kernel));
@@ -681,7 +687,71 @@ __global__ void stage_f32_kernel(const void* __restrict__ x, int x_f64, uint64_t
   }
 }
 
-// rows whose near ties overflowed the list: every bucket recomputed exactly
+// The near ties listed by hash_tc_kernel, decided exactly (recheck_item): kG
+// lanes per item, blocks dealt over the kernel's list segments (several
+// blocks per segment).  Items of rows whose list overflowed are left to the
+// second part, which recomputes every bucket of those rows exactly.  Slots
+// are reset to ~0 (the list is all ~0 between launches).
+__global__ void __launch_bounds__(256) recheck_near_kernel(const TcArgs a, uint32_t nseg) {
+  const uint32_t gl = threadIdx.x % kG, grp = threadIdx.x / kG, ngb = blockDim.x / kG;
+  const uint32_t P = gridDim.x / nseg;  // blocks per segment
+  const uint32_t b = blockIdx.x % nseg, sub = blockIdx.x / nseg;
+  const unsigned long long seg_cap = a.near_cap / nseg;
+  unsigned long long* seg = a.near_list + b * seg_cap;
+  const uint32_t cnt = sub < P ? a.seg_counts[b] : 0u;
+  const bool ovf = a.st->near_overflow != 0;
+  unsigned long long rr = 0, ff = 0, nt = 0;
+  const uint32_t per = P * ngb, rounds = (cnt + per - 1) / per;  // block-uniform (shuffles)
+  for (uint32_t rd = 0; rd < rounds; ++rd) {
+    const uint32_t i = rd * per + sub * ngb + grp;
+    bool live = i < cnt;
+    const unsigned long long item = live ? seg[i] : 0ull;
+    if (live && ovf) {
+      const uint64_t row = item >> 32;
+      if ((a.overflow_rows[row >> 5] >> (row & 31)) & 1u) live = false;  // whole row below
+    }
+    recheck_item(a, item, live, gl, rr, ff, nt);
+    if (i < cnt && gl == 0) seg[i] = ~0ull;
+  }
+  if (ovf) {
+    // rows whose near ties overflowed the list: every bucket recomputed exactly
+    const uint32_t K = a.k_bits;
+    for (uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < a.n * a.tables;
+         idx += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+      const uint64_t row = idx / a.tables;
+      const uint32_t table = static_cast<uint32_t>(idx % a.tables);
+      if (!((a.overflow_rows[row >> 5] >> (row & 31)) & 1u)) continue;
+      uint32_t bucket = 0;
+      for (uint32_t bb = 0; bb < K; ++bb) {
+        const uint32_t dir = table * K + bb;
+        double nx = 0.0;
+        const double p = exact_proj_nx(a.w64 + static_cast<uint64_t>(dir) * a.dim, a.x, a.x_f64, row, a.ld, a.dim, &nx);
+        bucket = (bucket << 1) | (p >= 0.0 ? 1u : 0u);
+        if (near_tie_1e6(p, nx, a.wnorm64[dir])) ++nt;
+      }
+      const uint64_t ix = static_cast<uint64_t>(table) * a.ids_ld + row;
+      const uint32_t old = id_get(a, ix);
+      id_put(a, ix, bucket);
+      if (a.fused_insert && old != bucket) {
+        uint32_t* ct = a.counters + (static_cast<uint64_t>(table) << K);
+        atomicSub(&ct[old], 1u);
+        atomicAdd(&ct[bucket], 1u);
+      }
+      rr += K;
+    }
+  }
+  rr = warp_sum_u64(rr);
+  ff = warp_sum_u64(ff);
+  nt = warp_sum_u64(nt);
+  if ((threadIdx.x & 31u) == 0) {
+    if (rr) atomicAdd(&a.st->rechecked, rr);
+    if (ff) atomicAdd(&a.st->flipped, ff);
+    if (nt) atomicAdd(&a.st->near_ties, nt);
+  }
+}
+
+// rows whose near ties overflowed the list (the K-streamed path, after its
+// own segment recheck): every bucket recomputed exactly
 __global__ void recheck_rows_kernel(const TcArgs a) {
   if (!a.st->near_overflow) return;
   const uint32_t K = a.k_bits;
@@ -872,8 +942,7 @@ cudaError_t launch_hash_tc(const TcArgs& a, void* stage, cudaStream_t s) {
                                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-  const uint64_t tiles = (a.n + kRows - 1) / kRows;
-  const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(tc_sms()));
+  const uint64_t grid = tc_grid(a.n);
   const size_t smem = tc_layout(a.dim, a.tw, a.k_bits * a.tables).total;
   // compile-time K packers for the BASELINE shapes (never with the fused insert, K > 20)
   if (a.k_bits == 15 && !a.fused_insert)
@@ -897,6 +966,21 @@ extern "C" int ace_debug_tc_prof(unsigned long long* out24, int reset) {
   return 0;
 }
 #endif
+
+uint32_t tc_grid(uint64_t n) {
+  return static_cast<uint32_t>(std::min<uint64_t>((n + kRows - 1) / kRows, static_cast<uint64_t>(tc_sms())));
+}
+
+cudaError_t launch_recheck_near(const TcArgs& a, cudaStream_t s) {
+  if (a.n == 0) return cudaSuccess;
+  const uint32_t nseg = tc_grid(a.n);
+  // eight blocks (256 items) per list segment: one round for the BASELINE
+  // shapes' ~40-260 items per segment
+  const uint32_t per = std::max<uint32_t>(1u, (8u * static_cast<uint32_t>(tc_sms()) + nseg - 1u) / nseg);
+  recheck_near_kernel<<<nseg * per, 256, 0, s>>>(a, nseg);
+  count_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t launch_recheck(const TcArgs& a, cudaStream_t s) {
   recheck_rows_kernel<<<148, 256, 0, s>>>(a);  // exits at once unless a list segment overflowed

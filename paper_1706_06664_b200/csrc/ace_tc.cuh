@@ -62,6 +62,11 @@ size_t tc_stage_bytes(uint64_t n, uint64_t dim);
 // Rows whose near ties overflowed their CTA's list: every bucket recomputed
 // exactly (counters moved when the insert was fused).
 cudaError_t launch_recheck(const TcArgs& a, cudaStream_t s);
+// d <= 256: the near ties hash_tc_kernel listed (per-CTA segments, lengths in
+// TcArgs::seg_counts, tc_grid(n) entries) and the overflowed rows, decided
+// exactly in one launch after the projection
+uint32_t tc_grid(uint64_t n);
+cudaError_t launch_recheck_near(const TcArgs& a, cudaStream_t s);
 // K-streamed kernel for d > 256 (nkc > 4): its own conversion, projection and
 // near-tie recheck (per-CTA list segments, counts in TcArgs::seg_counts)
 bool tc_kstream(uint32_t nkc);

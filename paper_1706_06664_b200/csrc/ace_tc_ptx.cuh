@@ -286,7 +286,7 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 // Cold path: push the near-tie columns (bit jj of mask = direction dir0 + jj)
 // into this CTA's list segment; a full segment flags the whole row for the
 // exact recompute instead (recheck_rows_kernel).
-__device__ __noinline__ inline void push_near_mask(DevState* st, unsigned long long* seg, unsigned long long seg_cap,
+__device__ __forceinline__ void push_near_mask(DevState* st, unsigned long long* seg, unsigned long long seg_cap,
                                                    uint32_t* seg_n, uint32_t* overflow_rows, uint32_t mask,
                                                    uint64_t row, uint32_t dir0) {
   while (mask) {
