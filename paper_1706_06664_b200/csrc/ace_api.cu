@@ -494,9 +494,18 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
       ACE_CUDA(sk->near.ensure(cap * sizeof(unsigned long long)));
       if (sk->near.p != before) ACE_CUDA(cudaMemsetAsync(sk->near.p, 0xff, sk->near.bytes, sk->stream));
     }
-    ACE_CUDA(sk->overflow.ensure(((n + 31) / 32) * sizeof(uint32_t)));
-    ACE_CUDA(cudaMemsetAsync(sk->overflow.p, 0, ((n + 31) / 32) * sizeof(uint32_t), sk->stream));
-    ACE_CUDA(cudaMemsetAsync(&sk->st->near_count, 0, 2 * sizeof(unsigned long long), sk->stream));
+    {
+      // the overflow-row bitmap is all 0 and the overflow flag clear between
+      // launches (recheck_near_kernel cleans what it used; the K-streamed path
+      // clears them per launch); fill a newly allocated bitmap
+      const void* before = sk->overflow.p;
+      ACE_CUDA(sk->overflow.ensure(((n + 31) / 32) * sizeof(uint32_t)));
+      if (sk->overflow.p != before) ACE_CUDA(cudaMemsetAsync(sk->overflow.p, 0, sk->overflow.bytes, sk->stream));
+      if (kstream) {
+        ACE_CUDA(cudaMemsetAsync(sk->overflow.p, 0, ((n + 31) / 32) * sizeof(uint32_t), sk->stream));
+        ACE_CUDA(cudaMemsetAsync(&sk->st->near_count, 0, 2 * sizeof(unsigned long long), sk->stream));
+      }
+    }
     t.near_list = sk->near.as<unsigned long long>();
     t.near_cap = sk->near.bytes / sizeof(unsigned long long);
     t.overflow_rows = sk->overflow.as<uint32_t>();

@@ -41,6 +41,7 @@ struct DevState {
   int live_ring[2];
   unsigned int ticket_s;         // phase-A blocks done (the last one commits T and n)
   unsigned long long dT_acc;     // phase-A increments of T pending the last block's commit
+  unsigned int ticket_r;         // recheck_near_kernel: blocks done (the last one cleans the overflow state)
 };
 
 // T / den correctly rounded to binary64 (round half to even), T, den < 2^64:

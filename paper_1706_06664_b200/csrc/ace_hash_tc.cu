@@ -748,6 +748,24 @@ __global__ void __launch_bounds__(256) recheck_near_kernel(const TcArgs a, uint3
     if (ff) atomicAdd(&a.st->flipped, ff);
     if (nt) atomicAdd(&a.st->near_ties, nt);
   }
+  if (ovf) {
+    // the last block to finish clears the overflow bitmap and flag, so the
+    // next projection launch starts clean without a memset
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last = atomicAdd(&a.st->ticket_r, 1u) == gridDim.x - 1u;
+    }
+    __syncthreads();
+    if (last) {
+      for (uint64_t wd = threadIdx.x; wd < (a.n + 31) / 32; wd += blockDim.x) a.overflow_rows[wd] = 0u;
+      if (threadIdx.x == 0) {
+        a.st->near_overflow = 0;
+        a.st->ticket_r = 0u;
+      }
+    }
+  }
 }
 
 // rows whose near ties overflowed the list (the K-streamed path, after its
