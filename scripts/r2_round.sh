@@ -10,7 +10,7 @@ timeout 600 python bench.py --api point > gpurun_out/bench_point.json 2> gpurun_
 if [ "${NCU:-1}" = "1" ]; then
   CFG=5 ROWS=2000000 TAG=r5 bash scripts/launches.sh; cat gpurun_out/launches_r5.txt
   SKIP=12 CFG=2 ROWS=500000 TAG=r2 bash scripts/launches.sh; cat gpurun_out/launches_r2.txt
-  TAG=h5 bash scripts/ncu_hash5.sh; echo "ncu h5 rc=$?"
+  ROWS=524288 TAG=h5 bash scripts/ncu_hash5.sh; echo "ncu h5 rc=$?"
   CFG=2 ROWS=500000 TAG=h2 bash scripts/ncu_hash5.sh; echo "ncu h2 rc=$?"
   TAG=pair bash scripts/ncu_pair.sh; echo "ncu pair rc=$?"
 fi
