@@ -130,6 +130,7 @@ struct AceSketch {
   cudaEvent_t s_copied[2] = {nullptr, nullptr}, s_used[2] = {nullptr, nullptr};
   DevBuf ids, sums, stage, flags, scores, demand, near, overflow, x16, rowthr, segc, xf32;
   DevBuf cnt[2];            // stream: counts at batch start (double-buffered)
+  DevBuf gco, gdT, gdone;   // group stream kernel: counts at batch start, T increments, batches done
   int h2d_chunks = 8;       // pinned host rows of a large batch: copy chunks hashed as they land
   int defer_mode = 0;       // ACE_OPT_DEFER_INSERT
   // stream driver: batches hashed by one projection launch (hashing does not
@@ -183,9 +184,9 @@ struct AceSketch {
     int dtype = 0, out_where = 0, group = 0;
     bool lat = false, ff = false;
     cudaStream_t stream = nullptr;
-    const void* bufs[6] = {};
+    const void* bufs[9] = {};
     bool operator==(const StreamKey& o) const {
-      for (int i = 0; i < 6; ++i)
+      for (int i = 0; i < 9; ++i)
         if (bufs[i] != o.bufs[i]) return false;
       return x == o.x && flags == o.flags && n == o.n && ld == o.ld && batch == o.batch && alpha == o.alpha &&
              dtype == o.dtype && out_where == o.out_where && group == o.group && lat == o.lat && ff == o.ff &&
@@ -447,6 +448,17 @@ ace_status ensure_stream_bufs(AceSketch* sk, uint64_t rows) {
   const size_t cnt_bytes = static_cast<size_t>(rows) * sk->fam->d.tables * sizeof(uint32_t);
   ACE_CUDA(sk->cnt[0].ensure(cnt_bytes));
   ACE_CUDA(sk->cnt[1].ensure(cnt_bytes));
+  return ACE_OK;
+}
+
+ace_status ensure_group_bufs(AceSketch* sk, uint64_t group_batches, uint64_t batch, uint64_t ids_ld) {
+  const uint64_t L = sk->fam->d.tables;
+  ACE_CUDA(sk->gco.ensure(static_cast<size_t>(group_batches) * L * batch * sizeof(uint32_t)));
+  ACE_CUDA(sk->gdT.ensure(static_cast<size_t>(group_batches) * 2 * L * sizeof(unsigned long long)));
+  const void* before = sk->gdone.p;
+  ACE_CUDA(sk->gdone.ensure(static_cast<size_t>(group_batches) * sizeof(unsigned int)));
+  if (sk->gdone.p != before) ACE_CUDA(cudaMemsetAsync(sk->gdone.p, 0, sk->gdone.bytes, sk->stream));
+  ACE_CUDA(sk->ids.ensure(static_cast<size_t>(ids_ld) * L * sizeof(uint16_t)));
   return ACE_OK;
 }
 
@@ -938,6 +950,9 @@ ace_status ace_sketch_destroy(AceSketch* sk) {
   sk->xf32.release();
   sk->cnt[0].release();
   sk->cnt[1].release();
+  sk->gco.release();
+  sk->gdT.release();
+  sk->gdone.release();
   if (sk->counters) cudaFree(sk->counters);
   if (sk->st) cudaFree(sk->st);
   if (sk->hst) cudaFreeHost(sk->hst);
@@ -1450,9 +1465,15 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
   // u16 bucket ids between the projection and the pair stream kernel: half
   // the id traffic (K <= 15, the d <= 256 tensor-core projection)
   const bool ids16 = fast && stream_pair_ok(f->d.tables, f->d.k_bits, batch) && f->use_tc() && !tc_kstream(f->tc.nkc);
+  // one stream launch per hashing group (stream_group_kernel): the tables'
+  // counts stay in shared memory across the group's batches
+  const bool gfast = ids16 && stream_group_ok(f->d.tables, f->d.k_bits, batch);
+  const uint64_t gl = std::min(G, nb);                    // batches per group
+  const uint64_t gld = (std::min(gl * batch, n) + 7) / 8 * 8;  // u16 id stride (16-byte rows)
   ACE_CUDA(sk->flags.ensure(((n + 31) / 32) * sizeof(uint32_t)));
   uint32_t* dflags = (flag_bits && out_where == ACE_DEVICE) ? flag_bits : sk->flags.as<uint32_t>();
-  if (fast && (r = ensure_stream_bufs(sk, std::min(batch, n))) != ACE_OK) return r;
+  if (fast && !gfast && (r = ensure_stream_bufs(sk, std::min(batch, n))) != ACE_OK) return r;
+  if (gfast && (r = ensure_group_bufs(sk, gl, batch, gld)) != ACE_OK) return r;
   // per-batch latency: from the start of the batch's work (its group's
   // hashing for a group's first batch) to the end of the launch that writes
   // its flags; events kept by the sketch across calls
@@ -1509,7 +1530,8 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
     uint32_t p_slot = 0;
     for (uint64_t g0 = 0; g0 < nb; g0 += G) {
       const uint64_t gb = std::min(G, nb - g0), gr0 = g0 * batch, grows = std::min(gb * batch, n - gr0);
-      if (batch_ms) ACE_CUDA(cudaEventRecord(sk->lat_a[g0], sk->stream));
+      if (batch_ms)
+        for (uint64_t b = g0; b < (gfast ? g0 + gb : g0 + 1); ++b) ACE_CUDA(cudaEventRecord(sk->lat_a[b], sk->stream));
       const void* xg = static_cast<const char*>(x) + gr0 * ld * esz;
       const void* xd;
       uint64_t ldd;
@@ -1523,7 +1545,9 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
         xd = sk->sstage[hb].p;
         ldd = ld;
         ACE_CUDA(tmark(0, false));
-        if ((rr = run_hash(sk, xd, dtype, grows, ldd, 0, nullptr, 0, ids16)) != ACE_OK) return rr;
+        if ((rr = run_hash(sk, xd, dtype, grows, ldd, 0, gfast ? sk->ids.as<uint32_t>() : nullptr, gfast ? gld : 0,
+                           ids16)) != ACE_OK)
+          return rr;
         ACE_CUDA(tmark(0, true));
         ACE_CUDA(cudaEventRecord(sk->s_used[hb], sk->stream));
         const uint64_t g1 = g0 + G;
@@ -1537,8 +1561,20 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
       } else {
         if ((rr = stage_x(sk, sk->stage, sk->stream, xg, dtype, grows, ld, x_where, &xd, &ldd)) != ACE_OK) return rr;
         ACE_CUDA(tmark(0, false));
-        if ((rr = run_hash(sk, xd, dtype, grows, ldd, 0, nullptr, 0, ids16)) != ACE_OK) return rr;
+        if ((rr = run_hash(sk, xd, dtype, grows, ldd, 0, gfast ? sk->ids.as<uint32_t>() : nullptr, gfast ? gld : 0,
+                           ids16)) != ACE_OK)
+          return rr;
         ACE_CUDA(tmark(0, true));
+      }
+      if (gfast) {
+        ACE_CUDA(tmark(1, false));
+        ACE_CUDA(launch_stream_group(sk->ids.as<uint16_t>(), gld, grows, batch, f->d.tables, f->d.k_bits, sk->counters,
+                                     sk->gco.as<uint32_t>(), sk->gdT.as<unsigned long long>(),
+                                     sk->gdone.as<unsigned int>(), dflags + gr0 / 32, alpha, sk->st, sk->stream));
+        ACE_CUDA(tmark(1, true));
+        if (batch_ms)
+          for (uint64_t b = g0; b < g0 + gb; ++b) ACE_CUDA(cudaEventRecord(sk->lat_b[b], sk->stream));
+        continue;
       }
       for (uint64_t b = g0; b < g0 + gb; ++b) {
         const uint64_t r0 = b * batch, rows = std::min(batch, n - r0);
@@ -1569,7 +1605,7 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
         if (batch_ms) ACE_CUDA(cudaEventRecord(sk->lat_b[b], sk->stream));
       }
     }
-    if (fast && p_rows) {  // the last batch's phase B
+    if (fast && !gfast && p_rows) {  // the last batch's phase B
       ACE_CUDA(tmark(1, false));
       ACE_CUDA(launch_stream_apply(nullptr, 0, 0, f->d.tables, f->d.k_bits, sk->counters, nullptr, 0, p_cnt, p_rows,
                                    p_flags, nullptr, p_slot, alpha, sk->st, sk->stream));
@@ -1598,8 +1634,9 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
   key.group = sk->stream_group;
   key.stream = sk->stream;
   key.ff = ff;
-  const DevBuf* sb[6] = {&sk->ids, &sk->flags, &sk->cnt[0], &sk->cnt[1], &sk->near, &sk->overflow};
-  for (int i = 0; i < 6; ++i) key.bufs[i] = sb[i]->p;
+  const DevBuf* sb[9] = {&sk->ids, &sk->flags, &sk->cnt[0], &sk->cnt[1], &sk->near, &sk->overflow,
+                         &sk->gco, &sk->gdT, &sk->gdone};
+  for (int i = 0; i < 9; ++i) key.bufs[i] = sb[i]->p;
   // (per-batch latency events are recorded only outside graphs)
   const bool eligible = x_where == ACE_DEVICE && !sk->timing && fast && !batch_ms;
   if (eligible && sk->sgexec && key == sk->sgkey) {

@@ -42,6 +42,10 @@ struct DevState {
   unsigned int ticket_s;         // phase-A blocks done (the last one commits T and n)
   unsigned long long dT_acc;     // phase-A increments of T pending the last block's commit
   unsigned int ticket_r;         // recheck_near_kernel: blocks done (the last one cleans the overflow state)
+  // stream_group_kernel: T and n before each group (two slots, alternating),
+  // recorded by the group's last phase-A CTA, read by its phase B one launch later
+  unsigned long long gbase[2][2];
+  unsigned int ticket_g;
 };
 
 // T / den correctly rounded to binary64 (round half to even), T, den < 2^64:

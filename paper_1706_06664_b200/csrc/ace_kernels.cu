@@ -1784,6 +1784,319 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_pair_ke
 }
 
 
+// The stream over one group of batches per launch (the stream driver's
+// hashing group), in the reference's streaming order (detect.cpp:76-84 on the
+// counts at batch start, then the insert, ace_cli.cpp:177-183 with the insert
+// deferred to each batch end).  Phase A: table t is owned by a cluster of two
+// CTAs for the whole group; both hold the table's counts in shared memory
+// (u32, 128 KB at K = 15), staged once per group and written back once.  Per
+// batch, CTA r takes rows [r n/2, (r+1) n/2) of the batch (u16 ids): each
+// row's count at batch start goes to co[b][t][i] (16-byte stores) and the row
+// is counted into the CTA's u16-pair histogram (at most 65,535 per bin and
+// batch).  After a cluster barrier CTA r adds both histograms (the peer's
+// through distributed shared memory) over its half of the bins into its own
+// copy of the counts and the peer's, with T += 2 c m + m^2 into dT[b][2 t + r];
+// a second barrier, the histograms are cleared, and the CTA counts itself into
+// done[b].  Phase B runs on the CTAs past the tables in the same launch: for
+// batch b they wait until every phase-A CTA has counted into done[b] (phase A
+// never waits on phase B, so this cannot deadlock), take the cut mean - alpha
+// from the exact T before the batch (T at launch start plus the earlier
+// batches' dT), and score the batch's rows while its counts are still in L2:
+// S_i = sum_t co[b][t][i], flag score <= cut.  The last phase-B CTA commits T
+// and n and clears done[] for the next launch.  No grid barrier.
+struct StreamGroupArgs {
+  const uint16_t* ids;          // table-major ids[t * ids_ld + r]
+  uint64_t ids_ld, n, batch;
+  uint32_t tables, k_bits;
+  uint32_t* counters;
+  uint32_t* co;                 // [batches][tables][batch]: counts at batch start
+  unsigned long long* dT;       // [batches][2 tables]
+  unsigned int* done;           // [batches]: phase-A CTAs done with the batch (0 at launch)
+  uint32_t* flags;              // flag words of the group's first row
+  double alpha;
+  DevState* st;
+};
+
+__device__ void stream_group_b(const StreamGroupArgs& a, uint32_t bb, uint32_t G, uint32_t nA,
+                               unsigned long long* red, unsigned long long* red2) {
+  DevState* st = a.st;
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const double L = static_cast<double>(a.tables);
+  const uint64_t nb = (a.n + a.batch - 1) / a.batch;
+  unsigned long long rep = 0ull, amb = 0ull;
+  unsigned long long T = st->T;          // committed by the last launch; this launch commits at its very end
+  const unsigned long long n0 = st->n;
+  const uint64_t nwarps = static_cast<uint64_t>(G) * (blockDim.x >> 5);
+  __shared__ unsigned long long dTb;
+  for (uint64_t b = 0; b < nb; ++b) {
+    if (threadIdx.x == 0)
+      while (*reinterpret_cast<volatile unsigned int*>(a.done + b) < nA) __nanosleep(100);
+    __syncthreads();
+    __threadfence();
+    if (wid == 0) {
+      // the batch's T increment, summed once per CTA
+      unsigned long long v = 0ull;
+      for (uint32_t c = lane; c < nA; c += 32u) v += __ldcg(a.dT + b * nA + c);
+      v = warp_sum_u64(v);
+      if (lane == 0) dTb = v;
+    }
+    const uint64_t r0 = b * a.batch, rows = min(a.batch, a.n - r0);
+    const unsigned long long nn = n0 + r0;
+    const double mu = nn ? ace_div_rn(T, nn * a.tables) : 0.0;
+    const double cut = mu - a.alpha;
+    const bool live = nn > 0;
+    const double band = kStreamBand * fmax(1.0, fabs(mu));
+    if (bb == 0 && threadIdx.x == 0 && b + 1 == nb) {
+      st->cut = cut;
+      st->mean_before = mu;
+    }
+    const uint32_t* cb = a.co + b * a.tables * a.batch;
+    uint32_t* fw = a.flags + r0 / 32;
+    auto score_flag = [&](unsigned long long S) -> bool {
+      const double sc = __ddiv_rn(static_cast<double>(S), L);
+      if (live && fabs(sc - cut) <= band) ++amb;
+      return live && sc <= cut;
+    };
+    if (rows % 32 == 0 && a.batch % 4 == 0) {
+      // one flag word (32 rows = 8 row quads) per warp: four lanes per quad,
+      // lane s of a quad loads tables s, s + 4, ... seven 16-byte loads in
+      // flight per round; the quad's four sums meet by two shuffles
+      const uint32_t sub = lane & 3u, qi = lane >> 2;
+      const uint64_t words = rows / 32, qs = a.batch / 4;
+      const uint4* c4 = reinterpret_cast<const uint4*>(cb);
+      for (uint64_t wd = static_cast<uint64_t>(wid) * G + bb; wd < words; wd += nwarps) {
+        const uint64_t qd = wd * 8 + qi;
+        unsigned long long S[4] = {0ull, 0ull, 0ull, 0ull};
+        for (uint32_t t0 = 0; t0 < a.tables; t0 += 28u) {
+          uint4 c[7];
+#pragma unroll
+          for (uint32_t u = 0; u < 7u; ++u) {
+            const uint32_t tt = t0 + sub + 4u * u;
+            c[u] = tt < a.tables ? __ldcg(c4 + static_cast<uint64_t>(tt) * qs + qd) : make_uint4(0u, 0u, 0u, 0u);
+          }
+#pragma unroll
+          for (uint32_t u = 0; u < 7u; ++u) {
+            S[0] += c[u].x;
+            S[1] += c[u].y;
+            S[2] += c[u].z;
+            S[3] += c[u].w;
+          }
+        }
+#pragma unroll
+        for (uint32_t o = 1; o < 4u; o <<= 1)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) S[e] += __shfl_xor_sync(0xffffffffu, S[e], o);
+        uint32_t word = 0u;
+        if (sub == 0u) {
+          uint32_t nib = 0u;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) nib |= (score_flag(S[e]) ? 1u : 0u) << e;
+          word = nib << (4u * qi);
+        }
+        word |= __shfl_xor_sync(0xffffffffu, word, 4);
+        word |= __shfl_xor_sync(0xffffffffu, word, 8);
+        word |= __shfl_xor_sync(0xffffffffu, word, 16);
+        if (lane == 0) {
+          fw[wd] = word;
+          rep += __popc(word);
+        }
+      }
+    } else {
+      // whole flag words, rows past the batch are 0 (only the stream's last
+      // batch can be ragged, so no word is shared with the next batch)
+      const uint64_t words = (rows + 31) / 32;
+      for (uint64_t w = static_cast<uint64_t>(wid) * G + bb; w < words; w += nwarps) {
+        const uint64_t i = w * 32 + lane;
+        bool f = false;
+        if (i < rows) {
+          unsigned long long S = 0ull;
+          for (uint32_t t0 = 0; t0 < a.tables; t0 += 16) {
+            uint32_t c[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) c[u] = __ldcs(cb + static_cast<uint64_t>(min(t0 + u, a.tables - 1)) * a.batch + i);
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+              if (t0 + u < a.tables) S += c[u];
+          }
+          f = score_flag(S);
+        }
+        const unsigned word = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) {
+          fw[w] = word;
+          rep += __popc(word);
+        }
+      }
+    }
+    __syncthreads();
+    T += dTb;
+  }
+  rep = warp_sum_u64(rep);
+  amb = warp_sum_u64(amb);
+  if (lane == 0) {
+    red[wid] = rep;
+    red2[wid] = amb;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long r = 0ull, m = 0ull;
+    for (uint32_t k = 0; k < (blockDim.x >> 5); ++k) {
+      r += red[k];
+      m += red2[k];
+    }
+    if (r) atomicAdd(&st->reported, r);
+    if (m) atomicAdd(&st->ambiguous, m);
+    __threadfence();
+    if (atomicAdd(&st->ticket_g, 1u) == G - 1u) {
+      // every phase-B CTA has read T and n: commit the group, clear done[]
+      st->T = T;
+      st->n = n0 + a.n;
+      for (uint64_t k = 0; k < nb; ++k) a.done[k] = 0u;
+      st->ticket_g = 0u;
+    }
+  }
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_group_kernel(const StreamGroupArgs a) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  __shared__ unsigned long long red[32];
+  __shared__ unsigned long long red2[32];
+#if ACE_SP_PROF
+  const unsigned long long sp_t0 = gtime();
+#endif
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t nA = 2u * a.tables;  // phase-A CTAs (one cluster per table)
+  if (blockIdx.x >= nA) {
+    stream_group_b(a, blockIdx.x - nA, gridDim.x - nA, nA, red, red2);
+    SPP(9);
+    SPC(15);
+    return;
+  }
+  SPC(14);
+  cg::cluster_group cl = cg::this_cluster();
+  const uint32_t r = cl.block_rank(), t = blockIdx.x >> 1;
+  const uint32_t nbin = 1u << a.k_bits, nw = nbin / 2u;  // bins, histogram words (two u16 bins each); K >= 4
+  uint32_t* cs = sm;         // the table's counts [nbin]
+  uint32_t* hs = sm + nbin;  // this CTA's histogram of the batch [nw]
+  uint32_t* ct = a.counters + (static_cast<uint64_t>(t) << a.k_bits);
+  {
+    // 16-byte loads, eight per thread in flight
+    const uint4* c4 = reinterpret_cast<const uint4*>(ct);
+    uint4* s4 = reinterpret_cast<uint4*>(cs);
+    constexpr uint32_t kU = 8;
+    const uint32_t n4 = nbin / 4;
+    for (uint32_t b0 = 0; b0 < n4; b0 += kU * blockDim.x) {
+      uint4 v[kU];
+#pragma unroll
+      for (uint32_t u = 0; u < kU; ++u) v[u] = __ldcg(c4 + min(b0 + u * blockDim.x + threadIdx.x, n4 - 1u));
+#pragma unroll
+      for (uint32_t u = 0; u < kU; ++u)
+        if (b0 + u * blockDim.x + threadIdx.x < n4) s4[b0 + u * blockDim.x + threadIdx.x] = v[u];
+    }
+  }
+  for (uint32_t w = threadIdx.x; w < nw; w += blockDim.x) hs[w] = 0u;
+  __syncthreads();
+  SPP(1);
+  uint32_t* peer_hs = cl.map_shared_rank(hs, r ^ 1u);
+  uint32_t* peer_cs = cl.map_shared_rank(cs, r ^ 1u);
+  const uint32_t w0 = nw * r / 2, w1 = nw * (r + 1) / 2;  // this CTA's half of the bins (merge, write-back)
+  const uint64_t nbat = (a.n + a.batch - 1) / a.batch;
+  for (uint64_t b = 0; b < nbat; ++b) {
+    const uint64_t r0 = b * a.batch, rows = min(a.batch, a.n - r0);
+    const uint64_t i0 = r ? ((rows / 2) & ~7ull) : 0ull, i1 = r ? rows : ((rows / 2) & ~7ull);
+    const uint16_t* idt = a.ids + static_cast<uint64_t>(t) * a.ids_ld + r0;
+    uint32_t* co = a.co + (b * a.tables + t) * a.batch;
+    // rows [i0, i0 + 8 n8) in eight-id vectors, the rest (< 8) one by one
+    const uint64_t n8 = (i1 - i0) / 8;
+    const uint4* id8 = reinterpret_cast<const uint4*>(idt + i0);
+    constexpr int kDepth = 4;
+    for (uint64_t g0 = 0; g0 < n8; g0 += kDepth * blockDim.x) {
+      uint4 q[kDepth];
+#pragma unroll
+      for (int u = 0; u < kDepth; ++u) q[u] = __ldcs(id8 + min(g0 + u * blockDim.x + threadIdx.x, n8 - 1));
+#pragma unroll
+      for (int u = 0; u < kDepth; ++u) {
+        const uint64_t j = g0 + u * blockDim.x + threadIdx.x;
+        if (j < n8) {
+          const uint32_t wv[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+          uint32_t c[8];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t lo = wv[e] & 0xffffu, hi = wv[e] >> 16;
+            c[2 * e] = cs[lo];
+            c[2 * e + 1] = cs[hi];
+            atomicAdd(&hs[lo >> 1], 1u << ((lo & 1u) << 4));
+            atomicAdd(&hs[hi >> 1], 1u << ((hi & 1u) << 4));
+          }
+          uint4* c4 = reinterpret_cast<uint4*>(co + i0 + 8 * j);
+          c4[0] = make_uint4(c[0], c[1], c[2], c[3]);
+          c4[1] = make_uint4(c[4], c[5], c[6], c[7]);
+        }
+      }
+    }
+    for (uint64_t i = i0 + 8 * n8 + threadIdx.x; i < i1; i += blockDim.x) {
+      const uint32_t id = idt[i];
+      co[i] = cs[id];
+      atomicAdd(&hs[id >> 1], 1u << ((id & 1u) << 4));
+    }
+    __syncthreads();
+    SPP(2);
+    cl.sync();  // both histograms complete (and both CTAs done reading the counts at batch start)
+    SPP(3);
+    unsigned long long dT = 0ull;
+    {
+      // this CTA's half of the bins: both histograms (the peer's through
+      // distributed shared memory, 16-byte loads), the new counts into both copies
+      const uint4* o4 = reinterpret_cast<const uint4*>(hs);
+      const uint4* p4 = reinterpret_cast<const uint4*>(peer_hs);
+      const uint32_t q0 = w0 / 4, q1 = w1 / 4;
+      for (uint32_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
+        const uint4 pv = p4[q], ov = o4[q];
+        const uint32_t ow[4] = {ov.x, ov.y, ov.z, ov.w}, pw[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if ((ow[e] | pw[e]) == 0u) continue;
+#pragma unroll
+          for (uint32_t h = 0; h < 2; ++h) {
+            const uint32_t bin = 2u * (4u * q + e) + h;
+            const uint32_t m = ((ow[e] >> (16 * h)) & 0xffffu) + ((pw[e] >> (16 * h)) & 0xffffu);
+            if (m) {
+              const uint32_t c = cs[bin];
+              cs[bin] = c + m;
+              peer_cs[bin] = c + m;
+              dT += 2ull * c * m + static_cast<unsigned long long>(m) * m;
+            }
+          }
+        }
+      }
+    }
+    dT = warp_sum_u64(dT);
+    if (lane == 0) red[wid] = dT;
+    __syncthreads();
+    SPP(4);
+    cl.sync();  // both CTAs done with the histograms and the counts
+    SPP(5);
+    for (uint32_t w = threadIdx.x; w < nw; w += blockDim.x) hs[w] = 0u;
+    __threadfence();  // this thread's co[b] stores visible GPU-wide before done[b] counts the CTA
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long sum = 0ull;
+      for (uint32_t k = 0; k < (blockDim.x >> 5); ++k) sum += red[k];
+      a.dT[b * 2u * a.tables + 2u * t + r] = sum;
+      __threadfence();
+      atomicAdd(a.done + b, 1u);
+    }
+  }
+  SPP(6);
+  // the counts after the group: this CTA writes its half of the bins
+  {
+    const uint4* s4 = reinterpret_cast<const uint4*>(cs);
+    uint4* c4 = reinterpret_cast<uint4*>(ct);
+    for (uint32_t q = w0 / 2 + threadIdx.x; q < w1 / 2; q += blockDim.x) c4[q] = s4[q];
+  }
+
+}
+
+
 int grid_for(uint64_t work, int threads, int max_blocks = 148 * 16) {
   uint64_t b = (work + threads - 1) / threads;
   if (b < 1) b = 1;
@@ -1985,6 +2298,43 @@ uint32_t stream_blocks(uint32_t tables, uint32_t k_bits) {
   const uint32_t nbins = 1u << k_bits;
   const uint32_t pmin = (nbins * 8u + (200u << 10) - 1u) / (200u << 10);  // 2 x u32 per bin <= 200 KB
   return std::max<uint32_t>(static_cast<uint32_t>(dev_sms()), tables * std::max(pmin, 1u));
+}
+
+bool stream_group_ok(uint32_t tables, uint32_t k_bits, uint64_t batch) {
+  return k_bits >= 4 && k_bits <= 15 && batch % 32 == 0 && batch / 2 <= 65535u &&
+         2u * tables + 32u <= static_cast<uint32_t>(dev_sms());
+}
+
+cudaError_t launch_stream_group(const uint16_t* ids, uint64_t ids_ld, uint64_t n, uint64_t batch, uint32_t tables,
+                                uint32_t k_bits, uint32_t* counters, uint32_t* co, unsigned long long* dT,
+                                unsigned int* done, uint32_t* flags, double alpha, DevState* st, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  if (!stream_group_ok(tables, k_bits, batch) || ids_ld % 8 != 0 || (reinterpret_cast<uintptr_t>(ids) & 15))
+    return cudaErrorInvalidValue;
+  StreamGroupArgs a{};
+  a.ids = ids;
+  a.ids_ld = ids_ld;
+  a.n = n;
+  a.batch = batch;
+  a.tables = tables;
+  a.k_bits = k_bits;
+  a.counters = counters;
+  a.co = co;
+  a.dT = dT;
+  a.done = done;
+  a.flags = flags;
+  a.alpha = alpha;
+  a.st = st;
+  // one cluster of two CTAs per table, the remaining CTAs (at least 32) score;
+  // one CTA per SM (192 KB of shared memory), every CTA resident at once
+  const uint32_t grid = static_cast<uint32_t>(dev_sms()) & ~1u;
+  const uint32_t nbin = 1u << k_bits;
+  const size_t smem = sizeof(uint32_t) * (nbin + nbin / 2u);
+  cudaError_t e;
+  if ((e = set_smem_once(reinterpret_cast<const void*>(stream_group_kernel), 200 * 1024, 6)) != cudaSuccess) return e;
+  stream_group_kernel<<<grid, 1024, smem, s>>>(a);
+  count_launch();
+  return cudaGetLastError();
 }
 
 bool stream_pair_ok(uint32_t tables, uint32_t k_bits, uint64_t batch) {

@@ -75,6 +75,14 @@ cudaError_t launch_stream_score(const uint32_t* ids, uint64_t n, uint32_t tables
 // against slot_b's cut) and phase A of batch b (counts at batch start into
 // cnt_out [L][n], insert, T exact; the cut of batch b recorded in slot_a).
 // n = 0: phase B only; n_prev = 0: phase A only.
+// The stream over one group of batches per launch (stream_group_kernel):
+// u16 ids [tables][ids_ld] of n rows in batches of `batch`; co ([batches]
+// [tables][batch] u32), dT ([batches][2 tables] u64) and done ([batches] u32,
+// all 0 between launches) are scratch; flags receive the group's flag words.
+bool stream_group_ok(uint32_t tables, uint32_t k_bits, uint64_t batch);
+cudaError_t launch_stream_group(const uint16_t* ids, uint64_t ids_ld, uint64_t n, uint64_t batch, uint32_t tables,
+                                uint32_t k_bits, uint32_t* counters, uint32_t* co, unsigned long long* dT,
+                                unsigned int* done, uint32_t* flags, double alpha, DevState* st, cudaStream_t s);
 // The stream driver hashes into u16 ids (ids16) where the pair kernel runs
 // (K <= 15, batches of at most 2 x 65,535 rows, two CTAs per table fit).
 bool stream_pair_ok(uint32_t tables, uint32_t k_bits, uint64_t batch);
