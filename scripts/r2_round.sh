@@ -8,7 +8,7 @@ timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; ech
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
 timeout 600 python bench.py --api point > gpurun_out/bench_point.json 2> gpurun_out/bench_point.err; echo "point rc=$?"
 if [ "${NCU:-1}" = "1" ]; then
-  CFG=5 ROWS=2000000 TAG=r5 bash scripts/launches.sh; cat gpurun_out/launches_r5.txt
+  SKIP=20 CFG=5 ROWS=4000000 TAG=r5 bash scripts/launches.sh; cat gpurun_out/launches_r5.txt
   SKIP=12 CFG=2 ROWS=500000 TAG=r2 bash scripts/launches.sh; cat gpurun_out/launches_r2.txt
   ROWS=524288 TAG=h5 bash scripts/ncu_hash5.sh; echo "ncu h5 rc=$?"
   CFG=2 ROWS=500000 TAG=h2 bash scripts/ncu_hash5.sh; echo "ncu h2 rc=$?"
