@@ -48,6 +48,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "ACE points/sec (hash+insert+score) on 1 B200; % of binding FP32/HBM/L2-atomic roofline"
 UNIT = "points/s"
 ORDER = [1, 2, 3, 4, 5]  # the headline (config 5) last
+STREAM_PIPE = 86  # config 5: projection SMs while pipelined beside the stream kernel (0 = not pipelined)
 STREAM_GROUP = 8  # config 5: batches per hashing launch (lookahead of the stream driver)
 
 # bounded CPU samples (rows): cpu_baseline leg (~10 s of reference CPU work
@@ -553,6 +554,7 @@ def run_stream(args, cfg, ws, rank, local, torch, N, ace, W):
     G = args.stream_group
     sk = ace.AceSketch(fam, ace.CounterWidth.k32)
     sk.set_option(N.ACE_OPT_STREAM_GROUP, G)
+    sk.set_option(N.ACE_OPT_STREAM_PIPE, args.stream_pipe)
     stream = torch.cuda.current_stream()
     sk.set_stream(stream.cuda_stream)
     flags = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
@@ -605,6 +607,7 @@ def run_stream(args, cfg, ws, rank, local, torch, N, ace, W):
         fn = N.dev().ace_sketch_stream_run
         sk_e = ace.AceSketch(fam, ace.CounterWidth.k32)
         sk_e.set_option(N.ACE_OPT_STREAM_GROUP, G)
+        sk_e.set_option(N.ACE_OPT_STREAM_PIPE, args.stream_pipe)
         sk_e.set_stream(stream.cuda_stream)
 
         def e2e_call():
@@ -677,6 +680,8 @@ def main():
     ap.add_argument("--rows", type=int, default=None, help="stream mode: limit N (smoke runs)")
     ap.add_argument("--stream-group", type=int, default=STREAM_GROUP,
                     help="stream mode: batches per hashing launch and per stream-kernel launch")
+    ap.add_argument("--stream-pipe", type=int, default=STREAM_PIPE,
+                    help="stream mode: SMs of the next group's projection beside the stream kernel (0 = off)")
     ap.add_argument("--api", default="batch", choices=["batch", "point"],
                     help="batch: the hot path over each config (default); point: the per-point API")
     args = ap.parse_args()

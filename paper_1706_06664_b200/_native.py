@@ -14,7 +14,7 @@ LIB_DIR = Path(__file__).resolve().parent / "lib"
 ACE_OK, ACE_E_CONTRACT, ACE_E_UNSUPPORTED, ACE_E_INCONSISTENT, ACE_E_DATA, ACE_E_CUDA, ACE_E_NOMEM = range(7)
 ACE_F32, ACE_F64 = 0, 1
 ACE_HOST, ACE_DEVICE = 0, 1
-ACE_OPT_H2D_CHUNKS, ACE_OPT_DEFER_INSERT, ACE_OPT_STREAM_GROUP = 1, 2, 3
+ACE_OPT_H2D_CHUNKS, ACE_OPT_DEFER_INSERT, ACE_OPT_STREAM_GROUP, ACE_OPT_STREAM_PIPE = 1, 2, 3, 4
 
 
 class AceHashStats(C.Structure):

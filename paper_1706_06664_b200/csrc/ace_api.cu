@@ -136,6 +136,12 @@ struct AceSketch {
   // stream driver: batches hashed by one projection launch (hashing does not
   // depend on the counts), amortising the persistent kernel's fill and drain
   int stream_group = 4;     // ACE_OPT_STREAM_GROUP
+  // stream driver pipeline: the projection of group g + 1 (capped at this many
+  // CTAs) runs beside the stream kernel of group g (one CTA per table on the
+  // other SMs, on pstream); 0 = one after the other on the whole GPU
+  int stream_pipe = 0;      // ACE_OPT_STREAM_PIPE
+  cudaStream_t pstream = nullptr;
+  cudaEvent_t p_hashed[2] = {nullptr, nullptr}, p_streamed[2] = {nullptr, nullptr};
   // build + detect over the same rows: run_hash leaves the insert to the
   // fused count-and-gather pass of the detect tail (detect_tail_kernel)
   bool defer_insert = false, insert_deferred = false;
@@ -451,14 +457,22 @@ ace_status ensure_stream_bufs(AceSketch* sk, uint64_t rows) {
   return ACE_OK;
 }
 
-ace_status ensure_group_bufs(AceSketch* sk, uint64_t group_batches, uint64_t batch, uint64_t ids_ld) {
+ace_status ensure_group_bufs(AceSketch* sk, uint64_t group_batches, uint64_t batch, uint64_t ids_ld, bool pipe) {
   const uint64_t L = sk->fam->d.tables;
   ACE_CUDA(sk->gco.ensure(static_cast<size_t>(group_batches) * L * batch * sizeof(uint32_t)));
   ACE_CUDA(sk->gdT.ensure(static_cast<size_t>(group_batches) * 2 * L * sizeof(unsigned long long)));
   const void* before = sk->gdone.p;
   ACE_CUDA(sk->gdone.ensure(static_cast<size_t>(group_batches) * sizeof(unsigned int)));
   if (sk->gdone.p != before) ACE_CUDA(cudaMemsetAsync(sk->gdone.p, 0, sk->gdone.bytes, sk->stream));
-  ACE_CUDA(sk->ids.ensure(static_cast<size_t>(ids_ld) * L * sizeof(uint16_t)));
+  // pipelined: two id buffers (the projection fills one while the stream kernel reads the other)
+  ACE_CUDA(sk->ids.ensure(static_cast<size_t>(ids_ld) * L * sizeof(uint16_t) * (pipe ? 2u : 1u)));
+  if (pipe) {
+    if (!sk->pstream) ACE_CUDA(cudaStreamCreateWithFlags(&sk->pstream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      if (!sk->p_hashed[i]) ACE_CUDA(cudaEventCreateWithFlags(&sk->p_hashed[i], cudaEventDisableTiming));
+      if (!sk->p_streamed[i]) ACE_CUDA(cudaEventCreateWithFlags(&sk->p_streamed[i], cudaEventDisableTiming));
+    }
+  }
   return ACE_OK;
 }
 
@@ -466,7 +480,7 @@ ace_status ensure_group_bufs(AceSketch* sk, uint64_t group_batches, uint64_t bat
 // Chunk mode (ids_out != null): the rows are rows [r0, r0 + n) of a longer
 // batch whose ids (stride ids_ld) the caller has sized.
 ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64_t ld, int insert,
-                    uint32_t* ids_out = nullptr, uint64_t ids_ld = 0, bool ids16 = false) {
+                    uint32_t* ids_out = nullptr, uint64_t ids_ld = 0, bool ids16 = false, uint32_t grid_cap = 0) {
   const AceFamily* f = sk->fam;
   if (!ids_out) {
     ACE_CUDA(sk->ids.ensure(static_cast<size_t>(n) * f->d.tables * sizeof(uint32_t)));
@@ -495,6 +509,7 @@ ace_status run_hash(AceSketch* sk, const void* xd, int dtype, uint64_t n, uint64
     t.ids = ids_out;
     t.ids_ld = ids_ld;
     t.ids16 = ids16 ? 1 : 0;  // callers ask for u16 ids only on this path (stream driver, K <= 15)
+    t.grid_cap = kstream ? 0u : grid_cap;
     // near-tie list: the K-streamed path's bound (large d, dense data) leaves
     // far more near ties per row, size its list accordingly
     uint64_t cap = kstream ? n * f->d.rows / 48 : n * f->d.rows / 1024;
@@ -966,6 +981,11 @@ ace_status ace_sketch_destroy(AceSketch* sk) {
     if (sk->s_used[i]) cudaEventDestroy(sk->s_used[i]);
   }
   if (sk->cstream) cudaStreamDestroy(sk->cstream);
+  for (int i = 0; i < 2; ++i) {
+    if (sk->p_hashed[i]) cudaEventDestroy(sk->p_hashed[i]);
+    if (sk->p_streamed[i]) cudaEventDestroy(sk->p_streamed[i]);
+  }
+  if (sk->pstream) cudaStreamDestroy(sk->pstream);
   if (sk->cstart) cudaEventDestroy(sk->cstart);
   for (cudaEvent_t e : sk->cev)
     if (e) cudaEventDestroy(e);
@@ -1001,6 +1021,10 @@ ace_status ace_sketch_set_option(AceSketch* sk, int option, int64_t value) {
     case ACE_OPT_STREAM_GROUP:
       if (value < 1 || value > 64) return fail(ACE_E_CONTRACT, "ace_sketch_set_option: group must be in [1, 64]");
       sk->stream_group = static_cast<int>(value);
+      break;
+    case ACE_OPT_STREAM_PIPE:
+      if (value < 0 || value > 1024) return fail(ACE_E_CONTRACT, "ace_sketch_set_option: pipe CTAs must be in [0, 1024]");
+      sk->stream_pipe = static_cast<int>(value);
       break;
     default:
       return fail(ACE_E_CONTRACT, "ace_sketch_set_option: unknown option " + std::to_string(option));
@@ -1473,7 +1497,13 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
   ACE_CUDA(sk->flags.ensure(((n + 31) / 32) * sizeof(uint32_t)));
   uint32_t* dflags = (flag_bits && out_where == ACE_DEVICE) ? flag_bits : sk->flags.as<uint32_t>();
   if (fast && !gfast && (r = ensure_stream_bufs(sk, std::min(batch, n))) != ACE_OK) return r;
-  if (gfast && (r = ensure_group_bufs(sk, gl, batch, gld)) != ACE_OK) return r;
+  // pipelined groups (ACE_OPT_STREAM_PIPE): the projection of group g + 1 on
+  // `pipe` SMs beside the stream kernel of group g on the others
+  const uint32_t pipe = (gfast && nb > G && sk->stream_pipe > 0 &&
+                         stream_solo_ok(f->d.tables, f->d.k_bits, batch, static_cast<uint32_t>(sk->stream_pipe)))
+                            ? static_cast<uint32_t>(sk->stream_pipe)
+                            : 0u;
+  if (gfast && (r = ensure_group_bufs(sk, gl, batch, gld, pipe != 0)) != ACE_OK) return r;
   // per-batch latency: from the start of the batch's work (its group's
   // hashing for a group's first batch) to the end of the launch that writes
   // its flags; events kept by the sketch across calls
@@ -1488,14 +1518,14 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
   }
   std::vector<cudaEvent_t> tev;  // timing on: (start, end) pairs, hashing then stream kernels
   std::vector<int> tkind;
-  auto tmark = [&](int kind, bool end) -> cudaError_t {
+  auto tmark = [&](int kind, bool end, cudaStream_t ts = nullptr) -> cudaError_t {
     if (!sk->timing) return cudaSuccess;
     cudaEvent_t e;
     cudaError_t err = cudaEventCreate(&e);
     if (err != cudaSuccess) return err;
     tev.push_back(e);
     if (!end) tkind.push_back(kind);
-    return cudaEventRecord(e, sk->stream);
+    return cudaEventRecord(e, ts ? ts : sk->stream);
   };
   // pinned host rows: H2D copies of the next group overlap this group's work
   const bool overlap = x_where == ACE_HOST && host_pinned(x) && nb > G;
@@ -1530,6 +1560,10 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
     uint32_t p_slot = 0;
     for (uint64_t g0 = 0; g0 < nb; g0 += G) {
       const uint64_t gb = std::min(G, nb - g0), gr0 = g0 * batch, grows = std::min(gb * batch, n - gr0);
+      // pipelined: id buffer g & 1, free once the stream kernel of group g - 2 has read it
+      const int pb = pipe ? static_cast<int>((g0 / G) & 1u) : 0;
+      uint16_t* gids = gfast ? sk->ids.as<uint16_t>() + static_cast<size_t>(pb) * gld * f->d.tables : nullptr;
+      if (pipe && g0 >= 2 * G) ACE_CUDA(cudaStreamWaitEvent(sk->stream, sk->p_streamed[pb], 0));
       if (batch_ms)
         for (uint64_t b = g0; b < (gfast ? g0 + gb : g0 + 1); ++b) ACE_CUDA(cudaEventRecord(sk->lat_a[b], sk->stream));
       const void* xg = static_cast<const char*>(x) + gr0 * ld * esz;
@@ -1545,8 +1579,8 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
         xd = sk->sstage[hb].p;
         ldd = ld;
         ACE_CUDA(tmark(0, false));
-        if ((rr = run_hash(sk, xd, dtype, grows, ldd, 0, gfast ? sk->ids.as<uint32_t>() : nullptr, gfast ? gld : 0,
-                           ids16)) != ACE_OK)
+        if ((rr = run_hash(sk, xd, dtype, grows, ldd, 0, reinterpret_cast<uint32_t*>(gids), gfast ? gld : 0, ids16,
+                           pipe)) != ACE_OK)
           return rr;
         ACE_CUDA(tmark(0, true));
         ACE_CUDA(cudaEventRecord(sk->s_used[hb], sk->stream));
@@ -1561,19 +1595,32 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
       } else {
         if ((rr = stage_x(sk, sk->stage, sk->stream, xg, dtype, grows, ld, x_where, &xd, &ldd)) != ACE_OK) return rr;
         ACE_CUDA(tmark(0, false));
-        if ((rr = run_hash(sk, xd, dtype, grows, ldd, 0, gfast ? sk->ids.as<uint32_t>() : nullptr, gfast ? gld : 0,
-                           ids16)) != ACE_OK)
+        if ((rr = run_hash(sk, xd, dtype, grows, ldd, 0, reinterpret_cast<uint32_t*>(gids), gfast ? gld : 0, ids16,
+                           pipe)) != ACE_OK)
           return rr;
         ACE_CUDA(tmark(0, true));
       }
       if (gfast) {
-        ACE_CUDA(tmark(1, false));
-        ACE_CUDA(launch_stream_group(sk->ids.as<uint16_t>(), gld, grows, batch, f->d.tables, f->d.k_bits, sk->counters,
+        // pipelined: on pstream, after this group's projection; the last
+        // group's stream kernel has the GPU to itself (pair kernel)
+        cudaStream_t ss = pipe ? sk->pstream : sk->stream;
+        if (pipe) {
+          ACE_CUDA(cudaEventRecord(sk->p_hashed[pb], sk->stream));
+          ACE_CUDA(cudaStreamWaitEvent(ss, sk->p_hashed[pb], 0));
+        }
+        ACE_CUDA(tmark(1, false, ss));
+        ACE_CUDA(launch_stream_group(gids, gld, grows, batch, f->d.tables, f->d.k_bits, sk->counters,
                                      sk->gco.as<uint32_t>(), sk->gdT.as<unsigned long long>(),
-                                     sk->gdone.as<unsigned int>(), dflags + gr0 / 32, alpha, sk->st, sk->stream));
-        ACE_CUDA(tmark(1, true));
+                                     sk->gdone.as<unsigned int>(), dflags + gr0 / 32, alpha, sk->st, ss,
+                                     g0 + G < nb ? pipe : 0u));
+        ACE_CUDA(tmark(1, true, ss));
         if (batch_ms)
-          for (uint64_t b = g0; b < g0 + gb; ++b) ACE_CUDA(cudaEventRecord(sk->lat_b[b], sk->stream));
+          for (uint64_t b = g0; b < g0 + gb; ++b) ACE_CUDA(cudaEventRecord(sk->lat_b[b], ss));
+        if (pipe) {
+          ACE_CUDA(cudaEventRecord(sk->p_streamed[pb], ss));
+          // join: the caller's stream continues after the last stream kernel
+          if (g0 + G >= nb) ACE_CUDA(cudaStreamWaitEvent(sk->stream, sk->p_streamed[pb], 0));
+        }
         continue;
       }
       for (uint64_t b = g0; b < g0 + gb; ++b) {
@@ -1631,7 +1678,7 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
   key.dtype = dtype;
   key.out_where = out_where;
   key.lat = batch_ms != nullptr;
-  key.group = sk->stream_group;
+  key.group = sk->stream_group * 4096 + sk->stream_pipe;
   key.stream = sk->stream;
   key.ff = ff;
   const DevBuf* sb[9] = {&sk->ids, &sk->flags, &sk->cnt[0], &sk->cnt[1], &sk->near, &sk->overflow,

@@ -960,7 +960,7 @@ cudaError_t launch_hash_tc(const TcArgs& a, void* stage, cudaStream_t s) {
                                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-  const uint64_t grid = tc_grid(a.n);
+  const uint64_t grid = tc_grid(a.n, a.grid_cap);
   const size_t smem = tc_layout(a.dim, a.tw, a.k_bits * a.tables).total;
   // compile-time K packers for the BASELINE shapes (never with the fused insert, K > 20)
   if (a.k_bits == 15 && !a.fused_insert)
@@ -985,13 +985,14 @@ extern "C" int ace_debug_tc_prof(unsigned long long* out24, int reset) {
 }
 #endif
 
-uint32_t tc_grid(uint64_t n) {
-  return static_cast<uint32_t>(std::min<uint64_t>((n + kRows - 1) / kRows, static_cast<uint64_t>(tc_sms())));
+uint32_t tc_grid(uint64_t n, uint32_t cap) {
+  const uint64_t sms = cap ? std::min<uint64_t>(cap, static_cast<uint64_t>(tc_sms())) : static_cast<uint64_t>(tc_sms());
+  return static_cast<uint32_t>(std::min<uint64_t>((n + kRows - 1) / kRows, sms));
 }
 
 cudaError_t launch_recheck_near(const TcArgs& a, cudaStream_t s) {
   if (a.n == 0) return cudaSuccess;
-  const uint32_t nseg = tc_grid(a.n);
+  const uint32_t nseg = tc_grid(a.n, a.grid_cap);
   // eight blocks (256 items) per list segment: one round for the BASELINE
   // shapes' ~40-260 items per segment
   const uint32_t per = std::max<uint32_t>(1u, (8u * static_cast<uint32_t>(tc_sms()) + nseg - 1u) / nseg);

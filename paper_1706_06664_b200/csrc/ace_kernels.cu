@@ -1828,11 +1828,51 @@ __device__ void stream_group_b(const StreamGroupArgs& a, uint32_t bb, uint32_t G
   const unsigned long long n0 = st->n;
   const uint64_t nwarps = static_cast<uint64_t>(G) * (blockDim.x >> 5);
   __shared__ unsigned long long dTb;
+  __shared__ long long cutS[3];  // integer forms of the batch's cut and ambiguity band (below)
   for (uint64_t b = 0; b < nb; ++b) {
-    if (threadIdx.x == 0)
+    const uint64_t r0 = b * a.batch, rows = min(a.batch, a.n - r0);
+    const unsigned long long nn = n0 + r0;
+    if (threadIdx.x == 32) {
+      // One thread, while the batch is still being counted: the cut mean - alpha
+      // from the exact T before the batch, as the largest integer score sum S
+      // with S / L <= cut (the reference's comparison, detect.cpp:83, on its
+      // rounded quotient: S / L is monotone in S), and the sums whose score
+      // lies within the ambiguity band of the cut.
+      const double mu = nn ? ace_div_rn(T, nn * a.tables) : 0.0;
+      const double cut = mu - a.alpha;
+      const double band = kStreamBand * fmax(1.0, fabs(mu));
+      auto sc_of = [&](long long S) { return __ddiv_rn(static_cast<double>(S), L); };
+      auto amb_of = [&](long long S) { return fabs(sc_of(S) - cut) <= band; };
+      long long s_cut = -1, s_lo = 0, s_hi = -1;
+      if (nn > 0 && cut >= 0.0) {
+        s_cut = static_cast<long long>(floor(cut * L));
+        while (sc_of(s_cut + 1) <= cut) ++s_cut;
+        while (s_cut >= 0 && sc_of(s_cut) > cut) --s_cut;
+      }
+      if (nn > 0 && cut + band >= 0.0) {
+        long long s = static_cast<long long>(floor(fmax(cut - band, 0.0) * L)) - 2;
+        if (s < 0) s = 0;
+        while (!amb_of(s) && sc_of(s) < cut) ++s;
+        if (amb_of(s)) {
+          s_lo = s;
+          s = static_cast<long long>(floor((cut + band) * L)) + 2;
+          while (s > s_lo && !amb_of(s)) --s;
+          s_hi = s;
+        }
+      }
+      cutS[0] = s_cut;
+      cutS[1] = s_lo;
+      cutS[2] = s_hi;
+      if (bb == 0 && b + 1 == nb) {
+        st->cut = cut;
+        st->mean_before = mu;
+      }
+    }
+    if (threadIdx.x == 0) {
       while (*reinterpret_cast<volatile unsigned int*>(a.done + b) < nA) __nanosleep(100);
+      __threadfence();  // the batch's counts (fenced before done[b] was counted) are read after this
+    }
     __syncthreads();
-    __threadfence();
     if (wid == 0) {
       // the batch's T increment, summed once per CTA
       unsigned long long v = 0ull;
@@ -1840,22 +1880,13 @@ __device__ void stream_group_b(const StreamGroupArgs& a, uint32_t bb, uint32_t G
       v = warp_sum_u64(v);
       if (lane == 0) dTb = v;
     }
-    const uint64_t r0 = b * a.batch, rows = min(a.batch, a.n - r0);
-    const unsigned long long nn = n0 + r0;
-    const double mu = nn ? ace_div_rn(T, nn * a.tables) : 0.0;
-    const double cut = mu - a.alpha;
-    const bool live = nn > 0;
-    const double band = kStreamBand * fmax(1.0, fabs(mu));
-    if (bb == 0 && threadIdx.x == 0 && b + 1 == nb) {
-      st->cut = cut;
-      st->mean_before = mu;
-    }
+    const long long s_cut = cutS[0], s_lo = cutS[1], s_hi = cutS[2];
     const uint32_t* cb = a.co + b * a.tables * a.batch;
     uint32_t* fw = a.flags + r0 / 32;
     auto score_flag = [&](unsigned long long S) -> bool {
-      const double sc = __ddiv_rn(static_cast<double>(S), L);
-      if (live && fabs(sc - cut) <= band) ++amb;
-      return live && sc <= cut;
+      const long long Ss = static_cast<long long>(S);
+      if (Ss >= s_lo && Ss <= s_hi) ++amb;
+      return Ss <= s_cut;
     };
     if (rows % 32 == 0 && a.batch % 4 == 0) {
       // one flag word (32 rows = 8 row quads) per warp: four lanes per quad,
@@ -1956,15 +1987,17 @@ __device__ void stream_group_b(const StreamGroupArgs& a, uint32_t bb, uint32_t G
   }
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_group_kernel(const StreamGroupArgs a) {
-  extern __shared__ __align__(16) uint32_t sm[];
-  __shared__ unsigned long long red[32];
-  __shared__ unsigned long long red2[32];
+// C = CTAs per table: 2 (a cluster pair, stream_group_kernel: the whole GPU) or
+// 1 (stream_solo_kernel: tables + a few scoring CTAs, leaving the other SMs to
+// the next group's projection kernel running beside it).
+template <uint32_t C>
+__device__ __forceinline__ void stream_group_body(const StreamGroupArgs& a, uint32_t* sm, unsigned long long* red,
+                                                  unsigned long long* red2) {
 #if ACE_SP_PROF
   const unsigned long long sp_t0 = gtime();
 #endif
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint32_t nA = 2u * a.tables;  // phase-A CTAs (one cluster per table)
+  const uint32_t nA = C * a.tables;  // phase-A CTAs (one cluster per table)
   if (blockIdx.x >= nA) {
     stream_group_b(a, blockIdx.x - nA, gridDim.x - nA, nA, red, red2);
     SPP(9);
@@ -1972,8 +2005,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_group_k
     return;
   }
   SPC(14);
-  cg::cluster_group cl = cg::this_cluster();
-  const uint32_t r = cl.block_rank(), t = blockIdx.x >> 1;
+  uint32_t r = 0;
+  if constexpr (C == 2) r = cg::this_cluster().block_rank();
+  const uint32_t t = blockIdx.x / C;
   const uint32_t nbin = 1u << a.k_bits, nw = nbin / 2u;  // bins, histogram words (two u16 bins each); K >= 4
   uint32_t* cs = sm;         // the table's counts [nbin]
   uint32_t* hs = sm + nbin;  // this CTA's histogram of the batch [nw]
@@ -1996,19 +2030,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_group_k
   for (uint32_t w = threadIdx.x; w < nw; w += blockDim.x) hs[w] = 0u;
   __syncthreads();
   SPP(1);
-  uint32_t* peer_hs = cl.map_shared_rank(hs, r ^ 1u);
-  uint32_t* peer_cs = cl.map_shared_rank(cs, r ^ 1u);
-  const uint32_t w0 = nw * r / 2, w1 = nw * (r + 1) / 2;  // this CTA's half of the bins (merge, write-back)
+  uint32_t* peer_hs = hs;
+  uint32_t* peer_cs = cs;
+  if constexpr (C == 2) {
+    cg::cluster_group cl = cg::this_cluster();
+    peer_hs = cl.map_shared_rank(hs, r ^ 1u);
+    peer_cs = cl.map_shared_rank(cs, r ^ 1u);
+  }
+  const uint32_t w0 = nw * r / C, w1 = nw * (r + 1) / C;  // this CTA's share of the bins (merge, write-back)
   const uint64_t nbat = (a.n + a.batch - 1) / a.batch;
   for (uint64_t b = 0; b < nbat; ++b) {
     const uint64_t r0 = b * a.batch, rows = min(a.batch, a.n - r0);
-    const uint64_t i0 = r ? ((rows / 2) & ~7ull) : 0ull, i1 = r ? rows : ((rows / 2) & ~7ull);
+    const uint64_t half = C == 2 ? ((rows / 2) & ~7ull) : rows;
+    const uint64_t i0 = r ? half : 0ull, i1 = r ? rows : half;
     const uint16_t* idt = a.ids + static_cast<uint64_t>(t) * a.ids_ld + r0;
     uint32_t* co = a.co + (b * a.tables + t) * a.batch;
     // rows [i0, i0 + 8 n8) in eight-id vectors, the rest (< 8) one by one
     const uint64_t n8 = (i1 - i0) / 8;
     const uint4* id8 = reinterpret_cast<const uint4*>(idt + i0);
     constexpr int kDepth = 4;
+    // one CTA per table sees the whole batch: a u16 half wraps only when all
+    // 65,536 rows of a batch share one bucket, which the loop watches for
+    // (diff stays 0) and the merge then handles by itself
+    const bool wrap_watch = C == 1 && i1 - i0 > 65535u;
+    const uint32_t first = wrap_watch ? static_cast<uint32_t>(idt[i0]) * 0x10001u : 0u;
+    uint32_t diff = 0u;
     for (uint64_t g0 = 0; g0 < n8; g0 += kDepth * blockDim.x) {
       uint4 q[kDepth];
 #pragma unroll
@@ -2022,6 +2068,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_group_k
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const uint32_t lo = wv[e] & 0xffffu, hi = wv[e] >> 16;
+            if constexpr (C == 1) diff |= wv[e] ^ first;
             c[2 * e] = cs[lo];
             c[2 * e + 1] = cs[hi];
             atomicAdd(&hs[lo >> 1], 1u << ((lo & 1u) << 4));
@@ -2035,14 +2082,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_group_k
     }
     for (uint64_t i = i0 + 8 * n8 + threadIdx.x; i < i1; i += blockDim.x) {
       const uint32_t id = idt[i];
+      if constexpr (C == 1) diff |= id ^ (first & 0xffffu);
       co[i] = cs[id];
       atomicAdd(&hs[id >> 1], 1u << ((id & 1u) << 4));
     }
+    unsigned long long dT = 0ull;
+    if constexpr (C == 1) {
+      if (wrap_watch) {
+        if (__syncthreads_and(diff == 0u)) {
+          // every row in bucket `first`: its half wrapped; add the rows here
+          // and leave the merge an empty histogram
+          if (threadIdx.x == 0) {
+            const uint32_t bin = first & 0xffffu, m = static_cast<uint32_t>(i1 - i0), c = cs[bin];
+            hs[bin >> 1] = 0u;
+            cs[bin] = c + m;
+            dT = 2ull * c * m + static_cast<unsigned long long>(m) * m;
+          }
+        }
+      }
+    }
     __syncthreads();
     SPP(2);
-    cl.sync();  // both histograms complete (and both CTAs done reading the counts at batch start)
+    if constexpr (C == 2) cg::this_cluster().sync();  // both histograms complete (and both CTAs done reading the counts at batch start)
     SPP(3);
-    unsigned long long dT = 0ull;
     {
       // this CTA's half of the bins: both histograms (the peer's through
       // distributed shared memory, 16-byte loads), the new counts into both copies
@@ -2050,7 +2112,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_group_k
       const uint4* p4 = reinterpret_cast<const uint4*>(peer_hs);
       const uint32_t q0 = w0 / 4, q1 = w1 / 4;
       for (uint32_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
-        const uint4 pv = p4[q], ov = o4[q];
+        const uint4 ov = o4[q];
+        uint4 pv = make_uint4(0u, 0u, 0u, 0u);
+        if constexpr (C == 2) pv = p4[q];
         const uint32_t ow[4] = {ov.x, ov.y, ov.z, ov.w}, pw[4] = {pv.x, pv.y, pv.z, pv.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -2062,7 +2126,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_group_k
             if (m) {
               const uint32_t c = cs[bin];
               cs[bin] = c + m;
-              peer_cs[bin] = c + m;
+              if constexpr (C == 2) peer_cs[bin] = c + m;
               dT += 2ull * c * m + static_cast<unsigned long long>(m) * m;
             }
           }
@@ -2073,7 +2137,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_group_k
     if (lane == 0) red[wid] = dT;
     __syncthreads();
     SPP(4);
-    cl.sync();  // both CTAs done with the histograms and the counts
+    if constexpr (C == 2) cg::this_cluster().sync();  // both CTAs done with the histograms and the counts
     SPP(5);
     for (uint32_t w = threadIdx.x; w < nw; w += blockDim.x) hs[w] = 0u;
     __threadfence();  // this thread's co[b] stores visible GPU-wide before done[b] counts the CTA
@@ -2081,7 +2145,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_group_k
     if (threadIdx.x == 0) {
       unsigned long long sum = 0ull;
       for (uint32_t k = 0; k < (blockDim.x >> 5); ++k) sum += red[k];
-      a.dT[b * 2u * a.tables + 2u * t + r] = sum;
+      a.dT[b * nA + C * t + r] = sum;
       __threadfence();
       atomicAdd(a.done + b, 1u);
     }
@@ -2093,7 +2157,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_group_k
     uint4* c4 = reinterpret_cast<uint4*>(ct);
     for (uint32_t q = w0 / 2 + threadIdx.x; q < w1 / 2; q += blockDim.x) c4[q] = s4[q];
   }
+  (void)peer_hs;
+  (void)peer_cs;
+}
 
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_group_kernel(const StreamGroupArgs a) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  __shared__ unsigned long long red[32];
+  __shared__ unsigned long long red2[32];
+  stream_group_body<2>(a, sm, red, red2);
+}
+
+__global__ void __launch_bounds__(1024) stream_solo_kernel(const StreamGroupArgs a) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  __shared__ unsigned long long red[32];
+  __shared__ unsigned long long red2[32];
+  stream_group_body<1>(a, sm, red, red2);
 }
 
 
@@ -2305,12 +2384,20 @@ bool stream_group_ok(uint32_t tables, uint32_t k_bits, uint64_t batch) {
          2u * tables + 32u <= static_cast<uint32_t>(dev_sms());
 }
 
+// The one-CTA-per-table variant beside a projection kernel on hash_ctas SMs.
+bool stream_solo_ok(uint32_t tables, uint32_t k_bits, uint64_t batch, uint32_t hash_ctas) {
+  return stream_group_ok(tables, k_bits, batch) && batch <= 65536u && hash_ctas >= 8u &&
+         tables + 4u + hash_ctas <= static_cast<uint32_t>(dev_sms());
+}
+
 cudaError_t launch_stream_group(const uint16_t* ids, uint64_t ids_ld, uint64_t n, uint64_t batch, uint32_t tables,
                                 uint32_t k_bits, uint32_t* counters, uint32_t* co, unsigned long long* dT,
-                                unsigned int* done, uint32_t* flags, double alpha, DevState* st, cudaStream_t s) {
+                                unsigned int* done, uint32_t* flags, double alpha, DevState* st, cudaStream_t s,
+                                uint32_t hash_ctas) {
   if (n == 0) return cudaSuccess;
   if (!stream_group_ok(tables, k_bits, batch) || ids_ld % 8 != 0 || (reinterpret_cast<uintptr_t>(ids) & 15))
     return cudaErrorInvalidValue;
+  if (hash_ctas && !stream_solo_ok(tables, k_bits, batch, hash_ctas)) return cudaErrorInvalidValue;
   StreamGroupArgs a{};
   a.ids = ids;
   a.ids_ld = ids_ld;
@@ -2325,14 +2412,21 @@ cudaError_t launch_stream_group(const uint16_t* ids, uint64_t ids_ld, uint64_t n
   a.flags = flags;
   a.alpha = alpha;
   a.st = st;
-  // one cluster of two CTAs per table, the remaining CTAs (at least 32) score;
-  // one CTA per SM (192 KB of shared memory), every CTA resident at once
-  const uint32_t grid = static_cast<uint32_t>(dev_sms()) & ~1u;
   const uint32_t nbin = 1u << k_bits;
   const size_t smem = sizeof(uint32_t) * (nbin + nbin / 2u);
   cudaError_t e;
-  if ((e = set_smem_once(reinterpret_cast<const void*>(stream_group_kernel), 200 * 1024, 6)) != cudaSuccess) return e;
-  stream_group_kernel<<<grid, 1024, smem, s>>>(a);
+  if (hash_ctas) {
+    // one CTA per table and the SMs the projection kernel leaves for scoring
+    const uint32_t grid = static_cast<uint32_t>(dev_sms()) - hash_ctas;
+    if ((e = set_smem_once(reinterpret_cast<const void*>(stream_solo_kernel), 200 * 1024, 7)) != cudaSuccess) return e;
+    stream_solo_kernel<<<grid, 1024, smem, s>>>(a);
+  } else {
+    // one cluster of two CTAs per table, the remaining CTAs (at least 32) score;
+    // one CTA per SM (192 KB of shared memory), every CTA resident at once
+    const uint32_t grid = static_cast<uint32_t>(dev_sms()) & ~1u;
+    if ((e = set_smem_once(reinterpret_cast<const void*>(stream_group_kernel), 200 * 1024, 6)) != cudaSuccess) return e;
+    stream_group_kernel<<<grid, 1024, smem, s>>>(a);
+  }
   count_launch();
   return cudaGetLastError();
 }

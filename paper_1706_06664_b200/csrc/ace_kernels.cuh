@@ -79,10 +79,15 @@ cudaError_t launch_stream_score(const uint32_t* ids, uint64_t n, uint32_t tables
 // u16 ids [tables][ids_ld] of n rows in batches of `batch`; co ([batches]
 // [tables][batch] u32), dT ([batches][2 tables] u64) and done ([batches] u32,
 // all 0 between launches) are scratch; flags receive the group's flag words.
+// hash_ctas != 0 selects stream_solo_kernel: one CTA per table plus scoring
+// CTAs on the SMs a projection kernel capped at hash_ctas CTAs leaves free, so
+// the next group's projection runs beside this group's stream kernel.
 bool stream_group_ok(uint32_t tables, uint32_t k_bits, uint64_t batch);
+bool stream_solo_ok(uint32_t tables, uint32_t k_bits, uint64_t batch, uint32_t hash_ctas);
 cudaError_t launch_stream_group(const uint16_t* ids, uint64_t ids_ld, uint64_t n, uint64_t batch, uint32_t tables,
                                 uint32_t k_bits, uint32_t* counters, uint32_t* co, unsigned long long* dT,
-                                unsigned int* done, uint32_t* flags, double alpha, DevState* st, cudaStream_t s);
+                                unsigned int* done, uint32_t* flags, double alpha, DevState* st, cudaStream_t s,
+                                uint32_t hash_ctas = 0);
 // The stream driver hashes into u16 ids (ids16) where the pair kernel runs
 // (K <= 15, batches of at most 2 x 65,535 rows, two CTAs per table fit).
 bool stream_pair_ok(uint32_t tables, uint32_t k_bits, uint64_t batch);

@@ -48,6 +48,7 @@ struct TcArgs {
   const float* w32;               // K-streamed recheck: W rounded to fp32 [rows][dim]
   uint32_t* overflow_rows;        // bitmap over rows; rows rechecked in full
   DevState* st;
+  uint32_t grid_cap;              // d <= 256: at most this many CTAs (0 = one per SM); the stream pipeline
 };
 
 cudaError_t tc_prepare_family(const FamilyDev& f, TcFamily* tc);
@@ -65,7 +66,7 @@ cudaError_t launch_recheck(const TcArgs& a, cudaStream_t s);
 // d <= 256: the near ties hash_tc_kernel listed (per-CTA segments, lengths in
 // TcArgs::seg_counts, tc_grid(n) entries) and the overflowed rows, decided
 // exactly in one launch after the projection
-uint32_t tc_grid(uint64_t n);
+uint32_t tc_grid(uint64_t n, uint32_t cap = 0);
 cudaError_t launch_recheck_near(const TcArgs& a, cudaStream_t s);
 // K-streamed kernel for d > 256 (nkc > 4): its own conversion, projection and
 // near-tie recheck (per-CTA list segments, counts in TcArgs::seg_counts)

@@ -126,14 +126,18 @@ def test_full_stream_config5_matches_oracle(cuda):
     assert ambiguous == 0
 
 
-def test_full_stream_run_config5_matches_oracle(cuda):
-    """The streaming driver (ace_sketch_stream_run: 2-batch hashing groups,
-    phase B of each batch in the next batch's launch) over all 100M rows at
-    once: per-batch flag digests, counters and n as the oracle's."""
+@pytest.mark.parametrize("group,pipe", [(4, 0), (8, 88)])
+def test_full_stream_run_config5_matches_oracle(cuda, group, pipe):
+    """The streaming driver (ace_sketch_stream_run; one stream launch per
+    hashing group, and pipelined: the next group's projection on `pipe` SMs
+    beside the one-CTA-per-table stream kernel) over all 100M rows at once:
+    per-batch flag digests, counters and n as the oracle's."""
     torch = cuda
     g = GOLD["5"]
     w = W.CONFIGS[5]
     sk = ace.AceSketch(family(5), ace.CounterWidth.k32)
+    sk.set_option(N.ACE_OPT_STREAM_GROUP, group)
+    sk.set_option(N.ACE_OPT_STREAM_PIPE, pipe)
     xd = torch.empty((w.n, w.dim), dtype=torch.float32, device="cuda")
     chunk = 8 * 1024 * 1024
     for r0 in range(0, w.n, chunk):

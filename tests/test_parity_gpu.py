@@ -395,3 +395,39 @@ def test_tied_scores_replay(cuda, oracle_c, gather):
     assert np.array_equal(rep.flags, flags)
     assert rep.reported == int(flags.sum())
     assert rep.threshold == thr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pipe", [0, 64, 90])
+def test_stream_run_pipelined_matches_oracle(cuda, pipe):
+    """ace_sketch_stream_run with ACE_OPT_STREAM_PIPE (the next group's
+    projection beside a one-CTA-per-table stream kernel) against the oracle's
+    stream order: clustered rows, then whole batches of one repeated row (a
+    bucket taking all 65,536 rows of a batch, the u16 histogram's wrap), a
+    ragged last batch."""
+    from oracle import Oracle
+    w = W.CONFIGS[5]
+    batch, nb = 65536, 7
+    n = batch * nb - 4001
+    x, _ = W.host_rows(5, 0, n)
+    x[2 * batch:4 * batch] = x[17]          # two batches of one point
+    x[5 * batch:5 * batch + 300] = x[17]
+    fam = family(5)
+    o = Oracle()
+    ids, _ = o.buckets(fam.directions, x, w.k_bits, w.num_tables)
+    osk = o.sketch(w.k_bits, w.num_tables, 32)
+    want = np.zeros(n, dtype=bool)
+    for b in range(nb):
+        r0, r1 = b * batch, min(n, (b + 1) * batch)
+        want[r0:r1], _ = osk.stream_ids(ids[:, r0:r1], w.alpha)
+    sk = ace.AceSketch(fam, ace.CounterWidth.k32)
+    sk.set_option(N.ACE_OPT_STREAM_GROUP, 2)
+    sk.set_option(N.ACE_OPT_STREAM_PIPE, pipe)
+    xd = cuda.from_numpy(x).cuda()
+    for rep_i in range(3):  # the third call replays the driver's CUDA graph
+        sk.reset()
+        flags, lat, rep = sk.stream_run(xd, batch, w.alpha, latencies=(rep_i == 0))
+        assert np.array_equal(flags, want), rep_i
+        assert np.array_equal(sk.counters_flat(), osk.counters())
+        assert sk.size() == n
+        assert rep.reported == int(want.sum())
