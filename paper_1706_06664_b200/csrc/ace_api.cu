@@ -462,7 +462,8 @@ ace_status ensure_group_bufs(AceSketch* sk, uint64_t group_batches, uint64_t bat
   ACE_CUDA(sk->gco.ensure(static_cast<size_t>(group_batches) * L * batch * sizeof(uint32_t)));
   ACE_CUDA(sk->gdT.ensure(static_cast<size_t>(group_batches) * 2 * L * sizeof(unsigned long long)));
   const void* before = sk->gdone.p;
-  ACE_CUDA(sk->gdone.ensure(static_cast<size_t>(group_batches) * sizeof(unsigned int)));
+  // done[batches] then claim[batches]
+  ACE_CUDA(sk->gdone.ensure(static_cast<size_t>(group_batches) * 2 * sizeof(unsigned int)));
   if (sk->gdone.p != before) ACE_CUDA(cudaMemsetAsync(sk->gdone.p, 0, sk->gdone.bytes, sk->stream));
   // pipelined: two id buffers (the projection fills one while the stream kernel reads the other)
   ACE_CUDA(sk->ids.ensure(static_cast<size_t>(ids_ld) * L * sizeof(uint16_t) * (pipe ? 2u : 1u)));
@@ -1611,7 +1612,8 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
         ACE_CUDA(tmark(1, false, ss));
         ACE_CUDA(launch_stream_group(gids, gld, grows, batch, f->d.tables, f->d.k_bits, sk->counters,
                                      sk->gco.as<uint32_t>(), sk->gdT.as<unsigned long long>(),
-                                     sk->gdone.as<unsigned int>(), dflags + gr0 / 32, alpha, sk->st, ss,
+                                     sk->gdone.as<unsigned int>(), sk->gdone.as<unsigned int>() + gl,
+                                     dflags + gr0 / 32, alpha, sk->st, ss,
                                      g0 + G < nb ? pipe : 0u));
         ACE_CUDA(tmark(1, true, ss));
         if (batch_ms)

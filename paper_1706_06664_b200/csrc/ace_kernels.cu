@@ -1812,13 +1812,22 @@ struct StreamGroupArgs {
   uint32_t* co;                 // [batches][tables][batch]: counts at batch start
   unsigned long long* dT;       // [batches][2 tables]
   unsigned int* done;           // [batches]: phase-A CTAs done with the batch (0 at launch)
+  unsigned int* claim;          // [batches]: scoring units of the batch handed out (0 at launch)
   uint32_t* flags;              // flag words of the group's first row
   double alpha;
   DevState* st;
 };
 
-__device__ void stream_group_b(const StreamGroupArgs& a, uint32_t bb, uint32_t G, uint32_t nA,
-                               unsigned long long* red, unsigned long long* red2) {
+// Scoring (phase B).  dyn (one CTA per table, few scoring CTAs): every CTA of
+// the launch ends up here, the CTAs past the tables from the start, the table
+// CTAs once their tables are done with the group; a batch's rows are claimed
+// in units of kUnitWords flag words from claim[b], so whoever is free scores
+// them.  Otherwise (cluster pairs, 48 scoring CTAs) only the CTAs past the
+// tables score, the flag words dealt out statically.
+constexpr uint32_t kUnitWords = 128;  // 4,096 rows per claim
+
+__device__ void stream_group_b(const StreamGroupArgs& a, uint32_t nA, unsigned long long* red,
+                               unsigned long long* red2, const bool dyn) {
   DevState* st = a.st;
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const double L = static_cast<double>(a.tables);
@@ -1826,9 +1835,11 @@ __device__ void stream_group_b(const StreamGroupArgs& a, uint32_t bb, uint32_t G
   unsigned long long rep = 0ull, amb = 0ull;
   unsigned long long T = st->T;          // committed by the last launch; this launch commits at its very end
   const unsigned long long n0 = st->n;
-  const uint64_t nwarps = static_cast<uint64_t>(G) * (blockDim.x >> 5);
+  const uint32_t nwarps = blockDim.x >> 5;
+  const uint32_t G = dyn ? gridDim.x : gridDim.x - nA, bb = dyn ? 0u : blockIdx.x - nA;  // static: scoring CTA bb of G
   __shared__ unsigned long long dTb;
   __shared__ long long cutS[3];  // integer forms of the batch's cut and ambiguity band (below)
+  __shared__ uint32_t unit_sh[2];
   for (uint64_t b = 0; b < nb; ++b) {
     const uint64_t r0 = b * a.batch, rows = min(a.batch, a.n - r0);
     const unsigned long long nn = n0 + r0;
@@ -1863,14 +1874,19 @@ __device__ void stream_group_b(const StreamGroupArgs& a, uint32_t bb, uint32_t G
       cutS[0] = s_cut;
       cutS[1] = s_lo;
       cutS[2] = s_hi;
-      if (bb == 0 && b + 1 == nb) {
+      if (blockIdx.x == gridDim.x - 1u && b + 1 == nb) {
         st->cut = cut;
         st->mean_before = mu;
       }
     }
+    const uint32_t words_all = static_cast<uint32_t>((rows + 31) / 32);
+    const uint32_t units = (words_all + kUnitWords - 1u) / kUnitWords;
     if (threadIdx.x == 0) {
       while (*reinterpret_cast<volatile unsigned int*>(a.done + b) < nA) __nanosleep(100);
       __threadfence();  // the batch's counts (fenced before done[b] was counted) are read after this
+      // first claim (none if the batch is already taken: a table CTA catching up)
+      if (dyn)
+        unit_sh[0] = *reinterpret_cast<volatile unsigned int*>(a.claim + b) < units ? atomicAdd(a.claim + b, 1u) : units;
     }
     __syncthreads();
     if (wid == 0) {
@@ -1895,7 +1911,13 @@ __device__ void stream_group_b(const StreamGroupArgs& a, uint32_t bb, uint32_t G
       const uint32_t sub = lane & 3u, qi = lane >> 2;
       const uint64_t words = rows / 32, qs = a.batch / 4;
       const uint4* c4 = reinterpret_cast<const uint4*>(cb);
-      for (uint64_t wd = static_cast<uint64_t>(wid) * G + bb; wd < words; wd += nwarps) {
+      uint32_t unit = dyn ? unit_sh[0] : 0u;
+      for (uint32_t ui = 0; unit < (dyn ? units : 1u); ++ui) {
+        if (dyn && threadIdx.x == 0) unit_sh[(ui + 1u) & 1u] = atomicAdd(a.claim + b, 1u);  // the next claim, ahead of use
+        const uint64_t wend = dyn ? min(static_cast<uint64_t>(unit + 1u) * kUnitWords, words) : words;
+        const uint64_t w0 = dyn ? static_cast<uint64_t>(unit) * kUnitWords + wid : static_cast<uint64_t>(wid) * G + bb;
+        const uint64_t wstep = dyn ? nwarps : static_cast<uint64_t>(nwarps) * G;
+      for (uint64_t wd = w0; wd < wend; wd += wstep) {
         const uint64_t qd = wd * 8 + qi;
         unsigned long long S[4] = {0ull, 0ull, 0ull, 0ull};
         for (uint32_t t0 = 0; t0 < a.tables; t0 += 28u) {
@@ -1932,11 +1954,21 @@ __device__ void stream_group_b(const StreamGroupArgs& a, uint32_t bb, uint32_t G
           rep += __popc(word);
         }
       }
+        if (!dyn) break;
+        __syncthreads();
+        unit = unit_sh[(ui + 1u) & 1u];
+      }
     } else {
       // whole flag words, rows past the batch are 0 (only the stream's last
       // batch can be ragged, so no word is shared with the next batch)
       const uint64_t words = (rows + 31) / 32;
-      for (uint64_t w = static_cast<uint64_t>(wid) * G + bb; w < words; w += nwarps) {
+      uint32_t unit = dyn ? unit_sh[0] : 0u;
+      for (uint32_t ui = 0; unit < (dyn ? units : 1u); ++ui) {
+        if (dyn && threadIdx.x == 0) unit_sh[(ui + 1u) & 1u] = atomicAdd(a.claim + b, 1u);
+        const uint64_t wend = dyn ? min(static_cast<uint64_t>(unit + 1u) * kUnitWords, words) : words;
+        const uint64_t w0 = dyn ? static_cast<uint64_t>(unit) * kUnitWords + wid : static_cast<uint64_t>(wid) * G + bb;
+        const uint64_t wstep = dyn ? nwarps : static_cast<uint64_t>(nwarps) * G;
+      for (uint64_t w = w0; w < wend; w += wstep) {
         const uint64_t i = w * 32 + lane;
         bool f = false;
         if (i < rows) {
@@ -1956,6 +1988,10 @@ __device__ void stream_group_b(const StreamGroupArgs& a, uint32_t bb, uint32_t G
           fw[w] = word;
           rep += __popc(word);
         }
+      }
+        if (!dyn) break;
+        __syncthreads();
+        unit = unit_sh[(ui + 1u) & 1u];
       }
     }
     __syncthreads();
@@ -1978,10 +2014,10 @@ __device__ void stream_group_b(const StreamGroupArgs& a, uint32_t bb, uint32_t G
     if (m) atomicAdd(&st->ambiguous, m);
     __threadfence();
     if (atomicAdd(&st->ticket_g, 1u) == G - 1u) {
-      // every phase-B CTA has read T and n: commit the group, clear done[]
+      // every CTA has read T and n: commit the group, clear done[] and claim[]
       st->T = T;
       st->n = n0 + a.n;
-      for (uint64_t k = 0; k < nb; ++k) a.done[k] = 0u;
+      for (uint64_t k = 0; k < nb; ++k) a.done[k] = a.claim[k] = 0u;
       st->ticket_g = 0u;
     }
   }
@@ -1999,7 +2035,7 @@ __device__ __forceinline__ void stream_group_body(const StreamGroupArgs& a, uint
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t nA = C * a.tables;  // phase-A CTAs (one cluster per table)
   if (blockIdx.x >= nA) {
-    stream_group_b(a, blockIdx.x - nA, gridDim.x - nA, nA, red, red2);
+    stream_group_b(a, nA, red, red2, C == 1);
     SPP(9);
     SPC(15);
     return;
@@ -2159,6 +2195,11 @@ __device__ __forceinline__ void stream_group_body(const StreamGroupArgs& a, uint
   }
   (void)peer_hs;
   (void)peer_cs;
+  // one CTA per table: this table is done with the group, help score what is left of it
+  if constexpr (C == 1) {
+    __syncthreads();
+    stream_group_b(a, nA, red, red2, true);
+  }
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024) stream_group_kernel(const StreamGroupArgs a) {
@@ -2392,8 +2433,8 @@ bool stream_solo_ok(uint32_t tables, uint32_t k_bits, uint64_t batch, uint32_t h
 
 cudaError_t launch_stream_group(const uint16_t* ids, uint64_t ids_ld, uint64_t n, uint64_t batch, uint32_t tables,
                                 uint32_t k_bits, uint32_t* counters, uint32_t* co, unsigned long long* dT,
-                                unsigned int* done, uint32_t* flags, double alpha, DevState* st, cudaStream_t s,
-                                uint32_t hash_ctas) {
+                                unsigned int* done, unsigned int* claim, uint32_t* flags, double alpha, DevState* st,
+                                cudaStream_t s, uint32_t hash_ctas) {
   if (n == 0) return cudaSuccess;
   if (!stream_group_ok(tables, k_bits, batch) || ids_ld % 8 != 0 || (reinterpret_cast<uintptr_t>(ids) & 15))
     return cudaErrorInvalidValue;
@@ -2409,6 +2450,7 @@ cudaError_t launch_stream_group(const uint16_t* ids, uint64_t ids_ld, uint64_t n
   a.co = co;
   a.dT = dT;
   a.done = done;
+  a.claim = claim;
   a.flags = flags;
   a.alpha = alpha;
   a.st = st;

@@ -86,8 +86,8 @@ bool stream_group_ok(uint32_t tables, uint32_t k_bits, uint64_t batch);
 bool stream_solo_ok(uint32_t tables, uint32_t k_bits, uint64_t batch, uint32_t hash_ctas);
 cudaError_t launch_stream_group(const uint16_t* ids, uint64_t ids_ld, uint64_t n, uint64_t batch, uint32_t tables,
                                 uint32_t k_bits, uint32_t* counters, uint32_t* co, unsigned long long* dT,
-                                unsigned int* done, uint32_t* flags, double alpha, DevState* st, cudaStream_t s,
-                                uint32_t hash_ctas = 0);
+                                unsigned int* done, unsigned int* claim, uint32_t* flags, double alpha, DevState* st,
+                                cudaStream_t s, uint32_t hash_ctas = 0);
 // The stream driver hashes into u16 ids (ids16) where the pair kernel runs
 // (K <= 15, batches of at most 2 x 65,535 rows, two CTAs per table fit).
 bool stream_pair_ok(uint32_t tables, uint32_t k_bits, uint64_t batch);

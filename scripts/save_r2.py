@@ -44,7 +44,7 @@ KEEP = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__
         "smsp__inst_executed.sum", "sm__cycles_elapsed.avg.per_second"]
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 tr_path = PROF / "traffic.json"
-traffic = json.loads(tr_path.read_text()) if tr_path.exists() else {}
+traffic = {}  # rebuilt from this round's captures
 for rep, cfg, name in (("prof_h5", 5, "ncu_hash_cfg5"), ("prof_h2", 2, "ncu_hash_cfg2"), ("prof_pair", 5, "ncu_stream_cfg5")):
     path = OUT / f"{rep}.ncu-rep"
     if not path.exists():
