@@ -594,6 +594,35 @@ def run_stream(args, cfg, ws, rank, local, torch, N, ace, W):
     N.dev().ace_sketch_set_timing(sk.handle, 0)
     hash_ms, apply_ms = ms5[4], ms5[2]
 
+    # the throughput / latency trade-off of the driver's options: smaller
+    # hashing groups without the pipeline flag each batch sooner
+    modes = []
+    for g_m, p_m in ((1, 0), (2, 0), (4, 0)):
+        if args.rows is not None:
+            break
+        sk_m = ace.AceSketch(fam, ace.CounterWidth.k32)
+        sk_m.set_option(N.ACE_OPT_STREAM_GROUP, g_m)
+        sk_m.set_option(N.ACE_OPT_STREAM_PIPE, p_m)
+        sk_m.set_stream(stream.cuda_stream)
+
+        def step_m(lat=False):
+            sk_m.reset()
+            return sk_m.stream_run(x, w.batch, w.alpha, flags_out=flags, latencies=lat)
+
+        _, lat_m, _ = step_m(lat=True)
+        for _ in range(3):
+            step_m()
+        m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        m0.record(stream)
+        for _ in range(3):
+            step_m()
+        m1.record(stream)
+        torch.cuda.synchronize()
+        modes.append({"hash_group_batches": g_m, "pipeline_sms": p_m,
+                      "points_per_s": replica_value(n, ws, max_over_ranks(m0.elapsed_time(m1) / 3, ws)),
+                      "p50_ms": float(np.percentile(lat_m, 50)), "p99_ms": float(np.percentile(lat_m, 99))})
+        del sk_m
+
     e2e = None
     if not args.no_e2e:
         # the same call with the rows in pinned host memory (the next hashing
@@ -680,6 +709,7 @@ def run_stream(args, cfg, ws, rank, local, torch, N, ace, W):
                              "definition": "start of the batch's work (its group's hashing for a group's first "
                                            "batch) to the end of the launch that writes its flags; CUDA events "
                                            "around every batch in one extra run (no graph)"},
+        "latency_modes": modes,
         "gpu_launches": int(round(launches)), "clocks": clk, "e2e": e2e,
         "exactness": {"near_ties_1e-6": int(st.near_ties), "rechecked": int(st.rechecked),
                       "flipped": int(st.flipped), "ambiguous": int(rep.ambiguous), "reported": int(rep.reported)},
