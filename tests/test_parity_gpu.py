@@ -431,3 +431,45 @@ def test_stream_run_pipelined_matches_oracle(cuda, pipe):
         assert np.array_equal(sk.counters_flat(), osk.counters())
         assert sk.size() == n
         assert rep.reported == int(want.sum())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,k,l,batch,group,pipe", [
+    (24, 8, 10, 1024, 4, 88),     # small tables, many scoring CTAs
+    (64, 15, 50, 4096, 3, 64),    # cfg-5 shape, short batches, group not dividing the batch count
+    (40, 12, 64, 8192, 2, 80),    # 64 tables + 4 + 80 = 148 SMs: the tightest split
+    (33, 4, 7, 256, 8, 100),      # K = 4 (the smallest), batches of one scoring chunk
+    (64, 15, 50, 4096, 3, 0),     # the pair kernel on the same stream
+])
+def test_stream_run_shapes_match_oracle(cuda, d, k, l, batch, group, pipe):
+    """The group stream kernels (pair and one CTA per table, pipelined with
+    the projection) on other shapes than config 5, device rows and pinned host
+    rows, against the oracle's stream order."""
+    from oracle import Oracle
+    torch = cuda
+    nb = 11
+    n = batch * nb - 96
+    rng = np.random.default_rng(1000 * k + l)
+    centres = rng.standard_normal((5, d)) * 3.0
+    x = (centres[rng.integers(0, 5, n)] + 0.3 * rng.standard_normal((n, d))).astype(np.float32)
+    x[rng.integers(0, n, n // 50)] = (rng.standard_normal((n // 50, d)) * 8.0).astype(np.float32)
+    fam = ace.SrpFamily(ace.SrpConfig(dim=d, k_bits=k, num_tables=l, seed=7))
+    o = Oracle()
+    ids, _ = o.buckets(fam.directions, x, k, l)
+    osk = o.sketch(k, l, 32)
+    want = np.zeros(n, dtype=bool)
+    alpha = 0.5
+    for b in range(nb):
+        r0, r1 = b * batch, min(n, (b + 1) * batch)
+        want[r0:r1], _ = osk.stream_ids(ids[:, r0:r1], alpha)
+    for src in ("device", "pinned"):
+        sk = ace.AceSketch(fam, ace.CounterWidth.k32)
+        sk.set_option(N.ACE_OPT_STREAM_GROUP, group)
+        sk.set_option(N.ACE_OPT_STREAM_PIPE, pipe)
+        xin = torch.from_numpy(x).cuda() if src == "device" else torch.from_numpy(x).pin_memory().numpy()
+        for rep_i in range(3):
+            sk.reset()
+            flags, _, rep = sk.stream_run(xin, batch, alpha, latencies=(rep_i == 1))
+            assert np.array_equal(flags, want), (src, rep_i)
+            assert np.array_equal(sk.counters_flat(), osk.counters()), (src, rep_i)
+            assert sk.size() == n and rep.reported == int(want.sum())
