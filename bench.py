@@ -48,7 +48,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "ACE points/sec (hash+insert+score) on 1 B200; % of binding FP32/HBM/L2-atomic roofline"
 UNIT = "points/s"
 ORDER = [1, 2, 3, 4, 5]  # the headline (config 5) last
-STREAM_PIPE = 88  # config 5: projection SMs while pipelined beside the stream kernel (0 = not pipelined)
+STREAM_PIPE = 90  # config 5: projection SMs while pipelined beside the stream kernel (0 = not pipelined)
 STREAM_GROUP = 8  # config 5: batches per hashing launch (lookahead of the stream driver)
 
 # bounded CPU samples (rows): cpu_baseline leg (~10 s of reference CPU work

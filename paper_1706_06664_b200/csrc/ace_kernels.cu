@@ -2141,7 +2141,25 @@ __device__ __forceinline__ void stream_group_body(const StreamGroupArgs& a, uint
     SPP(2);
     if constexpr (C == 2) cg::this_cluster().sync();  // both histograms complete (and both CTAs done reading the counts at batch start)
     SPP(3);
-    {
+    if constexpr (C == 1) {
+      // every bin: consecutive lanes take consecutive histogram words (two
+      // bins) and the two counts beside them as one 8-byte access, so neither
+      // array sees bank conflicts; a touched word is cleared on the way
+      uint2* cs2 = reinterpret_cast<uint2*>(cs);
+      for (uint32_t w = threadIdx.x; w < nw; w += blockDim.x) {
+        const uint32_t hv = hs[w];
+        if (hv) {
+          uint2 c = cs2[w];
+          const uint32_t m0 = hv & 0xffffu, m1 = hv >> 16;
+          dT += 2ull * c.x * m0 + static_cast<unsigned long long>(m0) * m0 + 2ull * c.y * m1 +
+                static_cast<unsigned long long>(m1) * m1;
+          c.x += m0;
+          c.y += m1;
+          cs2[w] = c;
+          hs[w] = 0u;
+        }
+      }
+    } else {
       // this CTA's half of the bins: both histograms (the peer's through
       // distributed shared memory, 16-byte loads), the new counts into both copies
       const uint4* o4 = reinterpret_cast<const uint4*>(hs);
@@ -2175,7 +2193,8 @@ __device__ __forceinline__ void stream_group_body(const StreamGroupArgs& a, uint
     SPP(4);
     if constexpr (C == 2) cg::this_cluster().sync();  // both CTAs done with the histograms and the counts
     SPP(5);
-    for (uint32_t w = threadIdx.x; w < nw; w += blockDim.x) hs[w] = 0u;
+    if constexpr (C == 2)
+      for (uint32_t w = threadIdx.x; w < nw; w += blockDim.x) hs[w] = 0u;
     __threadfence();  // this thread's co[b] stores visible GPU-wide before done[b] counts the CTA
     __syncthreads();
     if (threadIdx.x == 0) {

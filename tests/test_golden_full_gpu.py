@@ -126,7 +126,7 @@ def test_full_stream_config5_matches_oracle(cuda):
     assert ambiguous == 0
 
 
-@pytest.mark.parametrize("group,pipe", [(4, 0), (8, 88)])
+@pytest.mark.parametrize("group,pipe", [(4, 0), (8, 90)])
 def test_full_stream_run_config5_matches_oracle(cuda, group, pipe):
     """The streaming driver (ace_sketch_stream_run; one stream launch per
     hashing group, and pipelined: the next group's projection on `pipe` SMs
