@@ -144,13 +144,15 @@ ace_status ace_sketch_set_stream(AceSketch* sk, void* cuda_stream);
  *   ACE_OPT_STREAM_GROUP  ace_sketch_stream_run: batches hashed by one
  *                         projection launch (default 4; 1..64; throughput vs
  *                         per-batch latency);
- *   ACE_OPT_STREAM_PIPE   ace_sketch_stream_run: 0 (default) = projection and
- *                         stream kernels one after the other on the whole
- *                         GPU; P > 0 = the projection of group g + 1 runs on
- *                         P SMs beside the stream kernel of group g (one CTA
- *                         per table plus scoring CTAs on the other SMs; K <=
- *                         15, batches of at most 65,536 rows, tables + 4 + P
- *                         <= SM count, else ignored).  Same results. */
+ *   ACE_OPT_STREAM_PIPE   ace_sketch_stream_run: P > 0 = the projection of
+ *                         group g + 1 runs on P SMs beside the stream kernel
+ *                         of group g (one CTA per table plus scoring CTAs on
+ *                         the other SMs; K <= 15, batches of at most 65,536
+ *                         rows, more than one group, tables + 4 + P <= SM
+ *                         count, else ignored); 0 = projection and stream
+ *                         kernels one after the other on the whole GPU (lower
+ *                         per-batch latency); -1 (default) = P = SM count -
+ *                         tables - 8.  Same results. */
 enum { ACE_OPT_H2D_CHUNKS = 1, ACE_OPT_DEFER_INSERT = 2, ACE_OPT_STREAM_GROUP = 3, ACE_OPT_STREAM_PIPE = 4 };
 ace_status ace_sketch_set_option(AceSketch* sk, int option, int64_t value);
 

@@ -139,7 +139,7 @@ struct AceSketch {
   // stream driver pipeline: the projection of group g + 1 (capped at this many
   // CTAs) runs beside the stream kernel of group g (one CTA per table on the
   // other SMs, on pstream); 0 = one after the other on the whole GPU
-  int stream_pipe = 0;      // ACE_OPT_STREAM_PIPE
+  int stream_pipe = -1;     // ACE_OPT_STREAM_PIPE (-1 = automatic)
   cudaStream_t pstream = nullptr;
   cudaEvent_t p_hashed[2] = {nullptr, nullptr}, p_streamed[2] = {nullptr, nullptr};
   // build + detect over the same rows: run_hash leaves the insert to the
@@ -1024,7 +1024,7 @@ ace_status ace_sketch_set_option(AceSketch* sk, int option, int64_t value) {
       sk->stream_group = static_cast<int>(value);
       break;
     case ACE_OPT_STREAM_PIPE:
-      if (value < 0 || value > 1024) return fail(ACE_E_CONTRACT, "ace_sketch_set_option: pipe CTAs must be in [0, 1024]");
+      if (value < -1 || value > 1024) return fail(ACE_E_CONTRACT, "ace_sketch_set_option: pipe CTAs must be in [-1, 1024]");
       sk->stream_pipe = static_cast<int>(value);
       break;
     default:
@@ -1500,9 +1500,12 @@ ace_status ace_sketch_stream_run(AceSketch* sk, const void* x, int dtype, uint64
   if (fast && !gfast && (r = ensure_stream_bufs(sk, std::min(batch, n))) != ACE_OK) return r;
   // pipelined groups (ACE_OPT_STREAM_PIPE): the projection of group g + 1 on
   // `pipe` SMs beside the stream kernel of group g on the others
-  const uint32_t pipe = (gfast && nb > G && sk->stream_pipe > 0 &&
-                         stream_solo_ok(f->d.tables, f->d.k_bits, batch, static_cast<uint32_t>(sk->stream_pipe)))
-                            ? static_cast<uint32_t>(sk->stream_pipe)
+  // automatic: every SM but one per table and eight for scoring (cfg 5: 90 of 148)
+  const int sms_all = tc_sms();
+  const int pipe_req = sk->stream_pipe >= 0 ? sk->stream_pipe : std::max(0, sms_all - static_cast<int>(f->d.tables) - 8);
+  const uint32_t pipe = (gfast && nb > G && pipe_req > 0 &&
+                         stream_solo_ok(f->d.tables, f->d.k_bits, batch, static_cast<uint32_t>(pipe_req)))
+                            ? static_cast<uint32_t>(pipe_req)
                             : 0u;
   if (gfast && (r = ensure_group_bufs(sk, gl, batch, gld, pipe != 0)) != ACE_OK) return r;
   // per-batch latency: from the start of the batch's work (its group's
