@@ -2169,21 +2169,28 @@ __device__ __forceinline__ void stream_group_body(const StreamGroupArgs& a, uint
         const uint4 ov = o4[q];
         uint4 pv = make_uint4(0u, 0u, 0u, 0u);
         if constexpr (C == 2) pv = p4[q];
+        if ((ov.x | ov.y | ov.z | ov.w | pv.x | pv.y | pv.z | pv.w) == 0u) continue;
+        // the eight counts of these four words as two 16-byte accesses (local and peer copy)
         const uint32_t ow[4] = {ov.x, ov.y, ov.z, ov.w}, pw[4] = {pv.x, pv.y, pv.z, pv.w};
+        uint4* c4 = reinterpret_cast<uint4*>(cs) + 2u * q;
+        const uint4 ca = c4[0], cb = c4[1];
+        uint32_t cv[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          if ((ow[e] | pw[e]) == 0u) continue;
+        for (int e = 0; e < 4; ++e)
 #pragma unroll
           for (uint32_t h = 0; h < 2; ++h) {
-            const uint32_t bin = 2u * (4u * q + e) + h;
             const uint32_t m = ((ow[e] >> (16 * h)) & 0xffffu) + ((pw[e] >> (16 * h)) & 0xffffu);
-            if (m) {
-              const uint32_t c = cs[bin];
-              cs[bin] = c + m;
-              if constexpr (C == 2) peer_cs[bin] = c + m;
-              dT += 2ull * c * m + static_cast<unsigned long long>(m) * m;
-            }
+            const uint32_t c = cv[2 * e + h];
+            dT += 2ull * c * m + static_cast<unsigned long long>(m) * m;
+            cv[2 * e + h] = c + m;
           }
+        const uint4 na = make_uint4(cv[0], cv[1], cv[2], cv[3]), nb4 = make_uint4(cv[4], cv[5], cv[6], cv[7]);
+        c4[0] = na;
+        c4[1] = nb4;
+        if constexpr (C == 2) {
+          uint4* p4c = reinterpret_cast<uint4*>(peer_cs) + 2u * q;
+          p4c[0] = na;
+          p4c[1] = nb4;
         }
       }
     }
